@@ -1,0 +1,158 @@
+/*
+ * wavecast_b200.h -- C ABI of libwavecast_b200.so, the sm_100a render path.
+ *
+ * The reference (`wavecast`, /root/reference/pkg/src/wavecast) is a pure
+ * Python + numba package with no FFI of its own; its drop-in boundary is
+ * the Python API re-exported by wavecast/__init__.py:3-56.  Each entry point
+ * below is what that API's hot path binds to through ctypes
+ * (paper_2309_10212_b200/_lib.py); the reference interface it replaces is
+ * cited per function.  No torch types cross this boundary: plain pointers,
+ * sizes and opaque handles.  Every function returns 0 on success or a
+ * WC_E_* code, with a message in wc_last_error().
+ */
+#ifndef WAVECAST_B200_H
+#define WAVECAST_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WC_OK 0
+#define WC_E_USAGE 2     /* maps to wavecast.errors.UsageError (errors.py:4-5) */
+#define WC_E_DATA 3      /* maps to wavecast.errors.DataError  (errors.py:8-9) */
+#define WC_E_INVARIANT 4 /* maps to AssertionError (engine.py:302,332,341)    */
+#define WC_E_CUDA 5      /* CUDA runtime failure (no GPU, OOM, fault)         */
+
+typedef struct wc_volume wc_volume;
+typedef struct wc_session wc_session;
+
+/* engine.py:66-77 PassStats (+ evicted, n_entries, n_active_after) */
+typedef struct {
+    int64_t pass_index;
+    int64_t n_active_before;
+    int64_t n_spec;
+    int64_t visible_blocks;
+    int64_t active_blocks;
+    int64_t new_decompressed;
+    int64_t evicted;
+    int64_t cache_slots;
+    int64_t n_entries;
+    int64_t n_active_after;
+    double utilization;
+    double completeness;
+    double duration;
+} wc_pass_stats;
+
+/* Camera basis as computed by traversal.py:65-70 (look, right, up) and
+ * :111 (tan_half), plus the full image size (traversal.py:113-114). */
+typedef struct {
+    double eye[3];
+    double look[3];
+    double right[3];
+    double up[3];
+    double tan_half;
+    int32_t img_w;
+    int32_t img_h;
+} wc_camera;
+
+const char *wc_last_error(void);
+/* Select the CUDA device (fails loudly when no GPU is present). */
+int wc_init(int device);
+/* Build-time identity string (arch, flags). */
+const char *wc_build_info(void);
+
+/* ---- volume: CompressedVolume (codec.py:34-65) + build_grids (grids.py:71-94)
+ * Uploads a WCZ1 payload + raw ranges to HBM and builds the float64 fine /
+ * coarse value-range grids on the device. */
+int wc_volume_create(const uint8_t *payload, uint64_t payload_bytes, const float *ranges, int nx, int ny, int nz,
+                     int qbits, int stride, wc_volume **out);
+/* compress_volume (codec.py:177-198) of a dense float32 field (x-fastest,
+ * host pointer) on the device, then build_grids. */
+int wc_volume_compress(const float *values, int nx, int ny, int nz, int qbits, wc_volume **out);
+/* Same for a separable synthetic field v = sum_k ((amp[k]*fz[k][z])*fy[k][y])*fx[k][x]
+ * generated on the device block by block (no dense field in memory). */
+int wc_volume_synthesize(int K, const float *amp, const float *fx, const float *fy, const float *fz, int nx, int ny,
+                         int nz, int qbits, wc_volume **out);
+int wc_volume_destroy(wc_volume *v);
+/* Replace the device grids with caller-supplied MacrocellGrids arrays
+ * (grids.py:32-45; float64 fine n_blocks and coarse n_coarse entries). */
+int wc_volume_set_grids(wc_volume *v, const double *fine_min, const double *fine_max, const double *coarse_min,
+                        const double *coarse_max);
+/* n_blocks, n_coarse, payload bytes */
+int wc_volume_info(const wc_volume *v, int64_t *n_blocks, int64_t *n_coarse, int64_t *payload_bytes);
+/* Copy the device payload / ranges / grids back to host buffers (nullable). */
+int wc_volume_download(const wc_volume *v, uint8_t *payload, float *ranges, double *fine_min, double *fine_max,
+                       double *coarse_min, double *coarse_max);
+/* decompress_block(s) (codec.py:201-217): host ids in, host float32[n*64] out. */
+int wc_decode_blocks(const wc_volume *v, const int64_t *ids, int64_t n, float *out);
+/* Device-only timing of decode: decodes `n` blocks (ids on host, uploaded
+ * once) `reps` times into a device buffer; returns average ms per launch. */
+int wc_decode_bench(const wc_volume *v, const int64_t *ids, int64_t n, int reps, double *ms_per_launch);
+
+/* ---- session: engine.render_passes (engine.py:308-382)
+ * Camera rays (origins == dirs == NULL) for all w*h pixels or for the
+ * `pixel_ids` subset (tile sharding; n = number of pixels), or arbitrary
+ * rays (RaySoA.from_rays, traversal.py:122-170) through origins/dirs (n x 3).
+ * cache_capacity <= 0 selects initial_capacity (cache.py:122-125). */
+int wc_session_create(wc_volume *v, const wc_camera *cam, const uint32_t *pixel_ids, int64_t n, const double *origins,
+                      const double *dirs, double iso, int speculation, int max_spec, int64_t cache_capacity,
+                      int corrupt_cache, wc_session **out);
+int wc_session_set_base_color(wc_session *s, double r, double g, double b);
+/* One pass; *ran = 0 once every ray has terminated. */
+int wc_session_pass(wc_session *s, wc_pass_stats *stats, int *ran);
+/* Run passes until done (render, engine.py:385-401); returns pass count. */
+int wc_session_run(wc_session *s, wc_pass_stats *stats_out, int64_t max_stats, int64_t *n_passes);
+int wc_session_n_active(const wc_session *s, int64_t *n_active);
+/* Framebuffer.snapshot (engine.py:62-63): RGBA8 (n x 4) + float32 depth (n). */
+int wc_session_framebuffer(wc_session *s, uint8_t *rgba, float *depth);
+/* Same into caller-owned DEVICE buffers (for NCCL tile gathers). */
+int wc_session_framebuffer_device(wc_session *s, void *rgba_dev, void *depth_dev);
+/* Device time of the last pass (CUDA events on the session stream). */
+int wc_session_last_pass_ms(const wc_session *s, double *ms);
+int wc_session_destroy(wc_session *s);
+
+/* ---- per-stage views of the last pass (parity tests) */
+/* sizes[8] = slots_used, n_visible, n_active_blocks, n_entries, n_spec,
+ *            n_active_before, cache_capacity, cache_physical */
+int wc_session_sizes(const wc_session *s, int64_t *sizes);
+/* RaySoA fields (traversal.py:76-91), each nullable */
+int wc_session_rays(const wc_session *s, double *dir, double *t_enter, double *t_exit, uint8_t *status,
+                    uint8_t *exited, uint32_t *coarse_cell, uint32_t *fine_cell, double *coarse_tmax,
+                    double *fine_tmax);
+/* block_slots / ray_slots prefix [0, slots_used) and the last pass's
+ * compacted active-ray list [0, n_active_before) */
+int wc_session_slots(const wc_session *s, uint32_t *block_slots, uint32_t *ray_slots, uint32_t *active_list);
+int wc_session_blocks(const wc_session *s, uint32_t *visible_ids, uint32_t *active_ids);
+/* grouped RT inputs (engine.py:121-149): block_ray_offsets[n_visible+1],
+ * sorted entry ids (== sorted_hit_slots) and the owning ray per entry id */
+int wc_session_rt_inputs(const wc_session *s, uint32_t *block_ray_offsets, uint32_t *sorted_entries,
+                         uint32_t *entry_ray);
+/* rgbz per entry id: float4 (r, g, b, z) x n_entries */
+int wc_session_rgbz(const wc_session *s, float *rgbz);
+/* cache state over the physical slots: block_of_slot / last_used (int32),
+ * slot_values (float32 x 64) -- each nullable */
+int wc_session_cache(const wc_session *s, int32_t *block_of_slot, int32_t *last_used, float *slot_values);
+
+/* ---- standalone pieces */
+/* RaySoA.from_camera / from_rays (traversal.py:105-187) on the device */
+int wc_init_rays(const wc_camera *cam, const uint32_t *pixel_ids, int64_t n, const double *origins,
+                 const double *dirs, int nx, int ny, int nz, double *dir_out, double *t_enter, double *t_exit,
+                 uint8_t *status, uint8_t *exited, uint32_t *coarse_cell, uint32_t *fine_cell, double *coarse_tmax,
+                 double *fine_tmax);
+/* oracle.reference_render (oracle.py:42-122): brute-force over the fully
+ * decoded volume on the device (for parity at scales the CPU cannot do). */
+int wc_reference_render(const wc_volume *v, const double *origins, const double *dirs, int64_t n, double iso,
+                        double base_r, double base_g, double base_b, uint8_t *rgba, float *depth);
+/* same over a dense float32 field (x-fastest) given by the caller */
+int wc_reference_render_dense(const float *values, int nx, int ny, int nz, const double *origins, const double *dirs,
+                              int64_t n, double iso, double base_r, double base_g, double base_b, uint8_t *rgba,
+                              float *depth);
+/* prims.py:13-40 on the device (host arrays in/out) */
+int wc_exclusive_scan(const uint32_t *values, int64_t n, uint32_t *out, uint64_t *total);
+int wc_sort_by_key(uint32_t *keys, uint32_t *values, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,547 @@
+// wc_capi.cu -- extern "C" boundary of libwavecast_b200.so (include/wavecast_b200.h).
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/wavecast_b200.h"
+#include "wc_engine.cuh"
+
+struct wc_volume {
+    wc::Volume v;
+};
+struct wc_session {
+    wc::Session *s = nullptr;
+    wc_volume *vol = nullptr;
+};
+
+static thread_local std::string g_err;
+
+#define WC_API_BEGIN try {
+#define WC_API_END                              \
+    }                                           \
+    catch (const wc::UsageError &e) {           \
+        g_err = e.what();                       \
+        return WC_E_USAGE;                      \
+    }                                           \
+    catch (const wc::DataError &e) {            \
+        g_err = e.what();                       \
+        return WC_E_DATA;                       \
+    }                                           \
+    catch (const wc::InvariantError &e) {       \
+        g_err = e.what();                       \
+        return WC_E_INVARIANT;                  \
+    }                                           \
+    catch (const std::exception &e) {           \
+        g_err = e.what();                       \
+        return WC_E_CUDA;                       \
+    }                                           \
+    return WC_OK;
+
+#define WC_REQUIRE(cond, kind, msg) \
+    do {                            \
+        if (!(cond)) throw kind(msg); \
+    } while (0)
+
+static_assert(sizeof(wc_pass_stats) == sizeof(wc::PassStatsC), "stats layout");
+static_assert(sizeof(wc_camera) == sizeof(wc::CameraParams), "camera layout");
+
+namespace {
+
+void check_qbits(int qbits) {
+    if (qbits < 4 || qbits > 26)  // codec.py:26-27,76-78
+        throw wc::UsageError("qbits must be in [4, 26], got " + std::to_string(qbits));
+}
+void check_dims(int nx, int ny, int nz) {
+    if (nx < 1 || ny < 1 || nz < 1) throw wc::UsageError("dims must be positive");
+}
+
+template <typename T>
+void upload(wc::DevBuf<T> &d, const T *h, int64_t n, cudaStream_t st) {
+    d.alloc(n);
+    WC_CUDA(cudaMemcpyAsync(d.p, h, sizeof(T) * (size_t)n, cudaMemcpyHostToDevice, st));
+}
+
+template <typename T>
+void download(T *h, const T *d, int64_t n, cudaStream_t st) {
+    if (!h || n <= 0) return;
+    WC_CUDA(cudaMemcpyAsync(h, d, sizeof(T) * (size_t)n, cudaMemcpyDeviceToHost, st));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *wc_last_error(void) { return g_err.c_str(); }
+
+const char *wc_build_info(void) {
+    return "libwavecast_b200: sm_100a (compute_100a), -fmad=false -lineinfo -O3";
+}
+
+int wc_init(int device) {
+    WC_API_BEGIN
+    int n = 0;
+    WC_CUDA(cudaGetDeviceCount(&n));
+    WC_REQUIRE(device >= 0 && device < n, wc::UsageError, "no such CUDA device");
+    WC_CUDA(cudaSetDevice(device));
+    WC_CUDA(cudaFree(nullptr));
+    WC_API_END
+}
+
+int wc_volume_create(const uint8_t *payload, uint64_t payload_bytes, const float *ranges, int nx, int ny, int nz,
+                     int qbits, int stride, wc_volume **out) {
+    WC_API_BEGIN
+    check_qbits(qbits);
+    check_dims(nx, ny, nz);
+    WC_REQUIRE(stride == wc::stride_of(qbits), wc::DataError, "stride inconsistent with qbits");
+    auto *h = new wc_volume();
+    try {
+        h->v.set_dims(nx, ny, nz, qbits);
+        WC_REQUIRE((int64_t)payload_bytes == h->v.n_blocks * stride, wc::DataError, "payload size mismatch");
+        upload(h->v.payload, payload, h->v.n_blocks * stride, h->v.st);
+        upload(h->v.ranges, reinterpret_cast<const float2 *>(ranges), h->v.n_blocks, h->v.st);
+        h->v.build_grids();
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    WC_API_END
+}
+
+int wc_volume_compress(const float *values, int nx, int ny, int nz, int qbits, wc_volume **out) {
+    WC_API_BEGIN
+    check_qbits(qbits);
+    check_dims(nx, ny, nz);
+    auto *h = new wc_volume();
+    try {
+        h->v.set_dims(nx, ny, nz, qbits);
+        wc::DevBuf<float> dense;
+        upload(dense, values, (int64_t)nx * ny * nz, h->v.st);
+        wc::compress_dense_device(h->v, dense.p);
+        h->v.build_grids();
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    WC_API_END
+}
+
+int wc_volume_synthesize(int K, const float *amp, const float *fx, const float *fy, const float *fz, int nx, int ny,
+                         int nz, int qbits, wc_volume **out) {
+    WC_API_BEGIN
+    check_qbits(qbits);
+    check_dims(nx, ny, nz);
+    WC_REQUIRE(K >= 1, wc::UsageError, "need at least one separable term");
+    auto *h = new wc_volume();
+    try {
+        h->v.set_dims(nx, ny, nz, qbits);
+        wc::synth_separable_compress(h->v, K, amp, fx, fy, fz);
+        h->v.build_grids();
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    WC_API_END
+}
+
+int wc_volume_destroy(wc_volume *v) {
+    WC_API_BEGIN
+    delete v;
+    WC_API_END
+}
+
+int wc_volume_set_grids(wc_volume *v, const double *fine_min, const double *fine_max, const double *coarse_min,
+                        const double *coarse_max) {
+    WC_API_BEGIN
+    wc::Volume &V = v->v;
+    std::vector<double2> f(V.n_blocks), c(V.n_coarse);
+    for (int64_t i = 0; i < V.n_blocks; i++) f[i] = make_double2(fine_min[i], fine_max[i]);
+    for (int64_t i = 0; i < V.n_coarse; i++) c[i] = make_double2(coarse_min[i], coarse_max[i]);
+    upload(V.fine_mm, f.data(), V.n_blocks, V.st);
+    upload(V.coarse_mm, c.data(), V.n_coarse, V.st);
+    WC_CUDA(cudaStreamSynchronize(V.st));
+    WC_API_END
+}
+
+int wc_volume_info(const wc_volume *v, int64_t *n_blocks, int64_t *n_coarse, int64_t *payload_bytes) {
+    WC_API_BEGIN
+    if (n_blocks) *n_blocks = v->v.n_blocks;
+    if (n_coarse) *n_coarse = v->v.n_coarse;
+    if (payload_bytes) *payload_bytes = v->v.n_blocks * v->v.stride;
+    WC_API_END
+}
+
+int wc_volume_download(const wc_volume *v, uint8_t *payload, float *ranges, double *fine_min, double *fine_max,
+                       double *coarse_min, double *coarse_max) {
+    WC_API_BEGIN
+    const wc::Volume &V = v->v;
+    download(payload, V.payload.p, V.n_blocks * V.stride, V.st);
+    download(reinterpret_cast<float2 *>(ranges), V.ranges.p, V.n_blocks, V.st);
+    std::vector<double2> f, c;
+    if (fine_min || fine_max) {
+        f.resize(V.n_blocks);
+        download(f.data(), V.fine_mm.p, V.n_blocks, V.st);
+    }
+    if (coarse_min || coarse_max) {
+        c.resize(V.n_coarse);
+        download(c.data(), V.coarse_mm.p, V.n_coarse, V.st);
+    }
+    WC_CUDA(cudaStreamSynchronize(V.st));
+    for (int64_t i = 0; i < (int64_t)f.size(); i++) {
+        if (fine_min) fine_min[i] = f[i].x;
+        if (fine_max) fine_max[i] = f[i].y;
+    }
+    for (int64_t i = 0; i < (int64_t)c.size(); i++) {
+        if (coarse_min) coarse_min[i] = c[i].x;
+        if (coarse_max) coarse_max[i] = c[i].y;
+    }
+    WC_API_END
+}
+
+int wc_decode_blocks(const wc_volume *v, const int64_t *ids, int64_t n, float *out) {
+    WC_API_BEGIN
+    if (n <= 0) return WC_OK;
+    const wc::Volume &V = v->v;
+    for (int64_t i = 0; i < n; i++)
+        WC_REQUIRE(ids[i] >= 0 && ids[i] < V.n_blocks, wc::InvariantError, "block id out of range");
+    wc::DevBuf<int64_t> d_ids;
+    wc::DevBuf<float> d_out;
+    upload(d_ids, ids, n, V.st);
+    d_out.alloc(n * 64);
+    wc::decode_blocks_device(V, d_ids.p, n, d_out.p, V.st);
+    download(out, d_out.p, n * 64, V.st);
+    WC_CUDA(cudaStreamSynchronize(V.st));
+    WC_API_END
+}
+
+int wc_decode_bench(const wc_volume *v, const int64_t *ids, int64_t n, int reps, double *ms_per_launch) {
+    WC_API_BEGIN
+    const wc::Volume &V = v->v;
+    wc::DevBuf<int64_t> d_ids;
+    wc::DevBuf<float> d_out;
+    upload(d_ids, ids, n, V.st);
+    d_out.alloc(n * 64);
+    wc::decode_blocks_device(V, d_ids.p, n, d_out.p, V.st);  // warm-up
+    cudaEvent_t a, b;
+    WC_CUDA(cudaEventCreate(&a));
+    WC_CUDA(cudaEventCreate(&b));
+    WC_CUDA(cudaEventRecord(a, V.st));
+    for (int r = 0; r < reps; r++) wc::decode_blocks_device(V, d_ids.p, n, d_out.p, V.st);
+    WC_CUDA(cudaEventRecord(b, V.st));
+    WC_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    WC_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms_per_launch = (double)ms / (reps > 0 ? reps : 1);
+    WC_API_END
+}
+
+int wc_session_create(wc_volume *v, const wc_camera *cam, const uint32_t *pixel_ids, int64_t n, const double *origins,
+                      const double *dirs, double iso, int speculation, int max_spec, int64_t cache_capacity,
+                      int corrupt_cache, wc_session **out) {
+    WC_API_BEGIN
+    WC_REQUIRE(v != nullptr, wc::UsageError, "null volume");
+    WC_REQUIRE(max_spec >= 1, wc::UsageError, "max_spec must be >= 1");
+    const bool camera_mode = dirs == nullptr;
+    if (camera_mode) {
+        WC_REQUIRE(cam != nullptr, wc::UsageError, "camera rays need a camera");
+        WC_REQUIRE(cam->img_w >= 1 && cam->img_h >= 1, wc::UsageError, "image size must be at least 1x1");
+        if (!pixel_ids) n = (int64_t)cam->img_w * cam->img_h;
+    } else {
+        WC_REQUIRE(origins != nullptr, wc::UsageError, "arbitrary rays need origins");
+    }
+    WC_REQUIRE(n >= 1, wc::UsageError, "a session needs at least one ray");
+    auto *h = new wc_session();
+    try {
+        h->s = new wc::Session(&v->v, reinterpret_cast<const wc::CameraParams *>(cam), pixel_ids, n, origins, dirs, iso, speculation, max_spec, cache_capacity,
+                               corrupt_cache);
+        h->vol = v;
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    WC_API_END
+}
+
+int wc_session_set_base_color(wc_session *s, double r, double g, double b) {
+    WC_API_BEGIN
+    s->s->base[0] = r;
+    s->s->base[1] = g;
+    s->s->base[2] = b;
+    WC_API_END
+}
+
+int wc_session_pass(wc_session *s, wc_pass_stats *stats, int *ran) {
+    WC_API_BEGIN
+    wc::PassStatsC st{};
+    const bool r = s->s->pass(st);
+    if (ran) *ran = r ? 1 : 0;
+    if (r && stats) std::memcpy(stats, &st, sizeof(st));
+    WC_API_END
+}
+
+int wc_session_run(wc_session *s, wc_pass_stats *stats_out, int64_t max_stats, int64_t *n_passes) {
+    WC_API_BEGIN
+    int64_t k = 0;
+    wc::PassStatsC st{};
+    while (s->s->pass(st)) {
+        if (stats_out && k < max_stats) std::memcpy(stats_out + k, &st, sizeof(st));
+        k++;
+    }
+    if (n_passes) *n_passes = k;
+    WC_API_END
+}
+
+int wc_session_n_active(const wc_session *s, int64_t *n_active) {
+    WC_API_BEGIN
+    *n_active = s->s->n_act;
+    WC_API_END
+}
+
+int wc_session_framebuffer(wc_session *s, uint8_t *rgba, float *depth) {
+    WC_API_BEGIN
+    s->s->download_framebuffer(rgba, depth);
+    WC_API_END
+}
+
+int wc_session_framebuffer_device(wc_session *s, void *rgba_dev, void *depth_dev) {
+    WC_API_BEGIN
+    s->s->copy_framebuffer_device(rgba_dev, depth_dev);
+    WC_API_END
+}
+
+int wc_session_last_pass_ms(const wc_session *s, double *ms) {
+    WC_API_BEGIN
+    *ms = s->s->last_kernel_ms;
+    WC_API_END
+}
+
+int wc_session_destroy(wc_session *s) {
+    WC_API_BEGIN
+    if (s) delete s->s;
+    delete s;
+    WC_API_END
+}
+
+int wc_session_sizes(const wc_session *s, int64_t *sizes) {
+    WC_API_BEGIN
+    const wc::Session &S = *s->s;
+    sizes[0] = S.last_slots_used;
+    sizes[1] = S.last_nvis;
+    sizes[2] = S.last_nactb;
+    sizes[3] = S.last_nent;
+    sizes[4] = S.last_n_spec;
+    sizes[5] = S.last_slots_used / (S.last_n_spec ? S.last_n_spec : 1);
+    sizes[6] = S.cap;
+    sizes[7] = S.phys;
+    WC_API_END
+}
+
+int wc_session_rays(const wc_session *s, double *dir, double *t_enter, double *t_exit, uint8_t *status,
+                    uint8_t *exited, uint32_t *coarse_cell, uint32_t *fine_cell, double *coarse_tmax,
+                    double *fine_tmax) {
+    WC_API_BEGIN
+    const wc::Session &S = *s->s;
+    const int64_t n = S.n;
+    download(dir, S.dir.p, 3 * n, S.st);
+    download(t_enter, S.t_enter.p, n, S.st);
+    download(t_exit, S.t_exit.p, n, S.st);
+    download(status, S.status.p, n, S.st);
+    download(exited, S.exited.p, n, S.st);
+    download(coarse_cell, S.coarse_cell.p, n, S.st);
+    download(fine_cell, S.fine_cell.p, n, S.st);
+    download(coarse_tmax, S.coarse_tmax.p, 3 * n, S.st);
+    download(fine_tmax, S.fine_tmax.p, 3 * n, S.st);
+    WC_CUDA(cudaStreamSynchronize(S.st));
+    WC_API_END
+}
+
+int wc_session_slots(const wc_session *s, uint32_t *block_slots, uint32_t *ray_slots, uint32_t *active_list) {
+    WC_API_BEGIN
+    const wc::Session &S = *s->s;
+    download(block_slots, S.block_slots.p, S.last_slots_used, S.st);
+    download(ray_slots, S.ray_slots.p, S.last_slots_used, S.st);
+    const int64_t n_prev = S.last_slots_used / (S.last_n_spec ? S.last_n_spec : 1);
+    download(active_list, S.act_list[S.cur ^ 1].p, n_prev, S.st);
+    WC_CUDA(cudaStreamSynchronize(S.st));
+    WC_API_END
+}
+
+int wc_session_blocks(const wc_session *s, uint32_t *visible_ids, uint32_t *active_ids) {
+    WC_API_BEGIN
+    const wc::Session &S = *s->s;
+    download(visible_ids, S.visible_ids.p, S.last_nvis, S.st);
+    download(active_ids, S.active_ids.p, S.last_nactb, S.st);
+    WC_CUDA(cudaStreamSynchronize(S.st));
+    WC_API_END
+}
+
+int wc_session_rt_inputs(const wc_session *s, uint32_t *block_ray_offsets, uint32_t *sorted_entries,
+                         uint32_t *entry_ray) {
+    WC_API_BEGIN
+    const wc::Session &S = *s->s;
+    if (S.last_nent > 0) download(block_ray_offsets, S.block_ray_off.p, S.last_nvis + 1, S.st);
+    else if (block_ray_offsets) block_ray_offsets[0] = 0;
+    download(sorted_entries, S.ent_val.p, S.last_nent, S.st);
+    download(entry_ray, S.ent_ray.p, S.last_nent, S.st);
+    WC_CUDA(cudaStreamSynchronize(S.st));
+    WC_API_END
+}
+
+int wc_session_rgbz(const wc_session *s, float *rgbz) {
+    WC_API_BEGIN
+    const wc::Session &S = *s->s;
+    download(reinterpret_cast<float4 *>(rgbz), S.rgbz.p, S.last_nent, S.st);
+    WC_CUDA(cudaStreamSynchronize(S.st));
+    WC_API_END
+}
+
+int wc_session_cache(const wc_session *s, int32_t *block_of_slot, int32_t *last_used, float *slot_values) {
+    WC_API_BEGIN
+    const wc::Session &S = *s->s;
+    download(block_of_slot, S.block_of_slot.p, S.phys, S.st);
+    download(last_used, S.last_used.p, S.phys, S.st);
+    download(slot_values, S.slot_values.p, S.phys * 64, S.st);
+    WC_CUDA(cudaStreamSynchronize(S.st));
+    WC_API_END
+}
+
+int wc_init_rays(const wc_camera *cam, const uint32_t *pixel_ids, int64_t n, const double *origins,
+                 const double *dirs, int nx, int ny, int nz, double *dir_out, double *t_enter, double *t_exit,
+                 uint8_t *status, uint8_t *exited, uint32_t *coarse_cell, uint32_t *fine_cell, double *coarse_tmax,
+                 double *fine_tmax) {
+    WC_API_BEGIN
+    check_dims(nx, ny, nz);
+    if (!dirs && !pixel_ids) n = (int64_t)cam->img_w * cam->img_h;
+    if (n <= 0) return WC_OK;
+    cudaStream_t st;
+    WC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    wc::DevBuf<uint32_t> d_pix, d_cc, d_fc;
+    wc::DevBuf<double> d_o, d_d, d_dir, d_te, d_tx, d_ct, d_ft;
+    wc::DevBuf<uint8_t> d_st, d_ex;
+    if (pixel_ids) upload(d_pix, pixel_ids, n, st);
+    if (dirs) {
+        upload(d_o, origins, 3 * n, st);
+        upload(d_d, dirs, 3 * n, st);
+    }
+    d_dir.alloc(3 * n);
+    d_te.alloc(n);
+    d_tx.alloc(n);
+    d_st.alloc(n);
+    d_ex.alloc(n);
+    d_cc.alloc(n);
+    d_fc.alloc(n);
+    d_ct.alloc(3 * n);
+    d_ft.alloc(3 * n);
+    wc::CameraParams cp{};
+    if (cam) std::memcpy(&cp, cam, sizeof(cp));
+    wc::init_rays_device(cam ? &cp : nullptr, pixel_ids ? d_pix.p : nullptr, n, dirs ? d_o.p : nullptr,
+                         dirs ? d_d.p : nullptr, nx, ny, nz, nullptr, d_dir.p, d_te.p, d_tx.p, d_st.p, d_ex.p,
+                         d_cc.p, d_fc.p, d_ct.p, d_ft.p, st);
+    download(dir_out, d_dir.p, 3 * n, st);
+    download(t_enter, d_te.p, n, st);
+    download(t_exit, d_tx.p, n, st);
+    download(status, d_st.p, n, st);
+    download(exited, d_ex.p, n, st);
+    download(coarse_cell, d_cc.p, n, st);
+    download(fine_cell, d_fc.p, n, st);
+    download(coarse_tmax, d_ct.p, 3 * n, st);
+    download(fine_tmax, d_ft.p, 3 * n, st);
+    WC_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    WC_API_END
+}
+
+int wc_reference_render(const wc_volume *v, const double *origins, const double *dirs, int64_t n, double iso,
+                        double base_r, double base_g, double base_b, uint8_t *rgba, float *depth) {
+    WC_API_BEGIN
+    const wc::Volume &V = v->v;
+    if (n <= 0) return WC_OK;
+    wc::DevBuf<float> dense;
+    dense.alloc((int64_t)V.nx * V.ny * V.nz);
+    wc::decode_full_device(V, dense.p, V.st);
+    wc::DevBuf<double> d_o, d_d;
+    upload(d_o, origins, 3 * n, V.st);
+    upload(d_d, dirs, 3 * n, V.st);
+    wc::DevBuf<uint32_t> d_rgba;
+    wc::DevBuf<float> d_depth;
+    d_rgba.alloc(n);
+    d_depth.alloc(n);
+    wc::reference_render_device(dense.p, V.nx, V.ny, V.nz, d_o.p, d_d.p, n, iso, base_r, base_g, base_b, d_rgba.p,
+                                d_depth.p, V.st);
+    download(reinterpret_cast<uint32_t *>(rgba), d_rgba.p, n, V.st);
+    download(depth, d_depth.p, n, V.st);
+    WC_CUDA(cudaStreamSynchronize(V.st));
+    WC_API_END
+}
+
+int wc_reference_render_dense(const float *values, int nx, int ny, int nz, const double *origins, const double *dirs,
+                              int64_t n, double iso, double base_r, double base_g, double base_b, uint8_t *rgba,
+                              float *depth) {
+    WC_API_BEGIN
+    check_dims(nx, ny, nz);
+    if (n <= 0) return WC_OK;
+    cudaStream_t st;
+    WC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    wc::DevBuf<float> dense, d_depth;
+    wc::DevBuf<double> d_o, d_d;
+    wc::DevBuf<uint32_t> d_rgba;
+    upload(dense, values, (int64_t)nx * ny * nz, st);
+    upload(d_o, origins, 3 * n, st);
+    upload(d_d, dirs, 3 * n, st);
+    d_rgba.alloc(n);
+    d_depth.alloc(n);
+    wc::reference_render_device(dense.p, nx, ny, nz, d_o.p, d_d.p, n, iso, base_r, base_g, base_b, d_rgba.p,
+                                d_depth.p, st);
+    download(reinterpret_cast<uint32_t *>(rgba), d_rgba.p, n, st);
+    download(depth, d_depth.p, n, st);
+    WC_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    WC_API_END
+}
+
+int wc_exclusive_scan(const uint32_t *values, int64_t n, uint32_t *out, uint64_t *total) {
+    WC_API_BEGIN
+    if (n <= 0) {
+        if (total) *total = 0;
+        return WC_OK;
+    }
+    cudaStream_t st;
+    WC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    wc::DevBuf<uint32_t> d_in, d_out, d_part, d_tot;
+    upload(d_in, values, n, st);
+    d_out.alloc(n);
+    d_part.alloc(wc::scan_tiles(n));
+    d_tot.alloc(1);
+    wc::scan_exclusive(wc::LoadU32{d_in.p}, n, d_out.p, d_tot.p, d_part.p, st);
+    uint32_t t = 0;
+    download(out, d_out.p, n, st);
+    download(&t, d_tot.p, 1, st);
+    WC_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    if (total) *total = t;
+    WC_API_END
+}
+
+int wc_sort_by_key(uint32_t *keys, uint32_t *values, int64_t n) {
+    WC_API_BEGIN
+    if (n <= 1) return WC_OK;
+    cudaStream_t st;
+    WC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    wc::DevBuf<uint32_t> dk, dv;
+    upload(dk, keys, n, st);
+    upload(dv, values, n, st);
+    wc::RadixScratch rs;
+    wc::radix_sort_pairs(dk.p, dv.p, n, 32, rs, st);
+    download(keys, dk.p, n, st);
+    download(values, dv.p, n, st);
+    WC_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    WC_API_END
+}
+
+}  // extern "C"

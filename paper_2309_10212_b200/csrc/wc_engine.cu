@@ -1,0 +1,978 @@
+// wc_engine.cu -- per-pass wavefront pipeline on sm_100a (engine.py:308-382).
+//
+// One pass = traverse (+ fused visibility marking) -> scan of emitted
+// counts -> visible-id extraction from the bitmap -> +octant active marking
+// -> LRU residency with fused decode -> stable radix grouping of entries by
+// visible block -> warp-per-block dual-grid raytrace -> min-depth composite
+// + compaction of surviving rays.  Three small host reads per pass (entry /
+// block counts, miss / free counts, surviving-ray count).
+#include <math_constants.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "wc_engine.cuh"
+#include "wc_trace.cuh"
+
+namespace wc {
+
+// --------------------------------------------------------------- ray setup
+
+struct RayInitArgs {
+    CameraParams cam;
+    const uint32_t *pixel_ids;   // nullable: identity
+    const double *origin_in;     // nullable: camera rays
+    const double *dir_in;        // nullable: camera rays
+    int nx, ny, nz;
+};
+
+// traversal.py:105-187 (from_camera + from_rays + _tmax_init) for ray r.
+__global__ void k_init_rays(RayInitArgs a, int64_t n, double *origin_out, double *dir, double *t_enter, double *t_exit,
+                            uint8_t *status, uint8_t *exited, uint32_t *coarse_cell, uint32_t *fine_cell,
+                            double *coarse_tmax, double *fine_tmax, uint32_t *rgba, float *depth) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        double o[3], d[3];
+        if (a.dir_in) {
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+                o[k] = a.origin_in[3 * r + k];
+                d[k] = a.dir_in[3 * r + k];
+            }
+        } else {
+            const int64_t p = a.pixel_ids ? (int64_t)a.pixel_ids[r] : r;
+            const int64_t w = a.cam.img_w, h = a.cam.img_h;
+            const int64_t px = p % w, py = p / w;
+            const double aspect = (double)w / (double)h;
+            const double xs = ((2.0 * ((double)px + 0.5)) / (double)w - 1.0) * a.cam.tan_half * aspect;
+            const double ys = (1.0 - (2.0 * ((double)py + 0.5)) / (double)h) * a.cam.tan_half;
+#pragma unroll
+            for (int k = 0; k < 3; k++) d[k] = (a.cam.look[k] + xs * a.cam.right[k]) + ys * a.cam.up[k];
+            const double nrm = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+                d[k] = d[k] / nrm;
+                o[k] = a.cam.eye[k];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            dir[3 * r + k] = d[k];
+            if (origin_out) origin_out[3 * r + k] = o[k];
+        }
+        const double hi[3] = {(double)a.nx - 1.0, (double)a.ny - 1.0, (double)a.nz - 1.0};
+        const int fd[3] = {(a.nx + 3) / 4, (a.ny + 3) / 4, (a.nz + 3) / 4};
+        const int cd[3] = {(fd[0] + 3) / 4, (fd[1] + 3) / 4, (fd[2] + 3) / 4};
+        double nr[3], fr[3];
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            if (d[k] != 0.0) {
+                const double t1 = (0.0 - o[k]) / d[k];
+                const double t2 = (hi[k] - o[k]) / d[k];
+                nr[k] = t1 < t2 ? t1 : t2;  // np.minimum
+                fr[k] = t1 > t2 ? t1 : t2;  // np.maximum
+            } else if (o[k] < 0.0 || o[k] > hi[k]) {
+                nr[k] = CUDART_INF;
+                fr[k] = -CUDART_INF;
+            } else {
+                nr[k] = -CUDART_INF;
+                fr[k] = CUDART_INF;
+            }
+        }
+        double t_near = nr[0] > nr[1] ? nr[0] : nr[1];
+        t_near = t_near > nr[2] ? t_near : nr[2];
+        double t_far = fr[0] < fr[1] ? fr[0] : fr[1];
+        t_far = t_far < fr[2] ? t_far : fr[2];
+        const bool hit = (t_near <= t_far) && (t_far >= 0.0);
+        const double te = t_near > 0.0 ? t_near : 0.0;
+        t_enter[r] = te;
+        t_exit[r] = t_far;
+        status[r] = hit ? 0 : 2;
+        exited[r] = 0;
+        uint32_t fcell = WC_UINT_MAX, ccell = WC_UINT_MAX;
+        double ft[3] = {0.0, 0.0, 0.0}, ct[3] = {0.0, 0.0, 0.0};
+        if (hit) {
+            int fc[3], cc[3];
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+                const double p0 = o[k] + d[k] * (te + kEntryEps);
+                int c = (int)floor(p0 / 4.0);
+                c = c < 0 ? 0 : (c > fd[k] - 1 ? fd[k] - 1 : c);
+                fc[k] = c;
+                cc[k] = c / 4;
+                if (d[k] == 0.0) {
+                    ft[k] = CUDART_INF;
+                    ct[k] = CUDART_INF;
+                } else {
+                    const double flo = (double)c * 4.0, clo = (double)cc[k] * 16.0;
+                    ft[k] = ((d[k] > 0 ? flo + 4.0 : flo) - o[k]) / d[k];
+                    ct[k] = ((d[k] > 0 ? clo + 16.0 : clo) - o[k]) / d[k];
+                }
+            }
+            fcell = (uint32_t)(fc[0] + fd[0] * (fc[1] + fd[1] * fc[2]));
+            ccell = (uint32_t)(cc[0] + cd[0] * (cc[1] + cd[1] * cc[2]));
+        }
+        fine_cell[r] = fcell;
+        coarse_cell[r] = ccell;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            fine_tmax[3 * r + k] = ft[k];
+            coarse_tmax[3 * r + k] = ct[k];
+        }
+        if (rgba) {
+            rgba[r] = 0xFF000000u;  // BACKGROUND_RGBA (engine.py:29)
+            depth[r] = CUDART_INF_F;
+        }
+    }
+}
+
+void init_rays_device(const CameraParams *cam, const uint32_t *d_pixel_ids, int64_t n, const double *d_origin_in,
+                      const double *d_dir_in, int nx, int ny, int nz, double *d_origin_out, double *d_dir,
+                      double *t_enter, double *t_exit, uint8_t *status, uint8_t *exited, uint32_t *coarse_cell,
+                      uint32_t *fine_cell, double *coarse_tmax, double *fine_tmax, cudaStream_t st) {
+    RayInitArgs a{};
+    if (cam) a.cam = *cam;
+    a.pixel_ids = d_pixel_ids;
+    a.origin_in = d_origin_in;
+    a.dir_in = d_dir_in;
+    a.nx = nx;
+    a.ny = ny;
+    a.nz = nz;
+    k_init_rays<<<grid_for(n, 256), 256, 0, st>>>(a, n, d_origin_out, d_dir, t_enter, t_exit, status, exited,
+                                                  coarse_cell, fine_cell, coarse_tmax, fine_tmax, nullptr, nullptr);
+    WC_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------- compaction glue
+
+struct PredActive {  // status == STATUS_ACTIVE
+    const uint8_t *s;
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const { return s[i] == 0; }
+};
+struct PredMiss {  // active block not resident (cache.py:69-72)
+    const uint32_t *ids;
+    const int32_t *slot_of_block;
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const { return slot_of_block[ids[i]] < 0; }
+};
+struct PredFree {  // cache.py:79
+    const int32_t *bos;
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const { return bos[i] < 0; }
+};
+struct PredCand {  // resident, not stamped this pass (cache.py:84-87)
+    const int32_t *bos, *lu;
+    int32_t pass_no;
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const { return bos[i] >= 0 && lu[i] < pass_no; }
+};
+
+template <class Pred>
+__global__ void k_compact_index(Pred pred, int64_t n, const uint32_t *off, uint32_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (pred(i)) out[off[i]] = (uint32_t)i;
+}
+
+__global__ void k_compact_keep(const uint32_t *keep, const uint32_t *off, const uint32_t *in, int64_t n, uint32_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (keep[i]) out[off[i]] = in[i];
+}
+
+__global__ void k_compact_miss(PredMiss pred, int64_t n, const uint32_t *off, uint32_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (pred(i)) out[off[i]] = pred.ids[i];
+}
+
+__global__ void k_compact_cand(PredCand pred, int64_t n, const uint32_t *off, uint32_t *key, uint32_t *val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (pred(i)) {
+            key[off[i]] = (uint32_t)pred.bos[i];
+            val[off[i]] = (uint32_t)i;
+        }
+}
+
+// --------------------------------------------------------------- traverse
+
+struct RayView {
+    const double *origin;  // nullable -> eye
+    const double *dir, *t_enter;
+    double ex, ey, ez;
+    __device__ __forceinline__ void load(int64_t r, double o[3], double d[3]) const {
+        if (origin) {
+            o[0] = origin[3 * r];
+            o[1] = origin[3 * r + 1];
+            o[2] = origin[3 * r + 2];
+        } else {
+            o[0] = ex;
+            o[1] = ey;
+            o[2] = ez;
+        }
+        d[0] = dir[3 * r];
+        d[1] = dir[3 * r + 1];
+        d[2] = dir[3 * r + 2];
+    }
+};
+
+struct TraverseArgs {
+    RayView rays;
+    const double *t_exit;
+    uint8_t *exited;
+    uint32_t *coarse_cell, *fine_cell;
+    double *coarse_tmax, *fine_tmax;
+    const uint32_t *act_list;
+    int64_t n_act;
+    int n_spec;
+    const double2 *fine_mm, *coarse_mm;
+    int fdx, fdy, fdz, cdx, cdy, cdz;
+    double iso;
+    uint32_t *block_slots, *ray_slots, *emitted, *vis_bm;
+};
+
+// Mark block b visible: one RED.OR per distinct block among the lanes that
+// emit together (warp match), traversal emission fused with mark_blocks
+// (engine.py:97-106).
+__device__ __forceinline__ void mark_visible(uint32_t *bm, uint32_t b) {
+    const uint32_t active = __activemask();
+    const uint32_t peers = __match_any_sync(active, b);
+    const int lane = threadIdx.x & 31;
+    if ((peers & ((1u << lane) - 1u)) == 0) atomicOr(&bm[b >> 5], 1u << (b & 31));
+}
+
+// traversal.py:217-403 _traverse_kernel, one thread per active ray.
+__global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n_act; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = a.act_list[i];
+        double o[3], d[3];
+        a.rays.load(r, o, d);
+        const double ox = o[0], oy = o[1], oz = o[2], dx = d[0], dy = d[1], dz = d[2];
+        const double te = a.t_exit[r];
+        const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
+        const double iso = a.iso;
+        const int sx = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
+        const int sy = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
+        const int sz = dz > 0.0 ? 1 : (dz < 0.0 ? -1 : 0);
+        const double fdel_x = dx != 0.0 ? 4.0 / fabs(dx) : CUDART_INF;
+        const double fdel_y = dy != 0.0 ? 4.0 / fabs(dy) : CUDART_INF;
+        const double fdel_z = dz != 0.0 ? 4.0 / fabs(dz) : CUDART_INF;
+        const double cdel_x = dx != 0.0 ? 16.0 / fabs(dx) : CUDART_INF;
+        const double cdel_y = dy != 0.0 ? 16.0 / fabs(dy) : CUDART_INF;
+        const double cdel_z = dz != 0.0 ? 16.0 / fabs(dz) : CUDART_INF;
+        const uint32_t cc = a.coarse_cell[r];
+        int ccx = (int)(cc % (uint32_t)cdx), ccy = (int)((cc / (uint32_t)cdx) % (uint32_t)cdy),
+            ccz = (int)(cc / ((uint32_t)cdx * (uint32_t)cdy));
+        double ctx = a.coarse_tmax[3 * r], cty = a.coarse_tmax[3 * r + 1], ctz = a.coarse_tmax[3 * r + 2];
+        const uint32_t fc = a.fine_cell[r];
+        bool in_fine_run = fc != WC_UINT_MAX;
+        int fcx = 0, fcy = 0, fcz = 0;
+        if (in_fine_run) {
+            fcx = (int)(fc % (uint32_t)fdx);
+            fcy = (int)((fc / (uint32_t)fdx) % (uint32_t)fdy);
+            fcz = (int)(fc / ((uint32_t)fdx * (uint32_t)fdy));
+        }
+        double ftx = a.fine_tmax[3 * r], fty = a.fine_tmax[3 * r + 1], ftz = a.fine_tmax[3 * r + 2];
+        const int64_t base = i * (int64_t)a.n_spec;
+        int emitted = 0;
+        bool ray_done = false;
+        double t_cross;
+        for (;;) {
+            if (in_fine_run) {
+                for (;;) {
+                    const int f_lin = fcx + fdx * (fcy + fdy * fcz);
+                    const double2 mm = a.fine_mm[f_lin];
+                    if (mm.x <= iso && iso <= mm.y) {
+                        a.block_slots[base + emitted] = (uint32_t)f_lin;
+                        a.ray_slots[base + emitted] = (uint32_t)r;
+                        emitted++;
+                        mark_visible(a.vis_bm, (uint32_t)f_lin);
+                    }
+                    if (ftx <= fty && ftx <= ftz) {
+                        t_cross = ftx;
+                        fcx += sx;
+                        ftx += fdel_x;
+                    } else if (fty <= ftz) {
+                        t_cross = fty;
+                        fcy += sy;
+                        fty += fdel_y;
+                    } else {
+                        t_cross = ftz;
+                        fcz += sz;
+                        ftz += fdel_z;
+                    }
+                    if (t_cross > te || fcx < 0 || fcx >= fdx || fcy < 0 || fcy >= fdy || fcz < 0 || fcz >= fdz) {
+                        in_fine_run = false;
+                        ray_done = true;
+                    } else if ((fcx >> 2) != ccx || (fcy >> 2) != ccy || (fcz >> 2) != ccz) {
+                        in_fine_run = false;
+                    }
+                    if (emitted == a.n_spec || !in_fine_run) break;
+                }
+                if (emitted == a.n_spec || ray_done) break;
+            }
+            if (ctx <= cty && ctx <= ctz) {
+                t_cross = ctx;
+                ccx += sx;
+                ctx += cdel_x;
+            } else if (cty <= ctz) {
+                t_cross = cty;
+                ccy += sy;
+                cty += cdel_y;
+            } else {
+                t_cross = ctz;
+                ccz += sz;
+                ctz += cdel_z;
+            }
+            if (t_cross > te || ccx < 0 || ccx >= cdx || ccy < 0 || ccy >= cdy || ccz < 0 || ccz >= cdz) {
+                ray_done = true;
+                break;
+            }
+            const int c_lin = ccx + cdx * (ccy + cdy * ccz);
+            const double2 cm = a.coarse_mm[c_lin];
+            if (cm.x <= iso && iso <= cm.y) {
+                const double px = ox + dx * t_cross, py = oy + dy * t_cross, pz = oz + dz * t_cross;
+                const int lo_x = 4 * ccx, lo_y = 4 * ccy, lo_z = 4 * ccz;
+                const int hi_x = min(lo_x + 3, fdx - 1), hi_y = min(lo_y + 3, fdy - 1), hi_z = min(lo_z + 3, fdz - 1);
+                fcx = (int)floor(px / 4.0);
+                fcy = (int)floor(py / 4.0);
+                fcz = (int)floor(pz / 4.0);
+                fcx = fcx < lo_x ? lo_x : (fcx > hi_x ? hi_x : fcx);
+                fcy = fcy < lo_y ? lo_y : (fcy > hi_y ? hi_y : fcy);
+                fcz = fcz < lo_z ? lo_z : (fcz > hi_z ? hi_z : fcz);
+                ftx = dx > 0.0 ? ((double)(fcx + 1) * 4.0 - ox) / dx : (dx < 0.0 ? ((double)fcx * 4.0 - ox) / dx : CUDART_INF);
+                fty = dy > 0.0 ? ((double)(fcy + 1) * 4.0 - oy) / dy : (dy < 0.0 ? ((double)fcy * 4.0 - oy) / dy : CUDART_INF);
+                ftz = dz > 0.0 ? ((double)(fcz + 1) * 4.0 - oz) / dz : (dz < 0.0 ? ((double)fcz * 4.0 - oz) / dz : CUDART_INF);
+                in_fine_run = true;
+            }
+        }
+        for (int k = emitted; k < a.n_spec; k++) {  // traversal.py:423-424 sentinels
+            a.block_slots[base + k] = WC_UINT_MAX;
+            a.ray_slots[base + k] = WC_UINT_MAX;
+        }
+        a.emitted[i] = (uint32_t)emitted;
+        if (ray_done) {
+            a.exited[r] = 1;
+            a.coarse_cell[r] = WC_UINT_MAX;
+            a.fine_cell[r] = WC_UINT_MAX;
+        } else {
+            a.coarse_cell[r] = (uint32_t)(ccx + cdx * (ccy + cdy * ccz));
+            a.fine_cell[r] = in_fine_run ? (uint32_t)(fcx + fdx * (fcy + fdy * fcz)) : WC_UINT_MAX;
+        }
+        a.coarse_tmax[3 * r] = ctx;
+        a.coarse_tmax[3 * r + 1] = cty;
+        a.coarse_tmax[3 * r + 2] = ctz;
+        a.fine_tmax[3 * r] = ftx;
+        a.fine_tmax[3 * r + 1] = fty;
+        a.fine_tmax[3 * r + 2] = ftz;
+    }
+}
+
+// ------------------------------------------------------------------ marking
+
+// engine.py:107-117: each visible block activates itself and its existing
+// +octant neighbours.  Count-driven (reads *d_nvis) so no host round trip.
+__global__ void k_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvis, int bdx, int bdy, int bdz,
+                              uint32_t *act_bm) {
+    const int64_t nvis = *d_nvis;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nvis * 8; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = visible_ids[t >> 3];
+        const int o = (int)(t & 7), ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+        const int bx = (int)(b % (uint32_t)bdx), by = (int)((b / (uint32_t)bdx) % (uint32_t)bdy),
+                  bz = (int)(b / ((uint32_t)bdx * (uint32_t)bdy));
+        if (bx + ox >= bdx || by + oy >= bdy || bz + oz >= bdz) continue;
+        const uint32_t nid = (uint32_t)((bx + ox) + bdx * ((by + oy) + bdy * (bz + oz)));
+        atomicOr(&act_bm[nid >> 5], 1u << (nid & 31));
+    }
+}
+
+// Entries of active ray i: k = entry_off[i] + j for its j-th emitted slot
+// (== valid_prefix of the slot, engine.py:124-128).  Key = rank of the block
+// among visible ids (bitmap rank), value = k.
+__global__ void k_build_entries(int64_t n_act, int n_spec, const uint32_t *act_list, const uint32_t *emitted,
+                                const uint32_t *entry_off, const uint32_t *block_slots, const uint32_t *vis_bm,
+                                const uint32_t *vis_word_off, uint32_t *ent_key, uint32_t *ent_val, uint32_t *ent_ray) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_act; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t ne = emitted[i], eo = entry_off[i], r = act_list[i];
+        for (uint32_t j = 0; j < ne; j++) {
+            const uint32_t b = block_slots[i * (int64_t)n_spec + j];
+            const uint32_t w = b >> 5;
+            const uint32_t rank = vis_word_off[w] + __popc(vis_bm[w] & ((1u << (b & 31)) - 1u));
+            ent_key[eo + j] = rank;
+            ent_val[eo + j] = eo + j;
+            ent_ray[eo + j] = r;
+        }
+    }
+}
+
+// Run starts of the sorted keys -> block_ray_offsets (engine.py:133-139).
+__global__ void k_run_offsets(const uint32_t *key, int64_t n, int64_t nvis, uint32_t *off) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i == 0 || key[i] != key[i - 1]) off[key[i]] = (uint32_t)i;
+        if (i == 0) off[nvis] = (uint32_t)n;
+    }
+}
+
+// ---------------------------------------------------------------- cache
+
+__global__ void k_cache_stamp(const uint32_t *ids, int64_t n, const int32_t *slot_of_block, int32_t *last_used,
+                              int32_t pass_no) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t s = slot_of_block[ids[i]];
+        if (s >= 0) last_used[s] = pass_no;  // cache.py:73-74
+    }
+}
+
+__global__ void k_gather_last_used(const uint32_t *val, int64_t n, const int32_t *last_used, uint32_t *key) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        key[i] = (uint32_t)last_used[val[i]];
+}
+
+// cache.py:90-96: unmap the first n_evict candidates, append to the free list
+__global__ void k_evict(const uint32_t *victims, int64_t n_evict, int64_t n_free, int32_t *block_of_slot,
+                        int32_t *slot_of_block, uint32_t *free_slots) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_evict; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = victims[i];
+        slot_of_block[block_of_slot[s]] = -1;
+        block_of_slot[s] = -1;
+        free_slots[n_free + i] = s;
+    }
+}
+
+// cache.py:97-103 fused with codec.py:143-174: decode each miss straight
+// into its slot and publish the mapping.  Warp per block.
+__global__ void __launch_bounds__(256) k_decode_insert(const uint8_t *__restrict__ payload, int qbits, int stride,
+                                                       const uint32_t *__restrict__ miss_ids,
+                                                       const uint32_t *__restrict__ free_slots, int64_t n_miss,
+                                                       float *__restrict__ slot_values, int32_t *block_of_slot,
+                                                       int32_t *last_used, int32_t *slot_of_block, int32_t pass_no) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = warp0; j < n_miss; j += nwarps) {
+        const uint32_t b = miss_ids[j], s = free_slots[j];
+        const uint32_t *rec = reinterpret_cast<const uint32_t *>(payload + (int64_t)b * stride);
+        const BlockDecodeParams p = decode_params(rec, qbits);
+        float v0 = 0.0f, v1 = 0.0f;
+        if (!p.zero) {
+            v0 = decode_value(rec, lane, qbits, p.e, p.fast, p.pow2f, p.sf, p.sd, p.scale_d);
+            v1 = decode_value(rec, lane + 32, qbits, p.e, p.fast, p.pow2f, p.sf, p.sd, p.scale_d);
+        }
+        float *dst = slot_values + (int64_t)s * 64;
+        dst[lane] = v0;
+        dst[lane + 32] = v1;
+        if (lane == 0) {
+            block_of_slot[s] = (int32_t)b;
+            last_used[s] = pass_no;
+            slot_of_block[b] = (int32_t)s;
+        }
+    }
+}
+
+// -------------------------------------------------------------- raytrace
+
+struct DualField {  // 5x5x5 dual grid in shared memory, [z][y][x]
+    const float *p;
+    __device__ __forceinline__ void corners(int lx, int ly, int lz, float c[8]) const {
+        const float *q = p + lx + 5 * ly + 25 * lz;
+        c[0] = q[0];
+        c[1] = q[1];
+        c[2] = q[5];
+        c[3] = q[6];
+        c[4] = q[25];
+        c[5] = q[26];
+        c[6] = q[30];
+        c[7] = q[31];
+    }
+};
+
+struct DenseFieldView {  // fully decoded volume, x-fastest
+    const float *p;
+    int64_t sy, sz;
+    __device__ __forceinline__ void corners(int lx, int ly, int lz, float c[8]) const {
+        const float *q = p + lx + sy * ly + sz * lz;
+        c[0] = q[0];
+        c[1] = q[1];
+        c[2] = q[sy];
+        c[3] = q[sy + 1];
+        c[4] = q[sz];
+        c[5] = q[sz + 1];
+        c[6] = q[sz + sy];
+        c[7] = q[sz + sy + 1];
+    }
+};
+
+struct RaytraceArgs {
+    const uint32_t *visible_ids, *block_ray_off, *ent_val, *ent_ray;
+    int64_t nvis;
+    const int32_t *slot_of_block;
+    const float *slot_values;
+    int bdx, bdy, bdz, nx, ny, nz;
+    RayView rays;
+    double iso, br, bg, bb;
+    float4 *rgbz;
+    uint32_t *err;
+};
+
+// engine.py:161-219 _raytrace_visible_kernel: one warp per visible block.
+// The block's 5^3 dual grid (blocktrace.py:49-94, contributor slots from
+// engine.py:286-305) is assembled once in shared memory; the warp's lanes
+// then trace the block's ray entries (blocktrace.py:317-449).
+__global__ void __launch_bounds__(256) k_raytrace(RaytraceArgs a) {
+    __shared__ float dual[8][128];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    float *dg = dual[wib];
+    for (int64_t v = warp0; v < a.nvis; v += nwarps) {
+        const uint32_t b = a.visible_ids[v];
+        const int bx = (int)(b % (uint32_t)a.bdx), by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy),
+                  bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
+        int my_slot = -1;
+        if (lane < 8) {
+            const int ox = lane & 1, oy = (lane >> 1) & 1, oz = lane >> 2;
+            if (bx + ox < a.bdx && by + oy < a.bdy && bz + oz < a.bdz)
+                my_slot = a.slot_of_block[(bx + ox) + a.bdx * ((by + oy) + a.bdy * (bz + oz))];
+        }
+        int slots[8];
+#pragma unroll
+        for (int o = 0; o < 8; o++) slots[o] = __shfl_sync(0xffffffffu, my_slot, o);
+        if (slots[0] < 0 && lane == 0) atomicAdd(a.err, 1u);  // "visible block not resident"
+        for (int idx = lane; idx < 125; idx += 32) {
+            const int i = idx % 5, j = (idx / 5) % 5, k = idx / 25;
+            const int sl = slots[(i == 4) + 2 * (j == 4) + 4 * (k == 4)];
+            dg[idx] = sl >= 0 ? a.slot_values[(int64_t)sl * 64 + (i & 3) + 4 * (j & 3) + 16 * (k & 3)] : 0.0f;
+        }
+        __syncwarp();
+        const int cx = max(0, min(4, a.nx - 1 - 4 * bx));
+        const int cy = max(0, min(4, a.ny - 1 - 4 * by));
+        const int cz = max(0, min(4, a.nz - 1 - 4 * bz));
+        const uint32_t start = a.block_ray_off[v], end = a.block_ray_off[v + 1];
+        const DualField field{dg};
+        for (uint32_t e = start + lane; e < end; e += 32) {
+            const uint32_t k = a.ent_val[e];
+            const int64_t r = a.ent_ray[k];
+            double o[3], d[3];
+            a.rays.load(r, o, d);
+            float rgb[3];
+            const double t = trace_region(field, 4 * bx, 4 * by, 4 * bz, 4 * bx, 4 * by, 4 * bz, cx, cy, cz, o, d,
+                                          a.rays.t_enter[r], a.iso, a.br, a.bg, a.bb, rgb);
+            a.rgbz[k] = t != CUDART_INF ? make_float4(rgb[0], rgb[1], rgb[2], (float)t)
+                                        : make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------- composite
+
+// engine.py:222-258 _composite_kernel: closest speculated hit per active
+// ray (strict <, earliest entry wins ties), then terminate or keep.
+__global__ void k_composite(int64_t n_act, const uint32_t *act_list, const uint32_t *emitted, const uint32_t *entry_off,
+                            const float4 *rgbz, const uint8_t *exited, uint8_t *status, uint32_t *rgba, float *depth,
+                            uint32_t *keep) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_act; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = act_list[i], ne = emitted[i], eo = entry_off[i];
+        float best = CUDART_INF_F;
+        int64_t bk = -1;
+        for (uint32_t j = 0; j < ne; j++) {
+            const float z = rgbz[eo + j].w;
+            if (z < best) {
+                best = z;
+                bk = eo + j;
+            }
+        }
+        uint32_t kp = 0;
+        if (bk >= 0) {
+            const float4 c = rgbz[bk];
+            depth[r] = best;
+            rgba[r] = rgb_u8((double)c.x) | (rgb_u8((double)c.y) << 8) | (rgb_u8((double)c.z) << 16) | 0xFF000000u;
+            status[r] = 1;
+        } else if (exited[r] == 1) {
+            status[r] = 2;
+        } else {
+            kp = 1;
+        }
+        keep[i] = kp;
+    }
+}
+
+// ------------------------------------------------------------ brute force
+
+__global__ void __launch_bounds__(128) k_reference_render(const float *values, int nx, int ny, int nz,
+                                                          const double *origin, const double *dir, int64_t n,
+                                                          double iso, double br, double bg, double bb, uint32_t *rgba,
+                                                          float *depth) {
+    const DenseFieldView field{values, nx, (int64_t)nx * ny};
+    const double hi[3] = {(double)nx - 1.0, (double)ny - 1.0, (double)nz - 1.0};
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        double o[3], d[3];
+        for (int k = 0; k < 3; k++) {
+            o[k] = origin[3 * r + k];
+            d[k] = dir[3 * r + k];
+        }
+        // RaySoA.from_rays status / t_enter (traversal.py:132-154)
+        double nr[3], fr[3];
+        for (int k = 0; k < 3; k++) {
+            if (d[k] != 0.0) {
+                const double t1 = (0.0 - o[k]) / d[k], t2 = (hi[k] - o[k]) / d[k];
+                nr[k] = t1 < t2 ? t1 : t2;
+                fr[k] = t1 > t2 ? t1 : t2;
+            } else if (o[k] < 0.0 || o[k] > hi[k]) {
+                nr[k] = CUDART_INF;
+                fr[k] = -CUDART_INF;
+            } else {
+                nr[k] = -CUDART_INF;
+                fr[k] = CUDART_INF;
+            }
+        }
+        double t_near = nr[0] > nr[1] ? nr[0] : nr[1];
+        t_near = t_near > nr[2] ? t_near : nr[2];
+        double t_far = fr[0] < fr[1] ? fr[0] : fr[1];
+        t_far = t_far < fr[2] ? t_far : fr[2];
+        rgba[r] = 0xFF000000u;
+        depth[r] = CUDART_INF_F;
+        if (!((t_near <= t_far) && (t_far >= 0.0))) continue;
+        const double te = t_near > 0.0 ? t_near : 0.0;
+        double rgb[3];
+        const double t = trace_region(field, 0, 0, 0, 0, 0, 0, nx - 1, ny - 1, nz - 1, o, d, te, iso, br, bg, bb, rgb);
+        if (t != CUDART_INF) {
+            depth[r] = (float)t;
+            rgba[r] = rgb_u8(rgb[0]) | (rgb_u8(rgb[1]) << 8) | (rgb_u8(rgb[2]) << 16) | 0xFF000000u;
+        }
+    }
+}
+
+void reference_render_device(const float *d_values, int nx, int ny, int nz, const double *d_origin,
+                             const double *d_dir, int64_t n, double iso, double br, double bg, double bb,
+                             uint32_t *d_rgba, float *d_depth, cudaStream_t st) {
+    if (n <= 0) return;
+    k_reference_render<<<grid_for(n, 128, 16), 128, 0, st>>>(d_values, nx, ny, nz, d_origin, d_dir, n, iso, br, bg,
+                                                             bb, d_rgba, d_depth);
+    WC_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------ session
+
+static int bits_for(uint64_t max_value) {
+    int b = 0;
+    while (b < 64 && (max_value >> b)) b++;
+    return b;
+}
+
+Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, int64_t n_rays,
+                 const double *origins, const double *dirs, double iso_, int speculation_, int max_spec_,
+                 int64_t cache_capacity, int corrupt_)
+    : vol(v), n(n_rays), iso(iso_), speculation(speculation_), max_spec(max_spec_), corrupt(corrupt_) {
+    if (n < 1) throw UsageError("a session needs at least one ray");
+    WC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    WC_CUDA(cudaEventCreate(&ev_begin));
+    WC_CUDA(cudaEventCreate(&ev_end));
+    uniform_origin = dirs == nullptr;
+    if (cam) {
+        eye[0] = cam->eye[0];
+        eye[1] = cam->eye[1];
+        eye[2] = cam->eye[2];
+    }
+    dir.alloc(n * 3);
+    if (!uniform_origin) origin.alloc(n * 3);
+    t_enter.alloc(n);
+    t_exit.alloc(n);
+    coarse_tmax.alloc(n * 3);
+    fine_tmax.alloc(n * 3);
+    status.alloc(n);
+    exited.alloc(n);
+    coarse_cell.alloc(n);
+    fine_cell.alloc(n);
+    act_list[0].alloc(n);
+    act_list[1].alloc(n);
+    keep.alloc(n);
+    keep_off.alloc(n);
+    emitted.alloc(n);
+    entry_off.alloc(n);
+    block_slots.alloc(n);
+    ray_slots.alloc(n);
+    ent_key.alloc(n);
+    ent_val.alloc(n);
+    ent_ray.alloc(n);
+    rgbz.alloc(n);
+    visible_ids.alloc(n);
+    block_ray_off.alloc(n + 1);
+    rgba.alloc(n);
+    depth.alloc(n);
+    const int64_t nwords = ceil_div(vol->n_blocks, 32);
+    vis_bm.alloc(nwords);
+    act_bm.alloc(nwords);
+    vis_word_off.alloc(nwords);
+    act_word_off.alloc(nwords);
+    WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
+    WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
+    active_ids.alloc(std::min<int64_t>(8 * n, vol->n_blocks) + 1);
+    miss_off.alloc(active_ids.n);
+    miss_ids.alloc(active_ids.n);
+    counters.alloc(C_COUNT);
+    WC_CUDA(cudaMemsetAsync(counters.p, 0, 4 * C_COUNT, st));
+    h_counters.alloc(C_COUNT);
+    partials.alloc(scan_tiles(std::max<int64_t>({n, nwords, active_ids.n, 1})) + 8);
+
+    // device copies of the inputs
+    DevBuf<uint32_t> d_pix;
+    DevBuf<double> d_o, d_d;
+    if (pixel_ids) {
+        d_pix.alloc(n);
+        WC_CUDA(cudaMemcpyAsync(d_pix.p, pixel_ids, 4 * n, cudaMemcpyHostToDevice, st));
+    }
+    if (dirs) {
+        d_o.alloc(3 * n);
+        d_d.alloc(3 * n);
+        WC_CUDA(cudaMemcpyAsync(d_o.p, origins, 24 * n, cudaMemcpyHostToDevice, st));
+        WC_CUDA(cudaMemcpyAsync(d_d.p, dirs, 24 * n, cudaMemcpyHostToDevice, st));
+    }
+    RayInitArgs a{};
+    if (cam) a.cam = *cam;
+    a.pixel_ids = pixel_ids ? d_pix.p : nullptr;
+    a.origin_in = dirs ? d_o.p : nullptr;
+    a.dir_in = dirs ? d_d.p : nullptr;
+    a.nx = vol->nx;
+    a.ny = vol->ny;
+    a.nz = vol->nz;
+    k_init_rays<<<grid_for(n, 256), 256, 0, st>>>(a, n, uniform_origin ? nullptr : origin.p, dir.p, t_enter.p,
+                                                  t_exit.p, status.p, exited.p, coarse_cell.p, fine_cell.p,
+                                                  coarse_tmax.p, fine_tmax.p, rgba.p, depth.p);
+    WC_LAUNCH_CHECK();
+    // initial active list (engine.py:331 on pass 0)
+    PredActive pa{status.p};
+    scan_exclusive(pa, n, entry_off.p, counters.p + C_NACT, partials.p, st);
+    k_compact_index<<<grid_for(n, 256), 256, 0, st>>>(pa, n, entry_off.p, act_list[0].p);
+    WC_LAUNCH_CHECK();
+
+    // cache (cache.py:27-40, initial_capacity :122-125 with w*h == n)
+    if (cache_capacity <= 0) cache_capacity = std::max<int64_t>(1024, 2 * n / 64);
+    cap = std::max<int64_t>(1, cache_capacity);
+    phys = std::min<int64_t>(cap, vol->n_blocks);
+    slot_values.alloc(phys * 64);
+    block_of_slot.alloc(phys);
+    last_used.alloc(phys);
+    slot_of_block.alloc(vol->n_blocks);
+    WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * phys, st));
+    WC_CUDA(cudaMemsetAsync(block_of_slot.p, 0xFF, 4 * phys, st));
+    WC_CUDA(cudaMemsetAsync(last_used.p, 0, 4 * phys, st));
+    WC_CUDA(cudaMemsetAsync(slot_of_block.p, 0xFF, 4 * vol->n_blocks, st));
+    read_counters(C_NACT, 1);
+    n_act = h_counters.p[0];
+}
+
+Session::~Session() {
+    if (st) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+    }
+    if (ev_begin) cudaEventDestroy(ev_begin);
+    if (ev_end) cudaEventDestroy(ev_end);
+}
+
+void Session::read_counters(int first, int count) {
+    WC_CUDA(cudaMemcpyAsync(h_counters.p, counters.p + first, 4 * count, cudaMemcpyDeviceToHost, st));
+    WC_CUDA(cudaStreamSynchronize(st));
+}
+
+// cache.py:66-111 ensure_resident over the ascending active_ids[0..n_actb)
+void Session::ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict) {
+    pass_no += 1;
+    if (n_actb > cap) {  // cache.py:74-75: grow to ceil(1.5 * needed)
+        cap = (3 * n_actb + 1) / 2;
+        const int64_t new_phys = std::min<int64_t>(cap, vol->n_blocks);
+        if (new_phys > phys) {
+            slot_values.grow(new_phys * 64, st);
+            block_of_slot.grow(new_phys, st);
+            last_used.grow(new_phys, st);
+            WC_CUDA(cudaMemsetAsync(slot_values.p + phys * 64, 0, 4 * 64 * (new_phys - phys), st));
+            WC_CUDA(cudaMemsetAsync(block_of_slot.p + phys, 0xFF, 4 * (new_phys - phys), st));
+            WC_CUDA(cudaMemsetAsync(last_used.p + phys, 0, 4 * (new_phys - phys), st));
+            phys = new_phys;
+        }
+    }
+    if (free_off.n < phys) {
+        free_off.alloc(phys);
+        free_slots.alloc(phys);
+        cand_off.alloc(phys);
+        cand_key.alloc(phys);
+        cand_val.alloc(phys);
+        partials.ensure(scan_tiles(std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n, phys})) + 8);
+    }
+    n_miss = 0;
+    n_evict = 0;
+    if (n_actb == 0) return;
+    k_cache_stamp<<<grid_for(n_actb, 256), 256, 0, st>>>(active_ids.p, n_actb, slot_of_block.p, last_used.p, pass_no);
+    WC_LAUNCH_CHECK();
+    PredMiss pm{active_ids.p, slot_of_block.p};
+    scan_exclusive(pm, n_actb, miss_off.p, counters.p + C_NMISS, partials.p, st);
+    k_compact_miss<<<grid_for(n_actb, 256), 256, 0, st>>>(pm, n_actb, miss_off.p, miss_ids.p);
+    WC_LAUNCH_CHECK();
+    PredFree pf{block_of_slot.p};
+    scan_exclusive(pf, phys, free_off.p, counters.p + C_NFREE, partials.p, st);
+    k_compact_index<<<grid_for(phys, 256), 256, 0, st>>>(pf, phys, free_off.p, free_slots.p);
+    WC_LAUNCH_CHECK();
+    read_counters(C_NMISS, 2);
+    n_miss = h_counters.p[0];
+    const int64_t n_free_phys = h_counters.p[1];
+    const int64_t n_free = n_free_phys + (cap - phys);  // slots >= n_blocks are never occupied
+    if (n_miss == 0) return;
+    if (n_miss > n_free) {
+        n_evict = n_miss - n_free;
+        const int64_t n_hits = n_actb - n_miss;
+        const int64_t n_cand = (phys - n_free_phys) - n_hits;
+        if (n_cand < n_evict) throw InvariantError("cache: fewer eviction candidates than needed");
+        PredCand pc{block_of_slot.p, last_used.p, pass_no};
+        scan_exclusive(pc, phys, cand_off.p, counters.p + C_NCAND, partials.p, st);
+        k_compact_cand<<<grid_for(phys, 256), 256, 0, st>>>(pc, phys, cand_off.p, cand_key.p, cand_val.p);
+        WC_LAUNCH_CHECK();
+        // (last_used, block_id) order: stable LSD by block id, then by pass stamp
+        radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)(vol->n_blocks - 1)), rs, st);
+        k_gather_last_used<<<grid_for(n_cand, 256), 256, 0, st>>>(cand_val.p, n_cand, last_used.p, cand_key.p);
+        WC_LAUNCH_CHECK();
+        radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)pass_no), rs, st);
+        k_evict<<<grid_for(n_evict, 256), 256, 0, st>>>(cand_val.p, n_evict, n_free_phys, block_of_slot.p,
+                                                        slot_of_block.p, free_slots.p);
+        WC_LAUNCH_CHECK();
+    }
+    k_decode_insert<<<grid_for(n_miss * 32, 256, 8), 256, 0, st>>>(vol->payload.p, vol->qbits, vol->stride,
+                                                                   miss_ids.p, free_slots.p, n_miss, slot_values.p,
+                                                                   block_of_slot.p, last_used.p, slot_of_block.p,
+                                                                   pass_no);
+    WC_LAUNCH_CHECK();
+}
+
+bool Session::pass(PassStatsC &stats) {
+    if (n_act == 0) return false;
+    const auto t_start = std::chrono::steady_clock::now();
+    WC_CUDA(cudaEventRecord(ev_begin, st));
+    // engine.py:333 / :91-94 compute_n_spec (slot budget = rays in session)
+    int64_t n_spec = 1;
+    if (speculation) n_spec = std::min<int64_t>(max_spec, std::max<int64_t>(1, n / n_act));
+    if (n_act * n_spec > n) throw InvariantError("slot budget exceeded");
+    last_n_spec = n_spec;
+    last_slots_used = n_act * n_spec;
+    const int64_t nwords = ceil_div(vol->n_blocks, 32);
+    uint32_t *alist = act_list[cur].p;
+
+    // traverse_to_next_blocks + fused visibility marking
+    TraverseArgs ta{};
+    ta.rays = RayView{uniform_origin ? nullptr : origin.p, dir.p, t_enter.p, eye[0], eye[1], eye[2]};
+    ta.t_exit = t_exit.p;
+    ta.exited = exited.p;
+    ta.coarse_cell = coarse_cell.p;
+    ta.fine_cell = fine_cell.p;
+    ta.coarse_tmax = coarse_tmax.p;
+    ta.fine_tmax = fine_tmax.p;
+    ta.act_list = alist;
+    ta.n_act = n_act;
+    ta.n_spec = (int)n_spec;
+    ta.fine_mm = vol->fine_mm.p;
+    ta.coarse_mm = vol->coarse_mm.p;
+    ta.fdx = vol->bdx;
+    ta.fdy = vol->bdy;
+    ta.fdz = vol->bdz;
+    ta.cdx = vol->cdx;
+    ta.cdy = vol->cdy;
+    ta.cdz = vol->cdz;
+    ta.iso = iso;
+    ta.block_slots = block_slots.p;
+    ta.ray_slots = ray_slots.p;
+    ta.emitted = emitted.p;
+    ta.vis_bm = vis_bm.p;
+    k_traverse<<<grid_for(n_act, 128, 16), 128, 0, st>>>(ta);
+    WC_LAUNCH_CHECK();
+    // entry compaction: exclusive scan of per-ray emitted counts
+    scan_exclusive(LoadU32{emitted.p}, n_act, entry_off.p, counters.p + C_NENT, partials.p, st);
+    // visible ids (ascending) + active marking
+    bitmap_extract(vis_bm.p, nwords, vis_word_off.p, visible_ids.p, counters.p + C_NVIS, partials.p, st);
+    k_mark_active<<<grid_for((int64_t)8 * n, 256), 256, 0, st>>>(visible_ids.p, counters.p + C_NVIS, vol->bdx,
+                                                                 vol->bdy, vol->bdz, act_bm.p);
+    WC_LAUNCH_CHECK();
+    bitmap_extract(act_bm.p, nwords, act_word_off.p, active_ids.p, counters.p + C_NACTB, partials.p, st);
+    k_build_entries<<<grid_for(n_act, 256), 256, 0, st>>>(n_act, (int)n_spec, alist, emitted.p, entry_off.p,
+                                                          block_slots.p, vis_bm.p, vis_word_off.p, ent_key.p,
+                                                          ent_val.p, ent_ray.p);
+    WC_LAUNCH_CHECK();
+    WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
+    WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
+    read_counters(C_NENT, 3);
+    const int64_t n_ent = h_counters.p[0], nvis = h_counters.p[1], nactb = h_counters.p[2];
+    if (n_ent > n) throw InvariantError("slot budget exceeded");
+    last_nent = n_ent;
+    last_nvis = nvis;
+    last_nactb = nactb;
+
+    // cache.ensure_resident (+ fused decode)
+    int64_t n_miss = 0, n_evict = 0;
+    ensure_resident(nactb, n_miss, n_evict);
+    if (corrupt) WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * phys, st));  // engine.py:338-339
+
+    // build_rt_inputs: stable grouping of entries by visible block
+    if (n_ent > 0) {
+        radix_sort_pairs(ent_key.p, ent_val.p, n_ent, bits_for((uint64_t)(nvis - 1)), rs, st);
+        k_run_offsets<<<grid_for(n_ent, 256), 256, 0, st>>>(ent_key.p, n_ent, nvis, block_ray_off.p);
+        WC_LAUNCH_CHECK();
+        RaytraceArgs ra{};
+        ra.visible_ids = visible_ids.p;
+        ra.block_ray_off = block_ray_off.p;
+        ra.ent_val = ent_val.p;
+        ra.ent_ray = ent_ray.p;
+        ra.nvis = nvis;
+        ra.slot_of_block = slot_of_block.p;
+        ra.slot_values = slot_values.p;
+        ra.bdx = vol->bdx;
+        ra.bdy = vol->bdy;
+        ra.bdz = vol->bdz;
+        ra.nx = vol->nx;
+        ra.ny = vol->ny;
+        ra.nz = vol->nz;
+        ra.rays = ta.rays;
+        ra.iso = iso;
+        ra.br = base[0];
+        ra.bg = base[1];
+        ra.bb = base[2];
+        ra.rgbz = rgbz.p;
+        ra.err = counters.p + C_ERR;
+        k_raytrace<<<grid_for(nvis * 32, 256, 8), 256, 0, st>>>(ra);
+        WC_LAUNCH_CHECK();
+    }
+    // composite + compaction of the surviving rays (next pass's O_Act)
+    k_composite<<<grid_for(n_act, 256), 256, 0, st>>>(n_act, alist, emitted.p, entry_off.p, rgbz.p, exited.p,
+                                                      status.p, rgba.p, depth.p, keep.p);
+    WC_LAUNCH_CHECK();
+    scan_exclusive(LoadU32{keep.p}, n_act, keep_off.p, counters.p + C_NACT, partials.p, st);
+    k_compact_keep<<<grid_for(n_act, 256), 256, 0, st>>>(keep.p, keep_off.p, alist, n_act, act_list[cur ^ 1].p);
+    WC_LAUNCH_CHECK();
+    WC_CUDA(cudaEventRecord(ev_end, st));
+    read_counters(0, C_COUNT);
+    const int64_t n_after = h_counters.p[C_NACT];
+    if (h_counters.p[C_ERR]) throw InvariantError("visible block not resident");
+    WC_CUDA(cudaEventElapsedTime(&last_kernel_ms, ev_begin, ev_end));
+    stats.pass_index = pass_index;
+    stats.n_active_before = n_act;
+    stats.n_spec = n_spec;
+    stats.visible_blocks = nvis;
+    stats.active_blocks = nactb;
+    stats.new_decompressed = n_miss;
+    stats.evicted = n_evict;
+    stats.cache_slots = cap;
+    stats.n_entries = n_ent;
+    stats.n_active_after = n_after;
+    stats.utilization = (double)n_ent / (double)n;
+    stats.completeness = (double)(n - n_after) / (double)n;
+    stats.duration = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    cur ^= 1;
+    n_act = n_after;
+    pass_index++;
+    return true;
+}
+
+void Session::download_framebuffer(uint8_t *rgba_host, float *depth_host) {
+    if (rgba_host) WC_CUDA(cudaMemcpyAsync(rgba_host, rgba.p, 4 * n, cudaMemcpyDeviceToHost, st));
+    if (depth_host) WC_CUDA(cudaMemcpyAsync(depth_host, depth.p, 4 * n, cudaMemcpyDeviceToHost, st));
+    WC_CUDA(cudaStreamSynchronize(st));
+}
+
+void Session::copy_framebuffer_device(void *rgba_dst, void *depth_dst) {
+    if (rgba_dst) WC_CUDA(cudaMemcpyAsync(rgba_dst, rgba.p, 4 * n, cudaMemcpyDeviceToDevice, st));
+    if (depth_dst) WC_CUDA(cudaMemcpyAsync(depth_dst, depth.p, 4 * n, cudaMemcpyDeviceToDevice, st));
+    WC_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace wc

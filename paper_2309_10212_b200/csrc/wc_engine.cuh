@@ -1,0 +1,108 @@
+// wc_engine.cuh -- the per-pass wavefront session (engine.py:308-382).
+#pragma once
+
+#include "wc_common.cuh"
+#include "wc_prims.cuh"
+#include "wc_volume.cuh"
+
+namespace wc {
+
+struct CameraParams {  // traversal.py:65-70, :111 (basis computed on the host)
+    double eye[3], look[3], right[3], up[3];
+    double tan_half;
+    int32_t img_w, img_h;
+};
+
+struct PassStatsC {  // engine.py:66-77 PassStats (+ evicted, n_entries)
+    int64_t pass_index, n_active_before, n_spec, visible_blocks, active_blocks, new_decompressed, evicted,
+        cache_slots, n_entries, n_active_after;
+    double utilization, completeness, duration;
+};
+
+enum Counter : int {
+    C_NACT = 0,   // active rays after composite (next pass's n_act)
+    C_NENT,       // ray-block entries this pass
+    C_NVIS,       // visible blocks
+    C_NACTB,      // active blocks
+    C_NMISS,      // cache misses
+    C_NFREE,      // free slots
+    C_NCAND,      // eviction candidates
+    C_ERR,        // device-side invariant failures
+    C_COUNT
+};
+
+// Per-session device state.  Layout (N = rays in this session):
+//   ray SoA: dir f64[N*3] (origin f64[N*3] only for arbitrary rays; camera
+//   rays share `eye`), t_enter/t_exit f64[N], status/exited u8[N],
+//   coarse/fine cell u32[N], coarse/fine tmax f64[N*3]          (122 B/ray)
+//   act_list u32[N] x2 (ping-pong compacted active rays, ascending)
+//   slots: block_slots/ray_slots u32[N] (prefix n_act*n_spec used)
+//   entries: key/val/ray u32[N], rgbz float4[N]
+//   bitmaps: vis/act u32[ceil(n_blocks/32)] (15.7 MB at 8.05B voxels)
+//   cache: slot_values f32[phys*64], block_of_slot/last_used i32[phys],
+//          slot_of_block i32[n_blocks]
+//   framebuffer: rgba u32[N] (packed RGBA8), depth f32[N]
+struct Session {
+    Volume *vol = nullptr;
+    cudaStream_t st = nullptr;
+    int64_t n = 0;
+    double iso = 0.0;
+    int speculation = 1, max_spec = 64, corrupt = 0;
+    double base[3] = {0.85, 0.85, 0.85};
+    bool uniform_origin = true;
+    double eye[3] = {0, 0, 0};
+
+    DevBuf<double> origin, dir, t_enter, t_exit, coarse_tmax, fine_tmax;
+    DevBuf<uint8_t> status, exited;
+    DevBuf<uint32_t> coarse_cell, fine_cell;
+    DevBuf<uint32_t> act_list[2], keep, keep_off, emitted, entry_off;
+    int cur = 0;
+    DevBuf<uint32_t> block_slots, ray_slots;
+    DevBuf<uint32_t> ent_key, ent_val, ent_ray;
+    DevBuf<float4> rgbz;
+    DevBuf<uint32_t> vis_bm, act_bm, vis_word_off, act_word_off;
+    DevBuf<uint32_t> visible_ids, block_ray_off, active_ids;
+    DevBuf<uint32_t> rgba;
+    DevBuf<float> depth;
+    // cache (cache.py)
+    int64_t cap = 0, phys = 0;
+    int32_t pass_no = 0;
+    DevBuf<float> slot_values;
+    DevBuf<int32_t> block_of_slot, last_used, slot_of_block;
+    DevBuf<uint32_t> miss_off, miss_ids, free_off, free_slots, cand_off, cand_key, cand_val;
+    // scratch
+    DevBuf<uint32_t> counters, partials;
+    PinnedBuf<uint32_t> h_counters;
+    RadixScratch rs;
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+
+    int64_t n_act = 0, pass_index = 0;
+    int64_t last_slots_used = 0, last_nvis = 0, last_nactb = 0, last_nent = 0;
+    int64_t last_n_spec = 1;
+    float last_kernel_ms = 0.0f;
+
+    Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, int64_t n_rays, const double *origins,
+            const double *dirs, double iso, int speculation, int max_spec, int64_t cache_capacity, int corrupt);
+    ~Session();
+    bool pass(PassStatsC &st);
+    void download_framebuffer(uint8_t *rgba_host, float *depth_host);
+    void copy_framebuffer_device(void *rgba_dst, void *depth_dst);
+
+   private:
+    void read_counters(int first, int count);
+    void ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict);
+};
+
+// Brute-force oracle on the device (oracle.py:42-122): every ray marches all
+// dual cells of the fully decoded volume.  d_values dense float32 x-fastest.
+void reference_render_device(const float *d_values, int nx, int ny, int nz, const double *d_origin,
+                             const double *d_dir, int64_t n, double iso, double br, double bg, double bb,
+                             uint32_t *d_rgba, float *d_depth, cudaStream_t st);
+
+// Ray setup alone (traversal.py:105-187) for parity tests.
+void init_rays_device(const CameraParams *cam, const uint32_t *d_pixel_ids, int64_t n, const double *d_origin_in,
+                      const double *d_dir_in, int nx, int ny, int nz, double *d_origin_out, double *d_dir,
+                      double *t_enter, double *t_exit, uint8_t *status, uint8_t *exited, uint32_t *coarse_cell,
+                      uint32_t *fine_cell, double *coarse_tmax, double *fine_tmax, cudaStream_t st);
+
+}  // namespace wc

@@ -1,0 +1,296 @@
+// wc_volume.cu -- block codec (decode + encode) and grid construction.
+#include <math_constants.h>
+
+#include <vector>
+
+#include "wc_volume.cuh"
+
+namespace wc {
+
+Volume::~Volume() {
+    if (st) cudaStreamDestroy(st);
+}
+
+void Volume::set_dims(int nx_, int ny_, int nz_, int qbits_) {
+    nx = nx_;
+    ny = ny_;
+    nz = nz_;
+    qbits = qbits_;
+    stride = stride_of(qbits);
+    bdx = (nx + 3) / 4;
+    bdy = (ny + 3) / 4;
+    bdz = (nz + 3) / 4;
+    cdx = (bdx + 3) / 4;
+    cdy = (bdy + 3) / 4;
+    cdz = (bdz + 3) / 4;
+    n_blocks = (int64_t)bdx * bdy * bdz;
+    n_coarse = (int64_t)cdx * cdy * cdz;
+    if (!st) WC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+}
+
+// ------------------------------------------------------------------ decode
+
+// warp per block; lane writes values lane and lane+32 (coalesced 128B stores)
+__global__ void __launch_bounds__(256) k_decode_ids(const uint8_t *__restrict__ payload, int qbits, int stride,
+                                                    const int64_t *__restrict__ ids, int64_t n, float *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = warp0; j < n; j += nwarps) {
+        const uint32_t *rec = reinterpret_cast<const uint32_t *>(payload + ids[j] * (int64_t)stride);
+        const BlockDecodeParams p = decode_params(rec, qbits);
+        float v0 = 0.0f, v1 = 0.0f;
+        if (!p.zero) {
+            v0 = decode_value(rec, lane, qbits, p.e, p.fast, p.pow2f, p.sf, p.sd, p.scale_d);
+            v1 = decode_value(rec, lane + 32, qbits, p.e, p.fast, p.pow2f, p.sf, p.sd, p.scale_d);
+        }
+        out[j * 64 + lane] = v0;
+        out[j * 64 + lane + 32] = v1;
+    }
+}
+
+void decode_blocks_device(const Volume &v, const int64_t *d_ids, int64_t n, float *d_out, cudaStream_t st) {
+    if (n <= 0) return;
+    k_decode_ids<<<grid_for(n * 32, 256), 256, 0, st>>>(v.payload.p, v.qbits, v.stride, d_ids, n, d_out);
+    WC_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------- encode
+
+// Pack one block from its 64 values (x-fastest within the block) and the
+// valid-voxel mask: codec.py:81-105 + :183-185 + :120-140.  Warp per block.
+__device__ __forceinline__ void encode_block_warp(float v0, float v1, bool valid0, bool valid1, int qbits,
+                                                  uint32_t *rec_words, int n_words, float2 *range_out,
+                                                  uint32_t *smem_q /* 64 per warp */) {
+    const int lane = threadIdx.x & 31;
+    // ranges over valid voxels only (nanmin/nanmax in float64, cast back: exact)
+    float mn = valid0 ? v0 : CUDART_INF_F, mx = valid0 ? v0 : -CUDART_INF_F;
+    if (valid1) {
+        mn = fminf(mn, v1);
+        mx = fmaxf(mx, v1);
+    }
+    float m = fmaxf(fabsf(v0), fabsf(v1));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+    if (lane == 0) *range_out = make_float2(mn, mx);
+    // _block_exponents: smallest e with max|v| <= 2^e (frexp rule)
+    int e;
+    if ((double)m == 0.0) {
+        e = -32768;
+    } else {
+        int ex;
+        const double mant = frexp((double)m, &ex);
+        e = ex - (mant == 0.5 ? 1 : 0);
+    }
+    const uint32_t mask = (uint32_t)((1ull << qbits) - 1ull);
+    if (e != -32768) {
+        const double scale = ldexp(1.0, -e);
+        const double s = (double)((1ll << (qbits - 1)) - 1);
+        smem_q[lane] = (uint32_t)(int32_t)rint((double)v0 * scale * s) & mask;
+        smem_q[lane + 32] = (uint32_t)(int32_t)rint((double)v1 * scale * s) & mask;
+    }
+    __syncwarp();
+    for (int w = lane; w < n_words; w += 32) {
+        uint32_t word = 0;
+        if (w == 0) word = (uint32_t)(uint16_t)(int16_t)e;
+        if (e != -32768) {
+            // values whose bit span [16+i*q, 16+(i+1)*q) intersects [32w, 32w+32)
+            int i_lo = (32 * w - 16 - qbits + 1);
+            i_lo = i_lo <= 0 ? 0 : (i_lo + qbits - 1) / qbits;
+            for (int i = i_lo; i < 64; i++) {
+                const int rel = 16 + i * qbits - 32 * w;
+                if (rel >= 32) break;
+                const uint32_t q = smem_q[i];
+                word |= rel >= 0 ? (q << rel) : (q >> (-rel));
+            }
+        }
+        rec_words[w] = word;
+    }
+    __syncwarp();
+}
+
+struct SeparableField {
+    int K, nx, ny, nz;
+    const float *amp, *fx, *fy, *fz;  // device tables [K][n*]
+    __device__ __forceinline__ float operator()(int x, int y, int z) const {
+        float v = 0.0f;
+        for (int k = 0; k < K; k++) v = v + ((amp[k] * fz[k * nz + z]) * fy[k * ny + y]) * fx[k * nx + x];
+        return v;
+    }
+};
+
+struct DenseField {
+    const float *p;
+    int nx, ny;
+    __device__ __forceinline__ float operator()(int x, int y, int z) const {
+        return p[x + (int64_t)nx * (y + (int64_t)ny * z)];
+    }
+};
+
+template <class Field>
+__global__ void __launch_bounds__(256) k_compress(Field f, int nx, int ny, int nz, int bdx, int bdy, int64_t n_blocks,
+                                                  int qbits, int stride, uint8_t *payload, float2 *ranges) {
+    __shared__ uint32_t sq[8][64];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int n_words = stride / 4;
+    for (int64_t b = warp0; b < n_blocks; b += nwarps) {
+        const int bx = (int)(b % bdx), by = (int)((b / bdx) % bdy), bz = (int)(b / ((int64_t)bdx * bdy));
+        float v[2];
+        bool ok[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int i = lane + 32 * h;
+            int x = 4 * bx + (i & 3), y = 4 * by + ((i >> 2) & 3), z = 4 * bz + (i >> 4);
+            ok[h] = x < nx && y < ny && z < nz;
+            x = min(x, nx - 1);  // np.pad(mode="edge"), codec.py:88
+            y = min(y, ny - 1);
+            z = min(z, nz - 1);
+            v[h] = f(x, y, z);
+        }
+        encode_block_warp(v[0], v[1], ok[0], ok[1], qbits, reinterpret_cast<uint32_t *>(payload + b * stride),
+                          n_words, ranges + b, sq[wib]);
+    }
+}
+
+void synth_separable_compress(Volume &v, int K, const float *amp, const float *fx, const float *fy, const float *fz) {
+    DevBuf<float> d_amp, d_fx, d_fy, d_fz;
+    d_amp.alloc(K);
+    d_fx.alloc((int64_t)K * v.nx);
+    d_fy.alloc((int64_t)K * v.ny);
+    d_fz.alloc((int64_t)K * v.nz);
+    WC_CUDA(cudaMemcpyAsync(d_amp.p, amp, sizeof(float) * K, cudaMemcpyHostToDevice, v.st));
+    WC_CUDA(cudaMemcpyAsync(d_fx.p, fx, sizeof(float) * K * v.nx, cudaMemcpyHostToDevice, v.st));
+    WC_CUDA(cudaMemcpyAsync(d_fy.p, fy, sizeof(float) * K * v.ny, cudaMemcpyHostToDevice, v.st));
+    WC_CUDA(cudaMemcpyAsync(d_fz.p, fz, sizeof(float) * K * v.nz, cudaMemcpyHostToDevice, v.st));
+    v.payload.alloc(v.n_blocks * v.stride);
+    v.ranges.alloc(v.n_blocks);
+    SeparableField f{K, v.nx, v.ny, v.nz, d_amp.p, d_fx.p, d_fy.p, d_fz.p};
+    k_compress<<<grid_for(v.n_blocks * 32, 256, 8), 256, 0, v.st>>>(f, v.nx, v.ny, v.nz, v.bdx, v.bdy, v.n_blocks,
+                                                                    v.qbits, v.stride, v.payload.p, v.ranges.p);
+    WC_LAUNCH_CHECK();
+    WC_CUDA(cudaStreamSynchronize(v.st));
+}
+
+void compress_dense_device(Volume &v, const float *d_values) {
+    v.payload.alloc(v.n_blocks * v.stride);
+    v.ranges.alloc(v.n_blocks);
+    DenseField f{d_values, v.nx, v.ny};
+    k_compress<<<grid_for(v.n_blocks * 32, 256, 8), 256, 0, v.st>>>(f, v.nx, v.ny, v.nz, v.bdx, v.bdy, v.n_blocks,
+                                                                    v.qbits, v.stride, v.payload.p, v.ranges.p);
+    WC_LAUNCH_CHECK();
+    WC_CUDA(cudaStreamSynchronize(v.st));
+}
+
+// -------------------------------------------------------------------- grids
+
+// widened ranges: grids.py:76-79 with bounds from the payload exponents
+// (codec.py:113-117, :220-223)
+__global__ void k_widen(const uint8_t *payload, const float2 *ranges, int64_t n, int qbits, int stride, double2 *w) {
+    const double s = (double)((1ll << (qbits - 1)) - 1);
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t eu = payload[b * stride] | (payload[b * stride + 1] << 8);
+        const double bound = eu == 0x8000u ? 0.0 : ldexp(1.0, (int)(int16_t)eu) / (2.0 * s);
+        const float2 r = ranges[b];
+        w[b] = make_double2((double)r.x - bound, (double)r.y + bound);
+    }
+}
+
+__device__ __forceinline__ double np_min(double a, double b) { return a < b ? a : b; }
+__device__ __forceinline__ double np_max(double a, double b) { return a > b ? a : b; }
+
+// grids.py:48-57 _octant_union: min/max over the 2x2x2 window anchored at
+// each cell, in the reference's (oz, oy, ox) accumulation order.
+__global__ void k_octant_union(const double2 *a, int dx, int dy, int dz, double2 *out) {
+    const int64_t n = (int64_t)dx * dy * dz;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(c % dx), y = (int)((c / dx) % dy), z = (int)(c / ((int64_t)dx * dy));
+        double lo = CUDART_INF, hi = -CUDART_INF;
+        for (int oz = 0; oz < 2; oz++)
+            for (int oy = 0; oy < 2; oy++)
+                for (int ox = 0; ox < 2; ox++) {
+                    double vlo = CUDART_INF, vhi = -CUDART_INF;
+                    if (x + ox < dx && y + oy < dy && z + oz < dz) {
+                        const double2 v = a[(x + ox) + (int64_t)dx * ((y + oy) + (int64_t)dy * (z + oz))];
+                        vlo = v.x;
+                        vhi = v.y;
+                    }
+                    lo = np_min(lo, vlo);
+                    hi = np_max(hi, vhi);
+                }
+        out[c] = make_double2(lo, hi);
+    }
+}
+
+// grids.py:60-68 _group4 over 4^3 fine cells
+__global__ void k_group4(const double2 *w, int bdx, int bdy, int bdz, int cdx, int cdy, int cdz, double2 *out) {
+    const int64_t n = (int64_t)cdx * cdy * cdz;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        const int cx = (int)(c % cdx), cy = (int)((c / cdx) % cdy), cz = (int)(c / ((int64_t)cdx * cdy));
+        double lo = CUDART_INF, hi = -CUDART_INF;
+        for (int k = 0; k < 4; k++)
+            for (int j = 0; j < 4; j++)
+                for (int i = 0; i < 4; i++) {
+                    const int x = 4 * cx + i, y = 4 * cy + j, z = 4 * cz + k;
+                    if (x >= bdx || y >= bdy || z >= bdz) continue;
+                    const double2 v = w[x + (int64_t)bdx * (y + (int64_t)bdy * z)];
+                    lo = np_min(lo, v.x);
+                    hi = np_max(hi, v.y);
+                }
+        out[c] = make_double2(lo, hi);
+    }
+}
+
+void Volume::build_grids() {
+    DevBuf<double2> wmm, cmm;
+    wmm.alloc(n_blocks);
+    cmm.alloc(n_coarse);
+    fine_mm.alloc(n_blocks);
+    coarse_mm.alloc(n_coarse);
+    k_widen<<<grid_for(n_blocks, 256), 256, 0, st>>>(payload.p, ranges.p, n_blocks, qbits, stride, wmm.p);
+    WC_LAUNCH_CHECK();
+    k_octant_union<<<grid_for(n_blocks, 256), 256, 0, st>>>(wmm.p, bdx, bdy, bdz, fine_mm.p);
+    WC_LAUNCH_CHECK();
+    k_group4<<<grid_for(n_coarse, 256), 256, 0, st>>>(wmm.p, bdx, bdy, bdz, cdx, cdy, cdz, cmm.p);
+    WC_LAUNCH_CHECK();
+    k_octant_union<<<grid_for(n_coarse, 256), 256, 0, st>>>(cmm.p, cdx, cdy, cdz, coarse_mm.p);
+    WC_LAUNCH_CHECK();
+    WC_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace wc
+
+namespace wc {
+
+__global__ void __launch_bounds__(256) k_decode_full(const uint8_t *__restrict__ payload, int qbits, int stride, int nx,
+                                                     int ny, int nz, int bdx, int bdy, int64_t n_blocks,
+                                                     float *__restrict__ dense) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t b = warp0; b < n_blocks; b += nwarps) {
+        const uint32_t *rec = reinterpret_cast<const uint32_t *>(payload + b * (int64_t)stride);
+        const BlockDecodeParams p = decode_params(rec, qbits);
+        const int bx = (int)(b % bdx), by = (int)((b / bdx) % bdy), bz = (int)(b / ((int64_t)bdx * bdy));
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int i = lane + 32 * h;
+            const float v = p.zero ? 0.0f : decode_value(rec, i, qbits, p.e, p.fast, p.pow2f, p.sf, p.sd, p.scale_d);
+            const int x = 4 * bx + (i & 3), y = 4 * by + ((i >> 2) & 3), z = 4 * bz + (i >> 4);
+            if (x < nx && y < ny && z < nz) dense[x + (int64_t)nx * (y + (int64_t)ny * z)] = v;
+        }
+    }
+}
+
+void decode_full_device(const Volume &v, float *d_dense, cudaStream_t st) {
+    k_decode_full<<<grid_for(v.n_blocks * 32, 256, 8), 256, 0, st>>>(v.payload.p, v.qbits, v.stride, v.nx, v.ny, v.nz,
+                                                                     v.bdx, v.bdy, v.n_blocks, d_dense);
+    WC_LAUNCH_CHECK();
+}
+
+}  // namespace wc

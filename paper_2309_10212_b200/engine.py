@@ -1,0 +1,210 @@
+"""Per-pass wavefront renderer -- the drop-in boundary (mirrors wavecast/engine.py).
+
+``render_passes(cv, grids, cam, iso, opts)`` keeps the reference generator
+protocol (engine.py:308-382): one ``(Framebuffer, PassStats)`` per pass.
+Everything between ray setup and composite runs on the B200 inside one
+``wc_session`` (csrc/wc_engine.cu); the host only reads a few counters per
+pass and, when asked, the framebuffer.  Speculation never changes final
+pixels (engine.py:1-9), which is what makes image-tile sharding exact.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterator
+
+import numpy as np
+
+from . import _lib
+from .codec import CompressedVolume
+from .grids import MacrocellGrids
+from .traversal import Camera
+
+BACKGROUND_RGBA = (0, 0, 0, 255)
+MAX_SPEC_DEFAULT = 64
+AMBIENT = 0.2
+BASE_COLOR = (0.85, 0.85, 0.85)
+
+
+@dataclass
+class RenderOptions:
+    """engine.py:37-44 (+ cache_capacity: the LRU budget, cache.py:122-125 when None)."""
+
+    width: int = 1280
+    height: int = 720
+    speculation: bool = True
+    max_spec: int = MAX_SPEC_DEFAULT
+    base_color: tuple[float, float, float] = BASE_COLOR
+    corrupt_cache: bool = False  # test hook: zero the slot pool every pass
+    cache_capacity: int | None = None
+
+
+@dataclass
+class Framebuffer:
+    w: int
+    h: int
+    rgba: np.ndarray   # uint8 (h, w, 4)
+    depth: np.ndarray  # float32 (h, w), +inf = background
+    completeness: float
+
+    @classmethod
+    def blank(cls, w: int, h: int) -> "Framebuffer":
+        rgba = np.empty((h, w, 4), dtype=np.uint8)
+        rgba[...] = BACKGROUND_RGBA
+        return cls(w, h, rgba, np.full((h, w), np.inf, dtype=np.float32), 0.0)
+
+    def snapshot(self) -> "Framebuffer":
+        return Framebuffer(self.w, self.h, self.rgba.copy(), self.depth.copy(), self.completeness)
+
+
+@dataclass(frozen=True)
+class PassStats:
+    pass_index: int
+    n_active_before: int
+    n_spec: int
+    visible_blocks: int
+    active_blocks: int
+    new_decompressed: int
+    cache_slots: int
+    utilization: float
+    completeness: float
+    duration: float
+
+
+@dataclass(frozen=True)
+class PassBuffers:
+    visible_ids: np.ndarray
+    rays_per_block: np.ndarray
+    block_ray_offsets: np.ndarray
+    sorted_ray_ids: np.ndarray
+    sorted_hit_slots: np.ndarray
+    valid_prefix: np.ndarray
+    n_entries: int
+
+
+def compute_n_spec(n_act: int, w: int, h: int, max_spec: int = MAX_SPEC_DEFAULT) -> int:
+    """Free slots shared evenly, clamped to [1, max_spec] (engine.py:91-94)."""
+    assert n_act >= 1
+    return min(max_spec, max(1, (w * h) // n_act))
+
+
+def _stats_from_c(s: _lib.PassStatsC) -> PassStats:
+    return PassStats(int(s.pass_index), int(s.n_active_before), int(s.n_spec), int(s.visible_blocks),
+                     int(s.active_blocks), int(s.new_decompressed), int(s.cache_slots), float(s.utilization),
+                     float(s.completeness), float(s.duration))
+
+
+class RenderSession:
+    """One render on the device: rays, cache, scratch and framebuffer in HBM.
+
+    ``pixel_ids`` (optional) restricts the session to a subset of the
+    image's pixels -- the unit of image-tile sharding.  Arbitrary rays
+    (RaySoA.from_rays semantics) go through ``origins``/``dirs``.
+    """
+
+    def __init__(self, cv: CompressedVolume, grids: MacrocellGrids | None, cam: Camera | None, iso: float,
+                 opts: RenderOptions, pixel_ids=None, origins=None, dirs=None):
+        if grids is not None:
+            grids.bind(cv)
+        self.cv = cv
+        self.opts = opts
+        self.w, self.h = int(opts.width), int(opts.height)
+        self._pix = None if pixel_ids is None else np.ascontiguousarray(pixel_ids, dtype=np.uint32)
+        o = None if origins is None else np.ascontiguousarray(origins, dtype=np.float64)
+        d = None if dirs is None else np.ascontiguousarray(dirs, dtype=np.float64)
+        if d is not None:
+            n = d.shape[0]
+        elif self._pix is not None:
+            n = len(self._pix)
+        else:
+            n = self.w * self.h
+        self.n = n
+        cam_c = cam.to_c(self.w, self.h) if cam is not None else None
+        cap = 0 if opts.cache_capacity is None else int(opts.cache_capacity)
+        self._h = C.c_void_p()
+        _lib.call("wc_session_create", cv.device_handle(), None if cam_c is None else C.byref(cam_c),
+                  _lib.ptr(self._pix), n, _lib.ptr(o), _lib.ptr(d), float(iso), int(bool(opts.speculation)),
+                  int(opts.max_spec), cap, int(bool(opts.corrupt_cache)), C.byref(self._h))
+        if tuple(opts.base_color) != BASE_COLOR:
+            _lib.call("wc_session_set_base_color", self._h, *[float(c) for c in opts.base_color])
+        self.last_c_stats = None
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.lib().wc_session_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def n_active(self) -> int:
+        v = C.c_int64()
+        _lib.call("wc_session_n_active", self._h, C.byref(v))
+        return int(v.value)
+
+    def step(self) -> PassStats | None:
+        st = _lib.PassStatsC()
+        ran = C.c_int()
+        _lib.call("wc_session_pass", self._h, C.byref(st), C.byref(ran))
+        if not ran.value:
+            return None
+        self.last_c_stats = st
+        return _stats_from_c(st)
+
+    def run(self, max_passes: int = 100000) -> list[PassStats]:
+        buf = (_lib.PassStatsC * max_passes)()
+        k = C.c_int64()
+        _lib.call("wc_session_run", self._h, buf, max_passes, C.byref(k))
+        return [_stats_from_c(buf[i]) for i in range(min(k.value, max_passes))]
+
+    def last_pass_ms(self) -> float:
+        v = C.c_double()
+        _lib.call("wc_session_last_pass_ms", self._h, C.byref(v))
+        return float(v.value)
+
+    def read(self, rgba=None, depth=None):
+        """Framebuffer of this session's rays: (rgba (n,4) u8, depth (n,) f32)."""
+        if rgba is None:
+            rgba = np.empty((self.n, 4), dtype=np.uint8)
+        if depth is None:
+            depth = np.empty(self.n, dtype=np.float32)
+        _lib.call("wc_session_framebuffer", self._h, _lib.ptr(rgba), _lib.ptr(depth))
+        return rgba, depth
+
+    def framebuffer(self, completeness: float) -> Framebuffer:
+        rgba, depth = self.read()
+        return Framebuffer(self.w, self.h, rgba.reshape(self.h, self.w, 4), depth.reshape(self.h, self.w),
+                           completeness)
+
+
+def render_passes(cv: CompressedVolume, grids: MacrocellGrids, cam: Camera, iso: float,
+                  opts: RenderOptions) -> Iterator[tuple[Framebuffer, PassStats]]:
+    """engine.py:308-382: yield a framebuffer snapshot + stats per pass."""
+    with RenderSession(cv, grids, cam, iso, opts) as s:
+        while True:
+            ps = s.step()
+            if ps is None:
+                break
+            yield s.framebuffer(ps.completeness), ps
+
+
+def render(cv: CompressedVolume, grids: MacrocellGrids, cam: Camera, iso: float,
+           opts: RenderOptions) -> tuple[Framebuffer, list[PassStats]]:
+    """engine.py:385-401: render to completion; only the final frame is read back."""
+    with RenderSession(cv, grids, cam, iso, opts) as s:
+        stats = s.run()
+        if not stats:  # camera missed the volume on every pixel
+            fb = Framebuffer.blank(opts.width, opts.height)
+            fb.completeness = 1.0
+            return fb, stats
+        return s.framebuffer(stats[-1].completeness), stats

@@ -1,0 +1,231 @@
+"""GPU parity: the sm_100a render path vs the CPU oracle, bit for bit.
+
+Every test calls through the C ABI (libwavecast_b200.so via the package's
+public API) and compares with oracle/ (the CPU restatement pinned against
+the reference's own golden vectors in tests/golden/).  Bar: bit-exact for
+voxels, ray state, slot buffers, block sets, cache residency, grouped
+entries, RGBZ, RGBA and depth.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import host_volume, iso_at, lockstep, oracle_volume, orbit
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def wc():
+    import paper_2309_10212_b200 as wc
+
+    wc._lib.ensure_device(0)
+    return wc
+
+
+# ----------------------------------------------------------------- codec
+@pytest.mark.parametrize("qbits", [4, 7, 11, 16, 20, 25, 26])
+def test_compress_and_decode_bit_exact(wc, qbits):
+    rng = np.random.default_rng(qbits)
+    vals = rng.uniform(-100.0, 100.0, (13, 10, 9)).astype(np.float32)
+    vals[:4, :4, :4] = 0.0  # an all-zero block -> sentinel
+    vol = wc.volume.make_volume((9, 10, 13), vals)
+    cv = wc.compress_volume(vol, qbits)
+    pay, rng_, _ = orc.compress(vol.values, vol.dims, qbits)
+    assert np.array_equal(cv.payload, pay), "GPU compressor payload"
+    assert np.array_equal(cv.raw_block_ranges.view(np.uint32), rng_.view(np.uint32)), "GPU ranges"
+    ov = oracle_volume(cv)
+    ids = np.arange(cv.block_count)
+    got = np.empty((cv.block_count, 64), np.float32)
+    wc.decompress_blocks_into(cv, ids, got)
+    assert np.array_equal(got.view(np.uint32), orc.decode_blocks(ov, ids).view(np.uint32))
+
+
+def test_decode_extreme_exponents(wc):
+    # tiny and huge magnitudes exercise the float64 fallback (subnormal / e>127)
+    vals = np.zeros((8, 8, 8), np.float32)
+    vals[:4, :4, :4] = np.float32(3e-38) * np.linspace(-1, 1, 64).reshape(4, 4, 4).astype(np.float32)
+    vals[4:, 4:, 4:] = np.float32(3e38) * np.linspace(-1, 1, 64).reshape(4, 4, 4).astype(np.float32)
+    vals[:4, 4:, :4] = np.float32(1e-30)
+    vol = wc.volume.make_volume((8, 8, 8), vals)
+    for qbits in (8, 16, 25, 26):
+        cv = wc.compress_volume(vol, qbits)
+        pay, _, _ = orc.compress(vol.values, vol.dims, qbits)
+        assert np.array_equal(cv.payload, pay)
+        ids = np.arange(cv.block_count)
+        got = np.empty((cv.block_count, 64), np.float32)
+        wc.decompress_blocks_into(cv, ids, got)
+        assert np.array_equal(got.view(np.uint32), orc.decode_blocks(oracle_volume(cv), ids).view(np.uint32))
+
+
+def test_grids_bit_exact(wc):
+    vol = host_volume("value_noise", (37, 29, 45))
+    cv = wc.compress_volume(vol, 12)
+    g = wc.build_grids(cv)
+    ov = oracle_volume(cv)
+    for k in ("fine_min", "fine_max", "coarse_min", "coarse_max"):
+        assert np.array_equal(getattr(g, k), getattr(ov, k)), k
+
+
+def test_separable_synthesis_matches_host(wc):
+    f = wc.turbulence_field((40, 36, 44), seed=1)
+    cv = wc.compress_separable(f, 16)
+    pay, rng_, _ = orc.compress(f.evaluate().reshape(-1), f.dims, 16)
+    assert np.array_equal(cv.payload, pay)
+    assert np.array_equal(cv.raw_block_ranges, rng_)
+
+
+# ------------------------------------------------------------- full frames
+SCENES = [
+    # kind, n, qbits, w, h, iso frac, camera frac, speculation, max_spec, cache
+    ("marschner_lobb", 64, 16, 256, 256, 0.5, 0.0, False, 64, None),   # C1
+    ("marschner_lobb", 64, 16, 256, 256, 0.5, 0.0, True, 64, None),
+    ("sphere", 64, 16, 96, 96, 0.3, 0.13, True, 64, None),
+    ("value_noise", 64, 16, 64, 64, 0.5, 0.4, True, 64, None),
+    ("value_noise", 64, 8, 128, 100, 0.5, 0.4, False, 64, None),
+    ("value_noise", 48, 12, 120, 90, 0.35, 0.7, True, 64, 40),          # heavy eviction
+    ("marschner_lobb", 41, 26, 90, 70, 0.6, 0.25, True, 64, None),     # qbits 26 fallback
+    ("value_noise", 64, 4, 100, 100, 0.5, 0.1, True, 8, None),
+    ("gaussians", 96, 16, 160, 90, 0.3, 0.0, True, 64, None),
+    ("turbulence", (72, 64, 60), 16, 128, 72, 0.5, 0.3, True, 64, 1024),
+]
+
+
+@pytest.mark.parametrize("scene", SCENES, ids=[f"{s[0]}-{s[1]}-q{s[2]}-{s[3]}x{s[4]}-spec{int(s[7])}" for s in SCENES])
+def test_render_lockstep_vs_oracle(wc, scene):
+    kind, n, qbits, w, h, isof, camf, spec, max_spec, cache = scene
+    vol = host_volume(kind, n, seed=1 if kind == "turbulence" else (0 if kind == "gaussians" else 3))
+    cv = wc.compress_volume(vol, qbits)
+    ov = oracle_volume(cv)
+    lockstep(wc, cv, ov, orbit(cv.dims, camf), w, h, iso_at(vol, isof), speculation=spec, max_spec=max_spec,
+             cache_capacity=cache)
+
+
+def test_render_api_matches_generator(wc):
+    vol = host_volume("value_noise", 64)
+    cv = wc.compress_volume(vol, 16)
+    grids = wc.build_grids(cv)
+    cam = wc.Camera.look_at((31.5, 31.5, 31.5 + 115.2), (31.5, 31.5, 31.5))
+    opts = wc.RenderOptions(width=80, height=60)
+    fb, stats = wc.render(cv, grids, cam, iso_at(vol, 0.5), opts)
+    last = None
+    prev_written = None
+    for snap, ps in wc.render_passes(cv, grids, cam, iso_at(vol, 0.5), opts):
+        written = np.isfinite(snap.depth)
+        if prev_written is not None:  # pixels, once written, never change
+            assert np.array_equal(snap.rgba[prev_written], last.rgba[prev_written])
+        last, prev_written = snap, written
+    assert np.array_equal(last.rgba, fb.rgba) and np.array_equal(last.depth, fb.depth)
+    assert last.completeness == 1.0 == fb.completeness
+
+
+def test_speculation_invariance(wc):
+    vol = host_volume("value_noise", 64)
+    cv = wc.compress_volume(vol, 16)
+    grids = wc.build_grids(cv)
+    cam = wc.Camera.look_at((31.5 + 115.2 * np.sin(0.8 * np.pi), 31.5, 31.5 + 115.2 * np.cos(0.8 * np.pi)),
+                            (31.5, 31.5, 31.5))
+    iso = iso_at(vol, 0.5)
+    on, s_on = wc.render(cv, grids, cam, iso, wc.RenderOptions(width=64, height=64, speculation=True))
+    off, s_off = wc.render(cv, grids, cam, iso, wc.RenderOptions(width=64, height=64, speculation=False))
+    assert np.array_equal(on.rgba, off.rgba) and np.array_equal(on.depth, off.depth)
+    assert len(s_on) <= len(s_off) and all(s.n_spec == 1 for s in s_off)
+
+
+def test_camera_misses_volume(wc):
+    cv = wc.compress_volume(host_volume("sphere", 64), 16)
+    cam = wc.Camera((31.5, 31.5, 200.0), (0.0, 0.0, 1.0), (0.0, 1.0, 0.0), 45.0)
+    fb, stats = wc.render(cv, wc.build_grids(cv), cam, 20.0, wc.RenderOptions(width=16, height=16))
+    assert stats == [] and fb.completeness == 1.0 and not np.isfinite(fb.depth).any()
+
+
+def test_iso_outside_range_single_pass(wc):
+    cv = wc.compress_volume(host_volume("sphere", 64), 16)
+    cam = wc.Camera.look_at((31.5, 31.5, 31.5 + 115.2), (31.5, 31.5, 31.5))
+    fb, stats = wc.render(cv, wc.build_grids(cv), cam, 1000.0, wc.RenderOptions(width=32, height=32))
+    assert len(stats) == 1 and fb.completeness == 1.0 and not np.isfinite(fb.depth).any()
+
+
+def test_arbitrary_rays_lockstep(wc):
+    vol = host_volume("value_noise", 32)
+    cv = wc.compress_volume(vol, 8)
+    rng = np.random.default_rng(37)
+    hi = np.asarray(cv.dims, float) - 1.0
+    phi = rng.uniform(0, 2 * np.pi, 500)
+    ct = rng.uniform(-1, 1, 500)
+    st = np.sqrt(1 - ct**2)
+    origins = hi / 2 + (np.linalg.norm(hi) + 10) * np.stack([st * np.cos(phi), st * np.sin(phi), ct], 1)
+    d = rng.uniform(0.2, 0.8, (500, 3)) * hi - origins
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    lockstep(wc, cv, oracle_volume(cv), None, 500, 1, float(np.median(vol.values)), origins=origins, dirs=d,
+             max_spec=4)
+
+
+def test_corrupt_cache_hook_breaks_parity(wc):
+    vol = host_volume("sphere", 64)
+    cv = wc.compress_volume(vol, 16)
+    grids = wc.build_grids(cv)
+    cam = wc.Camera.look_at((31.5, 31.5, 31.5 + 115.2), (31.5, 31.5, 31.5))
+    good, _ = wc.render(cv, grids, cam, 20.0, wc.RenderOptions(width=48, height=48))
+    bad, _ = wc.render(cv, grids, cam, 20.0, wc.RenderOptions(width=48, height=48, corrupt_cache=True))
+    assert wc.compare_images(good, bad)["hit_mask_mismatches"] > 0
+
+
+def test_tile_sharding_stitches_bit_exact(wc):
+    """N interleaved tile sessions on one GPU, stitched == one full frame
+    (the multi-GPU decomposition)."""
+    from paper_2309_10212_b200 import dist
+
+    vol = host_volume("gaussians", 96, seed=0)
+    cv = wc.compress_volume(vol, 16)
+    grids = wc.build_grids(cv)
+    cam = wc.Camera.look_at((47.5, 47.5, 47.5 + 1.8 * 96), (47.5, 47.5, 47.5))
+    w, h = 150, 110
+    iso = iso_at(vol, 0.3)
+    full, _ = wc.render(cv, grids, cam, iso, wc.RenderOptions(width=w, height=h))
+    for world in (2, 3, 4, 8):
+        rgba = np.zeros((h * w, 4), np.uint8)
+        depth = np.zeros(h * w, np.float32)
+        for rank in range(world):
+            pix = dist.tile_pixels(w, h, rank, world, tile=16)
+            with wc.RenderSession(cv, grids, cam, iso, wc.RenderOptions(width=w, height=h), pixel_ids=pix) as s:
+                s.run()
+                r, d = s.read()
+            rgba[pix] = r
+            depth[pix] = d
+        assert np.array_equal(rgba.reshape(h, w, 4), full.rgba), world
+        assert np.array_equal(depth.reshape(h, w), full.depth), world
+
+
+# ------------------------------------------------------------- brute force
+def test_brute_force_reference_render(wc):
+    vol = host_volume("sphere", 64)
+    cv = wc.compress_volume(vol, 16)
+    cam_t = orbit(cv.dims, 0.13)
+    cam = wc.Camera(*cam_t)
+    dec = wc.decode_full(cv)
+    w = h = 96
+    ref = wc.reference_render(dec, cam, 20.0, w, h)
+    o, d = orc.camera_rays(cam_t, w, h)
+    rgba, depth = orc.reference_render(dec.as_3d(), o, d, 20.0)
+    assert np.array_equal(ref.rgba.reshape(-1, 4), rgba)
+    assert np.array_equal(ref.depth.reshape(-1), depth)
+    fb, _ = wc.render(cv, wc.build_grids(cv), cam, 20.0, wc.RenderOptions(width=w, height=h))
+    diff = wc.compare_images(fb, ref)  # test_engine.py:155-163
+    assert diff["hit_mask_mismatches"] == 0 and diff["max_rgb_delta"] == 0 and diff["max_depth_delta"] <= 1e-3
+
+
+# --------------------------------------------------------------- prims
+def test_prims_scan_sort(wc):
+    rng = np.random.default_rng(5)
+    for n in (0, 1, 7, 2048, 2049, 100000, 1 << 20):
+        v = rng.integers(0, 1000, n).astype(np.uint32)
+        out, tot = wc.prims.exclusive_scan(v)
+        ref = np.concatenate([[0], np.cumsum(v.astype(np.uint64))[:-1]]).astype(np.uint32) if n else v
+        assert np.array_equal(out, ref) and tot == int(v.astype(np.uint64).sum())
+        keys = rng.integers(0, 50, n).astype(np.uint32)
+        vals = np.arange(n, dtype=np.uint32)
+        k2, v2 = wc.prims.sort_by_key(keys, vals)
+        order = np.argsort(keys, kind="stable")
+        assert np.array_equal(k2, keys[order]) and np.array_equal(v2, vals[order])
