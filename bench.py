@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""bench.py -- ms/frame & Mrays/s at 1080p on the 8.05B-voxel compressed volume.
+
+Workload (BASELINE.json configs[2]): a 2048x2048x1920
+turbulence-like field (12 separable Fourier modes, seed 1), WCZ1 qbits 16
+(16.6 GB payload, 125.8M blocks), 1920x1080, iso at 50% of the value range,
+orbit camera step 0, speculation on (max_spec 64).  A step is one full
+progressive render to completeness 1.0 (all passes).
+
+  python bench.py [--gpus N --steps K --warmup W]         # B200 arm
+  python bench.py --impl reference [...]                  # CPU reference arm
+
+B200 arm: the volume is synthesised + compressed on the device (bit-exact
+with the CPU encoder), each rank renders its interleaved image tiles, per
+frame device time comes from CUDA events on the session stream (L2 flushed
+between frames with a 512 MB write, outside the timed frames), max over
+ranks.  `e2e` times the public `render()` call with the framebuffer read
+back to host memory every frame.  The CPU oracle (oracle/, the C
+restatement of the reference) supplies `cpu_baseline` on a bounded pixel
+sample and checks those pixels against the GPU frame.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms/frame & Mrays/s at 1080p on 8.05B-voxel compressed volume, 1/2/4/8 GPU"
+UNIT = "Mrays/s"
+
+CONFIGS = {
+    # name: dims, kind, seed, qbits, w, h, iso fraction
+    "c3": ((2048, 2048, 1920), "turbulence", 1, 16, 1920, 1080, 0.5),
+    "c2": ((512, 512, 512), "gaussians", 0, 16, 1920, 1080, 0.3),
+    "c4": ((2048, 2048, 1920), "turbulence", 1, 16, 3840, 2160, 0.5),
+}
+WORKLOAD_NAMES = {
+    "c3": "2048x2048x1920 (8.05B voxels) turbulence-like field, WCZ1 qbits 16, 1920x1080, iso 50%, orbit cam 0",
+    "c2": "512^3 sum-of-24-Gaussians, WCZ1 qbits 16, 1920x1080, iso 30%, orbit cam 0",
+    "c4": "8.05B-voxel turbulence at 3840x2160 with a small cache budget",
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    p.add_argument("--max-spec", type=int, default=64)
+    p.add_argument("--cache-slots", type=int, default=0, help="LRU budget (0 = reference initial_capacity)")
+    p.add_argument("--tile", type=int, default=32)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-tiles", type=int, default=0, help="tiles in the CPU-baseline sample (0=auto)")
+    p.add_argument("--threads", type=int, default=0, help="host threads for the reference arm (0=all)")
+    return p.parse_args()
+
+
+def workload(cfg):
+    dims, kind, seed, qbits, w, h, isof = CONFIGS[cfg]
+    return dict(dims=dims, kind=kind, seed=seed, qbits=qbits, w=w, h=h, iso_frac=isof)
+
+
+def config_json(args, wl, n_gpus, extra=None):
+    c = {
+        "workload": WORKLOAD_NAMES[args.config],
+        "volume": {"dims": list(wl["dims"]), "kind": wl["kind"], "seed": wl["seed"], "qbits": wl["qbits"]},
+        "image": [wl["w"], wl["h"]],
+        "iso_fraction": wl["iso_frac"],
+        "camera": "orbit step 0 (eye = centre + (0, 0, 1.8*max(dims))), fov 45",
+        "speculation": True,
+        "max_spec": args.max_spec,
+        "parallelism": f"image tiles {args.tile}x{args.tile} dealt round-robin over {n_gpus} GPU(s)",
+        "l2": "flushed between timed frames (512 MB device write, outside the frame timing)",
+    }
+    if extra:
+        c.update(extra)
+    return c
+
+
+def orbit(dims):
+    from oracle import oracle as orc
+
+    return orc.orbit_camera(dims, 0, 1)
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/wc_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except OSError:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and "Active" in r[5 + i]
+                          and "Not" not in r[5 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+# ------------------------------------------------------------------ models
+def frame_bytes(stats, n_rays, stride):
+    """SURVEY.md §8(d) algorithmic bytes of one frame from its PassStats."""
+    b = 130 * n_rays
+    for i, s in enumerate(stats):
+        a = s.n_active_before
+        e = round(s.utilization * n_rays)
+        t = a - (stats[i + 1].n_active_before if i + 1 < len(stats) else 0)
+        b += n_rays + 177 * a + 108 * e + (stride + 256) * s.new_decompressed + 500 * s.visible_blocks + 25 * t
+    return b
+
+
+def stage_bytes(stage, stats, n_rays, stride):
+    """Algorithmic bytes of one stage's kernels over a frame (per-unit figures
+    from SURVEY.md §8(d), restricted to the stage)."""
+    A = sum(s.n_active_before for s in stats)
+    E = sum(round(s.utilization * n_rays) for s in stats)
+    V = sum(s.visible_blocks for s in stats)
+    D = sum(s.new_decompressed for s in stats)
+    if stage == "traverse":      # O_Act 4 + dir 24 + t_exit 8 + iterators 2x28 r+w + exited 1 ; R_BID/R_ID 8/entry
+        return 4 * A + 24 * A + 8 * A + 112 * A + 1 * A + 8 * E
+    if stage == "raytrace":      # 5^3 f32 dual grid per visible block; ids 8 + ray 56 + rgbz 16 per entry
+        return 500 * V + 80 * E
+    if stage == "cache_decode":  # compressed record read + f32[64] slot write per decoded block
+        return (stride + 256) * D
+    if stage == "group":         # sort keys/values read+write per entry (one digit pass)
+        return 16 * E
+    if stage == "composite":     # slot id 4 + prefix 4 + z 4 per entry; winner rgbz 16 + fb 8 + status 1
+        return 12 * E + 25 * A
+    if stage == "mark":
+        return 8 * E
+    return 0
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2309_10212_b200 as wc
+    from paper_2309_10212_b200 import dist as wdist
+
+    wc._lib.ensure_device(local)
+    wl = workload(args.config)
+    t0 = time.perf_counter()
+    field = wc.volume.separable_field(wl["kind"], wl["dims"], wl["seed"])
+    cv = wc.compress_separable(field, wl["qbits"])
+    grids = wc.build_grids(cv)
+    ranges = cv.raw_block_ranges
+    lo, hi = float(ranges[:, 0].min()), float(ranges[:, 1].max())
+    setup_s = time.perf_counter() - t0
+    iso = lo + wl["iso_frac"] * (hi - lo)
+    cam = wc.Camera(*orbit(wl["dims"]))
+    w, h = wl["w"], wl["h"]
+    cache = args.cache_slots if args.cache_slots > 0 else None
+    if args.config == "c4" and cache is None:
+        cache = 1024
+    opts = wc.RenderOptions(width=w, height=h, max_spec=args.max_spec, cache_capacity=cache)
+    pix = wdist.tile_pixels(w, h, rank, world, args.tile) if world > 1 else None
+    sess = wc.RenderSession(cv, grids, cam, iso, opts, pixel_ids=pix)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def frame():
+        sess.reset(cam, iso)
+        return sess.run()
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        frame()
+    frame_ms, stage_tot, stats = [], {}, None
+    launches0 = wc._lib.lib().wc_launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            stats = frame()
+            frame_ms.append(sess.frame_ms())
+            for k, v in sess.stage_ms().items():
+                stage_tot[k] = stage_tot.get(k, 0.0) + v
+        barrier()
+        wall_s = time.perf_counter() - wall0
+    launches = wc._lib.lib().wc_launch_count() - launches0
+    clocks = clk.summary()
+    total_ms = float(np.sum(frame_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_frame = total_ms / args.steps
+    value = (w * h) / (ms_per_frame * 1e-3) / 1e6
+    n_local = sess.n
+    stride = cv.block_stride_bytes
+
+    # ---- e2e through the public API with host buffers (framebuffer D2H every frame)
+    e2e_ms = []
+    fb = None
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        barrier()
+        t = time.perf_counter()
+        if world > 1:
+            fb, _ = wdist.render_sharded(cv, grids, cam, iso, opts, tile=args.tile)
+        else:
+            fb, _ = wc.render(cv, grids, cam, iso, opts)
+        barrier()
+        if i >= args.warmup:
+            e2e_ms.append((time.perf_counter() - t) * 1e3)
+    e2e_frame = float(np.mean(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_frame], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_frame = float(t.item())
+
+    # ---- roofline of the dominant stage (per-frame algorithmic bytes / stage time)
+    pk = peaks()
+    stage_frame = {k: v / args.steps for k, v in stage_tot.items()}
+    top = max(stage_frame, key=stage_frame.get)
+    tb = stage_bytes(top, stats, n_local, stride)
+    achieved = tb / (stage_frame[top] * 1e-3) / 1e9 if stage_frame[top] > 0 else 0.0
+    fbytes = frame_bytes(stats, n_local, stride)
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_frame, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (device-generated separable turbulence field, compressed on the device)",
+        "config": config_json(args, wl, world),
+        "e2e": {"value": round((w * h) / (e2e_frame * 1e-3) / 1e6, 3), "unit": UNIT,
+                "ms_per_frame": round(e2e_frame, 3), "h2d_bytes_per_step": 120 * world,
+                "d2h_bytes_per_step": 8 * w * h,
+                "path": "paper_2309_10212_b200.render() (pooled session reset + passes + framebuffer to host)"},
+        "gpu_launches": int(launches // max(1, args.steps)),
+        "gpu_launches_note": "library kernel launches per frame (counted in libwavecast_b200.so)",
+        "passes": len(stats),
+        "pass_stats": [{"n_active_before": s.n_active_before, "n_spec": s.n_spec, "visible": s.visible_blocks,
+                        "active": s.active_blocks, "decoded": s.new_decompressed, "cache_slots": s.cache_slots,
+                        "utilization": round(s.utilization, 4)} for s in stats],
+        "stage_ms_per_frame": {k: round(v, 4) for k, v in stage_frame.items()},
+        "frame_ms_all": [round(x, 3) for x in frame_ms],
+        "wall_s_timed_region": round(wall_s, 3),
+        "roofline": {"bound": "hbm", "kernel": top, "achieved": round(achieved, 2), "peak": pk["hbm_gbs"],
+                     "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 5), "traffic": None,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "_fallback" not in pk
+                     else "fallback 6650 GB/s (B200_PROFILING.md)",
+                     "frame_algorithmic_bytes": int(fbytes),
+                     "frame_frac": round(fbytes / (ms_per_frame * 1e-3) / 1e9 / pk["hbm_gbs"], 5)},
+        "clocks": clocks,
+        "setup_s": round(setup_s, 2),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"], line["parity"] = cpu_baseline(args, wl, cv, iso, fb)
+    print(json.dumps(line), flush=True)
+    sess.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_baseline(args, wl, cv, iso, fb):
+    """Oracle (C port of the reference path) on one host core over a sample of
+    image tiles; the same pixels are checked against the GPU frame."""
+    from oracle import oracle as orc
+
+    threads = os.cpu_count() or 1
+    field = __import__("paper_2309_10212_b200").volume.separable_field(wl["kind"], wl["dims"], wl["seed"])
+    t = time.perf_counter()
+    pay, rng = orc.compress_separable(field.amp, field.fx, field.fy, field.fz, wl["dims"], wl["qbits"], threads)
+    synth_s = time.perf_counter() - t
+    volume_bit_exact = bool(np.array_equal(pay, cv.payload)) and bool(np.array_equal(rng, cv.raw_block_ranges))
+    ov = orc.volume_from_payload(wl["dims"], wl["qbits"], pay, rng)
+    w, h = wl["w"], wl["h"]
+    cam = orbit(wl["dims"])
+    # sample: every k-th 32x32 tile (interleaved), one thread
+    tiles_total = -(w // -32) * -(h // -32)
+    n_tiles = args.cpu_sample_tiles or max(1, tiles_total // 16)
+    world = max(1, tiles_total // n_tiles)
+    pix = orc.tile_pixels(w, h, 0, world, 32)
+    o, d = orc.camera_rays(cam, w, h, pix)
+    t = time.perf_counter()
+    rgba, depth, st = orc.render(ov, o, d, len(pix), 1, iso, max_spec=args.max_spec)  # budget = sample rays
+    cpu_s = time.perf_counter() - t
+    mism = None
+    if fb is not None:
+        g_rgba = fb.rgba.reshape(-1, 4)[pix]
+        g_depth = fb.depth.reshape(-1)[pix]
+        mism = int(np.count_nonzero((g_rgba != rgba).any(1) | (g_depth.view(np.uint32) != depth.view(np.uint32))))
+    base = {"value": round(len(pix) / cpu_s / 1e6, 5), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{len(pix)} rays = every {world}th 32x32 tile of the 1080p frame, full pass loop, 1 thread "
+                      f"({cpu_s:.1f} s, {len(st)} passes)", "seconds": round(cpu_s, 2)}
+    parity = {"cpu_volume_synth_bit_exact": volume_bit_exact, "cpu_synth_s": round(synth_s, 1),
+              "pixels_checked": int(len(pix)), "pixel_mismatches": mism}
+    return base, parity
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+
+    import paper_2309_10212_b200.volume as V  # host numpy generator only (no GPU code)
+
+    wl = workload(args.config)
+    threads = args.threads or os.cpu_count() or 1
+    field = V.separable_field(wl["kind"], wl["dims"], wl["seed"])
+    t = time.perf_counter()
+    pay, rng = orc.compress_separable(field.amp, field.fx, field.fy, field.fz, wl["dims"], wl["qbits"], threads)
+    ov = orc.volume_from_payload(wl["dims"], wl["qbits"], pay, rng)
+    setup_s = time.perf_counter() - t
+    lo, hi = float(rng[:, 0].min()), float(rng[:, 1].max())
+    iso = lo + wl["iso_frac"] * (hi - lo)
+    cam = orbit(wl["dims"])
+    w, h = wl["w"], wl["h"]
+    cache = args.cache_slots if args.cache_slots > 0 else (1024 if args.config == "c4" else 0)
+    for _ in range(args.warmup):
+        orc.render_parallel(ov, cam, w, h, iso, threads, max_spec=args.max_spec, cache_capacity=cache)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        orc.render_parallel(ov, cam, w, h, iso, threads, max_spec=args.max_spec, cache_capacity=cache)
+        times.append(time.perf_counter() - t)
+    ms = float(np.mean(times)) * 1e3
+    value = (w * h) / (ms * 1e-3) / 1e6
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "impl": "reference", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (host-generated, same field)",
+        "config": config_json(args, wl, 0, {"parallelism": f"{threads} host threads, interleaved 32x32 tiles"}),
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": "full 1920x1080 frame per step (oracle/ C restatement of the reference path, "
+                                   "tile-parallel over host threads)"},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": round(setup_s, 1),
+        "note": "reference is pure Python+numba (no C/C++ to compile); its CPU path is timed through oracle/, "
+                "the bit-exact C port pinned to the reference's golden vectors",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -59,6 +59,8 @@ typedef struct {
 const char *wc_last_error(void);
 /* Select the CUDA device (fails loudly when no GPU is present). */
 int wc_init(int device);
+/* Number of kernels this library has launched so far (all threads). */
+long long wc_launch_count(void);
 /* Build-time identity string (arch, flags). */
 const char *wc_build_info(void);
 
@@ -111,6 +113,16 @@ int wc_session_framebuffer_device(wc_session *s, void *rgba_dev, void *depth_dev
 /* Device time of the last pass (CUDA events on the session stream). */
 int wc_session_last_pass_ms(const wc_session *s, double *ms);
 int wc_session_destroy(wc_session *s);
+/* Start a new frame on the same allocations (a viewer moving its camera):
+ * fresh rays for `cam` (NULL keeps the camera; arbitrary-ray sessions
+ * re-seed their rays), new iso, blank framebuffer, empty cache. */
+int wc_session_reset(wc_session *s, const wc_camera *cam, double iso);
+/* Device time (CUDA events on the session stream) from the last
+ * create/reset to the end of the last pass. */
+int wc_session_frame_ms(wc_session *s, double *ms);
+/* Accumulated device ms per stage since the last reset:
+ * [traverse, mark+extract, cache+decode, group(sort), raytrace, composite] */
+int wc_session_stage_ms(const wc_session *s, double *ms6);
 
 /* ---- per-stage views of the last pass (parity tests) */
 /* sizes[8] = slots_used, n_visible, n_active_blocks, n_entries, n_spec,

@@ -99,6 +99,8 @@ def lib():
     L.orc_get_cache.argtypes = [_vp] * 4
     L.orc_decode_blocks.argtypes = [_vp, C.c_int, C.c_int, _vp, _i64, _vp]
     L.orc_compress.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp]
+    L.orc_compress_separable.argtypes = [C.c_int, _vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, _vp, _vp]
     L.orc_error_bounds.argtypes = [_vp, _i64, C.c_int, C.c_int, _vp]
     L.orc_build_grids.argtypes = [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp]
     L.orc_camera_rays.argtypes = [_vp, _vp, _i64, _vp, _vp]
@@ -212,6 +214,72 @@ def compress(values_xfast: np.ndarray, dims, qbits: int):
     v = np.ascontiguousarray(values_xfast, dtype=np.float32).reshape(-1)
     lib().orc_compress(_p(v), nx, ny, nz, qbits, _p(payload), _p(ranges), _p(expo))
     return payload, ranges, expo
+
+
+def compress_separable(amp, fx, fy, fz, dims, qbits: int, threads: int = 1):
+    """Synthesise + compress a separable field on host threads (ctypes drops
+    the GIL, so block layers run in parallel).  Bit-identical to compress()
+    of the evaluated field."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    nx, ny, nz = dims
+    bd = [-(d // -4) for d in dims]
+    nb = bd[0] * bd[1] * bd[2]
+    stride = stride_of(qbits)
+    payload = np.zeros(nb * stride, dtype=np.uint8)
+    ranges = np.empty((nb, 2), dtype=np.float32)
+    arrs = [np.ascontiguousarray(a, dtype=np.float32) for a in (amp, fx, fy, fz)]
+    K = len(arrs[0])
+    bz = bd[2]
+    chunks = max(1, min(bz, threads * 4))
+    edges = [bz * i // chunks for i in range(chunks + 1)]
+
+    def work(i):
+        lib().orc_compress_separable(K, *[_p(a) for a in arrs], nx, ny, nz, qbits, edges[i], edges[i + 1],
+                                     _p(payload), _p(ranges))
+
+    with ThreadPoolExecutor(max_workers=max(1, threads)) as ex:
+        list(ex.map(work, range(chunks)))
+    return payload, ranges
+
+
+def tile_pixels(w: int, h: int, rank: int, world: int, tile: int = 32) -> np.ndarray:
+    """Same interleaved tile deal as the product's dist.tile_pixels (restated
+    here so the oracle shares no code with the product)."""
+    tx = -(w // -tile)
+    ty = -(h // -tile)
+    out = []
+    for t in range(rank, tx * ty, world):
+        x0, y0 = (t % tx) * tile, (t // tx) * tile
+        xs = np.arange(x0, min(x0 + tile, w))
+        for y in range(y0, min(y0 + tile, h)):
+            out.append(y * w + xs)
+    return np.concatenate(out).astype(np.int64) if out else np.zeros(0, np.int64)
+
+
+def render_parallel(vol, cam, w, h, iso, threads: int, tile: int = 32, **kw):
+    """Tile-parallel oracle render on `threads` host threads (one oracle
+    session per thread over interleaved tiles; speculation invariance makes
+    the stitched frame identical to a single-thread render).  Returns
+    (rgba (w*h,4), depth (w*h,), per-thread stats lists)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rgba = np.zeros((w * h, 4), np.uint8)
+    depth = np.zeros(w * h, np.float32)
+
+    def work(t):
+        pix = tile_pixels(w, h, t, threads, tile)
+        if len(pix) == 0:
+            return []
+        o, d = camera_rays(cam, w, h, pix)
+        r, z, st = render(vol, o, d, len(pix), 1, iso, **kw)  # slot budget = rays of the tile set
+        rgba[pix] = r
+        depth[pix] = z
+        return st
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        stats = list(ex.map(work, range(threads)))
+    return rgba, depth, stats
 
 
 def volume_from_payload(dims, qbits, payload, ranges) -> OracleVolume:

@@ -20,6 +20,17 @@
 #define ENTRY_NUDGE 1e-7 /* blocktrace.py:31 */
 #define AMBIENT 0.2      /* blocktrace.py:26 */
 
+/* Reference invariant failures (AssertionError in the reference) end the
+ * checker loudly with the reference's own message. */
+#include <stdio.h>
+#define ORC_ASSERT(cond, msg)                                      \
+    do {                                                           \
+        if (!(cond)) {                                             \
+            fprintf(stderr, "oracle invariant failed: %s\n", msg); \
+            abort();                                               \
+        }                                                          \
+    } while (0)
+
 static void *xcalloc(size_t n, size_t sz) {
     void *p = calloc(n ? n : 1, sz ? sz : 1);
     if (!p) abort();
@@ -80,66 +91,120 @@ void orc_decode_blocks(const uint8_t *payload, int qbits, int stride,
     for (int64_t j = 0; j < n; j++) unpack_block(payload, ids[j], qbits, stride, out + 64 * j);
 }
 
-/* codec.py:177-198 compress_volume with _gather_blocks (:81-97),
- * _block_exponents (:100-105) and _pack_blocks (:120-140). */
-void orc_compress(const float *values, int nx, int ny, int nz, int qbits,
-                  uint8_t *payload, float *ranges, int32_t *exponents) {
-    const int bdx = (nx + 3) / 4, bdy = (ny + 3) / 4, bdz = (nz + 3) / 4;
-    const int stride = ((16 + 64 * qbits + 31) / 32) * 4;
+/* codec.py:100-105 _block_exponents + :183-185 quantisation + :120-140
+ * _pack_blocks for one gathered block (blk: 64 edge-replicated values,
+ * x fastest).  Returns the exponent. */
+static int32_t pack_block(const float *blk, int qbits, uint8_t *rec) {
     const double s = (double)(((int64_t)1 << (qbits - 1)) - 1);
     const int64_t mask = ((int64_t)1 << qbits) - 1;
+    float m = 0.0f;
+    for (int i = 0; i < 64; i++) {
+        const float a = fabsf(blk[i]);
+        if (a > m) m = a;
+    }
+    int32_t e;
+    if ((double)m == 0.0) {
+        e = -32768;
+    } else {
+        int ex;
+        const double mant = frexp((double)m, &ex);
+        e = ex - (mant == 0.5);
+    }
+    const uint16_t eu = (uint16_t)(int16_t)e;
+    rec[0] = (uint8_t)(eu & 0xFF);
+    rec[1] = (uint8_t)((eu >> 8) & 0xFF);
+    if (e == -32768) return e;
+    const double scale = ldexp(1.0, -e);
+    for (int i = 0; i < 64; i++) {
+        const double qd = rint((double)blk[i] * scale * s); /* np.rint: half-even */
+        const int64_t q = (int64_t)(int32_t)qd & mask;
+        const int64_t bitpos = 16 + (int64_t)i * qbits;
+        const int shift = (int)(bitpos & 7);
+        const int64_t accv = q << shift;
+        const int nbytes = (shift + qbits + 7) >> 3;
+        for (int k = 0; k < nbytes; k++) rec[(bitpos >> 3) + k] |= (uint8_t)((accv >> (8 * k)) & 0xFF);
+    }
+    return e;
+}
+
+/* codec.py:81-97 _gather_blocks for block (bx,by,bz) of a field given by
+ * a sampler; fills blk and the valid-voxel (min, max). */
+typedef float (*orc_sampler)(const void *ctx, int x, int y, int z);
+
+static void gather_block(orc_sampler f, const void *ctx, int nx, int ny, int nz, int bx, int by, int bz, float *blk,
+                         float *mn_out, float *mx_out) {
+    float mn = INFINITY, mx = -INFINITY;
+    for (int k = 0; k < 4; k++)
+        for (int j = 0; j < 4; j++)
+            for (int i = 0; i < 4; i++) {
+                int x = 4 * bx + i, y = 4 * by + j, z = 4 * bz + k;
+                const int valid = x < nx && y < ny && z < nz;
+                if (x >= nx) x = nx - 1; /* np.pad mode="edge" */
+                if (y >= ny) y = ny - 1;
+                if (z >= nz) z = nz - 1;
+                const float v = f(ctx, x, y, z);
+                blk[i + 4 * j + 16 * k] = v;
+                if (valid) {
+                    if (v < mn) mn = v;
+                    if (v > mx) mx = v;
+                }
+            }
+    *mn_out = mn;
+    *mx_out = mx;
+}
+
+typedef struct {
+    const float *v;
+    int nx, ny;
+} dense_ctx;
+
+static float dense_sample(const void *ctx, int x, int y, int z) {
+    const dense_ctx *c = (const dense_ctx *)ctx;
+    return c->v[x + (int64_t)c->nx * (y + (int64_t)c->ny * z)];
+}
+
+typedef struct {
+    int K, nx, ny, nz;
+    const float *amp, *fx, *fy, *fz;
+} sep_ctx;
+
+/* separable field, float32 in the same order as volume.SeparableField */
+static float sep_sample(const void *ctx, int x, int y, int z) {
+    const sep_ctx *c = (const sep_ctx *)ctx;
+    float v = 0.0f;
+    for (int k = 0; k < c->K; k++)
+        v = v + ((c->amp[k] * c->fz[(int64_t)k * c->nz + z]) * c->fy[(int64_t)k * c->ny + y]) * c->fx[(int64_t)k * c->nx + x];
+    return v;
+}
+
+static void compress_layers(orc_sampler f, const void *ctx, int nx, int ny, int nz, int qbits, int bz0, int bz1,
+                            uint8_t *payload, float *ranges, int32_t *exponents) {
+    const int bdx = (nx + 3) / 4, bdy = (ny + 3) / 4;
+    const int stride = ((16 + 64 * qbits + 31) / 32) * 4;
     float blk[64];
-    for (int bz = 0; bz < bdz; bz++)
+    for (int bz = bz0; bz < bz1; bz++)
         for (int by = 0; by < bdy; by++)
             for (int bx = 0; bx < bdx; bx++) {
                 const int64_t b = bx + (int64_t)bdx * (by + (int64_t)bdy * bz);
-                float mn = INFINITY, mx = -INFINITY;
-                float m = 0.0f;
-                for (int k = 0; k < 4; k++)
-                    for (int j = 0; j < 4; j++)
-                        for (int i = 0; i < 4; i++) {
-                            int x = 4 * bx + i, y = 4 * by + j, z = 4 * bz + k;
-                            const int valid = x < nx && y < ny && z < nz;
-                            if (x >= nx) x = nx - 1; /* np.pad mode="edge" */
-                            if (y >= ny) y = ny - 1;
-                            if (z >= nz) z = nz - 1;
-                            const float v = values[x + (int64_t)nx * (y + (int64_t)ny * z)];
-                            blk[i + 4 * j + 16 * k] = v;
-                            if (valid) {
-                                if (v < mn) mn = v;
-                                if (v > mx) mx = v;
-                            }
-                            const float a = fabsf(v);
-                            if (a > m) m = a;
-                        }
-                ranges[2 * b] = mn;
-                ranges[2 * b + 1] = mx;
-                int32_t e;
-                if ((double)m == 0.0) {
-                    e = -32768;
-                } else {
-                    int ex;
-                    const double mant = frexp((double)m, &ex);
-                    e = ex - (mant == 0.5);
-                }
+                gather_block(f, ctx, nx, ny, nz, bx, by, bz, blk, &ranges[2 * b], &ranges[2 * b + 1]);
+                const int32_t e = pack_block(blk, qbits, payload + b * stride);
                 if (exponents) exponents[b] = e;
-                const int64_t base = b * stride;
-                const uint16_t eu = (uint16_t)(int16_t)e;
-                payload[base] = (uint8_t)(eu & 0xFF);
-                payload[base + 1] = (uint8_t)((eu >> 8) & 0xFF);
-                if (e == -32768) continue;
-                const double scale = ldexp(1.0, -e);
-                for (int i = 0; i < 64; i++) {
-                    const double qd = rint((double)blk[i] * scale * s); /* np.rint: half-even */
-                    const int64_t q = (int64_t)(int32_t)qd & mask;
-                    const int64_t bitpos = 16 + (int64_t)i * qbits;
-                    const int64_t byte = base + (bitpos >> 3);
-                    const int shift = (int)(bitpos & 7);
-                    const int64_t accv = q << shift;
-                    const int nbytes = (shift + qbits + 7) >> 3;
-                    for (int k = 0; k < nbytes; k++) payload[byte + k] |= (uint8_t)((accv >> (8 * k)) & 0xFF);
-                }
             }
+}
+
+/* codec.py:177-198 compress_volume (payload zeroed by the caller) */
+void orc_compress(const float *values, int nx, int ny, int nz, int qbits,
+                  uint8_t *payload, float *ranges, int32_t *exponents) {
+    dense_ctx c = {values, nx, ny};
+    compress_layers(dense_sample, &c, nx, ny, nz, qbits, 0, (nz + 3) / 4, payload, ranges, exponents);
+}
+
+/* Same for a separable synthetic field, block layers [bz0, bz1) only, so
+ * callers can split an 8.05B-voxel volume across host threads. */
+void orc_compress_separable(int K, const float *amp, const float *fx, const float *fy, const float *fz, int nx,
+                            int ny, int nz, int qbits, int bz0, int bz1, uint8_t *payload, float *ranges) {
+    sep_ctx c = {K, nx, ny, nz, amp, fx, fy, fz};
+    compress_layers(sep_sample, &c, nx, ny, nz, qbits, bz0, bz1, payload, ranges, NULL);
 }
 
 /* codec.py:113-117 _bounds_from_exponents over codec.py:220-223 */
@@ -1029,7 +1094,7 @@ static void raytrace_block_entries(orc_session *s, int64_t v) {
                     slot[idx] = -1;
                 }
             }
-    if (slot[0] < 0) abort(); /* "visible block not resident" */
+    ORC_ASSERT(slot[0] >= 0, "visible block not resident"); /* engine.py:302 */
     const float *sv = s->cache->slot_values;
     /* blocktrace.py:49-94 _assemble_dual */
     for (int k = 0; k < 5; k++)
@@ -1084,7 +1149,7 @@ int orc_session_pass(orc_session *s, orc_pass_stats *st) {
         if (q < 1) q = 1;
         n_spec = q < s->max_spec ? q : s->max_spec;
     }
-    if (n_act * n_spec > n) abort(); /* traversal.py:422 slot budget */
+    ORC_ASSERT(n_act * n_spec <= n, "slot budget exceeded"); /* traversal.py:422 */
     /* traversal.py:423-424 */
     for (int64_t i = 0; i < n; i++) s->block_slots[i] = s->ray_slots[i] = ORC_UINT_MAX;
     for (int64_t r = 0; r < n; r++)
@@ -1122,7 +1187,7 @@ int orc_session_pass(orc_session *s, orc_pass_stats *st) {
         ne += s->block_slots[i] != ORC_UINT_MAX;
     }
     s->n_entries = ne;
-    if (ne > n) abort();
+    ORC_ASSERT(ne <= n, "slot budget exceeded"); /* engine.py:341 */
     for (int64_t v = 0; v < s->n_vis; v++) s->rays_per_block[v] = 0;
     for (int64_t i = 0; i < s->slots_used; i++) {
         const uint32_t b = s->block_slots[i];
@@ -1134,7 +1199,7 @@ int orc_session_pass(orc_session *s, orc_pass_stats *st) {
         s->block_ray_offsets[v] = run;
         run += s->rays_per_block[v];
     }
-    if ((int64_t)run != ne) abort(); /* engine.py:140 */
+    ORC_ASSERT((int64_t)run == ne, "ray-block grouping is inconsistent"); /* engine.py:140 */
     uint32_t *cursor = xmalloc(4 * (s->n_vis + 1));
     memcpy(cursor, s->block_ray_offsets, 4 * s->n_vis);
     for (int64_t i = 0; i < s->slots_used; i++) {

@@ -56,6 +56,9 @@ void orc_decode_blocks(const uint8_t *payload, int qbits, int stride,
  * _pack_blocks :120-140). payload must be zeroed by the caller. */
 void orc_compress(const float *values, int nx, int ny, int nz, int qbits,
                   uint8_t *payload, float *ranges, int32_t *exponents);
+/* compress of a separable field sum_k ((amp*fz)*fy)*fx, block layers [bz0,bz1) */
+void orc_compress_separable(int K, const float *amp, const float *fx, const float *fy, const float *fz, int nx,
+                            int ny, int nz, int qbits, int bz0, int bz1, uint8_t *payload, float *ranges);
 /* codec.py:113-117 over the exponents stored in the payload (:220-223) */
 void orc_error_bounds(const uint8_t *payload, int64_t n_blocks, int qbits,
                       int stride, double *bounds);

@@ -71,6 +71,7 @@ def build(verbose: bool = False) -> str:
 _SIGS = {
     "wc_last_error": (C.c_char_p, []),
     "wc_init": (_i32, [_i32]),
+    "wc_launch_count": (C.c_longlong, []),
     "wc_build_info": (C.c_char_p, []),
     "wc_volume_create": (_i32, [_vp, C.c_uint64, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
     "wc_volume_compress": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp]),
@@ -91,6 +92,9 @@ _SIGS = {
     "wc_session_last_pass_ms": (_i32, [_vp, _vp]),
     "wc_session_destroy": (_i32, [_vp]),
     "wc_session_sizes": (_i32, [_vp, _vp]),
+    "wc_session_reset": (_i32, [_vp, _vp, _dbl]),
+    "wc_session_frame_ms": (_i32, [_vp, _vp]),
+    "wc_session_stage_ms": (_i32, [_vp, _vp]),
     "wc_session_rays": (_i32, [_vp] * 10),
     "wc_session_slots": (_i32, [_vp] * 4),
     "wc_session_blocks": (_i32, [_vp] * 3),

@@ -77,6 +77,8 @@ const char *wc_build_info(void) {
     return "libwavecast_b200: sm_100a (compute_100a), -fmad=false -lineinfo -O3";
 }
 
+long long wc_launch_count(void) { return wc::g_launches.load(); }
+
 int wc_init(int device) {
     WC_API_BEGIN
     int n = 0;
@@ -324,6 +326,24 @@ int wc_session_destroy(wc_session *s) {
     WC_API_BEGIN
     if (s) delete s->s;
     delete s;
+    WC_API_END
+}
+
+int wc_session_reset(wc_session *s, const wc_camera *cam, double iso) {
+    WC_API_BEGIN
+    s->s->reset(reinterpret_cast<const wc::CameraParams *>(cam), iso);
+    WC_API_END
+}
+
+int wc_session_frame_ms(wc_session *s, double *ms) {
+    WC_API_BEGIN
+    *ms = s->s->frame_ms();
+    WC_API_END
+}
+
+int wc_session_stage_ms(const wc_session *s, double *ms6) {
+    WC_API_BEGIN
+    for (int k = 0; k < wc::Session::kStages; k++) ms6[k] = s->s->stage_ms[k];
     WC_API_END
 }
 

@@ -417,6 +417,14 @@ __global__ void k_cache_stamp(const uint32_t *ids, int64_t n, const int32_t *slo
     }
 }
 
+// BlockCache reset: forget every resident block of the previous frame
+__global__ void k_cache_unmap(const int32_t *block_of_slot, int64_t phys, int32_t *slot_of_block) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < phys; s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t b = block_of_slot[s];
+        if (b >= 0) slot_of_block[b] = -1;
+    }
+}
+
 __global__ void k_gather_last_used(const uint32_t *val, int64_t n, const int32_t *last_used, uint32_t *key) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         key[i] = (uint32_t)last_used[val[i]];
@@ -663,13 +671,10 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     WC_CUDA(cudaEventCreate(&ev_begin));
     WC_CUDA(cudaEventCreate(&ev_end));
     uniform_origin = dirs == nullptr;
-    if (cam) {
-        eye[0] = cam->eye[0];
-        eye[1] = cam->eye[1];
-        eye[2] = cam->eye[2];
-    }
     dir.alloc(n * 3);
     if (!uniform_origin) origin.alloc(n * 3);
+    for (auto &e : ev_stage) WC_CUDA(cudaEventCreate(&e));
+    WC_CUDA(cudaEventCreate(&ev_frame0));
     t_enter.alloc(n);
     t_exit.alloc(n);
     coarse_tmax.alloc(n * 3);
@@ -709,49 +714,69 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     h_counters.alloc(C_COUNT);
     partials.alloc(scan_tiles(std::max<int64_t>({n, nwords, active_ids.n, 1})) + 8);
 
-    // device copies of the inputs
-    DevBuf<uint32_t> d_pix;
-    DevBuf<double> d_o, d_d;
+    slot_of_block.alloc(vol->n_blocks);
+    WC_CUDA(cudaMemsetAsync(slot_of_block.p, 0xFF, 4 * vol->n_blocks, st));
     if (pixel_ids) {
-        d_pix.alloc(n);
-        WC_CUDA(cudaMemcpyAsync(d_pix.p, pixel_ids, 4 * n, cudaMemcpyHostToDevice, st));
+        pix.alloc(n);
+        WC_CUDA(cudaMemcpyAsync(pix.p, pixel_ids, 4 * n, cudaMemcpyHostToDevice, st));
     }
     if (dirs) {
-        d_o.alloc(3 * n);
-        d_d.alloc(3 * n);
-        WC_CUDA(cudaMemcpyAsync(d_o.p, origins, 24 * n, cudaMemcpyHostToDevice, st));
-        WC_CUDA(cudaMemcpyAsync(d_d.p, dirs, 24 * n, cudaMemcpyHostToDevice, st));
+        dir_in.alloc(3 * n);
+        WC_CUDA(cudaMemcpyAsync(origin.p, origins, 24 * n, cudaMemcpyHostToDevice, st));
+        WC_CUDA(cudaMemcpyAsync(dir_in.p, dirs, 24 * n, cudaMemcpyHostToDevice, st));
     }
+    init_cap = cache_capacity;
+    reset(cam, iso_);
+}
+
+// A new frame on the same allocations: fresh rays for (cam, iso), a blank
+// framebuffer and an empty cache of the initial logical capacity (the
+// reference builds a new RaySoA / BlockCache per render, engine.py:316-320).
+void Session::reset(const CameraParams *cam, double iso_) {
+    iso = iso_;
+    if (cam) {
+        cam_params = *cam;
+        eye[0] = cam->eye[0];
+        eye[1] = cam->eye[1];
+        eye[2] = cam->eye[2];
+    }
+    WC_CUDA(cudaEventRecord(ev_frame0, st));
     RayInitArgs a{};
-    if (cam) a.cam = *cam;
-    a.pixel_ids = pixel_ids ? d_pix.p : nullptr;
-    a.origin_in = dirs ? d_o.p : nullptr;
-    a.dir_in = dirs ? d_d.p : nullptr;
+    a.cam = cam_params;
+    a.pixel_ids = pix.p;
+    a.origin_in = uniform_origin ? nullptr : origin.p;
+    a.dir_in = uniform_origin ? nullptr : dir_in.p;
     a.nx = vol->nx;
     a.ny = vol->ny;
     a.nz = vol->nz;
-    k_init_rays<<<grid_for(n, 256), 256, 0, st>>>(a, n, uniform_origin ? nullptr : origin.p, dir.p, t_enter.p,
-                                                  t_exit.p, status.p, exited.p, coarse_cell.p, fine_cell.p,
-                                                  coarse_tmax.p, fine_tmax.p, rgba.p, depth.p);
+    k_init_rays<<<grid_for(n, 256), 256, 0, st>>>(a, n, nullptr, dir.p, t_enter.p, t_exit.p, status.p, exited.p,
+                                                  coarse_cell.p, fine_cell.p, coarse_tmax.p, fine_tmax.p, rgba.p,
+                                                  depth.p);
     WC_LAUNCH_CHECK();
     // initial active list (engine.py:331 on pass 0)
+    WC_CUDA(cudaMemsetAsync(counters.p, 0, 4 * C_COUNT, st));
     PredActive pa{status.p};
     scan_exclusive(pa, n, entry_off.p, counters.p + C_NACT, partials.p, st);
     k_compact_index<<<grid_for(n, 256), 256, 0, st>>>(pa, n, entry_off.p, act_list[0].p);
     WC_LAUNCH_CHECK();
+    cur = 0;
 
     // cache (cache.py:27-40, initial_capacity :122-125 with w*h == n)
-    if (cache_capacity <= 0) cache_capacity = std::max<int64_t>(1024, 2 * n / 64);
-    cap = std::max<int64_t>(1, cache_capacity);
+    if (phys > 0) {  // unmap whatever the previous frame left resident
+        k_cache_unmap<<<grid_for(phys, 256), 256, 0, st>>>(block_of_slot.p, phys, slot_of_block.p);
+        WC_LAUNCH_CHECK();
+    }
+    cap = std::max<int64_t>(1, init_cap <= 0 ? std::max<int64_t>(1024, 2 * n / 64) : init_cap);
     phys = std::min<int64_t>(cap, vol->n_blocks);
-    slot_values.alloc(phys * 64);
-    block_of_slot.alloc(phys);
-    last_used.alloc(phys);
-    slot_of_block.alloc(vol->n_blocks);
+    slot_values.grow(phys * 64, st);
+    block_of_slot.grow(phys, st);
+    last_used.grow(phys, st);
     WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * phys, st));
     WC_CUDA(cudaMemsetAsync(block_of_slot.p, 0xFF, 4 * phys, st));
     WC_CUDA(cudaMemsetAsync(last_used.p, 0, 4 * phys, st));
-    WC_CUDA(cudaMemsetAsync(slot_of_block.p, 0xFF, 4 * vol->n_blocks, st));
+    pass_no = 0;
+    pass_index = 0;
+    for (double &m : stage_ms) m = 0.0;
     read_counters(C_NACT, 1);
     n_act = h_counters.p[0];
 }
@@ -763,6 +788,9 @@ Session::~Session() {
     }
     if (ev_begin) cudaEventDestroy(ev_begin);
     if (ev_end) cudaEventDestroy(ev_end);
+    if (ev_frame0) cudaEventDestroy(ev_frame0);
+    for (auto &e : ev_stage)
+        if (e) cudaEventDestroy(e);
 }
 
 void Session::read_counters(int first, int count) {
@@ -777,7 +805,7 @@ void Session::ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict)
         cap = (3 * n_actb + 1) / 2;
         const int64_t new_phys = std::min<int64_t>(cap, vol->n_blocks);
         if (new_phys > phys) {
-            slot_values.grow(new_phys * 64, st);
+            slot_values.grow(new_phys * 64, st);  // keeps resident slots (cache.py:42-53)
             block_of_slot.grow(new_phys, st);
             last_used.grow(new_phys, st);
             WC_CUDA(cudaMemsetAsync(slot_values.p + phys * 64, 0, 4 * 64 * (new_phys - phys), st));
@@ -841,6 +869,7 @@ bool Session::pass(PassStatsC &stats) {
     if (n_act == 0) return false;
     const auto t_start = std::chrono::steady_clock::now();
     WC_CUDA(cudaEventRecord(ev_begin, st));
+    WC_CUDA(cudaEventRecord(ev_stage[0], st));
     // engine.py:333 / :91-94 compute_n_spec (slot budget = rays in session)
     int64_t n_spec = 1;
     if (speculation) n_spec = std::min<int64_t>(max_spec, std::max<int64_t>(1, n / n_act));
@@ -877,6 +906,7 @@ bool Session::pass(PassStatsC &stats) {
     ta.vis_bm = vis_bm.p;
     k_traverse<<<grid_for(n_act, 128, 16), 128, 0, st>>>(ta);
     WC_LAUNCH_CHECK();
+    WC_CUDA(cudaEventRecord(ev_stage[1], st));
     // entry compaction: exclusive scan of per-ray emitted counts
     scan_exclusive(LoadU32{emitted.p}, n_act, entry_off.p, counters.p + C_NENT, partials.p, st);
     // visible ids (ascending) + active marking
@@ -891,6 +921,7 @@ bool Session::pass(PassStatsC &stats) {
     WC_LAUNCH_CHECK();
     WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
     WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
+    WC_CUDA(cudaEventRecord(ev_stage[2], st));
     read_counters(C_NENT, 3);
     const int64_t n_ent = h_counters.p[0], nvis = h_counters.p[1], nactb = h_counters.p[2];
     if (n_ent > n) throw InvariantError("slot budget exceeded");
@@ -902,12 +933,14 @@ bool Session::pass(PassStatsC &stats) {
     int64_t n_miss = 0, n_evict = 0;
     ensure_resident(nactb, n_miss, n_evict);
     if (corrupt) WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * phys, st));  // engine.py:338-339
+    WC_CUDA(cudaEventRecord(ev_stage[3], st));
 
     // build_rt_inputs: stable grouping of entries by visible block
     if (n_ent > 0) {
         radix_sort_pairs(ent_key.p, ent_val.p, n_ent, bits_for((uint64_t)(nvis - 1)), rs, st);
         k_run_offsets<<<grid_for(n_ent, 256), 256, 0, st>>>(ent_key.p, n_ent, nvis, block_ray_off.p);
         WC_LAUNCH_CHECK();
+        WC_CUDA(cudaEventRecord(ev_stage[4], st));
         RaytraceArgs ra{};
         ra.visible_ids = visible_ids.p;
         ra.block_ray_off = block_ray_off.p;
@@ -931,7 +964,10 @@ bool Session::pass(PassStatsC &stats) {
         ra.err = counters.p + C_ERR;
         k_raytrace<<<grid_for(nvis * 32, 256, 8), 256, 0, st>>>(ra);
         WC_LAUNCH_CHECK();
+    } else {
+        WC_CUDA(cudaEventRecord(ev_stage[4], st));
     }
+    WC_CUDA(cudaEventRecord(ev_stage[5], st));
     // composite + compaction of the surviving rays (next pass's O_Act)
     k_composite<<<grid_for(n_act, 256), 256, 0, st>>>(n_act, alist, emitted.p, entry_off.p, rgbz.p, exited.p,
                                                       status.p, rgba.p, depth.p, keep.p);
@@ -940,10 +976,16 @@ bool Session::pass(PassStatsC &stats) {
     k_compact_keep<<<grid_for(n_act, 256), 256, 0, st>>>(keep.p, keep_off.p, alist, n_act, act_list[cur ^ 1].p);
     WC_LAUNCH_CHECK();
     WC_CUDA(cudaEventRecord(ev_end, st));
+    WC_CUDA(cudaEventRecord(ev_stage[6], st));
     read_counters(0, C_COUNT);
     const int64_t n_after = h_counters.p[C_NACT];
     if (h_counters.p[C_ERR]) throw InvariantError("visible block not resident");
     WC_CUDA(cudaEventElapsedTime(&last_kernel_ms, ev_begin, ev_end));
+    for (int k = 0; k < kStages; k++) {
+        float ms = 0.0f;
+        WC_CUDA(cudaEventElapsedTime(&ms, ev_stage[k], ev_stage[k + 1]));
+        stage_ms[k] += ms;
+    }
     stats.pass_index = pass_index;
     stats.n_active_before = n_act;
     stats.n_spec = n_spec;
@@ -961,6 +1003,13 @@ bool Session::pass(PassStatsC &stats) {
     n_act = n_after;
     pass_index++;
     return true;
+}
+
+float Session::frame_ms() {
+    float ms = 0.0f;
+    if (pass_index == 0) return 0.0f;
+    WC_CUDA(cudaEventElapsedTime(&ms, ev_frame0, ev_end));
+    return ms;
 }
 
 void Session::download_framebuffer(uint8_t *rgba_host, float *depth_host) {

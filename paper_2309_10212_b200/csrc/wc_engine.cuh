@@ -74,7 +74,14 @@ struct Session {
     DevBuf<uint32_t> counters, partials;
     PinnedBuf<uint32_t> h_counters;
     RadixScratch rs;
-    cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_frame0 = nullptr;
+    static constexpr int kStages = 6;  // traverse, mark, cache, group, raytrace, composite
+    cudaEvent_t ev_stage[kStages + 1] = {};
+    double stage_ms[kStages] = {};
+    DevBuf<uint32_t> pix;
+    DevBuf<double> dir_in;
+    CameraParams cam_params{};
+    int64_t init_cap = 0;
 
     int64_t n_act = 0, pass_index = 0;
     int64_t last_slots_used = 0, last_nvis = 0, last_nactb = 0, last_nent = 0;
@@ -85,6 +92,8 @@ struct Session {
             const double *dirs, double iso, int speculation, int max_spec, int64_t cache_capacity, int corrupt);
     ~Session();
     bool pass(PassStatsC &st);
+    void reset(const CameraParams *cam, double iso);
+    float frame_ms();  // device time from the last reset to the end of the last pass
     void download_framebuffer(uint8_t *rgba_host, float *depth_host);
     void copy_framebuffer_device(void *rgba_dst, void *depth_dst);
 

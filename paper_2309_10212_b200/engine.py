@@ -22,6 +22,7 @@ from .grids import MacrocellGrids
 from .traversal import Camera
 
 BACKGROUND_RGBA = (0, 0, 0, 255)
+STAGES = ("traverse", "mark", "cache_decode", "group", "raytrace", "composite")
 MAX_SPEC_DEFAULT = 64
 AMBIENT = 0.2
 BASE_COLOR = (0.85, 0.85, 0.85)
@@ -167,6 +168,23 @@ class RenderSession:
         _lib.call("wc_session_run", self._h, buf, max_passes, C.byref(k))
         return [_stats_from_c(buf[i]) for i in range(min(k.value, max_passes))]
 
+    def reset(self, cam: Camera | None, iso: float) -> None:
+        """New frame on the same allocations (fresh rays, framebuffer, cache)."""
+        cam_c = cam.to_c(self.w, self.h) if cam is not None else None
+        _lib.call("wc_session_reset", self._h, None if cam_c is None else C.byref(cam_c), float(iso))
+
+    def frame_ms(self) -> float:
+        """Device ms from the last create/reset to the end of the last pass."""
+        v = C.c_double()
+        _lib.call("wc_session_frame_ms", self._h, C.byref(v))
+        return float(v.value)
+
+    def stage_ms(self) -> dict:
+        """Accumulated device ms per stage since the last reset."""
+        a = (C.c_double * 6)()
+        _lib.call("wc_session_stage_ms", self._h, a)
+        return dict(zip(STAGES, [float(x) for x in a]))
+
     def last_pass_ms(self) -> float:
         v = C.c_double()
         _lib.call("wc_session_last_pass_ms", self._h, C.byref(v))
@@ -198,13 +216,46 @@ def render_passes(cv: CompressedVolume, grids: MacrocellGrids, cam: Camera, iso:
             yield s.framebuffer(ps.completeness), ps
 
 
+class _SessionPool:
+    """Keeps the last render session per (volume, image, options) so that
+    repeated ``render`` calls -- a viewer orbiting its camera -- reuse the
+    device allocations (wc_session_reset) instead of re-allocating HBM."""
+
+    def __init__(self, size: int = 2):
+        self.size = size
+        self.items: list[tuple[tuple, RenderSession]] = []
+
+    def get(self, cv, grids, cam, iso, opts) -> RenderSession:
+        key = (id(cv), int(opts.width), int(opts.height), bool(opts.speculation), int(opts.max_spec),
+               tuple(opts.base_color), bool(opts.corrupt_cache), opts.cache_capacity)
+        for i, (k, s) in enumerate(self.items):
+            if k == key and s.cv is cv:
+                if grids is not None:
+                    grids.bind(cv)
+                s.reset(cam, iso)
+                self.items.append(self.items.pop(i))
+                return s
+        s = RenderSession(cv, grids, cam, iso, opts)
+        self.items.append((key, s))
+        while len(self.items) > self.size:
+            self.items.pop(0)[1].close()
+        return s
+
+    def clear(self):
+        while self.items:
+            self.items.pop()[1].close()
+
+
+session_pool = _SessionPool()
+
+
 def render(cv: CompressedVolume, grids: MacrocellGrids, cam: Camera, iso: float,
            opts: RenderOptions) -> tuple[Framebuffer, list[PassStats]]:
     """engine.py:385-401: render to completion; only the final frame is read back."""
-    with RenderSession(cv, grids, cam, iso, opts) as s:
-        stats = s.run()
-        if not stats:  # camera missed the volume on every pixel
-            fb = Framebuffer.blank(opts.width, opts.height)
-            fb.completeness = 1.0
-            return fb, stats
-        return s.framebuffer(stats[-1].completeness), stats
+    s = session_pool.get(cv, grids, cam, iso, opts)
+    stats = s.run()
+    if not stats:  # camera missed the volume on every pixel
+        fb = Framebuffer.blank(opts.width, opts.height)
+        fb.completeness = 1.0
+        return fb, stats
+    return s.framebuffer(stats[-1].completeness), stats

@@ -229,3 +229,22 @@ def test_prims_scan_sort(wc):
         k2, v2 = wc.prims.sort_by_key(keys, vals)
         order = np.argsort(keys, kind="stable")
         assert np.array_equal(k2, keys[order]) and np.array_equal(v2, vals[order])
+
+
+def test_session_reset_reuses_allocations(wc):
+    """render() pools sessions: a reset with a new camera / iso must equal a
+    fresh oracle render (cache, rays and framebuffer all reset)."""
+    vol = host_volume("value_noise", 48)
+    cv = wc.compress_volume(vol, 12)
+    ov = oracle_volume(cv)
+    grids = wc.build_grids(cv)
+    opts = wc.RenderOptions(width=72, height=56, cache_capacity=64)
+    for i, (frac, isof) in enumerate([(0.1, 0.4), (0.6, 0.55), (0.1, 0.4), (0.35, 0.3)]):
+        cam_t = orbit(cv.dims, frac)
+        fb, stats = wc.render(cv, grids, wc.Camera(*cam_t), iso_at(vol, isof), opts)
+        o, d = orc.camera_rays(cam_t, 72, 56)
+        rgba, depth, ost = orc.render(ov, o, d, 72, 56, iso_at(vol, isof), cache_capacity=64)
+        assert np.array_equal(fb.rgba.reshape(-1, 4), rgba), i
+        assert np.array_equal(fb.depth.reshape(-1), depth), i
+        assert [s.new_decompressed for s in stats] == [s["new_decompressed"] for s in ost], i
+        assert [s.cache_slots for s in stats] == [s["cache_slots"] for s in ost], i
