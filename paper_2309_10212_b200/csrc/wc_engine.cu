@@ -473,18 +473,27 @@ __global__ void __launch_bounds__(256) k_decode_insert(const uint8_t *__restrict
 
 // -------------------------------------------------------------- raytrace
 
-struct DualField {  // 5x5x5 dual grid in shared memory, [z][y][x]
-    const float *p;
+// The dual grid of a visible block (blocktrace.py:49-94) read straight from
+// the cache slots: corner (x, y, z) of the block's local 5^3 lattice lives in
+// the slot of octant ((x>>2), (y>>2), (z>>2)) at offset (x&3)+4(y&3)+16(z&3).
+// The 8 contributor slots (engine.py:286-305) come from k_contrib.
+struct SlotField {
+    const float *sv;
+    int s0, s1, s2, s3, s4, s5, s6, s7;
+    __device__ __forceinline__ int pick(int o) const {
+        const int a0 = (o & 1) ? s1 : s0, a1 = (o & 1) ? s3 : s2, a2 = (o & 1) ? s5 : s4, a3 = (o & 1) ? s7 : s6;
+        const int b0 = (o & 2) ? a1 : a0, b1 = (o & 2) ? a3 : a2;
+        return (o & 4) ? b1 : b0;
+    }
     __device__ __forceinline__ void corners(int lx, int ly, int lz, float c[8]) const {
-        const float *q = p + lx + 5 * ly + 25 * lz;
-        c[0] = q[0];
-        c[1] = q[1];
-        c[2] = q[5];
-        c[3] = q[6];
-        c[4] = q[25];
-        c[5] = q[26];
-        c[6] = q[30];
-        c[7] = q[31];
+        const int ex = lx == 3, ey = ly == 3, ez = lz == 3;
+#pragma unroll
+        for (int idx = 0; idx < 8; idx++) {
+            const int dx = idx & 1, dy = (idx >> 1) & 1, dz = idx >> 2;
+            const int sl = pick((dx & ex) | ((dy & ey) << 1) | ((dz & ez) << 2));
+            const int off = ((lx + dx) & 3) + 4 * ((ly + dy) & 3) + 16 * ((lz + dz) & 3);
+            c[idx] = sl >= 0 ? __ldg(sv + (int64_t)sl * 64 + off) : 0.0f;
+        }
     }
 };
 
@@ -504,65 +513,63 @@ struct DenseFieldView {  // fully decoded volume, x-fastest
     }
 };
 
+// engine.py:286-305 _contributor_table: cache slots of each visible block
+// and its 7 +octant neighbours (-1 outside the volume), 32 B per block.
+__global__ void k_contrib(const uint32_t *visible_ids, int64_t nvis, const int32_t *slot_of_block, int bdx, int bdy,
+                          int bdz, int4 *contrib, uint32_t *err) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvis; v += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = visible_ids[v];
+        const int bx = (int)(b % (uint32_t)bdx), by = (int)((b / (uint32_t)bdx) % (uint32_t)bdy),
+                  bz = (int)(b / ((uint32_t)bdx * (uint32_t)bdy));
+        int s[8];
+#pragma unroll
+        for (int o = 0; o < 8; o++) {
+            const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+            s[o] = (bx + ox < bdx && by + oy < bdy && bz + oz < bdz)
+                       ? slot_of_block[(bx + ox) + bdx * ((by + oy) + bdy * (bz + oz))]
+                       : -1;
+        }
+        if (s[0] < 0) atomicAdd(err, 1u);  // "visible block not resident" (engine.py:302)
+        contrib[2 * v] = make_int4(s[0], s[1], s[2], s[3]);
+        contrib[2 * v + 1] = make_int4(s[4], s[5], s[6], s[7]);
+    }
+}
+
 struct RaytraceArgs {
-    const uint32_t *visible_ids, *block_ray_off, *ent_val, *ent_ray;
-    int64_t nvis;
-    const int32_t *slot_of_block;
+    const uint32_t *visible_ids, *ent_key, *ent_val, *ent_ray;
+    int64_t n_ent;
+    const int4 *contrib;
     const float *slot_values;
     int bdx, bdy, bdz, nx, ny, nz;
     RayView rays;
     double iso, br, bg, bb;
     float4 *rgbz;
-    uint32_t *err;
 };
 
-// engine.py:161-219 _raytrace_visible_kernel: one warp per visible block.
-// The block's 5^3 dual grid (blocktrace.py:49-94, contributor slots from
-// engine.py:286-305) is assembled once in shared memory; the warp's lanes
-// then trace the block's ray entries (blocktrace.py:317-449).
-__global__ void __launch_bounds__(256) k_raytrace(RaytraceArgs a) {
-    __shared__ float dual[8][128];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    float *dg = dual[wib];
-    for (int64_t v = warp0; v < a.nvis; v += nwarps) {
+// engine.py:161-219 _raytrace_visible_kernel, one thread per ray-block entry
+// of the grouped (sorted-by-block) list, so neighbouring lanes trace the
+// same block and share its slot lines in L1.  Each entry runs the region
+// tracer (blocktrace.py:317-449) over the block's <= 4^3 dual cells and
+// writes (rgb, z) -- or (0, 0, 0, +inf) on a miss -- at its entry id.
+__global__ void __launch_bounds__(128) k_raytrace(RaytraceArgs a) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n_ent; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = a.ent_key[j], k = a.ent_val[j];
+        const int64_t r = a.ent_ray[k];
         const uint32_t b = a.visible_ids[v];
         const int bx = (int)(b % (uint32_t)a.bdx), by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy),
                   bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
-        int my_slot = -1;
-        if (lane < 8) {
-            const int ox = lane & 1, oy = (lane >> 1) & 1, oz = lane >> 2;
-            if (bx + ox < a.bdx && by + oy < a.bdy && bz + oz < a.bdz)
-                my_slot = a.slot_of_block[(bx + ox) + a.bdx * ((by + oy) + a.bdy * (bz + oz))];
-        }
-        int slots[8];
-#pragma unroll
-        for (int o = 0; o < 8; o++) slots[o] = __shfl_sync(0xffffffffu, my_slot, o);
-        if (slots[0] < 0 && lane == 0) atomicAdd(a.err, 1u);  // "visible block not resident"
-        for (int idx = lane; idx < 125; idx += 32) {
-            const int i = idx % 5, j = (idx / 5) % 5, k = idx / 25;
-            const int sl = slots[(i == 4) + 2 * (j == 4) + 4 * (k == 4)];
-            dg[idx] = sl >= 0 ? a.slot_values[(int64_t)sl * 64 + (i & 3) + 4 * (j & 3) + 16 * (k & 3)] : 0.0f;
-        }
-        __syncwarp();
+        const int4 c0 = a.contrib[2 * v], c1 = a.contrib[2 * v + 1];
+        const SlotField field{a.slot_values, c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
         const int cx = max(0, min(4, a.nx - 1 - 4 * bx));
         const int cy = max(0, min(4, a.ny - 1 - 4 * by));
         const int cz = max(0, min(4, a.nz - 1 - 4 * bz));
-        const uint32_t start = a.block_ray_off[v], end = a.block_ray_off[v + 1];
-        const DualField field{dg};
-        for (uint32_t e = start + lane; e < end; e += 32) {
-            const uint32_t k = a.ent_val[e];
-            const int64_t r = a.ent_ray[k];
-            double o[3], d[3];
-            a.rays.load(r, o, d);
-            float rgb[3];
-            const double t = trace_region(field, 4 * bx, 4 * by, 4 * bz, 4 * bx, 4 * by, 4 * bz, cx, cy, cz, o, d,
-                                          a.rays.t_enter[r], a.iso, a.br, a.bg, a.bb, rgb);
-            a.rgbz[k] = t != CUDART_INF ? make_float4(rgb[0], rgb[1], rgb[2], (float)t)
-                                        : make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
-        }
-        __syncwarp();
+        double o[3], d[3];
+        a.rays.load(r, o, d);
+        float rgb[3];
+        const double t = trace_region(field, 4 * bx, 4 * by, 4 * bz, 4 * bx, 4 * by, 4 * bz, cx, cy, cz, o, d,
+                                      a.rays.t_enter[r], a.iso, a.br, a.bg, a.bb, rgb);
+        a.rgbz[k] = t != CUDART_INF ? make_float4(rgb[0], rgb[1], rgb[2], (float)t)
+                                    : make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
     }
 }
 
@@ -941,13 +948,17 @@ bool Session::pass(PassStatsC &stats) {
         k_run_offsets<<<grid_for(n_ent, 256), 256, 0, st>>>(ent_key.p, n_ent, nvis, block_ray_off.p);
         WC_LAUNCH_CHECK();
         WC_CUDA(cudaEventRecord(ev_stage[4], st));
+        contrib.ensure(2 * nvis);
+        k_contrib<<<grid_for(nvis, 256), 256, 0, st>>>(visible_ids.p, nvis, slot_of_block.p, vol->bdx, vol->bdy,
+                                                       vol->bdz, contrib.p, counters.p + C_ERR);
+        WC_LAUNCH_CHECK();
         RaytraceArgs ra{};
         ra.visible_ids = visible_ids.p;
-        ra.block_ray_off = block_ray_off.p;
+        ra.ent_key = ent_key.p;
         ra.ent_val = ent_val.p;
         ra.ent_ray = ent_ray.p;
-        ra.nvis = nvis;
-        ra.slot_of_block = slot_of_block.p;
+        ra.n_ent = n_ent;
+        ra.contrib = contrib.p;
         ra.slot_values = slot_values.p;
         ra.bdx = vol->bdx;
         ra.bdy = vol->bdy;
@@ -961,8 +972,7 @@ bool Session::pass(PassStatsC &stats) {
         ra.bg = base[1];
         ra.bb = base[2];
         ra.rgbz = rgbz.p;
-        ra.err = counters.p + C_ERR;
-        k_raytrace<<<grid_for(nvis * 32, 256, 8), 256, 0, st>>>(ra);
+        k_raytrace<<<grid_for(n_ent, 128, 16), 128, 0, st>>>(ra);
         WC_LAUNCH_CHECK();
     } else {
         WC_CUDA(cudaEventRecord(ev_stage[4], st));

@@ -60,6 +60,7 @@ struct Session {
     DevBuf<uint32_t> block_slots, ray_slots;
     DevBuf<uint32_t> ent_key, ent_val, ent_ray;
     DevBuf<float4> rgbz;
+    DevBuf<int4> contrib;  // 8 contributor slots per visible block
     DevBuf<uint32_t> vis_bm, act_bm, vis_word_off, act_word_off;
     DevBuf<uint32_t> visible_ids, block_ray_off, active_ids;
     DevBuf<uint32_t> rgba;
