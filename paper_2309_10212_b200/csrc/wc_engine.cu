@@ -236,7 +236,7 @@ __device__ __forceinline__ void mark_visible(uint32_t *bm, uint32_t b) {
 }
 
 // traversal.py:217-403 _traverse_kernel, one thread per active ray.
-__global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
+__global__ void __launch_bounds__(128, 6) k_traverse(TraverseArgs a) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n_act; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = a.act_list[i];
         double o[3], d[3];
@@ -271,39 +271,43 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
         int emitted = 0;
         bool ray_done = false;
         double t_cross;
+        // Flattened form of the reference's nested fine/coarse loops: one DDA
+        // step per iteration at whichever level the ray is on.  The step
+        // sequence is identical (a fine run ends by leaving its coarse cell,
+        // which hands the next iteration to the coarse grid), but divergent
+        // lanes of a warp now interleave fine and coarse steps instead of
+        // serialising whole runs.
         for (;;) {
             if (in_fine_run) {
-                for (;;) {
-                    const int f_lin = fcx + fdx * (fcy + fdy * fcz);
-                    const double2 mm = a.fine_mm[f_lin];
-                    if (mm.x <= iso && iso <= mm.y) {
-                        a.block_slots[base + emitted] = (uint32_t)f_lin;
-                        a.ray_slots[base + emitted] = (uint32_t)r;
-                        emitted++;
-                        mark_visible(a.vis_bm, (uint32_t)f_lin);
-                    }
-                    if (ftx <= fty && ftx <= ftz) {
-                        t_cross = ftx;
-                        fcx += sx;
-                        ftx += fdel_x;
-                    } else if (fty <= ftz) {
-                        t_cross = fty;
-                        fcy += sy;
-                        fty += fdel_y;
-                    } else {
-                        t_cross = ftz;
-                        fcz += sz;
-                        ftz += fdel_z;
-                    }
-                    if (t_cross > te || fcx < 0 || fcx >= fdx || fcy < 0 || fcy >= fdy || fcz < 0 || fcz >= fdz) {
-                        in_fine_run = false;
-                        ray_done = true;
-                    } else if ((fcx >> 2) != ccx || (fcy >> 2) != ccy || (fcz >> 2) != ccz) {
-                        in_fine_run = false;
-                    }
-                    if (emitted == a.n_spec || !in_fine_run) break;
+                const int f_lin = fcx + fdx * (fcy + fdy * fcz);
+                const double2 mm = a.fine_mm[f_lin];
+                if (mm.x <= iso && iso <= mm.y) {
+                    a.block_slots[base + emitted] = (uint32_t)f_lin;
+                    a.ray_slots[base + emitted] = (uint32_t)r;
+                    emitted++;
+                    mark_visible(a.vis_bm, (uint32_t)f_lin);
+                }
+                if (ftx <= fty && ftx <= ftz) {
+                    t_cross = ftx;
+                    fcx += sx;
+                    ftx += fdel_x;
+                } else if (fty <= ftz) {
+                    t_cross = fty;
+                    fcy += sy;
+                    fty += fdel_y;
+                } else {
+                    t_cross = ftz;
+                    fcz += sz;
+                    ftz += fdel_z;
+                }
+                if (t_cross > te || fcx < 0 || fcx >= fdx || fcy < 0 || fcy >= fdy || fcz < 0 || fcz >= fdz) {
+                    in_fine_run = false;
+                    ray_done = true;
+                } else if ((fcx >> 2) != ccx || (fcy >> 2) != ccy || (fcz >> 2) != ccz) {
+                    in_fine_run = false;
                 }
                 if (emitted == a.n_spec || ray_done) break;
+                continue;
             }
             if (ctx <= cty && ctx <= ctz) {
                 t_cross = ctx;
@@ -430,43 +434,60 @@ __global__ void k_gather_last_used(const uint32_t *val, int64_t n, const int32_t
         key[i] = (uint32_t)last_used[val[i]];
 }
 
-// cache.py:90-96: unmap the first n_evict candidates, append to the free list
-__global__ void k_evict(const uint32_t *victims, int64_t n_evict, int64_t n_free, int32_t *block_of_slot,
-                        int32_t *slot_of_block, uint32_t *free_slots) {
+// cache.py:90-95: unmap the first n_evict candidates (they become the
+// slots of the last n_evict misses, cache.py:96-97)
+__global__ void k_evict(const uint32_t *victims, int64_t n_evict, int32_t *block_of_slot, int32_t *slot_of_block) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_evict; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t s = victims[i];
         slot_of_block[block_of_slot[s]] = -1;
         block_of_slot[s] = -1;
-        free_slots[n_free + i] = s;
     }
 }
 
-// cache.py:97-103 fused with codec.py:143-174: decode each miss straight
-// into its slot and publish the mapping.  Warp per block.
-__global__ void __launch_bounds__(256) k_decode_insert(const uint8_t *__restrict__ payload, int qbits, int stride,
-                                                       const uint32_t *__restrict__ miss_ids,
-                                                       const uint32_t *__restrict__ free_slots, int64_t n_miss,
-                                                       float *__restrict__ slot_values, int32_t *block_of_slot,
-                                                       int32_t *last_used, int32_t *slot_of_block, int32_t pass_no) {
+// cache.py:97-103 fused with codec.py:143-174: miss j goes to slot hw + j
+// while free slots last, then to victim j - n_free; its record is decoded
+// straight into the slot and the mapping published.  Warp per block; the
+// miss count is read on the device (no host round trip).
+__global__ void __launch_bounds__(256)
+    k_decode_insert(const uint8_t *__restrict__ payload, int qbits, int stride, const uint32_t *__restrict__ miss_ids,
+                    const uint32_t *d_n_miss, int64_t hw, int64_t n_free, const uint32_t *__restrict__ victims,
+                    float *__restrict__ slot_values, int32_t *block_of_slot, int32_t *last_used,
+                    int32_t *slot_of_block, int32_t pass_no, uint32_t *d_hw, int64_t cap) {
     const int lane = threadIdx.x & 31;
+    const int64_t n_miss = *d_n_miss;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *d_hw = (uint32_t)(n_miss <= n_free ? hw + n_miss : cap);
     const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t j = warp0; j < n_miss; j += nwarps) {
-        const uint32_t b = miss_ids[j], s = free_slots[j];
-        const uint32_t *rec = reinterpret_cast<const uint32_t *>(payload + (int64_t)b * stride);
-        const BlockDecodeParams p = decode_params(rec, qbits);
-        float v0 = 0.0f, v1 = 0.0f;
-        if (!p.zero) {
-            v0 = decode_value(rec, lane, qbits, p.e, p.fast, p.pow2f, p.sf, p.sd, p.scale_d);
-            v1 = decode_value(rec, lane + 32, qbits, p.e, p.fast, p.pow2f, p.sf, p.sd, p.scale_d);
+    // kInFlight records per warp are loaded before any is decoded: random
+    // 132 B records need many requests in flight to approach HBM bandwidth.
+    constexpr int kInFlight = 4;
+    const int n_words = stride >> 2;
+    for (int64_t j0 = warp0 * kInFlight; j0 < n_miss; j0 += nwarps * kInFlight) {
+        uint32_t b[kInFlight], wa[kInFlight], wb[kInFlight];
+#pragma unroll
+        for (int u = 0; u < kInFlight; u++) {
+            const int64_t j = j0 + u;
+            b[u] = j < n_miss ? miss_ids[j] : 0u;
+            wa[u] = wb[u] = 0u;
+            if (j < n_miss)
+                load_record_warp(reinterpret_cast<const uint32_t *>(payload + (int64_t)b[u] * stride), n_words, lane,
+                                 wa[u], wb[u]);
         }
-        float *dst = slot_values + (int64_t)s * 64;
-        dst[lane] = v0;
-        dst[lane + 32] = v1;
-        if (lane == 0) {
-            block_of_slot[s] = (int32_t)b;
-            last_used[s] = pass_no;
-            slot_of_block[b] = (int32_t)s;
+#pragma unroll
+        for (int u = 0; u < kInFlight; u++) {
+            const int64_t j = j0 + u;
+            if (j >= n_miss) break;  // warp-uniform
+            const uint32_t s = j < n_free ? (uint32_t)(hw + j) : victims[j - n_free];
+            float v0, v1;
+            decode_loaded_warp(wa[u], wb[u], qbits, lane, v0, v1);
+            float *dst = slot_values + (int64_t)s * 64;
+            dst[lane] = v0;
+            dst[lane + 32] = v1;
+            if (lane == 0) {
+                block_of_slot[s] = (int32_t)b[u];
+                last_used[s] = pass_no;
+                slot_of_block[b[u]] = (int32_t)s;
+            }
         }
     }
 }
@@ -782,6 +803,7 @@ void Session::reset(const CameraParams *cam, double iso_) {
     WC_CUDA(cudaMemsetAsync(block_of_slot.p, 0xFF, 4 * phys, st));
     WC_CUDA(cudaMemsetAsync(last_used.p, 0, 4 * phys, st));
     pass_no = 0;
+    hw = 0;
     pass_index = 0;
     for (double &m : stage_ms) m = 0.0;
     read_counters(C_NACT, 1);
@@ -821,54 +843,55 @@ void Session::ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict)
             phys = new_phys;
         }
     }
-    if (free_off.n < phys) {
-        free_off.alloc(phys);
-        free_slots.alloc(phys);
+    if (cand_off.n < phys) {
         cand_off.alloc(phys);
         cand_key.alloc(phys);
         cand_val.alloc(phys);
         partials.ensure(scan_tiles(std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n, phys})) + 8);
     }
-    n_miss = 0;
+    n_miss = -1;  // unknown until the end-of-pass read unless fetched below
     n_evict = 0;
-    if (n_actb == 0) return;
+    if (n_actb == 0) {
+        n_miss = 0;
+        return;
+    }
     k_cache_stamp<<<grid_for(n_actb, 256), 256, 0, st>>>(active_ids.p, n_actb, slot_of_block.p, last_used.p, pass_no);
     WC_LAUNCH_CHECK();
     PredMiss pm{active_ids.p, slot_of_block.p};
     scan_exclusive(pm, n_actb, miss_off.p, counters.p + C_NMISS, partials.p, st);
     k_compact_miss<<<grid_for(n_actb, 256), 256, 0, st>>>(pm, n_actb, miss_off.p, miss_ids.p);
     WC_LAUNCH_CHECK();
-    PredFree pf{block_of_slot.p};
-    scan_exclusive(pf, phys, free_off.p, counters.p + C_NFREE, partials.p, st);
-    k_compact_index<<<grid_for(phys, 256), 256, 0, st>>>(pf, phys, free_off.p, free_slots.p);
-    WC_LAUNCH_CHECK();
-    read_counters(C_NMISS, 2);
-    n_miss = h_counters.p[0];
-    const int64_t n_free_phys = h_counters.p[1];
-    const int64_t n_free = n_free_phys + (cap - phys);  // slots >= n_blocks are never occupied
-    if (n_miss == 0) return;
-    if (n_miss > n_free) {
-        n_evict = n_miss - n_free;
-        const int64_t n_hits = n_actb - n_miss;
-        const int64_t n_cand = (phys - n_free_phys) - n_hits;
-        if (n_cand < n_evict) throw InvariantError("cache: fewer eviction candidates than needed");
-        PredCand pc{block_of_slot.p, last_used.p, pass_no};
-        scan_exclusive(pc, phys, cand_off.p, counters.p + C_NCAND, partials.p, st);
-        k_compact_cand<<<grid_for(phys, 256), 256, 0, st>>>(pc, phys, cand_off.p, cand_key.p, cand_val.p);
-        WC_LAUNCH_CHECK();
-        // (last_used, block_id) order: stable LSD by block id, then by pass stamp
-        radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)(vol->n_blocks - 1)), rs, st);
-        k_gather_last_used<<<grid_for(n_cand, 256), 256, 0, st>>>(cand_val.p, n_cand, last_used.p, cand_key.p);
-        WC_LAUNCH_CHECK();
-        radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)pass_no), rs, st);
-        k_evict<<<grid_for(n_evict, 256), 256, 0, st>>>(cand_val.p, n_evict, n_free_phys, block_of_slot.p,
-                                                        slot_of_block.p, free_slots.p);
-        WC_LAUNCH_CHECK();
+    // Free slots are always the suffix [hw, cap): misses take the lowest free
+    // slots (cache.py:79, :97) and an eviction pass consumes every free slot
+    // plus exactly its victims (cache.py:80-96), so no hole ever opens.
+    const int64_t n_free = cap - hw;
+    const uint32_t *victims = nullptr;
+    if (hw + n_actb > cap) {  // evictions possible: need the miss count now
+        read_counters(C_NMISS, 1);
+        n_miss = h_counters.p[0];
+        if (n_miss > n_free) {
+            n_evict = n_miss - n_free;
+            const int64_t n_hits = n_actb - n_miss;
+            const int64_t n_cand = hw - n_hits;  // resident and not stamped this pass
+            if (n_cand < n_evict) throw InvariantError("cache: fewer eviction candidates than needed");
+            PredCand pc{block_of_slot.p, last_used.p, pass_no};
+            scan_exclusive(pc, hw, cand_off.p, counters.p + C_NCAND, partials.p, st);
+            k_compact_cand<<<grid_for(hw, 256), 256, 0, st>>>(pc, hw, cand_off.p, cand_key.p, cand_val.p);
+            WC_LAUNCH_CHECK();
+            // (last_used, block_id) order: stable LSD by block id, then by pass stamp
+            radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)(vol->n_blocks - 1)), rs, st);
+            k_gather_last_used<<<grid_for(n_cand, 256), 256, 0, st>>>(cand_val.p, n_cand, last_used.p, cand_key.p);
+            WC_LAUNCH_CHECK();
+            radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)pass_no), rs, st);
+            k_evict<<<grid_for(n_evict, 256), 256, 0, st>>>(cand_val.p, n_evict, block_of_slot.p, slot_of_block.p);
+            WC_LAUNCH_CHECK();
+            victims = cand_val.p;
+        }
     }
-    k_decode_insert<<<grid_for(n_miss * 32, 256, 8), 256, 0, st>>>(vol->payload.p, vol->qbits, vol->stride,
-                                                                   miss_ids.p, free_slots.p, n_miss, slot_values.p,
-                                                                   block_of_slot.p, last_used.p, slot_of_block.p,
-                                                                   pass_no);
+    // the miss count stays on the device: the decode grid strides over it
+    k_decode_insert<<<grid_for(n_actb * 32, 256, 8), 256, 0, st>>>(
+        vol->payload.p, vol->qbits, vol->stride, miss_ids.p, counters.p + C_NMISS, hw, n_free, victims,
+        slot_values.p, block_of_slot.p, last_used.p, slot_of_block.p, pass_no, counters.p + C_HW, cap);
     WC_LAUNCH_CHECK();
 }
 
@@ -990,6 +1013,10 @@ bool Session::pass(PassStatsC &stats) {
     read_counters(0, C_COUNT);
     const int64_t n_after = h_counters.p[C_NACT];
     if (h_counters.p[C_ERR]) throw InvariantError("visible block not resident");
+    if (nactb > 0) {
+        n_miss = h_counters.p[C_NMISS];
+        hw = h_counters.p[C_HW];
+    }
     WC_CUDA(cudaEventElapsedTime(&last_kernel_ms, ev_begin, ev_end));
     for (int k = 0; k < kStages; k++) {
         float ms = 0.0f;

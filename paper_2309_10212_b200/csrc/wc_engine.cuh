@@ -28,6 +28,7 @@ enum Counter : int {
     C_NFREE,      // free slots
     C_NCAND,      // eviction candidates
     C_ERR,        // device-side invariant failures
+    C_HW,         // occupied cache slots: free slots are the suffix [hw, cap)
     C_COUNT
 };
 
@@ -66,11 +67,11 @@ struct Session {
     DevBuf<uint32_t> rgba;
     DevBuf<float> depth;
     // cache (cache.py)
-    int64_t cap = 0, phys = 0;
+    int64_t cap = 0, phys = 0, hw = 0;
     int32_t pass_no = 0;
     DevBuf<float> slot_values;
     DevBuf<int32_t> block_of_slot, last_used, slot_of_block;
-    DevBuf<uint32_t> miss_off, miss_ids, free_off, free_slots, cand_off, cand_key, cand_val;
+    DevBuf<uint32_t> miss_off, miss_ids, cand_off, cand_key, cand_val;
     // scratch
     DevBuf<uint32_t> counters, partials;
     PinnedBuf<uint32_t> h_counters;

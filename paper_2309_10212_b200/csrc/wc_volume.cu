@@ -38,12 +38,8 @@ __global__ void __launch_bounds__(256) k_decode_ids(const uint8_t *__restrict__ 
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t j = warp0; j < n; j += nwarps) {
         const uint32_t *rec = reinterpret_cast<const uint32_t *>(payload + ids[j] * (int64_t)stride);
-        const BlockDecodeParams p = decode_params(rec, qbits);
-        float v0 = 0.0f, v1 = 0.0f;
-        if (!p.zero) {
-            v0 = decode_value(rec, lane, qbits, p.e, p.fast, p.pow2f, p.sf, p.sd, p.scale_d);
-            v1 = decode_value(rec, lane + 32, qbits, p.e, p.fast, p.pow2f, p.sf, p.sd, p.scale_d);
-        }
+        float v0, v1;
+        decode_block_warp(rec, stride >> 2, qbits, lane, v0, v1);
         out[j * 64 + lane] = v0;
         out[j * 64 + lane + 32] = v1;
     }
@@ -275,12 +271,13 @@ __global__ void __launch_bounds__(256) k_decode_full(const uint8_t *__restrict__
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t b = warp0; b < n_blocks; b += nwarps) {
         const uint32_t *rec = reinterpret_cast<const uint32_t *>(payload + b * (int64_t)stride);
-        const BlockDecodeParams p = decode_params(rec, qbits);
         const int bx = (int)(b % bdx), by = (int)((b / bdx) % bdy), bz = (int)(b / ((int64_t)bdx * bdy));
+        float vv[2];
+        decode_block_warp(rec, stride >> 2, qbits, lane, vv[0], vv[1]);
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int i = lane + 32 * h;
-            const float v = p.zero ? 0.0f : decode_value(rec, i, qbits, p.e, p.fast, p.pow2f, p.sf, p.sd, p.scale_d);
+            const float v = vv[h];
             const int x = 4 * bx + (i & 3), y = 4 * by + ((i >> 2) & 3), z = 4 * bz + (i >> 4);
             if (x < nx && y < ny && z < nz) dense[x + (int64_t)nx * (y + (int64_t)ny * z)] = v;
         }

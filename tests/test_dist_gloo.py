@@ -1,0 +1,68 @@
+"""Multi-GPU host logic on CPU: 2 gloo ranks each render their interleaved
+tiles (oracle standing in for the per-rank GPU session) and
+dist.gather_tiles stitches the frame on rank 0; it must equal the one-rank
+frame bit for bit (speculation invariance, engine.py:1-9)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as orc
+    from paper_2309_10212_b200 import dist as wdist
+    import paper_2309_10212_b200.volume as V
+
+    vol = V.synthesize("gaussians", (40, 40, 40), seed=0)
+    ov = orc.volume_from_values(vol.values, vol.dims, 16)
+    w, h = 70, 50
+    lo, hi = vol.value_range
+    iso = lo + 0.3 * (hi - lo)
+    cam = orc.orbit_camera(vol.dims, 0, 1)
+    pix = wdist.tile_pixels(w, h, rank, world, 16)
+    o, d = orc.camera_rays(cam, w, h, pix)
+    rgba, depth, _ = orc.render(ov, o, d, len(pix), 1, iso)
+    out = wdist.gather_tiles(torch.from_numpy(rgba), torch.from_numpy(depth), torch.from_numpy(pix.astype(np.int64)),
+                             w, h)
+    if rank == 0:
+        o, d = orc.camera_rays(cam, w, h)
+        full_rgba, full_depth, _ = orc.render(ov, o, d, w, h, iso)
+        ok = np.array_equal(out[0].reshape(-1, 4), full_rgba) and np.array_equal(out[1].reshape(-1), full_depth)
+        q.put((ok, int(np.isfinite(full_depth).sum())))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_tile_gather_stitches_bit_exact(world):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ok, hits = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ok and hits > 0
