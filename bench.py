@@ -61,6 +61,7 @@ def parse():
     p.add_argument("--max-spec", type=int, default=64)
     p.add_argument("--cache-slots", type=int, default=0, help="LRU budget (0 = reference initial_capacity)")
     p.add_argument("--tile", type=int, default=32)
+    p.add_argument("--no-group", action="store_true", help="raytrace entries in ray order (skip the block sort)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-tiles", type=int, default=0, help="tiles in the CPU-baseline sample (0=auto)")
     p.add_argument("--threads", type=int, default=0, help="host threads for the reference arm (0=all)")
@@ -208,7 +209,8 @@ def run_b200(args):
     cache = args.cache_slots if args.cache_slots > 0 else None
     if args.config == "c4" and cache is None:
         cache = 1024
-    opts = wc.RenderOptions(width=w, height=h, max_spec=args.max_spec, cache_capacity=cache)
+    opts = wc.RenderOptions(width=w, height=h, max_spec=args.max_spec, cache_capacity=cache,
+                            group_entries=not args.no_group)
     pix = wdist.tile_pixels(w, h, rank, world, args.tile) if world > 1 else None
     sess = wc.RenderSession(cv, grids, cam, iso, opts, pixel_ids=pix)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -308,6 +310,8 @@ def run_b200(args):
                         "active": s.active_blocks, "decoded": s.new_decompressed, "cache_slots": s.cache_slots,
                         "utilization": round(s.utilization, 4)} for s in stats],
         "stage_ms_per_frame": {k: round(v, 4) for k, v in stage_frame.items()},
+        "stage_ms_per_pass_last_frame": [{k: round(v, 4) for k, v in sess.pass_stage_ms(p).items()}
+                                         for p in range(min(len(stats), 128))],
         "frame_ms_all": [round(x, 3) for x in frame_ms],
         "wall_s_timed_region": round(wall_s, 3),
         "roofline": {"bound": "hbm", "kernel": top, "achieved": round(achieved, 2), "peak": pk["hbm_gbs"],

@@ -101,6 +101,10 @@ int wc_session_create(wc_volume *v, const wc_camera *cam, const uint32_t *pixel_
                       const double *dirs, double iso, int speculation, int max_spec, int64_t cache_capacity,
                       int corrupt_cache, wc_session **out);
 int wc_session_set_base_color(wc_session *s, double r, double g, double b);
+/* build_rt_inputs (engine.py:121-149) grouping on (1, default) or off (0):
+ * the raytrace is correct either way; grouping adds L1 locality and the
+ * reference's PassBuffers layout (required by wc_session_rt_inputs). */
+int wc_session_set_grouping(wc_session *s, int group_entries);
 /* One pass; *ran = 0 once every ray has terminated. */
 int wc_session_pass(wc_session *s, wc_pass_stats *stats, int *ran);
 /* Run passes until done (render, engine.py:385-401); returns pass count. */
@@ -123,6 +127,8 @@ int wc_session_frame_ms(wc_session *s, double *ms);
 /* Accumulated device ms per stage since the last reset:
  * [traverse, mark+extract, cache+decode, group(sort), raytrace, composite] */
 int wc_session_stage_ms(const wc_session *s, double *ms6);
+/* The same split for one pass (pass_index < 128) of the current frame. */
+int wc_session_pass_stage_ms(const wc_session *s, int64_t pass_index, double *ms6);
 
 /* ---- per-stage views of the last pass (parity tests) */
 /* sizes[8] = slots_used, n_visible, n_active_blocks, n_entries, n_spec,

@@ -17,7 +17,8 @@ import numpy as np
 from .errors import DataError, UsageError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libwavecast_b200.so")
+# WAVECAST_LIB selects an alternative in-tree build (tuning variants).
+LIB_PATH = os.environ.get("WAVECAST_LIB") or os.path.join(_PKG, "libwavecast_b200.so")
 _CSRC = os.path.join(_PKG, "csrc")
 
 WC_OK, WC_E_USAGE, WC_E_DATA, WC_E_INVARIANT, WC_E_CUDA = 0, 2, 3, 4, 5
@@ -84,6 +85,7 @@ _SIGS = {
     "wc_decode_bench": (_i32, [_vp, _vp, _i64, _i32, _vp]),
     "wc_session_create": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp, _dbl, _i32, _i32, _i64, _i32, _vp]),
     "wc_session_set_base_color": (_i32, [_vp, _dbl, _dbl, _dbl]),
+    "wc_session_set_grouping": (_i32, [_vp, _i32]),
     "wc_session_pass": (_i32, [_vp, _vp, _vp]),
     "wc_session_run": (_i32, [_vp, _vp, _i64, _vp]),
     "wc_session_n_active": (_i32, [_vp, _vp]),
@@ -95,6 +97,7 @@ _SIGS = {
     "wc_session_reset": (_i32, [_vp, _vp, _dbl]),
     "wc_session_frame_ms": (_i32, [_vp, _vp]),
     "wc_session_stage_ms": (_i32, [_vp, _vp]),
+    "wc_session_pass_stage_ms": (_i32, [_vp, _i64, _vp]),
     "wc_session_rays": (_i32, [_vp] * 10),
     "wc_session_slots": (_i32, [_vp] * 4),
     "wc_session_blocks": (_i32, [_vp] * 3),

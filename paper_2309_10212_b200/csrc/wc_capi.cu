@@ -277,6 +277,12 @@ int wc_session_set_base_color(wc_session *s, double r, double g, double b) {
     WC_API_END
 }
 
+int wc_session_set_grouping(wc_session *s, int group_entries) {
+    WC_API_BEGIN
+    s->s->group_entries = group_entries != 0;
+    WC_API_END
+}
+
 int wc_session_pass(wc_session *s, wc_pass_stats *stats, int *ran) {
     WC_API_BEGIN
     wc::PassStatsC st{};
@@ -344,6 +350,13 @@ int wc_session_frame_ms(wc_session *s, double *ms) {
 int wc_session_stage_ms(const wc_session *s, double *ms6) {
     WC_API_BEGIN
     for (int k = 0; k < wc::Session::kStages; k++) ms6[k] = s->s->stage_ms[k];
+    WC_API_END
+}
+
+int wc_session_pass_stage_ms(const wc_session *s, int64_t pass_index, double *ms6) {
+    WC_API_BEGIN
+    WC_REQUIRE(pass_index >= 0 && pass_index < wc::Session::kMaxPassLog, wc::UsageError, "pass index out of range");
+    for (int k = 0; k < wc::Session::kStages; k++) ms6[k] = s->s->pass_stage_ms[pass_index][k];
     WC_API_END
 }
 

@@ -15,6 +15,19 @@
 #include "wc_engine.cuh"
 #include "wc_trace.cuh"
 
+// Resident CTAs (of 128 threads) per SM requested from ptxas for the two
+// float64-heavy kernels; trades registers for latency hiding (tuned on B200
+// with scripts/gpu_variants.sh).
+#ifndef WC_TRAVERSE_MIN_CTAS
+#define WC_TRAVERSE_MIN_CTAS 6
+#endif
+#ifndef WC_TRAVERSE_LOOKAHEAD
+#define WC_TRAVERSE_LOOKAHEAD 0
+#endif
+#ifndef WC_RAYTRACE_MIN_CTAS
+#define WC_RAYTRACE_MIN_CTAS 4
+#endif
+
 namespace wc {
 
 // --------------------------------------------------------------- ray setup
@@ -219,10 +232,11 @@ struct TraverseArgs {
     const uint32_t *act_list;
     int64_t n_act;
     int n_spec;
-    const double2 *fine_mm, *coarse_mm;
+    const uint32_t *fine_bm, *coarse_bm;  // per-iso range-test bitmaps (k_iso_bitmap)
     int fdx, fdy, fdz, cdx, cdy, cdz;
     double iso;
     uint32_t *block_slots, *ray_slots, *emitted, *vis_bm;
+    uint32_t *work;  // persistent-kernel ray counter (zeroed per pass)
 };
 
 // Mark block b visible: one RED.OR per distinct block among the lanes that
@@ -235,134 +249,282 @@ __device__ __forceinline__ void mark_visible(uint32_t *bm, uint32_t b) {
     if ((peers & ((1u << lane) - 1u)) == 0) atomicOr(&bm[b >> 5], 1u << (b & 31));
 }
 
-// traversal.py:217-403 _traverse_kernel, one thread per active ray.
-__global__ void __launch_bounds__(128, 6) k_traverse(TraverseArgs a) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n_act; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = a.act_list[i];
-        double o[3], d[3];
-        a.rays.load(r, o, d);
-        const double ox = o[0], oy = o[1], oz = o[2], dx = d[0], dy = d[1], dz = d[2];
-        const double te = a.t_exit[r];
-        const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
-        const double iso = a.iso;
-        const int sx = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
-        const int sy = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
-        const int sz = dz > 0.0 ? 1 : (dz < 0.0 ? -1 : 0);
-        const double fdel_x = dx != 0.0 ? 4.0 / fabs(dx) : CUDART_INF;
-        const double fdel_y = dy != 0.0 ? 4.0 / fabs(dy) : CUDART_INF;
-        const double fdel_z = dz != 0.0 ? 4.0 / fabs(dz) : CUDART_INF;
-        const double cdel_x = dx != 0.0 ? 16.0 / fabs(dx) : CUDART_INF;
-        const double cdel_y = dy != 0.0 ? 16.0 / fabs(dy) : CUDART_INF;
-        const double cdel_z = dz != 0.0 ? 16.0 / fabs(dz) : CUDART_INF;
-        const uint32_t cc = a.coarse_cell[r];
-        int ccx = (int)(cc % (uint32_t)cdx), ccy = (int)((cc / (uint32_t)cdx) % (uint32_t)cdy),
-            ccz = (int)(cc / ((uint32_t)cdx * (uint32_t)cdy));
-        double ctx = a.coarse_tmax[3 * r], cty = a.coarse_tmax[3 * r + 1], ctz = a.coarse_tmax[3 * r + 2];
-        const uint32_t fc = a.fine_cell[r];
-        bool in_fine_run = fc != WC_UINT_MAX;
-        int fcx = 0, fcy = 0, fcz = 0;
-        if (in_fine_run) {
-            fcx = (int)(fc % (uint32_t)fdx);
-            fcy = (int)((fc / (uint32_t)fdx) % (uint32_t)fdy);
-            fcz = (int)(fc / ((uint32_t)fdx * (uint32_t)fdy));
+// Amanatides-Woo state of one ray on one grid level.
+struct Dda {
+    int cx, cy, cz;
+    double tx, ty, tz;
+};
+
+// One step; ties step x, then y, then z (traversal.py:303-314, :333-344).
+// Returns the crossing parameter of the face just crossed.
+__device__ __forceinline__ double dda_step(Dda &s, int sx, int sy, int sz, double dlx, double dly, double dlz) {
+    double t;
+    if (s.tx <= s.ty && s.tx <= s.tz) {
+        t = s.tx;
+        s.cx += sx;
+        s.tx += dlx;
+    } else if (s.ty <= s.tz) {
+        t = s.ty;
+        s.cy += sy;
+        s.ty += dly;
+    } else {
+        t = s.tz;
+        s.cz += sz;
+        s.tz += dlz;
+    }
+    return t;
+}
+
+constexpr int kFineRun = 10;   // a monotone ray visits at most 4+4+4-2 fine cells of one coarse cell
+constexpr int kCoarseAhead = 8;
+
+// traversal.py:217-403 _traverse_kernel, restructured for latency on B200:
+//  * persistent: a lane that finishes its ray fetches the next active ray
+//    from a warp-aggregated work counter, so divergent per-ray step counts do
+//    not idle the warp;
+//  * look-ahead: the DDA itself never depends on the grid values, so a
+//    whole fine run (until the ray leaves its coarse cell) or kCoarseAhead
+//    coarse steps are first simulated arithmetically, their range bits
+//    fetched with independent loads from the L2-resident per-iso bitmaps, and
+//    only then consumed in the reference's order; the iterator state at the
+//    exact stop point (n_spec-th emit, descent, exit) is recovered by
+//    replaying the arithmetic.  Every emitted slot, saved iterator and exit
+//    flag is the reference's, bit for bit.
+template <bool LOOKAHEAD>
+__global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(TraverseArgs a) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
+    bool have = false, exhausted = false;
+    uint32_t i = 0, r = 0;
+    double ox = 0, oy = 0, oz = 0, dx = 0, dy = 0, dz = 0, te = 0;
+    double fdel_x = 0, fdel_y = 0, fdel_z = 0, cdel_x = 0, cdel_y = 0, cdel_z = 0;
+    int sx = 0, sy = 0, sz = 0, emitted = 0;
+    Dda f{0, 0, 0, 0, 0, 0}, c{0, 0, 0, 0, 0, 0};
+    bool in_fine_run = false;
+    int64_t base = 0;
+    for (;;) {
+        if (!exhausted) {  // refill idle lanes (warp-uniform branch)
+            const uint32_t need = __ballot_sync(0xffffffffu, !have);
+            if (need) {
+                const int leader = __ffs(need) - 1;
+                uint32_t first = 0;
+                if (lane == leader) first = atomicAdd(a.work, (uint32_t)__popc(need));
+                first = __shfl_sync(0xffffffffu, first, leader);
+                if (first + __popc(need) >= a.n_act) exhausted = true;
+                const uint32_t mine = first + __popc(need & lt);
+                if (!have && mine < a.n_act) {
+                    have = true;
+                    i = mine;
+                    r = a.act_list[i];
+                    double o[3], d[3];
+                    a.rays.load(r, o, d);
+                    ox = o[0], oy = o[1], oz = o[2], dx = d[0], dy = d[1], dz = d[2];
+                    te = a.t_exit[r];
+                    sx = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
+                    sy = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
+                    sz = dz > 0.0 ? 1 : (dz < 0.0 ? -1 : 0);
+                    fdel_x = dx != 0.0 ? 4.0 / fabs(dx) : CUDART_INF;
+                    fdel_y = dy != 0.0 ? 4.0 / fabs(dy) : CUDART_INF;
+                    fdel_z = dz != 0.0 ? 4.0 / fabs(dz) : CUDART_INF;
+                    cdel_x = dx != 0.0 ? 16.0 / fabs(dx) : CUDART_INF;
+                    cdel_y = dy != 0.0 ? 16.0 / fabs(dy) : CUDART_INF;
+                    cdel_z = dz != 0.0 ? 16.0 / fabs(dz) : CUDART_INF;
+                    const uint32_t cc = a.coarse_cell[r];
+                    c.cx = (int)(cc % (uint32_t)cdx);
+                    c.cy = (int)((cc / (uint32_t)cdx) % (uint32_t)cdy);
+                    c.cz = (int)(cc / ((uint32_t)cdx * (uint32_t)cdy));
+                    c.tx = a.coarse_tmax[3 * (int64_t)r];
+                    c.ty = a.coarse_tmax[3 * (int64_t)r + 1];
+                    c.tz = a.coarse_tmax[3 * (int64_t)r + 2];
+                    const uint32_t fc = a.fine_cell[r];
+                    in_fine_run = fc != WC_UINT_MAX;
+                    f.cx = f.cy = f.cz = 0;
+                    if (in_fine_run) {
+                        f.cx = (int)(fc % (uint32_t)fdx);
+                        f.cy = (int)((fc / (uint32_t)fdx) % (uint32_t)fdy);
+                        f.cz = (int)(fc / ((uint32_t)fdx * (uint32_t)fdy));
+                    }
+                    f.tx = a.fine_tmax[3 * (int64_t)r];
+                    f.ty = a.fine_tmax[3 * (int64_t)r + 1];
+                    f.tz = a.fine_tmax[3 * (int64_t)r + 2];
+                    base = (int64_t)i * a.n_spec;
+                    emitted = 0;
+                }
+            }
         }
-        double ftx = a.fine_tmax[3 * r], fty = a.fine_tmax[3 * r + 1], ftz = a.fine_tmax[3 * r + 2];
-        const int64_t base = i * (int64_t)a.n_spec;
-        int emitted = 0;
-        bool ray_done = false;
-        double t_cross;
-        // Flattened form of the reference's nested fine/coarse loops: one DDA
-        // step per iteration at whichever level the ray is on.  The step
-        // sequence is identical (a fine run ends by leaving its coarse cell,
-        // which hands the next iteration to the coarse grid), but divergent
-        // lanes of a warp now interleave fine and coarse steps instead of
-        // serialising whole runs.
-        for (;;) {
-            if (in_fine_run) {
-                const int f_lin = fcx + fdx * (fcy + fdy * fcz);
-                const double2 mm = a.fine_mm[f_lin];
-                if (mm.x <= iso && iso <= mm.y) {
-                    a.block_slots[base + emitted] = (uint32_t)f_lin;
-                    a.ray_slots[base + emitted] = (uint32_t)r;
+        if (!__any_sync(0xffffffffu, have)) break;
+        if (!have) continue;
+        bool finished = false, ray_done = false;
+        // traversal.py:357-386: seed the fine iterator where the ray enters
+        // coarse cell c (crossing parameter t_cross)
+        auto descend = [&](double t_cross) {
+            const double px = ox + dx * t_cross, py = oy + dy * t_cross, pz = oz + dz * t_cross;
+            const int lo_x = 4 * c.cx, lo_y = 4 * c.cy, lo_z = 4 * c.cz;
+            const int hi_x = min(lo_x + 3, fdx - 1), hi_y = min(lo_y + 3, fdy - 1), hi_z = min(lo_z + 3, fdz - 1);
+            f.cx = (int)floor(px / 4.0);
+            f.cy = (int)floor(py / 4.0);
+            f.cz = (int)floor(pz / 4.0);
+            f.cx = f.cx < lo_x ? lo_x : (f.cx > hi_x ? hi_x : f.cx);
+            f.cy = f.cy < lo_y ? lo_y : (f.cy > hi_y ? hi_y : f.cy);
+            f.cz = f.cz < lo_z ? lo_z : (f.cz > hi_z ? hi_z : f.cz);
+            f.tx = dx > 0.0 ? ((double)(f.cx + 1) * 4.0 - ox) / dx
+                            : (dx < 0.0 ? ((double)f.cx * 4.0 - ox) / dx : CUDART_INF);
+            f.ty = dy > 0.0 ? ((double)(f.cy + 1) * 4.0 - oy) / dy
+                            : (dy < 0.0 ? ((double)f.cy * 4.0 - oy) / dy : CUDART_INF);
+            f.tz = dz > 0.0 ? ((double)(f.cz + 1) * 4.0 - oz) / dz
+                            : (dz < 0.0 ? ((double)f.cz * 4.0 - oz) / dz : CUDART_INF);
+            in_fine_run = true;
+        };
+        if (!LOOKAHEAD && in_fine_run) {  // one fine step (traversal.py:295-331)
+            const uint32_t f_lin = (uint32_t)(f.cx + fdx * (f.cy + fdy * f.cz));
+            if ((__ldg(a.fine_bm + (f_lin >> 5)) >> (f_lin & 31)) & 1u) {
+                a.block_slots[base + emitted] = f_lin;
+                a.ray_slots[base + emitted] = r;
+                emitted++;
+                mark_visible(a.vis_bm, f_lin);
+            }
+            const double t = dda_step(f, sx, sy, sz, fdel_x, fdel_y, fdel_z);
+            if (t > te || f.cx < 0 || f.cx >= fdx || f.cy < 0 || f.cy >= fdy || f.cz < 0 || f.cz >= fdz) {
+                in_fine_run = false;
+                ray_done = true;
+            } else if ((f.cx >> 2) != c.cx || (f.cy >> 2) != c.cy || (f.cz >> 2) != c.cz) {
+                in_fine_run = false;
+            }
+            finished = emitted == a.n_spec || ray_done;
+        } else if (!LOOKAHEAD) {  // one coarse step (traversal.py:332-386)
+            const double t = dda_step(c, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+            if (t > te || c.cx < 0 || c.cx >= cdx || c.cy < 0 || c.cy >= cdy || c.cz < 0 || c.cz >= cdz) {
+                ray_done = true;
+                finished = true;
+            } else {
+                const uint32_t c_lin = (uint32_t)(c.cx + cdx * (c.cy + cdy * c.cz));
+                if ((__ldg(a.coarse_bm + (c_lin >> 5)) >> (c_lin & 31)) & 1u) descend(t);
+            }
+        } else if (in_fine_run) {
+            // ---- one fine run: simulate, fetch all range bits, consume
+            Dda g = f;
+            uint32_t cell[kFineRun];
+            int K = 0, term = 0;  // term: 0 run continues, 1 left the coarse cell, 2 left the ray
+#pragma unroll
+            for (int k = 0; k < kFineRun; k++) {
+                if (term == 0) {
+                    cell[k] = (uint32_t)(g.cx + fdx * (g.cy + fdy * g.cz));
+                    K = k + 1;
+                    const double t = dda_step(g, sx, sy, sz, fdel_x, fdel_y, fdel_z);
+                    if (t > te || g.cx < 0 || g.cx >= fdx || g.cy < 0 || g.cy >= fdy || g.cz < 0 || g.cz >= fdz)
+                        term = 2;
+                    else if ((g.cx >> 2) != c.cx || (g.cy >> 2) != c.cy || (g.cz >> 2) != c.cz)
+                        term = 1;
+                }
+            }
+            uint32_t bits = 0;
+#pragma unroll
+            for (int k = 0; k < kFineRun; k++)
+                if (k < K) bits |= ((__ldg(a.fine_bm + (cell[k] >> 5)) >> (cell[k] & 31)) & 1u) << k;
+            int m = -1;  // cell at which the n_spec-th block is emitted
+#pragma unroll
+            for (int k = 0; k < kFineRun; k++) {
+                if (m < 0 && k < K && ((bits >> k) & 1u)) {
+                    a.block_slots[base + emitted] = cell[k];
+                    a.ray_slots[base + emitted] = r;
                     emitted++;
-                    mark_visible(a.vis_bm, (uint32_t)f_lin);
+                    mark_visible(a.vis_bm, cell[k]);
+                    if (emitted == a.n_spec) m = k;
                 }
-                if (ftx <= fty && ftx <= ftz) {
-                    t_cross = ftx;
-                    fcx += sx;
-                    ftx += fdel_x;
-                } else if (fty <= ftz) {
-                    t_cross = fty;
-                    fcy += sy;
-                    fty += fdel_y;
-                } else {
-                    t_cross = ftz;
-                    fcz += sz;
-                    ftz += fdel_z;
-                }
-                if (t_cross > te || fcx < 0 || fcx >= fdx || fcy < 0 || fcy >= fdy || fcz < 0 || fcz >= fdz) {
+            }
+            if (m >= 0 && m < K - 1) {  // stopped inside the run: state after m+1 steps
+                for (int k = 0; k <= m; k++) dda_step(f, sx, sy, sz, fdel_x, fdel_y, fdel_z);
+                finished = true;
+            } else {
+                f = g;
+                if (term == 2) {
                     in_fine_run = false;
                     ray_done = true;
-                } else if ((fcx >> 2) != ccx || (fcy >> 2) != ccy || (fcz >> 2) != ccz) {
-                    in_fine_run = false;
+                    finished = true;
+                } else {
+                    if (term == 1) in_fine_run = false;
+                    finished = emitted == a.n_spec;
                 }
-                if (emitted == a.n_spec || ray_done) break;
-                continue;
             }
-            if (ctx <= cty && ctx <= ctz) {
-                t_cross = ctx;
-                ccx += sx;
-                ctx += cdel_x;
-            } else if (cty <= ctz) {
-                t_cross = cty;
-                ccy += sy;
-                cty += cdel_y;
-            } else {
-                t_cross = ctz;
-                ccz += sz;
-                ctz += cdel_z;
-            }
-            if (t_cross > te || ccx < 0 || ccx >= cdx || ccy < 0 || ccy >= cdy || ccz < 0 || ccz >= cdz) {
-                ray_done = true;
-                break;
-            }
-            const int c_lin = ccx + cdx * (ccy + cdy * ccz);
-            const double2 cm = a.coarse_mm[c_lin];
-            if (cm.x <= iso && iso <= cm.y) {
-                const double px = ox + dx * t_cross, py = oy + dy * t_cross, pz = oz + dz * t_cross;
-                const int lo_x = 4 * ccx, lo_y = 4 * ccy, lo_z = 4 * ccz;
-                const int hi_x = min(lo_x + 3, fdx - 1), hi_y = min(lo_y + 3, fdy - 1), hi_z = min(lo_z + 3, fdz - 1);
-                fcx = (int)floor(px / 4.0);
-                fcy = (int)floor(py / 4.0);
-                fcz = (int)floor(pz / 4.0);
-                fcx = fcx < lo_x ? lo_x : (fcx > hi_x ? hi_x : fcx);
-                fcy = fcy < lo_y ? lo_y : (fcy > hi_y ? hi_y : fcy);
-                fcz = fcz < lo_z ? lo_z : (fcz > hi_z ? hi_z : fcz);
-                ftx = dx > 0.0 ? ((double)(fcx + 1) * 4.0 - ox) / dx : (dx < 0.0 ? ((double)fcx * 4.0 - ox) / dx : CUDART_INF);
-                fty = dy > 0.0 ? ((double)(fcy + 1) * 4.0 - oy) / dy : (dy < 0.0 ? ((double)fcy * 4.0 - oy) / dy : CUDART_INF);
-                ftz = dz > 0.0 ? ((double)(fcz + 1) * 4.0 - oz) / dz : (dz < 0.0 ? ((double)fcz * 4.0 - oz) / dz : CUDART_INF);
-                in_fine_run = true;
-            }
-        }
-        for (int k = emitted; k < a.n_spec; k++) {  // traversal.py:423-424 sentinels
-            a.block_slots[base + k] = WC_UINT_MAX;
-            a.ray_slots[base + k] = WC_UINT_MAX;
-        }
-        a.emitted[i] = (uint32_t)emitted;
-        if (ray_done) {
-            a.exited[r] = 1;
-            a.coarse_cell[r] = WC_UINT_MAX;
-            a.fine_cell[r] = WC_UINT_MAX;
         } else {
-            a.coarse_cell[r] = (uint32_t)(ccx + cdx * (ccy + cdy * ccz));
-            a.fine_cell[r] = in_fine_run ? (uint32_t)(fcx + fdx * (fcy + fdy * fcz)) : WC_UINT_MAX;
+            // ---- coarse steps: simulate kCoarseAhead, fetch their bits, descend at the first hit
+            Dda g = c;
+            uint32_t cell[kCoarseAhead];
+            int J = 0;
+            bool done = false;
+#pragma unroll
+            for (int j = 0; j < kCoarseAhead; j++) {
+                if (!done) {
+                    const double t = dda_step(g, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+                    if (t > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 || g.cz >= cdz) {
+                        done = true;
+                    } else {
+                        cell[j] = (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz));
+                        J = j + 1;
+                    }
+                }
+            }
+            uint32_t bits = 0;
+#pragma unroll
+            for (int j = 0; j < kCoarseAhead; j++)
+                if (j < J) bits |= ((__ldg(a.coarse_bm + (cell[j] >> 5)) >> (cell[j] & 31)) & 1u) << j;
+            if (bits) {  // descend at the first coarse cell holding the iso
+                const int js = __ffs(bits) - 1;
+                double t_cross = 0.0;
+                for (int j = 0; j <= js; j++) t_cross = dda_step(c, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+                descend(t_cross);
+            } else {
+                c = g;  // includes the exiting step when done (traversal.py:333-355)
+                if (done) {
+                    ray_done = true;
+                    finished = true;
+                }
+            }
         }
-        a.coarse_tmax[3 * r] = ctx;
-        a.coarse_tmax[3 * r + 1] = cty;
-        a.coarse_tmax[3 * r + 2] = ctz;
-        a.fine_tmax[3 * r] = ftx;
-        a.fine_tmax[3 * r + 1] = fty;
-        a.fine_tmax[3 * r + 2] = ftz;
+        if (finished) {  // save the iterator past the last emit (traversal.py:388-403)
+            for (int k = emitted; k < a.n_spec; k++) {  // traversal.py:423-424 sentinels
+                a.block_slots[base + k] = WC_UINT_MAX;
+                a.ray_slots[base + k] = WC_UINT_MAX;
+            }
+            a.emitted[i] = (uint32_t)emitted;
+            if (ray_done) {
+                a.exited[r] = 1;
+                a.coarse_cell[r] = WC_UINT_MAX;
+                a.fine_cell[r] = WC_UINT_MAX;
+            } else {
+                a.coarse_cell[r] = (uint32_t)(c.cx + cdx * (c.cy + cdy * c.cz));
+                a.fine_cell[r] = in_fine_run ? (uint32_t)(f.cx + fdx * (f.cy + fdy * f.cz)) : WC_UINT_MAX;
+            }
+            a.coarse_tmax[3 * (int64_t)r] = c.tx;
+            a.coarse_tmax[3 * (int64_t)r + 1] = c.ty;
+            a.coarse_tmax[3 * (int64_t)r + 2] = c.tz;
+            a.fine_tmax[3 * (int64_t)r] = f.tx;
+            a.fine_tmax[3 * (int64_t)r + 1] = f.ty;
+            a.fine_tmax[3 * (int64_t)r + 2] = f.tz;
+            have = false;
+        }
+    }
+}
+
+// The traversal's range tests for one isovalue, precomputed: bit c of the
+// fine (coarse) bitmap is `min[c] <= iso && iso <= max[c]` evaluated in
+// float64 exactly as traversal.py:297 (:357) does.  The 15.7 MB fine bitmap
+// (8.05B voxels) stays in L2, so each DDA step of the traversal's dependent
+// chain costs an L2 hit instead of a DRAM read of the 2 GB float64 grid.
+__global__ void k_iso_bitmap(const double2 *__restrict__ mm, int64_t n, double iso, uint32_t *__restrict__ bm) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwords = (n + 31) >> 5;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t c = w * 32 + lane;
+        bool in = false;
+        if (c < n) {
+            const double2 v = mm[c];
+            in = v.x <= iso && iso <= v.y;
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, in);
+        if (lane == 0) bm[w] = word;
     }
 }
 
@@ -448,7 +610,7 @@ __global__ void k_evict(const uint32_t *victims, int64_t n_evict, int32_t *block
 // while free slots last, then to victim j - n_free; its record is decoded
 // straight into the slot and the mapping published.  Warp per block; the
 // miss count is read on the device (no host round trip).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
     k_decode_insert(const uint8_t *__restrict__ payload, int qbits, int stride, const uint32_t *__restrict__ miss_ids,
                     const uint32_t *d_n_miss, int64_t hw, int64_t n_free, const uint32_t *__restrict__ victims,
                     float *__restrict__ slot_values, int32_t *block_of_slot, int32_t *last_used,
@@ -458,35 +620,40 @@ __global__ void __launch_bounds__(256)
     if (blockIdx.x == 0 && threadIdx.x == 0) *d_hw = (uint32_t)(n_miss <= n_free ? hw + n_miss : cap);
     const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // kInFlight records per warp are loaded before any is decoded: random
-    // 132 B records need many requests in flight to approach HBM bandwidth.
-    constexpr int kInFlight = 4;
+    // A warp takes 32 consecutive misses: one coalesced load of their ids,
+    // then kInFlight records are requested before any is decoded (random
+    // 132 B records need many requests in flight to approach HBM bandwidth).
+    constexpr int kInFlight = 8;
     const int n_words = stride >> 2;
-    for (int64_t j0 = warp0 * kInFlight; j0 < n_miss; j0 += nwarps * kInFlight) {
-        uint32_t b[kInFlight], wa[kInFlight], wb[kInFlight];
-#pragma unroll
-        for (int u = 0; u < kInFlight; u++) {
-            const int64_t j = j0 + u;
-            b[u] = j < n_miss ? miss_ids[j] : 0u;
-            wa[u] = wb[u] = 0u;
-            if (j < n_miss)
-                load_record_warp(reinterpret_cast<const uint32_t *>(payload + (int64_t)b[u] * stride), n_words, lane,
-                                 wa[u], wb[u]);
+    for (int64_t g = warp0 * 32; g < n_miss; g += nwarps * 32) {
+        const int64_t jl = g + lane;
+        const uint32_t my_b = jl < n_miss ? miss_ids[jl] : 0u;
+        const uint32_t my_s = jl < n_miss ? (jl < n_free ? (uint32_t)(hw + jl) : victims[jl - n_free]) : 0u;
+        if (jl < n_miss) {  // lane-parallel bookkeeping for the 32 misses
+            block_of_slot[my_s] = (int32_t)my_b;
+            last_used[my_s] = pass_no;
+            slot_of_block[my_b] = (int32_t)my_s;
         }
+        const int cnt = n_miss - g < 32 ? (int)(n_miss - g) : 32;
+        for (int u0 = 0; u0 < cnt; u0 += kInFlight) {
+            uint32_t wa[kInFlight], wb[kInFlight];
 #pragma unroll
-        for (int u = 0; u < kInFlight; u++) {
-            const int64_t j = j0 + u;
-            if (j >= n_miss) break;  // warp-uniform
-            const uint32_t s = j < n_free ? (uint32_t)(hw + j) : victims[j - n_free];
-            float v0, v1;
-            decode_loaded_warp(wa[u], wb[u], qbits, lane, v0, v1);
-            float *dst = slot_values + (int64_t)s * 64;
-            dst[lane] = v0;
-            dst[lane + 32] = v1;
-            if (lane == 0) {
-                block_of_slot[s] = (int32_t)b[u];
-                last_used[s] = pass_no;
-                slot_of_block[b[u]] = (int32_t)s;
+            for (int u = 0; u < kInFlight; u++) {
+                const uint32_t b = __shfl_sync(0xffffffffu, my_b, (u0 + u) & 31);
+                wa[u] = wb[u] = 0u;
+                if (u0 + u < cnt)
+                    load_record_warp(reinterpret_cast<const uint32_t *>(payload + (int64_t)b * stride), n_words, lane,
+                                     wa[u], wb[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < kInFlight; u++) {
+                const uint32_t s = __shfl_sync(0xffffffffu, my_s, (u0 + u) & 31);
+                if (u0 + u >= cnt) break;  // warp-uniform
+                float v0, v1;
+                decode_loaded_warp(wa[u], wb[u], qbits, lane, v0, v1);
+                float *dst = slot_values + (int64_t)s * 64;
+                dst[lane] = v0;
+                dst[lane + 32] = v1;
             }
         }
     }
@@ -572,7 +739,7 @@ struct RaytraceArgs {
 // same block and share its slot lines in L1.  Each entry runs the region
 // tracer (blocktrace.py:317-449) over the block's <= 4^3 dual cells and
 // writes (rgb, z) -- or (0, 0, 0, +inf) on a miss -- at its entry id.
-__global__ void __launch_bounds__(128) k_raytrace(RaytraceArgs a) {
+__global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_raytrace(RaytraceArgs a) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n_ent; j += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t v = a.ent_key[j], k = a.ent_val[j];
         const int64_t r = a.ent_ray[k];
@@ -730,6 +897,8 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     const int64_t nwords = ceil_div(vol->n_blocks, 32);
     vis_bm.alloc(nwords);
     act_bm.alloc(nwords);
+    fine_bm.alloc(nwords);
+    coarse_bm.alloc(ceil_div(vol->n_coarse, 32));
     vis_word_off.alloc(nwords);
     act_word_off.alloc(nwords);
     WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
@@ -769,6 +938,10 @@ void Session::reset(const CameraParams *cam, double iso_) {
         eye[2] = cam->eye[2];
     }
     WC_CUDA(cudaEventRecord(ev_frame0, st));
+    k_iso_bitmap<<<grid_for(vol->n_blocks, 256, 8), 256, 0, st>>>(vol->fine_mm.p, vol->n_blocks, iso, fine_bm.p);
+    WC_LAUNCH_CHECK();
+    k_iso_bitmap<<<grid_for(vol->n_coarse, 256, 8), 256, 0, st>>>(vol->coarse_mm.p, vol->n_coarse, iso, coarse_bm.p);
+    WC_LAUNCH_CHECK();
     RayInitArgs a{};
     a.cam = cam_params;
     a.pixel_ids = pix.p;
@@ -806,6 +979,8 @@ void Session::reset(const CameraParams *cam, double iso_) {
     hw = 0;
     pass_index = 0;
     for (double &m : stage_ms) m = 0.0;
+    for (auto &p : pass_stage_ms)
+        for (double &m : p) m = 0.0;
     read_counters(C_NACT, 1);
     n_act = h_counters.p[0];
 }
@@ -921,8 +1096,8 @@ bool Session::pass(PassStatsC &stats) {
     ta.act_list = alist;
     ta.n_act = n_act;
     ta.n_spec = (int)n_spec;
-    ta.fine_mm = vol->fine_mm.p;
-    ta.coarse_mm = vol->coarse_mm.p;
+    ta.fine_bm = fine_bm.p;
+    ta.coarse_bm = coarse_bm.p;
     ta.fdx = vol->bdx;
     ta.fdy = vol->bdy;
     ta.fdz = vol->bdz;
@@ -934,7 +1109,12 @@ bool Session::pass(PassStatsC &stats) {
     ta.ray_slots = ray_slots.p;
     ta.emitted = emitted.p;
     ta.vis_bm = vis_bm.p;
-    k_traverse<<<grid_for(n_act, 128, 16), 128, 0, st>>>(ta);
+    ta.work = counters.p + C_WORK;
+    WC_CUDA(cudaMemsetAsync(ta.work, 0, 4, st));
+    if (WC_TRAVERSE_LOOKAHEAD)
+        k_traverse<true><<<grid_for(n_act, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st>>>(ta);
+    else
+        k_traverse<false><<<grid_for(n_act, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st>>>(ta);
     WC_LAUNCH_CHECK();
     WC_CUDA(cudaEventRecord(ev_stage[1], st));
     // entry compaction: exclusive scan of per-ray emitted counts
@@ -965,11 +1145,16 @@ bool Session::pass(PassStatsC &stats) {
     if (corrupt) WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * phys, st));  // engine.py:338-339
     WC_CUDA(cudaEventRecord(ev_stage[3], st));
 
-    // build_rt_inputs: stable grouping of entries by visible block
+    // build_rt_inputs: stable grouping of entries by visible block.  The
+    // thread-per-entry raytrace is correct on either order; grouping buys L1
+    // locality (neighbouring lanes on one block) and the reference's
+    // PassBuffers layout, and can be switched off (group_entries).
     if (n_ent > 0) {
-        radix_sort_pairs(ent_key.p, ent_val.p, n_ent, bits_for((uint64_t)(nvis - 1)), rs, st);
-        k_run_offsets<<<grid_for(n_ent, 256), 256, 0, st>>>(ent_key.p, n_ent, nvis, block_ray_off.p);
-        WC_LAUNCH_CHECK();
+        if (group_entries) {
+            radix_sort_pairs(ent_key.p, ent_val.p, n_ent, bits_for((uint64_t)(nvis - 1)), rs, st);
+            k_run_offsets<<<grid_for(n_ent, 256), 256, 0, st>>>(ent_key.p, n_ent, nvis, block_ray_off.p);
+            WC_LAUNCH_CHECK();
+        }
         WC_CUDA(cudaEventRecord(ev_stage[4], st));
         contrib.ensure(2 * nvis);
         k_contrib<<<grid_for(nvis, 256), 256, 0, st>>>(visible_ids.p, nvis, slot_of_block.p, vol->bdx, vol->bdy,
@@ -1022,6 +1207,7 @@ bool Session::pass(PassStatsC &stats) {
         float ms = 0.0f;
         WC_CUDA(cudaEventElapsedTime(&ms, ev_stage[k], ev_stage[k + 1]));
         stage_ms[k] += ms;
+        if (pass_index < kMaxPassLog) pass_stage_ms[pass_index][k] = ms;
     }
     stats.pass_index = pass_index;
     stats.n_active_before = n_act;

@@ -29,6 +29,7 @@ enum Counter : int {
     C_NCAND,      // eviction candidates
     C_ERR,        // device-side invariant failures
     C_HW,         // occupied cache slots: free slots are the suffix [hw, cap)
+    C_WORK,       // persistent traversal work counter
     C_COUNT
 };
 
@@ -51,6 +52,7 @@ struct Session {
     int speculation = 1, max_spec = 64, corrupt = 0;
     double base[3] = {0.85, 0.85, 0.85};
     bool uniform_origin = true;
+    bool group_entries = true;  // stable sort of entries by block before the raytrace
     double eye[3] = {0, 0, 0};
 
     DevBuf<double> origin, dir, t_enter, t_exit, coarse_tmax, fine_tmax;
@@ -63,6 +65,7 @@ struct Session {
     DevBuf<float4> rgbz;
     DevBuf<int4> contrib;  // 8 contributor slots per visible block
     DevBuf<uint32_t> vis_bm, act_bm, vis_word_off, act_word_off;
+    DevBuf<uint32_t> fine_bm, coarse_bm;  // per-iso range-test bitmaps, rebuilt at every reset
     DevBuf<uint32_t> visible_ids, block_ray_off, active_ids;
     DevBuf<uint32_t> rgba;
     DevBuf<float> depth;
@@ -80,6 +83,8 @@ struct Session {
     static constexpr int kStages = 6;  // traverse, mark, cache, group, raytrace, composite
     cudaEvent_t ev_stage[kStages + 1] = {};
     double stage_ms[kStages] = {};
+    static constexpr int kMaxPassLog = 128;
+    double pass_stage_ms[kMaxPassLog][kStages] = {};  // per-pass stage device ms since reset
     DevBuf<uint32_t> pix;
     DevBuf<double> dir_in;
     CameraParams cam_params{};

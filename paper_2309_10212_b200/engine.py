@@ -39,6 +39,7 @@ class RenderOptions:
     base_color: tuple[float, float, float] = BASE_COLOR
     corrupt_cache: bool = False  # test hook: zero the slot pool every pass
     cache_capacity: int | None = None
+    group_entries: bool = True  # build_rt_inputs grouping (locality + PassBuffers layout)
 
 
 @dataclass
@@ -129,6 +130,8 @@ class RenderSession:
                   int(opts.max_spec), cap, int(bool(opts.corrupt_cache)), C.byref(self._h))
         if tuple(opts.base_color) != BASE_COLOR:
             _lib.call("wc_session_set_base_color", self._h, *[float(c) for c in opts.base_color])
+        if not opts.group_entries:
+            _lib.call("wc_session_set_grouping", self._h, 0)
         self.last_c_stats = None
 
     def close(self):
@@ -185,6 +188,12 @@ class RenderSession:
         _lib.call("wc_session_stage_ms", self._h, a)
         return dict(zip(STAGES, [float(x) for x in a]))
 
+    def pass_stage_ms(self, pass_index: int) -> dict:
+        """Device ms per stage of one pass of the current frame."""
+        a = (C.c_double * 6)()
+        _lib.call("wc_session_pass_stage_ms", self._h, int(pass_index), a)
+        return dict(zip(STAGES, [float(x) for x in a]))
+
     def last_pass_ms(self) -> float:
         v = C.c_double()
         _lib.call("wc_session_last_pass_ms", self._h, C.byref(v))
@@ -227,6 +236,7 @@ class _SessionPool:
 
     def get(self, cv, grids, cam, iso, opts) -> RenderSession:
         key = (id(cv), int(opts.width), int(opts.height), bool(opts.speculation), int(opts.max_spec),
+               bool(opts.group_entries),
                tuple(opts.base_color), bool(opts.corrupt_cache), opts.cache_capacity)
         for i, (k, s) in enumerate(self.items):
             if k == key and s.cv is cv:

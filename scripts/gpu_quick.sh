@@ -1,0 +1,15 @@
+# parity tests + C3 bench variants (args passed to bench.py per line of $VARIANTS)
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+if [ -z "$SKIP_TESTS" ]; then
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?
+timeout 900 python -m pytest tests/ -m gpu -x -q -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo tests_rc=$?; tail -2 gpurun_out/gpu_tests.log
+fi
+i=0
+while IFS= read -r args; do
+  i=$((i+1))
+  timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline $args > gpurun_out/q_$i.json 2> gpurun_out/q_$i.err
+  python -c "
+import json; d=json.load(open('gpurun_out/q_$i.json'))
+print('[$args]', 'ms/frame', d['ms_per_step'], 'e2e', d['e2e']['ms_per_frame'], 'stages', d['stage_ms_per_frame'])
+for p, s in enumerate(d.get('stage_ms_per_pass_last_frame', [])): print('   pass', p, d['pass_stats'][p]['n_active_before'], s)" || tail -3 gpurun_out/q_$i.err
+done <<< "${VARIANTS:-}"

@@ -46,7 +46,8 @@ def lockstep(wc, cv, ov, cam_tuple, w, h, iso, *, speculation=True, max_spec=64,
     per-pass stat, per-stage buffer and the final framebuffer are identical."""
     cam = wc_camera(wc, cam_tuple) if cam_tuple is not None else None
     opts = wc.RenderOptions(width=w, height=h, speculation=speculation, max_spec=max_spec,
-                            cache_capacity=cache_capacity, corrupt_cache=corrupt)
+                            cache_capacity=cache_capacity, corrupt_cache=corrupt,
+                            group_entries=internals)  # grouped PassBuffers are compared when internals
     sess = wc.RenderSession(cv, wc.build_grids(cv), cam, iso, opts, pixel_ids=pixel_ids, origins=origins, dirs=dirs)
     if dirs is None:
         o, d = orc.camera_rays(cam_tuple, w, h, pixel_ids)
