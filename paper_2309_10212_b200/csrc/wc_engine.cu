@@ -583,6 +583,36 @@ __global__ void k_cache_stamp(const uint32_t *ids, int64_t n, const int32_t *slo
     }
 }
 
+// eviction candidates (resident, stamp < pass_no) per stamp value
+// (few distinct stamps: per-CTA shared-memory bins, one global add per bin)
+__global__ void k_stamp_hist(const int32_t *block_of_slot, const int32_t *last_used, int64_t hw, int32_t pass_no,
+                             uint32_t *hist) {
+    extern __shared__ uint32_t sh[];
+    for (int b = threadIdx.x; b < pass_no; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < hw; s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t lu = last_used[s];
+        if (block_of_slot[s] >= 0 && lu < pass_no) atomicAdd(&sh[lu], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < pass_no; b += blockDim.x)
+        if (sh[b]) atomicAdd(&hist[b], sh[b]);
+}
+
+// mark the blocks of the candidates stamped L in a block bitmap
+__global__ void k_mark_stamp(const int32_t *block_of_slot, const int32_t *last_used, int64_t hw, int32_t L,
+                             uint32_t *bm) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < hw; s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t b = block_of_slot[s];
+        if (b >= 0 && last_used[s] == L) atomicOr(&bm[b >> 5], 1u << (b & 31));
+    }
+}
+
+__global__ void k_blocks_to_slots(const uint32_t *blocks, int64_t n, const int32_t *slot_of_block, uint32_t *slots) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        slots[i] = (uint32_t)slot_of_block[blocks[i]];
+}
+
 // BlockCache reset: forget every resident block of the previous frame
 __global__ void k_cache_unmap(const int32_t *block_of_slot, int64_t phys, int32_t *slot_of_block) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < phys; s += (int64_t)gridDim.x * blockDim.x) {
@@ -1002,6 +1032,62 @@ void Session::read_counters(int first, int count) {
     WC_CUDA(cudaStreamSynchronize(st));
 }
 
+// cache.py:84-91: the n_evict first candidates in (last_used, block_id)
+// order -> cand_val[0..n_evict) (their slots).  Candidates are resident slots
+// not stamped this pass.  Exact selection without sorting every candidate:
+// a histogram over the pass stamps finds the stamp L* at which the count
+// reaches n_evict; each stamp bucket L <= L* then lists its blocks in
+// ascending id order by marking them in a block bitmap and extracting it (a
+// counting sort over the block-id universe), and only the last bucket is
+// truncated.  Many small buckets fall back to the 2-key stable radix sort.
+void Session::select_victims(int64_t n_cand, int64_t n_evict) {
+    const int64_t nb = pass_no;  // stamps are 1..pass_no-1 for candidates
+    stamp_hist.ensure(nb + 1);
+    h_stamp_hist.ensure_host(nb + 1);
+    WC_CUDA(cudaMemsetAsync(stamp_hist.p, 0, 4 * (nb + 1), st));
+    k_stamp_hist<<<grid_for(hw, 256), 256, 4 * (size_t)nb, st>>>(block_of_slot.p, last_used.p, hw, pass_no,
+                                                                 stamp_hist.p);
+    WC_LAUNCH_CHECK();
+    WC_CUDA(cudaMemcpyAsync(h_stamp_hist.p, stamp_hist.p, 4 * (nb + 1), cudaMemcpyDeviceToHost, st));
+    WC_CUDA(cudaStreamSynchronize(st));
+    int64_t acc = 0;
+    int n_buckets = 0;
+    int L_star = -1;
+    for (int L = 0; L <= nb && acc < n_evict; L++) {
+        const int64_t c = h_stamp_hist.p[L];
+        if (!c) continue;
+        n_buckets++;
+        acc += c;
+        L_star = L;
+    }
+    if (acc < n_evict) throw InvariantError("cache: fewer eviction candidates than needed");
+    if (n_buckets > 6) {  // many stamp buckets: one stable 2-key radix sort of all candidates
+        PredCand pc{block_of_slot.p, last_used.p, pass_no};
+        scan_exclusive(pc, hw, cand_off.p, counters.p + C_NCAND, partials.p, st);
+        k_compact_cand<<<grid_for(hw, 256), 256, 0, st>>>(pc, hw, cand_off.p, cand_key.p, cand_val.p);
+        WC_LAUNCH_CHECK();
+        radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)(vol->n_blocks - 1)), rs, st);
+        k_gather_last_used<<<grid_for(n_cand, 256), 256, 0, st>>>(cand_val.p, n_cand, last_used.p, cand_key.p);
+        WC_LAUNCH_CHECK();
+        radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)pass_no), rs, st);
+        return;
+    }
+    const int64_t nwords = ceil_div(vol->n_blocks, 32);
+    int64_t off = 0;
+    for (int L = 0; L <= L_star; L++) {
+        const int64_t c = h_stamp_hist.p[L];
+        if (!c) continue;
+        k_mark_stamp<<<grid_for(hw, 256), 256, 0, st>>>(block_of_slot.p, last_used.p, hw, L, act_bm.p);
+        WC_LAUNCH_CHECK();
+        // ascending block ids of bucket L -> cand_key[off..off+c)
+        bitmap_extract(act_bm.p, nwords, act_word_off.p, cand_key.p + off, counters.p + C_NCAND, partials.p, st);
+        WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
+        off += c;
+    }
+    k_blocks_to_slots<<<grid_for(n_evict, 256), 256, 0, st>>>(cand_key.p, n_evict, slot_of_block.p, cand_val.p);
+    WC_LAUNCH_CHECK();
+}
+
 // cache.py:66-111 ensure_resident over the ascending active_ids[0..n_actb)
 void Session::ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict) {
     pass_no += 1;
@@ -1049,15 +1135,7 @@ void Session::ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict)
             const int64_t n_hits = n_actb - n_miss;
             const int64_t n_cand = hw - n_hits;  // resident and not stamped this pass
             if (n_cand < n_evict) throw InvariantError("cache: fewer eviction candidates than needed");
-            PredCand pc{block_of_slot.p, last_used.p, pass_no};
-            scan_exclusive(pc, hw, cand_off.p, counters.p + C_NCAND, partials.p, st);
-            k_compact_cand<<<grid_for(hw, 256), 256, 0, st>>>(pc, hw, cand_off.p, cand_key.p, cand_val.p);
-            WC_LAUNCH_CHECK();
-            // (last_used, block_id) order: stable LSD by block id, then by pass stamp
-            radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)(vol->n_blocks - 1)), rs, st);
-            k_gather_last_used<<<grid_for(n_cand, 256), 256, 0, st>>>(cand_val.p, n_cand, last_used.p, cand_key.p);
-            WC_LAUNCH_CHECK();
-            radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)pass_no), rs, st);
+            select_victims(n_cand, n_evict);
             k_evict<<<grid_for(n_evict, 256), 256, 0, st>>>(cand_val.p, n_evict, block_of_slot.p, slot_of_block.p);
             WC_LAUNCH_CHECK();
             victims = cand_val.p;

@@ -107,6 +107,9 @@ struct Session {
    private:
     void read_counters(int first, int count);
     void ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict);
+    void select_victims(int64_t n_cand, int64_t n_evict);
+    DevBuf<uint32_t> stamp_hist;
+    PinnedBuf<uint32_t> h_stamp_hist;
 };
 
 // Brute-force oracle on the device (oracle.py:42-122): every ray marches all

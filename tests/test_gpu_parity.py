@@ -85,6 +85,7 @@ SCENES = [
     ("value_noise", 64, 16, 64, 64, 0.5, 0.4, True, 64, None),
     ("value_noise", 64, 8, 128, 100, 0.5, 0.4, False, 64, None),
     ("value_noise", 48, 12, 120, 90, 0.35, 0.7, True, 64, 40),          # heavy eviction
+    ("value_noise", 48, 12, 96, 72, 0.5, 0.3, False, 64, 48),           # eviction across many pass stamps
     ("marschner_lobb", 41, 26, 90, 70, 0.6, 0.25, True, 64, None),     # qbits 26 fallback
     ("value_noise", 64, 4, 100, 100, 0.5, 0.1, True, 8, None),
     ("gaussians", 96, 16, 160, 90, 0.3, 0.0, True, 64, None),
