@@ -61,7 +61,8 @@ def parse():
     p.add_argument("--max-spec", type=int, default=64)
     p.add_argument("--cache-slots", type=int, default=0, help="LRU budget (0 = reference initial_capacity)")
     p.add_argument("--tile", type=int, default=32)
-    p.add_argument("--no-group", action="store_true", help="raytrace entries in ray order (skip the block sort)")
+    p.add_argument("--group", action="store_true", help="sort entries by block before the raytrace "
+                   "(build_rt_inputs); default off: ray order, same pixels")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-tiles", type=int, default=0, help="tiles in the CPU-baseline sample (0=auto)")
     p.add_argument("--threads", type=int, default=0, help="host threads for the reference arm (0=all)")
@@ -210,7 +211,7 @@ def run_b200(args):
     if args.config == "c4" and cache is None:
         cache = 1024
     opts = wc.RenderOptions(width=w, height=h, max_spec=args.max_spec, cache_capacity=cache,
-                            group_entries=not args.no_group)
+                            group_entries=args.group)
     pix = wdist.tile_pixels(w, h, rank, world, args.tile) if world > 1 else None
     sess = wc.RenderSession(cv, grids, cam, iso, opts, pixel_ids=pix)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -221,8 +222,7 @@ def run_b200(args):
         torch.cuda.synchronize()
 
     def frame():
-        sess.reset(cam, iso)
-        return sess.run()
+        return sess.render_frame(cam, iso)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -310,6 +310,7 @@ def run_b200(args):
                         "active": s.active_blocks, "decoded": s.new_decompressed, "cache_slots": s.cache_slots,
                         "utilization": round(s.utilization, 4)} for s in stats],
         "stage_ms_per_frame": {k: round(v, 4) for k, v in stage_frame.items()},
+        "frame_ms_outside_stages": round(ms_per_frame - sum(stage_frame.values()), 4),
         "stage_ms_per_pass_last_frame": [{k: round(v, 4) for k, v in sess.pass_stage_ms(p).items()}
                                          for p in range(min(len(stats), 128))],
         "frame_ms_all": [round(x, 3) for x in frame_ms],

@@ -61,6 +61,9 @@ const char *wc_last_error(void);
 int wc_init(int device);
 /* Number of kernels this library has launched so far (all threads). */
 long long wc_launch_count(void);
+/* Page-locked host memory for framebuffer read-back (full-bandwidth D2H). */
+int wc_host_alloc(uint64_t bytes, void **out);
+int wc_host_free(void *p);
 /* Build-time identity string (arch, flags). */
 const char *wc_build_info(void);
 
@@ -101,14 +104,18 @@ int wc_session_create(wc_volume *v, const wc_camera *cam, const uint32_t *pixel_
                       const double *dirs, double iso, int speculation, int max_spec, int64_t cache_capacity,
                       int corrupt_cache, wc_session **out);
 int wc_session_set_base_color(wc_session *s, double r, double g, double b);
-/* build_rt_inputs (engine.py:121-149) grouping on (1, default) or off (0):
- * the raytrace is correct either way; grouping adds L1 locality and the
+/* build_rt_inputs (engine.py:121-149) grouping on (1) or off (0, default):
+ * the raytrace is correct either way (same pixels); grouping yields the
  * reference's PassBuffers layout (required by wc_session_rt_inputs). */
 int wc_session_set_grouping(wc_session *s, int group_entries);
 /* One pass; *ran = 0 once every ray has terminated. */
 int wc_session_pass(wc_session *s, wc_pass_stats *stats, int *ran);
 /* Run passes until done (render, engine.py:385-401); returns pass count. */
 int wc_session_run(wc_session *s, wc_pass_stats *stats_out, int64_t max_stats, int64_t *n_passes);
+/* reset(cam, iso) + run in one call: one frame of render (engine.py:385-401)
+ * on the session's allocations with no host round trip between the two. */
+int wc_session_render(wc_session *s, const wc_camera *cam, double iso, wc_pass_stats *stats_out, int64_t max_stats,
+                      int64_t *n_passes);
 int wc_session_n_active(const wc_session *s, int64_t *n_active);
 /* Framebuffer.snapshot (engine.py:62-63): RGBA8 (n x 4) + float32 depth (n). */
 int wc_session_framebuffer(wc_session *s, uint8_t *rgba, float *depth);
@@ -124,8 +131,8 @@ int wc_session_reset(wc_session *s, const wc_camera *cam, double iso);
 /* Device time (CUDA events on the session stream) from the last
  * create/reset to the end of the last pass. */
 int wc_session_frame_ms(wc_session *s, double *ms);
-/* Accumulated device ms per stage since the last reset:
- * [traverse, mark+extract, cache+decode, group(sort), raytrace, composite] */
+/* Accumulated device ms per stage since the last reset, then the reset itself:
+ * [traverse, mark+extract, cache+decode, group(sort), raytrace, composite, reset] (7 doubles) */
 int wc_session_stage_ms(const wc_session *s, double *ms6);
 /* The same split for one pass (pass_index < 128) of the current frame. */
 int wc_session_pass_stage_ms(const wc_session *s, int64_t pass_index, double *ms6);

@@ -73,6 +73,8 @@ _SIGS = {
     "wc_last_error": (C.c_char_p, []),
     "wc_init": (_i32, [_i32]),
     "wc_launch_count": (C.c_longlong, []),
+    "wc_host_alloc": (_i32, [C.c_uint64, _vp]),
+    "wc_host_free": (_i32, [_vp]),
     "wc_build_info": (C.c_char_p, []),
     "wc_volume_create": (_i32, [_vp, C.c_uint64, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
     "wc_volume_compress": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp]),
@@ -89,6 +91,7 @@ _SIGS = {
     "wc_session_pass": (_i32, [_vp, _vp, _vp]),
     "wc_session_run": (_i32, [_vp, _vp, _i64, _vp]),
     "wc_session_n_active": (_i32, [_vp, _vp]),
+    "wc_session_render": (_i32, [_vp, _vp, _dbl, _vp, _i64, _vp]),
     "wc_session_framebuffer": (_i32, [_vp, _vp, _vp]),
     "wc_session_framebuffer_device": (_i32, [_vp, _vp, _vp]),
     "wc_session_last_pass_ms": (_i32, [_vp, _vp]),
@@ -176,3 +179,41 @@ def ptr(a):
 
 def out(shape, dtype):
     return np.empty(shape, dtype=dtype)
+
+
+class PinnedPool:
+    """Recycled page-locked host buffers for framebuffer read-back.
+
+    ``get(nbytes)`` returns a uint8 numpy array over pinned memory.  A buffer
+    is handed out again only once every array viewing it has been garbage
+    collected (tracked with a weakref on the base array), so callers can
+    keep returned frames as long as they like; past ``limit`` live buffers
+    the pool falls back to ordinary (pageable) arrays."""
+
+    def __init__(self, limit: int = 8):
+        import weakref
+
+        self._weakref = weakref
+        self.limit = limit
+        self.slots: list[list] = []  # [ptr, nbytes, weakref to base or None]
+
+    def get(self, nbytes: int) -> np.ndarray:
+        for slot in self.slots:
+            ptr, cap, ref = slot
+            if cap >= nbytes and (ref is None or ref() is None):
+                return self._hand_out(slot, nbytes)
+        if len(self.slots) >= self.limit:
+            return np.empty(nbytes, dtype=np.uint8)
+        p = C.c_void_p()
+        call("wc_host_alloc", C.c_uint64(nbytes), C.byref(p))
+        slot = [p.value, nbytes, None]
+        self.slots.append(slot)
+        return self._hand_out(slot, nbytes)
+
+    def _hand_out(self, slot, nbytes):
+        base = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(slot[0]))
+        slot[2] = self._weakref.ref(base)
+        return base
+
+
+pinned_pool = PinnedPool()

@@ -79,6 +79,18 @@ const char *wc_build_info(void) {
 
 long long wc_launch_count(void) { return wc::g_launches.load(); }
 
+int wc_host_alloc(uint64_t bytes, void **out) {
+    WC_API_BEGIN
+    WC_CUDA(cudaMallocHost(out, bytes ? bytes : 1));
+    WC_API_END
+}
+
+int wc_host_free(void *p) {
+    WC_API_BEGIN
+    if (p) WC_CUDA(cudaFreeHost(p));
+    WC_API_END
+}
+
 int wc_init(int device) {
     WC_API_BEGIN
     int n = 0;
@@ -304,6 +316,20 @@ int wc_session_run(wc_session *s, wc_pass_stats *stats_out, int64_t max_stats, i
     WC_API_END
 }
 
+int wc_session_render(wc_session *s, const wc_camera *cam, double iso, wc_pass_stats *stats_out, int64_t max_stats,
+                      int64_t *n_passes) {
+    WC_API_BEGIN
+    s->s->reset(reinterpret_cast<const wc::CameraParams *>(cam), iso);
+    int64_t k = 0;
+    wc::PassStatsC st{};
+    while (s->s->pass(st)) {
+        if (stats_out && k < max_stats) std::memcpy(stats_out + k, &st, sizeof(st));
+        k++;
+    }
+    if (n_passes) *n_passes = k;
+    WC_API_END
+}
+
 int wc_session_n_active(const wc_session *s, int64_t *n_active) {
     WC_API_BEGIN
     *n_active = s->s->n_act;
@@ -350,6 +376,7 @@ int wc_session_frame_ms(wc_session *s, double *ms) {
 int wc_session_stage_ms(const wc_session *s, double *ms6) {
     WC_API_BEGIN
     for (int k = 0; k < wc::Session::kStages; k++) ms6[k] = s->s->stage_ms[k];
+    ms6[wc::Session::kStages] = s->s->reset_ms;
     WC_API_END
 }
 

@@ -21,6 +21,14 @@
 #ifndef WC_TRAVERSE_MIN_CTAS
 #define WC_TRAVERSE_MIN_CTAS 6
 #endif
+// 1: two-phase raytrace (k_rt_find / k_rt_solve / k_rt_shade); 0: fused k_raytrace.
+#ifndef WC_SPLIT_RAYTRACE
+#define WC_SPLIT_RAYTRACE 1
+#endif
+// Passes with at most this many active rays use the warp-per-ray traversal.
+#ifndef WC_WARP_TRAVERSE_MAX
+#define WC_WARP_TRAVERSE_MAX 16384
+#endif
 #ifndef WC_TRAVERSE_LOOKAHEAD
 #define WC_TRAVERSE_LOOKAHEAD 0
 #endif
@@ -188,7 +196,8 @@ __global__ void k_compact_keep(const uint32_t *keep, const uint32_t *off, const 
         if (keep[i]) out[off[i]] = in[i];
 }
 
-__global__ void k_compact_miss(PredMiss pred, int64_t n, const uint32_t *off, uint32_t *out) {
+__global__ void k_compact_miss(PredMiss pred, const uint32_t *d_n, int64_t n_max, const uint32_t *off, uint32_t *out) {
+    const int64_t n = min(n_max, (int64_t)*d_n);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         if (pred(i)) out[off[i]] = pred.ids[i];
 }
@@ -507,6 +516,190 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
     }
 }
 
+__device__ __forceinline__ Dda shfl_dda(const Dda &s, int src) {
+    Dda o;
+    o.cx = __shfl_sync(0xffffffffu, s.cx, src);
+    o.cy = __shfl_sync(0xffffffffu, s.cy, src);
+    o.cz = __shfl_sync(0xffffffffu, s.cz, src);
+    o.tx = __shfl_sync(0xffffffffu, s.tx, src);
+    o.ty = __shfl_sync(0xffffffffu, s.ty, src);
+    o.tz = __shfl_sync(0xffffffffu, s.tz, src);
+    return o;
+}
+
+// traversal.py:217-403 for passes with few active rays (the long rays of the
+// last passes, where one ray's serial DDA is the critical path): one warp
+// per ray.  The DDA never depends on grid values, so lane k simulates the
+// ray k steps ahead from the shared state -- the k-th cell of the current
+// fine run (<= 10 cells in a 4^3 coarse cell) or the (k+1)-th coarse step --
+// looks up its range bit, and ballots decide, in the reference's order,
+// which cells emit, where the n_spec-th emit or the descent happens, and
+// where the ray leaves.  The lane that simulated exactly that many steps
+// holds the reference's iterator state and shuffles it to the warp.
+__global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp0; i < a.n_act; i += nwarps) {
+        const uint32_t r = a.act_list[i];
+        double o[3], d[3];
+        a.rays.load(r, o, d);
+        const double ox = o[0], oy = o[1], oz = o[2], dx = d[0], dy = d[1], dz = d[2];
+        const double te = a.t_exit[r];
+        const int sx = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
+        const int sy = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
+        const int sz = dz > 0.0 ? 1 : (dz < 0.0 ? -1 : 0);
+        const double fdel_x = dx != 0.0 ? 4.0 / fabs(dx) : CUDART_INF;
+        const double fdel_y = dy != 0.0 ? 4.0 / fabs(dy) : CUDART_INF;
+        const double fdel_z = dz != 0.0 ? 4.0 / fabs(dz) : CUDART_INF;
+        const double cdel_x = dx != 0.0 ? 16.0 / fabs(dx) : CUDART_INF;
+        const double cdel_y = dy != 0.0 ? 16.0 / fabs(dy) : CUDART_INF;
+        const double cdel_z = dz != 0.0 ? 16.0 / fabs(dz) : CUDART_INF;
+        Dda c, f;
+        const uint32_t cc = a.coarse_cell[r];
+        c.cx = (int)(cc % (uint32_t)cdx);
+        c.cy = (int)((cc / (uint32_t)cdx) % (uint32_t)cdy);
+        c.cz = (int)(cc / ((uint32_t)cdx * (uint32_t)cdy));
+        c.tx = a.coarse_tmax[3 * (int64_t)r];
+        c.ty = a.coarse_tmax[3 * (int64_t)r + 1];
+        c.tz = a.coarse_tmax[3 * (int64_t)r + 2];
+        const uint32_t fc = a.fine_cell[r];
+        bool in_fine_run = fc != WC_UINT_MAX;
+        f.cx = f.cy = f.cz = 0;
+        if (in_fine_run) {
+            f.cx = (int)(fc % (uint32_t)fdx);
+            f.cy = (int)((fc / (uint32_t)fdx) % (uint32_t)fdy);
+            f.cz = (int)(fc / ((uint32_t)fdx * (uint32_t)fdy));
+        }
+        f.tx = a.fine_tmax[3 * (int64_t)r];
+        f.ty = a.fine_tmax[3 * (int64_t)r + 1];
+        f.tz = a.fine_tmax[3 * (int64_t)r + 2];
+        const int64_t base = i * (int64_t)a.n_spec;
+        int emitted = 0;
+        bool ray_done = false, finished = false;
+        while (!finished) {
+            if (in_fine_run) {
+                // lane k: cell X_k of the run (k steps from f), and the step that leaves it
+                Dda g = f;
+                bool valid = lane <= kFineRun;
+                for (int j = 0; j < lane && valid; j++) {
+                    const double t = dda_step(g, sx, sy, sz, fdel_x, fdel_y, fdel_z);
+                    if (t > te || g.cx < 0 || g.cx >= fdx || g.cy < 0 || g.cy >= fdy || g.cz < 0 || g.cz >= fdz ||
+                        (g.cx >> 2) != c.cx || (g.cy >> 2) != c.cy || (g.cz >> 2) != c.cz)
+                        valid = false;  // the run ended before cell k
+                }
+                uint32_t cell = 0;
+                int term = 0;
+                Dda h = g;
+                if (valid) {
+                    cell = (uint32_t)(g.cx + fdx * (g.cy + fdy * g.cz));
+                    const double t = dda_step(h, sx, sy, sz, fdel_x, fdel_y, fdel_z);
+                    if (t > te || h.cx < 0 || h.cx >= fdx || h.cy < 0 || h.cy >= fdy || h.cz < 0 || h.cz >= fdz)
+                        term = 2;
+                    else if ((h.cx >> 2) != c.cx || (h.cy >> 2) != c.cy || (h.cz >> 2) != c.cz)
+                        term = 1;
+                }
+                const bool bit = valid && ((__ldg(a.fine_bm + (cell >> 5)) >> (cell & 31)) & 1u);
+                const uint32_t tmask = __ballot_sync(0xffffffffu, valid && term != 0);
+                // last cell of the run in this batch (a run has <= 10 cells, so a
+                // termination is always found; kFineRun keeps the bound explicit)
+                const int K = tmask ? __ffs(tmask) - 1 : kFineRun;
+                uint32_t E = __ballot_sync(0xffffffffu, bit) & ((2u << K) - 1u);
+                const int left = a.n_spec - emitted;
+                int stop = K;
+                if (__popc(E) >= left) {  // the n_spec-th emit happens at cell m
+                    uint32_t e = E;
+                    for (int q = 1; q < left; q++) e &= e - 1;
+                    stop = __ffs(e) - 1;
+                    E &= (stop == 31 ? 0xffffffffu : ((2u << stop) - 1u));
+                }
+                if ((E >> lane) & 1u) {
+                    const int64_t slot = base + emitted + __popc(E & lt);
+                    a.block_slots[slot] = cell;
+                    a.ray_slots[slot] = r;
+                    atomicOr(&a.vis_bm[cell >> 5], 1u << (cell & 31));
+                }
+                emitted += __popc(E);
+                f = shfl_dda(h, stop);  // state after the step that follows cell `stop`
+                const int term_stop = __shfl_sync(0xffffffffu, term, stop);
+                if (term_stop == 2) {
+                    in_fine_run = false;
+                    ray_done = true;
+                } else if (term_stop == 1) {
+                    in_fine_run = false;
+                }
+                finished = emitted == a.n_spec || ray_done;
+            } else {
+                // lane k: the (k+1)-th coarse step from c
+                Dda g = c;
+                bool valid = true, term_here = false;
+                double t = 0.0;
+                for (int j = 0; j <= lane && valid; j++) {
+                    t = dda_step(g, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+                    if (t > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 || g.cz >= cdz) {
+                        valid = false;
+                        term_here = j == lane;
+                    }
+                }
+                const uint32_t cell = valid ? (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz)) : 0u;
+                const bool bit = valid && ((__ldg(a.coarse_bm + (cell >> 5)) >> (cell & 31)) & 1u);
+                const uint32_t B = __ballot_sync(0xffffffffu, bit), T = __ballot_sync(0xffffffffu, term_here);
+                const int first_term = T ? __ffs(T) - 1 : 32, first_hit = B ? __ffs(B) - 1 : 32;
+                if (first_hit < first_term) {  // descend (traversal.py:357-386)
+                    c = shfl_dda(g, first_hit);
+                    const double t_cross = __shfl_sync(0xffffffffu, t, first_hit);
+                    const double px = ox + dx * t_cross, py = oy + dy * t_cross, pz = oz + dz * t_cross;
+                    const int lo_x = 4 * c.cx, lo_y = 4 * c.cy, lo_z = 4 * c.cz;
+                    const int hi_x = min(lo_x + 3, fdx - 1), hi_y = min(lo_y + 3, fdy - 1),
+                              hi_z = min(lo_z + 3, fdz - 1);
+                    f.cx = (int)floor(px / 4.0);
+                    f.cy = (int)floor(py / 4.0);
+                    f.cz = (int)floor(pz / 4.0);
+                    f.cx = f.cx < lo_x ? lo_x : (f.cx > hi_x ? hi_x : f.cx);
+                    f.cy = f.cy < lo_y ? lo_y : (f.cy > hi_y ? hi_y : f.cy);
+                    f.cz = f.cz < lo_z ? lo_z : (f.cz > hi_z ? hi_z : f.cz);
+                    f.tx = dx > 0.0 ? ((double)(f.cx + 1) * 4.0 - ox) / dx
+                                    : (dx < 0.0 ? ((double)f.cx * 4.0 - ox) / dx : CUDART_INF);
+                    f.ty = dy > 0.0 ? ((double)(f.cy + 1) * 4.0 - oy) / dy
+                                    : (dy < 0.0 ? ((double)f.cy * 4.0 - oy) / dy : CUDART_INF);
+                    f.tz = dz > 0.0 ? ((double)(f.cz + 1) * 4.0 - oz) / dz
+                                    : (dz < 0.0 ? ((double)f.cz * 4.0 - oz) / dz : CUDART_INF);
+                    in_fine_run = true;
+                } else if (first_term < 32) {  // left the volume / passed t_exit
+                    c = shfl_dda(g, first_term);
+                    ray_done = true;
+                    finished = true;
+                } else {
+                    c = shfl_dda(g, 31);
+                }
+            }
+        }
+        for (int k = emitted + lane; k < a.n_spec; k += 32) {  // traversal.py:423-424 sentinels
+            a.block_slots[base + k] = WC_UINT_MAX;
+            a.ray_slots[base + k] = WC_UINT_MAX;
+        }
+        if (lane == 0) {
+            a.emitted[i] = (uint32_t)emitted;
+            if (ray_done) {
+                a.exited[r] = 1;
+                a.coarse_cell[r] = WC_UINT_MAX;
+                a.fine_cell[r] = WC_UINT_MAX;
+            } else {
+                a.coarse_cell[r] = (uint32_t)(c.cx + cdx * (c.cy + cdy * c.cz));
+                a.fine_cell[r] = in_fine_run ? (uint32_t)(f.cx + fdx * (f.cy + fdy * f.cz)) : WC_UINT_MAX;
+            }
+            a.coarse_tmax[3 * (int64_t)r] = c.tx;
+            a.coarse_tmax[3 * (int64_t)r + 1] = c.ty;
+            a.coarse_tmax[3 * (int64_t)r + 2] = c.tz;
+            a.fine_tmax[3 * (int64_t)r] = f.tx;
+            a.fine_tmax[3 * (int64_t)r + 1] = f.ty;
+            a.fine_tmax[3 * (int64_t)r + 2] = f.tz;
+        }
+    }
+}
+
 // The traversal's range tests for one isovalue, precomputed: bit c of the
 // fine (coarse) bitmap is `min[c] <= iso && iso <= max[c]` evaluated in
 // float64 exactly as traversal.py:297 (:357) does.  The 15.7 MB fine bitmap
@@ -575,8 +768,9 @@ __global__ void k_run_offsets(const uint32_t *key, int64_t n, int64_t nvis, uint
 
 // ---------------------------------------------------------------- cache
 
-__global__ void k_cache_stamp(const uint32_t *ids, int64_t n, const int32_t *slot_of_block, int32_t *last_used,
-                              int32_t pass_no) {
+__global__ void k_cache_stamp(const uint32_t *ids, const uint32_t *d_n, int64_t n_max, const int32_t *slot_of_block,
+                              int32_t *last_used, int32_t pass_no) {
+    const int64_t n = min(n_max, (int64_t)*d_n);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t s = slot_of_block[ids[i]];
         if (s >= 0) last_used[s] = pass_no;  // cache.py:73-74
@@ -791,6 +985,111 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_raytrace(Raytrace
     }
 }
 
+// ---- two-phase raytrace: the same per-entry result as k_raytrace, with the
+// float64 cubic solves run as a dense work list so that the divergent DDA
+// and the uniform root finding no longer share warps.
+struct SplitArgs {
+    RaytraceArgs a;
+    uint32_t *item_j, *item_cell, *n_items, *best;
+    double *item_t;
+    int64_t item_cap;
+};
+
+struct EntryCtx {  // everything an entry's trace needs, rebuilt from its position j
+    uint32_t k;
+    int64_t r;
+    int bx, by, bz, cx, cy, cz;
+    SlotField field;
+    double o[3], d[3], te;
+};
+
+__device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, int64_t j) {
+    EntryCtx e;
+    const uint32_t v = a.ent_key[j];
+    e.k = a.ent_val[j];
+    e.r = a.ent_ray[e.k];
+    const uint32_t b = a.visible_ids[v];
+    e.bx = (int)(b % (uint32_t)a.bdx);
+    e.by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy);
+    e.bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
+    const int4 c0 = a.contrib[2 * v], c1 = a.contrib[2 * v + 1];
+    e.field = SlotField{a.slot_values, c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    e.cx = max(0, min(4, a.nx - 1 - 4 * e.bx));
+    e.cy = max(0, min(4, a.ny - 1 - 4 * e.by));
+    e.cz = max(0, min(4, a.nz - 1 - 4 * e.bz));
+    a.rays.load(e.r, e.o, e.d);
+    e.te = a.rays.t_enter[e.r];
+    return e;
+}
+
+// phase 1: walk each entry's dual cells, list the bracketing ones
+__global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
+    const RaytraceArgs &a = s.a;
+    const int lane = threadIdx.x & 31;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n_ent; j += (int64_t)gridDim.x * blockDim.x) {
+        const EntryCtx e = entry_ctx(a, j);
+        s.best[e.k] = WC_UINT_MAX;
+        int found = 0;
+        walk_bracketing_cells(e.field, 4 * e.bx, 4 * e.by, 4 * e.bz, 4 * e.bx, 4 * e.by, 4 * e.bz, e.cx, e.cy, e.cz,
+                              e.o, e.d, e.te, a.iso, [&](int cx, int cy, int cz, int seq) {
+                                  const uint32_t am = __activemask();
+                                  const int leader = __ffs(am) - 1;
+                                  uint32_t first = 0;
+                                  if (lane == leader) first = atomicAdd(s.n_items, (uint32_t)__popc(am));
+                                  first = __shfl_sync(am, first, leader);
+                                  const uint32_t it = first + __popc(am & ((1u << lane) - 1u));
+                                  if (it < s.item_cap) {
+                                      s.item_j[it] = (uint32_t)j;
+                                      s.item_cell[it] = (uint32_t)((cx - 4 * e.bx) | ((cy - 4 * e.by) << 3) |
+                                                                   ((cz - 4 * e.bz) << 6) | (seq << 9));
+                                  }
+                                  found++;
+                              });
+        if (!found) a.rgbz[e.k] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
+    }
+}
+
+// phase 2: one thread per candidate cell; the earliest cell (in DDA order)
+// with a root wins through an atomicMin on (seq, item)
+__global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArgs s) {
+    const RaytraceArgs &a = s.a;
+    const int64_t n_items = min((int64_t)*s.n_items, s.item_cap);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_items; i += (int64_t)gridDim.x * blockDim.x) {
+        const EntryCtx e = entry_ctx(a, s.item_j[i]);
+        const uint32_t code = s.item_cell[i];
+        const int lx = code & 7, ly = (code >> 3) & 7, lz = (code >> 6) & 7, seq = code >> 9;
+        float c[8];
+        e.field.corners(lx, ly, lz, c);
+        const double th = solve_cell(c, e.o, e.d, 4 * e.bx + lx, 4 * e.by + ly, 4 * e.bz + lz, e.te, a.iso);
+        if (th != CUDART_INF) {
+            s.item_t[i] = th;
+            atomicMin(&s.best[e.k], ((uint32_t)seq << 27) | (uint32_t)i);
+        }
+    }
+}
+
+// phase 3: shade each entry's winning cell (or record the miss)
+__global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
+    const RaytraceArgs &a = s.a;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n_ent; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = a.ent_val[j];
+        const uint32_t bst = s.best[k];
+        if (bst == WC_UINT_MAX) {
+            a.rgbz[k] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
+            continue;
+        }
+        const EntryCtx e = entry_ctx(a, j);
+        const uint32_t i = bst & ((1u << 27) - 1u);
+        const uint32_t code = s.item_cell[i];
+        const int lx = code & 7, ly = (code >> 3) & 7, lz = (code >> 6) & 7;
+        float c[8], rgb[3];
+        e.field.corners(lx, ly, lz, c);
+        const double th = s.item_t[i];
+        shade_hit(c, e.o, e.d, 4 * e.bx + lx, 4 * e.by + ly, 4 * e.bz + lz, th, a.br, a.bg, a.bb, rgb);
+        a.rgbz[k] = make_float4(rgb[0], rgb[1], rgb[2], (float)th);
+    }
+}
+
 // ------------------------------------------------------------- composite
 
 // engine.py:222-258 _composite_kernel: closest speculated hit per active
@@ -900,6 +1199,7 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     if (!uniform_origin) origin.alloc(n * 3);
     for (auto &e : ev_stage) WC_CUDA(cudaEventCreate(&e));
     WC_CUDA(cudaEventCreate(&ev_frame0));
+    WC_CUDA(cudaEventCreate(&ev_reset_end));
     t_enter.alloc(n);
     t_exit.alloc(n);
     coarse_tmax.alloc(n * 3);
@@ -999,10 +1299,11 @@ void Session::reset(const CameraParams *cam, double iso_) {
     }
     cap = std::max<int64_t>(1, init_cap <= 0 ? std::max<int64_t>(1024, 2 * n / 64) : init_cap);
     phys = std::min<int64_t>(cap, vol->n_blocks);
+    // Free slots' values are never read (a slot is written by its decode
+    // before any lookup can reach it), so only the slot maps are reset.
     slot_values.grow(phys * 64, st);
     block_of_slot.grow(phys, st);
     last_used.grow(phys, st);
-    WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * phys, st));
     WC_CUDA(cudaMemsetAsync(block_of_slot.p, 0xFF, 4 * phys, st));
     WC_CUDA(cudaMemsetAsync(last_used.p, 0, 4 * phys, st));
     pass_no = 0;
@@ -1011,7 +1312,11 @@ void Session::reset(const CameraParams *cam, double iso_) {
     for (double &m : stage_ms) m = 0.0;
     for (auto &p : pass_stage_ms)
         for (double &m : p) m = 0.0;
+    WC_CUDA(cudaEventRecord(ev_reset_end, st));
     read_counters(C_NACT, 1);
+    float rms = 0.0f;
+    WC_CUDA(cudaEventElapsedTime(&rms, ev_frame0, ev_reset_end));
+    reset_ms = rms;
     n_act = h_counters.p[0];
 }
 
@@ -1023,6 +1328,7 @@ Session::~Session() {
     if (ev_begin) cudaEventDestroy(ev_begin);
     if (ev_end) cudaEventDestroy(ev_end);
     if (ev_frame0) cudaEventDestroy(ev_frame0);
+    if (ev_reset_end) cudaEventDestroy(ev_reset_end);
     for (auto &e : ev_stage)
         if (e) cudaEventDestroy(e);
 }
@@ -1089,8 +1395,23 @@ void Session::select_victims(int64_t n_cand, int64_t n_evict) {
 }
 
 // cache.py:66-111 ensure_resident over the ascending active_ids[0..n_actb)
-void Session::ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict) {
+// First half of ensure_resident, queued before the pass's one mid-pass host
+// read: stamp the hits and compact the misses of the active blocks whose
+// count is still on the device (cache.py:67-73, :76-78).
+void Session::cache_lookup() {
     pass_no += 1;
+    const int64_t nmax = active_ids.n - 1;  // upper bound of the active-block count
+    const uint32_t *d_nactb = counters.p + C_NACTB;
+    k_cache_stamp<<<grid_for(nmax, 256), 256, 0, st>>>(active_ids.p, d_nactb, nmax, slot_of_block.p, last_used.p,
+                                                      pass_no);
+    WC_LAUNCH_CHECK();
+    PredMiss pm{active_ids.p, slot_of_block.p};
+    scan_exclusive_dev(pm, d_nactb, nmax, miss_off.p, counters.p + C_NMISS, partials.p, st);
+    k_compact_miss<<<grid_for(nmax, 256), 256, 0, st>>>(pm, d_nactb, nmax, miss_off.p, miss_ids.p);
+    WC_LAUNCH_CHECK();
+}
+
+void Session::ensure_resident(int64_t n_actb, int64_t n_miss, int64_t &n_evict) {
     if (n_actb > cap) {  // cache.py:74-75: grow to ceil(1.5 * needed)
         cap = (3 * n_actb + 1) / 2;
         const int64_t new_phys = std::min<int64_t>(cap, vol->n_blocks);
@@ -1098,7 +1419,6 @@ void Session::ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict)
             slot_values.grow(new_phys * 64, st);  // keeps resident slots (cache.py:42-53)
             block_of_slot.grow(new_phys, st);
             last_used.grow(new_phys, st);
-            WC_CUDA(cudaMemsetAsync(slot_values.p + phys * 64, 0, 4 * 64 * (new_phys - phys), st));
             WC_CUDA(cudaMemsetAsync(block_of_slot.p + phys, 0xFF, 4 * (new_phys - phys), st));
             WC_CUDA(cudaMemsetAsync(last_used.p + phys, 0, 4 * (new_phys - phys), st));
             phys = new_phys;
@@ -1110,26 +1430,14 @@ void Session::ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict)
         cand_val.alloc(phys);
         partials.ensure(scan_tiles(std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n, phys})) + 8);
     }
-    n_miss = -1;  // unknown until the end-of-pass read unless fetched below
     n_evict = 0;
-    if (n_actb == 0) {
-        n_miss = 0;
-        return;
-    }
-    k_cache_stamp<<<grid_for(n_actb, 256), 256, 0, st>>>(active_ids.p, n_actb, slot_of_block.p, last_used.p, pass_no);
-    WC_LAUNCH_CHECK();
-    PredMiss pm{active_ids.p, slot_of_block.p};
-    scan_exclusive(pm, n_actb, miss_off.p, counters.p + C_NMISS, partials.p, st);
-    k_compact_miss<<<grid_for(n_actb, 256), 256, 0, st>>>(pm, n_actb, miss_off.p, miss_ids.p);
-    WC_LAUNCH_CHECK();
+    if (n_miss == 0) return;
     // Free slots are always the suffix [hw, cap): misses take the lowest free
     // slots (cache.py:79, :97) and an eviction pass consumes every free slot
     // plus exactly its victims (cache.py:80-96), so no hole ever opens.
     const int64_t n_free = cap - hw;
     const uint32_t *victims = nullptr;
-    if (hw + n_actb > cap) {  // evictions possible: need the miss count now
-        read_counters(C_NMISS, 1);
-        n_miss = h_counters.p[0];
+    {
         if (n_miss > n_free) {
             n_evict = n_miss - n_free;
             const int64_t n_hits = n_actb - n_miss;
@@ -1142,7 +1450,7 @@ void Session::ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict)
         }
     }
     // the miss count stays on the device: the decode grid strides over it
-    k_decode_insert<<<grid_for(n_actb * 32, 256, 8), 256, 0, st>>>(
+    k_decode_insert<<<grid_for(n_miss * 32, 256, 8), 256, 0, st>>>(
         vol->payload.p, vol->qbits, vol->stride, miss_ids.p, counters.p + C_NMISS, hw, n_free, victims,
         slot_values.p, block_of_slot.p, last_used.p, slot_of_block.p, pass_no, counters.p + C_HW, cap);
     WC_LAUNCH_CHECK();
@@ -1189,7 +1497,9 @@ bool Session::pass(PassStatsC &stats) {
     ta.vis_bm = vis_bm.p;
     ta.work = counters.p + C_WORK;
     WC_CUDA(cudaMemsetAsync(ta.work, 0, 4, st));
-    if (WC_TRAVERSE_LOOKAHEAD)
+    if (n_act <= WC_WARP_TRAVERSE_MAX)  // few (long) rays: warp-cooperative DDA per ray
+        k_traverse_warp<<<grid_for(n_act * 32, 128, 16), 128, 0, st>>>(ta);
+    else if (WC_TRAVERSE_LOOKAHEAD)
         k_traverse<true><<<grid_for(n_act, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st>>>(ta);
     else
         k_traverse<false><<<grid_for(n_act, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st>>>(ta);
@@ -1209,16 +1519,18 @@ bool Session::pass(PassStatsC &stats) {
     WC_LAUNCH_CHECK();
     WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
     WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
+    cache_lookup();  // cache hits stamped, misses compacted, counts still on the device
     WC_CUDA(cudaEventRecord(ev_stage[2], st));
-    read_counters(C_NENT, 3);
+    read_counters(C_NENT, 4);  // the pass's one mid-pass host read
     const int64_t n_ent = h_counters.p[0], nvis = h_counters.p[1], nactb = h_counters.p[2];
+    const int64_t n_miss = h_counters.p[3];
     if (n_ent > n) throw InvariantError("slot budget exceeded");
     last_nent = n_ent;
     last_nvis = nvis;
     last_nactb = nactb;
 
-    // cache.ensure_resident (+ fused decode)
-    int64_t n_miss = 0, n_evict = 0;
+    // cache.ensure_resident: growth, eviction, fused decode
+    int64_t n_evict = 0;
     ensure_resident(nactb, n_miss, n_evict);
     if (corrupt) WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * phys, st));  // engine.py:338-339
     WC_CUDA(cudaEventRecord(ev_stage[3], st));
@@ -1258,8 +1570,32 @@ bool Session::pass(PassStatsC &stats) {
         ra.bg = base[1];
         ra.bb = base[2];
         ra.rgbz = rgbz.p;
-        k_raytrace<<<grid_for(n_ent, 128, 16), 128, 0, st>>>(ra);
-        WC_LAUNCH_CHECK();
+        if (WC_SPLIT_RAYTRACE) {
+            SplitArgs sa{};
+            sa.a = ra;
+            sa.item_cap = 10 * n;  // <= 10 dual cells per entry (monotone ray in a 4^3 region)
+            if (item_j.n < sa.item_cap) {
+                item_j.alloc(sa.item_cap);
+                item_cell.alloc(sa.item_cap);
+                item_t.alloc(sa.item_cap);
+                best.alloc(n);
+            }
+            sa.item_j = item_j.p;
+            sa.item_cell = item_cell.p;
+            sa.item_t = item_t.p;
+            sa.best = best.p;
+            sa.n_items = counters.p + C_NITEMS;
+            WC_CUDA(cudaMemsetAsync(sa.n_items, 0, 4, st));
+            k_rt_find<<<grid_for(n_ent, 128, 16), 128, 0, st>>>(sa);
+            WC_LAUNCH_CHECK();
+            k_rt_solve<<<grid_for(sa.item_cap, 128, WC_RAYTRACE_MIN_CTAS), 128, 0, st>>>(sa);
+            WC_LAUNCH_CHECK();
+            k_rt_shade<<<grid_for(n_ent, 128, 16), 128, 0, st>>>(sa);
+            WC_LAUNCH_CHECK();
+        } else {
+            k_raytrace<<<grid_for(n_ent, 128, 16), 128, 0, st>>>(ra);
+            WC_LAUNCH_CHECK();
+        }
     } else {
         WC_CUDA(cudaEventRecord(ev_stage[4], st));
     }
@@ -1276,10 +1612,7 @@ bool Session::pass(PassStatsC &stats) {
     read_counters(0, C_COUNT);
     const int64_t n_after = h_counters.p[C_NACT];
     if (h_counters.p[C_ERR]) throw InvariantError("visible block not resident");
-    if (nactb > 0) {
-        n_miss = h_counters.p[C_NMISS];
-        hw = h_counters.p[C_HW];
-    }
+    if (n_miss > 0) hw = h_counters.p[C_HW];
     WC_CUDA(cudaEventElapsedTime(&last_kernel_ms, ev_begin, ev_end));
     for (int k = 0; k < kStages; k++) {
         float ms = 0.0f;

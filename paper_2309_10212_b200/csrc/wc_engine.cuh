@@ -30,6 +30,7 @@ enum Counter : int {
     C_ERR,        // device-side invariant failures
     C_HW,         // occupied cache slots: free slots are the suffix [hw, cap)
     C_WORK,       // persistent traversal work counter
+    C_NITEMS,     // candidate cells listed by the two-phase raytrace
     C_COUNT
 };
 
@@ -52,7 +53,11 @@ struct Session {
     int speculation = 1, max_spec = 64, corrupt = 0;
     double base[3] = {0.85, 0.85, 0.85};
     bool uniform_origin = true;
-    bool group_entries = true;  // stable sort of entries by block before the raytrace
+    // Stable sort of entries by block before the raytrace (build_rt_inputs,
+    // engine.py:121-149).  Off by default: the thread-per-entry raytrace gets
+    // its block locality from ray order + L1 (measured 1.70 vs 1.69 ms at C3)
+    // and the sort costs 0.5 ms/frame; on for the reference PassBuffers views.
+    bool group_entries = false;
     double eye[3] = {0, 0, 0};
 
     DevBuf<double> origin, dir, t_enter, t_exit, coarse_tmax, fine_tmax;
@@ -64,6 +69,8 @@ struct Session {
     DevBuf<uint32_t> ent_key, ent_val, ent_ray;
     DevBuf<float4> rgbz;
     DevBuf<int4> contrib;  // 8 contributor slots per visible block
+    DevBuf<uint32_t> item_j, item_cell, best;  // two-phase raytrace work list
+    DevBuf<double> item_t;
     DevBuf<uint32_t> vis_bm, act_bm, vis_word_off, act_word_off;
     DevBuf<uint32_t> fine_bm, coarse_bm;  // per-iso range-test bitmaps, rebuilt at every reset
     DevBuf<uint32_t> visible_ids, block_ray_off, active_ids;
@@ -79,7 +86,8 @@ struct Session {
     DevBuf<uint32_t> counters, partials;
     PinnedBuf<uint32_t> h_counters;
     RadixScratch rs;
-    cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_frame0 = nullptr;
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_frame0 = nullptr, ev_reset_end = nullptr;
+    double reset_ms = 0.0;  // device time of the last reset (iso bitmaps, rays, cache maps)
     static constexpr int kStages = 6;  // traverse, mark, cache, group, raytrace, composite
     cudaEvent_t ev_stage[kStages + 1] = {};
     double stage_ms[kStages] = {};
@@ -106,7 +114,8 @@ struct Session {
 
    private:
     void read_counters(int first, int count);
-    void ensure_resident(int64_t n_actb, int64_t &n_miss, int64_t &n_evict);
+    void cache_lookup();
+    void ensure_resident(int64_t n_actb, int64_t n_miss, int64_t &n_evict);
     void select_victims(int64_t n_cand, int64_t n_evict);
     DevBuf<uint32_t> stamp_hist;
     PinnedBuf<uint32_t> h_stamp_hist;

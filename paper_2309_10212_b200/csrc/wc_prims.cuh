@@ -61,9 +61,18 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *s
     return warp_prefix + x - v;
 }
 
+// d_n (nullable): element count read on the device, capped by n (the
+// launch-time upper bound), so a scan can follow a producer without a host
+// round trip.
+__device__ __forceinline__ int64_t scan_count(int64_t n, const uint32_t *d_n) {
+    return d_n ? min(n, (int64_t)*d_n) : n;
+}
+
 template <class Load>
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(Load ld, int64_t n, uint32_t *tile_sums) {
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_reduce(Load ld, int64_t n_max, const uint32_t *d_n, uint32_t *tile_sums) {
     __shared__ uint32_t sw[32];
+    const int64_t n = scan_count(n_max, d_n);
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
     uint32_t s = 0;
 #pragma unroll
@@ -81,10 +90,12 @@ __global__ void __launch_bounds__(1024) k_scan_partials(uint32_t *tile_sums, int
 
 template <class Load>
 __global__ void __launch_bounds__(kScanThreads)
-    k_scan_apply(Load ld, int64_t n, const uint32_t *tile_offsets, uint32_t *out) {
+    k_scan_apply(Load ld, int64_t n_max, const uint32_t *d_n, const uint32_t *tile_offsets, uint32_t *out) {
     __shared__ uint32_t sw[32];
     __shared__ uint32_t tile[kScanTile];
+    const int64_t n = scan_count(n_max, d_n);
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    if (base >= n) return;
 #pragma unroll
     for (int k = 0; k < kScanIPT; k++) {
         const int idx = k * kScanThreads + threadIdx.x;
@@ -123,11 +134,28 @@ void scan_exclusive(Load ld, int64_t n, uint32_t *out, uint32_t *d_total, uint32
         return;
     }
     const int64_t nt = scan_tiles(n);
-    k_scan_reduce<Load><<<(unsigned)nt, kScanThreads, 0, st>>>(ld, n, partials);
+    k_scan_reduce<Load><<<(unsigned)nt, kScanThreads, 0, st>>>(ld, n, nullptr, partials);
     WC_LAUNCH_CHECK();
     k_scan_partials<<<1, 1024, 0, st>>>(partials, nt, d_total);
     WC_LAUNCH_CHECK();
-    k_scan_apply<Load><<<(unsigned)nt, kScanThreads, 0, st>>>(ld, n, partials, out);
+    k_scan_apply<Load><<<(unsigned)nt, kScanThreads, 0, st>>>(ld, n, nullptr, partials, out);
+    WC_LAUNCH_CHECK();
+}
+
+// Same with the element count on the device (<= n_max, the launch bound).
+template <class Load>
+void scan_exclusive_dev(Load ld, const uint32_t *d_n, int64_t n_max, uint32_t *out, uint32_t *d_total,
+                        uint32_t *partials, cudaStream_t st) {
+    if (n_max <= 0) {
+        WC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
+        return;
+    }
+    const int64_t nt = scan_tiles(n_max);
+    k_scan_reduce<Load><<<(unsigned)nt, kScanThreads, 0, st>>>(ld, n_max, d_n, partials);
+    WC_LAUNCH_CHECK();
+    k_scan_partials<<<1, 1024, 0, st>>>(partials, nt, d_total);
+    WC_LAUNCH_CHECK();
+    k_scan_apply<Load><<<(unsigned)nt, kScanThreads, 0, st>>>(ld, n_max, d_n, partials, out);
     WC_LAUNCH_CHECK();
 }
 

@@ -279,6 +279,104 @@ __device__ double trace_region(const Field &field, int fox, int foy, int foz, in
     }
 }
 
+// ---- trace_region split in three, for the two-phase raytrace ------------
+// (walk the cells, solve every candidate cell with uniform SIMT work, shade
+// the first hit).  Together they compute exactly trace_region: the first
+// bracketing cell in DDA order whose cubic has a root in its overlap wins.
+
+// blocktrace.py:346-418: clip the ray to the region and walk its dual cells;
+// on_cell(cx, cy, cz, seq) is called, in DDA order, for every cell whose
+// corner range brackets iso (seq = 0, 1, ...).
+template <class Field, class OnCell>
+__device__ void walk_bracketing_cells(const Field &field, int fox, int foy, int foz, int lo_x, int lo_y, int lo_z,
+                                      int n_x, int n_y, int n_z, const double o[3], const double d[3],
+                                      double ray_t_enter, double iso, OnCell on_cell) {
+    if (n_x <= 0 || n_y <= 0 || n_z <= 0) return;
+    double t0 = ray_t_enter, t1 = CUDART_INF;
+    const int lo[3] = {lo_x, lo_y, lo_z}, nn[3] = {n_x, n_y, n_z};
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        if (d[a] != 0.0) {
+            double ta = ((double)lo[a] - o[a]) / d[a];
+            double tb = ((double)(lo[a] + nn[a]) - o[a]) / d[a];
+            if (ta > tb) {
+                const double t = ta;
+                ta = tb;
+                tb = t;
+            }
+            t0 = py_max(t0, ta);
+            t1 = py_min(t1, tb);
+        } else if (o[a] < (double)lo[a] || o[a] > (double)(lo[a] + nn[a])) {
+            return;
+        }
+    }
+    if (t0 > t1) return;
+    const double ts = t0 + kEntryNudge * py_max(1.0, t1 - t0);
+    int cx = (int)floor(o[0] + d[0] * ts);
+    int cy = (int)floor(o[1] + d[1] * ts);
+    int cz = (int)floor(o[2] + d[2] * ts);
+    cx = min(max(cx, lo_x), lo_x + n_x - 1);
+    cy = min(max(cy, lo_y), lo_y + n_y - 1);
+    cz = min(max(cz, lo_z), lo_z + n_z - 1);
+    const int sx = d[0] > 0.0 ? 1 : (d[0] < 0.0 ? -1 : 0);
+    const int sy = d[1] > 0.0 ? 1 : (d[1] < 0.0 ? -1 : 0);
+    const int sz = d[2] > 0.0 ? 1 : (d[2] < 0.0 ? -1 : 0);
+    const double del_x = d[0] != 0.0 ? 1.0 / fabs(d[0]) : CUDART_INF;
+    const double del_y = d[1] != 0.0 ? 1.0 / fabs(d[1]) : CUDART_INF;
+    const double del_z = d[2] != 0.0 ? 1.0 / fabs(d[2]) : CUDART_INF;
+    double tmx = d[0] > 0.0 ? ((double)(cx + 1) - o[0]) / d[0] : (d[0] < 0.0 ? ((double)cx - o[0]) / d[0] : CUDART_INF);
+    double tmy = d[1] > 0.0 ? ((double)(cy + 1) - o[1]) / d[1] : (d[1] < 0.0 ? ((double)cy - o[1]) / d[1] : CUDART_INF);
+    double tmz = d[2] > 0.0 ? ((double)(cz + 1) - o[2]) / d[2] : (d[2] < 0.0 ? ((double)cz - o[2]) / d[2] : CUDART_INF);
+    float c[8];
+    int seq = 0;
+    for (;;) {
+        field.corners(cx - fox, cy - foy, cz - foz, c);
+        float cmin = c[0], cmax = c[0];
+#pragma unroll
+        for (int q = 1; q < 8; q++) {
+            if (c[q] < cmin) cmin = c[q];
+            if (c[q] > cmax) cmax = c[q];
+        }
+        if ((double)cmin <= iso && iso <= (double)cmax) on_cell(cx, cy, cz, seq++);
+        if (tmx <= tmy && tmx <= tmz) {
+            cx += sx;
+            tmx += del_x;
+            if (cx < lo_x || cx >= lo_x + n_x) return;
+        } else if (tmy <= tmz) {
+            cy += sy;
+            tmy += del_y;
+            if (cy < lo_y || cy >= lo_y + n_y) return;
+        } else {
+            cz += sz;
+            tmz += del_z;
+            if (cz < lo_z || cz >= lo_z + n_z) return;
+        }
+    }
+}
+
+// blocktrace.py:420-427: the root in one bracketing cell, or +inf.
+__device__ __forceinline__ double solve_cell(const float c[8], const double o[3], const double d[3], int cx, int cy,
+                                             int cz, double ray_t_enter, double iso) {
+    const double cell[3] = {(double)cx, (double)cy, (double)cz};
+    double ct0, ct1;
+    cell_overlap(o, d, cell, ct0, ct1);
+    if (ct0 < ray_t_enter) ct0 = ray_t_enter;
+    if (!(ct0 <= ct1)) return CUDART_INF;
+    return intersect_cubic(c, o, d, cell, ct0, ct1, iso);
+}
+
+// blocktrace.py:428-433: shade the hit at parameter th in cell (cx, cy, cz).
+__device__ __forceinline__ void shade_hit(const float c[8], const double o[3], const double d[3], int cx, int cy,
+                                          int cz, double th, double br, double bg, double bb, float rgb[3]) {
+    double ux = o[0] + d[0] * th - (double)cx;
+    double uy = o[1] + d[1] * th - (double)cy;
+    double uz = o[2] + d[2] * th - (double)cz;
+    ux = py_min(py_max(ux, 0.0), 1.0);
+    uy = py_min(py_max(uy, 0.0), 1.0);
+    uz = py_min(py_max(uz, 0.0), 1.0);
+    grad_shade(c, ux, uy, uz, d, br, bg, bb, rgb);
+}
+
 // engine.py:152-158 _rgb_u8: clamp, scale in float64, truncating cast.
 __device__ __forceinline__ uint32_t rgb_u8(double v) {
     if (v < 0.0)

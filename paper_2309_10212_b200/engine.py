@@ -39,7 +39,10 @@ class RenderOptions:
     base_color: tuple[float, float, float] = BASE_COLOR
     corrupt_cache: bool = False  # test hook: zero the slot pool every pass
     cache_capacity: int | None = None
-    group_entries: bool = True  # build_rt_inputs grouping (locality + PassBuffers layout)
+    # build_rt_inputs grouping (engine.py:121-149).  Off by default on B200:
+    # the thread-per-entry raytrace is as fast on ray-ordered entries; turn
+    # on to get the reference's PassBuffers layout (debug.pass_buffers).
+    group_entries: bool = False
 
 
 @dataclass
@@ -130,8 +133,7 @@ class RenderSession:
                   int(opts.max_spec), cap, int(bool(opts.corrupt_cache)), C.byref(self._h))
         if tuple(opts.base_color) != BASE_COLOR:
             _lib.call("wc_session_set_base_color", self._h, *[float(c) for c in opts.base_color])
-        if not opts.group_entries:
-            _lib.call("wc_session_set_grouping", self._h, 0)
+        _lib.call("wc_session_set_grouping", self._h, int(bool(opts.group_entries)))
         self.last_c_stats = None
 
     def close(self):
@@ -165,11 +167,23 @@ class RenderSession:
         self.last_c_stats = st
         return _stats_from_c(st)
 
-    def run(self, max_passes: int = 100000) -> list[PassStats]:
-        buf = (_lib.PassStatsC * max_passes)()
+    _MAX_STATS = 4096
+
+    def run(self) -> list[PassStats]:
+        """All remaining passes (render, engine.py:385-401)."""
+        buf = (_lib.PassStatsC * self._MAX_STATS)()
         k = C.c_int64()
-        _lib.call("wc_session_run", self._h, buf, max_passes, C.byref(k))
-        return [_stats_from_c(buf[i]) for i in range(min(k.value, max_passes))]
+        _lib.call("wc_session_run", self._h, buf, self._MAX_STATS, C.byref(k))
+        return [_stats_from_c(buf[i]) for i in range(min(k.value, self._MAX_STATS))]
+
+    def render_frame(self, cam: Camera | None, iso: float) -> list[PassStats]:
+        """reset(cam, iso) + run() in a single C call (no Python inside the frame)."""
+        cam_c = cam.to_c(self.w, self.h) if cam is not None else None
+        buf = (_lib.PassStatsC * self._MAX_STATS)()
+        k = C.c_int64()
+        _lib.call("wc_session_render", self._h, None if cam_c is None else C.byref(cam_c), float(iso), buf,
+                  self._MAX_STATS, C.byref(k))
+        return [_stats_from_c(buf[i]) for i in range(min(k.value, self._MAX_STATS))]
 
     def reset(self, cam: Camera | None, iso: float) -> None:
         """New frame on the same allocations (fresh rays, framebuffer, cache)."""
@@ -184,9 +198,9 @@ class RenderSession:
 
     def stage_ms(self) -> dict:
         """Accumulated device ms per stage since the last reset."""
-        a = (C.c_double * 6)()
+        a = (C.c_double * 7)()
         _lib.call("wc_session_stage_ms", self._h, a)
-        return dict(zip(STAGES, [float(x) for x in a]))
+        return dict(zip(STAGES + ("reset",), [float(x) for x in a]))
 
     def pass_stage_ms(self, pass_index: int) -> dict:
         """Device ms per stage of one pass of the current frame."""
@@ -201,6 +215,10 @@ class RenderSession:
 
     def read(self, rgba=None, depth=None):
         """Framebuffer of this session's rays: (rgba (n,4) u8, depth (n,) f32)."""
+        if rgba is None and depth is None:  # one recycled pinned buffer for both (full-speed D2H)
+            base = _lib.pinned_pool.get(8 * self.n)
+            rgba = base[:4 * self.n].reshape(self.n, 4)
+            depth = base[4 * self.n:8 * self.n].view(np.float32)
         if rgba is None:
             rgba = np.empty((self.n, 4), dtype=np.uint8)
         if depth is None:
@@ -234,7 +252,8 @@ class _SessionPool:
         self.size = size
         self.items: list[tuple[tuple, RenderSession]] = []
 
-    def get(self, cv, grids, cam, iso, opts) -> RenderSession:
+    def get(self, cv, grids, opts, cam):
+        """A pooled session for (cv, opts), created (with `cam`) if needed."""
         key = (id(cv), int(opts.width), int(opts.height), bool(opts.speculation), int(opts.max_spec),
                bool(opts.group_entries),
                tuple(opts.base_color), bool(opts.corrupt_cache), opts.cache_capacity)
@@ -242,10 +261,9 @@ class _SessionPool:
             if k == key and s.cv is cv:
                 if grids is not None:
                     grids.bind(cv)
-                s.reset(cam, iso)
                 self.items.append(self.items.pop(i))
                 return s
-        s = RenderSession(cv, grids, cam, iso, opts)
+        s = RenderSession(cv, grids, cam, 0.0, opts)
         self.items.append((key, s))
         while len(self.items) > self.size:
             self.items.pop(0)[1].close()
@@ -262,8 +280,8 @@ session_pool = _SessionPool()
 def render(cv: CompressedVolume, grids: MacrocellGrids, cam: Camera, iso: float,
            opts: RenderOptions) -> tuple[Framebuffer, list[PassStats]]:
     """engine.py:385-401: render to completion; only the final frame is read back."""
-    s = session_pool.get(cv, grids, cam, iso, opts)
-    stats = s.run()
+    s = session_pool.get(cv, grids, opts, cam)
+    stats = s.render_frame(cam, iso)
     if not stats:  # camera missed the volume on every pixel
         fb = Framebuffer.blank(opts.width, opts.height)
         fb.completeness = 1.0

@@ -8,8 +8,5 @@ i=0
 while IFS= read -r args; do
   i=$((i+1))
   timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline $args > gpurun_out/q_$i.json 2> gpurun_out/q_$i.err
-  python -c "
-import json; d=json.load(open('gpurun_out/q_$i.json'))
-print('[$args]', 'ms/frame', d['ms_per_step'], 'e2e', d['e2e']['ms_per_frame'], 'stages', d['stage_ms_per_frame'])
-for p, s in enumerate(d.get('stage_ms_per_pass_last_frame', [])): print('   pass', p, d['pass_stats'][p]['n_active_before'], s)" || tail -3 gpurun_out/q_$i.err
+  echo "variant $i: [$args]"; python scripts/show_bench.py gpurun_out/q_$i.json || tail -3 gpurun_out/q_$i.err
 done <<< "${VARIANTS:-}"

@@ -118,8 +118,10 @@ def compare_pass(sess, os_, n_pass, with_values=True):
     assert np.array_equal(gc["block_of_slot"].astype(np.int64), bos[:phys]), f"{tag} block_of_slot"
     assert (bos[phys:] == -1).all(), f"{tag} slots beyond the physical pool must be free"
     assert np.array_equal(gc["last_used"].astype(np.int64), lu[:phys]), f"{tag} last_used"
-    if with_values:
-        assert np.array_equal(gc["slot_values"].view(np.uint32), sv[:phys].view(np.uint32)), f"{tag} slot values"
+    if with_values:  # occupied slots only: a free slot's contents are never read
+        occ = gc["block_of_slot"] >= 0
+        assert np.array_equal(gc["slot_values"][occ].view(np.uint32), sv[:phys][occ].view(np.uint32)), \
+            f"{tag} slot values"
     r = debug.session_rays(sess)
     orr = os_.rays()
     for k in ("status", "exited", "coarse_cell", "fine_cell", "coarse_tmax", "fine_tmax"):
