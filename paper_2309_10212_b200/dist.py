@@ -33,42 +33,75 @@ def tile_pixels(w: int, h: int, rank: int, world: int, tile: int = 32) -> np.nda
     return np.concatenate(out).astype(np.uint32)
 
 
-def gather_tiles(rgba_local, depth_local, pix_local, w: int, h: int, group=None):
-    """Gather every rank's (rgba u8 (n,4) as int32 words, depth f32) to rank 0
-    and stitch.  Inputs are torch tensors on the rank's device (CUDA for
-    NCCL, CPU for gloo).  Returns (rgba (h,w,4) uint8, depth (h,w)) numpy on
-    rank 0, None elsewhere."""
+_GATHER_CACHE: dict = {}
+
+
+def _gather_plan(w, h, world, tile, dev):
+    """Per (image, world, tile): every rank's pixel list is a pure function of
+    (w, h, rank, world, tile), so no pixel ids travel -- rank 0 scatters each
+    rank's block of words with a precomputed index (padding -> dummy slot w*h)."""
+    import torch
+
+    key = (w, h, world, tile, str(dev))
+    plan = _GATHER_CACHE.get(key)
+    if plan is None:
+        pix = [tile_pixels(w, h, r, world, tile) for r in range(world)]
+        n_max = max(1, max(len(p) for p in pix))
+        index = np.full((world, n_max), w * h, dtype=np.int64)
+        for r, p in enumerate(pix):
+            index[r, :len(p)] = p
+        plan = {
+            "n_max": n_max,
+            "index": torch.from_numpy(index.reshape(-1)).to(dev),
+            "send": torch.zeros((2, n_max), dtype=torch.int32, device=dev),
+            "recv": torch.empty((world, 2, n_max), dtype=torch.int32, device=dev),
+            "frame": torch.zeros((2, w * h + 1), dtype=torch.int32, device=dev),
+        }
+        _GATHER_CACHE.clear()
+        _GATHER_CACHE[key] = plan
+    return plan
+
+
+def gather_tiles(rgba_local, depth_local, w: int, h: int, tile: int = 32, group=None):
+    """The finished tiles -> rank 0 (the pass loop's only exchange step):
+    one all_gather_into_tensor of every rank's [RGBA words | depth bits]
+    (8 B per pixel, over NCCL/NVLink; gloo on CPU), then one scatter into the
+    frame on rank 0.  Inputs are the rank's (n,4) uint8 and (n,) float32
+    torch tensors in tile_pixels order.  Returns (rgba (h,w,4) uint8,
+    depth (h,w) float32) numpy on rank 0, None elsewhere."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = rgba_local.device
-    n_local = torch.tensor([rgba_local.shape[0]], dtype=torch.int64, device=dev)
-    counts = [torch.zeros_like(n_local) for _ in range(world)]
-    dist.all_gather(counts, n_local, group=group)
-    n_max = int(max(int(c.item()) for c in counts))
-    # one packed buffer per rank: [pixel id, rgba word, depth bits] x n_max
-    packed = torch.full((n_max, 3), -1, dtype=torch.int32, device=dev)
+    plan = _gather_plan(w, h, world, tile, dev)
     k = rgba_local.shape[0]
+    send = plan["send"]
     if k:
-        packed[:k, 0] = pix_local.to(torch.int32)
-        packed[:k, 1] = rgba_local.view(torch.int32).reshape(-1)
-        packed[:k, 2] = depth_local.view(torch.int32)
-    bufs = [torch.empty_like(packed) for _ in range(world)]
-    dist.all_gather(bufs, packed, group=group)
+        send[0, :k] = rgba_local.reshape(-1).view(torch.int32)
+        send[1, :k] = depth_local.view(torch.int32)
+    dist.all_gather_into_tensor(plan["recv"].view(-1), send.view(-1), group=group)
     if rank != 0:
         return None
-    allp = torch.cat(bufs, 0)
-    allp = allp[allp[:, 0] >= 0]
-    rgba = torch.zeros(w * h, dtype=torch.int32, device=dev)
-    depth = torch.zeros(w * h, dtype=torch.int32, device=dev)
-    idx = allp[:, 0].long()
-    rgba[idx] = allp[:, 1]
-    depth[idx] = allp[:, 2]
-    rgba_np = rgba.cpu().numpy().view(np.uint8).reshape(h, w, 4)
-    depth_np = depth.cpu().numpy().view(np.float32).reshape(h, w)
+    frame = plan["frame"]
+    idx = plan["index"]
+    frame[0].index_copy_(0, idx, plan["recv"][:, 0, :].reshape(-1))
+    frame[1].index_copy_(0, idx, plan["recv"][:, 1, :].reshape(-1))
+    frame = frame[:, : w * h]  # [rgba words | depth bits], dummy slot dropped
+    if dev.type == "cuda":  # read back into a recycled page-locked buffer (full-speed D2H)
+        from . import _lib
+
+        base = _lib.pinned_pool.get(8 * w * h)
+        torch.from_numpy(base.view(np.int32)).view(2, w * h).copy_(frame)
+    else:
+        base = frame.contiguous().numpy().view(np.uint8).reshape(-1)
+    rgba_np = base[:4 * w * h].reshape(h, w, 4)
+    depth_np = base[4 * w * h:].view(np.float32).reshape(h, w)
     return rgba_np, depth_np
+
+
+_SHARD_SESSIONS: dict = {}
 
 
 def render_sharded(cv, grids, cam, iso, opts, tile: int = 32, group=None):
@@ -79,23 +112,31 @@ def render_sharded(cv, grids, cam, iso, opts, tile: int = 32, group=None):
 
     from .engine import Framebuffer, RenderSession
 
+    from . import _lib
+
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    pix = tile_pixels(opts.width, opts.height, rank, world, tile)
     dev = torch.device("cuda", torch.cuda.current_device())
+    # one pooled session (and tile set) per (volume, image, options, world):
+    # later frames reuse its HBM allocations through wc_session_render
+    key = (id(cv), opts.width, opts.height, opts.speculation, opts.max_spec, opts.cache_capacity,
+           opts.group_entries, tuple(opts.base_color), world, rank, tile)
+    ent = _SHARD_SESSIONS.get(key)
+    if ent is None or ent[0].cv is not cv:
+        pix = tile_pixels(opts.width, opts.height, rank, world, tile)
+        s = RenderSession(cv, grids, cam, iso, opts, pixel_ids=pix) if len(pix) else None
+        ent = (s, pix)
+        _SHARD_SESSIONS.clear()
+        _SHARD_SESSIONS[key] = ent
+    s, pix = ent
     n = len(pix)
     rgba_t = torch.empty((n, 4), dtype=torch.uint8, device=dev)
     depth_t = torch.empty(n, dtype=torch.float32, device=dev)
     stats = []
     if n:
-        with RenderSession(cv, grids, cam, iso, opts, pixel_ids=pix) as s:
-            stats = s.run()
-            torch.cuda.synchronize()
-            from . import _lib
-
-            _lib.call("wc_session_framebuffer_device", s.handle, rgba_t.data_ptr(), depth_t.data_ptr())
-    pix_t = torch.from_numpy(pix.astype(np.int64)).to(dev)
-    out = gather_tiles(rgba_t, depth_t, pix_t, opts.width, opts.height, group)
+        stats = s.render_frame(cam, iso)
+        _lib.call("wc_session_framebuffer_device", s.handle, rgba_t.data_ptr(), depth_t.data_ptr())
+    out = gather_tiles(rgba_t, depth_t, opts.width, opts.height, tile, group)
     if out is None:
         return None, stats
     rgba, depth = out

@@ -41,8 +41,7 @@ def _worker(rank, world, port, q):
     pix = wdist.tile_pixels(w, h, rank, world, 16)
     o, d = orc.camera_rays(cam, w, h, pix)
     rgba, depth, _ = orc.render(ov, o, d, len(pix), 1, iso)
-    out = wdist.gather_tiles(torch.from_numpy(rgba), torch.from_numpy(depth), torch.from_numpy(pix.astype(np.int64)),
-                             w, h)
+    out = wdist.gather_tiles(torch.from_numpy(rgba), torch.from_numpy(depth), w, h, tile=16)
     if rank == 0:
         o, d = orc.camera_rays(cam, w, h)
         full_rgba, full_depth, _ = orc.render(ov, o, d, w, h, iso)
@@ -61,7 +60,7 @@ def test_gloo_tile_gather_stitches_bit_exact(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    ok, hits = q.get(timeout=300)
+    ok, hits = q.get(timeout=120)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
