@@ -575,7 +575,8 @@ int wc_exclusive_scan(const uint32_t *values, int64_t n, uint32_t *out, uint64_t
     wc::DevBuf<uint32_t> d_in, d_out, d_part, d_tot;
     upload(d_in, values, n, st);
     d_out.alloc(n);
-    d_part.alloc(wc::scan_tiles(n));
+    d_part.alloc(wc::scan_scratch_words(n));
+    WC_CUDA(cudaMemsetAsync(d_part.p, 0, 4 * d_part.n, st));
     d_tot.alloc(1);
     wc::scan_exclusive(wc::LoadU32{d_in.p}, n, d_out.p, d_tot.p, d_part.p, st);
     uint32_t t = 0;

@@ -897,6 +897,11 @@ struct SlotField {
         const int b0 = (o & 2) ? a1 : a0, b1 = (o & 2) ? a3 : a2;
         return (o & 4) ? b1 : b0;
     }
+    // value at local lattice point (x, y, z), each in [0, 4]
+    __device__ __forceinline__ float point(int x, int y, int z) const {
+        const int sl = pick((x >> 2) | ((y >> 2) << 1) | ((z >> 2) << 2));
+        return sl >= 0 ? __ldg(sv + (int64_t)sl * 64 + (x & 3) + 4 * (y & 3) + 16 * (z & 3)) : 0.0f;
+    }
     __device__ __forceinline__ void corners(int lx, int ly, int lz, float c[8]) const {
         const int ex = lx == 3, ey = ly == 3, ez = lz == 3;
 #pragma unroll
@@ -1239,7 +1244,8 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     counters.alloc(C_COUNT);
     WC_CUDA(cudaMemsetAsync(counters.p, 0, 4 * C_COUNT, st));
     h_counters.alloc(C_COUNT);
-    partials.alloc(scan_tiles(std::max<int64_t>({n, nwords, active_ids.n, 1})) + 8);
+    partials.alloc(scan_scratch_words(std::max<int64_t>({n, nwords, active_ids.n, 1})));
+    WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
 
     slot_of_block.alloc(vol->n_blocks);
     WC_CUDA(cudaMemsetAsync(slot_of_block.p, 0xFF, 4 * vol->n_blocks, st));
@@ -1428,7 +1434,11 @@ void Session::ensure_resident(int64_t n_actb, int64_t n_miss, int64_t &n_evict) 
         cand_off.alloc(phys);
         cand_key.alloc(phys);
         cand_val.alloc(phys);
-        partials.ensure(scan_tiles(std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n, phys})) + 8);
+        const int64_t words = scan_scratch_words(std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n, phys}));
+        if (partials.n < words) {
+            partials.ensure(words);
+            WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
+        }
     }
     n_evict = 0;
     if (n_miss == 0) return;

@@ -3,25 +3,6 @@
 
 namespace wc {
 
-__global__ void __launch_bounds__(1024) k_scan_partials(uint32_t *tile_sums, int64_t ntiles, uint32_t *total) {
-    __shared__ uint32_t sw[32];
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < ntiles; base += blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        const uint32_t v = i < ntiles ? tile_sums[i] : 0;
-        uint32_t tot;
-        const uint32_t ex = block_exclusive_scan(v, sw, &tot);
-        const uint32_t c = carry;
-        if (i < ntiles) tile_sums[i] = c + ex;
-        __syncthreads();
-        if (threadIdx.x == 0) carry = c + tot;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *total = carry;
-}
-
 // ---------------------------------------------------------------- radix
 
 __global__ void __launch_bounds__(kSortThreads)
@@ -101,7 +82,8 @@ void RadixScratch::reserve(int64_t n) {
     const int64_t hn = nt * kSortBins;
     if (hist.n < hn) {
         hist.alloc(hn);
-        hist_partials.alloc(scan_tiles(hn));
+        hist_partials.alloc(scan_scratch_words(hn));
+        WC_CUDA(cudaMemset(hist_partials.p, 0, 4 * hist_partials.n));
     }
     if (!total.p) total.alloc(1);
 }
@@ -138,24 +120,17 @@ void radix_sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int nbits, Radi
 
 // ----------------------------------------------------------- bitmap extract
 
-__global__ void k_bitmap_write(const uint32_t *bm, int64_t nwords, const uint32_t *word_offsets, uint32_t *out) {
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t v = bm[w];
-        if (!v) continue;
-        uint32_t o = word_offsets[w];
-        while (v) {
-            const int b = __ffs(v) - 1;
-            out[o++] = (uint32_t)(w * 32 + b);
-            v &= v - 1;
-        }
-    }
-}
-
 void bitmap_extract(const uint32_t *bm, int64_t nwords, uint32_t *word_offsets, uint32_t *out,
                     uint32_t *d_count, uint32_t *partials, cudaStream_t st) {
-    scan_exclusive(LoadPopc{bm}, nwords, word_offsets, d_count, partials, st);
-    if (nwords <= 0) return;
-    k_bitmap_write<<<grid_for(nwords, 256), 256, 0, st>>>(bm, nwords, word_offsets, out);
+    if (nwords <= 0) {
+        WC_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st));
+        return;
+    }
+    // one pass: popcount scan of the words, ids written by each tile as
+    // soon as its prefix is known
+    k_scan_onepass<LoadPopc, SinkBits><<<(unsigned)scan_tiles(nwords), kScanThreads, 0, st>>>(
+        LoadPopc{bm}, SinkBits{bm, word_offsets, out}, nwords, nullptr, reinterpret_cast<uint64_t *>(partials),
+        next_scan_epoch(), d_count);
     WC_LAUNCH_CHECK();
 }
 

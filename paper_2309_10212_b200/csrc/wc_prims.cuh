@@ -1,6 +1,6 @@
 // wc_prims.cuh -- device-wide data-parallel primitives (prims.py:13-40).
 //
-// exclusive_scan  -> scan_exclusive()  (3-phase reduce / scan-of-partials / scan)
+// exclusive_scan  -> scan_exclusive()  (single pass, decoupled look-back)
 // compact         -> fused into callers via the scan offsets
 // sort_by_key     -> radix_sort_pairs() (stable LSD, 8-bit digits, per-warp
 //                    match_any ranking so equal keys keep input order)
@@ -68,34 +68,57 @@ __device__ __forceinline__ int64_t scan_count(int64_t n, const uint32_t *d_n) {
     return d_n ? min(n, (int64_t)*d_n) : n;
 }
 
-template <class Load>
-__global__ void __launch_bounds__(kScanThreads)
-    k_scan_reduce(Load ld, int64_t n_max, const uint32_t *d_n, uint32_t *tile_sums) {
-    __shared__ uint32_t sw[32];
-    const int64_t n = scan_count(n_max, d_n);
-    const int64_t base = (int64_t)blockIdx.x * kScanTile;
-    uint32_t s = 0;
-#pragma unroll
-    for (int k = 0; k < kScanIPT; k++) {
-        const int64_t i = base + k * kScanThreads + threadIdx.x;  // striped: coalesced
-        if (i < n) s += ld(i);
-    }
-    uint32_t tot;
-    block_exclusive_scan(s, sw, &tot);
-    if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+// ---- single-pass scan (decoupled look-back) -----------------------------
+// Each tile publishes its aggregate, then its inclusive prefix, in one
+// 64-bit status word [epoch:30 | flag:2 | value:32]; successors look back
+// over the status words with a warp.  The epoch tags every scan call, so
+// the status array never needs clearing.  Tiles only wait on lower-numbered
+// tiles, which the hardware dispatches first.  One launch per scan.
+constexpr uint32_t kFlagAggregate = 1, kFlagPrefix = 2;
+
+inline uint32_t next_scan_epoch() {
+    static std::atomic<uint32_t> e{0};
+    uint32_t v = (e.fetch_add(1) + 1) & 0x3FFFFFFFu;
+    return v ? v : next_scan_epoch();
 }
 
-// Single CTA: exclusive scan of the tile sums in place; total -> *total.
-__global__ void __launch_bounds__(1024) k_scan_partials(uint32_t *tile_sums, int64_t ntiles, uint32_t *total);
+// scratch words (uint32) a scan over n elements needs
+inline int64_t scan_scratch_words(int64_t n) { return 2 * scan_tiles(n) + 8; }
 
-template <class Load>
+__device__ __forceinline__ void store_status(uint64_t *p, uint32_t epoch, uint32_t flag, uint32_t v) {
+    atomicExch(reinterpret_cast<unsigned long long *>(p),
+               ((unsigned long long)epoch << 34) | ((unsigned long long)flag << 32) | v);
+}
+
+struct SinkStore {  // out[i] = exclusive prefix
+    uint32_t *out;
+    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const { out[i] = prefix; }
+};
+struct SinkBits {  // word offsets + ascending ids of the set bits of bm
+    const uint32_t *bm;
+    uint32_t *word_offsets, *ids;
+    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const {
+        word_offsets[i] = prefix;
+        uint32_t v = bm[i];
+        while (v) {
+            ids[prefix++] = (uint32_t)(i * 32 + __ffs(v) - 1);
+            v &= v - 1;
+        }
+    }
+};
+
+template <class Load, class Sink>
 __global__ void __launch_bounds__(kScanThreads)
-    k_scan_apply(Load ld, int64_t n_max, const uint32_t *d_n, const uint32_t *tile_offsets, uint32_t *out) {
+    k_scan_onepass(Load ld, Sink sink, int64_t n_max, const uint32_t *d_n, uint64_t *status, uint32_t epoch,
+                   uint32_t *d_total) {
     __shared__ uint32_t sw[32];
     __shared__ uint32_t tile[kScanTile];
+    __shared__ uint32_t s_excl;
     const int64_t n = scan_count(n_max, d_n);
-    const int64_t base = (int64_t)blockIdx.x * kScanTile;
-    if (base >= n) return;
+    const int64_t t = blockIdx.x;
+    const int64_t base = t * kScanTile;
+    const int64_t last = n > 0 ? (n - 1) / kScanTile : 0;
+    if (t > last) return;
 #pragma unroll
     for (int k = 0; k < kScanIPT; k++) {
         const int idx = k * kScanThreads + threadIdx.x;
@@ -109,7 +132,43 @@ __global__ void __launch_bounds__(kScanThreads)
         v[k] = tile[threadIdx.x * kScanIPT + k];
         s += v[k];
     }
-    uint32_t pre = block_exclusive_scan(s, sw, nullptr) + tile_offsets[blockIdx.x];
+    uint32_t agg;
+    uint32_t pre = block_exclusive_scan(s, sw, &agg);
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        uint32_t excl = 0;
+        if (t == 0) {
+            if (lane == 0) store_status(status, epoch, kFlagPrefix, agg);
+        } else {
+            if (lane == 0) store_status(status + t, epoch, kFlagAggregate, agg);
+            for (int64_t pred = t - 1;; pred -= 32) {
+                const int64_t idx = pred - lane;
+                uint32_t flag = kFlagPrefix, val = 0;  // before tile 0: an implicit zero prefix
+                if (idx >= 0) {
+                    unsigned long long w;
+                    do {
+                        w = *reinterpret_cast<volatile unsigned long long *>(status + idx);
+                        flag = (uint32_t)(w >> 34) == epoch ? (uint32_t)(w >> 32) & 3u : 0u;
+                    } while (flag == 0);
+                    val = (uint32_t)w;
+                }
+                const uint32_t pm = __ballot_sync(0xffffffffu, flag == kFlagPrefix);
+                const int fp = pm ? __ffs(pm) - 1 : 31;  // nearest predecessor holding a prefix
+                uint32_t c = lane <= fp ? val : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                excl += c;
+                if (pm) break;
+            }
+            if (lane == 0) store_status(status + t, epoch, kFlagPrefix, excl + agg);
+        }
+        if (lane == 0) {
+            s_excl = excl;
+            if (t == last && d_total) *d_total = n > 0 ? excl + agg : 0u;
+        }
+    }
+    __syncthreads();
+    pre += s_excl;
 #pragma unroll
     for (int k = 0; k < kScanIPT; k++) {
         tile[threadIdx.x * kScanIPT + k] = pre;
@@ -120,42 +179,33 @@ __global__ void __launch_bounds__(kScanThreads)
     for (int k = 0; k < kScanIPT; k++) {
         const int idx = k * kScanThreads + threadIdx.x;
         const int64_t i = base + idx;
-        if (i < n) out[i] = tile[idx];
+        if (i < n) sink(i, tile[idx]);
     }
 }
 
 // Exclusive scan of ld(0..n) into out[0..n); grand total into *d_total.
-// `partials` must hold scan_tiles(n) uint32.
+// `scratch` must hold scan_scratch_words(n) uint32 (zeroed once at allocation).
 template <class Load>
-void scan_exclusive(Load ld, int64_t n, uint32_t *out, uint32_t *d_total, uint32_t *partials,
-                    cudaStream_t st) {
+void scan_exclusive(Load ld, int64_t n, uint32_t *out, uint32_t *d_total, uint32_t *scratch, cudaStream_t st) {
     if (n <= 0) {
         WC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
         return;
     }
-    const int64_t nt = scan_tiles(n);
-    k_scan_reduce<Load><<<(unsigned)nt, kScanThreads, 0, st>>>(ld, n, nullptr, partials);
-    WC_LAUNCH_CHECK();
-    k_scan_partials<<<1, 1024, 0, st>>>(partials, nt, d_total);
-    WC_LAUNCH_CHECK();
-    k_scan_apply<Load><<<(unsigned)nt, kScanThreads, 0, st>>>(ld, n, nullptr, partials, out);
+    k_scan_onepass<Load, SinkStore><<<(unsigned)scan_tiles(n), kScanThreads, 0, st>>>(
+        ld, SinkStore{out}, n, nullptr, reinterpret_cast<uint64_t *>(scratch), next_scan_epoch(), d_total);
     WC_LAUNCH_CHECK();
 }
 
 // Same with the element count on the device (<= n_max, the launch bound).
 template <class Load>
 void scan_exclusive_dev(Load ld, const uint32_t *d_n, int64_t n_max, uint32_t *out, uint32_t *d_total,
-                        uint32_t *partials, cudaStream_t st) {
+                        uint32_t *scratch, cudaStream_t st) {
     if (n_max <= 0) {
         WC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
         return;
     }
-    const int64_t nt = scan_tiles(n_max);
-    k_scan_reduce<Load><<<(unsigned)nt, kScanThreads, 0, st>>>(ld, n_max, d_n, partials);
-    WC_LAUNCH_CHECK();
-    k_scan_partials<<<1, 1024, 0, st>>>(partials, nt, d_total);
-    WC_LAUNCH_CHECK();
-    k_scan_apply<Load><<<(unsigned)nt, kScanThreads, 0, st>>>(ld, n_max, d_n, partials, out);
+    k_scan_onepass<Load, SinkStore><<<(unsigned)scan_tiles(n_max), kScanThreads, 0, st>>>(
+        ld, SinkStore{out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), next_scan_epoch(), d_total);
     WC_LAUNCH_CHECK();
 }
 

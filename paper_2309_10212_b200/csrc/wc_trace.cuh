@@ -327,10 +327,12 @@ __device__ void walk_bracketing_cells(const Field &field, int fox, int foy, int 
     double tmx = d[0] > 0.0 ? ((double)(cx + 1) - o[0]) / d[0] : (d[0] < 0.0 ? ((double)cx - o[0]) / d[0] : CUDART_INF);
     double tmy = d[1] > 0.0 ? ((double)(cy + 1) - o[1]) / d[1] : (d[1] < 0.0 ? ((double)cy - o[1]) / d[1] : CUDART_INF);
     double tmz = d[2] > 0.0 ? ((double)(cz + 1) - o[2]) / d[2] : (d[2] < 0.0 ? ((double)cz - o[2]) / d[2] : CUDART_INF);
+    // Corners are carried across steps: a step shares a face with the previous
+    // cell, so only the 4 corners of the far face are loaded (same values).
     float c[8];
+    field.corners(cx - fox, cy - foy, cz - foz, c);
     int seq = 0;
     for (;;) {
-        field.corners(cx - fox, cy - foy, cz - foz, c);
         float cmin = c[0], cmax = c[0];
 #pragma unroll
         for (int q = 1; q < 8; q++) {
@@ -338,18 +340,62 @@ __device__ void walk_bracketing_cells(const Field &field, int fox, int foy, int 
             if (c[q] > cmax) cmax = c[q];
         }
         if ((double)cmin <= iso && iso <= (double)cmax) on_cell(cx, cy, cz, seq++);
+        const int lx = cx - fox, ly = cy - foy, lz = cz - foz;
         if (tmx <= tmy && tmx <= tmz) {
             cx += sx;
             tmx += del_x;
             if (cx < lo_x || cx >= lo_x + n_x) return;
+            // corner bit 0 is x: keep the shared face, load the new one
+            // (compile-time corner indices: c[] stays in registers)
+            if (sx > 0) {
+#pragma unroll
+                for (int q = 0; q < 8; q += 2) {
+                    c[q] = c[q + 1];
+                    c[q + 1] = field.point(lx + 2, ly + ((q >> 1) & 1), lz + (q >> 2));
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; q += 2) {
+                    c[q + 1] = c[q];
+                    c[q] = field.point(lx - 1, ly + ((q >> 1) & 1), lz + (q >> 2));
+                }
+            }
         } else if (tmy <= tmz) {
             cy += sy;
             tmy += del_y;
             if (cy < lo_y || cy >= lo_y + n_y) return;
+            if (sy > 0) {
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    if (q & 2) continue;  // the corners with y bit 0
+                    c[q] = c[q + 2];
+                    c[q + 2] = field.point(lx + (q & 1), ly + 2, lz + (q >> 2));
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    if (q & 2) continue;
+                    c[q + 2] = c[q];
+                    c[q] = field.point(lx + (q & 1), ly - 1, lz + (q >> 2));
+                }
+            }
         } else {
             cz += sz;
             tmz += del_z;
             if (cz < lo_z || cz >= lo_z + n_z) return;
+            if (sz > 0) {
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    c[q] = c[q + 4];
+                    c[q + 4] = field.point(lx + (q & 1), ly + (q >> 1), lz + 2);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    c[q + 4] = c[q];
+                    c[q] = field.point(lx + (q & 1), ly + (q >> 1), lz - 1);
+                }
+            }
         }
     }
 }
