@@ -176,6 +176,7 @@ int wc_volume_set_grids(wc_volume *v, const double *fine_min, const double *fine
     upload(V.fine_mm, f.data(), V.n_blocks, V.st);
     upload(V.coarse_mm, c.data(), V.n_coarse, V.st);
     WC_CUDA(cudaStreamSynchronize(V.st));
+    V.build_range_index();
     WC_API_END
 }
 

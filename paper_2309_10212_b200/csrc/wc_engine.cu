@@ -721,6 +721,29 @@ __global__ void k_iso_bitmap(const double2 *__restrict__ mm, int64_t n, double i
     }
 }
 
+// Same bitmap from the 16-bit screening copy (Volume::fine_q): a bound in a
+// different bucket than iso decides its comparison; a shared bucket re-reads
+// the exact float64 bound.  Reads 4 B per block instead of 16.
+__global__ void k_iso_bitmap_q(const ushort2 *__restrict__ q, const double2 *__restrict__ mm, int64_t n, double iso,
+                               double base, double inv, uint32_t *__restrict__ bm) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwords = (n + 31) >> 5;
+    const bool iso_nan = iso != iso;
+    const uint32_t qi = iso_nan ? 0u : range_q(iso, base, inv);
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t c = w * 32 + lane;
+        bool in = false;
+        if (c < n && !iso_nan) {
+            const ushort2 v = q[c];
+            const bool lo_ok = qi != v.x ? qi > v.x : mm[c].x <= iso;
+            in = lo_ok && (qi != v.y ? qi < v.y : iso <= mm[c].y);
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, in);
+        if (lane == 0) bm[w] = word;
+    }
+}
+
 // ------------------------------------------------------------------ marking
 
 // engine.py:107-117: each visible block activates itself and its existing
@@ -1274,7 +1297,8 @@ void Session::reset(const CameraParams *cam, double iso_) {
         eye[2] = cam->eye[2];
     }
     WC_CUDA(cudaEventRecord(ev_frame0, st));
-    k_iso_bitmap<<<grid_for(vol->n_blocks, 256, 8), 256, 0, st>>>(vol->fine_mm.p, vol->n_blocks, iso, fine_bm.p);
+    k_iso_bitmap_q<<<grid_for(vol->n_blocks, 256, 8), 256, 0, st>>>(vol->fine_q.p, vol->fine_mm.p, vol->n_blocks,
+                                                                     iso, vol->q_base, vol->q_inv, fine_bm.p);
     WC_LAUNCH_CHECK();
     k_iso_bitmap<<<grid_for(vol->n_coarse, 256, 8), 256, 0, st>>>(vol->coarse_mm.p, vol->n_coarse, iso, coarse_bm.p);
     WC_LAUNCH_CHECK();

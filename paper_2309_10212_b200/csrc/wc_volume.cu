@@ -1,6 +1,8 @@
 // wc_volume.cu -- block codec (decode + encode) and grid construction.
 #include <math_constants.h>
 
+#include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "wc_volume.cuh"
@@ -255,6 +257,79 @@ void Volume::build_grids() {
     k_group4<<<grid_for(n_coarse, 256), 256, 0, st>>>(wmm.p, bdx, bdy, bdz, cdx, cdy, cdz, cmm.p);
     WC_LAUNCH_CHECK();
     k_octant_union<<<grid_for(n_coarse, 256), 256, 0, st>>>(cmm.p, cdx, cdy, cdz, coarse_mm.p);
+    WC_LAUNCH_CHECK();
+    WC_CUDA(cudaStreamSynchronize(st));
+    build_range_index();
+}
+
+// ------------------------------------------------------------- range index
+
+// order-preserving uint64 key of a double (for atomicMin/Max)
+__device__ __forceinline__ unsigned long long dkey(double d) {
+    const long long b = __double_as_longlong(d);
+    return b < 0 ? ~(unsigned long long)b : ((unsigned long long)b | 0x8000000000000000ull);
+}
+static double dkey_inv(unsigned long long k) {
+    const unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    double d;
+    memcpy(&d, &b, 8);
+    return d;
+}
+
+// min of the finite fine minima, max of the finite fine maxima
+__global__ void k_range_extent(const double2 *mm, int64_t n, unsigned long long *ext) {
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+        const double2 v = mm[b];
+        if (isfinite(v.x)) lo = min(lo, dkey(v.x));
+        if (isfinite(v.y)) hi = max(hi, dkey(v.y));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(ext, lo);
+        atomicMax(ext + 1, hi);
+    }
+}
+
+__global__ void k_range_quantize(const double2 *mm, int64_t n, double base, double inv, ushort2 *q) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+        const double2 v = mm[b];
+        // a NaN bound never passes the iso test: (65535, 0) sends every iso
+        // either to a proven "out" or to the exact re-test
+        if (v.x != v.x || v.y != v.y)
+            q[b] = make_ushort2(65535, 0);
+        else
+            q[b] = make_ushort2((unsigned short)range_q(v.x, base, inv), (unsigned short)range_q(v.y, base, inv));
+    }
+}
+
+void Volume::build_range_index() {
+    if (n_blocks <= 0) return;
+    DevBuf<unsigned long long> ext;
+    ext.alloc(2);
+    const unsigned long long init[2] = {~0ull, 0ull};
+    WC_CUDA(cudaMemcpyAsync(ext.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    k_range_extent<<<grid_for(n_blocks, 256, 4), 256, 0, st>>>(fine_mm.p, n_blocks, ext.p);
+    WC_LAUNCH_CHECK();
+    unsigned long long h[2];
+    WC_CUDA(cudaMemcpyAsync(h, ext.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    WC_CUDA(cudaStreamSynchronize(st));
+    double lo = 0.0, hi = 1.0;
+    if (h[0] != ~0ull && h[1] != 0ull) {
+        lo = dkey_inv(h[0]);
+        hi = dkey_inv(h[1]);
+    }
+    const double span = hi - lo;
+    q_base = lo;
+    // any positive finite inv keeps the test exact; a useful one spreads
+    // the finite bounds over the 16-bit range
+    q_inv = (span > 0.0 && std::isfinite(65535.0 / span)) ? 65535.0 / span : 1.0;
+    fine_q.alloc(n_blocks);
+    k_range_quantize<<<grid_for(n_blocks, 256, 4), 256, 0, st>>>(fine_mm.p, n_blocks, q_base, q_inv, fine_q.p);
     WC_LAUNCH_CHECK();
     WC_CUDA(cudaStreamSynchronize(st));
 }

@@ -103,6 +103,19 @@ def test_render_lockstep_vs_oracle(wc, scene):
              cache_capacity=cache)
 
 
+@pytest.mark.parametrize("bound", ["fine_min", "fine_max"])
+def test_iso_on_a_grid_bound(wc, bound):
+    # iso exactly equal to a float64 grid bound: the 16-bit screening bitmap
+    # (Volume::fine_q) must fall through to the exact test for that block
+    vol = host_volume("value_noise", 40, seed=5)
+    cv = wc.compress_volume(vol, 12)
+    g = wc.build_grids(cv)
+    vals = np.sort(getattr(g, bound)[np.isfinite(getattr(g, bound))])
+    iso = float(vals[len(vals) // 2])
+    ov = oracle_volume(cv)
+    lockstep(wc, cv, ov, orbit(cv.dims, 0.2), 64, 48, iso, speculation=True, max_spec=64, cache_capacity=None)
+
+
 def test_render_api_matches_generator(wc):
     vol = host_volume("value_noise", 64)
     cv = wc.compress_volume(vol, 16)
