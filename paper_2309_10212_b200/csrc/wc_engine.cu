@@ -29,9 +29,6 @@
 #ifndef WC_WARP_TRAVERSE_MAX
 #define WC_WARP_TRAVERSE_MAX 16384
 #endif
-#ifndef WC_TRAVERSE_LOOKAHEAD
-#define WC_TRAVERSE_LOOKAHEAD 0
-#endif
 #ifndef WC_RAYTRACE_MIN_CTAS
 #define WC_RAYTRACE_MIN_CTAS 4
 #endif
@@ -241,7 +238,8 @@ struct TraverseArgs {
     const uint32_t *act_list;
     int64_t n_act;
     int n_spec;
-    const uint32_t *fine_bm, *coarse_bm;  // per-iso range-test bitmaps (k_iso_bitmap)
+    const uint32_t *coarse_bm;                // per-iso coarse range-test bitmap (k_iso_bitmap)
+    const unsigned long long *cell_mask;  // per-iso fine tests, one word per coarse cell (k_iso_cell_mask)
     int fdx, fdy, fdz, cdx, cdy, cdz;
     double iso;
     uint32_t *block_slots, *ray_slots, *emitted, *vis_bm;
@@ -284,22 +282,29 @@ __device__ __forceinline__ double dda_step(Dda &s, int sx, int sy, int sz, doubl
     return t;
 }
 
-constexpr int kFineRun = 10;   // a monotone ray visits at most 4+4+4-2 fine cells of one coarse cell
-constexpr int kCoarseAhead = 8;
+constexpr int kFineRun = 10;  // a monotone ray visits at most 4+4+4-2 fine cells of one coarse cell
+#ifndef WC_COARSE_AHEAD
+#define WC_COARSE_AHEAD 2
+#endif
+
+// bit of fine cell f in its coarse cell's iso mask (k_iso_cell_mask)
+__device__ __forceinline__ int fine_local(const Dda &f) { return (f.cx & 3) + 4 * (f.cy & 3) + 16 * (f.cz & 3); }
 
 // traversal.py:217-403 _traverse_kernel, restructured for latency on B200:
 //  * persistent: a lane that finishes its ray fetches the next active ray
 //    from a warp-aggregated work counter, so divergent per-ray step counts do
 //    not idle the warp;
-//  * look-ahead: the DDA itself never depends on the grid values, so a
-//    whole fine run (until the ray leaves its coarse cell) or kCoarseAhead
-//    coarse steps are first simulated arithmetically, their range bits
-//    fetched with independent loads from the L2-resident per-iso bitmaps, and
-//    only then consumed in the reference's order; the iterator state at the
-//    exact stop point (n_spec-th emit, descent, exit) is recovered by
-//    replaying the arithmetic.  Every emitted slot, saved iterator and exit
-//    flag is the reference's, bit for bit.
-template <bool LOOKAHEAD>
+//  * one L2 round trip per coarse cell: a coarse step loads the coarse range
+//    bit and the 64-bit fine mask of the cell together; the fine run inside
+//    the cell (<= 10 cells) then walks from registers.  Every iteration is
+//    "coarse step (if not inside a run), then the rest of the run", so lanes
+//    stay converged;
+//  * CA > 1: CA coarse steps are simulated arithmetically first (the DDA
+//    never depends on grid values) and their range bits fetched with
+//    independent loads, then consumed in the reference's order.
+// Every emitted slot, saved iterator and exit flag is the reference's, bit
+// for bit.
+template <int CA>
 __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(TraverseArgs a) {
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
@@ -311,6 +316,7 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
     int sx = 0, sy = 0, sz = 0, emitted = 0;
     Dda f{0, 0, 0, 0, 0, 0}, c{0, 0, 0, 0, 0, 0};
     bool in_fine_run = false;
+    unsigned long long fm = 0;  // iso mask of the fine cells of coarse cell c
     int64_t base = 0;
     for (;;) {
         if (!exhausted) {  // refill idle lanes (warp-uniform branch)
@@ -353,6 +359,7 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
                         f.cx = (int)(fc % (uint32_t)fdx);
                         f.cy = (int)((fc / (uint32_t)fdx) % (uint32_t)fdy);
                         f.cz = (int)(fc / ((uint32_t)fdx * (uint32_t)fdy));
+                        fm = __ldg(a.cell_mask + cc);
                     }
                     f.tx = a.fine_tmax[3 * (int64_t)r];
                     f.ty = a.fine_tmax[3 * (int64_t)r + 1];
@@ -385,111 +392,80 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
                             : (dz < 0.0 ? ((double)f.cz * 4.0 - oz) / dz : CUDART_INF);
             in_fine_run = true;
         };
-        if (!LOOKAHEAD && in_fine_run) {  // one fine step (traversal.py:295-331)
-            const uint32_t f_lin = (uint32_t)(f.cx + fdx * (f.cy + fdy * f.cz));
-            if ((__ldg(a.fine_bm + (f_lin >> 5)) >> (f_lin & 31)) & 1u) {
-                a.block_slots[base + emitted] = f_lin;
-                a.ray_slots[base + emitted] = r;
-                emitted++;
-                mark_visible(a.vis_bm, f_lin);
-            }
-            const double t = dda_step(f, sx, sy, sz, fdel_x, fdel_y, fdel_z);
-            if (t > te || f.cx < 0 || f.cx >= fdx || f.cy < 0 || f.cy >= fdy || f.cz < 0 || f.cz >= fdz) {
-                in_fine_run = false;
-                ray_done = true;
-            } else if ((f.cx >> 2) != c.cx || (f.cy >> 2) != c.cy || (f.cz >> 2) != c.cz) {
-                in_fine_run = false;
-            }
-            finished = emitted == a.n_spec || ray_done;
-        } else if (!LOOKAHEAD) {  // one coarse step (traversal.py:332-386)
-            const double t = dda_step(c, sx, sy, sz, cdel_x, cdel_y, cdel_z);
-            if (t > te || c.cx < 0 || c.cx >= cdx || c.cy < 0 || c.cy >= cdy || c.cz < 0 || c.cz >= cdz) {
-                ray_done = true;
-                finished = true;
-            } else {
-                const uint32_t c_lin = (uint32_t)(c.cx + cdx * (c.cy + cdy * c.cz));
-                if ((__ldg(a.coarse_bm + (c_lin >> 5)) >> (c_lin & 31)) & 1u) descend(t);
-            }
-        } else if (in_fine_run) {
-            // ---- one fine run: simulate, fetch all range bits, consume
-            Dda g = f;
-            uint32_t cell[kFineRun];
-            int K = 0, term = 0;  // term: 0 run continues, 1 left the coarse cell, 2 left the ray
-#pragma unroll
-            for (int k = 0; k < kFineRun; k++) {
-                if (term == 0) {
-                    cell[k] = (uint32_t)(g.cx + fdx * (g.cy + fdy * g.cz));
-                    K = k + 1;
-                    const double t = dda_step(g, sx, sy, sz, fdel_x, fdel_y, fdel_z);
-                    if (t > te || g.cx < 0 || g.cx >= fdx || g.cy < 0 || g.cy >= fdy || g.cz < 0 || g.cz >= fdz)
-                        term = 2;
-                    else if ((g.cx >> 2) != c.cx || (g.cy >> 2) != c.cy || (g.cz >> 2) != c.cz)
-                        term = 1;
-                }
-            }
-            uint32_t bits = 0;
-#pragma unroll
-            for (int k = 0; k < kFineRun; k++)
-                if (k < K) bits |= ((__ldg(a.fine_bm + (cell[k] >> 5)) >> (cell[k] & 31)) & 1u) << k;
-            int m = -1;  // cell at which the n_spec-th block is emitted
-#pragma unroll
-            for (int k = 0; k < kFineRun; k++) {
-                if (m < 0 && k < K && ((bits >> k) & 1u)) {
-                    a.block_slots[base + emitted] = cell[k];
-                    a.ray_slots[base + emitted] = r;
-                    emitted++;
-                    mark_visible(a.vis_bm, cell[k]);
-                    if (emitted == a.n_spec) m = k;
-                }
-            }
-            if (m >= 0 && m < K - 1) {  // stopped inside the run: state after m+1 steps
-                for (int k = 0; k <= m; k++) dda_step(f, sx, sy, sz, fdel_x, fdel_y, fdel_z);
-                finished = true;
-            } else {
-                f = g;
-                if (term == 2) {
-                    in_fine_run = false;
+        if (!in_fine_run) {
+            if (CA == 1) {  // one coarse step (traversal.py:332-386)
+                const double t = dda_step(c, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+                if (t > te || c.cx < 0 || c.cx >= cdx || c.cy < 0 || c.cy >= cdy || c.cz < 0 || c.cz >= cdz) {
                     ray_done = true;
                     finished = true;
                 } else {
-                    if (term == 1) in_fine_run = false;
-                    finished = emitted == a.n_spec;
+                    const uint32_t c_lin = (uint32_t)(c.cx + cdx * (c.cy + cdy * c.cz));
+                    const uint32_t cw = __ldg(a.coarse_bm + (c_lin >> 5));
+                    const unsigned long long m = __ldg(a.cell_mask + c_lin);  // same round trip
+                    if ((cw >> (c_lin & 31)) & 1u) {
+                        descend(t);
+                        fm = m;
+                    }
                 }
-            }
-        } else {
-            // ---- coarse steps: simulate kCoarseAhead, fetch their bits, descend at the first hit
-            Dda g = c;
-            uint32_t cell[kCoarseAhead];
-            int J = 0;
-            bool done = false;
+            } else {  // CA coarse steps: simulate, fetch all range bits, descend at the first hit
+                Dda g = c;
+                uint32_t cell[CA];
+                int J = 0;
+                bool done = false;
 #pragma unroll
-            for (int j = 0; j < kCoarseAhead; j++) {
-                if (!done) {
-                    const double t = dda_step(g, sx, sy, sz, cdel_x, cdel_y, cdel_z);
-                    if (t > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 || g.cz >= cdz) {
-                        done = true;
-                    } else {
-                        cell[j] = (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz));
-                        J = j + 1;
+                for (int j = 0; j < CA; j++) {
+                    if (!done) {
+                        const double t = dda_step(g, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+                        if (t > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 ||
+                            g.cz >= cdz) {
+                            done = true;
+                        } else {
+                            cell[j] = (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz));
+                            J = j + 1;
+                        }
+                    }
+                }
+                uint32_t bits = 0;
+#pragma unroll
+                for (int j = 0; j < CA; j++)
+                    if (j < J) bits |= ((__ldg(a.coarse_bm + (cell[j] >> 5)) >> (cell[j] & 31)) & 1u) << j;
+                if (bits) {
+                    const int js = __ffs(bits) - 1;
+                    double t_cross = 0.0;
+                    for (int j = 0; j <= js; j++) t_cross = dda_step(c, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+                    descend(t_cross);
+                    fm = __ldg(a.cell_mask + (c.cx + cdx * (c.cy + cdy * c.cz)));
+                } else {
+                    c = g;  // includes the exiting step when done (traversal.py:333-355)
+                    if (done) {
+                        ray_done = true;
+                        finished = true;
                     }
                 }
             }
-            uint32_t bits = 0;
-#pragma unroll
-            for (int j = 0; j < kCoarseAhead; j++)
-                if (j < J) bits |= ((__ldg(a.coarse_bm + (cell[j] >> 5)) >> (cell[j] & 31)) & 1u) << j;
-            if (bits) {  // descend at the first coarse cell holding the iso
-                const int js = __ffs(bits) - 1;
-                double t_cross = 0.0;
-                for (int j = 0; j <= js; j++) t_cross = dda_step(c, sx, sy, sz, cdel_x, cdel_y, cdel_z);
-                descend(t_cross);
-            } else {
-                c = g;  // includes the exiting step when done (traversal.py:333-355)
-                if (done) {
-                    ray_done = true;
-                    finished = true;
+        }
+        if (in_fine_run) {  // the rest of the run, from the register mask (traversal.py:295-331)
+            for (int k = 0; k < kFineRun; k++) {
+                if ((fm >> fine_local(f)) & 1ull) {
+                    const uint32_t f_lin = (uint32_t)(f.cx + fdx * (f.cy + fdy * f.cz));
+                    a.block_slots[base + emitted] = f_lin;
+                    a.ray_slots[base + emitted] = r;
+                    emitted++;
+                    mark_visible(a.vis_bm, f_lin);
                 }
+                const double t = dda_step(f, sx, sy, sz, fdel_x, fdel_y, fdel_z);
+                if (t > te || f.cx < 0 || f.cx >= fdx || f.cy < 0 || f.cy >= fdy || f.cz < 0 || f.cz >= fdz) {
+                    in_fine_run = false;
+                    ray_done = true;
+                    break;
+                }
+                if ((f.cx >> 2) != c.cx || (f.cy >> 2) != c.cy || (f.cz >> 2) != c.cz) {
+                    in_fine_run = false;
+                    break;
+                }
+                if (emitted == a.n_spec) break;
             }
+            finished = emitted == a.n_spec || ray_done;
         }
         if (finished) {  // save the iterator past the last emit (traversal.py:388-403)
             for (int k = emitted; k < a.n_spec; k++) {  // traversal.py:423-424 sentinels
@@ -576,6 +552,7 @@ __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a) {
         f.tx = a.fine_tmax[3 * (int64_t)r];
         f.ty = a.fine_tmax[3 * (int64_t)r + 1];
         f.tz = a.fine_tmax[3 * (int64_t)r + 2];
+        unsigned long long fm = in_fine_run ? __ldg(a.cell_mask + cc) : 0ull;  // warp-uniform
         const int64_t base = i * (int64_t)a.n_spec;
         int emitted = 0;
         bool ray_done = false, finished = false;
@@ -601,7 +578,7 @@ __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a) {
                     else if ((h.cx >> 2) != c.cx || (h.cy >> 2) != c.cy || (h.cz >> 2) != c.cz)
                         term = 1;
                 }
-                const bool bit = valid && ((__ldg(a.fine_bm + (cell >> 5)) >> (cell & 31)) & 1u);
+                const bool bit = valid && ((fm >> fine_local(g)) & 1ull);
                 const uint32_t tmask = __ballot_sync(0xffffffffu, valid && term != 0);
                 // last cell of the run in this batch (a run has <= 10 cells, so a
                 // termination is always found; kFineRun keeps the bound explicit)
@@ -667,6 +644,7 @@ __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a) {
                     f.tz = dz > 0.0 ? ((double)(f.cz + 1) * 4.0 - oz) / dz
                                     : (dz < 0.0 ? ((double)f.cz * 4.0 - oz) / dz : CUDART_INF);
                     in_fine_run = true;
+                    fm = __ldg(a.cell_mask + (c.cx + cdx * (c.cy + cdy * c.cz)));
                 } else if (first_term < 32) {  // left the volume / passed t_exit
                     c = shfl_dda(g, first_term);
                     ray_done = true;
@@ -724,23 +702,49 @@ __global__ void k_iso_bitmap(const double2 *__restrict__ mm, int64_t n, double i
 // Same bitmap from the 16-bit screening copy (Volume::fine_q): a bound in a
 // different bucket than iso decides its comparison; a shared bucket re-reads
 // the exact float64 bound.  Reads 4 B per block instead of 16.
-__global__ void k_iso_bitmap_q(const ushort2 *__restrict__ q, const double2 *__restrict__ mm, int64_t n, double iso,
-                               double base, double inv, uint32_t *__restrict__ bm) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nwords = (n + 31) >> 5;
+//
+// Laid out per coarse cell: cell_mask[c] bit (fx&3) + 4*(fy&3) + 16*(fz&3)
+// is the test of fine cell f inside coarse cell c (fine cells past the grid
+// edge read 0).  A ray descending into c loads this one word and walks its
+// whole fine run (<= 10 cells) from registers.
+__device__ __forceinline__ bool iso_in_q(const ushort2 v, uint32_t qi, const double2 *mm, int64_t b, double iso) {
+    const bool lo_ok = qi != v.x ? qi > v.x : mm[b].x <= iso;
+    return lo_ok && (qi != v.y ? qi < v.y : iso <= mm[b].y);
+}
+
+__global__ void k_iso_cell_mask(const ushort2 *__restrict__ q, const double2 *__restrict__ mm, int fdx, int fdy,
+                                int fdz, int cdx, int cdy, int cdz, double iso, double base, double inv,
+                                unsigned long long *__restrict__ cell_mask) {
+    const int64_t n_coarse = (int64_t)cdx * cdy * cdz;
     const bool iso_nan = iso != iso;
     const uint32_t qi = iso_nan ? 0u : range_q(iso, base, inv);
-    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords;
-         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int64_t c = w * 32 + lane;
-        bool in = false;
-        if (c < n && !iso_nan) {
-            const ushort2 v = q[c];
-            const bool lo_ok = qi != v.x ? qi > v.x : mm[c].x <= iso;
-            in = lo_ok && (qi != v.y ? qi < v.y : iso <= mm[c].y);
+    const bool vec = (fdx & 3) == 0;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_coarse;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int cx = (int)(c % cdx), cy = (int)((c / cdx) % cdy), cz = (int)(c / ((int64_t)cdx * cdy));
+        unsigned long long m = 0;
+        if (!iso_nan) {
+            for (int k = 0; k < 16; k++) {
+                const int fy = 4 * cy + (k & 3), fz = 4 * cz + (k >> 2);
+                if (fy >= fdy || fz >= fdz) continue;
+                const int64_t row = 4 * (int64_t)cx + (int64_t)fdx * (fy + (int64_t)fdy * fz);
+                ushort2 v[4];
+                if (vec) {
+                    const uint4 w = __ldg(reinterpret_cast<const uint4 *>(q + row));
+                    v[0] = *reinterpret_cast<const ushort2 *>(&w.x);
+                    v[1] = *reinterpret_cast<const ushort2 *>(&w.y);
+                    v[2] = *reinterpret_cast<const ushort2 *>(&w.z);
+                    v[3] = *reinterpret_cast<const ushort2 *>(&w.w);
+                } else {
+#pragma unroll
+                    for (int x = 0; x < 4; x++) v[x] = 4 * cx + x < fdx ? q[row + x] : make_ushort2(65535, 0);
+                }
+#pragma unroll
+                for (int x = 0; x < 4; x++)
+                    if (4 * cx + x < fdx && iso_in_q(v[x], qi, mm, row + x, iso)) m |= 1ull << (x + 4 * k);
+            }
         }
-        const uint32_t word = __ballot_sync(0xffffffffu, in);
-        if (lane == 0) bm[w] = word;
+        cell_mask[c] = m;
     }
 }
 
@@ -1255,7 +1259,7 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     const int64_t nwords = ceil_div(vol->n_blocks, 32);
     vis_bm.alloc(nwords);
     act_bm.alloc(nwords);
-    fine_bm.alloc(nwords);
+    cell_mask.alloc(vol->n_coarse);
     coarse_bm.alloc(ceil_div(vol->n_coarse, 32));
     vis_word_off.alloc(nwords);
     act_word_off.alloc(nwords);
@@ -1297,8 +1301,9 @@ void Session::reset(const CameraParams *cam, double iso_) {
         eye[2] = cam->eye[2];
     }
     WC_CUDA(cudaEventRecord(ev_frame0, st));
-    k_iso_bitmap_q<<<grid_for(vol->n_blocks, 256, 8), 256, 0, st>>>(vol->fine_q.p, vol->fine_mm.p, vol->n_blocks,
-                                                                     iso, vol->q_base, vol->q_inv, fine_bm.p);
+    k_iso_cell_mask<<<grid_for(vol->n_coarse, 128, 16), 128, 0, st>>>(
+        vol->fine_q.p, vol->fine_mm.p, vol->bdx, vol->bdy, vol->bdz, vol->cdx, vol->cdy, vol->cdz, iso, vol->q_base,
+        vol->q_inv, cell_mask.p);
     WC_LAUNCH_CHECK();
     k_iso_bitmap<<<grid_for(vol->n_coarse, 256, 8), 256, 0, st>>>(vol->coarse_mm.p, vol->n_coarse, iso, coarse_bm.p);
     WC_LAUNCH_CHECK();
@@ -1516,7 +1521,7 @@ bool Session::pass(PassStatsC &stats) {
     ta.act_list = alist;
     ta.n_act = n_act;
     ta.n_spec = (int)n_spec;
-    ta.fine_bm = fine_bm.p;
+    ta.cell_mask = cell_mask.p;
     ta.coarse_bm = coarse_bm.p;
     ta.fdx = vol->bdx;
     ta.fdy = vol->bdy;
@@ -1533,10 +1538,8 @@ bool Session::pass(PassStatsC &stats) {
     WC_CUDA(cudaMemsetAsync(ta.work, 0, 4, st));
     if (n_act <= WC_WARP_TRAVERSE_MAX)  // few (long) rays: warp-cooperative DDA per ray
         k_traverse_warp<<<grid_for(n_act * 32, 128, 16), 128, 0, st>>>(ta);
-    else if (WC_TRAVERSE_LOOKAHEAD)
-        k_traverse<true><<<grid_for(n_act, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st>>>(ta);
     else
-        k_traverse<false><<<grid_for(n_act, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st>>>(ta);
+        k_traverse<WC_COARSE_AHEAD><<<grid_for(n_act, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st>>>(ta);
     WC_LAUNCH_CHECK();
     WC_CUDA(cudaEventRecord(ev_stage[1], st));
     // entry compaction: exclusive scan of per-ray emitted counts

@@ -72,7 +72,8 @@ struct Session {
     DevBuf<uint32_t> item_j, item_cell, best;  // two-phase raytrace work list
     DevBuf<double> item_t;
     DevBuf<uint32_t> vis_bm, act_bm, vis_word_off, act_word_off;
-    DevBuf<uint32_t> fine_bm, coarse_bm;  // per-iso range-test bitmaps, rebuilt at every reset
+    DevBuf<uint32_t> coarse_bm;            // per-iso coarse range-test bitmap, rebuilt at every reset
+    DevBuf<unsigned long long> cell_mask;  // per-iso fine range tests, 64 per coarse cell
     DevBuf<uint32_t> visible_ids, block_ray_off, active_ids;
     DevBuf<uint32_t> rgba;
     DevBuf<float> depth;
