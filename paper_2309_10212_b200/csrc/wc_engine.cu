@@ -556,6 +556,15 @@ __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a) {
         const int64_t base = i * (int64_t)a.n_spec;
         int emitted = 0;
         bool ray_done = false, finished = false;
+        // coarse chunk: lane k holds the state after step k+1 from the chunk
+        // start.  The coarse walk never depends on the fine runs, so a chunk
+        // interrupted by a descent resumes at step p after the run.
+        bool chunk_ok = false;
+        int p = 0;
+        uint32_t B = 0, T = 0;
+        Dda g;
+        double tk = 0.0;
+        unsigned long long mk = 0;
         while (!finished) {
             if (in_fine_run) {
                 // lane k: cell X_k of the run (k steps from f), and the step that leaves it
@@ -609,24 +618,31 @@ __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a) {
                 }
                 finished = emitted == a.n_spec || ray_done;
             } else {
-                // lane k: the (k+1)-th coarse step from c
-                Dda g = c;
-                bool valid = true, term_here = false;
-                double t = 0.0;
-                for (int j = 0; j <= lane && valid; j++) {
-                    t = dda_step(g, sx, sy, sz, cdel_x, cdel_y, cdel_z);
-                    if (t > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 || g.cz >= cdz) {
-                        valid = false;
-                        term_here = j == lane;
+                if (!chunk_ok) {  // lane k: the (k+1)-th coarse step from c, its range bit and fine mask
+                    g = c;
+                    bool valid = true, term_here = false;
+                    for (int j = 0; j <= lane && valid; j++) {
+                        tk = dda_step(g, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+                        if (tk > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 || g.cz >= cdz) {
+                            valid = false;
+                            term_here = j == lane;
+                        }
                     }
+                    const uint32_t cell = valid ? (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz)) : 0u;
+                    const uint32_t cw = valid ? __ldg(a.coarse_bm + (cell >> 5)) : 0u;
+                    mk = valid ? __ldg(a.cell_mask + cell) : 0ull;  // same round trip as the bit
+                    B = __ballot_sync(0xffffffffu, (cw >> (cell & 31)) & 1u);
+                    T = __ballot_sync(0xffffffffu, term_here);
+                    p = 0;
+                    chunk_ok = true;
                 }
-                const uint32_t cell = valid ? (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz)) : 0u;
-                const bool bit = valid && ((__ldg(a.coarse_bm + (cell >> 5)) >> (cell & 31)) & 1u);
-                const uint32_t B = __ballot_sync(0xffffffffu, bit), T = __ballot_sync(0xffffffffu, term_here);
-                const int first_term = T ? __ffs(T) - 1 : 32, first_hit = B ? __ffs(B) - 1 : 32;
+                const uint32_t rem = p >= 32 ? 0u : ~((1u << p) - 1u);
+                const int first_term = (T & rem) ? __ffs(T & rem) - 1 : 32;
+                const int first_hit = (B & rem) ? __ffs(B & rem) - 1 : 32;
                 if (first_hit < first_term) {  // descend (traversal.py:357-386)
                     c = shfl_dda(g, first_hit);
-                    const double t_cross = __shfl_sync(0xffffffffu, t, first_hit);
+                    const double t_cross = __shfl_sync(0xffffffffu, tk, first_hit);
+                    fm = __shfl_sync(0xffffffffu, mk, first_hit);
                     const double px = ox + dx * t_cross, py = oy + dy * t_cross, pz = oz + dz * t_cross;
                     const int lo_x = 4 * c.cx, lo_y = 4 * c.cy, lo_z = 4 * c.cz;
                     const int hi_x = min(lo_x + 3, fdx - 1), hi_y = min(lo_y + 3, fdy - 1),
@@ -644,13 +660,14 @@ __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a) {
                     f.tz = dz > 0.0 ? ((double)(f.cz + 1) * 4.0 - oz) / dz
                                     : (dz < 0.0 ? ((double)f.cz * 4.0 - oz) / dz : CUDART_INF);
                     in_fine_run = true;
-                    fm = __ldg(a.cell_mask + (c.cx + cdx * (c.cy + cdy * c.cz)));
+                    p = first_hit + 1;
                 } else if (first_term < 32) {  // left the volume / passed t_exit
                     c = shfl_dda(g, first_term);
                     ray_done = true;
                     finished = true;
                 } else {
                     c = shfl_dda(g, 31);
+                    chunk_ok = false;
                 }
             }
         }
@@ -772,16 +789,18 @@ __global__ void k_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvi
 __global__ void k_build_entries(int64_t n_act, int n_spec, const uint32_t *act_list, const uint32_t *emitted,
                                 const uint32_t *entry_off, const uint32_t *block_slots, const uint32_t *vis_bm,
                                 const uint32_t *vis_word_off, uint32_t *ent_key, uint32_t *ent_val, uint32_t *ent_ray) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_act; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t ne = emitted[i], eo = entry_off[i], r = act_list[i];
-        for (uint32_t j = 0; j < ne; j++) {
-            const uint32_t b = block_slots[i * (int64_t)n_spec + j];
-            const uint32_t w = b >> 5;
-            const uint32_t rank = vis_word_off[w] + __popc(vis_bm[w] & ((1u << (b & 31)) - 1u));
-            ent_key[eo + j] = rank;
-            ent_val[eo + j] = eo + j;
-            ent_ray[eo + j] = r;
-        }
+    // thread per slot (i, j): no per-ray serial chain of rank lookups
+    const int64_t n_slots = n_act * n_spec;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_slots; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / n_spec;
+        const uint32_t j = (uint32_t)(t - i * n_spec);
+        if (j >= emitted[i]) continue;
+        const uint32_t eo = entry_off[i] + j;
+        const uint32_t b = block_slots[t];
+        const uint32_t w = b >> 5;
+        ent_key[eo] = vis_word_off[w] + __popc(vis_bm[w] & ((1u << (b & 31)) - 1u));
+        ent_val[eo] = eo;
+        ent_ray[eo] = act_list[i];
     }
 }
 
@@ -1152,6 +1171,51 @@ __global__ void k_composite(int64_t n_act, const uint32_t *act_list, const uint3
             kp = 1;
         }
         keep[i] = kp;
+    }
+}
+
+// Same with a warp per ray, for speculative passes (n_spec entries per ray):
+// lexicographic (depth, entry) minimum == the first strict minimum in order.
+__global__ void k_composite_warp(int64_t n_act, const uint32_t *act_list, const uint32_t *emitted,
+                                 const uint32_t *entry_off, const float4 *rgbz, const uint8_t *exited, uint8_t *status,
+                                 uint32_t *rgba, float *depth, uint32_t *keep) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w0; i < n_act; i += nw) {
+        const uint32_t r = act_list[i], ne = emitted[i], eo = entry_off[i];
+        float best = CUDART_INF_F;
+        uint32_t bj = 0xFFFFFFFFu;
+        for (uint32_t j = lane; j < ne; j += 32) {
+            const float z = rgbz[eo + j].w;
+            if (z < best) {
+                best = z;
+                bj = j;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float zb = __shfl_xor_sync(0xffffffffu, best, o);
+            const uint32_t jb = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (zb < best || (zb == best && jb < bj)) {
+                best = zb;
+                bj = jb;
+            }
+        }
+        if (lane == 0) {
+            uint32_t kp = 0;
+            if (bj != 0xFFFFFFFFu) {
+                const float4 c = rgbz[eo + bj];
+                depth[r] = best;
+                rgba[r] = rgb_u8((double)c.x) | (rgb_u8((double)c.y) << 8) | (rgb_u8((double)c.z) << 16) | 0xFF000000u;
+                status[r] = 1;
+            } else if (exited[r] == 1) {
+                status[r] = 2;
+            } else {
+                kp = 1;
+            }
+            keep[i] = kp;
+        }
     }
 }
 
@@ -1550,7 +1614,7 @@ bool Session::pass(PassStatsC &stats) {
                                                                  vol->bdy, vol->bdz, act_bm.p);
     WC_LAUNCH_CHECK();
     bitmap_extract(act_bm.p, nwords, act_word_off.p, active_ids.p, counters.p + C_NACTB, partials.p, st);
-    k_build_entries<<<grid_for(n_act, 256), 256, 0, st>>>(n_act, (int)n_spec, alist, emitted.p, entry_off.p,
+    k_build_entries<<<grid_for(n_act * n_spec, 256), 256, 0, st>>>(n_act, (int)n_spec, alist, emitted.p, entry_off.p,
                                                           block_slots.p, vis_bm.p, vis_word_off.p, ent_key.p,
                                                           ent_val.p, ent_ray.p);
     WC_LAUNCH_CHECK();
@@ -1638,8 +1702,12 @@ bool Session::pass(PassStatsC &stats) {
     }
     WC_CUDA(cudaEventRecord(ev_stage[5], st));
     // composite + compaction of the surviving rays (next pass's O_Act)
-    k_composite<<<grid_for(n_act, 256), 256, 0, st>>>(n_act, alist, emitted.p, entry_off.p, rgbz.p, exited.p,
-                                                      status.p, rgba.p, depth.p, keep.p);
+    if (n_spec >= 8)
+        k_composite_warp<<<grid_for(n_act * 32, 256), 256, 0, st>>>(n_act, alist, emitted.p, entry_off.p, rgbz.p,
+                                                                    exited.p, status.p, rgba.p, depth.p, keep.p);
+    else
+        k_composite<<<grid_for(n_act, 256), 256, 0, st>>>(n_act, alist, emitted.p, entry_off.p, rgbz.p, exited.p,
+                                                          status.p, rgba.p, depth.p, keep.p);
     WC_LAUNCH_CHECK();
     scan_exclusive(LoadU32{keep.p}, n_act, keep_off.p, counters.p + C_NACT, partials.p, st);
     k_compact_keep<<<grid_for(n_act, 256), 256, 0, st>>>(keep.p, keep_off.p, alist, n_act, act_list[cur ^ 1].p);
