@@ -1077,26 +1077,44 @@ __device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, int64_t j) 
 __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
     const RaytraceArgs &a = s.a;
     const int lane = threadIdx.x & 31;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n_ent; j += (int64_t)gridDim.x * blockDim.x) {
-        const EntryCtx e = entry_ctx(a, j);
-        s.best[e.k] = WC_UINT_MAX;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // warp-uniform trip count: the list append below is a full-warp scan
+    for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); j0 < a.n_ent; j0 += stride) {
+        const int64_t j = j0 + lane;
+        // the <= 10 bracketing cells of the walk, 6-bit local codes in DDA order
         int found = 0;
-        walk_bracketing_cells(e.field, 4 * e.bx, 4 * e.by, 4 * e.bz, 4 * e.bx, 4 * e.by, 4 * e.bz, e.cx, e.cy, e.cz,
-                              e.o, e.d, e.te, a.iso, [&](int cx, int cy, int cz, int seq) {
-                                  const uint32_t am = __activemask();
-                                  const int leader = __ffs(am) - 1;
-                                  uint32_t first = 0;
-                                  if (lane == leader) first = atomicAdd(s.n_items, (uint32_t)__popc(am));
-                                  first = __shfl_sync(am, first, leader);
-                                  const uint32_t it = first + __popc(am & ((1u << lane) - 1u));
-                                  if (it < s.item_cap) {
-                                      s.item_j[it] = (uint32_t)j;
-                                      s.item_cell[it] = (uint32_t)((cx - 4 * e.bx) | ((cy - 4 * e.by) << 3) |
-                                                                   ((cz - 4 * e.bz) << 6) | (seq << 9));
-                                  }
-                                  found++;
-                              });
-        if (!found) a.rgbz[e.k] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
+        unsigned long long codes = 0;
+        if (j < a.n_ent) {
+            const EntryCtx e = entry_ctx(a, j);
+            s.best[e.k] = WC_UINT_MAX;
+            walk_bracketing_cells(e.field, 4 * e.bx, 4 * e.by, 4 * e.bz, 4 * e.bx, 4 * e.by, 4 * e.bz, e.cx, e.cy,
+                                  e.cz, e.o, e.d, e.te, a.iso, [&](int cx, int cy, int cz, int seq) {
+                                      const uint32_t lc = (uint32_t)((cx - 4 * e.bx) | ((cy - 4 * e.by) << 2) |
+                                                                     ((cz - 4 * e.bz) << 4));
+                                      codes |= (unsigned long long)lc << (6 * seq);
+                                      found++;
+                                  });
+            if (!found) a.rgbz[e.k] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
+        }
+        // one list append per warp (a per-cell atomic on the shared counter
+        // serialises at L2)
+        uint32_t incl = (uint32_t)found;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        uint32_t first = 0;
+        if (lane == 31 && incl) first = atomicAdd(s.n_items, incl);
+        first = __shfl_sync(0xffffffffu, first, 31) + incl - (uint32_t)found;
+        for (int q = 0; q < found; q++) {
+            const uint32_t it = first + q;
+            if (it < s.item_cap) {
+                const uint32_t lc = (uint32_t)(codes >> (6 * q)) & 63u;
+                s.item_j[it] = (uint32_t)j;
+                s.item_cell[it] = (lc & 3u) | (((lc >> 2) & 3u) << 3) | ((lc >> 4) << 6) | ((uint32_t)q << 9);
+            }
+        }
     }
 }
 
