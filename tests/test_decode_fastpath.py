@@ -3,7 +3,9 @@
 exact while the result stays normal (e in [-100, 127]).  The reference
 computes float32(float64(q)/S * 2^e) (codec.py:168); the kernel uses
 __fdiv_rn((float)q, (float)S) * 2^e on that range and the float64 formula
-elsewhere (qbits 26, extreme exponents)."""
+elsewhere (qbits 26, extreme exponents).  The cache-fill kernel computes the
+same quotient as y0 = q * r, r = RN32(1/S), corrected once with two fmas
+(y0 + fma(-y0, S, q) * r), also checked here for every q in [-S-1, S]."""
 
 import os
 import subprocess
@@ -21,10 +23,13 @@ int main(void) {
     for (int qb = 4; qb <= 25; qb++) {
         const long S = (1L << (qb - 1)) - 1;
         const float sf = (float)S;
-        for (long q = -S; q <= S; q++) {
+        const float r = 1.0f / sf;
+        for (long q = -S - 1; q <= S; q++) {
             const float ref = (float)((double)q / (double)S);
             const float fast = (float)q / sf;
-            if (bits(ref) != bits(fast)) bad++;
+            const float y0 = (float)q * r;
+            const float mul = fmaf(fmaf(-y0, sf, (float)q), r, y0);
+            if (bits(ref) != bits(fast) || bits(ref) != bits(mul)) bad++;
         }
     }
     /* scaling: float32(x * 2^e) == float32(x) * 2^e for normal results */
