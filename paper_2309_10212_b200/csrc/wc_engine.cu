@@ -1574,7 +1574,6 @@ void Session::ensure_resident(int64_t n_actb, int64_t n_miss, int64_t &n_evict) 
     k_decode_insert<<<grid_for(n_miss * 32, 256, 8), 256, 0, st>>>(
         vol->payload.p, vol->qbits, vol->stride, miss_ids.p, counters.p + C_NMISS, hw, n_free, victims,
         slot_values.p, block_of_slot.p, last_used.p, slot_of_block.p, pass_no, counters.p + C_HW, cap);
-}
     WC_LAUNCH_CHECK();
 }
 
