@@ -29,6 +29,9 @@
 #ifndef WC_WARP_TRAVERSE_MAX
 #define WC_WARP_TRAVERSE_MAX 16384
 #endif
+#ifndef WC_EARLY_HIST
+#define WC_EARLY_HIST 1
+#endif
 #ifndef WC_RAYTRACE_MIN_CTAS
 #define WC_RAYTRACE_MIN_CTAS 4
 #endif
@@ -815,7 +818,9 @@ __global__ void k_run_offsets(const uint32_t *key, int64_t n, int64_t nvis, uint
 // ---------------------------------------------------------------- cache
 
 __global__ void k_cache_stamp(const uint32_t *ids, const uint32_t *d_n, int64_t n_max, const int32_t *slot_of_block,
-                              int32_t *last_used, int32_t pass_no) {
+                              int32_t *last_used, int32_t pass_no, uint32_t *hist_zero, int n_zero) {
+    if (blockIdx.x == 0)  // the stamp histogram queued after this kernel accumulates into zeroed bins
+        for (int b = threadIdx.x; b < n_zero; b += blockDim.x) hist_zero[b] = 0;
     const int64_t n = min(n_max, (int64_t)*d_n);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t s = slot_of_block[ids[i]];
@@ -830,9 +835,18 @@ __global__ void k_stamp_hist(const int32_t *block_of_slot, const int32_t *last_u
     extern __shared__ uint32_t sh[];
     for (int b = threadIdx.x; b < pass_no; b += blockDim.x) sh[b] = 0;
     __syncthreads();
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < hw; s += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t lu = last_used[s];
-        if (block_of_slot[s] >= 0 && lu < pass_no) atomicAdd(&sh[lu], 1u);
+    // few distinct stamps: one shared atomic per (warp, stamp) via match_any
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t s0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); s0 < hw; s0 += stride) {
+        const int64_t s = s0 + lane;
+        int32_t key = -1;
+        if (s < hw) {
+            const int32_t lu = last_used[s];
+            if (block_of_slot[s] >= 0 && lu < pass_no) key = lu;
+        }
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        if (key >= 0 && lane == __ffs(peers) - 1) atomicAdd(&sh[key], (uint32_t)__popc(peers));
     }
     __syncthreads();
     for (int b = threadIdx.x; b < pass_no; b += blockDim.x)
@@ -1350,9 +1364,9 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     active_ids.alloc(std::min<int64_t>(8 * n, vol->n_blocks) + 1);
     miss_off.alloc(active_ids.n);
     miss_ids.alloc(active_ids.n);
-    counters.alloc(C_COUNT);
+    counters.alloc(C_COUNT + kHistBins);
     WC_CUDA(cudaMemsetAsync(counters.p, 0, 4 * C_COUNT, st));
-    h_counters.alloc(C_COUNT);
+    h_counters.alloc(C_COUNT + kHistBins);
     partials.alloc(scan_scratch_words(std::max<int64_t>({n, nwords, active_ids.n, 1})));
     WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
 
@@ -1424,6 +1438,7 @@ void Session::reset(const CameraParams *cam, double iso_) {
     WC_CUDA(cudaMemsetAsync(block_of_slot.p, 0xFF, 4 * phys, st));
     WC_CUDA(cudaMemsetAsync(last_used.p, 0, 4 * phys, st));
     pass_no = 0;
+    hist_pass = -1;
     hw = 0;
     pass_index = 0;
     for (double &m : stage_ms) m = 0.0;
@@ -1465,19 +1480,17 @@ void Session::read_counters(int first, int count) {
 // truncated.  Many small buckets fall back to the 2-key stable radix sort.
 void Session::select_victims(int64_t n_cand, int64_t n_evict) {
     const int64_t nb = pass_no;  // stamps are 1..pass_no-1 for candidates
-    stamp_hist.ensure(nb + 1);
-    h_stamp_hist.ensure_host(nb + 1);
-    WC_CUDA(cudaMemsetAsync(stamp_hist.p, 0, 4 * (nb + 1), st));
-    k_stamp_hist<<<grid_for(hw, 256), 256, 4 * (size_t)nb, st>>>(block_of_slot.p, last_used.p, hw, pass_no,
-                                                                 stamp_hist.p);
-    WC_LAUNCH_CHECK();
-    WC_CUDA(cudaMemcpyAsync(h_stamp_hist.p, stamp_hist.p, 4 * (nb + 1), cudaMemcpyDeviceToHost, st));
-    WC_CUDA(cudaStreamSynchronize(st));
+    const uint32_t *hh = h_counters.p + (C_COUNT - C_NENT);  // read with the mid-pass counters
+    if (hist_pass != pass_no) {  // not queued by cache_lookup: build and read it now
+        launch_stamp_hist();
+        WC_CUDA(cudaStreamSynchronize(st));
+        hh = h_stamp_hist.p;
+    }
     int64_t acc = 0;
     int n_buckets = 0;
     int L_star = -1;
     for (int L = 0; L <= nb && acc < n_evict; L++) {
-        const int64_t c = h_stamp_hist.p[L];
+        const int64_t c = hh[L];
         if (!c) continue;
         n_buckets++;
         acc += c;
@@ -1498,7 +1511,7 @@ void Session::select_victims(int64_t n_cand, int64_t n_evict) {
     const int64_t nwords = ceil_div(vol->n_blocks, 32);
     int64_t off = 0;
     for (int L = 0; L <= L_star; L++) {
-        const int64_t c = h_stamp_hist.p[L];
+        const int64_t c = hh[L];
         if (!c) continue;
         k_mark_stamp<<<grid_for(hw, 256), 256, 0, st>>>(block_of_slot.p, last_used.p, hw, L, act_bm.p);
         WC_LAUNCH_CHECK();
@@ -1515,13 +1528,37 @@ void Session::select_victims(int64_t n_cand, int64_t n_evict) {
 // First half of ensure_resident, queued before the pass's one mid-pass host
 // read: stamp the hits and compact the misses of the active blocks whose
 // count is still on the device (cache.py:67-73, :76-78).
+// Histogram of the pass stamps of the resident slots not stamped this pass
+// (the eviction candidates), queued with its read-back to h_stamp_hist.
+void Session::launch_stamp_hist() {
+    const int64_t nb = pass_no;
+    stamp_hist.ensure(nb + 1);
+    h_stamp_hist.ensure_host(nb + 1);
+    WC_CUDA(cudaMemsetAsync(stamp_hist.p, 0, 4 * (nb + 1), st));
+    k_stamp_hist<<<grid_for(hw, 256), 256, 4 * (size_t)nb, st>>>(block_of_slot.p, last_used.p, hw, pass_no,
+                                                                 stamp_hist.p);
+    WC_LAUNCH_CHECK();
+    WC_CUDA(cudaMemcpyAsync(h_stamp_hist.p, stamp_hist.p, 4 * (nb + 1), cudaMemcpyDeviceToHost, st));
+    hist_pass = pass_no;
+}
+
 void Session::cache_lookup() {
     pass_no += 1;
     const int64_t nmax = active_ids.n - 1;  // upper bound of the active-block count
     const uint32_t *d_nactb = counters.p + C_NACTB;
+    // a pass over a non-empty cache may evict: its stamp histogram is built
+    // right after the stamping, in the counter block, so that it arrives
+    // with the mid-pass counter read (no extra host round trip)
+    const bool early = WC_EARLY_HIST && hw > 0 && pass_no + 1 <= kHistBins;
     k_cache_stamp<<<grid_for(nmax, 256), 256, 0, st>>>(active_ids.p, d_nactb, nmax, slot_of_block.p, last_used.p,
-                                                      pass_no);
+                                                      pass_no, counters.p + C_COUNT, early ? pass_no + 1 : 0);
     WC_LAUNCH_CHECK();
+    if (early) {
+        k_stamp_hist<<<grid_for(hw, 256), 256, 4 * (size_t)pass_no, st>>>(block_of_slot.p, last_used.p, hw, pass_no,
+                                                                         counters.p + C_COUNT);
+        WC_LAUNCH_CHECK();
+        hist_pass = pass_no;
+    }
     PredMiss pm{active_ids.p, slot_of_block.p};
     scan_exclusive_dev(pm, d_nactb, nmax, miss_off.p, counters.p + C_NMISS, partials.p, st);
     k_compact_miss<<<grid_for(nmax, 256), 256, 0, st>>>(pm, d_nactb, nmax, miss_off.p, miss_ids.p);
@@ -1640,7 +1677,8 @@ bool Session::pass(PassStatsC &stats) {
     WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
     cache_lookup();  // cache hits stamped, misses compacted, counts still on the device
     WC_CUDA(cudaEventRecord(ev_stage[2], st));
-    read_counters(C_NENT, 4);  // the pass's one mid-pass host read
+    // the pass's one mid-pass host read (+ the stamp histogram when queued)
+    read_counters(C_NENT, hist_pass == pass_no ? C_COUNT - C_NENT + pass_no + 1 : 4);
     const int64_t n_ent = h_counters.p[0], nvis = h_counters.p[1], nactb = h_counters.p[2];
     const int64_t n_miss = h_counters.p[3];
     if (n_ent > n) throw InvariantError("slot budget exceeded");

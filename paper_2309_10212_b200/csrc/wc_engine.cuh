@@ -19,6 +19,8 @@ struct PassStatsC {  // engine.py:66-77 PassStats (+ evicted, n_entries)
     double utilization, completeness, duration;
 };
 
+constexpr int kHistBins = 64;  // stamp histogram bins kept after the counters (passes < 64)
+
 enum Counter : int {
     C_NACT = 0,   // active rays after composite (next pass's n_act)
     C_NENT,       // ray-block entries this pass
@@ -116,9 +118,11 @@ struct Session {
    private:
     void read_counters(int first, int count);
     void cache_lookup();
+    void launch_stamp_hist();
     void ensure_resident(int64_t n_actb, int64_t n_miss, int64_t &n_evict);
     void select_victims(int64_t n_cand, int64_t n_evict);
     DevBuf<uint32_t> stamp_hist;
+    int64_t hist_pass = -1;  // pass whose stamp histogram sits in h_stamp_hist
     PinnedBuf<uint32_t> h_stamp_hist;
 };
 
