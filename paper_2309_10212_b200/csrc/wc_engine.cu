@@ -732,39 +732,58 @@ __device__ __forceinline__ bool iso_in_q(const ushort2 v, uint32_t qi, const dou
     return lo_ok && (qi != v.y ? qi < v.y : iso <= mm[b].y);
 }
 
-__global__ void k_iso_cell_mask(const ushort2 *__restrict__ q, const double2 *__restrict__ mm, int fdx, int fdy,
-                                int fdz, int cdx, int cdy, int cdz, double iso, double base, double inv,
+//
+// Only coarse cells whose own range test passes are filled: the traversal
+// reads a cell's mask only after descending into it (traversal.py:357), so
+// the others are left 0.
+__global__ void k_iso_cell_mask(const ushort2 *__restrict__ q, const double2 *__restrict__ mm,
+                                const uint32_t *__restrict__ coarse_bm, int fdx, int fdy, int fdz, int cdx, int cdy,
+                                int cdz, double iso, double base, double inv,
                                 unsigned long long *__restrict__ cell_mask) {
+    // Streams the bricked screening copy: 16 lanes cover one coarse cell's
+    // 256 B (lane: 4 fine cells = one x-row), 4 cells per lane in flight; the
+    // 16 nibbles of a cell are OR-ed with shuffles.
+    constexpr int kU = 4;
     const int64_t n_coarse = (int64_t)cdx * cdy * cdz;
     const bool iso_nan = iso != iso;
     const uint32_t qi = iso_nan ? 0u : range_q(iso, base, inv);
-    const bool vec = (fdx & 3) == 0;
-    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_coarse;
-         c += (int64_t)gridDim.x * blockDim.x) {
-        const int cx = (int)(c % cdx), cy = (int)((c / cdx) % cdy), cz = (int)(c / ((int64_t)cdx * cdy));
-        unsigned long long m = 0;
-        if (!iso_nan) {
-            for (int k = 0; k < 16; k++) {
-                const int fy = 4 * cy + (k & 3), fz = 4 * cz + (k >> 2);
-                if (fy >= fdy || fz >= fdz) continue;
-                const int64_t row = 4 * (int64_t)cx + (int64_t)fdx * (fy + (int64_t)fdy * fz);
-                ushort2 v[4];
-                if (vec) {
-                    const uint4 w = __ldg(reinterpret_cast<const uint4 *>(q + row));
-                    v[0] = *reinterpret_cast<const ushort2 *>(&w.x);
-                    v[1] = *reinterpret_cast<const ushort2 *>(&w.y);
-                    v[2] = *reinterpret_cast<const ushort2 *>(&w.z);
-                    v[3] = *reinterpret_cast<const ushort2 *>(&w.w);
-                } else {
+    const int lane = threadIdx.x & 31, half = lane >> 4, row = lane & 15;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c0 = w0 * 2 * kU; c0 < n_coarse; c0 += nw * 2 * kU) {
+        uint4 w[kU];
+        bool on[kU];
 #pragma unroll
-                    for (int x = 0; x < 4; x++) v[x] = 4 * cx + x < fdx ? q[row + x] : make_ushort2(65535, 0);
-                }
-#pragma unroll
-                for (int x = 0; x < 4; x++)
-                    if (4 * cx + x < fdx && iso_in_q(v[x], qi, mm, row + x, iso)) m |= 1ull << (x + 4 * k);
-            }
+        for (int u = 0; u < kU; u++) {
+            const int64_t c = c0 + 2 * u + half;
+            on[u] = c < n_coarse && !iso_nan && ((coarse_bm[c >> 5] >> (c & 31)) & 1u);
+            w[u] = on[u] ? __ldg(reinterpret_cast<const uint4 *>(q + c * 64) + row) : make_uint4(0, 0, 0, 0);
         }
-        cell_mask[c] = m;
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const int64_t c = c0 + 2 * u + half;
+            unsigned long long m = 0;
+            if (on[u]) {
+                const uint32_t ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+                for (int x = 0; x < 4; x++) {
+                    const ushort2 v = *reinterpret_cast<const ushort2 *>(&ws[x]);
+                    bool in = qi > v.x && qi < v.y;  // decided by the buckets (the common case)
+                    if (qi == v.x || qi == v.y) {    // shared bucket: exact float64 test (rare)
+                        const uint32_t cu = (uint32_t)c;
+                        const int fx = 4 * (int)(cu % (uint32_t)cdx) + x;
+                        const int fy = 4 * (int)((cu / (uint32_t)cdx) % (uint32_t)cdy) + (row & 3);
+                        const int fz = 4 * (int)(cu / ((uint32_t)cdx * (uint32_t)cdy)) + (row >> 2);
+                        in = fx < fdx && fy < fdy && fz < fdz &&
+                             iso_in_q(v, qi, mm, fx + (int64_t)fdx * (fy + (int64_t)fdy * fz), iso);
+                    }
+                    if (in) m |= 1ull << (x + 4 * row);
+                }
+            }
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
+            if (row == 0 && c < n_coarse) cell_mask[c] = m;
+        }
     }
 }
 
@@ -1397,11 +1416,11 @@ void Session::reset(const CameraParams *cam, double iso_) {
         eye[2] = cam->eye[2];
     }
     WC_CUDA(cudaEventRecord(ev_frame0, st));
-    k_iso_cell_mask<<<grid_for(vol->n_coarse, 128, 16), 128, 0, st>>>(
-        vol->fine_q.p, vol->fine_mm.p, vol->bdx, vol->bdy, vol->bdz, vol->cdx, vol->cdy, vol->cdz, iso, vol->q_base,
-        vol->q_inv, cell_mask.p);
-    WC_LAUNCH_CHECK();
     k_iso_bitmap<<<grid_for(vol->n_coarse, 256, 8), 256, 0, st>>>(vol->coarse_mm.p, vol->n_coarse, iso, coarse_bm.p);
+    WC_LAUNCH_CHECK();
+    k_iso_cell_mask<<<grid_for(vol->n_coarse * 16, 256, 8), 256, 0, st>>>(
+        vol->fine_q.p, vol->fine_mm.p, coarse_bm.p, vol->bdx, vol->bdy, vol->bdz, vol->cdx, vol->cdy, vol->cdz, iso,
+        vol->q_base, vol->q_inv, cell_mask.p);
     WC_LAUNCH_CHECK();
     RayInitArgs a{};
     a.cam = cam_params;

@@ -295,15 +295,24 @@ __global__ void k_range_extent(const double2 *mm, int64_t n, unsigned long long 
     }
 }
 
-__global__ void k_range_quantize(const double2 *mm, int64_t n, double base, double inv, ushort2 *q) {
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
-        const double2 v = mm[b];
-        // a NaN bound never passes the iso test: (65535, 0) sends every iso
-        // either to a proven "out" or to the exact re-test
-        if (v.x != v.x || v.y != v.y)
-            q[b] = make_ushort2(65535, 0);
-        else
-            q[b] = make_ushort2((unsigned short)range_q(v.x, base, inv), (unsigned short)range_q(v.y, base, inv));
+// Bricked: entry c * 64 + (lx + 4 ly + 16 lz) is fine cell (4 cx + lx, ...)
+// of coarse cell c; cells past the grid edge get (65535, 0) like a NaN bound
+// (a NaN bound never passes the iso test: (65535, 0) sends every iso either
+// to a proven "out" or to the exact re-test).
+__global__ void k_range_quantize(const double2 *mm, int bdx, int bdy, int bdz, int cdx, int cdy, int64_t n_q,
+                                 double base, double inv, ushort2 *q) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_q; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e >> 6;
+        const int l = (int)(e & 63);
+        const int x = 4 * (int)(c % cdx) + (l & 3), y = 4 * (int)((c / cdx) % cdy) + ((l >> 2) & 3),
+                  z = 4 * (int)(c / ((int64_t)cdx * cdy)) + (l >> 4);
+        ushort2 out = make_ushort2(65535, 0);
+        if (x < bdx && y < bdy && z < bdz) {
+            const double2 v = mm[x + (int64_t)bdx * (y + (int64_t)bdy * z)];
+            if (v.x == v.x && v.y == v.y)
+                out = make_ushort2((unsigned short)range_q(v.x, base, inv), (unsigned short)range_q(v.y, base, inv));
+        }
+        q[e] = out;
     }
 }
 
@@ -328,8 +337,9 @@ void Volume::build_range_index() {
     // any positive finite inv keeps the test exact; a useful one spreads
     // the finite bounds over the 16-bit range
     q_inv = (span > 0.0 && std::isfinite(65535.0 / span)) ? 65535.0 / span : 1.0;
-    fine_q.alloc(n_blocks);
-    k_range_quantize<<<grid_for(n_blocks, 256, 4), 256, 0, st>>>(fine_mm.p, n_blocks, q_base, q_inv, fine_q.p);
+    fine_q.alloc(n_coarse * 64);
+    k_range_quantize<<<grid_for(n_coarse * 64, 256, 4), 256, 0, st>>>(fine_mm.p, bdx, bdy, bdz, cdx, cdy,
+                                                                      n_coarse * 64, q_base, q_inv, fine_q.p);
     WC_LAUNCH_CHECK();
     WC_CUDA(cudaStreamSynchronize(st));
 }
