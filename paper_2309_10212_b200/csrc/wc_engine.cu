@@ -952,11 +952,15 @@ __global__ void __launch_bounds__(256, 3)
             for (int u = 0; u < kInFlight; u++) {
                 const uint32_t s = __shfl_sync(0xffffffffu, my_s, (u0 + u) & 31);
                 if (u0 + u >= cnt) break;  // warp-uniform
-                float v0, v1;
-                decode_loaded_warp(wa[u], wb[u], qbits, lane, v0, v1);
                 float *dst = slot_values + (int64_t)s * 64;
-                dst[lane] = v0;
-                dst[lane + 32] = v1;
+                if (qbits == 16) {  // the common rate: lane decodes values 2l, 2l+1 (one 8 B store)
+                    reinterpret_cast<float2 *>(dst)[lane] = decode16_pair(wa[u], wb[u], lane);
+                } else {
+                    float v0, v1;
+                    decode_loaded_warp(wa[u], wb[u], qbits, lane, v0, v1);
+                    dst[lane] = v0;
+                    dst[lane + 32] = v1;
+                }
             }
         }
     }
