@@ -12,6 +12,8 @@
 #include <chrono>
 #include <cstring>
 
+#include <cstdlib>
+
 #include "wc_engine.cuh"
 #include "wc_trace.cuh"
 
@@ -1076,9 +1078,15 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_raytrace(Raytrace
 // ---- two-phase raytrace: the same per-entry result as k_raytrace, with the
 // float64 cubic solves run as a dense work list so that the divergent DDA
 // and the uniform root finding no longer share warps.
+// A candidate cell carries everything the solve and the shade need, so they
+// start from one coalesced read instead of the entry -> ray -> block -> slot
+// chain: info = (entry k, ray r, block b, lx | ly << 3 | lz << 6 | seq << 9)
+// and the cell's 8 float corners (corner order idx = dx + 2 dy + 4 dz).
 struct SplitArgs {
     RaytraceArgs a;
-    uint32_t *item_j, *item_cell, *n_items, *best;
+    uint4 *item_info;
+    float4 *item_corners;  // 2 per item
+    uint32_t *n_items, *best;
     double *item_t;
     int64_t item_cap;
 };
@@ -1144,12 +1152,22 @@ __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
         uint32_t first = 0;
         if (lane == 31 && incl) first = atomicAdd(s.n_items, incl);
         first = __shfl_sync(0xffffffffu, first, 31) + incl - (uint32_t)found;
-        for (int q = 0; q < found; q++) {
-            const uint32_t it = first + q;
-            if (it < s.item_cap) {
-                const uint32_t lc = (uint32_t)(codes >> (6 * q)) & 63u;
-                s.item_j[it] = (uint32_t)j;
-                s.item_cell[it] = (lc & 3u) | (((lc >> 2) & 3u) << 3) | ((lc >> 4) << 6) | ((uint32_t)q << 9);
+        if (found) {
+            // the corners were just walked: these loads hit L1
+            const EntryCtx e = entry_ctx(a, j);
+            const uint32_t b = a.visible_ids[a.ent_key[j]];
+            for (int q = 0; q < found; q++) {
+                const uint32_t it = first + q;
+                if (it < s.item_cap) {
+                    const uint32_t lc = (uint32_t)(codes >> (6 * q)) & 63u;
+                    const int lx = lc & 3, ly = (lc >> 2) & 3, lz = lc >> 4;
+                    float c[8];
+                    e.field.corners(lx, ly, lz, c);
+                    s.item_info[it] = make_uint4(e.k, (uint32_t)e.r, b,
+                                                 (uint32_t)(lx | (ly << 3) | (lz << 6)) | ((uint32_t)q << 9));
+                    s.item_corners[2 * (int64_t)it] = make_float4(c[0], c[1], c[2], c[3]);
+                    s.item_corners[2 * (int64_t)it + 1] = make_float4(c[4], c[5], c[6], c[7]);
+                }
             }
         }
     }
@@ -1161,15 +1179,19 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArg
     const RaytraceArgs &a = s.a;
     const int64_t n_items = min((int64_t)*s.n_items, s.item_cap);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_items; i += (int64_t)gridDim.x * blockDim.x) {
-        const EntryCtx e = entry_ctx(a, s.item_j[i]);
-        const uint32_t code = s.item_cell[i];
+        const uint4 info = s.item_info[i];
+        const float4 c0 = s.item_corners[2 * i], c1 = s.item_corners[2 * i + 1];
+        const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        const uint32_t k = info.x, r = info.y, b = info.z, code = info.w;
         const int lx = code & 7, ly = (code >> 3) & 7, lz = (code >> 6) & 7, seq = code >> 9;
-        float c[8];
-        e.field.corners(lx, ly, lz, c);
-        const double th = solve_cell(c, e.o, e.d, 4 * e.bx + lx, 4 * e.by + ly, 4 * e.bz + lz, e.te, a.iso);
+        const int bx = (int)(b % (uint32_t)a.bdx), by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy),
+                  bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
+        double o[3], d[3];
+        a.rays.load(r, o, d);
+        const double th = solve_cell(c, o, d, 4 * bx + lx, 4 * by + ly, 4 * bz + lz, a.rays.t_enter[r], a.iso);
         if (th != CUDART_INF) {
             s.item_t[i] = th;
-            atomicMin(&s.best[e.k], ((uint32_t)seq << 27) | (uint32_t)i);
+            atomicMin(&s.best[k], ((uint32_t)seq << 27) | (uint32_t)i);
         }
     }
 }
@@ -1184,14 +1206,19 @@ __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
             a.rgbz[k] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
             continue;
         }
-        const EntryCtx e = entry_ctx(a, j);
         const uint32_t i = bst & ((1u << 27) - 1u);
-        const uint32_t code = s.item_cell[i];
+        const uint4 info = s.item_info[i];
+        const float4 c0 = s.item_corners[2 * (int64_t)i], c1 = s.item_corners[2 * (int64_t)i + 1];
+        const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        const uint32_t r = info.y, b = info.z, code = info.w;
         const int lx = code & 7, ly = (code >> 3) & 7, lz = (code >> 6) & 7;
-        float c[8], rgb[3];
-        e.field.corners(lx, ly, lz, c);
+        const int bx = (int)(b % (uint32_t)a.bdx), by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy),
+                  bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
+        double o[3], d[3];
+        a.rays.load(r, o, d);
+        float rgb[3];
         const double th = s.item_t[i];
-        shade_hit(c, e.o, e.d, 4 * e.bx + lx, 4 * e.by + ly, 4 * e.bz + lz, th, a.br, a.bg, a.bb, rgb);
+        shade_hit(c, o, d, 4 * bx + lx, 4 * by + ly, 4 * bz + lz, th, a.br, a.bg, a.bb, rgb);
         a.rgbz[k] = make_float4(rgb[0], rgb[1], rgb[2], (float)th);
     }
 }
@@ -1754,14 +1781,14 @@ bool Session::pass(PassStatsC &stats) {
             SplitArgs sa{};
             sa.a = ra;
             sa.item_cap = 10 * n;  // <= 10 dual cells per entry (monotone ray in a 4^3 region)
-            if (item_j.n < sa.item_cap) {
-                item_j.alloc(sa.item_cap);
-                item_cell.alloc(sa.item_cap);
+            if (item_info.n < sa.item_cap) {
+                item_info.alloc(sa.item_cap);
+                item_corners.alloc(2 * sa.item_cap);
                 item_t.alloc(sa.item_cap);
                 best.alloc(n);
             }
-            sa.item_j = item_j.p;
-            sa.item_cell = item_cell.p;
+            sa.item_info = item_info.p;
+            sa.item_corners = item_corners.p;
             sa.item_t = item_t.p;
             sa.best = best.p;
             sa.n_items = counters.p + C_NITEMS;
@@ -1804,6 +1831,12 @@ bool Session::pass(PassStatsC &stats) {
         stage_ms[k] += ms;
         if (pass_index < kMaxPassLog) pass_stage_ms[pass_index][k] = ms;
     }
+    static const bool trace = getenv("WAVECAST_TRACE") != nullptr;
+    if (trace)
+        fprintf(stderr, "[wavecast] pass %lld n_act %lld n_spec %lld entries %lld visible %lld active %lld miss %lld "
+                        "evict %lld items %u after %lld\n",
+                (long long)pass_index, (long long)n_act, (long long)n_spec, (long long)n_ent, (long long)nvis,
+                (long long)nactb, (long long)n_miss, (long long)n_evict, h_counters.p[C_NITEMS], (long long)n_after);
     stats.pass_index = pass_index;
     stats.n_active_before = n_act;
     stats.n_spec = n_spec;

@@ -71,7 +71,9 @@ struct Session {
     DevBuf<uint32_t> ent_key, ent_val, ent_ray;
     DevBuf<float4> rgbz;
     DevBuf<int4> contrib;  // 8 contributor slots per visible block
-    DevBuf<uint32_t> item_j, item_cell, best;  // two-phase raytrace work list
+    DevBuf<uint4> item_info;  // two-phase raytrace work list (SplitArgs)
+    DevBuf<float4> item_corners;
+    DevBuf<uint32_t> best;
     DevBuf<double> item_t;
     DevBuf<uint32_t> vis_bm, act_bm, vis_word_off, act_word_off;
     DevBuf<uint32_t> coarse_bm;            // per-iso coarse range-test bitmap, rebuilt at every reset
