@@ -35,7 +35,7 @@
 #define WC_EARLY_HIST 1
 #endif
 #ifndef WC_RAYTRACE_MIN_CTAS
-#define WC_RAYTRACE_MIN_CTAS 4
+#define WC_RAYTRACE_MIN_CTAS 6
 #endif
 
 namespace wc {

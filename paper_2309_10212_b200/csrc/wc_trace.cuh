@@ -100,9 +100,9 @@ __device__ __forceinline__ double intersect_cubic(const float c[8], const double
         D += w * ((axa * aya) * aza);
     }
     D -= iso;
-    double bounds[4];
-    int nb = 0;
-    bounds[nb++] = t0;
+    // split points t0 < [m1 < m2] < t1 (registers, no local array)
+    double m1 = 0.0, m2 = 0.0;
+    int nm = 0;
     const double qa = 3.0 * A, qb = 2.0 * B;
     if (qa != 0.0) {
         const double disc = qb * qb - 4.0 * qa * C;
@@ -116,20 +116,29 @@ __device__ __forceinline__ double intersect_cubic(const float c[8], const double
                 r1 = r2;
                 r2 = t;
             }
-            if (t0 < r1 && r1 < t1) bounds[nb++] = r1;
-            if (t0 < r2 && r2 < t1 && r2 != r1) bounds[nb++] = r2;
+            if (t0 < r1 && r1 < t1) m1 = r1, nm = 1;
+            if (t0 < r2 && r2 < t1 && r2 != r1) {
+                if (nm == 0)
+                    m1 = r2;
+                else
+                    m2 = r2;
+                nm++;
+            }
         }
     } else if (qb != 0.0) {
         const double r1 = -C / qb;
-        if (t0 < r1 && r1 < t1) bounds[nb++] = r1;
+        if (t0 < r1 && r1 < t1) m1 = r1, nm = 1;
     }
-    bounds[nb++] = t1;
-    double g_prev = poly_eval(A, B, C, D, bounds[0]);
-    if (g_prev == 0.0) return bounds[0];
-    for (int i = 1; i < nb; i++) {
-        const double g_here = poly_eval(A, B, C, D, bounds[i]);
-        if (g_here == 0.0) return bounds[i];
-        if ((g_prev < 0.0) != (g_here < 0.0)) return refine_root(A, B, C, D, bounds[i - 1], bounds[i], g_prev, g_here);
+    double t_prev = t0, g_prev = poly_eval(A, B, C, D, t0);
+    if (g_prev == 0.0) return t0;
+#pragma unroll
+    for (int i = 1; i <= 3; i++) {
+        if (i > nm + 1) break;
+        const double t_here = i > nm ? t1 : (i == 1 ? m1 : m2);
+        const double g_here = poly_eval(A, B, C, D, t_here);
+        if (g_here == 0.0) return t_here;
+        if ((g_prev < 0.0) != (g_here < 0.0)) return refine_root(A, B, C, D, t_prev, t_here, g_prev, g_here);
+        t_prev = t_here;
         g_prev = g_here;
     }
     return CUDART_INF;
