@@ -148,6 +148,26 @@ def peaks():
 
 
 # ------------------------------------------------------------------ models
+TRAFFIC_FILE = "profiles/frame_traffic_c3.json"
+
+
+def traffic_of(stage, config):
+    """DRAM bytes (read + write) per frame of the stage's kernels, from the
+    committed ncu launch list of this bench (scripts/ncu_frame_traffic.py over
+    `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
+    dram__bytes_write.sum`), so roofline.traffic compares with
+    roofline.achieved's algorithmic bytes per frame.  None when absent."""
+    if config != "c3":
+        return None
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), TRAFFIC_FILE)
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return int(d["per_frame_by_stage"][stage]["dram_bytes"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def frame_bytes(stats, n_rays, stride):
     """SURVEY.md §8(d) algorithmic bytes of one frame from its PassStats."""
     b = 130 * n_rays
@@ -323,7 +343,9 @@ def run_b200(args):
         "frame_ms_all": [round(x, 3) for x in frame_ms],
         "wall_s_timed_region": round(wall_s, 3),
         "roofline": {"bound": "hbm", "kernel": top, "achieved": round(achieved, 2), "peak": pk["hbm_gbs"],
-                     "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 5), "traffic": None,
+                     "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 5),
+                     "traffic": traffic_of(top, args.config),
+                     "traffic_source": TRAFFIC_FILE if traffic_of(top, args.config) is not None else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "_fallback" not in pk
                      else "fallback 6650 GB/s (B200_PROFILING.md)",
                      "frame_algorithmic_bytes": int(fbytes),

@@ -20,11 +20,12 @@ STAGE_OF = [
     ("k_decode_insert", "cache_decode"), ("k_evict", "cache_decode"), ("k_stamp_hist", "cache_decode"),
     ("k_mark_stamp", "cache_decode"), ("k_blocks_to_slots", "cache_decode"), ("k_gather_last_used", "cache_decode"),
     ("k_compact_cand", "cache_decode"),
-    ("k_iso_bitmap", "reset"), ("k_init_rays", "reset"), ("k_cache_unmap", "reset"),
+    ("k_iso_bitmap", "reset"), ("k_iso_cell_mask", "reset"), ("k_init_rays", "reset"), ("k_cache_unmap", "reset"),
+    ("k_stamp_hist", "cache_decode"),
     ("k_composite", "composite"), ("k_compact_keep", "composite"),
     ("k_radix", "group"), ("k_run_offsets", "group"),
 ]
-SETUP = ("k_compress", "k_widen", "k_octant_union", "k_group4")
+SETUP = ("k_compress", "k_widen", "k_octant_union", "k_group4", "k_range_extent", "k_range_quantize")
 
 
 def unit_scale(u):
