@@ -43,11 +43,13 @@ CONFIGS = {
     "c3": ((2048, 2048, 1920), "turbulence", 1, 16, 1920, 1080, 0.5),
     "c2": ((512, 512, 512), "gaussians", 0, 16, 1920, 1080, 0.3),
     "c4": ((2048, 2048, 1920), "turbulence", 1, 16, 3840, 2160, 0.5),
+    "c5": ((2048, 2048, 1920), "turbulence", 1, 16, 1920, 1080, 0.5),
 }
 WORKLOAD_NAMES = {
     "c3": "2048x2048x1920 (8.05B voxels) turbulence-like field, WCZ1 qbits 16, 1920x1080, iso 50%, orbit cam 0",
     "c2": "512^3 sum-of-24-Gaussians, WCZ1 qbits 16, 1920x1080, iso 30%, orbit cam 0",
     "c4": "8.05B-voxel turbulence at 3840x2160 with a small cache budget",
+    "c5": "C3 volume, bench protocol (cli.py:122-195): random isovalues x camera orbit at 1920x1080",
 }
 
 
@@ -67,6 +69,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-tiles", type=int, default=0, help="tiles in the CPU-baseline sample (0=auto)")
     p.add_argument("--threads", type=int, default=0, help="host threads for the reference arm (0=all)")
+    p.add_argument("--isovalues", type=int, default=9, help="c5: random isovalues (cli.py bench protocol)")
+    p.add_argument("--orbit-steps", type=int, default=10, help="c5: cameras per isovalue")
+    p.add_argument("--seed", type=int, default=0, help="c5: isovalue seed")
     return p.parse_args()
 
 
@@ -93,6 +98,7 @@ def config_json(args, wl, n_gpus, extra=None):
 
 
 def orbit(dims):
+    """The orbit-step-0 camera as the oracle's tuple (CPU legs only)."""
     from oracle import oracle as orc
 
     return orc.orbit_camera(dims, 0, 1)
@@ -220,6 +226,7 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2309_10212_b200 as wc
     from paper_2309_10212_b200 import dist as wdist
+    from paper_2309_10212_b200.benchmark import orbit_camera
 
     wc._lib.ensure_device(local)
     wl = workload(args.config)
@@ -231,7 +238,7 @@ def run_b200(args):
     lo, hi = float(ranges[:, 0].min()), float(ranges[:, 1].max())
     setup_s = time.perf_counter() - t0
     iso = lo + wl["iso_frac"] * (hi - lo)
-    cam = wc.Camera(*orbit(wl["dims"]))
+    cam = orbit_camera(wl["dims"], 0, 1)  # cli.py:48-58, orbit step 0
     w, h = wl["w"], wl["h"]
     cache = args.cache_slots if args.cache_slots > 0 else None
     if args.config == "c4" and cache is None:
@@ -443,10 +450,63 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_c5(args):
+    """C5: the reference's bench protocol (cli.py:122-195) over the C3 volume on
+    one GPU -- isovalues drawn from the decoded value range x an orbit of
+    cameras, every render a full frame to completeness 1.0.  Reports the
+    protocol's report plus the device time of every frame."""
+    import paper_2309_10212_b200 as wc
+    from paper_2309_10212_b200.benchmark import bench_report
+
+    wc._lib.ensure_device(int(os.environ.get("LOCAL_RANK", "0")))
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    wl = workload("c3")
+    t0 = time.perf_counter()
+    field = wc.volume.separable_field(wl["kind"], wl["dims"], wl["seed"])
+    cv = wc.compress_separable(field, wl["qbits"])
+    grids = wc.build_grids(cv)
+    setup_s = time.perf_counter() - t0
+    w, h = wl["w"], wl["h"]
+    # warm-up renders (untimed): the first isovalue's orbit
+    bench_report(cv, grids, isovalues=1, orbit_steps=max(1, args.warmup), seed=args.seed, width=w, height=h,
+                 max_spec=args.max_spec)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        rep, tim = bench_report(cv, grids, isovalues=args.isovalues, orbit_steps=args.orbit_steps, seed=args.seed,
+                                width=w, height=h, max_spec=args.max_spec, volume="C3 (device-synthesised)")
+    ms = tim["mean_frame_ms"]
+    wall = float(np.mean(tim["wall_ms"]))
+    line = {
+        "metric": METRIC, "value": round((w * h) / (ms * 1e-3) / 1e6, 3), "unit": UNIT, "n_gpus": 1,
+        "steps": rep["n_renders"], "warmup": max(1, args.warmup), "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (device-generated separable turbulence field, compressed on the device)",
+        "config": config_json(args, wl, 1, {"workload": WORKLOAD_NAMES["c5"], "isovalues": args.isovalues,
+                                           "orbit_steps": args.orbit_steps, "seed": args.seed,
+                                           "camera": "cli.py orbit_camera(k, orbit_steps)",
+                                           "iso_fraction": "uniform in [5%, 95%] of the decoded range",
+                                           "l2": "not flushed between frames (back-to-back protocol renders)"}),
+        "e2e": {"value": round((w * h) / (wall * 1e-3) / 1e6, 3), "unit": UNIT, "ms_per_frame": round(wall, 3),
+                "h2d_bytes_per_step": 120, "d2h_bytes_per_step": 0,
+                "path": "benchmark.bench_report -> RenderSession.render_frame (stats to host, framebuffer stays "
+                        "on the device)"},
+        "frame_ms": {"mean": round(ms, 4), "median": round(tim["median_frame_ms"], 4),
+                     "max": round(tim["max_frame_ms"], 4), "all": [round(x, 3) for x in tim["frame_ms"]]},
+        "passes_all": tim["passes"],
+        "report": rep,
+        "value_range": tim["value_range"],
+        "clocks": clk.summary(),
+        "setup_s": round(setup_s, 2),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c5":
+        run_c5(args)
     else:
         run_b200(args)
 

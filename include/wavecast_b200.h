@@ -89,6 +89,26 @@ int wc_volume_info(const wc_volume *v, int64_t *n_blocks, int64_t *n_coarse, int
 /* Copy the device payload / ranges / grids back to host buffers (nullable). */
 int wc_volume_download(const wc_volume *v, uint8_t *payload, float *ranges, double *fine_min, double *fine_max,
                        double *coarse_min, double *coarse_max);
+/* (min, max) of the decoded voxels inside dims -- the value_range of
+ * oracle.decode_full (oracle.py:22-39), computed on the device. */
+int wc_volume_value_range(const wc_volume *v, double *lo, double *hi);
+
+/* ---- .wcz container (read_wcz, codec.py:243-273) straight to HBM
+ * Header/size validation with read_wcz's DataError / UsageError messages
+ * (no device needed). */
+int wc_wcz_probe(const char *path, int *nx, int *ny, int *nz, int *qbits, int *stride, int64_t *n_blocks);
+/* Stream the ranges and payload from the file into device memory through two
+ * pinned chunks (chunk_bytes, 0 = 64 MiB; reads overlap the H2D copies),
+ * then build the grids on the device. */
+int wc_volume_load_wcz(const char *path, int64_t chunk_bytes, wc_volume **out);
+/* A volume whose payload/ranges are filled on the device by the caller
+ * (e.g. an NCCL broadcast from the rank that loaded the file): alloc, write
+ * through wc_volume_device_buffers, then wc_volume_finalize builds the grids. */
+int wc_volume_alloc(int nx, int ny, int nz, int qbits, wc_volume **out);
+int wc_volume_device_buffers(wc_volume *v, void **payload, uint64_t *payload_bytes, void **ranges,
+                             uint64_t *ranges_bytes);
+int wc_volume_finalize(wc_volume *v);
+
 /* decompress_block(s) (codec.py:201-217): host ids in, host float32[n*64] out. */
 int wc_decode_blocks(const wc_volume *v, const int64_t *ids, int64_t n, float *out);
 /* Device-only timing of decode: decodes `n` blocks (ids on host, uploaded

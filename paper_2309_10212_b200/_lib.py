@@ -83,6 +83,12 @@ _SIGS = {
     "wc_volume_info": (_i32, [_vp, _vp, _vp, _vp]),
     "wc_volume_download": (_i32, [_vp] * 7),
     "wc_volume_set_grids": (_i32, [_vp] * 5),
+    "wc_volume_value_range": (_i32, [_vp, _vp, _vp]),
+    "wc_wcz_probe": (_i32, [C.c_char_p, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "wc_volume_load_wcz": (_i32, [C.c_char_p, _i64, _vp]),
+    "wc_volume_alloc": (_i32, [_i32, _i32, _i32, _i32, _vp]),
+    "wc_volume_device_buffers": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "wc_volume_finalize": (_i32, [_vp]),
     "wc_decode_blocks": (_i32, [_vp, _vp, _i64, _vp]),
     "wc_decode_bench": (_i32, [_vp, _vp, _i64, _i32, _vp]),
     "wc_session_create": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp, _dbl, _i32, _i32, _i64, _i32, _vp]),
@@ -166,6 +172,11 @@ def check(status: int) -> None:
 def call(name: str, *args) -> None:
     if not _initialised:
         ensure_device()
+    check(getattr(lib(), name)(*args))
+
+
+def call_host(name: str, *args) -> None:
+    """A library call that touches no device (header parsing and the like)."""
     check(getattr(lib(), name)(*args))
 
 

@@ -14,7 +14,9 @@ Compression and decoding run on the GPU (csrc/wc_volume.cu); only the
 
 from __future__ import annotations
 
+import ctypes as C
 import math
+import os
 import struct
 
 import numpy as np
@@ -198,6 +200,36 @@ def write_wcz(cv: CompressedVolume, path) -> None:
         f.write(header)
         f.write(cv.raw_block_ranges.astype("<f4").tobytes())
         f.write(cv.payload.tobytes())
+
+
+def probe_wcz(path):
+    """Header of a .wcz container with read_wcz's validation (codec.py:246-262):
+    returns (dims, qbits, stride, n_blocks); errors are DataError/UsageError
+    with the reference's messages.  Host only."""
+    v = [C.c_int() for _ in range(5)]
+    nb = C.c_int64()
+    _lib.call_host("wc_wcz_probe", os.fsencode(os.fspath(path)), *[C.byref(x) for x in v], C.byref(nb))
+    return (v[0].value, v[1].value, v[2].value), v[3].value, v[4].value, nb.value
+
+
+def load_wcz(path, chunk_bytes: int = 0) -> CompressedVolume:
+    """read_wcz (codec.py:243-273) straight into HBM: the native loader streams
+    the ranges and payload through two pinned chunks (file reads overlap the
+    host-to-device copies) and builds the grids on the device.  The host
+    views (payload, raw_block_ranges) are downloaded only if asked for."""
+    dims, qbits, _, _ = probe_wcz(path)
+    h = C.c_void_p()
+    _lib.call("wc_volume_load_wcz", os.fsencode(os.fspath(path)), int(chunk_bytes), C.byref(h))
+    return CompressedVolume(dims, qbits, handle=h)
+
+
+def decoded_value_range(cv: CompressedVolume) -> tuple[float, float]:
+    """oracle.decode_full(cv).value_range (oracle.py:22-39) computed on the
+    device without materialising the dense volume: (min, max) of the decoded
+    voxels inside dims, as float32 values widened to float."""
+    lo, hi = C.c_double(), C.c_double()
+    _lib.call("wc_volume_value_range", cv.device_handle(), C.byref(lo), C.byref(hi))
+    return float(lo.value), float(hi.value)
 
 
 def read_wcz(path) -> CompressedVolume:

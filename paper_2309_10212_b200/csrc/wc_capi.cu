@@ -1,4 +1,8 @@
 // wc_capi.cu -- extern "C" boundary of libwavecast_b200.so (include/wavecast_b200.h).
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <cstring>
 #include <string>
 #include <vector>
@@ -119,6 +123,168 @@ int wc_volume_create(const uint8_t *payload, uint64_t payload_bytes, const float
         throw;
     }
     *out = h;
+    WC_API_END
+}
+
+// ---- .wcz container straight to the device (codec.py:243-273) ----------
+
+namespace {
+
+struct WczHeader {
+    int nx, ny, nz, qbits, stride;
+    int64_t n_blocks, file_bytes;
+};
+
+// Same checks and messages as read_wcz (codec.py:246-262).
+WczHeader wcz_header(const char *path, int fd) {
+    const std::string p(path);
+    struct stat sb;
+    if (fstat(fd, &sb) != 0) throw wc::DataError(p + ": cannot stat");
+    unsigned char h[28];
+    const ssize_t got = sb.st_size >= 28 ? pread(fd, h, 28, 0) : 0;
+    if (got != 28 || memcmp(h, "WCZ1", 4) != 0) throw wc::DataError(p + ": not a WCZ1 container");
+    uint32_t f[6];
+    memcpy(f, h + 4, 24);  // little-endian host (x86-64 / aarch64)
+    if (f[0] != 1) throw wc::DataError(p + ": unsupported container version " + std::to_string(f[0]));
+    check_qbits((int)f[4]);
+    if ((int)f[5] != wc::stride_of((int)f[4]))
+        throw wc::DataError(p + ": stride " + std::to_string(f[5]) + " inconsistent with qbits " +
+                            std::to_string(f[4]));
+    WczHeader w{(int)f[1], (int)f[2], (int)f[3], (int)f[4], (int)f[5], 0, (int64_t)sb.st_size};
+    w.n_blocks = (int64_t)((w.nx + 3) / 4) * ((w.ny + 3) / 4) * ((w.nz + 3) / 4);
+    const int64_t expected = 28 + 8 * w.n_blocks + w.n_blocks * (int64_t)w.stride;
+    if (w.file_bytes != expected)
+        throw wc::DataError(p + ": expected " + std::to_string(expected) + " bytes, found " +
+                            std::to_string(w.file_bytes));
+    return w;
+}
+
+struct Fd {
+    int fd;
+    explicit Fd(const char *path) : fd(open(path, O_RDONLY)) {
+        if (fd < 0) throw wc::DataError(std::string(path) + ": cannot open");
+    }
+    ~Fd() { close(fd); }
+};
+
+// Stream [off, off+bytes) of the file into device memory: pread into two
+// pinned chunks alternately while the other chunk's copy runs, so disk (or
+// page cache) reads overlap the PCIe/C2C transfer.
+void stream_to_device(int fd, const char *path, int64_t off, int64_t bytes, void *dst, int64_t chunk,
+                      cudaStream_t st) {
+    if (bytes <= 0) return;
+    chunk = std::max<int64_t>(1 << 20, std::min<int64_t>(chunk, bytes));
+    wc::PinnedBuf<uint8_t> buf[2];
+    cudaEvent_t ev[2];
+    for (int i = 0; i < 2; i++) {
+        buf[i].alloc(chunk);
+        WC_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        WC_CUDA(cudaEventRecord(ev[i], st));
+    }
+    int64_t done = 0;
+    int k = 0;
+    try {
+        while (done < bytes) {
+            const int64_t n = std::min<int64_t>(chunk, bytes - done);
+            WC_CUDA(cudaEventSynchronize(ev[k]));  // this chunk's previous copy has drained
+            int64_t r = 0;
+            while (r < n) {
+                const ssize_t got = pread(fd, buf[k].p + r, (size_t)(n - r), (off_t)(off + done + r));
+                if (got <= 0) throw wc::DataError(std::string(path) + ": short read");
+                r += got;
+            }
+            WC_CUDA(cudaMemcpyAsync(static_cast<uint8_t *>(dst) + done, buf[k].p, (size_t)n, cudaMemcpyHostToDevice,
+                                    st));
+            WC_CUDA(cudaEventRecord(ev[k], st));
+            done += n;
+            k ^= 1;
+        }
+        WC_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+        cudaStreamSynchronize(st);
+        for (auto &e : ev) cudaEventDestroy(e);
+        throw;
+    }
+    for (auto &e : ev) WC_CUDA(cudaEventDestroy(e));
+}
+
+}  // namespace
+
+int wc_wcz_probe(const char *path, int *nx, int *ny, int *nz, int *qbits, int *stride, int64_t *n_blocks) {
+    WC_API_BEGIN
+    Fd f(path);
+    const WczHeader h = wcz_header(path, f.fd);
+    if (nx) *nx = h.nx;
+    if (ny) *ny = h.ny;
+    if (nz) *nz = h.nz;
+    if (qbits) *qbits = h.qbits;
+    if (stride) *stride = h.stride;
+    if (n_blocks) *n_blocks = h.n_blocks;
+    WC_API_END
+}
+
+int wc_volume_load_wcz(const char *path, int64_t chunk_bytes, wc_volume **out) {
+    WC_API_BEGIN
+    Fd f(path);
+    const WczHeader h = wcz_header(path, f.fd);
+    check_dims(h.nx, h.ny, h.nz);
+    auto *v = new wc_volume();
+    try {
+        v->v.set_dims(h.nx, h.ny, h.nz, h.qbits);
+        v->v.ranges.alloc(h.n_blocks);
+        v->v.payload.alloc(h.n_blocks * h.stride);
+        const int64_t chunk = chunk_bytes > 0 ? chunk_bytes : (int64_t)64 << 20;
+        stream_to_device(f.fd, path, 28, 8 * h.n_blocks, v->v.ranges.p, chunk, v->v.st);
+        stream_to_device(f.fd, path, 28 + 8 * h.n_blocks, h.n_blocks * h.stride, v->v.payload.p, chunk, v->v.st);
+        v->v.build_grids();
+    } catch (...) {
+        delete v;
+        throw;
+    }
+    *out = v;
+    WC_API_END
+}
+
+int wc_volume_alloc(int nx, int ny, int nz, int qbits, wc_volume **out) {
+    WC_API_BEGIN
+    check_qbits(qbits);
+    check_dims(nx, ny, nz);
+    auto *v = new wc_volume();
+    try {
+        v->v.set_dims(nx, ny, nz, qbits);
+        v->v.ranges.alloc(v->v.n_blocks);
+        v->v.payload.alloc(v->v.n_blocks * v->v.stride);
+    } catch (...) {
+        delete v;
+        throw;
+    }
+    *out = v;
+    WC_API_END
+}
+
+int wc_volume_device_buffers(wc_volume *v, void **payload, uint64_t *payload_bytes, void **ranges,
+                             uint64_t *ranges_bytes) {
+    WC_API_BEGIN
+    if (payload) *payload = v->v.payload.p;
+    if (payload_bytes) *payload_bytes = (uint64_t)(v->v.n_blocks * v->v.stride);
+    if (ranges) *ranges = v->v.ranges.p;
+    if (ranges_bytes) *ranges_bytes = (uint64_t)(8 * v->v.n_blocks);
+    WC_API_END
+}
+
+int wc_volume_finalize(wc_volume *v) {
+    WC_API_BEGIN
+    WC_CUDA(cudaDeviceSynchronize());  // payload/ranges were written by other streams (e.g. NCCL)
+    v->v.build_grids();
+    WC_API_END
+}
+
+int wc_volume_value_range(const wc_volume *v, double *lo, double *hi) {
+    WC_API_BEGIN
+    float l = 0.0f, h = 0.0f;
+    wc::decoded_value_range(v->v, &l, &h);
+    *lo = l;
+    *hi = h;
     WC_API_END
 }
 

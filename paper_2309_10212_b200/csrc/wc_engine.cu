@@ -1432,6 +1432,8 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
         WC_CUDA(cudaMemcpyAsync(dir_in.p, dirs, 24 * n, cudaMemcpyHostToDevice, st));
     }
     init_cap = cache_capacity;
+    contrib.alloc(2 * n);
+    reserve_slots(std::min<int64_t>(vol->n_blocks, 2 * n));
     reset(cam, iso_);
 }
 
@@ -1482,9 +1484,7 @@ void Session::reset(const CameraParams *cam, double iso_) {
     phys = std::min<int64_t>(cap, vol->n_blocks);
     // Free slots' values are never read (a slot is written by its decode
     // before any lookup can reach it), so only the slot maps are reset.
-    slot_values.grow(phys * 64, st);
-    block_of_slot.grow(phys, st);
-    last_used.grow(phys, st);
+    reserve_slots(phys);
     WC_CUDA(cudaMemsetAsync(block_of_slot.p, 0xFF, 4 * phys, st));
     WC_CUDA(cudaMemsetAsync(last_used.p, 0, 4 * phys, st));
     pass_no = 0;
@@ -1615,27 +1615,39 @@ void Session::cache_lookup() {
     WC_LAUNCH_CHECK();
 }
 
+// Physical slot storage for `need` logical slots.  The logical capacity
+// follows the reference (cache.py:74-75); the allocation grows geometrically
+// (first to 2 slots per ray) because every growth is a cudaMalloc + copy of
+// up to GBs: once per new maximum, not once per frame.  Slots past `phys` are
+// never read.
+void Session::reserve_slots(int64_t need) {
+    if (need <= slot_alloc) return;
+    const int64_t target = std::max<int64_t>(
+        need, std::min<int64_t>(vol->n_blocks, std::max<int64_t>(2 * n, slot_alloc + slot_alloc / 2)));
+    slot_values.grow(target * 64, st);
+    block_of_slot.grow(target, st);
+    last_used.grow(target, st);
+    cand_off.alloc(target);
+    cand_key.alloc(target);
+    cand_val.alloc(target);
+    const int64_t words =
+        scan_scratch_words(std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n, target}));
+    if (partials.n < words) {
+        partials.ensure(words);
+        WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
+    }
+    slot_alloc = target;
+}
+
 void Session::ensure_resident(int64_t n_actb, int64_t n_miss, int64_t &n_evict) {
     if (n_actb > cap) {  // cache.py:74-75: grow to ceil(1.5 * needed)
         cap = (3 * n_actb + 1) / 2;
         const int64_t new_phys = std::min<int64_t>(cap, vol->n_blocks);
         if (new_phys > phys) {
-            slot_values.grow(new_phys * 64, st);  // keeps resident slots (cache.py:42-53)
-            block_of_slot.grow(new_phys, st);
-            last_used.grow(new_phys, st);
+            reserve_slots(new_phys);  // keeps resident slots (cache.py:42-53)
             WC_CUDA(cudaMemsetAsync(block_of_slot.p + phys, 0xFF, 4 * (new_phys - phys), st));
             WC_CUDA(cudaMemsetAsync(last_used.p + phys, 0, 4 * (new_phys - phys), st));
             phys = new_phys;
-        }
-    }
-    if (cand_off.n < phys) {
-        cand_off.alloc(phys);
-        cand_key.alloc(phys);
-        cand_val.alloc(phys);
-        const int64_t words = scan_scratch_words(std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n, phys}));
-        if (partials.n < words) {
-            partials.ensure(words);
-            WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
         }
     }
     n_evict = 0;
@@ -1753,7 +1765,7 @@ bool Session::pass(PassStatsC &stats) {
             WC_LAUNCH_CHECK();
         }
         WC_CUDA(cudaEventRecord(ev_stage[4], st));
-        contrib.ensure(2 * nvis);
+        contrib.ensure(2 * nvis);  // nvis <= n: sized 2 n at creation
         k_contrib<<<grid_for(nvis, 256), 256, 0, st>>>(visible_ids.p, nvis, slot_of_block.p, vol->bdx, vol->bdy,
                                                        vol->bdz, contrib.p, counters.p + C_ERR);
         WC_LAUNCH_CHECK();
@@ -1834,9 +1846,11 @@ bool Session::pass(PassStatsC &stats) {
     static const bool trace = getenv("WAVECAST_TRACE") != nullptr;
     if (trace)
         fprintf(stderr, "[wavecast] pass %lld n_act %lld n_spec %lld entries %lld visible %lld active %lld miss %lld "
-                        "evict %lld items %u after %lld\n",
+                        "evict %lld items %u after %lld cap %lld phys %lld gpu %.3f ms host %.3f ms\n",
                 (long long)pass_index, (long long)n_act, (long long)n_spec, (long long)n_ent, (long long)nvis,
-                (long long)nactb, (long long)n_miss, (long long)n_evict, h_counters.p[C_NITEMS], (long long)n_after);
+                (long long)nactb, (long long)n_miss, (long long)n_evict, h_counters.p[C_NITEMS], (long long)n_after,
+                (long long)cap, (long long)phys, (double)last_kernel_ms,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count() * 1e3);
     stats.pass_index = pass_index;
     stats.n_active_before = n_act;
     stats.n_spec = n_spec;

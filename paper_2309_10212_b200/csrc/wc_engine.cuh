@@ -83,6 +83,7 @@ struct Session {
     DevBuf<float> depth;
     // cache (cache.py)
     int64_t cap = 0, phys = 0, hw = 0;
+    int64_t slot_alloc = 0;  // allocated slots (>= phys, grown geometrically)
     int32_t pass_no = 0;
     DevBuf<float> slot_values;
     DevBuf<int32_t> block_of_slot, last_used, slot_of_block;
@@ -120,6 +121,7 @@ struct Session {
    private:
     void read_counters(int first, int count);
     void cache_lookup();
+    void reserve_slots(int64_t need);
     void launch_stamp_hist();
     void ensure_resident(int64_t n_actb, int64_t n_miss, int64_t &n_evict);
     void select_victims(int64_t n_cand, int64_t n_evict);

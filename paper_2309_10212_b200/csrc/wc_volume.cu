@@ -262,6 +262,68 @@ void Volume::build_grids() {
     build_range_index();
 }
 
+// ------------------------------------------------------ decoded value range
+
+__device__ __forceinline__ uint32_t fkey(float f) {  // order-preserving (no NaN: decoded q/S * 2^e)
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+static float fkey_inv(uint32_t k) {
+    const uint32_t b = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+    float f;
+    memcpy(&f, &b, 4);
+    return f;
+}
+
+// min / max of the decoded voxels inside dims (oracle.py:22-39 value_range,
+// padding dropped); warp per block.
+__global__ void __launch_bounds__(256) k_decoded_range(const uint8_t *__restrict__ payload, int qbits, int stride,
+                                                       int nx, int ny, int nz, int bdx, int bdy, int64_t n_blocks,
+                                                       uint32_t *ext) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+    for (int64_t b = warp0; b < n_blocks; b += nwarps) {
+        const int bx = (int)(b % bdx), by = (int)((b / bdx) % bdy), bz = (int)(b / ((int64_t)bdx * bdy));
+        float v[2];
+        decode_block_warp(reinterpret_cast<const uint32_t *>(payload + b * stride), stride >> 2, qbits, lane, v[0],
+                          v[1]);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int i = lane + 32 * h;
+            if (4 * bx + (i & 3) < nx && 4 * by + ((i >> 2) & 3) < ny && 4 * bz + (i >> 4) < nz) {
+                lo = min(lo, fkey(v[h]));
+                hi = max(hi, fkey(v[h]));
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+        atomicMin(ext, lo);
+        atomicMax(ext + 1, hi);
+    }
+}
+
+void decoded_value_range(const Volume &v, float *lo, float *hi) {
+    DevBuf<uint32_t> ext;
+    ext.alloc(2);
+    const uint32_t init[2] = {0xFFFFFFFFu, 0u};
+    WC_CUDA(cudaMemcpyAsync(ext.p, init, sizeof(init), cudaMemcpyHostToDevice, v.st));
+    k_decoded_range<<<grid_for(v.n_blocks * 32, 256, 8), 256, 0, v.st>>>(v.payload.p, v.qbits, v.stride, v.nx, v.ny,
+                                                                         v.nz, v.bdx, v.bdy, v.n_blocks, ext.p);
+    WC_LAUNCH_CHECK();
+    uint32_t h[2];
+    WC_CUDA(cudaMemcpyAsync(h, ext.p, sizeof(h), cudaMemcpyDeviceToHost, v.st));
+    WC_CUDA(cudaStreamSynchronize(v.st));
+    *lo = fkey_inv(h[0]);
+    *hi = fkey_inv(h[1]);
+}
+
 // ------------------------------------------------------------- range index
 
 // order-preserving uint64 key of a double (for atomicMin/Max)

@@ -141,3 +141,71 @@ def render_sharded(cv, grids, cam, iso, opts, tile: int = 32, group=None):
         return None, stats
     rgba, depth = out
     return Framebuffer(opts.width, opts.height, rgba, depth, 1.0), stats
+
+
+class _DeviceBytes:
+    """``__cuda_array_interface__`` view of raw device memory, so torch (and
+    NCCL through torch.distributed) can write straight into library buffers."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False),
+                                         "version": 3}
+
+
+def broadcast_volume(cv, src: int = 0, group=None):
+    """Give every rank the same compressed volume.
+
+    Rank ``src`` passes its CompressedVolume (e.g. from ``codec.load_wcz``);
+    the other ranks pass None.  Over NCCL the payload and raw ranges are
+    broadcast from the source's HBM straight into a volume the receivers
+    allocated on their GPU (``wc_volume_alloc`` / ``wc_volume_device_buffers``),
+    and each receiver builds its grids locally (``wc_volume_finalize``; the
+    grids are a pure function of payload and ranges, grids.py:71-94), so no
+    rank stages 16.6 GB through host memory.  Over gloo (CPU tests) the host
+    arrays are broadcast instead and host-backed volumes are returned."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib
+    from .codec import CompressedVolume
+
+    rank = dist.get_rank(group)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+    meta = torch.zeros(4, dtype=torch.int64, device=dev)
+    if rank == src:
+        meta[:] = torch.tensor([*cv.dims, cv.qbits], dtype=torch.int64)
+    dist.broadcast(meta, src, group)
+    dims, qbits = tuple(int(x) for x in meta[:3].tolist()), int(meta[3])
+    if not nccl:
+        if rank == src:
+            pay = torch.from_numpy(cv.payload.copy())
+            rng = torch.from_numpy(cv.raw_block_ranges.reshape(-1).copy())
+        else:
+            from .codec import _block_dims, block_stride_bytes
+
+            bd = _block_dims(dims)
+            nb = bd[0] * bd[1] * bd[2]
+            pay = torch.empty(nb * block_stride_bytes(qbits), dtype=torch.uint8)
+            rng = torch.empty(2 * nb, dtype=torch.float32)
+        dist.broadcast(pay, src, group)
+        dist.broadcast(rng, src, group)
+        if rank == src:
+            return cv
+        return CompressedVolume(dims, qbits, payload=pay.numpy(), raw_block_ranges=rng.numpy().reshape(-1, 2))
+    if rank != src:
+        h = C.c_void_p()
+        _lib.call("wc_volume_alloc", *dims, qbits, C.byref(h))
+        cv = CompressedVolume(dims, qbits, handle=h)
+    pp, pb, rp, rb = C.c_void_p(), C.c_uint64(), C.c_void_p(), C.c_uint64()
+    _lib.call("wc_volume_device_buffers", cv.device_handle(), C.byref(pp), C.byref(pb), C.byref(rp), C.byref(rb))
+    torch.cuda.synchronize()  # the source's volume stream has finished writing
+    for p_, n_ in ((pp, pb), (rp, rb)):
+        t = torch.as_tensor(_DeviceBytes(p_.value, n_.value), device=dev)
+        dist.broadcast(t, src, group)
+    torch.cuda.synchronize()
+    if rank != src:
+        _lib.call("wc_volume_finalize", cv.device_handle())
+    return cv

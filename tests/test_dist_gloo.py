@@ -65,3 +65,45 @@ def test_gloo_tile_gather_stitches_bit_exact(world):
         p.join(timeout=120)
         assert p.exitcode == 0
     assert ok and hits > 0
+
+
+def _bcast_worker(rank, world, port, q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as orc
+    from paper_2309_10212_b200 import dist as wdist
+    from paper_2309_10212_b200.codec import CompressedVolume
+
+    dims = (13, 9, 11)
+    v = np.random.default_rng(7).uniform(-2, 5, int(np.prod(dims))).astype(np.float32)
+    pay, ranges, _ = orc.compress(v, dims, 12)
+    cv = CompressedVolume(dims, 12, payload=pay, raw_block_ranges=ranges) if rank == 0 else None
+    got = wdist.broadcast_volume(cv, src=0)
+    ok = (got.dims == dims and got.qbits == 12 and np.array_equal(got.payload, pay)
+          and np.array_equal(got.raw_block_ranges, ranges))
+    q.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+def test_gloo_volume_broadcast():
+    # host orchestration of dist.broadcast_volume (metadata, sizes, payload and
+    # ranges); on NCCL the same calls write straight into the receivers' HBM
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert res == {0: True, 1: True}

@@ -262,3 +262,80 @@ def test_session_reset_reuses_allocations(wc):
         assert np.array_equal(fb.depth.reshape(-1), depth), i
         assert [s.new_decompressed for s in stats] == [s["new_decompressed"] for s in ost], i
         assert [s.cache_slots for s in stats] == [s["cache_slots"] for s in ost], i
+
+
+# ------------------------------------------------- volume I/O (§8(f) row 2)
+def test_load_wcz_streams_to_device(wc, tmp_path):
+    vol = host_volume("value_noise", (150, 131, 170), seed=2)
+    cv = wc.compress_volume(vol, 16)
+    p = tmp_path / "v.wcz"
+    wc.write_wcz(cv, p)
+    # 1 MiB chunks: the 10 MB payload crosses both pinned buffers many times
+    dv = wc.codec.load_wcz(p, chunk_bytes=1 << 20)
+    assert dv.dims == cv.dims and dv.qbits == 16
+    assert np.array_equal(dv.payload, cv.payload)
+    assert np.array_equal(dv.raw_block_ranges.view(np.uint32), cv.raw_block_ranges.view(np.uint32))
+    g0, g1 = wc.build_grids(cv), wc.build_grids(dv)
+    for k in ("fine_min", "fine_max", "coarse_min", "coarse_max"):
+        assert np.array_equal(getattr(g0, k), getattr(g1, k)), k
+    with pytest.raises(wc.DataError):
+        (tmp_path / "t.wcz").write_bytes(p.read_bytes()[:-3])
+        wc.codec.load_wcz(tmp_path / "t.wcz")
+
+
+def test_volume_alloc_fill_finalize_matches_upload(wc):
+    # the receiving side of dist.broadcast_volume on one GPU: allocate, write
+    # payload + ranges into the device buffers through __cuda_array_interface__
+    # views, finalize -> same grids as a volume uploaded from the host
+    import ctypes as C
+
+    import torch
+
+    from paper_2309_10212_b200 import _lib, dist
+
+    vol = host_volume("sphere", 48)
+    cv = wc.compress_volume(vol, 12)
+    h = C.c_void_p()
+    _lib.call("wc_volume_alloc", *cv.dims, cv.qbits, C.byref(h))
+    rv = wc.CompressedVolume(cv.dims, cv.qbits, handle=h)
+    pp, pb, rp, rb = C.c_void_p(), C.c_uint64(), C.c_void_p(), C.c_uint64()
+    _lib.call("wc_volume_device_buffers", h, C.byref(pp), C.byref(pb), C.byref(rp), C.byref(rb))
+    assert pb.value == cv.payload.nbytes and rb.value == cv.raw_block_ranges.nbytes
+    torch.as_tensor(dist._DeviceBytes(pp.value, pb.value), device="cuda").copy_(torch.from_numpy(cv.payload))
+    torch.as_tensor(dist._DeviceBytes(rp.value, rb.value), device="cuda").copy_(
+        torch.from_numpy(cv.raw_block_ranges.reshape(-1).view(np.uint8)))
+    torch.cuda.synchronize()
+    _lib.call("wc_volume_finalize", h)
+    assert np.array_equal(rv.payload, cv.payload)
+    g0, g1 = wc.build_grids(cv), wc.build_grids(rv)
+    for k in ("fine_min", "fine_max", "coarse_min", "coarse_max"):
+        assert np.array_equal(getattr(g0, k), getattr(g1, k)), k
+
+
+def test_decoded_value_range_matches_oracle(wc):
+    for kind, n, q in (("value_noise", (37, 29, 45), 16), ("gaussians", 40, 9)):
+        vol = host_volume(kind, n, seed=0)
+        cv = wc.compress_volume(vol, q)
+        dense = orc.decode_full(oracle_volume(cv))
+        lo, hi = wc.codec.decoded_value_range(cv)
+        assert (lo, hi) == (float(dense.min()), float(dense.max()))
+
+
+# --------------------------------------------- bench protocol (§8(f) row 4)
+def test_bench_report_matches_reference(wc):
+    # cmd_bench's report (cli.py:136-195) from the device path equals the one
+    # the reference wrote for the same .wcz and arguments
+    # (tests/golden/make_bench_golden.py)
+    import json
+    import os
+
+    from paper_2309_10212_b200.benchmark import bench_report
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    gold = json.load(open(os.path.join(here, "bench_small_report.json")))
+    a = gold["args"]
+    kw = {a[i].lstrip("-").replace("-", "_"): int(a[i + 1]) for i in range(0, len(a), 2)}
+    cv = wc.read_wcz(os.path.join(here, "bench_small.wcz"))
+    rep, tim = bench_report(cv, wc.build_grids(cv), volume="bench_small.wcz", **kw)
+    assert rep == gold["report"]
+    assert len(tim["frame_ms"]) == rep["n_renders"] and all(t > 0 for t in tim["frame_ms"])

@@ -95,6 +95,38 @@ def test_wcz_errors(tmp_path):
         wc.read_wcz(tmp_path / "s.wcz")
 
 
+def test_native_wcz_probe_matches_read_wcz(tmp_path):
+    # the device loader's header checks (wc_wcz_probe, host only) raise what
+    # read_wcz raises, with the reference's messages (codec.py:246-262)
+    cv = _host_cv((9, 10, 11), 14)
+    good = tmp_path / "g.wcz"
+    wc.write_wcz(cv, good)
+    assert wc.codec.probe_wcz(good) == ((9, 10, 11), 14, cv.block_stride_bytes, cv.block_count)
+    blob = good.read_bytes()
+    nb = cv.block_count
+    cases = {
+        "magic.wcz": (b"NOPE" + blob[4:], wc.DataError, "not a WCZ1 container"),
+        "short.wcz": (blob[:20], wc.DataError, "not a WCZ1 container"),
+        "version.wcz": (blob[:4] + (2).to_bytes(4, "little") + blob[8:], wc.DataError,
+                        "unsupported container version 2"),
+        "qbits.wcz": (blob[:20] + (30).to_bytes(4, "little") + blob[24:], wc.UsageError,
+                      "qbits must be in [4, 26], got 30"),
+        "stride.wcz": (blob[:24] + (999).to_bytes(4, "little") + blob[28:], wc.DataError,
+                       "stride 999 inconsistent with qbits 14"),
+        "size.wcz": (blob[:-1], wc.DataError,
+                     f"expected {28 + 8 * nb + nb * cv.block_stride_bytes} bytes, found {len(blob) - 1}"),
+    }
+    for name, (data, exc, msg) in cases.items():
+        p = tmp_path / name
+        p.write_bytes(data)
+        for fn in (wc.read_wcz, wc.codec.probe_wcz):
+            with pytest.raises(exc) as ei:
+                fn(p)
+            assert msg in str(ei.value), (name, fn.__name__, str(ei.value))
+            if exc is wc.DataError:
+                assert str(ei.value).startswith(str(p)), str(ei.value)
+
+
 def test_block_id_round_trip():  # test_codec.py:71-83
     cv = _host_cv((16, 16, 16), 8)
     assert cv.block_dims == (4, 4, 4) and cv.block_id(1, 2, 3) == 57
