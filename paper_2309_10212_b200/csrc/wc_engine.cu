@@ -999,6 +999,29 @@ struct SlotField {
     }
 };
 
+// SlotField with the 8 contributor slots as row pointers in shared memory
+// (octant-major, one column per thread: conflict-free), so a lattice lookup
+// is one LDS.64 plus an offset instead of a 7-way select and a slot multiply.
+// Missing neighbours (slot -1) point at a zero row.
+__device__ float g_zero_row[64];
+
+template <int kThreads>
+struct SlotFieldSmem {
+    const float *const *rows;  // &table[0][threadIdx.x], stride kThreads
+    __device__ __forceinline__ static void fill(const float **col, const float *sv, const int s[8]) {
+#pragma unroll
+        for (int o = 0; o < 8; o++) col[o * kThreads] = s[o] >= 0 ? sv + (int64_t)s[o] * 64 : g_zero_row;
+    }
+    __device__ __forceinline__ float point(int x, int y, int z) const {
+        const int o = (x >> 2) | ((y >> 2) << 1) | ((z >> 2) << 2);
+        return __ldg(rows[o * kThreads] + ((x & 3) + 4 * (y & 3) + 16 * (z & 3)));
+    }
+    __device__ __forceinline__ void corners(int lx, int ly, int lz, float c[8]) const {
+#pragma unroll
+        for (int idx = 0; idx < 8; idx++) c[idx] = point(lx + (idx & 1), ly + ((idx >> 1) & 1), lz + (idx >> 2));
+    }
+};
+
 struct DenseFieldView {  // fully decoded volume, x-fastest
     const float *p;
     int64_t sy, sz;
@@ -1122,6 +1145,8 @@ __device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, int64_t j) 
 __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
     const RaytraceArgs &a = s.a;
     const int lane = threadIdx.x & 31;
+    __shared__ const float *rowtab[8][128];
+    const SlotFieldSmem<128> sf{&rowtab[0][threadIdx.x]};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     // warp-uniform trip count: the list append below is a full-warp scan
     for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); j0 < a.n_ent; j0 += stride) {
@@ -1129,10 +1154,18 @@ __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
         // the <= 10 bracketing cells of the walk, 6-bit local codes in DDA order
         int found = 0;
         unsigned long long codes = 0;
+        uint32_t ek = 0, er = 0, eb = 0;  // kept for the item write-out
+        SlotField ef{a.slot_values, -1, -1, -1, -1, -1, -1, -1, -1};
         if (j < a.n_ent) {
             const EntryCtx e = entry_ctx(a, j);
+            ek = e.k;
+            er = (uint32_t)e.r;
+            eb = (uint32_t)(e.bx + a.bdx * (e.by + a.bdy * e.bz));
+            ef = e.field;
             s.best[e.k] = WC_UINT_MAX;
-            walk_bracketing_cells(e.field, 4 * e.bx, 4 * e.by, 4 * e.bz, 4 * e.bx, 4 * e.by, 4 * e.bz, e.cx, e.cy,
+            const int sl[8] = {ef.s0, ef.s1, ef.s2, ef.s3, ef.s4, ef.s5, ef.s6, ef.s7};
+            SlotFieldSmem<128>::fill(&rowtab[0][threadIdx.x], a.slot_values, sl);
+            walk_bracketing_cells(sf, 4 * e.bx, 4 * e.by, 4 * e.bz, 4 * e.bx, 4 * e.by, 4 * e.bz, e.cx, e.cy,
                                   e.cz, e.o, e.d, e.te, a.iso, [&](int cx, int cy, int cz, int seq) {
                                       const uint32_t lc = (uint32_t)((cx - 4 * e.bx) | ((cy - 4 * e.by) << 2) |
                                                                      ((cz - 4 * e.bz) << 4));
@@ -1154,16 +1187,14 @@ __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
         first = __shfl_sync(0xffffffffu, first, 31) + incl - (uint32_t)found;
         if (found) {
             // the corners were just walked: these loads hit L1
-            const EntryCtx e = entry_ctx(a, j);
-            const uint32_t b = a.visible_ids[a.ent_key[j]];
             for (int q = 0; q < found; q++) {
                 const uint32_t it = first + q;
                 if (it < s.item_cap) {
                     const uint32_t lc = (uint32_t)(codes >> (6 * q)) & 63u;
                     const int lx = lc & 3, ly = (lc >> 2) & 3, lz = lc >> 4;
                     float c[8];
-                    e.field.corners(lx, ly, lz, c);
-                    s.item_info[it] = make_uint4(e.k, (uint32_t)e.r, b,
+                    sf.corners(lx, ly, lz, c);
+                    s.item_info[it] = make_uint4(ek, er, eb,
                                                  (uint32_t)(lx | (ly << 3) | (lz << 6)) | ((uint32_t)q << 9));
                     s.item_corners[2 * (int64_t)it] = make_float4(c[0], c[1], c[2], c[3]);
                     s.item_corners[2 * (int64_t)it + 1] = make_float4(c[4], c[5], c[6], c[7]);
