@@ -11,8 +11,11 @@
 
 namespace wc {
 
+#ifndef WC_SCAN_IPT
+#define WC_SCAN_IPT 4
+#endif
 constexpr int kScanThreads = 256;
-constexpr int kScanIPT = 8;
+constexpr int kScanIPT = WC_SCAN_IPT;
 constexpr int kScanTile = kScanThreads * kScanIPT;  // 2048 items per CTA
 
 // Loaders: value of element i as uint32.
