@@ -473,12 +473,7 @@ int wc_session_pass(wc_session *s, wc_pass_stats *stats, int *ran) {
 
 int wc_session_run(wc_session *s, wc_pass_stats *stats_out, int64_t max_stats, int64_t *n_passes) {
     WC_API_BEGIN
-    int64_t k = 0;
-    wc::PassStatsC st{};
-    while (s->s->pass(st)) {
-        if (stats_out && k < max_stats) std::memcpy(stats_out + k, &st, sizeof(st));
-        k++;
-    }
+    const int64_t k = s->s->run_frame(reinterpret_cast<wc::PassStatsC *>(stats_out), stats_out ? max_stats : 0);
     if (n_passes) *n_passes = k;
     WC_API_END
 }
@@ -487,19 +482,14 @@ int wc_session_render(wc_session *s, const wc_camera *cam, double iso, wc_pass_s
                       int64_t *n_passes) {
     WC_API_BEGIN
     s->s->reset(reinterpret_cast<const wc::CameraParams *>(cam), iso);
-    int64_t k = 0;
-    wc::PassStatsC st{};
-    while (s->s->pass(st)) {
-        if (stats_out && k < max_stats) std::memcpy(stats_out + k, &st, sizeof(st));
-        k++;
-    }
+    const int64_t k = s->s->run_frame(reinterpret_cast<wc::PassStatsC *>(stats_out), stats_out ? max_stats : 0);
     if (n_passes) *n_passes = k;
     WC_API_END
 }
 
 int wc_session_n_active(const wc_session *s, int64_t *n_active) {
     WC_API_BEGIN
-    *n_active = s->s->n_act;
+    *n_active = s->s->active_count();
     WC_API_END
 }
 
@@ -543,7 +533,7 @@ int wc_session_frame_ms(wc_session *s, double *ms) {
 int wc_session_stage_ms(const wc_session *s, double *ms6) {
     WC_API_BEGIN
     for (int k = 0; k < wc::Session::kStages; k++) ms6[k] = s->s->stage_ms[k];
-    ms6[wc::Session::kStages] = s->s->reset_ms;
+    ms6[wc::Session::kStages] = s->s->reset_device_ms();
     WC_API_END
 }
 
@@ -593,7 +583,7 @@ int wc_session_slots(const wc_session *s, uint32_t *block_slots, uint32_t *ray_s
     download(block_slots, S.block_slots.p, S.last_slots_used, S.st);
     download(ray_slots, S.ray_slots.p, S.last_slots_used, S.st);
     const int64_t n_prev = S.last_slots_used / (S.last_n_spec ? S.last_n_spec : 1);
-    download(active_list, S.act_list[S.cur ^ 1].p, n_prev, S.st);
+    download(active_list, S.act_list[(S.pass_index - 1) & 1].p, n_prev, S.st);  // the last pass's list
     WC_CUDA(cudaStreamSynchronize(S.st));
     WC_API_END
 }

@@ -193,7 +193,9 @@ __global__ void k_compact_index(Pred pred, int64_t n, const uint32_t *off, uint3
         if (pred(i)) out[off[i]] = (uint32_t)i;
 }
 
-__global__ void k_compact_keep(const uint32_t *keep, const uint32_t *off, const uint32_t *in, int64_t n, uint32_t *out) {
+__global__ void k_compact_keep(const uint32_t *keep, const uint32_t *off, const uint32_t *in, const uint32_t *d_n,
+                               uint32_t *out) {
+    const int64_t n = *d_n;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         if (keep[i]) out[off[i]] = in[i];
 }
@@ -248,7 +250,8 @@ struct TraverseArgs {
     int fdx, fdy, fdz, cdx, cdy, cdz;
     double iso;
     uint32_t *block_slots, *ray_slots, *emitted, *vis_bm;
-    uint32_t *work;  // persistent-kernel ray counter (zeroed per pass)
+    uint32_t *work;        // persistent-kernel ray counter (zeroed per pass)
+    const uint32_t *ctl;   // control block: n_act and n_spec of the pass (Counter)
 };
 
 // Mark block b visible: one RED.OR per distinct block among the lanes that
@@ -310,7 +313,10 @@ __device__ __forceinline__ int fine_local(const Dda &f) { return (f.cx & 3) + 4 
 // Every emitted slot, saved iterator and exit flag is the reference's, bit
 // for bit.
 template <int CA>
-__global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(TraverseArgs a) {
+__global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(TraverseArgs a_in) {
+    TraverseArgs a = a_in;
+    a.n_act = a.ctl[C_NACT];
+    a.n_spec = (int)a.ctl[C_NSPEC];
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
@@ -517,7 +523,10 @@ __device__ __forceinline__ Dda shfl_dda(const Dda &s, int src) {
 // which cells emit, where the n_spec-th emit or the descent happens, and
 // where the ray leaves.  The lane that simulated exactly that many steps
 // holds the reference's iterator state and shuffles it to the warp.
-__global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a) {
+__global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a_in) {
+    TraverseArgs a = a_in;
+    a.n_act = a.ctl[C_NACT];
+    a.n_spec = (int)a.ctl[C_NSPEC];
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
@@ -810,10 +819,11 @@ __global__ void k_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvi
 // Entries of active ray i: k = entry_off[i] + j for its j-th emitted slot
 // (== valid_prefix of the slot, engine.py:124-128).  Key = rank of the block
 // among visible ids (bitmap rank), value = k.
-__global__ void k_build_entries(int64_t n_act, int n_spec, const uint32_t *act_list, const uint32_t *emitted,
+__global__ void k_build_entries(const uint32_t *ctl, const uint32_t *act_list, const uint32_t *emitted,
                                 const uint32_t *entry_off, const uint32_t *block_slots, const uint32_t *vis_bm,
                                 const uint32_t *vis_word_off, uint32_t *ent_key, uint32_t *ent_val, uint32_t *ent_ray) {
     // thread per slot (i, j): no per-ray serial chain of rank lookups
+    const int64_t n_act = ctl[C_NACT], n_spec = ctl[C_NSPEC];
     const int64_t n_slots = n_act * n_spec;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_slots; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = t / n_spec;
@@ -851,9 +861,10 @@ __global__ void k_cache_stamp(const uint32_t *ids, const uint32_t *d_n, int64_t 
 
 // eviction candidates (resident, stamp < pass_no) per stamp value
 // (few distinct stamps: per-CTA shared-memory bins, one global add per bin)
-__global__ void k_stamp_hist(const int32_t *block_of_slot, const int32_t *last_used, int64_t hw, int32_t pass_no,
-                             uint32_t *hist) {
+__global__ void k_stamp_hist(const int32_t *block_of_slot, const int32_t *last_used, const uint32_t *ctl,
+                             int32_t pass_no, uint32_t *hist) {
     extern __shared__ uint32_t sh[];
+    const int64_t hw = ctl[C_NACT] ? ctl[C_HW] : 0;
     for (int b = threadIdx.x; b < pass_no; b += blockDim.x) sh[b] = 0;
     __syncthreads();
     // few distinct stamps: one shared atomic per (warp, stamp) via match_any
@@ -883,13 +894,50 @@ __global__ void k_mark_stamp(const int32_t *block_of_slot, const int32_t *last_u
     }
 }
 
-__global__ void k_blocks_to_slots(const uint32_t *blocks, int64_t n, const int32_t *slot_of_block, uint32_t *slots) {
+// Candidates (resident, not stamped this pass) with stamp L <= L* marked in
+// the block bitmap of region L: one extraction over regions 0..L* then lists
+// them in (last_used, block_id) order (cache.py:84-91).
+__global__ void k_mark_victims(const int32_t *block_of_slot, const int32_t *last_used, const uint32_t *ctl,
+                               int32_t pass_no, int64_t nwords, uint32_t *regions) {
+    if (ctl[C_NEVICT] == 0) return;
+    const int64_t hw = ctl[C_HW];
+    const int32_t lstar = (int32_t)ctl[C_LSTAR];
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < hw; s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t b = block_of_slot[s];
+        const int32_t lu = last_used[s];
+        if (b >= 0 && lu < pass_no && lu <= lstar)
+            atomicOr(&regions[(int64_t)lu * nwords + (b >> 5)], 1u << (b & 31));
+    }
+}
+
+// bitmap_extract sink over the concatenated regions: block ids in (region,
+// id) order; each word is cleared once read (the regions start the next
+// pass empty without a memset)
+struct SinkRegions {
+    uint32_t *bm, *ids;
+    int64_t nwords;
+    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const {
+        uint32_t v = bm[i];
+        if (!v) return;
+        bm[i] = 0;
+        const uint32_t base = (uint32_t)((i % nwords) * 32);
+        while (v) {
+            ids[prefix++] = base + __ffs(v) - 1;
+            v &= v - 1;
+        }
+    }
+};
+
+__global__ void k_blocks_to_slots(const uint32_t *blocks, const uint32_t *d_n, const int32_t *slot_of_block,
+                                  uint32_t *slots) {
+    const int64_t n = *d_n;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         slots[i] = (uint32_t)slot_of_block[blocks[i]];
 }
 
 // BlockCache reset: forget every resident block of the previous frame
-__global__ void k_cache_unmap(const int32_t *block_of_slot, int64_t phys, int32_t *slot_of_block) {
+__global__ void k_cache_unmap(const int32_t *block_of_slot, const uint32_t *d_phys, int32_t *slot_of_block) {
+    const int64_t phys = *d_phys;
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < phys; s += (int64_t)gridDim.x * blockDim.x) {
         const int32_t b = block_of_slot[s];
         if (b >= 0) slot_of_block[b] = -1;
@@ -903,7 +951,9 @@ __global__ void k_gather_last_used(const uint32_t *val, int64_t n, const int32_t
 
 // cache.py:90-95: unmap the first n_evict candidates (they become the
 // slots of the last n_evict misses, cache.py:96-97)
-__global__ void k_evict(const uint32_t *victims, int64_t n_evict, int32_t *block_of_slot, int32_t *slot_of_block) {
+__global__ void k_evict(const uint32_t *victims, const uint32_t *d_n_evict, int32_t *block_of_slot,
+                        int32_t *slot_of_block) {
+    const int64_t n_evict = *d_n_evict;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_evict; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t s = victims[i];
         slot_of_block[block_of_slot[s]] = -1;
@@ -917,12 +967,11 @@ __global__ void k_evict(const uint32_t *victims, int64_t n_evict, int32_t *block
 // miss count is read on the device (no host round trip).
 __global__ void __launch_bounds__(256, 3)
     k_decode_insert(const uint8_t *__restrict__ payload, int qbits, int stride, const uint32_t *__restrict__ miss_ids,
-                    const uint32_t *d_n_miss, int64_t hw, int64_t n_free, const uint32_t *__restrict__ victims,
-                    float *__restrict__ slot_values, int32_t *block_of_slot, int32_t *last_used,
-                    int32_t *slot_of_block, int32_t pass_no, uint32_t *d_hw, int64_t cap) {
+                    uint32_t *ctl, const uint32_t *__restrict__ victims, float *__restrict__ slot_values,
+                    int32_t *block_of_slot, int32_t *last_used, int32_t *slot_of_block, int32_t pass_no) {
     const int lane = threadIdx.x & 31;
-    const int64_t n_miss = *d_n_miss;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *d_hw = (uint32_t)(n_miss <= n_free ? hw + n_miss : cap);
+    const int64_t n_miss = ctl[C_NMISS], hw = ctl[C_HW], n_free = ctl[C_NFREE], cap = ctl[C_CAP];
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl[C_HW_NEXT] = (uint32_t)(n_miss <= n_free ? hw + n_miss : cap);
     const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     // A warp takes 32 consecutive misses: one coalesced load of their ids,
@@ -1040,8 +1089,9 @@ struct DenseFieldView {  // fully decoded volume, x-fastest
 
 // engine.py:286-305 _contributor_table: cache slots of each visible block
 // and its 7 +octant neighbours (-1 outside the volume), 32 B per block.
-__global__ void k_contrib(const uint32_t *visible_ids, int64_t nvis, const int32_t *slot_of_block, int bdx, int bdy,
-                          int bdz, int4 *contrib, uint32_t *err) {
+__global__ void k_contrib(const uint32_t *visible_ids, const uint32_t *d_nvis, const int32_t *slot_of_block, int bdx,
+                          int bdy, int bdz, int4 *contrib, uint32_t *err) {
+    const int64_t nvis = *d_nvis;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvis; v += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t b = visible_ids[v];
         const int bx = (int)(b % (uint32_t)bdx), by = (int)((b / (uint32_t)bdx) % (uint32_t)bdy),
@@ -1069,6 +1119,7 @@ struct RaytraceArgs {
     RayView rays;
     double iso, br, bg, bb;
     float4 *rgbz;
+    const uint32_t *d_n_ent;  // entry count on the device (Counter C_NENT)
 };
 
 // engine.py:161-219 _raytrace_visible_kernel, one thread per ray-block entry
@@ -1077,7 +1128,8 @@ struct RaytraceArgs {
 // tracer (blocktrace.py:317-449) over the block's <= 4^3 dual cells and
 // writes (rgb, z) -- or (0, 0, 0, +inf) on a miss -- at its entry id.
 __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_raytrace(RaytraceArgs a) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n_ent; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n_ent = *a.d_n_ent;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_ent; j += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t v = a.ent_key[j], k = a.ent_val[j];
         const int64_t r = a.ent_ray[k];
         const uint32_t b = a.visible_ids[v];
@@ -1149,14 +1201,15 @@ __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
     const SlotFieldSmem<128> sf{&rowtab[0][threadIdx.x]};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     // warp-uniform trip count: the list append below is a full-warp scan
-    for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); j0 < a.n_ent; j0 += stride) {
+    const int64_t n_ent = *a.d_n_ent;
+    for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); j0 < n_ent; j0 += stride) {
         const int64_t j = j0 + lane;
         // the <= 10 bracketing cells of the walk, 6-bit local codes in DDA order
         int found = 0;
         unsigned long long codes = 0;
         uint32_t ek = 0, er = 0, eb = 0;  // kept for the item write-out
         SlotField ef{a.slot_values, -1, -1, -1, -1, -1, -1, -1, -1};
-        if (j < a.n_ent) {
+        if (j < n_ent) {
             const EntryCtx e = entry_ctx(a, j);
             ek = e.k;
             er = (uint32_t)e.r;
@@ -1230,7 +1283,8 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArg
 // phase 3: shade each entry's winning cell (or record the miss)
 __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
     const RaytraceArgs &a = s.a;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < a.n_ent; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n_ent = *a.d_n_ent;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_ent; j += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t k = a.ent_val[j];
         const uint32_t bst = s.best[k];
         if (bst == WC_UINT_MAX) {
@@ -1258,9 +1312,10 @@ __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
 
 // engine.py:222-258 _composite_kernel: closest speculated hit per active
 // ray (strict <, earliest entry wins ties), then terminate or keep.
-__global__ void k_composite(int64_t n_act, const uint32_t *act_list, const uint32_t *emitted, const uint32_t *entry_off,
-                            const float4 *rgbz, const uint8_t *exited, uint8_t *status, uint32_t *rgba, float *depth,
-                            uint32_t *keep) {
+__global__ void k_composite(const uint32_t *ctl, const uint32_t *act_list, const uint32_t *emitted,
+                            const uint32_t *entry_off, const float4 *rgbz, const uint8_t *exited, uint8_t *status,
+                            uint32_t *rgba, float *depth, uint32_t *keep) {
+    const int64_t n_act = ctl[C_NACT];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_act; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t r = act_list[i], ne = emitted[i], eo = entry_off[i];
         float best = CUDART_INF_F;
@@ -1289,9 +1344,10 @@ __global__ void k_composite(int64_t n_act, const uint32_t *act_list, const uint3
 
 // Same with a warp per ray, for speculative passes (n_spec entries per ray):
 // lexicographic (depth, entry) minimum == the first strict minimum in order.
-__global__ void k_composite_warp(int64_t n_act, const uint32_t *act_list, const uint32_t *emitted,
+__global__ void k_composite_warp(const uint32_t *ctl, const uint32_t *act_list, const uint32_t *emitted,
                                  const uint32_t *entry_off, const float4 *rgbz, const uint8_t *exited, uint8_t *status,
                                  uint32_t *rgba, float *depth, uint32_t *keep) {
+    const int64_t n_act = ctl[C_NACT];
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1387,6 +1443,101 @@ void reference_render_device(const float *d_values, int nx, int ny, int nz, cons
     WC_LAUNCH_CHECK();
 }
 
+// ------------------------------------------------------------- control
+// Single-thread kernels that make the pass's host decisions on the device,
+// so passes are enqueued back to back without host round trips.
+
+// engine.py:91-94 compute_n_spec (1 when speculation is off, engine.py:333)
+__device__ __forceinline__ int64_t n_spec_of(int64_t n, int64_t n_act, int speculation, int max_spec) {
+    if (!speculation || n_act <= 0) return 1;
+    const int64_t q = n / n_act;
+    return min((int64_t)max_spec, q > 1 ? q : (int64_t)1);
+}
+
+// after the initial active scan (C_NACT): the first pass's n_spec and an
+// empty cache of the initial capacity (cache.py:27-40)
+__global__ void k_frame_start(uint32_t *ctl, int64_t n, int speculation, int max_spec, int64_t cap, int64_t phys,
+                              int64_t nwords) {
+    const int64_t n_act = ctl[C_NACT];
+    ctl[C_NSPEC] = (uint32_t)n_spec_of(n, n_act, speculation, max_spec);
+    ctl[C_CAP] = (uint32_t)cap;
+    ctl[C_PHYS] = ctl[C_PHYS_OLD] = (uint32_t)phys;
+    ctl[C_HW] = ctl[C_HW_NEXT] = 0;
+    ctl[C_NWORDS_ON] = n_act > 0 ? (uint32_t)nwords : 0u;
+}
+
+// cache.py:66-96 decisions of ensure_resident once the hits are stamped and
+// the misses listed: growth to ceil(1.5 * needed), free suffix, number of
+// victims and the last stamp bucket they reach (from the stamp histogram)
+__global__ void k_cache_plan(uint32_t *ctl, const uint32_t *hist, int32_t pass_no, int64_t n_blocks,
+                             int64_t slot_alloc, int64_t nwords) {
+    const int64_t nactb = ctl[C_NACTB], n_miss = ctl[C_NMISS], hw = ctl[C_HW];
+    int64_t cap = ctl[C_CAP], phys = ctl[C_PHYS];
+    ctl[C_PHYS_OLD] = (uint32_t)phys;
+    if (nactb > cap) {  // cache.py:74-75
+        cap = (3 * nactb + 1) / 2;
+        phys = max(phys, min(cap, n_blocks));
+    }
+    if (phys > slot_alloc) {  // cannot happen: slots are reserved for the largest possible capacity
+        ctl[C_ERR_CAP] = 1;
+        phys = slot_alloc;
+    }
+    ctl[C_CAP] = (uint32_t)cap;
+    ctl[C_PHYS] = (uint32_t)phys;
+    const int64_t n_free = cap - hw;
+    ctl[C_NFREE] = (uint32_t)n_free;
+    int64_t n_evict = 0, nreg = 0;
+    uint32_t lstar = 0xFFFFFFFFu;
+    if (n_miss > n_free) {  // cache.py:80-96
+        n_evict = n_miss - n_free;
+        if (hw - (nactb - n_miss) < n_evict) ctl[C_ERR_CAND] = 1;
+        int64_t acc = 0;
+        for (int L = 0; L < pass_no && acc < n_evict; L++) {
+            acc += hist[L];
+            lstar = (uint32_t)L;
+        }
+        if (acc < n_evict) ctl[C_ERR_CAND] = 1;
+        nreg = (int64_t)(lstar + 1) * nwords;
+    }
+    ctl[C_NEVICT] = (uint32_t)n_evict;
+    ctl[C_LSTAR] = lstar;
+    ctl[C_NREG] = (uint32_t)nreg;
+}
+
+// maps of the slots the growth just brought into use (cache.py:42-53)
+__global__ void k_phys_init(const uint32_t *ctl, int32_t *block_of_slot, int32_t *last_used) {
+    const int64_t lo = ctl[C_PHYS_OLD], hi = ctl[C_PHYS];
+    for (int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < hi; s += (int64_t)gridDim.x * blockDim.x) {
+        block_of_slot[s] = -1;
+        last_used[s] = 0;
+    }
+}
+
+// end of pass: the PassStats record, then the next pass's n_act / n_spec
+// (engine.py:331-333, slot budget engine.py:341)
+__global__ void k_pass_end(uint32_t *ctl, uint32_t *row, int64_t n, int speculation, int max_spec, int64_t nwords) {
+    const int64_t n_act = ctl[C_NACT], n_after = ctl[C_NACT_NEXT];
+    row[L_NACT] = (uint32_t)n_act;
+    row[L_NSPEC] = ctl[C_NSPEC];
+    row[L_NVIS] = ctl[C_NVIS];
+    row[L_NACTB] = ctl[C_NACTB];
+    row[L_NMISS] = ctl[C_NMISS];
+    row[L_NEVICT] = ctl[C_NEVICT];
+    row[L_CAP] = ctl[C_CAP];
+    row[L_NENT] = ctl[C_NENT];
+    row[L_NAFTER] = (uint32_t)n_after;
+    row[L_NITEMS] = ctl[C_NITEMS];
+    row[L_PHYS] = ctl[C_PHYS];
+    row[L_HW] = ctl[C_HW_NEXT];
+    if (n_act == 0) return;  // an enqueued pass after the last one: no state change
+    ctl[C_HW] = ctl[C_HW_NEXT];
+    const int64_t n_spec = n_spec_of(n, n_after, speculation, max_spec);
+    if (n_after * n_spec > n) ctl[C_ERR_BUDGET] = 1;
+    ctl[C_NACT] = (uint32_t)n_after;
+    ctl[C_NSPEC] = (uint32_t)n_spec;
+    ctl[C_NWORDS_ON] = n_after > 0 ? (uint32_t)nwords : 0u;
+}
+
 // ------------------------------------------------------------------ session
 
 static int bits_for(uint64_t max_value) {
@@ -1464,7 +1615,18 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     }
     init_cap = cache_capacity;
     contrib.alloc(2 * n);
-    reserve_slots(std::min<int64_t>(vol->n_blocks, 2 * n));
+    // every buffer a pass touches, at its largest size (a pass never allocates):
+    // the cache for ceil(1.5 * min(8 N, n_blocks)) slots (cache.py:74-75 on the
+    // most active blocks a pass can have), the raytrace work list for 10 N items
+    const int64_t cap0 = std::max<int64_t>(1, init_cap <= 0 ? std::max<int64_t>(1024, 2 * n / 64) : init_cap);
+    const int64_t max_active = std::min<int64_t>(8 * n, vol->n_blocks);
+    reserve_slots(std::min<int64_t>(vol->n_blocks, std::max<int64_t>(cap0, (3 * max_active + 1) / 2)));
+    item_info.alloc(10 * n);
+    item_corners.alloc(20 * n);
+    item_t.alloc(10 * n);
+    best.alloc(n);
+    plog.alloc((int64_t)kMaxPassLog * L_COUNT);
+    h_plog.alloc((int64_t)kMaxPassLog * L_COUNT);
     reset(cam, iso_);
 }
 
@@ -1498,39 +1660,52 @@ void Session::reset(const CameraParams *cam, double iso_) {
                                                   coarse_cell.p, fine_cell.p, coarse_tmax.p, fine_tmax.p, rgba.p,
                                                   depth.p);
     WC_LAUNCH_CHECK();
-    // initial active list (engine.py:331 on pass 0)
+    // cache (cache.py:27-40, initial_capacity :122-125 with w*h == n):
+    // unmap whatever the previous frame left resident (its slot count is
+    // still in the control block)
+    k_cache_unmap<<<grid_for(slot_alloc, 256), 256, 0, st>>>(block_of_slot.p, counters.p + C_PHYS, slot_of_block.p);
+    WC_LAUNCH_CHECK();
+    cap = std::max<int64_t>(1, init_cap <= 0 ? std::max<int64_t>(1024, 2 * n / 64) : init_cap);
+    phys = std::min<int64_t>(cap, vol->n_blocks);
+    reserve_slots(phys);  // no-op after creation (the session reserved the largest capacity)
+    // Free slots' values are never read (a slot is written by its decode
+    // before any lookup can reach it), so only the slot maps are reset.
+    WC_CUDA(cudaMemsetAsync(block_of_slot.p, 0xFF, 4 * phys, st));
+    WC_CUDA(cudaMemsetAsync(last_used.p, 0, 4 * phys, st));
+
+    // initial active list (engine.py:331 on pass 0) and the device control block
     WC_CUDA(cudaMemsetAsync(counters.p, 0, 4 * C_COUNT, st));
     PredActive pa{status.p};
     scan_exclusive(pa, n, entry_off.p, counters.p + C_NACT, partials.p, st);
     k_compact_index<<<grid_for(n, 256), 256, 0, st>>>(pa, n, entry_off.p, act_list[0].p);
     WC_LAUNCH_CHECK();
-    cur = 0;
-
-    // cache (cache.py:27-40, initial_capacity :122-125 with w*h == n)
-    if (phys > 0) {  // unmap whatever the previous frame left resident
-        k_cache_unmap<<<grid_for(phys, 256), 256, 0, st>>>(block_of_slot.p, phys, slot_of_block.p);
-        WC_LAUNCH_CHECK();
-    }
-    cap = std::max<int64_t>(1, init_cap <= 0 ? std::max<int64_t>(1024, 2 * n / 64) : init_cap);
-    phys = std::min<int64_t>(cap, vol->n_blocks);
-    // Free slots' values are never read (a slot is written by its decode
-    // before any lookup can reach it), so only the slot maps are reset.
-    reserve_slots(phys);
-    WC_CUDA(cudaMemsetAsync(block_of_slot.p, 0xFF, 4 * phys, st));
-    WC_CUDA(cudaMemsetAsync(last_used.p, 0, 4 * phys, st));
+    k_frame_start<<<1, 1, 0, st>>>(counters.p, n, speculation, max_spec, cap, phys, ceil_div(vol->n_blocks, 32));
+    WC_LAUNCH_CHECK();
     pass_no = 0;
-    hist_pass = -1;
     hw = 0;
     pass_index = 0;
+    n_act = -1;  // on the device until the first pass reads it
+    frame_end = nullptr;
     for (double &m : stage_ms) m = 0.0;
     for (auto &p : pass_stage_ms)
         for (double &m : p) m = 0.0;
     WC_CUDA(cudaEventRecord(ev_reset_end, st));
-    read_counters(C_NACT, 1);
+    reset_ms = 0.0;  // known once the frame's first host read has happened (reset_device_ms)
+}
+
+int64_t Session::active_count() {
+    if (n_act < 0) {
+        read_counters(0, C_COUNT);
+        n_act = h_counters.p[C_NACT];
+    }
+    return n_act;
+}
+
+double Session::reset_device_ms() {
     float rms = 0.0f;
+    if (cudaEventQuery(ev_reset_end) != cudaSuccess) return 0.0;
     WC_CUDA(cudaEventElapsedTime(&rms, ev_frame0, ev_reset_end));
-    reset_ms = rms;
-    n_act = h_counters.p[0];
+    return rms;
 }
 
 Session::~Session() {
@@ -1544,6 +1719,9 @@ Session::~Session() {
     if (ev_reset_end) cudaEventDestroy(ev_reset_end);
     for (auto &e : ev_stage)
         if (e) cudaEventDestroy(e);
+    for (auto &row : pass_ev)
+        for (auto &e : row)
+            if (e) cudaEventDestroy(e);
 }
 
 void Session::read_counters(int first, int count) {
@@ -1551,177 +1729,63 @@ void Session::read_counters(int first, int count) {
     WC_CUDA(cudaStreamSynchronize(st));
 }
 
-// cache.py:84-91: the n_evict first candidates in (last_used, block_id)
-// order -> cand_val[0..n_evict) (their slots).  Candidates are resident slots
-// not stamped this pass.  Exact selection without sorting every candidate:
-// a histogram over the pass stamps finds the stamp L* at which the count
-// reaches n_evict; each stamp bucket L <= L* then lists its blocks in
-// ascending id order by marking them in a block bitmap and extracting it (a
-// counting sort over the block-id universe), and only the last bucket is
-// truncated.  Many small buckets fall back to the 2-key stable radix sort.
-void Session::select_victims(int64_t n_cand, int64_t n_evict) {
-    const int64_t nb = pass_no;  // stamps are 1..pass_no-1 for candidates
-    const uint32_t *hh = h_counters.p + (C_COUNT - C_NENT);  // read with the mid-pass counters
-    if (hist_pass != pass_no) {  // not queued by cache_lookup: build and read it now
-        launch_stamp_hist();
-        WC_CUDA(cudaStreamSynchronize(st));
-        hh = h_stamp_hist.p;
-    }
-    int64_t acc = 0;
-    int n_buckets = 0;
-    int L_star = -1;
-    for (int L = 0; L <= nb && acc < n_evict; L++) {
-        const int64_t c = hh[L];
-        if (!c) continue;
-        n_buckets++;
-        acc += c;
-        L_star = L;
-    }
-    if (acc < n_evict) throw InvariantError("cache: fewer eviction candidates than needed");
-    if (n_buckets > 6) {  // many stamp buckets: one stable 2-key radix sort of all candidates
-        PredCand pc{block_of_slot.p, last_used.p, pass_no};
-        scan_exclusive(pc, hw, cand_off.p, counters.p + C_NCAND, partials.p, st);
-        k_compact_cand<<<grid_for(hw, 256), 256, 0, st>>>(pc, hw, cand_off.p, cand_key.p, cand_val.p);
-        WC_LAUNCH_CHECK();
-        radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)(vol->n_blocks - 1)), rs, st);
-        k_gather_last_used<<<grid_for(n_cand, 256), 256, 0, st>>>(cand_val.p, n_cand, last_used.p, cand_key.p);
-        WC_LAUNCH_CHECK();
-        radix_sort_pairs(cand_key.p, cand_val.p, n_cand, bits_for((uint64_t)pass_no), rs, st);
-        return;
-    }
-    const int64_t nwords = ceil_div(vol->n_blocks, 32);
-    int64_t off = 0;
-    for (int L = 0; L <= L_star; L++) {
-        const int64_t c = hh[L];
-        if (!c) continue;
-        k_mark_stamp<<<grid_for(hw, 256), 256, 0, st>>>(block_of_slot.p, last_used.p, hw, L, act_bm.p);
-        WC_LAUNCH_CHECK();
-        // ascending block ids of bucket L -> cand_key[off..off+c)
-        bitmap_extract(act_bm.p, nwords, act_word_off.p, cand_key.p + off, counters.p + C_NCAND, partials.p, st);
-        WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
-        off += c;
-    }
-    k_blocks_to_slots<<<grid_for(n_evict, 256), 256, 0, st>>>(cand_key.p, n_evict, slot_of_block.p, cand_val.p);
-    WC_LAUNCH_CHECK();
-}
-
-// cache.py:66-111 ensure_resident over the ascending active_ids[0..n_actb)
-// First half of ensure_resident, queued before the pass's one mid-pass host
-// read: stamp the hits and compact the misses of the active blocks whose
-// count is still on the device (cache.py:67-73, :76-78).
-// Histogram of the pass stamps of the resident slots not stamped this pass
-// (the eviction candidates), queued with its read-back to h_stamp_hist.
-void Session::launch_stamp_hist() {
-    const int64_t nb = pass_no;
-    stamp_hist.ensure(nb + 1);
-    h_stamp_hist.ensure_host(nb + 1);
-    WC_CUDA(cudaMemsetAsync(stamp_hist.p, 0, 4 * (nb + 1), st));
-    k_stamp_hist<<<grid_for(hw, 256), 256, 4 * (size_t)nb, st>>>(block_of_slot.p, last_used.p, hw, pass_no,
-                                                                 stamp_hist.p);
-    WC_LAUNCH_CHECK();
-    WC_CUDA(cudaMemcpyAsync(h_stamp_hist.p, stamp_hist.p, 4 * (nb + 1), cudaMemcpyDeviceToHost, st));
-    hist_pass = pass_no;
-}
-
-void Session::cache_lookup() {
-    pass_no += 1;
-    const int64_t nmax = active_ids.n - 1;  // upper bound of the active-block count
-    const uint32_t *d_nactb = counters.p + C_NACTB;
-    // a pass over a non-empty cache may evict: its stamp histogram is built
-    // right after the stamping, in the counter block, so that it arrives
-    // with the mid-pass counter read (no extra host round trip)
-    const bool early = WC_EARLY_HIST && hw > 0 && pass_no + 1 <= kHistBins;
-    k_cache_stamp<<<grid_for(nmax, 256), 256, 0, st>>>(active_ids.p, d_nactb, nmax, slot_of_block.p, last_used.p,
-                                                      pass_no, counters.p + C_COUNT, early ? pass_no + 1 : 0);
-    WC_LAUNCH_CHECK();
-    if (early) {
-        k_stamp_hist<<<grid_for(hw, 256), 256, 4 * (size_t)pass_no, st>>>(block_of_slot.p, last_used.p, hw, pass_no,
-                                                                         counters.p + C_COUNT);
-        WC_LAUNCH_CHECK();
-        hist_pass = pass_no;
-    }
-    PredMiss pm{active_ids.p, slot_of_block.p};
-    scan_exclusive_dev(pm, d_nactb, nmax, miss_off.p, counters.p + C_NMISS, partials.p, st);
-    k_compact_miss<<<grid_for(nmax, 256), 256, 0, st>>>(pm, d_nactb, nmax, miss_off.p, miss_ids.p);
-    WC_LAUNCH_CHECK();
-}
-
-// Physical slot storage for `need` logical slots.  The logical capacity
-// follows the reference (cache.py:74-75); the allocation grows geometrically
-// (first to 2 slots per ray) because every growth is a cudaMalloc + copy of
-// up to GBs: once per new maximum, not once per frame.  Slots past `phys` are
-// never read.
+// Physical slot storage for `need` slots (maps, values, eviction scratch).
+// The session reserves, at creation, slots for the largest capacity the
+// reference's growth rule can reach -- ceil(1.5 * active blocks) with at most
+// min(8 N, n_blocks) active blocks per pass -- so a pass never allocates and
+// the cache decisions can stay on the device.
 void Session::reserve_slots(int64_t need) {
     if (need <= slot_alloc) return;
-    const int64_t target = std::max<int64_t>(
-        need, std::min<int64_t>(vol->n_blocks, std::max<int64_t>(2 * n, slot_alloc + slot_alloc / 2)));
-    slot_values.grow(target * 64, st);
-    block_of_slot.grow(target, st);
-    last_used.grow(target, st);
-    cand_off.alloc(target);
-    cand_key.alloc(target);
-    cand_val.alloc(target);
+    slot_values.grow(need * 64, st);
+    block_of_slot.grow(need, st);
+    last_used.grow(need, st);
+    cand_key.alloc(need);
+    cand_val.alloc(need);
     const int64_t words =
-        scan_scratch_words(std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n, target}));
+        scan_scratch_words(std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n, need}));
     if (partials.n < words) {
         partials.ensure(words);
         WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
     }
-    slot_alloc = target;
+    slot_alloc = need;
 }
 
-void Session::ensure_resident(int64_t n_actb, int64_t n_miss, int64_t &n_evict) {
-    if (n_actb > cap) {  // cache.py:74-75: grow to ceil(1.5 * needed)
-        cap = (3 * n_actb + 1) / 2;
-        const int64_t new_phys = std::min<int64_t>(cap, vol->n_blocks);
-        if (new_phys > phys) {
-            reserve_slots(new_phys);  // keeps resident slots (cache.py:42-53)
-            WC_CUDA(cudaMemsetAsync(block_of_slot.p + phys, 0xFF, 4 * (new_phys - phys), st));
-            WC_CUDA(cudaMemsetAsync(last_used.p + phys, 0, 4 * (new_phys - phys), st));
-            phys = new_phys;
-        }
-    }
-    n_evict = 0;
-    if (n_miss == 0) return;
-    // Free slots are always the suffix [hw, cap): misses take the lowest free
-    // slots (cache.py:79, :97) and an eviction pass consumes every free slot
-    // plus exactly its victims (cache.py:80-96), so no hole ever opens.
-    const int64_t n_free = cap - hw;
-    const uint32_t *victims = nullptr;
-    {
-        if (n_miss > n_free) {
-            n_evict = n_miss - n_free;
-            const int64_t n_hits = n_actb - n_miss;
-            const int64_t n_cand = hw - n_hits;  // resident and not stamped this pass
-            if (n_cand < n_evict) throw InvariantError("cache: fewer eviction candidates than needed");
-            select_victims(n_cand, n_evict);
-            k_evict<<<grid_for(n_evict, 256), 256, 0, st>>>(cand_val.p, n_evict, block_of_slot.p, slot_of_block.p);
-            WC_LAUNCH_CHECK();
-            victims = cand_val.p;
-        }
-    }
-    // the miss count stays on the device: the decode grid strides over it
-    k_decode_insert<<<grid_for(n_miss * 32, 256, 8), 256, 0, st>>>(
-        vol->payload.p, vol->qbits, vol->stride, miss_ids.p, counters.p + C_NMISS, hw, n_free, victims,
-        slot_values.p, block_of_slot.p, last_used.p, slot_of_block.p, pass_no, counters.p + C_HW, cap);
-    WC_LAUNCH_CHECK();
+cudaEvent_t *Session::pass_events(int64_t p) {
+    if (p >= kMaxPassLog) return nullptr;
+    if (!pass_ev[p][0])
+        for (auto &e : pass_ev[p]) WC_CUDA(cudaEventCreate(&e));
+    return pass_ev[p];
 }
 
-bool Session::pass(PassStatsC &stats) {
-    if (n_act == 0) return false;
-    const auto t_start = std::chrono::steady_clock::now();
-    WC_CUDA(cudaEventRecord(ev_begin, st));
-    WC_CUDA(cudaEventRecord(ev_stage[0], st));
-    // engine.py:333 / :91-94 compute_n_spec (slot budget = rays in session)
-    int64_t n_spec = 1;
-    if (speculation) n_spec = std::min<int64_t>(max_spec, std::max<int64_t>(1, n / n_act));
-    if (n_act * n_spec > n) throw InvariantError("slot budget exceeded");
-    last_n_spec = n_spec;
-    last_slots_used = n_act * n_spec;
+// One pass of render_passes (engine.py:326-382), enqueued without any host
+// read: every size comes from the device control block (Counter).  p is the
+// pass index since the last reset; its cache stamp is p + 1.
+void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     const int64_t nwords = ceil_div(vol->n_blocks, 32);
-    uint32_t *alist = act_list[cur].p;
+    const int32_t stamp = (int32_t)(p + 1);
+    pass_no = stamp;
+    uint32_t *ctl = counters.p;
+    uint32_t *alist = act_list[p & 1].p;
+    cudaEvent_t *ev = pass_events(p);
+    auto mark = [&](int k) {
+        if (ev) WC_CUDA(cudaEventRecord(ev[k], st));
+    };
+    // the victim regions must hold one bitmap per stamp a candidate can carry
+    if (vict_regions < stamp) {
+        const int64_t r = std::max<int64_t>(stamp, std::max<int64_t>(8, 2 * vict_regions));
+        vict_bm.alloc(r * nwords);
+        WC_CUDA(cudaMemsetAsync(vict_bm.p, 0, 4 * r * nwords, st));
+        vict_regions = r;
+        const int64_t words = scan_scratch_words(r * nwords);
+        if (partials.n < words) {
+            partials.ensure(words);
+            WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
+        }
+    }
+    mark(0);
 
-    // traverse_to_next_blocks + fused visibility marking
+    // traverse_to_next_blocks + fused visibility marking (one of the two
+    // kernels runs, by the device n_act)
     TraverseArgs ta{};
     ta.rays = RayView{uniform_origin ? nullptr : origin.p, dir.p, t_enter.p, eye[0], eye[1], eye[2]};
     ta.t_exit = t_exit.p;
@@ -1731,8 +1795,6 @@ bool Session::pass(PassStatsC &stats) {
     ta.coarse_tmax = coarse_tmax.p;
     ta.fine_tmax = fine_tmax.p;
     ta.act_list = alist;
-    ta.n_act = n_act;
-    ta.n_spec = (int)n_spec;
     ta.cell_mask = cell_mask.p;
     ta.coarse_bm = coarse_bm.p;
     ta.fdx = vol->bdx;
@@ -1746,165 +1808,276 @@ bool Session::pass(PassStatsC &stats) {
     ta.ray_slots = ray_slots.p;
     ta.emitted = emitted.p;
     ta.vis_bm = vis_bm.p;
-    ta.work = counters.p + C_WORK;
-    WC_CUDA(cudaMemsetAsync(ta.work, 0, 4, st));
-    if (n_act <= WC_WARP_TRAVERSE_MAX)  // few (long) rays: warp-cooperative DDA per ray
-        k_traverse_warp<<<grid_for(n_act * 32, 128, 16), 128, 0, st>>>(ta);
+    ta.work = ctl + C_WORK;
+    ta.ctl = ctl;
+    WC_CUDA(cudaMemsetAsync(ctl + C_WORK, 0, 4, st));
+    WC_CUDA(cudaMemsetAsync(ctl + C_NITEMS, 0, 4, st));
+    if (nact_guess <= WC_WARP_TRAVERSE_MAX)  // few (long) rays: warp-cooperative DDA per ray
+        k_traverse_warp<<<grid_for(std::max<int64_t>(1, nact_guess) * 32, 128, 16), 128, 0, st>>>(ta);
     else
-        k_traverse<WC_COARSE_AHEAD><<<grid_for(n_act, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st>>>(ta);
+        k_traverse<WC_COARSE_AHEAD><<<grid_for(n, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st>>>(ta);
     WC_LAUNCH_CHECK();
-    WC_CUDA(cudaEventRecord(ev_stage[1], st));
+    mark(1);
     // entry compaction: exclusive scan of per-ray emitted counts
-    scan_exclusive(LoadU32{emitted.p}, n_act, entry_off.p, counters.p + C_NENT, partials.p, st);
+    scan_exclusive_dev(LoadU32{emitted.p}, ctl + C_NACT, n, entry_off.p, ctl + C_NENT, partials.p, st);
     // visible ids (ascending) + active marking
-    bitmap_extract(vis_bm.p, nwords, vis_word_off.p, visible_ids.p, counters.p + C_NVIS, partials.p, st);
-    k_mark_active<<<grid_for((int64_t)8 * n, 256), 256, 0, st>>>(visible_ids.p, counters.p + C_NVIS, vol->bdx,
-                                                                 vol->bdy, vol->bdz, act_bm.p);
+    bitmap_extract_dev(vis_bm.p, ctl + C_NWORDS_ON, nwords, vis_word_off.p, visible_ids.p, ctl + C_NVIS, partials.p,
+                       st);
+    k_mark_active<<<grid_for((int64_t)8 * n, 256), 256, 0, st>>>(visible_ids.p, ctl + C_NVIS, vol->bdx, vol->bdy,
+                                                                 vol->bdz, act_bm.p);
     WC_LAUNCH_CHECK();
-    bitmap_extract(act_bm.p, nwords, act_word_off.p, active_ids.p, counters.p + C_NACTB, partials.p, st);
-    k_build_entries<<<grid_for(n_act * n_spec, 256), 256, 0, st>>>(n_act, (int)n_spec, alist, emitted.p, entry_off.p,
-                                                          block_slots.p, vis_bm.p, vis_word_off.p, ent_key.p,
-                                                          ent_val.p, ent_ray.p);
+    bitmap_extract_dev(act_bm.p, ctl + C_NWORDS_ON, nwords, act_word_off.p, active_ids.p, ctl + C_NACTB, partials.p,
+                       st);
+    k_build_entries<<<grid_for(n, 256), 256, 0, st>>>(ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p,
+                                                      vis_word_off.p, ent_key.p, ent_val.p, ent_ray.p);
     WC_LAUNCH_CHECK();
     WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
     WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
-    cache_lookup();  // cache hits stamped, misses compacted, counts still on the device
-    WC_CUDA(cudaEventRecord(ev_stage[2], st));
-    // the pass's one mid-pass host read (+ the stamp histogram when queued)
-    read_counters(C_NENT, hist_pass == pass_no ? C_COUNT - C_NENT + pass_no + 1 : 4);
-    const int64_t n_ent = h_counters.p[0], nvis = h_counters.p[1], nactb = h_counters.p[2];
-    const int64_t n_miss = h_counters.p[3];
-    if (n_ent > n) throw InvariantError("slot budget exceeded");
-    last_nent = n_ent;
-    last_nvis = nvis;
-    last_nactb = nactb;
 
-    // cache.ensure_resident: growth, eviction, fused decode
-    int64_t n_evict = 0;
-    ensure_resident(nactb, n_miss, n_evict);
-    if (corrupt) WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * phys, st));  // engine.py:338-339
-    WC_CUDA(cudaEventRecord(ev_stage[3], st));
+    // cache.ensure_resident (cache.py:66-111): stamp hits, list misses
+    // (ascending), then growth / victims / decode, all sized on the device
+    const int64_t nmax = active_ids.n - 1;  // upper bound of the active-block count
+    const bool hist = p >= 1 && stamp + 1 <= kHistBins;
+    k_cache_stamp<<<grid_for(nmax, 256), 256, 0, st>>>(active_ids.p, ctl + C_NACTB, nmax, slot_of_block.p, last_used.p,
+                                                      stamp, ctl + C_COUNT, hist ? stamp + 1 : 0);
+    WC_LAUNCH_CHECK();
+    if (hist) {
+        k_stamp_hist<<<grid_for(slot_alloc, 256), 256, 4 * (size_t)stamp, st>>>(block_of_slot.p, last_used.p, ctl,
+                                                                               stamp, ctl + C_COUNT);
+        WC_LAUNCH_CHECK();
+    }
+    PredMiss pm{active_ids.p, slot_of_block.p};
+    scan_exclusive_dev(pm, ctl + C_NACTB, nmax, miss_off.p, ctl + C_NMISS, partials.p, st);
+    k_compact_miss<<<grid_for(nmax, 256), 256, 0, st>>>(pm, ctl + C_NACTB, nmax, miss_off.p, miss_ids.p);
+    WC_LAUNCH_CHECK();
+    mark(2);
+    if (p >= 1 && !hist) {  // > kHistBins passes: histogram over all stamps through the host (rare)
+        read_counters(0, C_COUNT);
+        if (h_counters.p[C_NACT]) {
+            stamp_hist.ensure(stamp + 1);
+            h_stamp_hist.ensure_host(stamp + 1);
+            WC_CUDA(cudaMemsetAsync(stamp_hist.p, 0, 4 * (stamp + 1), st));
+            k_stamp_hist<<<grid_for(slot_alloc, 256), 256, 4 * (size_t)stamp, st>>>(block_of_slot.p, last_used.p,
+                                                                                   ctl, stamp, stamp_hist.p);
+            WC_LAUNCH_CHECK();
+        }
+    }
+    k_cache_plan<<<1, 1, 0, st>>>(ctl, p >= 1 && !hist ? stamp_hist.p : ctl + C_COUNT, stamp, vol->n_blocks,
+                                 slot_alloc, nwords);
+    WC_LAUNCH_CHECK();
+    k_phys_init<<<grid_for(slot_alloc, 256), 256, 0, st>>>(ctl, block_of_slot.p, last_used.p);
+    WC_LAUNCH_CHECK();
+    if (p >= 1) {  // victims in (last_used, block_id) order: one extraction over the stamp regions
+        k_mark_victims<<<grid_for(slot_alloc, 256), 256, 0, st>>>(block_of_slot.p, last_used.p, ctl, stamp, nwords,
+                                                                  vict_bm.p);
+        WC_LAUNCH_CHECK();
+        const int64_t nreg_max = (int64_t)stamp * nwords;
+        k_scan_onepass<LoadPopc, SinkRegions><<<(unsigned)scan_tiles(nreg_max), kScanThreads, 0, st>>>(
+            LoadPopc{vict_bm.p}, SinkRegions{vict_bm.p, cand_key.p, nwords}, nreg_max, ctl + C_NREG,
+            reinterpret_cast<uint64_t *>(partials.p), next_scan_epoch(), ctl + C_NCAND);
+        WC_LAUNCH_CHECK();
+        k_blocks_to_slots<<<grid_for(slot_alloc, 256), 256, 0, st>>>(cand_key.p, ctl + C_NEVICT, slot_of_block.p,
+                                                                     cand_val.p);
+        WC_LAUNCH_CHECK();
+        k_evict<<<grid_for(slot_alloc, 256), 256, 0, st>>>(cand_val.p, ctl + C_NEVICT, block_of_slot.p,
+                                                           slot_of_block.p);
+        WC_LAUNCH_CHECK();
+    }
+    // the misses' records decoded straight into their slots (free slots
+    // first, then the victims in order, cache.py:97-103)
+    k_decode_insert<<<grid_for(nmax * 32, 256, 8), 256, 0, st>>>(vol->payload.p, vol->qbits, vol->stride,
+                                                                 miss_ids.p, ctl, cand_val.p, slot_values.p,
+                                                                 block_of_slot.p, last_used.p, slot_of_block.p, stamp);
+    WC_LAUNCH_CHECK();
+    if (corrupt) WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * slot_alloc, st));  // engine.py:338-339
+    mark(3);
 
-    // build_rt_inputs: stable grouping of entries by visible block.  The
-    // thread-per-entry raytrace is correct on either order; grouping buys L1
-    // locality (neighbouring lanes on one block) and the reference's
-    // PassBuffers layout, and can be switched off (group_entries).
-    if (n_ent > 0) {
-        if (group_entries) {
+    // build_rt_inputs grouping (debug views only: the raytrace is correct on
+    // ray order; the radix sort needs the entry and visible counts on the host)
+    if (group_entries) {
+        read_counters(0, C_COUNT);
+        const int64_t n_ent = h_counters.p[C_NENT], nvis = h_counters.p[C_NVIS];
+        if (n_ent > 0) {
             radix_sort_pairs(ent_key.p, ent_val.p, n_ent, bits_for((uint64_t)(nvis - 1)), rs, st);
             k_run_offsets<<<grid_for(n_ent, 256), 256, 0, st>>>(ent_key.p, n_ent, nvis, block_ray_off.p);
             WC_LAUNCH_CHECK();
         }
-        WC_CUDA(cudaEventRecord(ev_stage[4], st));
-        contrib.ensure(2 * nvis);  // nvis <= n: sized 2 n at creation
-        k_contrib<<<grid_for(nvis, 256), 256, 0, st>>>(visible_ids.p, nvis, slot_of_block.p, vol->bdx, vol->bdy,
-                                                       vol->bdz, contrib.p, counters.p + C_ERR);
+    }
+    mark(4);
+    k_contrib<<<grid_for(n, 256), 256, 0, st>>>(visible_ids.p, ctl + C_NVIS, slot_of_block.p, vol->bdx, vol->bdy,
+                                                vol->bdz, contrib.p, ctl + C_ERR);
+    WC_LAUNCH_CHECK();
+    RaytraceArgs ra{};
+    ra.visible_ids = visible_ids.p;
+    ra.ent_key = ent_key.p;
+    ra.ent_val = ent_val.p;
+    ra.ent_ray = ent_ray.p;
+    ra.d_n_ent = ctl + C_NENT;
+    ra.contrib = contrib.p;
+    ra.slot_values = slot_values.p;
+    ra.bdx = vol->bdx;
+    ra.bdy = vol->bdy;
+    ra.bdz = vol->bdz;
+    ra.nx = vol->nx;
+    ra.ny = vol->ny;
+    ra.nz = vol->nz;
+    ra.rays = ta.rays;
+    ra.iso = iso;
+    ra.br = base[0];
+    ra.bg = base[1];
+    ra.bb = base[2];
+    ra.rgbz = rgbz.p;
+    if (WC_SPLIT_RAYTRACE) {
+        SplitArgs sa{};
+        sa.a = ra;
+        sa.item_cap = 10 * n;  // <= 10 dual cells per entry (monotone ray in a 4^3 region)
+        sa.item_info = item_info.p;
+        sa.item_corners = item_corners.p;
+        sa.item_t = item_t.p;
+        sa.best = best.p;
+        sa.n_items = ctl + C_NITEMS;
+        k_rt_find<<<grid_for(n, 128, 16), 128, 0, st>>>(sa);
         WC_LAUNCH_CHECK();
-        RaytraceArgs ra{};
-        ra.visible_ids = visible_ids.p;
-        ra.ent_key = ent_key.p;
-        ra.ent_val = ent_val.p;
-        ra.ent_ray = ent_ray.p;
-        ra.n_ent = n_ent;
-        ra.contrib = contrib.p;
-        ra.slot_values = slot_values.p;
-        ra.bdx = vol->bdx;
-        ra.bdy = vol->bdy;
-        ra.bdz = vol->bdz;
-        ra.nx = vol->nx;
-        ra.ny = vol->ny;
-        ra.nz = vol->nz;
-        ra.rays = ta.rays;
-        ra.iso = iso;
-        ra.br = base[0];
-        ra.bg = base[1];
-        ra.bb = base[2];
-        ra.rgbz = rgbz.p;
-        if (WC_SPLIT_RAYTRACE) {
-            SplitArgs sa{};
-            sa.a = ra;
-            sa.item_cap = 10 * n;  // <= 10 dual cells per entry (monotone ray in a 4^3 region)
-            if (item_info.n < sa.item_cap) {
-                item_info.alloc(sa.item_cap);
-                item_corners.alloc(2 * sa.item_cap);
-                item_t.alloc(sa.item_cap);
-                best.alloc(n);
-            }
-            sa.item_info = item_info.p;
-            sa.item_corners = item_corners.p;
-            sa.item_t = item_t.p;
-            sa.best = best.p;
-            sa.n_items = counters.p + C_NITEMS;
-            WC_CUDA(cudaMemsetAsync(sa.n_items, 0, 4, st));
-            k_rt_find<<<grid_for(n_ent, 128, 16), 128, 0, st>>>(sa);
-            WC_LAUNCH_CHECK();
-            k_rt_solve<<<grid_for(sa.item_cap, 128, WC_RAYTRACE_MIN_CTAS), 128, 0, st>>>(sa);
-            WC_LAUNCH_CHECK();
-            k_rt_shade<<<grid_for(n_ent, 128, 16), 128, 0, st>>>(sa);
-            WC_LAUNCH_CHECK();
-        } else {
-            k_raytrace<<<grid_for(n_ent, 128, 16), 128, 0, st>>>(ra);
-            WC_LAUNCH_CHECK();
-        }
+        k_rt_solve<<<grid_for(sa.item_cap, 128, WC_RAYTRACE_MIN_CTAS), 128, 0, st>>>(sa);
+        WC_LAUNCH_CHECK();
+        k_rt_shade<<<grid_for(n, 128, 16), 128, 0, st>>>(sa);
+        WC_LAUNCH_CHECK();
     } else {
-        WC_CUDA(cudaEventRecord(ev_stage[4], st));
+        k_raytrace<<<grid_for(n, 128, 16), 128, 0, st>>>(ra);
+        WC_LAUNCH_CHECK();
     }
-    WC_CUDA(cudaEventRecord(ev_stage[5], st));
+    mark(5);
     // composite + compaction of the surviving rays (next pass's O_Act)
-    if (n_spec >= 8)
-        k_composite_warp<<<grid_for(n_act * 32, 256), 256, 0, st>>>(n_act, alist, emitted.p, entry_off.p, rgbz.p,
-                                                                    exited.p, status.p, rgba.p, depth.p, keep.p);
+    if (speculation && n / std::max<int64_t>(1, nact_guess) >= 8)  // n_spec >= 8: a warp per ray
+        k_composite_warp<<<grid_for(n * 32, 256), 256, 0, st>>>(ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p,
+                                                                status.p, rgba.p, depth.p, keep.p);
     else
-        k_composite<<<grid_for(n_act, 256), 256, 0, st>>>(n_act, alist, emitted.p, entry_off.p, rgbz.p, exited.p,
-                                                          status.p, rgba.p, depth.p, keep.p);
+        k_composite<<<grid_for(n, 256), 256, 0, st>>>(ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p, status.p,
+                                                      rgba.p, depth.p, keep.p);
     WC_LAUNCH_CHECK();
-    scan_exclusive(LoadU32{keep.p}, n_act, keep_off.p, counters.p + C_NACT, partials.p, st);
-    k_compact_keep<<<grid_for(n_act, 256), 256, 0, st>>>(keep.p, keep_off.p, alist, n_act, act_list[cur ^ 1].p);
+    scan_exclusive_dev(LoadU32{keep.p}, ctl + C_NACT, n, keep_off.p, ctl + C_NACT_NEXT, partials.p, st);
+    k_compact_keep<<<grid_for(n, 256), 256, 0, st>>>(keep.p, keep_off.p, alist, ctl + C_NACT, act_list[(p + 1) & 1].p);
     WC_LAUNCH_CHECK();
-    WC_CUDA(cudaEventRecord(ev_end, st));
-    WC_CUDA(cudaEventRecord(ev_stage[6], st));
-    read_counters(0, C_COUNT);
-    const int64_t n_after = h_counters.p[C_NACT];
+    k_pass_end<<<1, 1, 0, st>>>(ctl, plog.p + std::min<int64_t>(p, kMaxPassLog - 1) * L_COUNT, n, speculation,
+                                max_spec, nwords);
+    WC_LAUNCH_CHECK();
+    mark(6);
+}
+
+void Session::check_device_errors() {
     if (h_counters.p[C_ERR]) throw InvariantError("visible block not resident");
-    if (n_miss > 0) hw = h_counters.p[C_HW];
-    WC_CUDA(cudaEventElapsedTime(&last_kernel_ms, ev_begin, ev_end));
-    for (int k = 0; k < kStages; k++) {
-        float ms = 0.0f;
-        WC_CUDA(cudaEventElapsedTime(&ms, ev_stage[k], ev_stage[k + 1]));
-        stage_ms[k] += ms;
-        if (pass_index < kMaxPassLog) pass_stage_ms[pass_index][k] = ms;
+    if (h_counters.p[C_ERR_BUDGET]) throw InvariantError("slot budget exceeded");
+    if (h_counters.p[C_ERR_CAND]) throw InvariantError("cache: fewer eviction candidates than needed");
+    if (h_counters.p[C_ERR_CAP]) throw InvariantError("cache: capacity beyond the reserved slots");
+}
+
+// PassStats of pass p from its device record (h_plog holds it) and events.
+void Session::collect_pass(int64_t p, PassStatsC &stats) {
+    const uint32_t *r = h_plog.p + std::min<int64_t>(p, kMaxPassLog - 1) * L_COUNT;
+    double ms_pass = 0.0;
+    if (cudaEvent_t *ev = pass_events(p)) {
+        for (int k = 0; k < kStages; k++) {
+            float ms = 0.0f;
+            WC_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+            stage_ms[k] += ms;
+            pass_stage_ms[p][k] = ms;
+            ms_pass += ms;
+        }
+        last_kernel_ms = (float)ms_pass;
+        frame_end = ev[kStages];
     }
+    stats.pass_index = p;
+    stats.n_active_before = r[L_NACT];
+    stats.n_spec = r[L_NSPEC];
+    stats.visible_blocks = r[L_NVIS];
+    stats.active_blocks = r[L_NACTB];
+    stats.new_decompressed = r[L_NMISS];
+    stats.evicted = r[L_NEVICT];
+    stats.cache_slots = r[L_CAP];
+    stats.n_entries = r[L_NENT];
+    stats.n_active_after = r[L_NAFTER];
+    stats.utilization = (double)r[L_NENT] / (double)n;
+    stats.completeness = (double)(n - (int64_t)r[L_NAFTER]) / (double)n;
+    stats.duration = ms_pass * 1e-3;  // device time of the pass
+    // host mirrors for the stage views (wc_session_sizes & co.)
+    last_n_spec = r[L_NSPEC];
+    last_slots_used = (int64_t)r[L_NACT] * r[L_NSPEC];
+    last_nvis = r[L_NVIS];
+    last_nactb = r[L_NACTB];
+    last_nent = r[L_NENT];
+    cap = r[L_CAP];
+    phys = r[L_PHYS];
+    hw = r[L_HW];
+    n_act = r[L_NAFTER];
     static const bool trace = getenv("WAVECAST_TRACE") != nullptr;
     if (trace)
-        fprintf(stderr, "[wavecast] pass %lld n_act %lld n_spec %lld entries %lld visible %lld active %lld miss %lld "
-                        "evict %lld items %u after %lld cap %lld phys %lld gpu %.3f ms host %.3f ms\n",
-                (long long)pass_index, (long long)n_act, (long long)n_spec, (long long)n_ent, (long long)nvis,
-                (long long)nactb, (long long)n_miss, (long long)n_evict, h_counters.p[C_NITEMS], (long long)n_after,
-                (long long)cap, (long long)phys, (double)last_kernel_ms,
-                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count() * 1e3);
-    stats.pass_index = pass_index;
-    stats.n_active_before = n_act;
-    stats.n_spec = n_spec;
-    stats.visible_blocks = nvis;
-    stats.active_blocks = nactb;
-    stats.new_decompressed = n_miss;
-    stats.evicted = n_evict;
-    stats.cache_slots = cap;
-    stats.n_entries = n_ent;
-    stats.n_active_after = n_after;
-    stats.utilization = (double)n_ent / (double)n;
-    stats.completeness = (double)(n - n_after) / (double)n;
-    stats.duration = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
-    cur ^= 1;
-    n_act = n_after;
+        fprintf(stderr, "[wavecast] pass %lld n_act %u n_spec %u entries %u visible %u active %u miss %u evict %u "
+                        "items %u after %u cap %u phys %u gpu %.3f ms\n",
+                (long long)p, r[L_NACT], r[L_NSPEC], r[L_NENT], r[L_NVIS], r[L_NACTB], r[L_NMISS], r[L_NEVICT],
+                r[L_NITEMS], r[L_NAFTER], r[L_CAP], r[L_PHYS], ms_pass);
+}
+
+// render_passes step (engine.py:326-382): one pass, then its stats.
+bool Session::pass(PassStatsC &stats) {
+    if (n_act < 0) {  // the count the reset left on the device
+        read_counters(0, C_COUNT);
+        n_act = h_counters.p[C_NACT];
+    }
+    if (n_act == 0) return false;
+    enqueue_pass(pass_index, n_act);
+    WC_CUDA(cudaMemcpyAsync(h_plog.p, plog.p, 4 * L_COUNT * std::min<int64_t>(pass_index + 1, kMaxPassLog),
+                            cudaMemcpyDeviceToHost, st));
+    read_counters(0, C_COUNT);
+    check_device_errors();
+    collect_pass(pass_index, stats);
     pass_index++;
     return true;
 }
 
+// A whole frame: passes are enqueued in batches (first as many as the last
+// frame needed) and the host looks at the device only between batches.  A
+// pass enqueued after the last one finds no active ray and does no work.
+int64_t Session::run_frame(PassStatsC *out, int64_t max_out) {
+    int64_t k = 0;
+    int64_t batch = std::max<int64_t>(1, frame_passes_hint);
+    if (n_act < 0 && nact_hist[0] == 0) active_count();  // first frame: no history to guess from
+    for (;;) {
+        const int64_t p0 = pass_index;
+        batch = p0 < kMaxPassLog ? std::min<int64_t>(batch, kMaxPassLog - p0) : 1;  // one log row per pass
+        for (int64_t b = 0; b < batch; b++) {  // active-count guesses: exact for the first, last frame's after
+            const int64_t p = p0 + b;
+            enqueue_pass(p, b == 0 && n_act >= 0 ? n_act : (p < kMaxPassLog ? nact_hist[p] : 1));
+        }
+        WC_CUDA(cudaMemcpyAsync(h_plog.p, plog.p, 4 * L_COUNT * std::min<int64_t>(p0 + batch, kMaxPassLog),
+                                cudaMemcpyDeviceToHost, st));
+        read_counters(0, C_COUNT);
+        check_device_errors();
+        bool done = false;
+        for (int64_t b = 0; b < batch; b++) {
+            const int64_t p = p0 + b;
+            if (h_plog.p[std::min<int64_t>(p, kMaxPassLog - 1) * L_COUNT + L_NACT] == 0) {
+                done = true;
+                break;
+            }
+            PassStatsC st_{};
+            collect_pass(p, st_);
+            if (p < kMaxPassLog) nact_hist[p] = st_.n_active_before;
+            if (out && k < max_out) out[k] = st_;
+            k++;
+            pass_index++;
+        }
+        if (done || h_counters.p[C_NACT] == 0) break;
+        batch = 1;
+    }
+    n_act = 0;
+    frame_passes_hint = std::max<int64_t>(1, k);
+    return k;
+}
+
 float Session::frame_ms() {
     float ms = 0.0f;
-    if (pass_index == 0) return 0.0f;
-    WC_CUDA(cudaEventElapsedTime(&ms, ev_frame0, ev_end));
+    if (pass_index == 0 || !frame_end) return 0.0f;
+    WC_CUDA(cudaEventElapsedTime(&ms, ev_frame0, frame_end));
     return ms;
 }
 

@@ -21,19 +21,40 @@ struct PassStatsC {  // engine.py:66-77 PassStats (+ evicted, n_entries)
 
 constexpr int kHistBins = 64;  // stamp histogram bins kept after the counters (passes < 64)
 
+// Device control block: every count a pass needs lives here, so a pass is
+// enqueued without host round trips (each kernel reads its sizes).
 enum Counter : int {
-    C_NACT = 0,   // active rays after composite (next pass's n_act)
+    C_NACT = 0,   // active rays of the current pass (engine.py:331)
     C_NENT,       // ray-block entries this pass
     C_NVIS,       // visible blocks
     C_NACTB,      // active blocks
     C_NMISS,      // cache misses
-    C_NFREE,      // free slots
-    C_NCAND,      // eviction candidates
-    C_ERR,        // device-side invariant failures
+    C_NFREE,      // free slots (cap - hw)
+    C_NCAND,      // eviction candidates listed (bucket extraction count)
+    C_ERR,        // device-side invariant failure: visible block not resident
     C_HW,         // occupied cache slots: free slots are the suffix [hw, cap)
     C_WORK,       // persistent traversal work counter
     C_NITEMS,     // candidate cells listed by the two-phase raytrace
+    C_NACT_NEXT,  // active rays after composite (next pass's n_act)
+    C_NSPEC,      // n_spec of the current pass (engine.py:91-94)
+    C_CAP,        // logical cache capacity (cache.py:74-75)
+    C_PHYS,       // slots with initialised maps: min(cap, n_blocks)
+    C_PHYS_OLD,   // C_PHYS before this pass's growth
+    C_NEVICT,     // victims this pass
+    C_LSTAR,      // last stamp bucket the victims reach (0xFFFFFFFF: none)
+    C_NREG,       // bitmap words the victim extraction scans ((L*+1) regions)
+    C_HW_NEXT,    // occupied slots after this pass's inserts
+    C_NWORDS_ON,  // bitmap words the visibility extraction scans (0 once no ray is active)
+    C_ERR_BUDGET, // device-side invariant failure: slot budget exceeded
+    C_ERR_CAND,   // device-side invariant failure: fewer eviction candidates than needed
+    C_ERR_CAP,    // logical capacity beyond the reserved slots (host must reserve more)
     C_COUNT
+};
+
+// Per-pass record written on the device by k_pass_end (PassStats fields).
+enum PassLog : int {
+    L_NACT = 0, L_NSPEC, L_NVIS, L_NACTB, L_NMISS, L_NEVICT, L_CAP, L_NENT, L_NAFTER, L_NITEMS, L_PHYS, L_HW,
+    L_COUNT
 };
 
 // Per-session device state.  Layout (N = rays in this session):
@@ -66,7 +87,6 @@ struct Session {
     DevBuf<uint8_t> status, exited;
     DevBuf<uint32_t> coarse_cell, fine_cell;
     DevBuf<uint32_t> act_list[2], keep, keep_off, emitted, entry_off;
-    int cur = 0;
     DevBuf<uint32_t> block_slots, ray_slots;
     DevBuf<uint32_t> ent_key, ent_val, ent_ray;
     DevBuf<float4> rgbz;
@@ -105,6 +125,12 @@ struct Session {
     int64_t init_cap = 0;
 
     int64_t n_act = 0, pass_index = 0;
+    int64_t frame_passes_hint = 1;  // passes to enqueue before the first host check of a frame
+    int64_t nact_hist[kMaxPassLog] = {};  // active rays per pass of the last frame (variant guesses)
+    DevBuf<uint32_t> plog;          // kMaxPassLog x L_COUNT per-pass records (device)
+    PinnedBuf<uint32_t> h_plog;
+    DevBuf<uint32_t> vict_bm;       // per-stamp block bitmaps for victim selection
+    int64_t vict_regions = 0;
     int64_t last_slots_used = 0, last_nvis = 0, last_nactb = 0, last_nent = 0;
     int64_t last_n_spec = 1;
     float last_kernel_ms = 0.0f;
@@ -113,20 +139,29 @@ struct Session {
             const double *dirs, double iso, int speculation, int max_spec, int64_t cache_capacity, int corrupt);
     ~Session();
     bool pass(PassStatsC &st);
+    // a whole frame (passes until no ray is active), host-checked once per
+    // batch of enqueued passes; stats of the passes that ran -> out
+    int64_t run_frame(PassStatsC *out, int64_t max_out);
     void reset(const CameraParams *cam, double iso);
     float frame_ms();  // device time from the last reset to the end of the last pass
     void download_framebuffer(uint8_t *rgba_host, float *depth_host);
     void copy_framebuffer_device(void *rgba_dst, void *depth_dst);
 
+    double reset_device_ms();  // device time of the last reset, once it has run
+    int64_t active_count();    // active rays now (read from the device after a reset)
+
    private:
     void read_counters(int first, int count);
-    void cache_lookup();
+    // nact_guess picks the traversal / composite kernel variants (each is
+    // exact for any count; the guess only matters for speed)
+    void enqueue_pass(int64_t p, int64_t nact_guess);
+    void collect_pass(int64_t p, PassStatsC &stats);
+    void check_device_errors();
     void reserve_slots(int64_t need);
-    void launch_stamp_hist();
-    void ensure_resident(int64_t n_actb, int64_t n_miss, int64_t &n_evict);
-    void select_victims(int64_t n_cand, int64_t n_evict);
-    DevBuf<uint32_t> stamp_hist;
-    int64_t hist_pass = -1;  // pass whose stamp histogram sits in h_stamp_hist
+    cudaEvent_t *pass_events(int64_t p);  // stage events of pass p (nullptr past kMaxPassLog)
+    cudaEvent_t pass_ev[kMaxPassLog][kStages + 1] = {};
+    cudaEvent_t frame_end = nullptr;      // end of the last pass that ran
+    DevBuf<uint32_t> stamp_hist;          // > kHistBins passes only
     PinnedBuf<uint32_t> h_stamp_hist;
 };
 

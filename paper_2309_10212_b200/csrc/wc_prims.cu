@@ -134,4 +134,16 @@ void bitmap_extract(const uint32_t *bm, int64_t nwords, uint32_t *word_offsets, 
     WC_LAUNCH_CHECK();
 }
 
+void bitmap_extract_dev(const uint32_t *bm, const uint32_t *d_nwords, int64_t nwords_max, uint32_t *word_offsets,
+                        uint32_t *out, uint32_t *d_count, uint32_t *partials, cudaStream_t st) {
+    if (nwords_max <= 0) {
+        WC_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st));
+        return;
+    }
+    k_scan_onepass<LoadPopc, SinkBits><<<(unsigned)scan_tiles(nwords_max), kScanThreads, 0, st>>>(
+        LoadPopc{bm}, SinkBits{bm, word_offsets, out}, nwords_max, d_nwords, reinterpret_cast<uint64_t *>(partials),
+        next_scan_epoch(), d_count);
+    WC_LAUNCH_CHECK();
+}
+
 }  // namespace wc

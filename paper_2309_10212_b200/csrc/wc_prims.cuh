@@ -234,5 +234,8 @@ void radix_sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int nbits, Radi
 // later rank a set bit: rank(b) = word_offsets[b>>5] + popc(bm[b>>5] & lowmask).
 void bitmap_extract(const uint32_t *bm, int64_t nwords, uint32_t *word_offsets, uint32_t *out,
                     uint32_t *d_count, uint32_t *partials, cudaStream_t st);
+// Same over the first *d_nwords (<= nwords_max, read on the device) words.
+void bitmap_extract_dev(const uint32_t *bm, const uint32_t *d_nwords, int64_t nwords_max, uint32_t *word_offsets,
+                        uint32_t *out, uint32_t *d_count, uint32_t *partials, cudaStream_t st);
 
 }  // namespace wc
