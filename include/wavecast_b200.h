@@ -136,6 +136,13 @@ int wc_session_run(wc_session *s, wc_pass_stats *stats_out, int64_t max_stats, i
  * on the session's allocations with no host round trip between the two. */
 int wc_session_render(wc_session *s, const wc_camera *cam, double iso, wc_pass_stats *stats_out, int64_t max_stats,
                       int64_t *n_passes);
+/* reset + run (as wc_session_render) with the framebuffer delivered into
+ * host memory (RGBA8 packed u32[n], depth f32[n]; page-locked buffers from
+ * wc_host_alloc for full-speed copies): the bulk of the copy starts on a
+ * second stream once most rays are done (the last frame tells when) and
+ * overlaps the tail passes; the pixels still active then are patched after. */
+int wc_session_render_host(wc_session *s, const wc_camera *cam, double iso, wc_pass_stats *stats_out,
+                           int64_t max_stats, int64_t *n_passes, uint32_t *rgba, float *depth);
 int wc_session_n_active(const wc_session *s, int64_t *n_active);
 /* Framebuffer.snapshot (engine.py:62-63): RGBA8 (n x 4) + float32 depth (n). */
 int wc_session_framebuffer(wc_session *s, uint8_t *rgba, float *depth);

@@ -96,6 +96,7 @@ _SIGS = {
     "wc_session_set_grouping": (_i32, [_vp, _i32]),
     "wc_session_pass": (_i32, [_vp, _vp, _vp]),
     "wc_session_run": (_i32, [_vp, _vp, _i64, _vp]),
+    "wc_session_render_host": (_i32, [_vp, _vp, _dbl, _vp, _i64, _vp, _vp, _vp]),
     "wc_session_n_active": (_i32, [_vp, _vp]),
     "wc_session_render": (_i32, [_vp, _vp, _dbl, _vp, _i64, _vp]),
     "wc_session_framebuffer": (_i32, [_vp, _vp, _vp]),

@@ -487,6 +487,16 @@ int wc_session_render(wc_session *s, const wc_camera *cam, double iso, wc_pass_s
     WC_API_END
 }
 
+int wc_session_render_host(wc_session *s, const wc_camera *cam, double iso, wc_pass_stats *stats_out,
+                           int64_t max_stats, int64_t *n_passes, uint32_t *rgba, float *depth) {
+    WC_API_BEGIN
+    const int64_t k = s->s->render_to_host(reinterpret_cast<const wc::CameraParams *>(cam), iso,
+                                           reinterpret_cast<wc::PassStatsC *>(stats_out), stats_out ? max_stats : 0,
+                                           rgba, depth);
+    if (n_passes) *n_passes = k;
+    WC_API_END
+}
+
 int wc_session_n_active(const wc_session *s, int64_t *n_active) {
     WC_API_BEGIN
     *n_active = s->s->active_count();

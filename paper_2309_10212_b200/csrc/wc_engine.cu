@@ -177,15 +177,6 @@ struct PredMiss {  // active block not resident (cache.py:69-72)
     const int32_t *slot_of_block;
     __device__ __forceinline__ uint32_t operator()(int64_t i) const { return slot_of_block[ids[i]] < 0; }
 };
-struct PredFree {  // cache.py:79
-    const int32_t *bos;
-    __device__ __forceinline__ uint32_t operator()(int64_t i) const { return bos[i] < 0; }
-};
-struct PredCand {  // resident, not stamped this pass (cache.py:84-87)
-    const int32_t *bos, *lu;
-    int32_t pass_no;
-    __device__ __forceinline__ uint32_t operator()(int64_t i) const { return bos[i] >= 0 && lu[i] < pass_no; }
-};
 
 template <class Pred>
 __global__ void k_compact_index(Pred pred, int64_t n, const uint32_t *off, uint32_t *out) {
@@ -204,14 +195,6 @@ __global__ void k_compact_miss(PredMiss pred, const uint32_t *d_n, int64_t n_max
     const int64_t n = min(n_max, (int64_t)*d_n);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         if (pred(i)) out[off[i]] = pred.ids[i];
-}
-
-__global__ void k_compact_cand(PredCand pred, int64_t n, const uint32_t *off, uint32_t *key, uint32_t *val) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        if (pred(i)) {
-            key[off[i]] = (uint32_t)pred.bos[i];
-            val[off[i]] = (uint32_t)i;
-        }
 }
 
 // --------------------------------------------------------------- traverse
@@ -885,15 +868,6 @@ __global__ void k_stamp_hist(const int32_t *block_of_slot, const int32_t *last_u
         if (sh[b]) atomicAdd(&hist[b], sh[b]);
 }
 
-// mark the blocks of the candidates stamped L in a block bitmap
-__global__ void k_mark_stamp(const int32_t *block_of_slot, const int32_t *last_used, int64_t hw, int32_t L,
-                             uint32_t *bm) {
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < hw; s += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t b = block_of_slot[s];
-        if (b >= 0 && last_used[s] == L) atomicOr(&bm[b >> 5], 1u << (b & 31));
-    }
-}
-
 // Candidates (resident, not stamped this pass) with stamp L <= L* marked in
 // the block bitmap of region L: one extraction over regions 0..L* then lists
 // them in (last_used, block_id) order (cache.py:84-91).
@@ -942,11 +916,6 @@ __global__ void k_cache_unmap(const int32_t *block_of_slot, const uint32_t *d_ph
         const int32_t b = block_of_slot[s];
         if (b >= 0) slot_of_block[b] = -1;
     }
-}
-
-__global__ void k_gather_last_used(const uint32_t *val, int64_t n, const int32_t *last_used, uint32_t *key) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        key[i] = (uint32_t)last_used[val[i]];
 }
 
 // cache.py:90-95: unmap the first n_evict candidates (they become the
@@ -1538,6 +1507,26 @@ __global__ void k_pass_end(uint32_t *ctl, uint32_t *row, int64_t n, int speculat
     ctl[C_NWORDS_ON] = n_after > 0 ? (uint32_t)nwords : 0u;
 }
 
+// ---------------------------------------------------- framebuffer read-back
+
+// rays still active after the snapshot pass (their pixels may still change)
+__global__ void k_snapshot_list(uint32_t *ctl, const uint32_t *act, uint32_t *snap) {
+    const int64_t n = ctl[C_NACT];
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl[C_NSNAP] = (uint32_t)n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        snap[i] = act[i];
+}
+
+// their final pixels: (ray, rgba, depth bits)
+__global__ void k_gather_patch(const uint32_t *ctl, const uint32_t *snap, const uint32_t *rgba, const float *depth,
+                               uint4 *patch) {
+    const int64_t n = ctl[C_NSNAP];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = snap[i];
+        patch[i] = make_uint4(r, rgba[r], __float_as_uint(depth[r]), 0u);
+    }
+}
+
 // ------------------------------------------------------------------ session
 
 static int bits_for(uint64_t max_value) {
@@ -1552,12 +1541,9 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     : vol(v), n(n_rays), iso(iso_), speculation(speculation_), max_spec(max_spec_), corrupt(corrupt_) {
     if (n < 1) throw UsageError("a session needs at least one ray");
     WC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    WC_CUDA(cudaEventCreate(&ev_begin));
-    WC_CUDA(cudaEventCreate(&ev_end));
     uniform_origin = dirs == nullptr;
     dir.alloc(n * 3);
     if (!uniform_origin) origin.alloc(n * 3);
-    for (auto &e : ev_stage) WC_CUDA(cudaEventCreate(&e));
     WC_CUDA(cudaEventCreate(&ev_frame0));
     WC_CUDA(cudaEventCreate(&ev_reset_end));
     t_enter.alloc(n);
@@ -1690,7 +1676,6 @@ void Session::reset(const CameraParams *cam, double iso_) {
     for (auto &p : pass_stage_ms)
         for (double &m : p) m = 0.0;
     WC_CUDA(cudaEventRecord(ev_reset_end, st));
-    reset_ms = 0.0;  // known once the frame's first host read has happened (reset_device_ms)
 }
 
 int64_t Session::active_count() {
@@ -1713,12 +1698,14 @@ Session::~Session() {
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
     }
-    if (ev_begin) cudaEventDestroy(ev_begin);
-    if (ev_end) cudaEventDestroy(ev_end);
+    if (st_copy) {
+        cudaStreamSynchronize(st_copy);
+        cudaStreamDestroy(st_copy);
+    }
+    if (ev_fb) cudaEventDestroy(ev_fb);
+    if (ev_fb_done) cudaEventDestroy(ev_fb_done);
     if (ev_frame0) cudaEventDestroy(ev_frame0);
     if (ev_reset_end) cudaEventDestroy(ev_reset_end);
-    for (auto &e : ev_stage)
-        if (e) cudaEventDestroy(e);
     for (auto &row : pass_ev)
         for (auto &e : row)
             if (e) cudaEventDestroy(e);
@@ -2047,6 +2034,7 @@ int64_t Session::run_frame(PassStatsC *out, int64_t max_out) {
         for (int64_t b = 0; b < batch; b++) {  // active-count guesses: exact for the first, last frame's after
             const int64_t p = p0 + b;
             enqueue_pass(p, b == 0 && n_act >= 0 ? n_act : (p < kMaxPassLog ? nact_hist[p] : 1));
+            if (p == fb_snap_pass && fb_rgba) enqueue_fb_snapshot(p);
         }
         WC_CUDA(cudaMemcpyAsync(h_plog.p, plog.p, 4 * L_COUNT * std::min<int64_t>(p0 + batch, kMaxPassLog),
                                 cudaMemcpyDeviceToHost, st));
@@ -2061,7 +2049,10 @@ int64_t Session::run_frame(PassStatsC *out, int64_t max_out) {
             }
             PassStatsC st_{};
             collect_pass(p, st_);
-            if (p < kMaxPassLog) nact_hist[p] = st_.n_active_before;
+            if (p < kMaxPassLog) {
+                nact_hist[p] = st_.n_active_before;
+                pass_ms_hist[p] = st_.duration * 1e3;
+            }
             if (out && k < max_out) out[k] = st_;
             k++;
             pass_index++;
@@ -2079,6 +2070,90 @@ float Session::frame_ms() {
     if (pass_index == 0 || !frame_end) return 0.0f;
     WC_CUDA(cudaEventElapsedTime(&ms, ev_frame0, frame_end));
     return ms;
+}
+
+// After pass p: remember the rays still active (only their pixels can
+// change from here on) and start copying the whole framebuffer to the host on
+// a second stream while the remaining passes run.
+void Session::enqueue_fb_snapshot(int64_t p) {
+    if (!st_copy) {
+        WC_CUDA(cudaStreamCreateWithFlags(&st_copy, cudaStreamNonBlocking));
+        WC_CUDA(cudaEventCreateWithFlags(&ev_fb, cudaEventDisableTiming));
+        WC_CUDA(cudaEventCreateWithFlags(&ev_fb_done, cudaEventDisableTiming));
+        snap_list.alloc(n);
+        patch.alloc(n);
+    }
+    k_snapshot_list<<<grid_for(n, 256), 256, 0, st>>>(counters.p, act_list[(p + 1) & 1].p, snap_list.p);
+    WC_LAUNCH_CHECK();
+    WC_CUDA(cudaEventRecord(ev_fb, st));
+    WC_CUDA(cudaStreamWaitEvent(st_copy, ev_fb, 0));
+    WC_CUDA(cudaMemcpyAsync(fb_rgba, rgba.p, 4 * n, cudaMemcpyDeviceToHost, st_copy));
+    WC_CUDA(cudaMemcpyAsync(fb_depth, depth.p, 4 * n, cudaMemcpyDeviceToHost, st_copy));
+    WC_CUDA(cudaEventRecord(ev_fb_done, st_copy));
+    fb_snapped = true;
+}
+
+int64_t Session::render_to_host(const CameraParams *cam, double iso_, PassStatsC *out, int64_t max_out,
+                                uint32_t *rgba_host, float *depth_host) {
+    reset(cam, iso_);
+    // Start the bulk copy after the latest pass whose successors (last frame)
+    // took longer than the copy itself (8 B/pixel at ~40 GB/s), so it hides
+    // behind them and few pixels need patching; the first frame of a session
+    // has no history and copies at the end.
+    fb_snap_pass = -1;
+    const double copy_ms = 8.0 * (double)n / 40e6;
+    double tail_ms = 0.0;
+    int64_t last = 0;
+    while (last < kMaxPassLog && nact_hist[last] > 0) last++;
+    for (int64_t p = last - 2; p >= 0; p--) {
+        tail_ms += pass_ms_hist[p + 1];
+        if (tail_ms >= copy_ms) {
+            fb_snap_pass = p;
+            break;
+        }
+    }
+    fb_rgba = rgba_host;
+    fb_depth = depth_host;
+    fb_snapped = false;
+    int64_t k = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    try {
+        k = run_frame(out, max_out);
+    } catch (...) {
+        fb_rgba = nullptr;
+        if (st_copy) cudaStreamSynchronize(st_copy);
+        throw;
+    }
+    fb_rgba = nullptr;
+    fb_depth = nullptr;
+    if (!fb_snapped) {  // no snapshot this frame: the whole framebuffer now
+        download_framebuffer(reinterpret_cast<uint8_t *>(rgba_host), depth_host);
+        return k;
+    }
+    const int64_t nsnap = h_counters.p[C_NSNAP];  // read with the frame's last counters
+    if (nsnap > 0) {
+        k_gather_patch<<<grid_for(nsnap, 256), 256, 0, st>>>(counters.p, snap_list.p, rgba.p, depth.p, patch.p);
+        WC_LAUNCH_CHECK();
+        h_patch.ensure_host(nsnap);
+        WC_CUDA(cudaMemcpyAsync(h_patch.p, patch.p, sizeof(uint4) * nsnap, cudaMemcpyDeviceToHost, st));
+    }
+    WC_CUDA(cudaStreamSynchronize(st));
+    WC_CUDA(cudaEventSynchronize(ev_fb_done));  // the bulk copy has landed before it is patched
+    const auto t2 = std::chrono::steady_clock::now();
+    for (int64_t i = 0; i < nsnap; i++) {
+        const uint4 q = h_patch.p[i];
+        rgba_host[q.x] = q.y;
+        std::memcpy(depth_host + q.x, &q.z, 4);
+    }
+    static const bool trace = getenv("WAVECAST_TRACE") != nullptr;
+    if (trace) {
+        const auto t3 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[wavecast] render_to_host: snap after pass %lld, %lld patched; frame+patch %.3f ms, scatter %.3f ms\n",
+                (long long)fb_snap_pass, (long long)nsnap,
+                std::chrono::duration<double>(t2 - t0).count() * 1e3,
+                std::chrono::duration<double>(t3 - t2).count() * 1e3);
+    }
+    return k;
 }
 
 void Session::download_framebuffer(uint8_t *rgba_host, float *depth_host) {

@@ -48,6 +48,7 @@ enum Counter : int {
     C_ERR_BUDGET, // device-side invariant failure: slot budget exceeded
     C_ERR_CAND,   // device-side invariant failure: fewer eviction candidates than needed
     C_ERR_CAP,    // logical capacity beyond the reserved slots (host must reserve more)
+    C_NSNAP,      // rays still active when the framebuffer read-back started
     C_COUNT
 };
 
@@ -107,15 +108,13 @@ struct Session {
     int32_t pass_no = 0;
     DevBuf<float> slot_values;
     DevBuf<int32_t> block_of_slot, last_used, slot_of_block;
-    DevBuf<uint32_t> miss_off, miss_ids, cand_off, cand_key, cand_val;
+    DevBuf<uint32_t> miss_off, miss_ids, cand_key, cand_val;
     // scratch
     DevBuf<uint32_t> counters, partials;
     PinnedBuf<uint32_t> h_counters;
     RadixScratch rs;
-    cudaEvent_t ev_begin = nullptr, ev_end = nullptr, ev_frame0 = nullptr, ev_reset_end = nullptr;
-    double reset_ms = 0.0;  // device time of the last reset (iso bitmaps, rays, cache maps)
+    cudaEvent_t ev_frame0 = nullptr, ev_reset_end = nullptr;
     static constexpr int kStages = 6;  // traverse, mark, cache, group, raytrace, composite
-    cudaEvent_t ev_stage[kStages + 1] = {};
     double stage_ms[kStages] = {};
     static constexpr int kMaxPassLog = 128;
     double pass_stage_ms[kMaxPassLog][kStages] = {};  // per-pass stage device ms since reset
@@ -127,6 +126,7 @@ struct Session {
     int64_t n_act = 0, pass_index = 0;
     int64_t frame_passes_hint = 1;  // passes to enqueue before the first host check of a frame
     int64_t nact_hist[kMaxPassLog] = {};  // active rays per pass of the last frame (variant guesses)
+    double pass_ms_hist[kMaxPassLog] = {};  // device ms per pass of the last frame (read-back scheduling)
     DevBuf<uint32_t> plog;          // kMaxPassLog x L_COUNT per-pass records (device)
     PinnedBuf<uint32_t> h_plog;
     DevBuf<uint32_t> vict_bm;       // per-stamp block bitmaps for victim selection
@@ -142,6 +142,10 @@ struct Session {
     // a whole frame (passes until no ray is active), host-checked once per
     // batch of enqueued passes; stats of the passes that ran -> out
     int64_t run_frame(PassStatsC *out, int64_t max_out);
+    // reset + run_frame with the framebuffer read back into pinned host
+    // memory, the bulk of it overlapped with the tail passes
+    int64_t render_to_host(const CameraParams *cam, double iso, PassStatsC *out, int64_t max_out,
+                           uint32_t *rgba_host, float *depth_host);
     void reset(const CameraParams *cam, double iso);
     float frame_ms();  // device time from the last reset to the end of the last pass
     void download_framebuffer(uint8_t *rgba_host, float *depth_host);
@@ -161,6 +165,17 @@ struct Session {
     cudaEvent_t *pass_events(int64_t p);  // stage events of pass p (nullptr past kMaxPassLog)
     cudaEvent_t pass_ev[kMaxPassLog][kStages + 1] = {};
     cudaEvent_t frame_end = nullptr;      // end of the last pass that ran
+    // overlapped read-back (render_to_host)
+    void enqueue_fb_snapshot(int64_t p);
+    cudaStream_t st_copy = nullptr;
+    cudaEvent_t ev_fb = nullptr, ev_fb_done = nullptr;
+    int64_t fb_snap_pass = -1;  // pass after which the bulk copy starts (-1: none)
+    bool fb_snapped = false;
+    uint32_t *fb_rgba = nullptr;
+    float *fb_depth = nullptr;
+    DevBuf<uint32_t> snap_list;
+    DevBuf<uint4> patch;
+    PinnedBuf<uint4> h_patch;
     DevBuf<uint32_t> stamp_hist;          // > kHistBins passes only
     PinnedBuf<uint32_t> h_stamp_hist;
 };

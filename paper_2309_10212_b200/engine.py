@@ -185,6 +185,19 @@ class RenderSession:
                   self._MAX_STATS, C.byref(k))
         return [_stats_from_c(buf[i]) for i in range(min(k.value, self._MAX_STATS))]
 
+    def render_frame_host(self, cam: Camera | None, iso: float):
+        """render_frame + the framebuffer in (pinned) host memory, most of the
+        copy overlapped with the frame's last passes.  -> (stats, rgba, depth)."""
+        cam_c = cam.to_c(self.w, self.h) if cam is not None else None
+        buf = (_lib.PassStatsC * self._MAX_STATS)()
+        k = C.c_int64()
+        base = _lib.pinned_pool.get(8 * self.n)
+        rgba = base[:4 * self.n].reshape(self.n, 4)
+        depth = base[4 * self.n:8 * self.n].view(np.float32)
+        _lib.call("wc_session_render_host", self._h, None if cam_c is None else C.byref(cam_c), float(iso), buf,
+                  self._MAX_STATS, C.byref(k), _lib.ptr(rgba), _lib.ptr(depth))
+        return [_stats_from_c(buf[i]) for i in range(min(k.value, self._MAX_STATS))], rgba, depth
+
     def reset(self, cam: Camera | None, iso: float) -> None:
         """New frame on the same allocations (fresh rays, framebuffer, cache)."""
         cam_c = cam.to_c(self.w, self.h) if cam is not None else None
@@ -281,9 +294,9 @@ def render(cv: CompressedVolume, grids: MacrocellGrids, cam: Camera, iso: float,
            opts: RenderOptions) -> tuple[Framebuffer, list[PassStats]]:
     """engine.py:385-401: render to completion; only the final frame is read back."""
     s = session_pool.get(cv, grids, opts, cam)
-    stats = s.render_frame(cam, iso)
+    stats, rgba, depth = s.render_frame_host(cam, iso)
     if not stats:  # camera missed the volume on every pixel
         fb = Framebuffer.blank(opts.width, opts.height)
         fb.completeness = 1.0
         return fb, stats
-    return s.framebuffer(stats[-1].completeness), stats
+    return Framebuffer(s.w, s.h, rgba.reshape(s.h, s.w, 4), depth.reshape(s.h, s.w), stats[-1].completeness), stats

@@ -339,3 +339,24 @@ def test_bench_report_matches_reference(wc):
     rep, tim = bench_report(cv, wc.build_grids(cv), volume="bench_small.wcz", **kw)
     assert rep == gold["report"]
     assert len(tim["frame_ms"]) == rep["n_renders"] and all(t > 0 for t in tim["frame_ms"])
+
+
+def test_repeated_renders_with_overlapped_readback(wc):
+    # render() reuses a pooled session: from its second frame the framebuffer
+    # copy starts after the pass that (last frame) left <= 1/8 of the rays
+    # active and the still-active pixels are patched afterwards.  Every frame
+    # must equal the step-by-step generator's final frame.
+    vol = host_volume("value_noise", 64, seed=4)
+    cv = wc.compress_volume(vol, 16)
+    grids = wc.build_grids(cv)
+    opts = wc.RenderOptions(width=96, height=80)
+    for k, frac in enumerate((0.0, 0.0, 0.3, 0.55, 0.55)):
+        eye, look, up, fov = orbit(cv.dims, frac)
+        cam = wc.Camera(tuple(eye), tuple(look), tuple(up), fov)
+        iso = iso_at(vol, 0.45 + 0.05 * (k % 2))
+        fb, stats = wc.render(cv, grids, cam, iso, opts)
+        last = None
+        for snap, _ in wc.render_passes(cv, grids, cam, iso, opts):
+            last = snap
+        assert np.array_equal(fb.rgba, last.rgba) and np.array_equal(fb.depth, last.depth), k
+        assert len(stats) >= 2
