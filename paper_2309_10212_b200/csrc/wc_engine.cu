@@ -2078,8 +2078,8 @@ float Session::frame_ms() {
 void Session::enqueue_fb_snapshot(int64_t p) {
     if (!st_copy) {
         WC_CUDA(cudaStreamCreateWithFlags(&st_copy, cudaStreamNonBlocking));
-        WC_CUDA(cudaEventCreateWithFlags(&ev_fb, cudaEventDisableTiming));
-        WC_CUDA(cudaEventCreateWithFlags(&ev_fb_done, cudaEventDisableTiming));
+        WC_CUDA(cudaEventCreate(&ev_fb));
+        WC_CUDA(cudaEventCreate(&ev_fb_done));
         snap_list.alloc(n);
         patch.alloc(n);
     }
@@ -2096,20 +2096,21 @@ void Session::enqueue_fb_snapshot(int64_t p) {
 int64_t Session::render_to_host(const CameraParams *cam, double iso_, PassStatsC *out, int64_t max_out,
                                 uint32_t *rgba_host, float *depth_host) {
     reset(cam, iso_);
-    // Start the bulk copy after the latest pass whose successors (last frame)
-    // took longer than the copy itself (8 B/pixel at ~40 GB/s), so it hides
-    // behind them and few pixels need patching; the first frame of a session
-    // has no history and copies at the end.
+    // Start the bulk copy after the pass that minimises (from the last
+    // frame's pass times) the copy time left exposed after the frame plus the
+    // host patching of the pixels still active then (~5 ns each); the first
+    // frame of a session has no history and copies at the end.
     fb_snap_pass = -1;
-    const double copy_ms = 8.0 * (double)n / 40e6;
-    double tail_ms = 0.0;
+    const double copy_ms = fb_copy_ms > 0.0 ? fb_copy_ms : 8.0 * (double)n / 50e6;
     int64_t last = 0;
     while (last < kMaxPassLog && nact_hist[last] > 0) last++;
+    double best_cost = copy_ms, tail_ms = 0.0;
     for (int64_t p = last - 2; p >= 0; p--) {
         tail_ms += pass_ms_hist[p + 1];
-        if (tail_ms >= copy_ms) {
+        const double cost = std::max(0.0, copy_ms - tail_ms) + 5e-6 * (double)nact_hist[p + 1];
+        if (cost < best_cost) {
+            best_cost = cost;
             fb_snap_pass = p;
-            break;
         }
     }
     fb_rgba = rgba_host;
@@ -2139,6 +2140,8 @@ int64_t Session::render_to_host(const CameraParams *cam, double iso_, PassStatsC
     }
     WC_CUDA(cudaStreamSynchronize(st));
     WC_CUDA(cudaEventSynchronize(ev_fb_done));  // the bulk copy has landed before it is patched
+    float cms = 0.0f;
+    if (cudaEventElapsedTime(&cms, ev_fb, ev_fb_done) == cudaSuccess && cms > 0.0f) fb_copy_ms = cms;
     const auto t2 = std::chrono::steady_clock::now();
     for (int64_t i = 0; i < nsnap; i++) {
         const uint4 q = h_patch.p[i];

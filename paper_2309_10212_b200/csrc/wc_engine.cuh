@@ -171,6 +171,7 @@ struct Session {
     cudaEvent_t ev_fb = nullptr, ev_fb_done = nullptr;
     int64_t fb_snap_pass = -1;  // pass after which the bulk copy starts (-1: none)
     bool fb_snapped = false;
+    double fb_copy_ms = 0.0;  // measured duration of the last bulk copy
     uint32_t *fb_rgba = nullptr;
     float *fb_depth = nullptr;
     DevBuf<uint32_t> snap_list;

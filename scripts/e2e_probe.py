@@ -8,7 +8,9 @@ cv = wc.compress_separable(f, 16); g = wc.build_grids(cv)
 r = cv.raw_block_ranges; lo, hi = float(r[:,0].min()), float(r[:,1].max()); iso = lo + 0.5*(hi-lo)
 cam = orbit_camera(cv.dims, 0, 1)
 opts = wc.RenderOptions(width=1920, height=1080)
-for i in range(8):
+flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+for i in range(12):
+    if i >= 6: flush.zero_()
     torch.cuda.synchronize(); t=time.perf_counter()
     fb, st = wc.render(cv, g, cam, iso, opts)
     t1=time.perf_counter()
