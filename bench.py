@@ -64,6 +64,8 @@ def parse():
     p.add_argument("--cache-slots", type=int, default=0, help="LRU budget (0 = reference initial_capacity)")
     p.add_argument("--tile", type=int, default=32)
     p.add_argument("--force-shard", action="store_true", help="tile sessions + NCCL gather even on one GPU")
+    p.add_argument("--rank-share", type=int, default=0,
+                   help="diagnostic: time one rank's session of an N-GPU tile split (rank 0 of N) on this GPU")
     p.add_argument("--group", action="store_true", help="sort entries by block before the raytrace "
                    "(build_rt_inputs); default off: ray order, same pixels")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -246,6 +248,8 @@ def run_b200(args):
     opts = wc.RenderOptions(width=w, height=h, max_spec=args.max_spec, cache_capacity=cache,
                             group_entries=args.group)
     pix = wdist.tile_pixels(w, h, rank, world, args.tile) if sharded else None
+    if args.rank_share > 1 and not sharded:  # one rank's share of an N-way split, alone on this GPU
+        pix = wdist.tile_pixels(w, h, 0, args.rank_share, args.tile)
     sess = wc.RenderSession(cv, grids, cam, iso, opts, pixel_ids=pix)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 

@@ -884,24 +884,6 @@ __global__ void k_mark_victims(const int32_t *block_of_slot, const int32_t *last
     }
 }
 
-// bitmap_extract sink over the concatenated regions: block ids in (region,
-// id) order; each word is cleared once read (the regions start the next
-// pass empty without a memset)
-struct SinkRegions {
-    uint32_t *bm, *ids;
-    int64_t nwords;
-    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const {
-        uint32_t v = bm[i];
-        if (!v) return;
-        bm[i] = 0;
-        const uint32_t base = (uint32_t)((i % nwords) * 32);
-        while (v) {
-            ids[prefix++] = base + __ffs(v) - 1;
-            v &= v - 1;
-        }
-    }
-};
-
 __global__ void k_blocks_to_slots(const uint32_t *blocks, const uint32_t *d_n, const int32_t *slot_of_block,
                                   uint32_t *slots) {
     const int64_t n = *d_n;
@@ -1575,8 +1557,7 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     act_bm.alloc(nwords);
     cell_mask.alloc(vol->n_coarse);
     coarse_bm.alloc(ceil_div(vol->n_coarse, 32));
-    vis_word_off.alloc(nwords);
-    act_word_off.alloc(nwords);
+    vis_word_off.alloc(2 * nwords);  // visible word offsets + the active extraction's (unused) offsets
     WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
     WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
     active_ids.alloc(std::min<int64_t>(8 * n, vol->n_blocks) + 1);
@@ -1763,6 +1744,8 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
         vict_bm.alloc(r * nwords);
         WC_CUDA(cudaMemsetAsync(vict_bm.p, 0, 4 * r * nwords, st));
         vict_regions = r;
+        sp_summary.alloc(r * nwords / 32 + 2);
+        sp_words.alloc(r * nwords + r * nwords / 32 + 2);
         const int64_t words = scan_scratch_words(r * nwords);
         if (partials.n < words) {
             partials.ensure(words);
@@ -1813,8 +1796,8 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     k_mark_active<<<grid_for((int64_t)8 * n, 256), 256, 0, st>>>(visible_ids.p, ctl + C_NVIS, vol->bdx, vol->bdy,
                                                                  vol->bdz, act_bm.p);
     WC_LAUNCH_CHECK();
-    bitmap_extract_dev(act_bm.p, ctl + C_NWORDS_ON, nwords, act_word_off.p, active_ids.p, ctl + C_NACTB, partials.p,
-                       st);
+    bitmap_extract_dev(act_bm.p, ctl + C_NWORDS_ON, nwords, vis_word_off.p + nwords, active_ids.p, ctl + C_NACTB,
+                       partials.p, st);
     k_build_entries<<<grid_for(n, 256), 256, 0, st>>>(ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p,
                                                       vis_word_off.p, ent_key.p, ent_val.p, ent_ray.p);
     WC_LAUNCH_CHECK();
@@ -1854,15 +1837,13 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     WC_LAUNCH_CHECK();
     k_phys_init<<<grid_for(slot_alloc, 256), 256, 0, st>>>(ctl, block_of_slot.p, last_used.p);
     WC_LAUNCH_CHECK();
-    if (p >= 1) {  // victims in (last_used, block_id) order: one extraction over the stamp regions
+    if (p >= 1) {  // victims in (last_used, block_id) order: one (sparse) extraction over the stamp regions
+        const SparseScratch sc{sp_summary.p, sp_words.p, ctl + C_NLIST};
         k_mark_victims<<<grid_for(slot_alloc, 256), 256, 0, st>>>(block_of_slot.p, last_used.p, ctl, stamp, nwords,
                                                                   vict_bm.p);
         WC_LAUNCH_CHECK();
-        const int64_t nreg_max = (int64_t)stamp * nwords;
-        k_scan_onepass<LoadPopc, SinkRegions><<<(unsigned)scan_tiles(nreg_max), kScanThreads, 0, st>>>(
-            LoadPopc{vict_bm.p}, SinkRegions{vict_bm.p, cand_key.p, nwords}, nreg_max, ctl + C_NREG,
-            reinterpret_cast<uint64_t *>(partials.p), next_scan_epoch(), ctl + C_NCAND);
-        WC_LAUNCH_CHECK();
+        bitmap_extract_sparse(vict_bm.p, ctl + C_NREG, (int64_t)stamp * nwords, nwords, nullptr, cand_key.p,
+                              ctl + C_NCAND, true, sc, partials.p, st);  // clears the regions
         k_blocks_to_slots<<<grid_for(slot_alloc, 256), 256, 0, st>>>(cand_key.p, ctl + C_NEVICT, slot_of_block.p,
                                                                      cand_val.p);
         WC_LAUNCH_CHECK();

@@ -49,6 +49,7 @@ enum Counter : int {
     C_ERR_CAND,   // device-side invariant failure: fewer eviction candidates than needed
     C_ERR_CAP,    // logical capacity beyond the reserved slots (host must reserve more)
     C_NSNAP,      // rays still active when the framebuffer read-back started
+    C_NLIST,      // non-zero bitmap words listed by bitmap_extract_sparse
     C_COUNT
 };
 
@@ -96,7 +97,7 @@ struct Session {
     DevBuf<float4> item_corners;
     DevBuf<uint32_t> best;
     DevBuf<double> item_t;
-    DevBuf<uint32_t> vis_bm, act_bm, vis_word_off, act_word_off;
+    DevBuf<uint32_t> vis_bm, act_bm, vis_word_off;
     DevBuf<uint32_t> coarse_bm;            // per-iso coarse range-test bitmap, rebuilt at every reset
     DevBuf<unsigned long long> cell_mask;  // per-iso fine range tests, 64 per coarse cell
     DevBuf<uint32_t> visible_ids, block_ray_off, active_ids;
@@ -130,6 +131,7 @@ struct Session {
     DevBuf<uint32_t> plog;          // kMaxPassLog x L_COUNT per-pass records (device)
     PinnedBuf<uint32_t> h_plog;
     DevBuf<uint32_t> vict_bm;       // per-stamp block bitmaps for victim selection
+    DevBuf<uint32_t> sp_summary, sp_words;  // bitmap_extract_sparse scratch (sized with the regions)
     int64_t vict_regions = 0;
     int64_t last_slots_used = 0, last_nvis = 0, last_nactb = 0, last_nent = 0;
     int64_t last_n_spec = 1;

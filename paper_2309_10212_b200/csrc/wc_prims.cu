@@ -146,4 +146,65 @@ void bitmap_extract_dev(const uint32_t *bm, const uint32_t *d_nwords, int64_t nw
     WC_LAUNCH_CHECK();
 }
 
+// ---- two-level extraction ----------------------------------------------
+
+// summary bit w = (bm[w] != 0), warp per 32 words (one coalesced 128 B read)
+__global__ void k_summarize(const uint32_t *__restrict__ bm, const uint32_t *d_nwords, int64_t nwords_max,
+                            uint32_t *__restrict__ summary) {
+    const int64_t n = d_nwords ? min(nwords_max, (int64_t)*d_nwords) : nwords_max;
+    const int64_t ns = (nwords_max + 31) >> 5;  // every summary word (zero past n): no stale bits
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t sidx = w0; sidx < ns; sidx += nw) {
+        const int64_t w = sidx * 32 + lane;
+        const uint32_t bits = __ballot_sync(0xffffffffu, w < n && bm[w] != 0u);
+        if (lane == 0) summary[sidx] = bits;
+    }
+}
+
+struct LoadPopcIdx {
+    const uint32_t *bm, *idx;
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const { return __popc(bm[idx[i]]); }
+};
+
+struct SinkBitsIdx {
+    uint32_t *bm;
+    const uint32_t *idx;
+    uint32_t *word_offsets, *ids;
+    int64_t id_mod;
+    bool clear;
+    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const {
+        const uint32_t w = idx[i];
+        uint32_t v = bm[w];
+        if (word_offsets) word_offsets[w] = prefix;
+        if (clear) bm[w] = 0u;
+        const uint32_t base = (uint32_t)((w % id_mod) * 32);
+        while (v) {
+            ids[prefix++] = base + __ffs(v) - 1;
+            v &= v - 1;
+        }
+    }
+};
+
+void bitmap_extract_sparse(uint32_t *bm, const uint32_t *d_nwords, int64_t nwords_max, int64_t id_mod,
+                           uint32_t *word_offsets, uint32_t *ids, uint32_t *d_count, bool clear,
+                           const SparseScratch &sc, uint32_t *partials, cudaStream_t st) {
+    if (nwords_max <= 0) {
+        WC_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st));
+        return;
+    }
+    const int64_t ns_max = (nwords_max + 31) / 32;
+    k_summarize<<<grid_for(ns_max * 32, 256, 8), 256, 0, st>>>(bm, d_nwords, nwords_max, sc.summary);
+    WC_LAUNCH_CHECK();
+    k_scan_onepass<LoadPopc, SinkBits><<<(unsigned)scan_tiles(ns_max), kScanThreads, 0, st>>>(
+        LoadPopc{sc.summary}, SinkBits{sc.summary, sc.word_list + nwords_max, sc.word_list}, ns_max, nullptr,
+        reinterpret_cast<uint64_t *>(partials), next_scan_epoch(), sc.d_nlist);
+    WC_LAUNCH_CHECK();
+    k_scan_onepass<LoadPopcIdx, SinkBitsIdx><<<(unsigned)scan_tiles(nwords_max), kScanThreads, 0, st>>>(
+        LoadPopcIdx{bm, sc.word_list}, SinkBitsIdx{bm, sc.word_list, word_offsets, ids, id_mod, clear}, nwords_max,
+        sc.d_nlist, reinterpret_cast<uint64_t *>(partials), next_scan_epoch(), d_count);
+    WC_LAUNCH_CHECK();
+}
+
 }  // namespace wc

@@ -238,4 +238,21 @@ void bitmap_extract(const uint32_t *bm, int64_t nwords, uint32_t *word_offsets, 
 void bitmap_extract_dev(const uint32_t *bm, const uint32_t *d_nwords, int64_t nwords_max, uint32_t *word_offsets,
                         uint32_t *out, uint32_t *d_count, uint32_t *partials, cudaStream_t st);
 
+// Two-level extraction for sparse bitmaps: cost grows with the non-zero
+// words, not with the bitmap.  A streaming pass writes a summary (bit w of
+// the summary = word w is non-zero), a scan of the summary lists the
+// non-zero words in order, and a scan of their popcounts writes the ids
+// (bit b of word w -> (w % id_mod) * 32 + b, so concatenated bitmaps of
+// id_mod words each list (bitmap, id) pairs in order).  word_offsets
+// (nullable) receives the prefix of each non-zero word; clear zeroes the
+// non-zero words as they are read.  Scratch: summary >= nwords_max/32 + 1,
+// word_list >= nwords_max + nwords_max/32 + 1 words, partials >=
+// scan_scratch_words(nwords_max).
+struct SparseScratch {
+    uint32_t *summary, *word_list, *d_nlist;
+};
+void bitmap_extract_sparse(uint32_t *bm, const uint32_t *d_nwords, int64_t nwords_max, int64_t id_mod,
+                           uint32_t *word_offsets, uint32_t *ids, uint32_t *d_count, bool clear,
+                           const SparseScratch &sc, uint32_t *partials, cudaStream_t st);
+
 }  // namespace wc
