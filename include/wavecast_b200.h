@@ -128,6 +128,10 @@ int wc_session_set_base_color(wc_session *s, double r, double g, double b);
  * the raytrace is correct either way (same pixels); grouping yields the
  * reference's PassBuffers layout (required by wc_session_rt_inputs). */
 int wc_session_set_grouping(wc_session *s, int group_entries);
+/* Replay passes as captured CUDA graphs (default on; WAVECAST_NO_GRAPHS=1 in
+ * the environment turns it off).  Off = plain launches with per-stage
+ * timing (wc_session_stage_ms); on = the pass timed as a whole. */
+int wc_session_set_graphs(wc_session *s, int on);
 /* One pass; *ran = 0 once every ray has terminated. */
 int wc_session_pass(wc_session *s, wc_pass_stats *stats, int *ran);
 /* Run passes until done (render, engine.py:385-401); returns pass count. */

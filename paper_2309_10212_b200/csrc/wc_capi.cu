@@ -456,6 +456,12 @@ int wc_session_set_base_color(wc_session *s, double r, double g, double b) {
     WC_API_END
 }
 
+int wc_session_set_graphs(wc_session *s, int on) {
+    WC_API_BEGIN
+    s->s->use_graphs = on != 0;
+    WC_API_END
+}
+
 int wc_session_set_grouping(wc_session *s, int group_entries) {
     WC_API_BEGIN
     s->s->group_entries = group_entries != 0;

@@ -202,7 +202,15 @@ __global__ void k_compact_miss(PredMiss pred, const uint32_t *d_n, int64_t n_max
 struct RayView {
     const double *origin;  // nullable -> eye
     const double *dir, *t_enter;
-    double ex, ey, ez;
+    const double *eye;  // FrameParams (device): the camera eye of this frame
+    double ex = 0.0, ey = 0.0, ez = 0.0;
+    __device__ __forceinline__ void bind() {  // once per kernel: the eye into registers
+        if (!origin) {
+            ex = eye[0];
+            ey = eye[1];
+            ez = eye[2];
+        }
+    }
     __device__ __forceinline__ void load(int64_t r, double o[3], double d[3]) const {
         if (origin) {
             o[0] = origin[3 * r];
@@ -300,6 +308,7 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
     TraverseArgs a = a_in;
     a.n_act = a.ctl[C_NACT];
     a.n_spec = (int)a.ctl[C_NSPEC];
+    a.rays.bind();
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
@@ -510,6 +519,7 @@ __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a_in) {
     TraverseArgs a = a_in;
     a.n_act = a.ctl[C_NACT];
     a.n_spec = (int)a.ctl[C_NSPEC];
+    a.rays.bind();
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
@@ -1068,7 +1078,7 @@ struct RaytraceArgs {
     const float *slot_values;
     int bdx, bdy, bdz, nx, ny, nz;
     RayView rays;
-    double iso, br, bg, bb;
+    const double *fp;  // FrameParams (device): [3] iso, [4..6] base colour
     float4 *rgbz;
     const uint32_t *d_n_ent;  // entry count on the device (Counter C_NENT)
 };
@@ -1079,7 +1089,9 @@ struct RaytraceArgs {
 // tracer (blocktrace.py:317-449) over the block's <= 4^3 dual cells and
 // writes (rgb, z) -- or (0, 0, 0, +inf) on a miss -- at its entry id.
 __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_raytrace(RaytraceArgs a) {
+    a.rays.bind();
     const int64_t n_ent = *a.d_n_ent;
+    const double iso = a.fp[3], br = a.fp[4], bg = a.fp[5], bb = a.fp[6];
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_ent; j += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t v = a.ent_key[j], k = a.ent_val[j];
         const int64_t r = a.ent_ray[k];
@@ -1095,7 +1107,7 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_raytrace(Raytrace
         a.rays.load(r, o, d);
         float rgb[3];
         const double t = trace_region(field, 4 * bx, 4 * by, 4 * bz, 4 * bx, 4 * by, 4 * bz, cx, cy, cz, o, d,
-                                      a.rays.t_enter[r], a.iso, a.br, a.bg, a.bb, rgb);
+                                      a.rays.t_enter[r], iso, br, bg, bb, rgb);
         a.rgbz[k] = t != CUDART_INF ? make_float4(rgb[0], rgb[1], rgb[2], (float)t)
                                     : make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
     }
@@ -1125,7 +1137,7 @@ struct EntryCtx {  // everything an entry's trace needs, rebuilt from its positi
     double o[3], d[3], te;
 };
 
-__device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, int64_t j) {
+__device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, const RayView &rv, int64_t j) {
     EntryCtx e;
     const uint32_t v = a.ent_key[j];
     e.k = a.ent_val[j];
@@ -1139,20 +1151,23 @@ __device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, int64_t j) 
     e.cx = max(0, min(4, a.nx - 1 - 4 * e.bx));
     e.cy = max(0, min(4, a.ny - 1 - 4 * e.by));
     e.cz = max(0, min(4, a.nz - 1 - 4 * e.bz));
-    a.rays.load(e.r, e.o, e.d);
-    e.te = a.rays.t_enter[e.r];
+    rv.load(e.r, e.o, e.d);
+    e.te = rv.t_enter[e.r];
     return e;
 }
 
 // phase 1: walk each entry's dual cells, list the bracketing ones
 __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
     const RaytraceArgs &a = s.a;
+    RayView rv = a.rays;
+    rv.bind();
     const int lane = threadIdx.x & 31;
     __shared__ const float *rowtab[8][128];
     const SlotFieldSmem<128> sf{&rowtab[0][threadIdx.x]};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     // warp-uniform trip count: the list append below is a full-warp scan
     const int64_t n_ent = *a.d_n_ent;
+    const double iso = a.fp[3];
     for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); j0 < n_ent; j0 += stride) {
         const int64_t j = j0 + lane;
         // the <= 10 bracketing cells of the walk, 6-bit local codes in DDA order
@@ -1161,7 +1176,7 @@ __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
         uint32_t ek = 0, er = 0, eb = 0;  // kept for the item write-out
         SlotField ef{a.slot_values, -1, -1, -1, -1, -1, -1, -1, -1};
         if (j < n_ent) {
-            const EntryCtx e = entry_ctx(a, j);
+            const EntryCtx e = entry_ctx(a, rv, j);
             ek = e.k;
             er = (uint32_t)e.r;
             eb = (uint32_t)(e.bx + a.bdx * (e.by + a.bdy * e.bz));
@@ -1170,7 +1185,7 @@ __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
             const int sl[8] = {ef.s0, ef.s1, ef.s2, ef.s3, ef.s4, ef.s5, ef.s6, ef.s7};
             SlotFieldSmem<128>::fill(&rowtab[0][threadIdx.x], a.slot_values, sl);
             walk_bracketing_cells(sf, 4 * e.bx, 4 * e.by, 4 * e.bz, 4 * e.bx, 4 * e.by, 4 * e.bz, e.cx, e.cy,
-                                  e.cz, e.o, e.d, e.te, a.iso, [&](int cx, int cy, int cz, int seq) {
+                                  e.cz, e.o, e.d, e.te, iso, [&](int cx, int cy, int cz, int seq) {
                                       const uint32_t lc = (uint32_t)((cx - 4 * e.bx) | ((cy - 4 * e.by) << 2) |
                                                                      ((cz - 4 * e.bz) << 4));
                                       codes |= (unsigned long long)lc << (6 * seq);
@@ -1212,7 +1227,10 @@ __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
 // with a root wins through an atomicMin on (seq, item)
 __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArgs s) {
     const RaytraceArgs &a = s.a;
+    RayView rv = a.rays;
+    rv.bind();
     const int64_t n_items = min((int64_t)*s.n_items, s.item_cap);
+    const double iso = a.fp[3];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_items; i += (int64_t)gridDim.x * blockDim.x) {
         const uint4 info = s.item_info[i];
         const float4 c0 = s.item_corners[2 * i], c1 = s.item_corners[2 * i + 1];
@@ -1222,8 +1240,8 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArg
         const int bx = (int)(b % (uint32_t)a.bdx), by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy),
                   bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
         double o[3], d[3];
-        a.rays.load(r, o, d);
-        const double th = solve_cell(c, o, d, 4 * bx + lx, 4 * by + ly, 4 * bz + lz, a.rays.t_enter[r], a.iso);
+        rv.load(r, o, d);
+        const double th = solve_cell(c, o, d, 4 * bx + lx, 4 * by + ly, 4 * bz + lz, rv.t_enter[r], iso);
         if (th != CUDART_INF) {
             s.item_t[i] = th;
             atomicMin(&s.best[k], ((uint32_t)seq << 27) | (uint32_t)i);
@@ -1234,6 +1252,8 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArg
 // phase 3: shade each entry's winning cell (or record the miss)
 __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
     const RaytraceArgs &a = s.a;
+    RayView rv = a.rays;
+    rv.bind();
     const int64_t n_ent = *a.d_n_ent;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_ent; j += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t k = a.ent_val[j];
@@ -1251,10 +1271,10 @@ __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
         const int bx = (int)(b % (uint32_t)a.bdx), by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy),
                   bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
         double o[3], d[3];
-        a.rays.load(r, o, d);
+        rv.load(r, o, d);
         float rgb[3];
         const double th = s.item_t[i];
-        shade_hit(c, o, d, 4 * bx + lx, 4 * by + ly, 4 * bz + lz, th, a.br, a.bg, a.bb, rgb);
+        shade_hit(c, o, d, 4 * bx + lx, 4 * by + ly, 4 * bz + lz, th, a.fp[4], a.fp[5], a.fp[6], rgb);
         a.rgbz[k] = make_float4(rgb[0], rgb[1], rgb[2], (float)th);
     }
 }
@@ -1408,7 +1428,18 @@ __device__ __forceinline__ int64_t n_spec_of(int64_t n, int64_t n_act, int specu
 // after the initial active scan (C_NACT): the first pass's n_spec and an
 // empty cache of the initial capacity (cache.py:27-40)
 __global__ void k_frame_start(uint32_t *ctl, int64_t n, int speculation, int max_spec, int64_t cap, int64_t phys,
-                              int64_t nwords) {
+                              int64_t nwords, uint32_t frame, double *fp, double ex, double ey, double ez, double iso,
+                              double br, double bg, double bb) {
+    // FrameParams: what changes between frames lives in device memory, so the
+    // captured pass graphs are frame-invariant
+    fp[0] = ex;
+    fp[1] = ey;
+    fp[2] = ez;
+    fp[3] = iso;
+    fp[4] = br;
+    fp[5] = bg;
+    fp[6] = bb;
+    ctl[C_FRAME] = frame;
     const int64_t n_act = ctl[C_NACT];
     ctl[C_NSPEC] = (uint32_t)n_spec_of(n, n_act, speculation, max_spec);
     ctl[C_CAP] = (uint32_t)cap;
@@ -1581,6 +1612,7 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
         WC_CUDA(cudaMemcpyAsync(dir_in.p, dirs, 24 * n, cudaMemcpyHostToDevice, st));
     }
     init_cap = cache_capacity;
+    use_graphs = getenv("WAVECAST_NO_GRAPHS") == nullptr;
     contrib.alloc(2 * n);
     // every buffer a pass touches, at its largest size (a pass never allocates):
     // the cache for ceil(1.5 * min(8 N, n_blocks)) slots (cache.py:74-75 on the
@@ -1593,6 +1625,7 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     item_t.alloc(10 * n);
     best.alloc(n);
     plog.alloc((int64_t)kMaxPassLog * L_COUNT);
+    fparams.alloc(8);
     h_plog.alloc((int64_t)kMaxPassLog * L_COUNT);
     reset(cam, iso_);
 }
@@ -1646,7 +1679,10 @@ void Session::reset(const CameraParams *cam, double iso_) {
     scan_exclusive(pa, n, entry_off.p, counters.p + C_NACT, partials.p, st);
     k_compact_index<<<grid_for(n, 256), 256, 0, st>>>(pa, n, entry_off.p, act_list[0].p);
     WC_LAUNCH_CHECK();
-    k_frame_start<<<1, 1, 0, st>>>(counters.p, n, speculation, max_spec, cap, phys, ceil_div(vol->n_blocks, 32));
+    if ((++frame_no & 0x1FFFFu) == 0)  // device-derived scan epochs wrap: forget old status words
+        WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
+    k_frame_start<<<1, 1, 0, st>>>(counters.p, n, speculation, max_spec, cap, phys, ceil_div(vol->n_blocks, 32),
+                                   frame_no, fparams.p, eye[0], eye[1], eye[2], iso, base[0], base[1], base[2]);
     WC_LAUNCH_CHECK();
     pass_no = 0;
     hw = 0;
@@ -1654,6 +1690,7 @@ void Session::reset(const CameraParams *cam, double iso_) {
     n_act = -1;  // on the device until the first pass reads it
     frame_end = nullptr;
     for (double &m : stage_ms) m = 0.0;
+    graph_ms = 0.0;
     for (auto &p : pass_stage_ms)
         for (double &m : p) m = 0.0;
     WC_CUDA(cudaEventRecord(ev_reset_end, st));
@@ -1675,6 +1712,7 @@ double Session::reset_device_ms() {
 }
 
 Session::~Session() {
+    drop_graphs();
     if (st) {
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
@@ -1704,6 +1742,7 @@ void Session::read_counters(int first, int count) {
 // the cache decisions can stay on the device.
 void Session::reserve_slots(int64_t need) {
     if (need <= slot_alloc) return;
+    drop_graphs();  // they hold the old buffers
     slot_values.grow(need * 64, st);
     block_of_slot.grow(need, st);
     last_used.grow(need, st);
@@ -1725,20 +1764,13 @@ cudaEvent_t *Session::pass_events(int64_t p) {
     return pass_ev[p];
 }
 
-// One pass of render_passes (engine.py:326-382), enqueued without any host
-// read: every size comes from the device control block (Counter).  p is the
-// pass index since the last reset; its cache stamp is p + 1.
-void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
+// Host-side preparation of pass p (allocations happen here, never inside a
+// captured pass): the victim regions must hold one bitmap per stamp a
+// candidate can carry.  Reallocation invalidates the captured pass graphs.
+void Session::prepare_pass(int64_t p) {
     const int64_t nwords = ceil_div(vol->n_blocks, 32);
-    const int32_t stamp = (int32_t)(p + 1);
-    pass_no = stamp;
-    uint32_t *ctl = counters.p;
-    uint32_t *alist = act_list[p & 1].p;
-    cudaEvent_t *ev = pass_events(p);
-    auto mark = [&](int k) {
-        if (ev) WC_CUDA(cudaEventRecord(ev[k], st));
-    };
-    // the victim regions must hold one bitmap per stamp a candidate can carry
+    const int64_t stamp = p + 1;
+    pass_events(p);
     if (vict_regions < stamp) {
         const int64_t r = std::max<int64_t>(stamp, std::max<int64_t>(8, 2 * vict_regions));
         vict_bm.alloc(r * nwords);
@@ -1751,13 +1783,98 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
             partials.ensure(words);
             WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
         }
+        drop_graphs();
     }
+}
+
+void Session::drop_graphs() {
+    for (auto &g : graphs) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+}
+
+// Pass p as a CUDA graph: captured once per (p, kernel variants) and then
+// replayed every frame.  Everything that changes between frames is read on
+// the device (control block, FrameParams, device-derived scan epochs), so a
+// replay is exactly the enqueued pass.  Modes with host reads inside a pass
+// (entry grouping, more passes than histogram bins) are enqueued directly.
+void Session::launch_pass(int64_t p, int64_t nact_guess) {
+    const bool warp_trav = nact_guess <= WC_WARP_TRAVERSE_MAX;
+    const bool warp_comp = speculation && n / std::max<int64_t>(1, nact_guess) >= 8;
+    if (!use_graphs || group_entries || p + 2 > kHistBins || p >= kMaxPassLog) {
+        enqueue_pass(p, nact_guess);
+        return;
+    }
+    prepare_pass(p);
+    PassGraph *g = nullptr;
+    for (auto &x : graphs)
+        if (x.p == p && x.warp_trav == warp_trav && x.warp_comp == warp_comp) g = &x;
+    if (!g) {
+        const long long launches0 = g_launches.load();
+        cudaGraph_t graph = nullptr;
+        WC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_pass(p, nact_guess);
+        } catch (...) {
+            cudaStreamEndCapture(st, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        WC_CUDA(cudaStreamEndCapture(st, &graph));
+        PassGraph pg{p, warp_trav, warp_comp, nullptr, g_launches.load() - launches0};
+        g_launches -= pg.kernels;  // captured, not launched
+        const cudaError_t e = cudaGraphInstantiate(&pg.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        WC_CUDA(e);
+        graphs.push_back(pg);
+        g = &graphs.back();
+    }
+    cudaEvent_t *ev = pass_events(p);
+    WC_CUDA(cudaEventRecord(ev[0], st));
+    WC_CUDA(cudaGraphLaunch(g->exec, st));
+    WC_CUDA(cudaEventRecord(ev[kStages], st));
+    pass_staged[p] = false;
+    g_launches += g->kernels;
+}
+
+// One pass of render_passes (engine.py:326-382), enqueued without any host
+// read: every size comes from the device control block (Counter).  p is the
+// pass index since the last reset; its cache stamp is p + 1.
+namespace {
+// scan epochs of the pass derived on the device (the pass may be captured
+// into a graph and replayed; see scan_epoch)
+struct DeviceEpochs {
+    DeviceEpochs(const uint32_t *d_frame, uint32_t salt) {
+        t_epoch_frame = d_frame;
+        t_epoch_salt = salt;
+    }
+    ~DeviceEpochs() { t_epoch_frame = nullptr; }
+};
+}  // namespace
+
+void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
+    const int64_t nwords = ceil_div(vol->n_blocks, 32);
+    const int32_t stamp = (int32_t)(p + 1);
+    pass_no = stamp;
+    uint32_t *ctl = counters.p;
+    const DeviceEpochs epochs(ctl + C_FRAME, (uint32_t)(p % 256) * 16u);
+    uint32_t *alist = act_list[p & 1].p;
+    cudaEvent_t *ev = pass_events(p);
+    // stage events only when the pass is launched directly (a captured pass
+    // is timed as a whole, around its graph launch)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    WC_CUDA(cudaStreamIsCapturing(st, &cap));
+    const bool capturing = cap != cudaStreamCaptureStatusNone;
+    pass_staged[std::min<int64_t>(p, kMaxPassLog - 1)] = !capturing;
+    auto mark = [&](int k) {
+        if (ev && !capturing) WC_CUDA(cudaEventRecord(ev[k], st));
+    };
+    prepare_pass(p);
     mark(0);
 
     // traverse_to_next_blocks + fused visibility marking (one of the two
     // kernels runs, by the device n_act)
     TraverseArgs ta{};
-    ta.rays = RayView{uniform_origin ? nullptr : origin.p, dir.p, t_enter.p, eye[0], eye[1], eye[2]};
+    ta.rays = RayView{uniform_origin ? nullptr : origin.p, dir.p, t_enter.p, fparams.p};
     ta.t_exit = t_exit.p;
     ta.exited = exited.p;
     ta.coarse_cell = coarse_cell.p;
@@ -1773,7 +1890,6 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     ta.cdx = vol->cdx;
     ta.cdy = vol->cdy;
     ta.cdz = vol->cdz;
-    ta.iso = iso;
     ta.block_slots = block_slots.p;
     ta.ray_slots = ray_slots.p;
     ta.emitted = emitted.p;
@@ -1890,10 +2006,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     ra.ny = vol->ny;
     ra.nz = vol->nz;
     ra.rays = ta.rays;
-    ra.iso = iso;
-    ra.br = base[0];
-    ra.bg = base[1];
-    ra.bb = base[2];
+    ra.fp = fparams.p;
     ra.rgbz = rgbz.p;
     if (WC_SPLIT_RAYTRACE) {
         SplitArgs sa{};
@@ -1944,12 +2057,20 @@ void Session::collect_pass(int64_t p, PassStatsC &stats) {
     const uint32_t *r = h_plog.p + std::min<int64_t>(p, kMaxPassLog - 1) * L_COUNT;
     double ms_pass = 0.0;
     if (cudaEvent_t *ev = pass_events(p)) {
-        for (int k = 0; k < kStages; k++) {
+        if (pass_staged[p]) {
+            for (int k = 0; k < kStages; k++) {
+                float ms = 0.0f;
+                WC_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+                stage_ms[k] += ms;
+                pass_stage_ms[p][k] = ms;
+                ms_pass += ms;
+            }
+        } else {  // graph replay: the pass as a whole
             float ms = 0.0f;
-            WC_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
-            stage_ms[k] += ms;
-            pass_stage_ms[p][k] = ms;
-            ms_pass += ms;
+            WC_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[kStages]));
+            ms_pass = ms;
+            for (int k = 0; k < kStages; k++) pass_stage_ms[p][k] = 0.0;
+            graph_ms += ms;
         }
         last_kernel_ms = (float)ms_pass;
         frame_end = ev[kStages];
@@ -1992,7 +2113,7 @@ bool Session::pass(PassStatsC &stats) {
         n_act = h_counters.p[C_NACT];
     }
     if (n_act == 0) return false;
-    enqueue_pass(pass_index, n_act);
+    launch_pass(pass_index, n_act);
     WC_CUDA(cudaMemcpyAsync(h_plog.p, plog.p, 4 * L_COUNT * std::min<int64_t>(pass_index + 1, kMaxPassLog),
                             cudaMemcpyDeviceToHost, st));
     read_counters(0, C_COUNT);
@@ -2014,7 +2135,7 @@ int64_t Session::run_frame(PassStatsC *out, int64_t max_out) {
         batch = p0 < kMaxPassLog ? std::min<int64_t>(batch, kMaxPassLog - p0) : 1;  // one log row per pass
         for (int64_t b = 0; b < batch; b++) {  // active-count guesses: exact for the first, last frame's after
             const int64_t p = p0 + b;
-            enqueue_pass(p, b == 0 && n_act >= 0 ? n_act : (p < kMaxPassLog ? nact_hist[p] : 1));
+            launch_pass(p, b == 0 && n_act >= 0 ? n_act : (p < kMaxPassLog ? nact_hist[p] : 1));
             if (p == fb_snap_pass && fb_rgba) enqueue_fb_snapshot(p);
         }
         WC_CUDA(cudaMemcpyAsync(h_plog.p, plog.p, 4 * L_COUNT * std::min<int64_t>(p0 + batch, kMaxPassLog),

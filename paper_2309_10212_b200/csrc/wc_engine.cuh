@@ -1,6 +1,8 @@
 // wc_engine.cuh -- the per-pass wavefront session (engine.py:308-382).
 #pragma once
 
+#include <vector>
+
 #include "wc_common.cuh"
 #include "wc_prims.cuh"
 #include "wc_volume.cuh"
@@ -50,6 +52,7 @@ enum Counter : int {
     C_ERR_CAP,    // logical capacity beyond the reserved slots (host must reserve more)
     C_NSNAP,      // rays still active when the framebuffer read-back started
     C_NLIST,      // non-zero bitmap words listed by bitmap_extract_sparse
+    C_FRAME,      // frame counter (device-derived scan epochs)
     C_COUNT
 };
 
@@ -83,6 +86,7 @@ struct Session {
     // its block locality from ray order + L1 (measured 1.70 vs 1.69 ms at C3)
     // and the sort costs 0.5 ms/frame; on for the reference PassBuffers views.
     bool group_entries = false;
+    bool use_graphs = true;  // replay passes as captured CUDA graphs (WAVECAST_NO_GRAPHS=1: plain launches)
     double eye[3] = {0, 0, 0};
 
     DevBuf<double> origin, dir, t_enter, t_exit, coarse_tmax, fine_tmax;
@@ -119,6 +123,8 @@ struct Session {
     double stage_ms[kStages] = {};
     static constexpr int kMaxPassLog = 128;
     double pass_stage_ms[kMaxPassLog][kStages] = {};  // per-pass stage device ms since reset
+    bool pass_staged[kMaxPassLog] = {};  // pass timed per stage (launched directly) or as a whole (graph)
+    double graph_ms = 0.0;               // device ms of the graph-replayed passes since reset
     DevBuf<uint32_t> pix;
     DevBuf<double> dir_in;
     CameraParams cam_params{};
@@ -131,6 +137,8 @@ struct Session {
     DevBuf<uint32_t> plog;          // kMaxPassLog x L_COUNT per-pass records (device)
     PinnedBuf<uint32_t> h_plog;
     DevBuf<uint32_t> vict_bm;       // per-stamp block bitmaps for victim selection
+    DevBuf<double> fparams;         // FrameParams: eye[3], iso, base colour[3] (written by k_frame_start)
+    uint32_t frame_no = 0;
     DevBuf<uint32_t> sp_summary, sp_words;  // bitmap_extract_sparse scratch (sized with the regions)
     int64_t vict_regions = 0;
     int64_t last_slots_used = 0, last_nvis = 0, last_nactb = 0, last_nent = 0;
@@ -161,6 +169,16 @@ struct Session {
     // nact_guess picks the traversal / composite kernel variants (each is
     // exact for any count; the guess only matters for speed)
     void enqueue_pass(int64_t p, int64_t nact_guess);
+    void prepare_pass(int64_t p);
+    void launch_pass(int64_t p, int64_t nact_guess);  // enqueue_pass through a cached CUDA graph
+    void drop_graphs();
+    struct PassGraph {
+        int64_t p;
+        bool warp_trav, warp_comp;
+        cudaGraphExec_t exec;
+        long long kernels;  // kernels per replay (the launch counter)
+    };
+    std::vector<PassGraph> graphs;
     void collect_pass(int64_t p, PassStatsC &stats);
     void check_device_errors();
     void reserve_slots(int64_t need);

@@ -130,7 +130,7 @@ void bitmap_extract(const uint32_t *bm, int64_t nwords, uint32_t *word_offsets, 
     // soon as its prefix is known
     k_scan_onepass<LoadPopc, SinkBits><<<(unsigned)scan_tiles(nwords), kScanThreads, 0, st>>>(
         LoadPopc{bm}, SinkBits{bm, word_offsets, out}, nwords, nullptr, reinterpret_cast<uint64_t *>(partials),
-        next_scan_epoch(), d_count);
+        scan_epoch(), d_count);
     WC_LAUNCH_CHECK();
 }
 
@@ -142,7 +142,7 @@ void bitmap_extract_dev(const uint32_t *bm, const uint32_t *d_nwords, int64_t nw
     }
     k_scan_onepass<LoadPopc, SinkBits><<<(unsigned)scan_tiles(nwords_max), kScanThreads, 0, st>>>(
         LoadPopc{bm}, SinkBits{bm, word_offsets, out}, nwords_max, d_nwords, reinterpret_cast<uint64_t *>(partials),
-        next_scan_epoch(), d_count);
+        scan_epoch(), d_count);
     WC_LAUNCH_CHECK();
 }
 
@@ -199,11 +199,11 @@ void bitmap_extract_sparse(uint32_t *bm, const uint32_t *d_nwords, int64_t nword
     WC_LAUNCH_CHECK();
     k_scan_onepass<LoadPopc, SinkBits><<<(unsigned)scan_tiles(ns_max), kScanThreads, 0, st>>>(
         LoadPopc{sc.summary}, SinkBits{sc.summary, sc.word_list + nwords_max, sc.word_list}, ns_max, nullptr,
-        reinterpret_cast<uint64_t *>(partials), next_scan_epoch(), sc.d_nlist);
+        reinterpret_cast<uint64_t *>(partials), scan_epoch(), sc.d_nlist);
     WC_LAUNCH_CHECK();
     k_scan_onepass<LoadPopcIdx, SinkBitsIdx><<<(unsigned)scan_tiles(nwords_max), kScanThreads, 0, st>>>(
         LoadPopcIdx{bm, sc.word_list}, SinkBitsIdx{bm, sc.word_list, word_offsets, ids, id_mod, clear}, nwords_max,
-        sc.d_nlist, reinterpret_cast<uint64_t *>(partials), next_scan_epoch(), d_count);
+        sc.d_nlist, reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
     WC_LAUNCH_CHECK();
 }
 

@@ -79,10 +79,31 @@ __device__ __forceinline__ int64_t scan_count(int64_t n, const uint32_t *d_n) {
 // tiles, which the hardware dispatches first.  One launch per scan.
 constexpr uint32_t kFlagAggregate = 1, kFlagPrefix = 2;
 
+// Host-issued epochs have bit 29 set; epochs derived on the device (below)
+// have it clear, so the two never collide.
 inline uint32_t next_scan_epoch() {
     static std::atomic<uint32_t> e{0};
-    uint32_t v = (e.fetch_add(1) + 1) & 0x3FFFFFFFu;
-    return v ? v : next_scan_epoch();
+    return ((e.fetch_add(1) + 1) & 0x1FFFFFFFu) | 0x20000000u;
+}
+
+// A scan inside a captured (replayed) pass must get a new epoch at every
+// replay: it is then derived on the device from the frame counter and a
+// per-call salt, (frame << 12) + salt.  The session sets the thread-local
+// frame pointer and salt base while it enqueues a pass.
+struct ScanEpoch {
+    const uint32_t *d_frame;  // nullptr: `value` is the epoch
+    uint32_t value;
+};
+inline thread_local const uint32_t *t_epoch_frame = nullptr;
+inline thread_local uint32_t t_epoch_salt = 0;
+inline ScanEpoch scan_epoch() {
+    if (t_epoch_frame) return ScanEpoch{t_epoch_frame, (t_epoch_salt++) & 4095u};
+    return ScanEpoch{nullptr, next_scan_epoch()};
+}
+__device__ __forceinline__ uint32_t resolve_epoch(const ScanEpoch e) {
+    if (!e.d_frame) return e.value;
+    const uint32_t v = ((*e.d_frame << 12) + e.value) & 0x1FFFFFFFu;
+    return v ? v : 0x1FFFFFFFu;
 }
 
 // scratch words (uint32) a scan over n elements needs
@@ -112,11 +133,12 @@ struct SinkBits {  // word offsets + ascending ids of the set bits of bm
 
 template <class Load, class Sink>
 __global__ void __launch_bounds__(kScanThreads)
-    k_scan_onepass(Load ld, Sink sink, int64_t n_max, const uint32_t *d_n, uint64_t *status, uint32_t epoch,
+    k_scan_onepass(Load ld, Sink sink, int64_t n_max, const uint32_t *d_n, uint64_t *status, ScanEpoch ep,
                    uint32_t *d_total) {
     __shared__ uint32_t sw[32];
     __shared__ uint32_t tile[kScanTile];
     __shared__ uint32_t s_excl;
+    const uint32_t epoch = resolve_epoch(ep);
     const int64_t n = scan_count(n_max, d_n);
     const int64_t t = blockIdx.x;
     const int64_t base = t * kScanTile;
@@ -195,7 +217,7 @@ void scan_exclusive(Load ld, int64_t n, uint32_t *out, uint32_t *d_total, uint32
         return;
     }
     k_scan_onepass<Load, SinkStore><<<(unsigned)scan_tiles(n), kScanThreads, 0, st>>>(
-        ld, SinkStore{out}, n, nullptr, reinterpret_cast<uint64_t *>(scratch), next_scan_epoch(), d_total);
+        ld, SinkStore{out}, n, nullptr, reinterpret_cast<uint64_t *>(scratch), scan_epoch(), d_total);
     WC_LAUNCH_CHECK();
 }
 
@@ -208,7 +230,7 @@ void scan_exclusive_dev(Load ld, const uint32_t *d_n, int64_t n_max, uint32_t *o
         return;
     }
     k_scan_onepass<Load, SinkStore><<<(unsigned)scan_tiles(n_max), kScanThreads, 0, st>>>(
-        ld, SinkStore{out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), next_scan_epoch(), d_total);
+        ld, SinkStore{out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), scan_epoch(), d_total);
     WC_LAUNCH_CHECK();
 }
 

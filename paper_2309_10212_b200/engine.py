@@ -185,6 +185,11 @@ class RenderSession:
                   self._MAX_STATS, C.byref(k))
         return [_stats_from_c(buf[i]) for i in range(min(k.value, self._MAX_STATS))]
 
+    def set_graphs(self, on: bool) -> None:
+        """Replay passes as captured CUDA graphs (default) or launch them one
+        kernel at a time with per-stage timing (stage_ms)."""
+        _lib.call("wc_session_set_graphs", self._h, int(bool(on)))
+
     def render_frame_host(self, cam: Camera | None, iso: float):
         """render_frame + the framebuffer in (pinned) host memory, most of the
         copy overlapped with the frame's last passes.  -> (stats, rgba, depth)."""
