@@ -37,7 +37,7 @@ def unit_scale(u):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("csv")
-    ap.add_argument("--frames", type=int, default=4)
+    ap.add_argument("--frames", type=int, default=5)  # bench --steps 1 --warmup 1: warm-up, timed, staged, e2e x2
     a = ap.parse_args()
     rows = list(csv.reader(open(a.csv)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
