@@ -263,7 +263,28 @@ struct Dda {
 
 // One step; ties step x, then y, then z (traversal.py:303-314, :333-344).
 // Returns the crossing parameter of the face just crossed.
+// Branch-free form (predicated selects): lanes walking different rays (or
+// the same ray different steps ahead) take different axes, and a branchy
+// step would serialise the three paths across the warp.  The adds of the
+// axes not taken are computed and discarded, so every value is unchanged.
+#ifndef WC_DDA_BRANCHFREE
+#define WC_DDA_BRANCHFREE 1
+#endif
 __device__ __forceinline__ double dda_step(Dda &s, int sx, int sy, int sz, double dlx, double dly, double dlz) {
+#if WC_DDA_BRANCHFREE
+    const bool mx = s.tx <= s.ty && s.tx <= s.tz;
+    const bool my = !mx && s.ty <= s.tz;
+    const bool mz = !mx && !my;
+    const double t = mx ? s.tx : (my ? s.ty : s.tz);
+    const double nx = s.tx + dlx, ny = s.ty + dly, nz = s.tz + dlz;
+    s.cx += mx ? sx : 0;
+    s.cy += my ? sy : 0;
+    s.cz += mz ? sz : 0;
+    s.tx = mx ? nx : s.tx;
+    s.ty = my ? ny : s.ty;
+    s.tz = mz ? nz : s.tz;
+    return t;
+#else
     double t;
     if (s.tx <= s.ty && s.tx <= s.tz) {
         t = s.tx;
@@ -279,6 +300,7 @@ __device__ __forceinline__ double dda_step(Dda &s, int sx, int sy, int sz, doubl
         s.tz += dlz;
     }
     return t;
+#endif
 }
 
 constexpr int kFineRun = 10;  // a monotone ray visits at most 4+4+4-2 fine cells of one coarse cell
