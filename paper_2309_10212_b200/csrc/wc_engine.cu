@@ -836,7 +836,8 @@ __global__ void k_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvi
 // among visible ids (bitmap rank), value = k.
 __global__ void k_build_entries(const uint32_t *ctl, const uint32_t *act_list, const uint32_t *emitted,
                                 const uint32_t *entry_off, const uint32_t *block_slots, const uint32_t *vis_bm,
-                                const uint32_t *vis_word_off, uint32_t *ent_key, uint32_t *ent_val, uint32_t *ent_ray) {
+                                const uint32_t *vis_word_off, uint32_t *ent_key, uint32_t *ent_val, uint32_t *ent_ray,
+                                uint32_t *ent_blk) {
     // thread per slot (i, j): no per-ray serial chain of rank lookups
     const int64_t n_act = ctl[C_NACT], n_spec = ctl[C_NSPEC];
     const int64_t n_slots = n_act * n_spec;
@@ -850,6 +851,7 @@ __global__ void k_build_entries(const uint32_t *ctl, const uint32_t *act_list, c
         ent_key[eo] = vis_word_off[w] + __popc(vis_bm[w] & ((1u << (b & 31)) - 1u));
         ent_val[eo] = eo;
         ent_ray[eo] = act_list[i];
+        ent_blk[eo] = b;
     }
 }
 
@@ -1094,7 +1096,8 @@ __global__ void k_contrib(const uint32_t *visible_ids, const uint32_t *d_nvis, c
 }
 
 struct RaytraceArgs {
-    const uint32_t *visible_ids, *ent_key, *ent_val, *ent_ray;
+    const uint32_t *visible_ids, *ent_key, *ent_val, *ent_ray, *ent_blk;
+    bool identity;  // entries in their build order (not grouped): entry k at position k
     int64_t n_ent;
     const int4 *contrib;
     const float *slot_values;
@@ -1161,10 +1164,12 @@ struct EntryCtx {  // everything an entry's trace needs, rebuilt from its positi
 
 __device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, const RayView &rv, int64_t j) {
     EntryCtx e;
+    // ungrouped entries sit at their own index: ray and block load in the
+    // same round trip as the visible rank
     const uint32_t v = a.ent_key[j];
-    e.k = a.ent_val[j];
+    e.k = a.identity ? (uint32_t)j : a.ent_val[j];
     e.r = a.ent_ray[e.k];
-    const uint32_t b = a.visible_ids[v];
+    const uint32_t b = a.ent_blk[e.k];
     e.bx = (int)(b % (uint32_t)a.bdx);
     e.by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy);
     e.bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
@@ -1278,7 +1283,7 @@ __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
     rv.bind();
     const int64_t n_ent = *a.d_n_ent;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_ent; j += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t k = a.ent_val[j];
+        const uint32_t k = a.identity ? (uint32_t)j : a.ent_val[j];
         const uint32_t bst = s.best[k];
         if (bst == WC_UINT_MAX) {
             a.rgbz[k] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
@@ -1600,6 +1605,7 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     ent_key.alloc(n);
     ent_val.alloc(n);
     ent_ray.alloc(n);
+    ent_blk.alloc(n);
     rgbz.alloc(n);
     visible_ids.alloc(n);
     block_ray_off.alloc(n + 1);
@@ -1937,7 +1943,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     bitmap_extract_dev(act_bm.p, ctl + C_NWORDS_ON, nwords, vis_word_off.p + nwords, active_ids.p, ctl + C_NACTB,
                        partials.p, st);
     k_build_entries<<<grid_for(n, 256), 256, 0, st>>>(ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p,
-                                                      vis_word_off.p, ent_key.p, ent_val.p, ent_ray.p);
+                                                      vis_word_off.p, ent_key.p, ent_val.p, ent_ray.p, ent_blk.p);
     WC_LAUNCH_CHECK();
     WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
     WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
@@ -2018,6 +2024,8 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     ra.ent_key = ent_key.p;
     ra.ent_val = ent_val.p;
     ra.ent_ray = ent_ray.p;
+    ra.ent_blk = ent_blk.p;
+    ra.identity = !group_entries;
     ra.d_n_ent = ctl + C_NENT;
     ra.contrib = contrib.p;
     ra.slot_values = slot_values.p;

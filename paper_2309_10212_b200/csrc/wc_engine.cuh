@@ -94,7 +94,7 @@ struct Session {
     DevBuf<uint32_t> coarse_cell, fine_cell;
     DevBuf<uint32_t> act_list[2], keep, keep_off, emitted, entry_off;
     DevBuf<uint32_t> block_slots, ray_slots;
-    DevBuf<uint32_t> ent_key, ent_val, ent_ray;
+    DevBuf<uint32_t> ent_key, ent_val, ent_ray, ent_blk;
     DevBuf<float4> rgbz;
     DevBuf<int4> contrib;  // 8 contributor slots per visible block
     DevBuf<uint4> item_info;  // two-phase raytrace work list (SplitArgs)
