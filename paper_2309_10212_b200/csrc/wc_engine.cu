@@ -191,12 +191,6 @@ __global__ void k_compact_keep(const uint32_t *keep, const uint32_t *off, const 
         if (keep[i]) out[off[i]] = in[i];
 }
 
-__global__ void k_compact_miss(PredMiss pred, const uint32_t *d_n, int64_t n_max, const uint32_t *off, uint32_t *out) {
-    const int64_t n = min(n_max, (int64_t)*d_n);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        if (pred(i)) out[off[i]] = pred.ids[i];
-}
-
 // --------------------------------------------------------------- traverse
 
 struct RayView {
@@ -1620,7 +1614,6 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
     WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
     active_ids.alloc(std::min<int64_t>(8 * n, vol->n_blocks) + 1);
-    miss_off.alloc(active_ids.n);
     miss_ids.alloc(active_ids.n);
     counters.alloc(C_COUNT + kHistBins);
     WC_CUDA(cudaMemsetAsync(counters.p, 0, 4 * C_COUNT, st));
@@ -1960,10 +1953,9 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
                                                                                stamp, ctl + C_COUNT);
         WC_LAUNCH_CHECK();
     }
-    PredMiss pm{active_ids.p, slot_of_block.p};
-    scan_exclusive_dev(pm, ctl + C_NACTB, nmax, miss_off.p, ctl + C_NMISS, partials.p, st);
-    k_compact_miss<<<grid_for(nmax, 256), 256, 0, st>>>(pm, ctl + C_NACTB, nmax, miss_off.p, miss_ids.p);
-    WC_LAUNCH_CHECK();
+    // misses in ascending id order (cache.py:76-78), scan and compaction in one pass
+    compact_dev(PredMiss{active_ids.p, slot_of_block.p}, active_ids.p, ctl + C_NACTB, nmax, miss_ids.p,
+                ctl + C_NMISS, partials.p, st);
     mark(2);
     if (p >= 1 && !hist) {  // > kHistBins passes: histogram over all stamps through the host (rare)
         read_counters(0, C_COUNT);

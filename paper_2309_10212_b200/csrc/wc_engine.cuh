@@ -113,7 +113,7 @@ struct Session {
     int32_t pass_no = 0;
     DevBuf<float> slot_values;
     DevBuf<int32_t> block_of_slot, last_used, slot_of_block;
-    DevBuf<uint32_t> miss_off, miss_ids, cand_key, cand_val;
+    DevBuf<uint32_t> miss_ids, cand_key, cand_val;
     // scratch
     DevBuf<uint32_t> counters, partials;
     PinnedBuf<uint32_t> h_counters;

@@ -131,6 +131,17 @@ struct SinkBits {  // word offsets + ascending ids of the set bits of bm
     }
 };
 
+// exclusive-scan consumer that compacts the ids whose predicate holds
+template <class Pred>
+struct SinkCompact {
+    Pred pred;
+    const uint32_t *ids;
+    uint32_t *out;
+    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const {
+        if (pred(i)) out[prefix] = ids[i];
+    }
+};
+
 template <class Load, class Sink>
 __global__ void __launch_bounds__(kScanThreads)
     k_scan_onepass(Load ld, Sink sink, int64_t n_max, const uint32_t *d_n, uint64_t *status, ScanEpoch ep,
@@ -231,6 +242,21 @@ void scan_exclusive_dev(Load ld, const uint32_t *d_n, int64_t n_max, uint32_t *o
     }
     k_scan_onepass<Load, SinkStore><<<(unsigned)scan_tiles(n_max), kScanThreads, 0, st>>>(
         ld, SinkStore{out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), scan_epoch(), d_total);
+    WC_LAUNCH_CHECK();
+}
+
+// Stable compaction of ids[i] for pred(i), i < *d_n (<= n_max), in one
+// pass: out[...] in input order, count -> *d_total.
+template <class Pred>
+void compact_dev(Pred pred, const uint32_t *ids, const uint32_t *d_n, int64_t n_max, uint32_t *out,
+                 uint32_t *d_total, uint32_t *scratch, cudaStream_t st) {
+    if (n_max <= 0) {
+        WC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
+        return;
+    }
+    k_scan_onepass<Pred, SinkCompact<Pred>><<<(unsigned)scan_tiles(n_max), kScanThreads, 0, st>>>(
+        pred, SinkCompact<Pred>{pred, ids, out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), scan_epoch(),
+        d_total);
     WC_LAUNCH_CHECK();
 }
 
