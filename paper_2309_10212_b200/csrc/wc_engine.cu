@@ -184,13 +184,6 @@ __global__ void k_compact_index(Pred pred, int64_t n, const uint32_t *off, uint3
         if (pred(i)) out[off[i]] = (uint32_t)i;
 }
 
-__global__ void k_compact_keep(const uint32_t *keep, const uint32_t *off, const uint32_t *in, const uint32_t *d_n,
-                               uint32_t *out) {
-    const int64_t n = *d_n;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        if (keep[i]) out[off[i]] = in[i];
-}
-
 // --------------------------------------------------------------- traverse
 
 struct RayView {
@@ -1591,7 +1584,6 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     act_list[0].alloc(n);
     act_list[1].alloc(n);
     keep.alloc(n);
-    keep_off.alloc(n);
     emitted.alloc(n);
     entry_off.alloc(n);
     block_slots.alloc(n);
@@ -2058,9 +2050,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
         k_composite<<<grid_for(n, 256), 256, 0, st>>>(ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p, status.p,
                                                       rgba.p, depth.p, keep.p);
     WC_LAUNCH_CHECK();
-    scan_exclusive_dev(LoadU32{keep.p}, ctl + C_NACT, n, keep_off.p, ctl + C_NACT_NEXT, partials.p, st);
-    k_compact_keep<<<grid_for(n, 256), 256, 0, st>>>(keep.p, keep_off.p, alist, ctl + C_NACT, act_list[(p + 1) & 1].p);
-    WC_LAUNCH_CHECK();
+    compact_dev(LoadU32{keep.p}, alist, ctl + C_NACT, n, act_list[(p + 1) & 1].p, ctl + C_NACT_NEXT, partials.p, st);
     k_pass_end<<<1, 1, 0, st>>>(ctl, plog.p + std::min<int64_t>(p, kMaxPassLog - 1) * L_COUNT, n, speculation,
                                 max_spec, nwords);
     WC_LAUNCH_CHECK();

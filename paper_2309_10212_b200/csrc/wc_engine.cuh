@@ -92,7 +92,7 @@ struct Session {
     DevBuf<double> origin, dir, t_enter, t_exit, coarse_tmax, fine_tmax;
     DevBuf<uint8_t> status, exited;
     DevBuf<uint32_t> coarse_cell, fine_cell;
-    DevBuf<uint32_t> act_list[2], keep, keep_off, emitted, entry_off;
+    DevBuf<uint32_t> act_list[2], keep, emitted, entry_off;
     DevBuf<uint32_t> block_slots, ray_slots;
     DevBuf<uint32_t> ent_key, ent_val, ent_ray, ent_blk;
     DevBuf<float4> rgbz;
