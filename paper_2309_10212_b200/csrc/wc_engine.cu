@@ -34,6 +34,9 @@
 #ifndef WC_EARLY_HIST
 #define WC_EARLY_HIST 1
 #endif
+#ifndef WC_SPARSE_VISACT
+#define WC_SPARSE_VISACT 0
+#endif
 #ifndef WC_RAYTRACE_MIN_CTAS
 #define WC_RAYTRACE_MIN_CTAS 6
 #endif
@@ -1920,18 +1923,30 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     // entry compaction: exclusive scan of per-ray emitted counts
     scan_exclusive_dev(LoadU32{emitted.p}, ctl + C_NACT, n, entry_off.p, ctl + C_NENT, partials.p, st);
     // visible ids (ascending) + active marking
-    bitmap_extract_dev(vis_bm.p, ctl + C_NWORDS_ON, nwords, vis_word_off.p, visible_ids.p, ctl + C_NVIS, partials.p,
-                       st);
+    // few rays per block (e.g. one rank's share of a multi-GPU frame): the
+    // two-level extraction, whose cost follows the non-zero words
+    const bool sparse = WC_SPARSE_VISACT || n * 100 < vol->n_blocks;
+    const SparseScratch vsc{sp_summary.p, sp_words.p, ctl + C_NLIST};
+    if (sparse)
+        bitmap_extract_sparse(vis_bm.p, ctl + C_NWORDS_ON, nwords, nwords, vis_word_off.p, visible_ids.p,
+                              ctl + C_NVIS, false, vsc, partials.p, st);
+    else
+        bitmap_extract_dev(vis_bm.p, ctl + C_NWORDS_ON, nwords, vis_word_off.p, visible_ids.p, ctl + C_NVIS,
+                           partials.p, st);
     k_mark_active<<<grid_for((int64_t)8 * n, 256), 256, 0, st>>>(visible_ids.p, ctl + C_NVIS, vol->bdx, vol->bdy,
                                                                  vol->bdz, act_bm.p);
     WC_LAUNCH_CHECK();
-    bitmap_extract_dev(act_bm.p, ctl + C_NWORDS_ON, nwords, vis_word_off.p + nwords, active_ids.p, ctl + C_NACTB,
-                       partials.p, st);
+    if (sparse)
+        bitmap_extract_sparse(act_bm.p, ctl + C_NWORDS_ON, nwords, nwords, nullptr, active_ids.p, ctl + C_NACTB, true,
+                              vsc, partials.p, st);  // clears act_bm
+    else
+        bitmap_extract_dev(act_bm.p, ctl + C_NWORDS_ON, nwords, vis_word_off.p + nwords, active_ids.p, ctl + C_NACTB,
+                           partials.p, st);
     k_build_entries<<<grid_for(n, 256), 256, 0, st>>>(ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p,
                                                       vis_word_off.p, ent_key.p, ent_val.p, ent_ray.p, ent_blk.p);
     WC_LAUNCH_CHECK();
     WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
-    WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
+    if (!sparse) WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
 
     // cache.ensure_resident (cache.py:66-111): stamp hits, list misses
     // (ascending), then growth / victims / decode, all sized on the device

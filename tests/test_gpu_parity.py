@@ -90,6 +90,8 @@ SCENES = [
     ("value_noise", 64, 4, 100, 100, 0.5, 0.1, True, 8, None),
     ("gaussians", 96, 16, 160, 90, 0.3, 0.0, True, 64, None),
     ("turbulence", (72, 64, 60), 16, 128, 72, 0.5, 0.3, True, 64, 1024),
+    ("value_noise", 128, 12, 12, 12, 0.5, 0.2, True, 64, None),        # few rays per block: sparse extraction
+    ("value_noise", 112, 10, 14, 11, 0.45, 0.6, False, 64, 40),         # ... with eviction
 ]
 
 
