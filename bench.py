@@ -258,8 +258,8 @@ def run_b200(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    def frame():
-        return sess.render_frame(cam, iso)
+    def frame():  # multi-GPU: the per-iso range tests are split across the ranks and all-gathered
+        return wdist.render_frame_split(sess, cam, iso) if sharded else sess.render_frame(cam, iso)
 
     for _ in range(args.warmup):
         flush.zero_()

@@ -128,6 +128,15 @@ int wc_session_set_base_color(wc_session *s, double r, double g, double b);
  * the raytrace is correct either way (same pixels); grouping yields the
  * reference's PassBuffers layout (required by wc_session_rt_inputs). */
 int wc_session_set_grouping(wc_session *s, int group_entries);
+/* Tile-split frames: reset computing the per-iso range
+ * tests (coarse bitmap words, 64-bit fine masks) only for coarse-cell slice
+ * `part` of `parts`; the caller all-gathers the slices (each `chunk_words`
+ * bitmap words = 32 x chunk_words masks, at offset part x chunk) into the
+ * buffers wc_session_mask_buffers returns, then runs the passes
+ * (wc_session_run).  wc_session_sync waits for the session's stream. */
+int wc_session_reset_part(wc_session *s, const wc_camera *cam, double iso, int64_t part, int64_t parts);
+int wc_session_mask_buffers(wc_session *s, int64_t parts, void **coarse_bm, void **cell_mask, int64_t *chunk_words);
+int wc_session_sync(wc_session *s);
 /* Replay passes as captured CUDA graphs (default on; WAVECAST_NO_GRAPHS=1 in
  * the environment turns it off).  Off = plain launches with per-stage
  * timing (wc_session_stage_ms); on = the pass timed as a whole. */

@@ -94,6 +94,9 @@ _SIGS = {
     "wc_session_create": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp, _dbl, _i32, _i32, _i64, _i32, _vp]),
     "wc_session_set_base_color": (_i32, [_vp, _dbl, _dbl, _dbl]),
     "wc_session_set_grouping": (_i32, [_vp, _i32]),
+    "wc_session_reset_part": (_i32, [_vp, _vp, _dbl, _i64, _i64]),
+    "wc_session_mask_buffers": (_i32, [_vp, _i64, _vp, _vp, _vp]),
+    "wc_session_sync": (_i32, [_vp]),
     "wc_session_set_graphs": (_i32, [_vp, _i32]),
     "wc_session_pass": (_i32, [_vp, _vp, _vp]),
     "wc_session_run": (_i32, [_vp, _vp, _i64, _vp]),

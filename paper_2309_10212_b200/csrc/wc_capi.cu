@@ -540,6 +540,30 @@ int wc_session_reset(wc_session *s, const wc_camera *cam, double iso) {
     WC_API_END
 }
 
+int wc_session_reset_part(wc_session *s, const wc_camera *cam, double iso, int64_t part, int64_t parts) {
+    WC_API_BEGIN
+    WC_REQUIRE(parts >= 1 && part >= 0 && part < parts, wc::UsageError, "part out of range");
+    s->s->reset_part(reinterpret_cast<const wc::CameraParams *>(cam), iso, part, parts);
+    WC_API_END
+}
+
+int wc_session_mask_buffers(wc_session *s, int64_t parts, void **coarse_bm, void **cell_mask, int64_t *chunk_words) {
+    WC_API_BEGIN
+    WC_REQUIRE(parts >= 1, wc::UsageError, "parts must be positive");
+    int64_t chunk = 0;
+    s->s->mask_buffers(parts, chunk);
+    if (coarse_bm) *coarse_bm = s->s->coarse_bm.p;
+    if (cell_mask) *cell_mask = s->s->cell_mask.p;
+    if (chunk_words) *chunk_words = chunk;
+    WC_API_END
+}
+
+int wc_session_sync(wc_session *s) {
+    WC_API_BEGIN
+    WC_CUDA(cudaStreamSynchronize(s->s->st));
+    WC_API_END
+}
+
 int wc_session_frame_ms(wc_session *s, double *ms) {
     WC_API_BEGIN
     *ms = s->s->frame_ms();

@@ -719,10 +719,11 @@ __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a_in) {
 // float64 exactly as traversal.py:297 (:357) does.  The 15.7 MB fine bitmap
 // (8.05B voxels) stays in L2, so each DDA step of the traversal's dependent
 // chain costs an L2 hit instead of a DRAM read of the 2 GB float64 grid.
-__global__ void k_iso_bitmap(const double2 *__restrict__ mm, int64_t n, double iso, uint32_t *__restrict__ bm) {
+__global__ void k_iso_bitmap(const double2 *__restrict__ mm, int64_t n, double iso, uint32_t *__restrict__ bm,
+                             int64_t w_begin, int64_t w_end) {
     const int lane = threadIdx.x & 31;
-    const int64_t nwords = (n + 31) >> 5;
-    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords;
+    const int64_t nwords = min((n + 31) >> 5, w_end);
+    for (int64_t w = w_begin + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w < nwords;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t c = w * 32 + lane;
         bool in = false;
@@ -755,18 +756,18 @@ __device__ __forceinline__ bool iso_in_q(const ushort2 v, uint32_t qi, const dou
 __global__ void k_iso_cell_mask(const ushort2 *__restrict__ q, const double2 *__restrict__ mm,
                                 const uint32_t *__restrict__ coarse_bm, int fdx, int fdy, int fdz, int cdx, int cdy,
                                 int cdz, double iso, double base, double inv,
-                                unsigned long long *__restrict__ cell_mask) {
+                                unsigned long long *__restrict__ cell_mask, int64_t c_begin, int64_t c_end) {
     // Streams the bricked screening copy: 16 lanes cover one coarse cell's
     // 256 B (lane: 4 fine cells = one x-row), 4 cells per lane in flight; the
     // 16 nibbles of a cell are OR-ed with shuffles.
     constexpr int kU = 4;
-    const int64_t n_coarse = (int64_t)cdx * cdy * cdz;
+    const int64_t n_coarse = min((int64_t)cdx * cdy * cdz, c_end);  // cells [c_begin, c_end): c_begin % 8 == 0
     const bool iso_nan = iso != iso;
     const uint32_t qi = iso_nan ? 0u : range_q(iso, base, inv);
     const int lane = threadIdx.x & 31, half = lane >> 4, row = lane & 15;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t c0 = w0 * 2 * kU; c0 < n_coarse; c0 += nw * 2 * kU) {
+    for (int64_t c0 = c_begin + w0 * 2 * kU; c0 < n_coarse; c0 += nw * 2 * kU) {
         uint4 w[kU];
         bool on[kU];
 #pragma unroll
@@ -1603,8 +1604,8 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     const int64_t nwords = ceil_div(vol->n_blocks, 32);
     vis_bm.alloc(nwords);
     act_bm.alloc(nwords);
-    cell_mask.alloc(vol->n_coarse);
-    coarse_bm.alloc(ceil_div(vol->n_coarse, 32));
+    int64_t chunk0;
+    mask_buffers(1, chunk0);
     vis_word_off.alloc(2 * nwords);  // visible word offsets + the active extraction's (unused) offsets
     WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
     WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
@@ -1649,7 +1650,32 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
 // A new frame on the same allocations: fresh rays for (cam, iso), a blank
 // framebuffer and an empty cache of the initial logical capacity (the
 // reference builds a new RaySoA / BlockCache per render, engine.py:316-320).
-void Session::reset(const CameraParams *cam, double iso_) {
+// Coarse-cell words [w0, w1) of part `part` of `parts` (32 cells per word),
+// and the per-part chunk the mask buffers are padded to.
+static void mask_part(int64_t n_coarse, int64_t part, int64_t parts, int64_t &w0, int64_t &w1, int64_t &chunk) {
+    const int64_t nw = ceil_div(n_coarse, 32);
+    chunk = ceil_div(nw, std::max<int64_t>(1, parts));
+    w0 = std::min<int64_t>(nw, part * chunk);
+    w1 = std::min<int64_t>(nw, w0 + chunk);
+}
+
+void Session::mask_buffers(int64_t parts, int64_t &chunk_words) {
+    int64_t w0, w1;
+    mask_part(vol->n_coarse, 0, parts, w0, w1, chunk_words);
+    const int64_t words = std::max<int64_t>(parts * chunk_words, ceil_div(vol->n_coarse, 32));
+    if (coarse_bm.n < words || cell_mask.n < 32 * words) {
+        coarse_bm.alloc(words);
+        cell_mask.alloc(32 * words);
+        drop_graphs();  // they read the old buffers
+    }
+}
+
+void Session::reset(const CameraParams *cam, double iso_) { reset_part(cam, iso_, 0, 1); }
+
+// reset for part `part` of `parts`: the per-iso range tests are computed for
+// that slice of coarse cells only; the caller assembles the others (an
+// all-gather across the ranks of a tile split) before running the passes.
+void Session::reset_part(const CameraParams *cam, double iso_, int64_t part, int64_t parts) {
     iso = iso_;
     if (cam) {
         cam_params = *cam;
@@ -1658,12 +1684,19 @@ void Session::reset(const CameraParams *cam, double iso_) {
         eye[2] = cam->eye[2];
     }
     WC_CUDA(cudaEventRecord(ev_frame0, st));
-    k_iso_bitmap<<<grid_for(vol->n_coarse, 256, 8), 256, 0, st>>>(vol->coarse_mm.p, vol->n_coarse, iso, coarse_bm.p);
-    WC_LAUNCH_CHECK();
-    k_iso_cell_mask<<<grid_for(vol->n_coarse * 16, 256, 8), 256, 0, st>>>(
-        vol->fine_q.p, vol->fine_mm.p, coarse_bm.p, vol->bdx, vol->bdy, vol->bdz, vol->cdx, vol->cdy, vol->cdz, iso,
-        vol->q_base, vol->q_inv, cell_mask.p);
-    WC_LAUNCH_CHECK();
+    int64_t w0, w1, chunk;
+    mask_buffers(parts, chunk);
+    mask_part(vol->n_coarse, part, parts, w0, w1, chunk);
+    const int64_t c_end = std::min<int64_t>(vol->n_coarse, 32 * w1);
+    if (w1 > w0) {
+        k_iso_bitmap<<<grid_for((w1 - w0) * 32, 256, 8), 256, 0, st>>>(vol->coarse_mm.p, vol->n_coarse, iso,
+                                                                      coarse_bm.p, w0, w1);
+        WC_LAUNCH_CHECK();
+        k_iso_cell_mask<<<grid_for((c_end - 32 * w0) * 16, 256, 8), 256, 0, st>>>(
+            vol->fine_q.p, vol->fine_mm.p, coarse_bm.p, vol->bdx, vol->bdy, vol->bdz, vol->cdx, vol->cdy, vol->cdz,
+            iso, vol->q_base, vol->q_inv, cell_mask.p, 32 * w0, c_end);
+        WC_LAUNCH_CHECK();
+    }
     RayInitArgs a{};
     a.cam = cam_params;
     a.pixel_ids = pix.p;

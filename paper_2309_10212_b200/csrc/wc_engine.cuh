@@ -157,6 +157,8 @@ struct Session {
     int64_t render_to_host(const CameraParams *cam, double iso, PassStatsC *out, int64_t max_out,
                            uint32_t *rgba_host, float *depth_host);
     void reset(const CameraParams *cam, double iso);
+    void reset_part(const CameraParams *cam, double iso, int64_t part, int64_t parts);
+    void mask_buffers(int64_t parts, int64_t &chunk_words);  // sized for `parts` slices of chunk_words
     float frame_ms();  // device time from the last reset to the end of the last pass
     void download_framebuffer(uint8_t *rgba_host, float *depth_host);
     void copy_framebuffer_device(void *rgba_dst, void *depth_dst);

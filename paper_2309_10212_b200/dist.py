@@ -101,6 +101,31 @@ def gather_tiles(rgba_local, depth_local, w: int, h: int, tile: int = 32, group=
     return rgba_np, depth_np
 
 
+def render_frame_split(sess, cam, iso, group=None):
+    """One frame of a rank's tile session with the per-iso range tests split
+    across the ranks (the exchange step of a multi-GPU frame besides the tile
+    gather): each rank computes its slice of coarse cells (coarse bitmap
+    words and 64-bit fine masks) during reset, one all-gather per buffer over
+    NCCL assembles them in place, then the passes run.  Returns the stats."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if world == 1:
+        return sess.render_frame(cam, iso)
+    rank = dist.get_rank(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sess.reset_part(cam, iso, rank, world)
+    cb, cm, chunk = sess.mask_buffers(world)
+    bits = torch.as_tensor(_DeviceBytes(cb, 4 * chunk * world), device=dev)
+    masks = torch.as_tensor(_DeviceBytes(cm, 8 * 32 * chunk * world), device=dev)
+    sess.sync()  # the slice is written (session stream) before NCCL reads it
+    for buf, per in ((bits, 4 * chunk), (masks, 8 * 32 * chunk)):
+        dist.all_gather_into_tensor(buf, buf[rank * per:(rank + 1) * per], group=group)
+    torch.cuda.current_stream(dev).synchronize()  # gathered before the passes read them
+    return sess.run()
+
+
 _SHARD_SESSIONS: dict = {}
 
 
@@ -134,7 +159,7 @@ def render_sharded(cv, grids, cam, iso, opts, tile: int = 32, group=None):
     depth_t = torch.empty(n, dtype=torch.float32, device=dev)
     stats = []
     if n:
-        stats = s.render_frame(cam, iso)
+        stats = render_frame_split(s, cam, iso, group)
         _lib.call("wc_session_framebuffer_device", s.handle, rgba_t.data_ptr(), depth_t.data_ptr())
     out = gather_tiles(rgba_t, depth_t, opts.width, opts.height, tile, group)
     if out is None:

@@ -185,6 +185,22 @@ class RenderSession:
                   self._MAX_STATS, C.byref(k))
         return [_stats_from_c(buf[i]) for i in range(min(k.value, self._MAX_STATS))]
 
+    def reset_part(self, cam: Camera | None, iso: float, part: int, parts: int) -> None:
+        """reset with the per-iso range tests computed for coarse-cell slice
+        `part` of `parts` only (dist.render_frame_split gathers the rest)."""
+        cam_c = cam.to_c(self.w, self.h) if cam is not None else None
+        _lib.call("wc_session_reset_part", self._h, None if cam_c is None else C.byref(cam_c), float(iso), int(part),
+                  int(parts))
+
+    def mask_buffers(self, parts: int):
+        """(coarse bitmap ptr, fine mask ptr, words per part) of the range-test buffers."""
+        cb, cm, ch = C.c_void_p(), C.c_void_p(), C.c_int64()
+        _lib.call("wc_session_mask_buffers", self._h, int(parts), C.byref(cb), C.byref(cm), C.byref(ch))
+        return cb.value, cm.value, ch.value
+
+    def sync(self) -> None:
+        _lib.call("wc_session_sync", self._h)
+
     def set_graphs(self, on: bool) -> None:
         """Replay passes as captured CUDA graphs (default) or launch them one
         kernel at a time with per-stage timing (stage_ms)."""

@@ -362,3 +362,42 @@ def test_repeated_renders_with_overlapped_readback(wc):
             last = snap
         assert np.array_equal(fb.rgba, last.rgba) and np.array_equal(fb.depth, last.depth), k
         assert len(stats) >= 2
+
+
+def test_split_range_tests_assemble_to_the_whole(wc):
+    # dist.render_frame_split on one GPU: the per-iso range tests computed in
+    # 3 coarse-cell slices (wc_session_reset_part), assembled as the NCCL
+    # all-gather would, give the same frame as the whole reset
+    import torch
+
+    from paper_2309_10212_b200 import dist
+
+    vol = host_volume("value_noise", (96, 80, 72), seed=6)
+    cv = wc.compress_volume(vol, 16)
+    grids = wc.build_grids(cv)
+    eye, look, up, fov = orbit(cv.dims, 0.15)
+    cam = wc.Camera(tuple(eye), tuple(look), tuple(up), fov)
+    iso = iso_at(vol, 0.5)
+    opts = wc.RenderOptions(width=72, height=64)
+    s = wc.RenderSession(cv, grids, cam, iso, opts)
+    ref = s.render_frame(cam, iso)
+    rgba0, depth0 = (x.copy() for x in s.read())
+    parts = 3
+    cb, cm, chunk = s.mask_buffers(parts)
+    bits = torch.as_tensor(dist._DeviceBytes(cb, 4 * chunk * parts), device="cuda")
+    masks = torch.as_tensor(dist._DeviceBytes(cm, 8 * 32 * chunk * parts), device="cuda")
+    acc_b, acc_m = torch.zeros_like(bits), torch.zeros_like(masks)
+    for part in range(parts):
+        s.reset_part(cam, iso, part, parts)
+        s.sync()
+        pb, pm = 4 * chunk, 8 * 32 * chunk
+        acc_b[part * pb:(part + 1) * pb] = bits[part * pb:(part + 1) * pb]
+        acc_m[part * pm:(part + 1) * pm] = masks[part * pm:(part + 1) * pm]
+    bits.copy_(acc_b)
+    masks.copy_(acc_m)
+    torch.cuda.synchronize()
+    stats = s.run()
+    rgba1, depth1 = s.read()
+    assert [x.n_active_before for x in stats] == [x.n_active_before for x in ref]
+    assert np.array_equal(rgba0, rgba1) and np.array_equal(depth0, depth1)
+    s.close()
