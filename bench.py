@@ -259,7 +259,12 @@ def run_b200(args):
         torch.cuda.synchronize()
 
     def frame():  # multi-GPU: the per-iso range tests are split across the ranks and all-gathered
-        return wdist.render_frame_split(sess, cam, iso) if sharded else sess.render_frame(cam, iso)
+        if sharded:
+            return wdist.render_frame_split(sess, cam, iso)
+        if args.rank_share > 1:  # rank 0's share incl. its slice of the range tests (the all-gather not timed)
+            sess.reset_part(cam, iso, 0, args.rank_share)
+            return sess.run()
+        return sess.render_frame(cam, iso)
 
     for _ in range(args.warmup):
         flush.zero_()
