@@ -34,9 +34,6 @@
 #ifndef WC_EARLY_HIST
 #define WC_EARLY_HIST 1
 #endif
-#ifndef WC_SPARSE_VISACT
-#define WC_SPARSE_VISACT 0
-#endif
 #ifndef WC_RAYTRACE_MIN_CTAS
 #define WC_RAYTRACE_MIN_CTAS 6
 #endif
@@ -822,6 +819,35 @@ __global__ void k_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvi
     }
 }
 
+// Same marking a word at a time when rows are whole words (bdx % 32 == 0):
+// the first visible id of each non-zero visible word v activates
+// v | v << 1 in its own word, the bit shifted out into the next word of the
+// row, and both again one row (+y) and one plane (+z) further on, where those
+// neighbours exist.  Up to 8 word ORs per visible word instead of 8 bit ORs
+// per visible block.
+__global__ void k_mark_active_words(const uint32_t *visible_ids, const uint32_t *d_nvis, const uint32_t *vis_bm,
+                                    int wx_words, int bdy, int bdz, uint32_t *act_bm) {
+    const int64_t nvis = *d_nvis;
+    const uint32_t plane = (uint32_t)wx_words * (uint32_t)bdy;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvis; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t w = visible_ids[i] >> 5;
+        if (i > 0 && (visible_ids[i - 1] >> 5) == w) continue;  // ids ascend: one thread per word
+        const uint32_t v = vis_bm[w];
+        const uint32_t row = w / (uint32_t)wx_words;
+        const uint32_t wx = w - row * (uint32_t)wx_words;
+        const uint32_t by = row % (uint32_t)bdy, bz = row / (uint32_t)bdy;
+        const uint32_t a = v | (v << 1);                               // +x inside the word
+        const uint32_t b = wx + 1 < (uint32_t)wx_words ? v >> 31 : 0u;  // +x into the next word
+        const int ny = by + 1 < (uint32_t)bdy ? 2 : 1, nz = bz + 1 < (uint32_t)bdz ? 2 : 1;
+        for (int oz = 0; oz < nz; oz++)
+            for (int oy = 0; oy < ny; oy++) {
+                const uint32_t t = w + oy * (uint32_t)wx_words + oz * plane;
+                atomicOr(&act_bm[t], a);
+                if (b) atomicOr(&act_bm[t + 1], b);
+            }
+    }
+}
+
 // Entries of active ray i: k = entry_off[i] + j for its j-th emitted slot
 // (== valid_prefix of the slot, engine.py:124-128).  Key = rank of the block
 // among visible ids (bitmap rank), value = k.
@@ -833,8 +859,8 @@ __global__ void k_build_entries(const uint32_t *ctl, const uint32_t *act_list, c
     const int64_t n_act = ctl[C_NACT], n_spec = ctl[C_NSPEC];
     const int64_t n_slots = n_act * n_spec;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_slots; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = t / n_spec;
-        const uint32_t j = (uint32_t)(t - i * n_spec);
+        const uint32_t i = (uint32_t)t / (uint32_t)n_spec;  // slots <= rays < 2^32
+        const uint32_t j = (uint32_t)t - i * (uint32_t)n_spec;
         if (j >= emitted[i]) continue;
         const uint32_t eo = entry_off[i] + j;
         const uint32_t b = block_slots[t];
@@ -897,7 +923,7 @@ __global__ void k_stamp_hist(const int32_t *block_of_slot, const int32_t *last_u
 // the block bitmap of region L: one extraction over regions 0..L* then lists
 // them in (last_used, block_id) order (cache.py:84-91).
 __global__ void k_mark_victims(const int32_t *block_of_slot, const int32_t *last_used, const uint32_t *ctl,
-                               int32_t pass_no, int64_t nwords, uint32_t *regions) {
+                               int32_t pass_no, int64_t nwords, uint32_t *regions, uint32_t *summary) {
     if (ctl[C_NEVICT] == 0) return;
     const int64_t hw = ctl[C_HW];
     const int32_t lstar = (int32_t)ctl[C_LSTAR];
@@ -905,7 +931,7 @@ __global__ void k_mark_victims(const int32_t *block_of_slot, const int32_t *last
         const int32_t b = block_of_slot[s];
         const int32_t lu = last_used[s];
         if (b >= 0 && lu < pass_no && lu <= lstar)
-            atomicOr(&regions[(int64_t)lu * nwords + (b >> 5)], 1u << (b & 31));
+            bitmap_set(regions, summary, (uint64_t)lu * nwords + (b >> 5), b & 31);
     }
 }
 
@@ -941,19 +967,23 @@ __global__ void k_evict(const uint32_t *victims, const uint32_t *d_n_evict, int3
 // while free slots last, then to victim j - n_free; its record is decoded
 // straight into the slot and the mapping published.  Warp per block; the
 // miss count is read on the device (no host round trip).
-__global__ void __launch_bounds__(256, 3)
+// A warp takes 32 consecutive misses (one coalesced load of their ids and
+// lane-parallel slot bookkeeping), then streams their records through shared
+// memory: kDecRec records are requested with cp.async (no registers held per
+// request, so many random 132 B records are in flight per SM), then decoded
+// from shared memory straight into the slots.
+constexpr int kDecWarps = 8, kDecRec = 16, kDecWords = 64;  // words: the largest record (qbits 31)
+__global__ void __launch_bounds__(kDecWarps * 32, 4)
     k_decode_insert(const uint8_t *__restrict__ payload, int qbits, int stride, const uint32_t *__restrict__ miss_ids,
                     uint32_t *ctl, const uint32_t *__restrict__ victims, float *__restrict__ slot_values,
                     int32_t *block_of_slot, int32_t *last_used, int32_t *slot_of_block, int32_t pass_no) {
+    __shared__ uint32_t stage[kDecWarps][kDecRec][kDecWords];
     const int lane = threadIdx.x & 31;
+    uint32_t(*sw)[kDecWords] = stage[threadIdx.x >> 5];
     const int64_t n_miss = ctl[C_NMISS], hw = ctl[C_HW], n_free = ctl[C_NFREE], cap = ctl[C_CAP];
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl[C_HW_NEXT] = (uint32_t)(n_miss <= n_free ? hw + n_miss : cap);
     const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // A warp takes 32 consecutive misses: one coalesced load of their ids,
-    // then kInFlight records are requested before any is decoded (random
-    // 132 B records need many requests in flight to approach HBM bandwidth).
-    constexpr int kInFlight = 8;
     const int n_words = stride >> 2;
     for (int64_t g = warp0 * 32; g < n_miss; g += nwarps * 32) {
         const int64_t jl = g + lane;
@@ -965,30 +995,35 @@ __global__ void __launch_bounds__(256, 3)
             slot_of_block[my_b] = (int32_t)my_s;
         }
         const int cnt = n_miss - g < 32 ? (int)(n_miss - g) : 32;
-        for (int u0 = 0; u0 < cnt; u0 += kInFlight) {
-            uint32_t wa[kInFlight], wb[kInFlight];
+        for (int u0 = 0; u0 < cnt; u0 += kDecRec) {
 #pragma unroll
-            for (int u = 0; u < kInFlight; u++) {
+            for (int u = 0; u < kDecRec; u++) {
                 const uint32_t b = __shfl_sync(0xffffffffu, my_b, (u0 + u) & 31);
-                wa[u] = wb[u] = 0u;
-                if (u0 + u < cnt)
-                    load_record_warp(reinterpret_cast<const uint32_t *>(payload + (int64_t)b * stride), n_words, lane,
-                                     wa[u], wb[u]);
+                if (u0 + u < cnt) {
+                    const uint32_t *rec = reinterpret_cast<const uint32_t *>(payload + (int64_t)b * stride);
+                    if (lane < n_words) cp_async4(&sw[u][lane], rec + lane);
+                    if (lane + 32 < n_words) cp_async4(&sw[u][lane + 32], rec + lane + 32);
+                }
             }
-#pragma unroll
-            for (int u = 0; u < kInFlight; u++) {
+            cp_async_wait_all();
+            __syncwarp();
+#pragma unroll 4
+            for (int u = 0; u < kDecRec; u++) {
                 const uint32_t s = __shfl_sync(0xffffffffu, my_s, (u0 + u) & 31);
                 if (u0 + u >= cnt) break;  // warp-uniform
                 float *dst = slot_values + (int64_t)s * 64;
                 if (qbits == 16) {  // the common rate: lane decodes values 2l, 2l+1 (one 8 B store)
-                    reinterpret_cast<float2 *>(dst)[lane] = decode16_pair(wa[u], wb[u], lane);
+                    reinterpret_cast<float2 *>(dst)[lane] = decode16_words(sw[u][lane], sw[u][lane + 1], sw[u][0]);
                 } else {
+                    const uint32_t wa = lane < n_words ? sw[u][lane] : 0u;
+                    const uint32_t wb = lane + 32 < n_words ? sw[u][lane + 32] : 0u;
                     float v0, v1;
-                    decode_loaded_warp(wa[u], wb[u], qbits, lane, v0, v1);
+                    decode_loaded_warp(wa, wb, qbits, lane, v0, v1);
                     dst[lane] = v0;
                     dst[lane + 32] = v1;
                 }
             }
+            __syncwarp();  // the stage is refilled by the next batch
         }
     }
 }
@@ -1065,11 +1100,14 @@ struct DenseFieldView {  // fully decoded volume, x-fastest
 
 // engine.py:286-305 _contributor_table: cache slots of each visible block
 // and its 7 +octant neighbours (-1 outside the volume), 32 B per block.
+// Also clears the visibility bitmap for the next pass (its ranks were last
+// read by k_build_entries): every visible id zeroes its word.
 __global__ void k_contrib(const uint32_t *visible_ids, const uint32_t *d_nvis, const int32_t *slot_of_block, int bdx,
-                          int bdy, int bdz, int4 *contrib, uint32_t *err) {
+                          int bdy, int bdz, int4 *contrib, uint32_t *err, uint32_t *vis_bm) {
     const int64_t nvis = *d_nvis;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvis; v += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t b = visible_ids[v];
+        vis_bm[b >> 5] = 0u;
         const int bx = (int)(b % (uint32_t)bdx), by = (int)((b / (uint32_t)bdx) % (uint32_t)bdy),
                   bz = (int)(b / ((uint32_t)bdx * (uint32_t)bdy));
         int s[8];
@@ -1463,7 +1501,6 @@ __global__ void k_frame_start(uint32_t *ctl, int64_t n, int speculation, int max
     ctl[C_CAP] = (uint32_t)cap;
     ctl[C_PHYS] = ctl[C_PHYS_OLD] = (uint32_t)phys;
     ctl[C_HW] = ctl[C_HW_NEXT] = 0;
-    ctl[C_NWORDS_ON] = n_act > 0 ? (uint32_t)nwords : 0u;
 }
 
 // cache.py:66-96 decisions of ensure_resident once the hits are stamped and
@@ -1486,7 +1523,7 @@ __global__ void k_cache_plan(uint32_t *ctl, const uint32_t *hist, int32_t pass_n
     ctl[C_PHYS] = (uint32_t)phys;
     const int64_t n_free = cap - hw;
     ctl[C_NFREE] = (uint32_t)n_free;
-    int64_t n_evict = 0, nreg = 0;
+    int64_t n_evict = 0;
     uint32_t lstar = 0xFFFFFFFFu;
     if (n_miss > n_free) {  // cache.py:80-96
         n_evict = n_miss - n_free;
@@ -1497,11 +1534,9 @@ __global__ void k_cache_plan(uint32_t *ctl, const uint32_t *hist, int32_t pass_n
             lstar = (uint32_t)L;
         }
         if (acc < n_evict) ctl[C_ERR_CAND] = 1;
-        nreg = (int64_t)(lstar + 1) * nwords;
     }
     ctl[C_NEVICT] = (uint32_t)n_evict;
     ctl[C_LSTAR] = lstar;
-    ctl[C_NREG] = (uint32_t)nreg;
 }
 
 // maps of the slots the growth just brought into use (cache.py:42-53)
@@ -1535,7 +1570,6 @@ __global__ void k_pass_end(uint32_t *ctl, uint32_t *row, int64_t n, int speculat
     if (n_after * n_spec > n) ctl[C_ERR_BUDGET] = 1;
     ctl[C_NACT] = (uint32_t)n_after;
     ctl[C_NSPEC] = (uint32_t)n_spec;
-    ctl[C_NWORDS_ON] = n_after > 0 ? (uint32_t)nwords : 0u;
 }
 
 // ---------------------------------------------------- framebuffer read-back
@@ -1606,7 +1640,7 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     act_bm.alloc(nwords);
     int64_t chunk0;
     mask_buffers(1, chunk0);
-    vis_word_off.alloc(2 * nwords);  // visible word offsets + the active extraction's (unused) offsets
+    vis_word_off.alloc(nwords);  // prefix of each non-zero visible word (bitmap rank)
     WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
     WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
     active_ids.alloc(std::min<int64_t>(8 * n, vol->n_blocks) + 1);
@@ -1797,6 +1831,7 @@ void Session::reserve_slots(int64_t need) {
     last_used.grow(need, st);
     cand_key.alloc(need);
     cand_val.alloc(need);
+    word_list.ensure(need);  // victim words <= resident slots
     const int64_t words =
         scan_scratch_words(std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n, need}));
     if (partials.n < words) {
@@ -1825,8 +1860,8 @@ void Session::prepare_pass(int64_t p) {
         vict_bm.alloc(r * nwords);
         WC_CUDA(cudaMemsetAsync(vict_bm.p, 0, 4 * r * nwords, st));
         vict_regions = r;
-        sp_summary.alloc(r * nwords / 32 + 2);
-        sp_words.alloc(r * nwords + r * nwords / 32 + 2);
+        vict_sum.alloc(ceil_div(r * nwords, 32));
+        WC_CUDA(cudaMemsetAsync(vict_sum.p, 0, 4 * vict_sum.n, st));
         const int64_t words = scan_scratch_words(r * nwords);
         if (partials.n < words) {
             partials.ensure(words);
@@ -1914,6 +1949,19 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     WC_CUDA(cudaStreamIsCapturing(st, &cap));
     const bool capturing = cap != cudaStreamCaptureStatusNone;
     pass_staged[std::min<int64_t>(p, kMaxPassLog - 1)] = !capturing;
+    static const bool ktime_on = getenv("WAVECAST_KTIME") != nullptr;
+    struct KTimeScope {  // per-launch events while this pass is enqueued directly
+        KTimeScope(bool on, cudaStream_t s, std::vector<KTime> *v, int64_t p) {
+            if (!on) return;
+            t_ktime_stream = s;
+            t_ktime = v;
+            ktime_tick("pass", (int)p);
+        }
+        ~KTimeScope() {
+            t_ktime_stream = nullptr;
+            t_ktime = nullptr;
+        }
+    } kscope(ktime_on && !capturing, st, &ktime, p);
     auto mark = [&](int k) {
         if (ev && !capturing) WC_CUDA(cudaEventRecord(ev[k], st));
     };
@@ -1955,31 +2003,20 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     mark(1);
     // entry compaction: exclusive scan of per-ray emitted counts
     scan_exclusive_dev(LoadU32{emitted.p}, ctl + C_NACT, n, entry_off.p, ctl + C_NENT, partials.p, st);
-    // visible ids (ascending) + active marking
-    // few rays per block (e.g. one rank's share of a multi-GPU frame): the
-    // two-level extraction, whose cost follows the non-zero words
-    const bool sparse = WC_SPARSE_VISACT || n * 100 < vol->n_blocks;
-    const SparseScratch vsc{sp_summary.p, sp_words.p, ctl + C_NLIST};
-    if (sparse)
-        bitmap_extract_sparse(vis_bm.p, ctl + C_NWORDS_ON, nwords, nwords, vis_word_off.p, visible_ids.p,
-                              ctl + C_NVIS, false, vsc, partials.p, st);
+    // visible ids (ascending) + active marking, from the maintained
+    // summaries: the cost follows the non-zero bitmap words
+    bitmap_extract_dense(vis_bm.p, nwords, vis_word_off.p, visible_ids.p, ctl + C_NVIS, false, partials.p, st);
+    if (vol->bdx % 32 == 0)
+        k_mark_active_words<<<grid_for(n, 256), 256, 0, st>>>(visible_ids.p, ctl + C_NVIS, vis_bm.p, vol->bdx / 32,
+                                                              vol->bdy, vol->bdz, act_bm.p);
     else
-        bitmap_extract_dev(vis_bm.p, ctl + C_NWORDS_ON, nwords, vis_word_off.p, visible_ids.p, ctl + C_NVIS,
-                           partials.p, st);
-    k_mark_active<<<grid_for((int64_t)8 * n, 256), 256, 0, st>>>(visible_ids.p, ctl + C_NVIS, vol->bdx, vol->bdy,
-                                                                 vol->bdz, act_bm.p);
+        k_mark_active<<<grid_for((int64_t)8 * n, 256), 256, 0, st>>>(visible_ids.p, ctl + C_NVIS, vol->bdx, vol->bdy,
+                                                                     vol->bdz, act_bm.p);
     WC_LAUNCH_CHECK();
-    if (sparse)
-        bitmap_extract_sparse(act_bm.p, ctl + C_NWORDS_ON, nwords, nwords, nullptr, active_ids.p, ctl + C_NACTB, true,
-                              vsc, partials.p, st);  // clears act_bm
-    else
-        bitmap_extract_dev(act_bm.p, ctl + C_NWORDS_ON, nwords, vis_word_off.p + nwords, active_ids.p, ctl + C_NACTB,
-                           partials.p, st);
+    bitmap_extract_dense(act_bm.p, nwords, nullptr, active_ids.p, ctl + C_NACTB, true, partials.p, st);  // clears act_bm
     k_build_entries<<<grid_for(n, 256), 256, 0, st>>>(ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p,
                                                       vis_word_off.p, ent_key.p, ent_val.p, ent_ray.p, ent_blk.p);
-    WC_LAUNCH_CHECK();
-    WC_CUDA(cudaMemsetAsync(vis_bm.p, 0, 4 * nwords, st));
-    if (!sparse) WC_CUDA(cudaMemsetAsync(act_bm.p, 0, 4 * nwords, st));
+    WC_LAUNCH_CHECK();  // vis_bm is cleared by k_contrib
 
     // cache.ensure_resident (cache.py:66-111): stamp hits, list misses
     // (ascending), then growth / victims / decode, all sized on the device
@@ -2013,13 +2050,12 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     WC_LAUNCH_CHECK();
     k_phys_init<<<grid_for(slot_alloc, 256), 256, 0, st>>>(ctl, block_of_slot.p, last_used.p);
     WC_LAUNCH_CHECK();
-    if (p >= 1) {  // victims in (last_used, block_id) order: one (sparse) extraction over the stamp regions
-        const SparseScratch sc{sp_summary.p, sp_words.p, ctl + C_NLIST};
+    if (p >= 1) {  // victims in (last_used, block_id) order: one extraction over the stamp regions
         k_mark_victims<<<grid_for(slot_alloc, 256), 256, 0, st>>>(block_of_slot.p, last_used.p, ctl, stamp, nwords,
-                                                                  vict_bm.p);
+                                                                  vict_bm.p, vict_sum.p);
         WC_LAUNCH_CHECK();
-        bitmap_extract_sparse(vict_bm.p, ctl + C_NREG, (int64_t)stamp * nwords, nwords, nullptr, cand_key.p,
-                              ctl + C_NCAND, true, sc, partials.p, st);  // clears the regions
+        bitmap_extract_listed(vict_bm.p, vict_sum.p, (int64_t)stamp * nwords, slot_alloc, nwords, nullptr, cand_key.p,
+                              ctl + C_NCAND, true, word_list.p, ctl + C_NLIST, partials.p, st);  // clears the regions
         k_blocks_to_slots<<<grid_for(slot_alloc, 256), 256, 0, st>>>(cand_key.p, ctl + C_NEVICT, slot_of_block.p,
                                                                      cand_val.p);
         WC_LAUNCH_CHECK();
@@ -2029,7 +2065,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     }
     // the misses' records decoded straight into their slots (free slots
     // first, then the victims in order, cache.py:97-103)
-    k_decode_insert<<<grid_for(nmax * 32, 256, 8), 256, 0, st>>>(vol->payload.p, vol->qbits, vol->stride,
+    k_decode_insert<<<grid_for(nmax * 32, kDecWarps * 32, 4), kDecWarps * 32, 0, st>>>(vol->payload.p, vol->qbits, vol->stride,
                                                                  miss_ids.p, ctl, cand_val.p, slot_values.p,
                                                                  block_of_slot.p, last_used.p, slot_of_block.p, stamp);
     WC_LAUNCH_CHECK();
@@ -2049,7 +2085,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     }
     mark(4);
     k_contrib<<<grid_for(n, 256), 256, 0, st>>>(visible_ids.p, ctl + C_NVIS, slot_of_block.p, vol->bdx, vol->bdy,
-                                                vol->bdz, contrib.p, ctl + C_ERR);
+                                                vol->bdz, contrib.p, ctl + C_ERR, vis_bm.p);
     WC_LAUNCH_CHECK();
     RaytraceArgs ra{};
     ra.visible_ids = visible_ids.p;
@@ -2103,6 +2139,28 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
                                 max_spec, nwords);
     WC_LAUNCH_CHECK();
     mark(6);
+}
+
+// WAVECAST_KTIME: device time of every launch since the last report, by
+// pass and launch site (the stream has been synchronised by the caller).
+void Session::ktime_report() {
+    if (ktime.empty()) return;
+    int pass = -1, k = 0;
+    for (size_t i = 0; i < ktime.size(); i++) {
+        const KTime &t = ktime[i];
+        if (std::string(t.file) == "pass") {
+            pass = t.line;
+            k = 0;
+            continue;
+        }
+        float ms = 0.0f;
+        if (i > 0) cudaEventElapsedTime(&ms, ktime[i - 1].ev, t.ev);
+        const char *base = strrchr(t.file, '/');
+        fprintf(stderr, "[ktime] pass %d #%02d %s:%d %.1f us\n", pass, k++, base ? base + 1 : t.file, t.line,
+                ms * 1e3f);
+    }
+    for (auto &t : ktime) cudaEventDestroy(t.ev);
+    ktime.clear();
 }
 
 void Session::check_device_errors() {
@@ -2201,6 +2259,7 @@ int64_t Session::run_frame(PassStatsC *out, int64_t max_out) {
         WC_CUDA(cudaMemcpyAsync(h_plog.p, plog.p, 4 * L_COUNT * std::min<int64_t>(p0 + batch, kMaxPassLog),
                                 cudaMemcpyDeviceToHost, st));
         read_counters(0, C_COUNT);
+        ktime_report();
         check_device_errors();
         bool done = false;
         for (int64_t b = 0; b < batch; b++) {

@@ -44,14 +44,12 @@ enum Counter : int {
     C_PHYS_OLD,   // C_PHYS before this pass's growth
     C_NEVICT,     // victims this pass
     C_LSTAR,      // last stamp bucket the victims reach (0xFFFFFFFF: none)
-    C_NREG,       // bitmap words the victim extraction scans ((L*+1) regions)
     C_HW_NEXT,    // occupied slots after this pass's inserts
-    C_NWORDS_ON,  // bitmap words the visibility extraction scans (0 once no ray is active)
     C_ERR_BUDGET, // device-side invariant failure: slot budget exceeded
     C_ERR_CAND,   // device-side invariant failure: fewer eviction candidates than needed
     C_ERR_CAP,    // logical capacity beyond the reserved slots (host must reserve more)
     C_NSNAP,      // rays still active when the framebuffer read-back started
-    C_NLIST,      // non-zero bitmap words listed by bitmap_extract_sparse
+    C_NLIST,      // non-zero bitmap words listed by bitmap_extract_listed
     C_FRAME,      // frame counter (device-derived scan epochs)
     C_COUNT
 };
@@ -139,11 +137,14 @@ struct Session {
     DevBuf<uint32_t> vict_bm;       // per-stamp block bitmaps for victim selection
     DevBuf<double> fparams;         // FrameParams: eye[3], iso, base colour[3] (written by k_frame_start)
     uint32_t frame_no = 0;
-    DevBuf<uint32_t> sp_summary, sp_words;  // bitmap_extract_sparse scratch (sized with the regions)
+    DevBuf<uint32_t> vict_sum;   // summary of the victim regions
+    DevBuf<uint32_t> word_list;  // non-zero words listed by bitmap_extract_listed
     int64_t vict_regions = 0;
     int64_t last_slots_used = 0, last_nvis = 0, last_nactb = 0, last_nent = 0;
     int64_t last_n_spec = 1;
     float last_kernel_ms = 0.0f;
+    std::vector<KTime> ktime;  // WAVECAST_KTIME: per-launch events of the directly enqueued passes
+    void ktime_report();
 
     Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, int64_t n_rays, const double *origins,
             const double *dirs, double iso, int speculation, int max_spec, int64_t cache_capacity, int corrupt);

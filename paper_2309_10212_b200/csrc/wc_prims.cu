@@ -120,48 +120,83 @@ void radix_sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int nbits, Radi
 
 // ----------------------------------------------------------- bitmap extract
 
-void bitmap_extract(const uint32_t *bm, int64_t nwords, uint32_t *word_offsets, uint32_t *out,
-                    uint32_t *d_count, uint32_t *partials, cudaStream_t st) {
+template <bool kClear>
+__global__ void __launch_bounds__(256) k_bitmap_dense(uint32_t *__restrict__ bm, int64_t nwords, int k4,
+                                                      uint32_t *__restrict__ word_offsets, uint32_t *__restrict__ ids,
+                                                      uint64_t *status, ScanEpoch ep, uint32_t *d_count) {
+    __shared__ uint32_t sw[32];
+    __shared__ uint32_t s_excl;
+    const uint32_t epoch = resolve_epoch(ep);
+    const int64_t chunk = 256LL * k4;
+    const int64_t t = blockIdx.x;
+    const int64_t last = (nwords - 1) / chunk;
+    const int64_t w0 = t * chunk + (int64_t)threadIdx.x * k4;
+    const int64_t w1 = min(nwords, w0 + k4);
+    uint32_t cnt = 0;
+    for (int64_t w = w0; w < w1; w += 4) {
+        if (w + 4 <= w1) {
+            const uint4 q = *reinterpret_cast<const uint4 *>(bm + w);
+            cnt += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+        } else {
+            for (int64_t x = w; x < w1; x++) cnt += __popc(bm[x]);
+        }
+    }
+    uint32_t agg;
+    uint32_t pre = block_exclusive_scan(cnt, sw, &agg);
+    if (threadIdx.x < 32) {
+        const uint32_t excl = tile_lookback(t, agg, status, epoch);
+        if (threadIdx.x == 0) {
+            s_excl = excl;
+            if (t == last) *d_count = excl + agg;
+        }
+    }
+    __syncthreads();
+    pre += s_excl;
+    if (!cnt) return;
+    for (int64_t w = w0; w < w1; w++) {
+        uint32_t v = bm[w];
+        if (!v) continue;
+        if (word_offsets) word_offsets[w] = pre;
+        if (kClear) bm[w] = 0u;
+        const uint32_t base = (uint32_t)(w * 32);
+        while (v) {
+            ids[pre++] = base + __ffs(v) - 1;
+            v &= v - 1;
+        }
+    }
+}
+
+void bitmap_extract_dense(uint32_t *bm, int64_t nwords, uint32_t *word_offsets, uint32_t *ids, uint32_t *d_count,
+                          bool clear, uint32_t *partials, cudaStream_t st) {
     if (nwords <= 0) {
         WC_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st));
         return;
     }
-    // one pass: popcount scan of the words, ids written by each tile as
-    // soon as its prefix is known
-    k_scan_onepass<LoadPopc, SinkBits><<<(unsigned)scan_tiles(nwords), kScanThreads, 0, st>>>(
-        LoadPopc{bm}, SinkBits{bm, word_offsets, out}, nwords, nullptr, reinterpret_cast<uint64_t *>(partials),
-        scan_epoch(), d_count);
+    // one wave of 4 CTAs per SM; at least 4 words (one 16 B load) per thread
+    const int64_t k4 = std::max<int64_t>(4, ceil_div(ceil_div(nwords, (int64_t)kNumSMs * 4 * 256), 4) * 4);
+    const unsigned grid = (unsigned)ceil_div(nwords, 256 * k4);
+    if (clear)
+        k_bitmap_dense<true><<<grid, 256, 0, st>>>(bm, nwords, (int)k4, word_offsets, ids,
+                                                  reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
+    else
+        k_bitmap_dense<false><<<grid, 256, 0, st>>>(bm, nwords, (int)k4, word_offsets, ids,
+                                                   reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
     WC_LAUNCH_CHECK();
 }
 
-void bitmap_extract_dev(const uint32_t *bm, const uint32_t *d_nwords, int64_t nwords_max, uint32_t *word_offsets,
-                        uint32_t *out, uint32_t *d_count, uint32_t *partials, cudaStream_t st) {
-    if (nwords_max <= 0) {
-        WC_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st));
-        return;
+// summary word i -> ascending indices of its set bits (the non-zero words of
+// the bitmap), clearing the summary word
+struct SinkList {
+    uint32_t *summary, *list;
+    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const {
+        uint32_t v = summary[i];
+        if (v) summary[i] = 0u;
+        while (v) {
+            list[prefix++] = (uint32_t)(i * 32 + __ffs(v) - 1);
+            v &= v - 1;
+        }
     }
-    k_scan_onepass<LoadPopc, SinkBits><<<(unsigned)scan_tiles(nwords_max), kScanThreads, 0, st>>>(
-        LoadPopc{bm}, SinkBits{bm, word_offsets, out}, nwords_max, d_nwords, reinterpret_cast<uint64_t *>(partials),
-        scan_epoch(), d_count);
-    WC_LAUNCH_CHECK();
-}
-
-// ---- two-level extraction ----------------------------------------------
-
-// summary bit w = (bm[w] != 0), warp per 32 words (one coalesced 128 B read)
-__global__ void k_summarize(const uint32_t *__restrict__ bm, const uint32_t *d_nwords, int64_t nwords_max,
-                            uint32_t *__restrict__ summary) {
-    const int64_t n = d_nwords ? min(nwords_max, (int64_t)*d_nwords) : nwords_max;
-    const int64_t ns = (nwords_max + 31) >> 5;  // every summary word (zero past n): no stale bits
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t sidx = w0; sidx < ns; sidx += nw) {
-        const int64_t w = sidx * 32 + lane;
-        const uint32_t bits = __ballot_sync(0xffffffffu, w < n && bm[w] != 0u);
-        if (lane == 0) summary[sidx] = bits;
-    }
-}
+};
 
 struct LoadPopcIdx {
     const uint32_t *bm, *idx;
@@ -187,23 +222,22 @@ struct SinkBitsIdx {
     }
 };
 
-void bitmap_extract_sparse(uint32_t *bm, const uint32_t *d_nwords, int64_t nwords_max, int64_t id_mod,
-                           uint32_t *word_offsets, uint32_t *ids, uint32_t *d_count, bool clear,
-                           const SparseScratch &sc, uint32_t *partials, cudaStream_t st) {
-    if (nwords_max <= 0) {
+void bitmap_extract_listed(uint32_t *bm, uint32_t *summary, int64_t nwords_max, int64_t nlist_max, int64_t id_mod,
+                           uint32_t *word_offsets, uint32_t *ids, uint32_t *d_count, bool clear, uint32_t *word_list,
+                           uint32_t *d_nlist, uint32_t *partials, cudaStream_t st) {
+    const int64_t ns = ceil_div(nwords_max, 32);
+    nlist_max = std::min(nlist_max, nwords_max);
+    if (ns <= 0 || nlist_max <= 0) {
         WC_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st));
         return;
     }
-    const int64_t ns_max = (nwords_max + 31) / 32;
-    k_summarize<<<grid_for(ns_max * 32, 256, 8), 256, 0, st>>>(bm, d_nwords, nwords_max, sc.summary);
+    k_scan_onepass<LoadPopc, SinkList><<<(unsigned)scan_tiles(ns), kScanThreads, 0, st>>>(
+        LoadPopc{summary}, SinkList{summary, word_list}, ns, nullptr, reinterpret_cast<uint64_t *>(partials),
+        scan_epoch(), d_nlist);
     WC_LAUNCH_CHECK();
-    k_scan_onepass<LoadPopc, SinkBits><<<(unsigned)scan_tiles(ns_max), kScanThreads, 0, st>>>(
-        LoadPopc{sc.summary}, SinkBits{sc.summary, sc.word_list + nwords_max, sc.word_list}, ns_max, nullptr,
-        reinterpret_cast<uint64_t *>(partials), scan_epoch(), sc.d_nlist);
-    WC_LAUNCH_CHECK();
-    k_scan_onepass<LoadPopcIdx, SinkBitsIdx><<<(unsigned)scan_tiles(nwords_max), kScanThreads, 0, st>>>(
-        LoadPopcIdx{bm, sc.word_list}, SinkBitsIdx{bm, sc.word_list, word_offsets, ids, id_mod, clear}, nwords_max,
-        sc.d_nlist, reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
+    k_scan_onepass<LoadPopcIdx, SinkBitsIdx><<<(unsigned)scan_tiles(nlist_max), kScanThreads, 0, st>>>(
+        LoadPopcIdx{bm, word_list}, SinkBitsIdx{bm, word_list, word_offsets, ids, id_mod, clear}, nlist_max, d_nlist,
+        reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
     WC_LAUNCH_CHECK();
 }
 

@@ -4,7 +4,8 @@
 // compact         -> fused into callers via the scan offsets
 // sort_by_key     -> radix_sort_pairs() (stable LSD, 8-bit digits, per-warp
 //                    match_any ranking so equal keys keep input order)
-// Bitmap ranking  -> bitmap_extract() (ascending ids of set bits)
+// Bitmap ranking  -> bitmap_extract_listed() (ascending ids of set bits, from
+//                    a summary maintained by the kernels that set them)
 #pragma once
 
 #include "wc_common.cuh"
@@ -142,6 +143,40 @@ struct SinkCompact {
     }
 };
 
+// Decoupled look-back of tile t (called by warp 0 of its CTA): publishes the
+// tile's aggregate, sums predecessors back to the nearest published prefix,
+// publishes the tile's inclusive prefix and returns its exclusive prefix.
+__device__ __forceinline__ uint32_t tile_lookback(int64_t t, uint32_t agg, uint64_t *status, uint32_t epoch) {
+    const int lane = threadIdx.x & 31;
+    uint32_t excl = 0;
+    if (t == 0) {
+        if (lane == 0) store_status(status, epoch, kFlagPrefix, agg);
+        return 0;
+    }
+    if (lane == 0) store_status(status + t, epoch, kFlagAggregate, agg);
+    for (int64_t pred = t - 1;; pred -= 32) {
+        const int64_t idx = pred - lane;
+        uint32_t flag = kFlagPrefix, val = 0;  // before tile 0: an implicit zero prefix
+        if (idx >= 0) {
+            unsigned long long w;
+            do {
+                w = *reinterpret_cast<volatile unsigned long long *>(status + idx);
+                flag = (uint32_t)(w >> 34) == epoch ? (uint32_t)(w >> 32) & 3u : 0u;
+            } while (flag == 0);
+            val = (uint32_t)w;
+        }
+        const uint32_t pm = __ballot_sync(0xffffffffu, flag == kFlagPrefix);
+        const int fp = pm ? __ffs(pm) - 1 : 31;  // nearest predecessor holding a prefix
+        uint32_t c = lane <= fp ? val : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        excl += c;
+        if (pm) break;
+    }
+    if (lane == 0) store_status(status + t, epoch, kFlagPrefix, excl + agg);
+    return excl;
+}
+
 template <class Load, class Sink>
 __global__ void __launch_bounds__(kScanThreads)
     k_scan_onepass(Load ld, Sink sink, int64_t n_max, const uint32_t *d_n, uint64_t *status, ScanEpoch ep,
@@ -171,34 +206,8 @@ __global__ void __launch_bounds__(kScanThreads)
     uint32_t agg;
     uint32_t pre = block_exclusive_scan(s, sw, &agg);
     if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        uint32_t excl = 0;
-        if (t == 0) {
-            if (lane == 0) store_status(status, epoch, kFlagPrefix, agg);
-        } else {
-            if (lane == 0) store_status(status + t, epoch, kFlagAggregate, agg);
-            for (int64_t pred = t - 1;; pred -= 32) {
-                const int64_t idx = pred - lane;
-                uint32_t flag = kFlagPrefix, val = 0;  // before tile 0: an implicit zero prefix
-                if (idx >= 0) {
-                    unsigned long long w;
-                    do {
-                        w = *reinterpret_cast<volatile unsigned long long *>(status + idx);
-                        flag = (uint32_t)(w >> 34) == epoch ? (uint32_t)(w >> 32) & 3u : 0u;
-                    } while (flag == 0);
-                    val = (uint32_t)w;
-                }
-                const uint32_t pm = __ballot_sync(0xffffffffu, flag == kFlagPrefix);
-                const int fp = pm ? __ffs(pm) - 1 : 31;  // nearest predecessor holding a prefix
-                uint32_t c = lane <= fp ? val : 0u;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-                excl += c;
-                if (pm) break;
-            }
-            if (lane == 0) store_status(status + t, epoch, kFlagPrefix, excl + agg);
-        }
-        if (lane == 0) {
+        const uint32_t excl = tile_lookback(t, agg, status, epoch);
+        if (threadIdx.x == 0) {
             s_excl = excl;
             if (t == last && d_total) *d_total = n > 0 ? excl + agg : 0u;
         }
@@ -277,30 +286,43 @@ struct RadixScratch {
 void radix_sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int nbits, RadixScratch &scratch,
                       cudaStream_t st);
 
-// Ascending ids of the set bits of bm[0..nwords) -> out; count -> *d_count.
-// word_offsets (nwords uint32) receives the exclusive popcount prefix and can
-// later rank a set bit: rank(b) = word_offsets[b>>5] + popc(bm[b>>5] & lowmask).
-void bitmap_extract(const uint32_t *bm, int64_t nwords, uint32_t *word_offsets, uint32_t *out,
-                    uint32_t *d_count, uint32_t *partials, cudaStream_t st);
-// Same over the first *d_nwords (<= nwords_max, read on the device) words.
-void bitmap_extract_dev(const uint32_t *bm, const uint32_t *d_nwords, int64_t nwords_max, uint32_t *word_offsets,
-                        uint32_t *out, uint32_t *d_count, uint32_t *partials, cudaStream_t st);
+// Bitmaps with a maintained summary: bit w of the summary is set whenever
+// word w of the bitmap becomes non-zero, by the kernel that sets the bit
+// (bitmap_set) or by a pass over the same ids, so an extraction never streams the whole
+// bitmap: its cost follows the non-zero words.  Summaries are cleared by the
+// extraction that reads them; bitmaps are cleared by it (clear = true) or by
+// the caller after the ranks have been used.
+__device__ __forceinline__ void bitmap_set_word(uint32_t *bm, uint32_t *summary, uint64_t word, uint32_t bits) {
+    if (atomicOr(&bm[word], bits) == 0u) atomicOr(&summary[word >> 5], 1u << (word & 31));
+}
+__device__ __forceinline__ void bitmap_set(uint32_t *bm, uint32_t *summary, uint64_t word, uint32_t bit) {
+    bitmap_set_word(bm, summary, word, 1u << bit);
+}
+// Ascending ids of the set bits of bm[0..nwords) -> ids, count -> *d_count,
+// in one single-pass launch sized to one wave: each CTA owns a contiguous
+// chunk of words (16 B loads, a contiguous run per thread), publishes its
+// popcount through the decoupled look-back and writes its ids in order.
+// word_offsets (nullable) receives the exclusive prefix of every non-zero
+// word (bitmap rank: word_offsets[b >> 5] + popc(bm[b >> 5] & lowmask(b)));
+// clear zeroes the non-zero words.  For bitmaps that live in L2 (set by
+// atomics just before), the cost is one read of the bitmap plus the ids.
+void bitmap_extract_dense(uint32_t *bm, int64_t nwords, uint32_t *word_offsets, uint32_t *ids, uint32_t *d_count,
+                          bool clear, uint32_t *partials, cudaStream_t st);
 
-// Two-level extraction for sparse bitmaps: cost grows with the non-zero
-// words, not with the bitmap.  A streaming pass writes a summary (bit w of
-// the summary = word w is non-zero), a scan of the summary lists the
-// non-zero words in order, and a scan of their popcounts writes the ids
-// (bit b of word w -> (w % id_mod) * 32 + b, so concatenated bitmaps of
-// id_mod words each list (bitmap, id) pairs in order).  word_offsets
-// (nullable) receives the prefix of each non-zero word; clear zeroes the
-// non-zero words as they are read.  Scratch: summary >= nwords_max/32 + 1,
-// word_list >= nwords_max + nwords_max/32 + 1 words, partials >=
-// scan_scratch_words(nwords_max).
-struct SparseScratch {
-    uint32_t *summary, *word_list, *d_nlist;
-};
-void bitmap_extract_sparse(uint32_t *bm, const uint32_t *d_nwords, int64_t nwords_max, int64_t id_mod,
-                           uint32_t *word_offsets, uint32_t *ids, uint32_t *d_count, bool clear,
-                           const SparseScratch &sc, uint32_t *partials, cudaStream_t st);
+// Ascending ids of the set bits of bm -> ids, count -> *d_count, from its
+// summary (summary words [0, ceil(nwords_max / 32))):
+//   1. a scan of the summary's popcounts lists the non-zero words in order
+//      (and clears the summary);
+//   2. a scan of those words' popcounts writes the ids: bit b of word w ->
+//      (w % id_mod) * 32 + b, so concatenated bitmaps of id_mod words each
+//      list (bitmap, id) pairs in order.
+// nlist_max bounds the non-zero words (launch size of step 2).  word_offsets
+// (nullable) receives the exclusive prefix of each non-zero word, so a set
+// bit ranks as word_offsets[b >> 5] + popc(bm[b >> 5] & lowmask(b)); clear
+// zeroes the listed words as they are read.  Scratch: word_list >= nlist_max
+// words, partials >= scan_scratch_words(max(nlist_max, summary words)).
+void bitmap_extract_listed(uint32_t *bm, uint32_t *summary, int64_t nwords_max, int64_t nlist_max, int64_t id_mod,
+                           uint32_t *word_offsets, uint32_t *ids, uint32_t *d_count, bool clear, uint32_t *word_list,
+                           uint32_t *d_nlist, uint32_t *partials, cudaStream_t st);
 
 }  // namespace wc

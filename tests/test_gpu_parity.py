@@ -92,10 +92,15 @@ SCENES = [
     ("turbulence", (72, 64, 60), 16, 128, 72, 0.5, 0.3, True, 64, 1024),
     ("value_noise", 128, 12, 12, 12, 0.5, 0.2, True, 64, None),        # few rays per block: sparse extraction
     ("value_noise", 112, 10, 14, 11, 0.45, 0.6, False, 64, 40),         # ... with eviction
+    # rows of whole bitmap words (bdx % 32 == 0): word-level active marking,
+    # +x carries across words and the row / plane edges
+    ("turbulence", (256, 40, 36), 16, 120, 90, 0.5, 0.2, True, 64, None),
+    ("gaussians", (128, 72, 56), 16, 96, 80, 0.3, 0.35, True, 64, None),
+    ("value_noise", (256, 36, 28), 12, 96, 72, 0.5, 0.3, True, 64, 60),  # ... with eviction
 ]
 
 
-@pytest.mark.parametrize("scene", SCENES, ids=[f"{s[0]}-{s[1]}-q{s[2]}-{s[3]}x{s[4]}-spec{int(s[7])}" for s in SCENES])
+@pytest.mark.parametrize("scene", SCENES, ids=[f"{s[0]}-{s[1] if isinstance(s[1], int) else 'x'.join(map(str, s[1]))}-q{s[2]}-{s[3]}x{s[4]}-spec{int(s[7])}" for s in SCENES])
 def test_render_lockstep_vs_oracle(wc, scene):
     kind, n, qbits, w, h, isof, camf, spec, max_spec, cache = scene
     vol = host_volume(kind, n, seed=1 if kind == "turbulence" else (0 if kind == "gaussians" else 3))
