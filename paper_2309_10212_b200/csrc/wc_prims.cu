@@ -231,11 +231,11 @@ void bitmap_extract_listed(uint32_t *bm, uint32_t *summary, int64_t nwords_max, 
         WC_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st));
         return;
     }
-    k_scan_onepass<LoadPopc, SinkList><<<(unsigned)scan_tiles(ns), kScanThreads, 0, st>>>(
+    k_scan_onepass<LoadPopc, SinkList><<<scan_grid(ns), kScanThreads, 0, st>>>(
         LoadPopc{summary}, SinkList{summary, word_list}, ns, nullptr, reinterpret_cast<uint64_t *>(partials),
         scan_epoch(), d_nlist);
     WC_LAUNCH_CHECK();
-    k_scan_onepass<LoadPopcIdx, SinkBitsIdx><<<(unsigned)scan_tiles(nlist_max), kScanThreads, 0, st>>>(
+    k_scan_onepass<LoadPopcIdx, SinkBitsIdx><<<scan_grid(nlist_max), kScanThreads, 0, st>>>(
         LoadPopcIdx{bm, word_list}, SinkBitsIdx{bm, word_list, word_offsets, ids, id_mod, clear}, nlist_max, d_nlist,
         reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
     WC_LAUNCH_CHECK();

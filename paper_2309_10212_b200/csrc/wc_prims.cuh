@@ -177,6 +177,13 @@ __device__ __forceinline__ uint32_t tile_lookback(int64_t t, uint32_t agg, uint6
     return excl;
 }
 
+// The grid is capped (kScanMaxCtas) so that a scan sized for a large upper
+// bound does not launch thousands of CTAs that find no work: with more tiles
+// than CTAs, each CTA owns m consecutive tiles, publishes their total through
+// the look-back, then scans them in order (loading each twice).
+constexpr int kScanMaxCtas = kNumSMs * 8;
+inline unsigned scan_grid(int64_t n_max) { return (unsigned)std::min<int64_t>(scan_tiles(n_max), kScanMaxCtas); }
+
 template <class Load, class Sink>
 __global__ void __launch_bounds__(kScanThreads)
     k_scan_onepass(Load ld, Sink sink, int64_t n_max, const uint32_t *d_n, uint64_t *status, ScanEpoch ep,
@@ -186,45 +193,67 @@ __global__ void __launch_bounds__(kScanThreads)
     __shared__ uint32_t s_excl;
     const uint32_t epoch = resolve_epoch(ep);
     const int64_t n = scan_count(n_max, d_n);
+    const int64_t ntiles = n > 0 ? (n - 1) / kScanTile + 1 : 1;
+    const int64_t m = (ntiles + gridDim.x - 1) / gridDim.x;  // tiles per CTA
     const int64_t t = blockIdx.x;
-    const int64_t base = t * kScanTile;
-    const int64_t last = n > 0 ? (n - 1) / kScanTile : 0;
+    const int64_t last = (ntiles - 1) / m;
     if (t > last) return;
-#pragma unroll
-    for (int k = 0; k < kScanIPT; k++) {
-        const int idx = k * kScanThreads + threadIdx.x;
-        const int64_t i = base + idx;
-        tile[idx] = i < n ? ld(i) : 0;
-    }
-    __syncthreads();
-    uint32_t v[kScanIPT], s = 0;
-#pragma unroll
-    for (int k = 0; k < kScanIPT; k++) {
-        v[k] = tile[threadIdx.x * kScanIPT + k];
-        s += v[k];
-    }
-    uint32_t agg;
-    uint32_t pre = block_exclusive_scan(s, sw, &agg);
-    if (threadIdx.x < 32) {
-        const uint32_t excl = tile_lookback(t, agg, status, epoch);
-        if (threadIdx.x == 0) {
-            s_excl = excl;
-            if (t == last && d_total) *d_total = n > 0 ? excl + agg : 0u;
+    const int64_t base = t * m * kScanTile;
+    if (m > 1) {  // the chunk's total first, so successors can look back early
+        uint32_t s = 0;
+        for (int64_t i = base + threadIdx.x; i < min(n, base + m * kScanTile); i += kScanThreads) s += ld(i);
+        uint32_t agg;
+        block_exclusive_scan(s, sw, &agg);
+        if (threadIdx.x < 32) {
+            const uint32_t excl = tile_lookback(t, agg, status, epoch);
+            if (threadIdx.x == 0) {
+                s_excl = excl;
+                if (t == last && d_total) *d_total = excl + agg;
+            }
         }
+        __syncthreads();
     }
-    __syncthreads();
-    pre += s_excl;
+    uint32_t running = 0;
+    for (int64_t sub = 0; sub < m; sub++) {
+        const int64_t tb = base + sub * kScanTile;
 #pragma unroll
-    for (int k = 0; k < kScanIPT; k++) {
-        tile[threadIdx.x * kScanIPT + k] = pre;
-        pre += v[k];
-    }
-    __syncthreads();
+        for (int k = 0; k < kScanIPT; k++) {
+            const int idx = k * kScanThreads + threadIdx.x;
+            const int64_t i = tb + idx;
+            tile[idx] = i < n ? ld(i) : 0;
+        }
+        __syncthreads();
+        uint32_t v[kScanIPT], s = 0;
 #pragma unroll
-    for (int k = 0; k < kScanIPT; k++) {
-        const int idx = k * kScanThreads + threadIdx.x;
-        const int64_t i = base + idx;
-        if (i < n) sink(i, tile[idx]);
+        for (int k = 0; k < kScanIPT; k++) {
+            v[k] = tile[threadIdx.x * kScanIPT + k];
+            s += v[k];
+        }
+        uint32_t agg;
+        uint32_t pre = block_exclusive_scan(s, sw, &agg);
+        if (m == 1 && threadIdx.x < 32) {
+            const uint32_t excl = tile_lookback(t, agg, status, epoch);
+            if (threadIdx.x == 0) {
+                s_excl = excl;
+                if (t == last && d_total) *d_total = n > 0 ? excl + agg : 0u;
+            }
+        }
+        __syncthreads();
+        pre += s_excl + running;
+#pragma unroll
+        for (int k = 0; k < kScanIPT; k++) {
+            tile[threadIdx.x * kScanIPT + k] = pre;
+            pre += v[k];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kScanIPT; k++) {
+            const int idx = k * kScanThreads + threadIdx.x;
+            const int64_t i = tb + idx;
+            if (i < n) sink(i, tile[idx]);
+        }
+        running += agg;
+        __syncthreads();  // tile and sw are reused by the next tile
     }
 }
 
@@ -236,7 +265,7 @@ void scan_exclusive(Load ld, int64_t n, uint32_t *out, uint32_t *d_total, uint32
         WC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
         return;
     }
-    k_scan_onepass<Load, SinkStore><<<(unsigned)scan_tiles(n), kScanThreads, 0, st>>>(
+    k_scan_onepass<Load, SinkStore><<<scan_grid(n), kScanThreads, 0, st>>>(
         ld, SinkStore{out}, n, nullptr, reinterpret_cast<uint64_t *>(scratch), scan_epoch(), d_total);
     WC_LAUNCH_CHECK();
 }
@@ -249,7 +278,7 @@ void scan_exclusive_dev(Load ld, const uint32_t *d_n, int64_t n_max, uint32_t *o
         WC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
         return;
     }
-    k_scan_onepass<Load, SinkStore><<<(unsigned)scan_tiles(n_max), kScanThreads, 0, st>>>(
+    k_scan_onepass<Load, SinkStore><<<scan_grid(n_max), kScanThreads, 0, st>>>(
         ld, SinkStore{out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), scan_epoch(), d_total);
     WC_LAUNCH_CHECK();
 }
@@ -263,7 +292,7 @@ void compact_dev(Pred pred, const uint32_t *ids, const uint32_t *d_n, int64_t n_
         WC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
         return;
     }
-    k_scan_onepass<Pred, SinkCompact<Pred>><<<(unsigned)scan_tiles(n_max), kScanThreads, 0, st>>>(
+    k_scan_onepass<Pred, SinkCompact<Pred>><<<scan_grid(n_max), kScanThreads, 0, st>>>(
         pred, SinkCompact<Pred>{pred, ids, out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), scan_epoch(),
         d_total);
     WC_LAUNCH_CHECK();

@@ -240,7 +240,7 @@ def test_brute_force_reference_render(wc):
 # --------------------------------------------------------------- prims
 def test_prims_scan_sort(wc):
     rng = np.random.default_rng(5)
-    for n in (0, 1, 7, 2048, 2049, 100000, 1 << 20):
+    for n in (0, 1, 7, 2048, 2049, 100000, 1 << 20, 3_000_017):  # > 1184 tiles: several tiles per CTA
         v = rng.integers(0, 1000, n).astype(np.uint32)
         out, tot = wc.prims.exclusive_scan(v)
         ref = np.concatenate([[0], np.cumsum(v.astype(np.uint64))[:-1]]).astype(np.uint32) if n else v
