@@ -31,9 +31,6 @@
 #ifndef WC_WARP_TRAVERSE_MAX
 #define WC_WARP_TRAVERSE_MAX 16384
 #endif
-#ifndef WC_EARLY_HIST
-#define WC_EARLY_HIST 1
-#endif
 #ifndef WC_RAYTRACE_MIN_CTAS
 #define WC_RAYTRACE_MIN_CTAS 6
 #endif
@@ -882,15 +879,36 @@ __global__ void k_run_offsets(const uint32_t *key, int64_t n, int64_t nvis, uint
 
 // ---------------------------------------------------------------- cache
 
+// Stamp the hits (cache.py:73-74) and keep the stamp histogram (resident
+// slots per last_used value, after the counters) current: a hit moves its
+// slot from bin old to bin pass_no.  Per-CTA shared-memory bins, one global
+// update per touched bin.  Passes past kHistBins use the full recount.
 __global__ void k_cache_stamp(const uint32_t *ids, const uint32_t *d_n, int64_t n_max, const int32_t *slot_of_block,
-                              int32_t *last_used, int32_t pass_no, uint32_t *hist_zero, int n_zero) {
-    if (blockIdx.x == 0)  // the stamp histogram queued after this kernel accumulates into zeroed bins
-        for (int b = threadIdx.x; b < n_zero; b += blockDim.x) hist_zero[b] = 0;
+                              int32_t *last_used, int32_t pass_no, uint32_t *hist) {
+    __shared__ int32_t sh[kHistBins];
+    const bool keep = pass_no < kHistBins;
+    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
     const int64_t n = min(n_max, (int64_t)*d_n);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t s = slot_of_block[ids[i]];
-        if (s >= 0) last_used[s] = pass_no;  // cache.py:73-74
+        if (s < 0) continue;
+        const int32_t old = last_used[s];
+        if (old == pass_no) continue;
+        last_used[s] = pass_no;
+        if (keep) atomicSub(&sh[old], 1);
     }
+    __syncthreads();
+    if (!keep) return;
+    int32_t moved = 0;
+    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x)
+        if (sh[b]) {
+            atomicAdd(&hist[b], (uint32_t)sh[b]);  // two's complement: subtracts
+            moved -= sh[b];
+        }
+    // hits moved into bin pass_no (block-wide sum of the subtractions)
+    for (int o = 16; o > 0; o >>= 1) moved += __shfl_xor_sync(0xffffffffu, moved, o);
+    if ((threadIdx.x & 31) == 0 && moved) atomicAdd(&hist[pass_no], (uint32_t)moved);
 }
 
 // eviction candidates (resident, stamp < pass_no) per stamp value
@@ -1501,13 +1519,14 @@ __global__ void k_frame_start(uint32_t *ctl, int64_t n, int speculation, int max
     ctl[C_CAP] = (uint32_t)cap;
     ctl[C_PHYS] = ctl[C_PHYS_OLD] = (uint32_t)phys;
     ctl[C_HW] = ctl[C_HW_NEXT] = 0;
+    for (int b = 0; b < kHistBins; b++) ctl[C_COUNT + b] = 0;  // the cache is empty: no stamps
 }
 
 // cache.py:66-96 decisions of ensure_resident once the hits are stamped and
 // the misses listed: growth to ceil(1.5 * needed), free suffix, number of
 // victims and the last stamp bucket they reach (from the stamp histogram)
-__global__ void k_cache_plan(uint32_t *ctl, const uint32_t *hist, int32_t pass_no, int64_t n_blocks,
-                             int64_t slot_alloc, int64_t nwords) {
+__global__ void k_cache_plan(uint32_t *ctl, uint32_t *hist, int32_t pass_no, int64_t n_blocks, int64_t slot_alloc,
+                             int64_t nwords, bool maintain) {
     const int64_t nactb = ctl[C_NACTB], n_miss = ctl[C_NMISS], hw = ctl[C_HW];
     int64_t cap = ctl[C_CAP], phys = ctl[C_PHYS];
     ctl[C_PHYS_OLD] = (uint32_t)phys;
@@ -1537,6 +1556,15 @@ __global__ void k_cache_plan(uint32_t *ctl, const uint32_t *hist, int32_t pass_n
     }
     ctl[C_NEVICT] = (uint32_t)n_evict;
     ctl[C_LSTAR] = lstar;
+    if (maintain) {  // the victims leave their bins (in (last_used, id) order), the misses enter bin pass_no
+        int64_t left = n_evict;
+        for (int L = 0; L < pass_no && left > 0; L++) {
+            const int64_t take = min(left, (int64_t)hist[L]);
+            hist[L] -= (uint32_t)take;
+            left -= take;
+        }
+        hist[pass_no] += (uint32_t)n_miss;
+    }
 }
 
 // maps of the slots the growth just brought into use (cache.py:42-53)
@@ -2021,15 +2049,10 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     // cache.ensure_resident (cache.py:66-111): stamp hits, list misses
     // (ascending), then growth / victims / decode, all sized on the device
     const int64_t nmax = active_ids.n - 1;  // upper bound of the active-block count
-    const bool hist = p >= 1 && stamp + 1 <= kHistBins;
+    const bool hist = stamp < kHistBins;  // the histogram after the counters is kept current by the passes
     k_cache_stamp<<<grid_for(nmax, 256), 256, 0, st>>>(active_ids.p, ctl + C_NACTB, nmax, slot_of_block.p, last_used.p,
-                                                      stamp, ctl + C_COUNT, hist ? stamp + 1 : 0);
+                                                      stamp, ctl + C_COUNT);
     WC_LAUNCH_CHECK();
-    if (hist) {
-        k_stamp_hist<<<grid_for(slot_alloc, 256), 256, 4 * (size_t)stamp, st>>>(block_of_slot.p, last_used.p, ctl,
-                                                                               stamp, ctl + C_COUNT);
-        WC_LAUNCH_CHECK();
-    }
     // misses in ascending id order (cache.py:76-78), scan and compaction in one pass
     compact_dev(PredMiss{active_ids.p, slot_of_block.p}, active_ids.p, ctl + C_NACTB, nmax, miss_ids.p,
                 ctl + C_NMISS, partials.p, st);
@@ -2046,7 +2069,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
         }
     }
     k_cache_plan<<<1, 1, 0, st>>>(ctl, p >= 1 && !hist ? stamp_hist.p : ctl + C_COUNT, stamp, vol->n_blocks,
-                                 slot_alloc, nwords);
+                                 slot_alloc, nwords, hist);
     WC_LAUNCH_CHECK();
     k_phys_init<<<grid_for(slot_alloc, 256), 256, 0, st>>>(ctl, block_of_slot.p, last_used.p);
     WC_LAUNCH_CHECK();

@@ -120,27 +120,38 @@ void radix_sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int nbits, Radi
 
 // ----------------------------------------------------------- bitmap extract
 
+// A thread owns kDenseQ16 16-byte groups (up to 32 words): all loads are
+// issued before any is used and the words stay in registers for the id pass.
+constexpr int kDenseQ16 = 8;
 template <bool kClear>
-__global__ void __launch_bounds__(256) k_bitmap_dense(uint32_t *__restrict__ bm, int64_t nwords, int k4,
+__global__ void __launch_bounds__(256) k_bitmap_dense(uint32_t *__restrict__ bm, int64_t nwords, int q16,
                                                       uint32_t *__restrict__ word_offsets, uint32_t *__restrict__ ids,
                                                       uint64_t *status, ScanEpoch ep, uint32_t *d_count) {
     __shared__ uint32_t sw[32];
     __shared__ uint32_t s_excl;
     const uint32_t epoch = resolve_epoch(ep);
-    const int64_t chunk = 256LL * k4;
+    const int64_t chunk = 256LL * 4 * q16;
     const int64_t t = blockIdx.x;
     const int64_t last = (nwords - 1) / chunk;
-    const int64_t w0 = t * chunk + (int64_t)threadIdx.x * k4;
-    const int64_t w1 = min(nwords, w0 + k4);
+    const int64_t w0 = t * chunk + (int64_t)threadIdx.x * 4 * q16;
+    uint4 q[kDenseQ16];
     uint32_t cnt = 0;
-    for (int64_t w = w0; w < w1; w += 4) {
-        if (w + 4 <= w1) {
-            const uint4 q = *reinterpret_cast<const uint4 *>(bm + w);
-            cnt += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
-        } else {
-            for (int64_t x = w; x < w1; x++) cnt += __popc(bm[x]);
+#pragma unroll
+    for (int j = 0; j < kDenseQ16; j++) {
+        const int64_t w = w0 + 4 * j;
+        q[j] = make_uint4(0u, 0u, 0u, 0u);
+        if (j < q16) {
+            if (w + 4 <= nwords) {
+                q[j] = *reinterpret_cast<const uint4 *>(bm + w);
+            } else {
+                if (w < nwords) q[j].x = bm[w];
+                if (w + 1 < nwords) q[j].y = bm[w + 1];
+                if (w + 2 < nwords) q[j].z = bm[w + 2];
+            }
         }
     }
+#pragma unroll
+    for (int j = 0; j < kDenseQ16; j++) cnt += __popc(q[j].x) + __popc(q[j].y) + __popc(q[j].z) + __popc(q[j].w);
     uint32_t agg;
     uint32_t pre = block_exclusive_scan(cnt, sw, &agg);
     if (threadIdx.x < 32) {
@@ -153,15 +164,21 @@ __global__ void __launch_bounds__(256) k_bitmap_dense(uint32_t *__restrict__ bm,
     __syncthreads();
     pre += s_excl;
     if (!cnt) return;
-    for (int64_t w = w0; w < w1; w++) {
-        uint32_t v = bm[w];
-        if (!v) continue;
-        if (word_offsets) word_offsets[w] = pre;
-        if (kClear) bm[w] = 0u;
-        const uint32_t base = (uint32_t)(w * 32);
-        while (v) {
-            ids[pre++] = base + __ffs(v) - 1;
-            v &= v - 1;
+#pragma unroll
+    for (int j = 0; j < kDenseQ16; j++) {
+        const uint32_t wv[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            uint32_t v = wv[c];
+            if (!v) continue;
+            const int64_t w = w0 + 4 * j + c;
+            if (word_offsets) word_offsets[w] = pre;
+            if (kClear) bm[w] = 0u;
+            const uint32_t base = (uint32_t)(w * 32);
+            while (v) {
+                ids[pre++] = base + __ffs(v) - 1;
+                v &= v - 1;
+            }
         }
     }
 }
@@ -172,14 +189,15 @@ void bitmap_extract_dense(uint32_t *bm, int64_t nwords, uint32_t *word_offsets, 
         WC_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st));
         return;
     }
-    // one wave of 4 CTAs per SM; at least 4 words (one 16 B load) per thread
-    const int64_t k4 = std::max<int64_t>(4, ceil_div(ceil_div(nwords, (int64_t)kNumSMs * 4 * 256), 4) * 4);
-    const unsigned grid = (unsigned)ceil_div(nwords, 256 * k4);
+    // about one wave of 4 CTAs per SM, 1..kDenseQ16 16-byte groups per thread
+    // (larger bitmaps launch more waves)
+    const int64_t q16 = std::min<int64_t>(kDenseQ16, std::max<int64_t>(1, ceil_div(nwords, (int64_t)kNumSMs * 4 * 256 * 4)));
+    const unsigned grid = (unsigned)ceil_div(nwords, 256 * 4 * q16);
     if (clear)
-        k_bitmap_dense<true><<<grid, 256, 0, st>>>(bm, nwords, (int)k4, word_offsets, ids,
+        k_bitmap_dense<true><<<grid, 256, 0, st>>>(bm, nwords, (int)q16, word_offsets, ids,
                                                   reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
     else
-        k_bitmap_dense<false><<<grid, 256, 0, st>>>(bm, nwords, (int)k4, word_offsets, ids,
+        k_bitmap_dense<false><<<grid, 256, 0, st>>>(bm, nwords, (int)q16, word_offsets, ids,
                                                    reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
     WC_LAUNCH_CHECK();
 }
