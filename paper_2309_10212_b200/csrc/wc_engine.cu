@@ -293,7 +293,7 @@ constexpr int kFineRun = 10;  // a monotone ray visits at most 4+4+4-2 fine cell
 #endif
 
 // bit of fine cell f in its coarse cell's iso mask (k_iso_cell_mask)
-__device__ __forceinline__ int fine_local(const Dda &f) { return (f.cx & 3) + 4 * (f.cy & 3) + 16 * (f.cz & 3); }
+__device__ __forceinline__ int fine_local(const Dda &f) { return 16 * (f.cx & 3) + (f.cy & 3) + 4 * (f.cz & 3); }
 
 // traversal.py:217-403 _traverse_kernel, restructured for latency on B200:
 //  * persistent: a lane that finishes its ray fetches the next active ray
@@ -734,7 +734,7 @@ __global__ void k_iso_bitmap(const double2 *__restrict__ mm, int64_t n, double i
 // different bucket than iso decides its comparison; a shared bucket re-reads
 // the exact float64 bound.  Reads 4 B per block instead of 16.
 //
-// Laid out per coarse cell: cell_mask[c] bit (fx&3) + 4*(fy&3) + 16*(fz&3)
+// Laid out per coarse cell: cell_mask[c] bit 16*(fx&3) + (fy&3) + 4*(fz&3)
 // is the test of fine cell f inside coarse cell c (fine cells past the grid
 // edge read 0).  A ray descending into c loads this one word and walks its
 // whole fine run (<= 10 cells) from registers.
@@ -752,8 +752,9 @@ __global__ void k_iso_cell_mask(const ushort2 *__restrict__ q, const double2 *__
                                 int cdz, double iso, double base, double inv,
                                 unsigned long long *__restrict__ cell_mask, int64_t c_begin, int64_t c_end) {
     // Streams the bricked screening copy: 16 lanes cover one coarse cell's
-    // 256 B (lane: 4 fine cells = one x-row), 4 cells per lane in flight; the
-    // 16 nibbles of a cell are OR-ed with shuffles.
+    // 256 B (lane: 4 fine cells = one x-row), 4 cells per lane in flight.
+    // One ballot per x position collects the 16 rows of both half-warps'
+    // cells: bits [16x, 16x + 16) of a cell's mask.
     constexpr int kU = 4;
     const int64_t n_coarse = min((int64_t)cdx * cdy * cdz, c_end);  // cells [c_begin, c_end): c_begin % 8 == 0
     const bool iso_nan = iso != iso;
@@ -773,26 +774,24 @@ __global__ void k_iso_cell_mask(const ushort2 *__restrict__ q, const double2 *__
 #pragma unroll
         for (int u = 0; u < kU; u++) {
             const int64_t c = c0 + 2 * u + half;
+            const uint32_t ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
             unsigned long long m = 0;
-            if (on[u]) {
-                const uint32_t ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
 #pragma unroll
-                for (int x = 0; x < 4; x++) {
-                    const ushort2 v = *reinterpret_cast<const ushort2 *>(&ws[x]);
-                    bool in = qi > v.x && qi < v.y;  // decided by the buckets (the common case)
-                    if (qi == v.x || qi == v.y) {    // shared bucket: exact float64 test (rare)
-                        const uint32_t cu = (uint32_t)c;
-                        const int fx = 4 * (int)(cu % (uint32_t)cdx) + x;
-                        const int fy = 4 * (int)((cu / (uint32_t)cdx) % (uint32_t)cdy) + (row & 3);
-                        const int fz = 4 * (int)(cu / ((uint32_t)cdx * (uint32_t)cdy)) + (row >> 2);
-                        in = fx < fdx && fy < fdy && fz < fdz &&
-                             iso_in_q(v, qi, mm, fx + (int64_t)fdx * (fy + (int64_t)fdy * fz), iso);
-                    }
-                    if (in) m |= 1ull << (x + 4 * row);
+            for (int x = 0; x < 4; x++) {
+                const uint32_t lo = ws[x] & 0xFFFFu, hi = ws[x] >> 16;
+                bool in = on[u] && qi > lo && qi < hi;  // decided by the buckets (the common case)
+                if (on[u] && (qi == lo || qi == hi)) {  // shared bucket: exact float64 test (rare)
+                    const uint32_t cu = (uint32_t)c;
+                    const int fx = 4 * (int)(cu % (uint32_t)cdx) + x;
+                    const int fy = 4 * (int)((cu / (uint32_t)cdx) % (uint32_t)cdy) + (row & 3);
+                    const int fz = 4 * (int)(cu / ((uint32_t)cdx * (uint32_t)cdy)) + (row >> 2);
+                    in = fx < fdx && fy < fdy && fz < fdz &&
+                         iso_in_q(make_ushort2((unsigned short)lo, (unsigned short)hi), qi, mm,
+                                  fx + (int64_t)fdx * (fy + (int64_t)fdy * fz), iso);
                 }
+                const uint32_t b = __ballot_sync(0xffffffffu, in);
+                m |= (unsigned long long)((b >> (16 * half)) & 0xFFFFu) << (16 * x);
             }
-#pragma unroll
-            for (int o = 1; o < 16; o <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
             if (row == 0 && c < n_coarse) cell_mask[c] = m;
         }
     }
@@ -1634,6 +1633,8 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     : vol(v), n(n_rays), iso(iso_), speculation(speculation_), max_spec(max_spec_), corrupt(corrupt_) {
     if (n < 1) throw UsageError("a session needs at least one ray");
     WC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    WC_CUDA(cudaStreamCreateWithFlags(&st_side, cudaStreamNonBlocking));
+    WC_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
     uniform_origin = dirs == nullptr;
     dir.alloc(n * 3);
     if (!uniform_origin) origin.alloc(n * 3);
@@ -1750,14 +1751,21 @@ void Session::reset_part(const CameraParams *cam, double iso_, int64_t part, int
     mask_buffers(parts, chunk);
     mask_part(vol->n_coarse, part, parts, w0, w1, chunk);
     const int64_t c_end = std::min<int64_t>(vol->n_coarse, 32 * w1);
-    if (w1 > w0) {
-        k_iso_bitmap<<<grid_for((w1 - w0) * 32, 256, 8), 256, 0, st>>>(vol->coarse_mm.p, vol->n_coarse, iso,
-                                                                      coarse_bm.p, w0, w1);
+    // The per-iso range tests run on a side stream, overlapped with the ray
+    // and cache setup below (they depend on neither); joined before the
+    // reset ends.  The fork follows ev_frame0, i.e. the previous frame's
+    // passes that read the old tests.
+    const bool masks = w1 > w0;
+    if (masks) {
+        WC_CUDA(cudaStreamWaitEvent(st_side, ev_frame0, 0));
+        k_iso_bitmap<<<grid_for((w1 - w0) * 32, 256, 8), 256, 0, st_side>>>(vol->coarse_mm.p, vol->n_coarse, iso,
+                                                                           coarse_bm.p, w0, w1);
         WC_LAUNCH_CHECK();
-        k_iso_cell_mask<<<grid_for((c_end - 32 * w0) * 16, 256, 8), 256, 0, st>>>(
+        k_iso_cell_mask<<<grid_for((c_end - 32 * w0) * 16, 256, 8), 256, 0, st_side>>>(
             vol->fine_q.p, vol->fine_mm.p, coarse_bm.p, vol->bdx, vol->bdy, vol->bdz, vol->cdx, vol->cdy, vol->cdz,
             iso, vol->q_base, vol->q_inv, cell_mask.p, 32 * w0, c_end);
         WC_LAUNCH_CHECK();
+        WC_CUDA(cudaEventRecord(ev_side, st_side));
     }
     RayInitArgs a{};
     a.cam = cam_params;
@@ -1804,6 +1812,7 @@ void Session::reset_part(const CameraParams *cam, double iso_, int64_t part, int
     graph_ms = 0.0;
     for (auto &p : pass_stage_ms)
         for (double &m : p) m = 0.0;
+    if (masks) WC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
     WC_CUDA(cudaEventRecord(ev_reset_end, st));
 }
 
@@ -1828,6 +1837,11 @@ Session::~Session() {
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
     }
+    if (st_side) {
+        cudaStreamSynchronize(st_side);
+        cudaStreamDestroy(st_side);
+    }
+    if (ev_side) cudaEventDestroy(ev_side);
     if (st_copy) {
         cudaStreamSynchronize(st_copy);
         cudaStreamDestroy(st_copy);

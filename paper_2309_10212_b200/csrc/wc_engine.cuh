@@ -117,6 +117,8 @@ struct Session {
     PinnedBuf<uint32_t> h_counters;
     RadixScratch rs;
     cudaEvent_t ev_frame0 = nullptr, ev_reset_end = nullptr;
+    cudaStream_t st_side = nullptr;  // reset: per-iso range tests overlapped with the ray setup
+    cudaEvent_t ev_side = nullptr;
     static constexpr int kStages = 6;  // traverse, mark, cache, group, raytrace, composite
     double stage_ms[kStages] = {};
     static constexpr int kMaxPassLog = 128;
