@@ -51,6 +51,7 @@ struct RayInitArgs {
 __global__ void k_init_rays(RayInitArgs a, int64_t n, double *origin_out, double *dir, double *t_enter, double *t_exit,
                             uint8_t *status, uint8_t *exited, uint32_t *coarse_cell, uint32_t *fine_cell,
                             double *coarse_tmax, double *fine_tmax, uint32_t *rgba, float *depth) {
+    pdl_wait();
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
         double o[3], d[3];
         if (a.dir_in) {
@@ -158,7 +159,7 @@ void init_rays_device(const CameraParams *cam, const uint32_t *d_pixel_ids, int6
     a.nx = nx;
     a.ny = ny;
     a.nz = nz;
-    k_init_rays<<<grid_for(n, 256), 256, 0, st>>>(a, n, d_origin_out, d_dir, t_enter, t_exit, status, exited,
+    launch_pdl(k_init_rays, grid_for(n, 256), 256, 0, st, a, n, d_origin_out, d_dir, t_enter, t_exit, status, exited,
                                                   coarse_cell, fine_cell, coarse_tmax, fine_tmax, nullptr, nullptr);
     WC_LAUNCH_CHECK();
 }
@@ -177,6 +178,7 @@ struct PredMiss {  // active block not resident (cache.py:69-72)
 
 template <class Pred>
 __global__ void k_compact_index(Pred pred, int64_t n, const uint32_t *off, uint32_t *out) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         if (pred(i)) out[off[i]] = (uint32_t)i;
 }
@@ -311,6 +313,7 @@ __device__ __forceinline__ int fine_local(const Dda &f) { return 16 * (f.cx & 3)
 // for bit.
 template <int CA>
 __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(TraverseArgs a_in) {
+    pdl_wait();
     TraverseArgs a = a_in;
     a.n_act = a.ctl[C_NACT];
     a.n_spec = (int)a.ctl[C_NSPEC];
@@ -522,6 +525,7 @@ __device__ __forceinline__ Dda shfl_dda(const Dda &s, int src) {
 // where the ray leaves.  The lane that simulated exactly that many steps
 // holds the reference's iterator state and shuffles it to the warp.
 __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a_in) {
+    pdl_wait();
     TraverseArgs a = a_in;
     a.n_act = a.ctl[C_NACT];
     a.n_spec = (int)a.ctl[C_NSPEC];
@@ -715,6 +719,7 @@ __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a_in) {
 // chain costs an L2 hit instead of a DRAM read of the 2 GB float64 grid.
 __global__ void k_iso_bitmap(const double2 *__restrict__ mm, int64_t n, double iso, uint32_t *__restrict__ bm,
                              int64_t w_begin, int64_t w_end) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t nwords = min((n + 31) >> 5, w_end);
     for (int64_t w = w_begin + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w < nwords;
@@ -751,6 +756,7 @@ __global__ void k_iso_cell_mask(const ushort2 *__restrict__ q, const double2 *__
                                 const uint32_t *__restrict__ coarse_bm, int fdx, int fdy, int fdz, int cdx, int cdy,
                                 int cdz, double iso, double base, double inv,
                                 unsigned long long *__restrict__ cell_mask, int64_t c_begin, int64_t c_end) {
+    pdl_wait();
     // Streams the bricked screening copy: 16 lanes cover one coarse cell's
     // 256 B (lane: 4 fine cells = one x-row), 4 cells per lane in flight.
     // One ballot per x position collects the 16 rows of both half-warps'
@@ -803,6 +809,7 @@ __global__ void k_iso_cell_mask(const ushort2 *__restrict__ q, const double2 *__
 // +octant neighbours.  Count-driven (reads *d_nvis) so no host round trip.
 __global__ void k_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvis, int bdx, int bdy, int bdz,
                               uint32_t *act_bm) {
+    pdl_wait();
     const int64_t nvis = *d_nvis;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nvis * 8; t += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t b = visible_ids[t >> 3];
@@ -823,6 +830,7 @@ __global__ void k_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvi
 // per visible block.
 __global__ void k_mark_active_words(const uint32_t *visible_ids, const uint32_t *d_nvis, const uint32_t *vis_bm,
                                     int wx_words, int bdy, int bdz, uint32_t *act_bm) {
+    pdl_wait();
     const int64_t nvis = *d_nvis;
     const uint32_t plane = (uint32_t)wx_words * (uint32_t)bdy;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvis; i += (int64_t)gridDim.x * blockDim.x) {
@@ -851,6 +859,7 @@ __global__ void k_build_entries(const uint32_t *ctl, const uint32_t *act_list, c
                                 const uint32_t *entry_off, const uint32_t *block_slots, const uint32_t *vis_bm,
                                 const uint32_t *vis_word_off, uint32_t *ent_key, uint32_t *ent_val, uint32_t *ent_ray,
                                 uint32_t *ent_blk) {
+    pdl_wait();
     // thread per slot (i, j): no per-ray serial chain of rank lookups
     const int64_t n_act = ctl[C_NACT], n_spec = ctl[C_NSPEC];
     const int64_t n_slots = n_act * n_spec;
@@ -870,6 +879,7 @@ __global__ void k_build_entries(const uint32_t *ctl, const uint32_t *act_list, c
 
 // Run starts of the sorted keys -> block_ray_offsets (engine.py:133-139).
 __global__ void k_run_offsets(const uint32_t *key, int64_t n, int64_t nvis, uint32_t *off) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         if (i == 0 || key[i] != key[i - 1]) off[key[i]] = (uint32_t)i;
         if (i == 0) off[nvis] = (uint32_t)n;
@@ -884,6 +894,7 @@ __global__ void k_run_offsets(const uint32_t *key, int64_t n, int64_t nvis, uint
 // update per touched bin.  Passes past kHistBins use the full recount.
 __global__ void k_cache_stamp(const uint32_t *ids, const uint32_t *d_n, int64_t n_max, const int32_t *slot_of_block,
                               int32_t *last_used, int32_t pass_no, uint32_t *hist) {
+    pdl_wait();
     __shared__ int32_t sh[kHistBins];
     const bool keep = pass_no < kHistBins;
     for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) sh[b] = 0;
@@ -914,6 +925,7 @@ __global__ void k_cache_stamp(const uint32_t *ids, const uint32_t *d_n, int64_t 
 // (few distinct stamps: per-CTA shared-memory bins, one global add per bin)
 __global__ void k_stamp_hist(const int32_t *block_of_slot, const int32_t *last_used, const uint32_t *ctl,
                              int32_t pass_no, uint32_t *hist) {
+    pdl_wait();
     extern __shared__ uint32_t sh[];
     const int64_t hw = ctl[C_NACT] ? ctl[C_HW] : 0;
     for (int b = threadIdx.x; b < pass_no; b += blockDim.x) sh[b] = 0;
@@ -941,6 +953,7 @@ __global__ void k_stamp_hist(const int32_t *block_of_slot, const int32_t *last_u
 // them in (last_used, block_id) order (cache.py:84-91).
 __global__ void k_mark_victims(const int32_t *block_of_slot, const int32_t *last_used, const uint32_t *ctl,
                                int32_t pass_no, int64_t nwords, uint32_t *regions, uint32_t *summary) {
+    pdl_wait();
     if (ctl[C_NEVICT] == 0) return;
     const int64_t hw = ctl[C_HW];
     const int32_t lstar = (int32_t)ctl[C_LSTAR];
@@ -954,6 +967,7 @@ __global__ void k_mark_victims(const int32_t *block_of_slot, const int32_t *last
 
 __global__ void k_blocks_to_slots(const uint32_t *blocks, const uint32_t *d_n, const int32_t *slot_of_block,
                                   uint32_t *slots) {
+    pdl_wait();
     const int64_t n = *d_n;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         slots[i] = (uint32_t)slot_of_block[blocks[i]];
@@ -961,6 +975,7 @@ __global__ void k_blocks_to_slots(const uint32_t *blocks, const uint32_t *d_n, c
 
 // BlockCache reset: forget every resident block of the previous frame
 __global__ void k_cache_unmap(const int32_t *block_of_slot, const uint32_t *d_phys, int32_t *slot_of_block) {
+    pdl_wait();
     const int64_t phys = *d_phys;
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < phys; s += (int64_t)gridDim.x * blockDim.x) {
         const int32_t b = block_of_slot[s];
@@ -972,6 +987,7 @@ __global__ void k_cache_unmap(const int32_t *block_of_slot, const uint32_t *d_ph
 // slots of the last n_evict misses, cache.py:96-97)
 __global__ void k_evict(const uint32_t *victims, const uint32_t *d_n_evict, int32_t *block_of_slot,
                         int32_t *slot_of_block) {
+    pdl_wait();
     const int64_t n_evict = *d_n_evict;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_evict; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t s = victims[i];
@@ -994,6 +1010,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4)
     k_decode_insert(const uint8_t *__restrict__ payload, int qbits, int stride, const uint32_t *__restrict__ miss_ids,
                     uint32_t *ctl, const uint32_t *__restrict__ victims, float *__restrict__ slot_values,
                     int32_t *block_of_slot, int32_t *last_used, int32_t *slot_of_block, int32_t pass_no) {
+    pdl_wait();
     __shared__ uint32_t stage[kDecWarps][kDecRec][kDecWords];
     const int lane = threadIdx.x & 31;
     uint32_t(*sw)[kDecWords] = stage[threadIdx.x >> 5];
@@ -1121,6 +1138,7 @@ struct DenseFieldView {  // fully decoded volume, x-fastest
 // read by k_build_entries): every visible id zeroes its word.
 __global__ void k_contrib(const uint32_t *visible_ids, const uint32_t *d_nvis, const int32_t *slot_of_block, int bdx,
                           int bdy, int bdz, int4 *contrib, uint32_t *err, uint32_t *vis_bm) {
+    pdl_wait();
     const int64_t nvis = *d_nvis;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvis; v += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t b = visible_ids[v];
@@ -1160,6 +1178,7 @@ struct RaytraceArgs {
 // tracer (blocktrace.py:317-449) over the block's <= 4^3 dual cells and
 // writes (rgb, z) -- or (0, 0, 0, +inf) on a miss -- at its entry id.
 __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_raytrace(RaytraceArgs a) {
+    pdl_wait();
     a.rays.bind();
     const int64_t n_ent = *a.d_n_ent;
     const double iso = a.fp[3], br = a.fp[4], bg = a.fp[5], bb = a.fp[6];
@@ -1231,6 +1250,7 @@ __device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, const RayVi
 
 // phase 1: walk each entry's dual cells, list the bracketing ones
 __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
+    pdl_wait();
     const RaytraceArgs &a = s.a;
     RayView rv = a.rays;
     rv.bind();
@@ -1299,6 +1319,7 @@ __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
 // phase 2: one thread per candidate cell; the earliest cell (in DDA order)
 // with a root wins through an atomicMin on (seq, item)
 __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArgs s) {
+    pdl_wait();
     const RaytraceArgs &a = s.a;
     RayView rv = a.rays;
     rv.bind();
@@ -1324,6 +1345,7 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArg
 
 // phase 3: shade each entry's winning cell (or record the miss)
 __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
+    pdl_wait();
     const RaytraceArgs &a = s.a;
     RayView rv = a.rays;
     rv.bind();
@@ -1359,6 +1381,7 @@ __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
 __global__ void k_composite(const uint32_t *ctl, const uint32_t *act_list, const uint32_t *emitted,
                             const uint32_t *entry_off, const float4 *rgbz, const uint8_t *exited, uint8_t *status,
                             uint32_t *rgba, float *depth, uint32_t *keep) {
+    pdl_wait();
     const int64_t n_act = ctl[C_NACT];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_act; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t r = act_list[i], ne = emitted[i], eo = entry_off[i];
@@ -1391,6 +1414,7 @@ __global__ void k_composite(const uint32_t *ctl, const uint32_t *act_list, const
 __global__ void k_composite_warp(const uint32_t *ctl, const uint32_t *act_list, const uint32_t *emitted,
                                  const uint32_t *entry_off, const float4 *rgbz, const uint8_t *exited, uint8_t *status,
                                  uint32_t *rgba, float *depth, uint32_t *keep) {
+    pdl_wait();
     const int64_t n_act = ctl[C_NACT];
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1438,6 +1462,7 @@ __global__ void __launch_bounds__(128) k_reference_render(const float *values, i
                                                           const double *origin, const double *dir, int64_t n,
                                                           double iso, double br, double bg, double bb, uint32_t *rgba,
                                                           float *depth) {
+    pdl_wait();
     const DenseFieldView field{values, nx, (int64_t)nx * ny};
     const double hi[3] = {(double)nx - 1.0, (double)ny - 1.0, (double)nz - 1.0};
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
@@ -1482,7 +1507,7 @@ void reference_render_device(const float *d_values, int nx, int ny, int nz, cons
                              const double *d_dir, int64_t n, double iso, double br, double bg, double bb,
                              uint32_t *d_rgba, float *d_depth, cudaStream_t st) {
     if (n <= 0) return;
-    k_reference_render<<<grid_for(n, 128, 16), 128, 0, st>>>(d_values, nx, ny, nz, d_origin, d_dir, n, iso, br, bg,
+    launch_pdl(k_reference_render, grid_for(n, 128, 16), 128, 0, st, d_values, nx, ny, nz, d_origin, d_dir, n, iso, br, bg,
                                                              bb, d_rgba, d_depth);
     WC_LAUNCH_CHECK();
 }
@@ -1503,6 +1528,7 @@ __device__ __forceinline__ int64_t n_spec_of(int64_t n, int64_t n_act, int specu
 __global__ void k_frame_start(uint32_t *ctl, int64_t n, int speculation, int max_spec, int64_t cap, int64_t phys,
                               int64_t nwords, uint32_t frame, double *fp, double ex, double ey, double ez, double iso,
                               double br, double bg, double bb) {
+    pdl_wait();
     // FrameParams: what changes between frames lives in device memory, so the
     // captured pass graphs are frame-invariant
     fp[0] = ex;
@@ -1526,6 +1552,7 @@ __global__ void k_frame_start(uint32_t *ctl, int64_t n, int speculation, int max
 // victims and the last stamp bucket they reach (from the stamp histogram)
 __global__ void k_cache_plan(uint32_t *ctl, uint32_t *hist, int32_t pass_no, int64_t n_blocks, int64_t slot_alloc,
                              int64_t nwords, bool maintain) {
+    pdl_wait();
     const int64_t nactb = ctl[C_NACTB], n_miss = ctl[C_NMISS], hw = ctl[C_HW];
     int64_t cap = ctl[C_CAP], phys = ctl[C_PHYS];
     ctl[C_PHYS_OLD] = (uint32_t)phys;
@@ -1568,6 +1595,7 @@ __global__ void k_cache_plan(uint32_t *ctl, uint32_t *hist, int32_t pass_no, int
 
 // maps of the slots the growth just brought into use (cache.py:42-53)
 __global__ void k_phys_init(const uint32_t *ctl, int32_t *block_of_slot, int32_t *last_used) {
+    pdl_wait();
     const int64_t lo = ctl[C_PHYS_OLD], hi = ctl[C_PHYS];
     for (int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < hi; s += (int64_t)gridDim.x * blockDim.x) {
         block_of_slot[s] = -1;
@@ -1578,6 +1606,7 @@ __global__ void k_phys_init(const uint32_t *ctl, int32_t *block_of_slot, int32_t
 // end of pass: the PassStats record, then the next pass's n_act / n_spec
 // (engine.py:331-333, slot budget engine.py:341)
 __global__ void k_pass_end(uint32_t *ctl, uint32_t *row, int64_t n, int speculation, int max_spec, int64_t nwords) {
+    pdl_wait();
     const int64_t n_act = ctl[C_NACT], n_after = ctl[C_NACT_NEXT];
     row[L_NACT] = (uint32_t)n_act;
     row[L_NSPEC] = ctl[C_NSPEC];
@@ -1603,6 +1632,7 @@ __global__ void k_pass_end(uint32_t *ctl, uint32_t *row, int64_t n, int speculat
 
 // rays still active after the snapshot pass (their pixels may still change)
 __global__ void k_snapshot_list(uint32_t *ctl, const uint32_t *act, uint32_t *snap) {
+    pdl_wait();
     const int64_t n = ctl[C_NACT];
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl[C_NSNAP] = (uint32_t)n;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -1612,6 +1642,7 @@ __global__ void k_snapshot_list(uint32_t *ctl, const uint32_t *act, uint32_t *sn
 // their final pixels: (ray, rgba, depth bits)
 __global__ void k_gather_patch(const uint32_t *ctl, const uint32_t *snap, const uint32_t *rgba, const float *depth,
                                uint4 *patch) {
+    pdl_wait();
     const int64_t n = ctl[C_NSNAP];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t r = snap[i];
@@ -1758,10 +1789,10 @@ void Session::reset_part(const CameraParams *cam, double iso_, int64_t part, int
     const bool masks = w1 > w0;
     if (masks) {
         WC_CUDA(cudaStreamWaitEvent(st_side, ev_frame0, 0));
-        k_iso_bitmap<<<grid_for((w1 - w0) * 32, 256, 8), 256, 0, st_side>>>(vol->coarse_mm.p, vol->n_coarse, iso,
+        launch_pdl(k_iso_bitmap, grid_for((w1 - w0) * 32, 256, 8), 256, 0, st_side, vol->coarse_mm.p, vol->n_coarse, iso,
                                                                            coarse_bm.p, w0, w1);
         WC_LAUNCH_CHECK();
-        k_iso_cell_mask<<<grid_for((c_end - 32 * w0) * 16, 256, 8), 256, 0, st_side>>>(
+        launch_pdl(k_iso_cell_mask, grid_for((c_end - 32 * w0) * 16, 256, 8), 256, 0, st_side, 
             vol->fine_q.p, vol->fine_mm.p, coarse_bm.p, vol->bdx, vol->bdy, vol->bdz, vol->cdx, vol->cdy, vol->cdz,
             iso, vol->q_base, vol->q_inv, cell_mask.p, 32 * w0, c_end);
         WC_LAUNCH_CHECK();
@@ -1775,14 +1806,14 @@ void Session::reset_part(const CameraParams *cam, double iso_, int64_t part, int
     a.nx = vol->nx;
     a.ny = vol->ny;
     a.nz = vol->nz;
-    k_init_rays<<<grid_for(n, 256), 256, 0, st>>>(a, n, nullptr, dir.p, t_enter.p, t_exit.p, status.p, exited.p,
+    launch_pdl(k_init_rays, grid_for(n, 256), 256, 0, st, a, n, nullptr, dir.p, t_enter.p, t_exit.p, status.p, exited.p,
                                                   coarse_cell.p, fine_cell.p, coarse_tmax.p, fine_tmax.p, rgba.p,
                                                   depth.p);
     WC_LAUNCH_CHECK();
     // cache (cache.py:27-40, initial_capacity :122-125 with w*h == n):
     // unmap whatever the previous frame left resident (its slot count is
     // still in the control block)
-    k_cache_unmap<<<grid_for(slot_alloc, 256), 256, 0, st>>>(block_of_slot.p, counters.p + C_PHYS, slot_of_block.p);
+    launch_pdl(k_cache_unmap, grid_for(slot_alloc, 256), 256, 0, st, block_of_slot.p, counters.p + C_PHYS, slot_of_block.p);
     WC_LAUNCH_CHECK();
     cap = std::max<int64_t>(1, init_cap <= 0 ? std::max<int64_t>(1024, 2 * n / 64) : init_cap);
     phys = std::min<int64_t>(cap, vol->n_blocks);
@@ -1796,11 +1827,11 @@ void Session::reset_part(const CameraParams *cam, double iso_, int64_t part, int
     WC_CUDA(cudaMemsetAsync(counters.p, 0, 4 * C_COUNT, st));
     PredActive pa{status.p};
     scan_exclusive(pa, n, entry_off.p, counters.p + C_NACT, partials.p, st);
-    k_compact_index<<<grid_for(n, 256), 256, 0, st>>>(pa, n, entry_off.p, act_list[0].p);
+    launch_pdl(k_compact_index<PredActive>, grid_for(n, 256), 256, 0, st, pa, n, entry_off.p, act_list[0].p);
     WC_LAUNCH_CHECK();
     if ((++frame_no & 0x1FFFFu) == 0)  // device-derived scan epochs wrap: forget old status words
         WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
-    k_frame_start<<<1, 1, 0, st>>>(counters.p, n, speculation, max_spec, cap, phys, ceil_div(vol->n_blocks, 32),
+    launch_pdl(k_frame_start, 1, 1, 0, st, counters.p, n, speculation, max_spec, cap, phys, ceil_div(vol->n_blocks, 32),
                                    frame_no, fparams.p, eye[0], eye[1], eye[2], iso, base[0], base[1], base[2]);
     WC_LAUNCH_CHECK();
     pass_no = 0;
@@ -2038,9 +2069,9 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     WC_CUDA(cudaMemsetAsync(ctl + C_WORK, 0, 4, st));
     WC_CUDA(cudaMemsetAsync(ctl + C_NITEMS, 0, 4, st));
     if (nact_guess <= WC_WARP_TRAVERSE_MAX)  // few (long) rays: warp-cooperative DDA per ray
-        k_traverse_warp<<<grid_for(std::max<int64_t>(1, nact_guess) * 32, 128, 16), 128, 0, st>>>(ta);
+        launch_pdl(k_traverse_warp, grid_for(std::max<int64_t>(1, nact_guess) * 32, 128, 16), 128, 0, st, ta);
     else
-        k_traverse<WC_COARSE_AHEAD><<<grid_for(n, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st>>>(ta);
+        launch_pdl(k_traverse<WC_COARSE_AHEAD>, grid_for(n, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st, ta);
     WC_LAUNCH_CHECK();
     mark(1);
     // entry compaction: exclusive scan of per-ray emitted counts
@@ -2049,14 +2080,14 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     // summaries: the cost follows the non-zero bitmap words
     bitmap_extract_dense(vis_bm.p, nwords, vis_word_off.p, visible_ids.p, ctl + C_NVIS, false, partials.p, st);
     if (vol->bdx % 32 == 0)
-        k_mark_active_words<<<grid_for(n, 256), 256, 0, st>>>(visible_ids.p, ctl + C_NVIS, vis_bm.p, vol->bdx / 32,
+        launch_pdl(k_mark_active_words, grid_for(n, 256), 256, 0, st, visible_ids.p, ctl + C_NVIS, vis_bm.p, vol->bdx / 32,
                                                               vol->bdy, vol->bdz, act_bm.p);
     else
-        k_mark_active<<<grid_for((int64_t)8 * n, 256), 256, 0, st>>>(visible_ids.p, ctl + C_NVIS, vol->bdx, vol->bdy,
+        launch_pdl(k_mark_active, grid_for((int64_t)8 * n, 256), 256, 0, st, visible_ids.p, ctl + C_NVIS, vol->bdx, vol->bdy,
                                                                      vol->bdz, act_bm.p);
     WC_LAUNCH_CHECK();
     bitmap_extract_dense(act_bm.p, nwords, nullptr, active_ids.p, ctl + C_NACTB, true, partials.p, st);  // clears act_bm
-    k_build_entries<<<grid_for(n, 256), 256, 0, st>>>(ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p,
+    launch_pdl(k_build_entries, grid_for(n, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p,
                                                       vis_word_off.p, ent_key.p, ent_val.p, ent_ray.p, ent_blk.p);
     WC_LAUNCH_CHECK();  // vis_bm is cleared by k_contrib
 
@@ -2064,7 +2095,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     // (ascending), then growth / victims / decode, all sized on the device
     const int64_t nmax = active_ids.n - 1;  // upper bound of the active-block count
     const bool hist = stamp < kHistBins;  // the histogram after the counters is kept current by the passes
-    k_cache_stamp<<<grid_for(nmax, 256), 256, 0, st>>>(active_ids.p, ctl + C_NACTB, nmax, slot_of_block.p, last_used.p,
+    launch_pdl(k_cache_stamp, grid_for(nmax, 256), 256, 0, st, active_ids.p, ctl + C_NACTB, nmax, slot_of_block.p, last_used.p,
                                                       stamp, ctl + C_COUNT);
     WC_LAUNCH_CHECK();
     // misses in ascending id order (cache.py:76-78), scan and compaction in one pass
@@ -2077,32 +2108,32 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
             stamp_hist.ensure(stamp + 1);
             h_stamp_hist.ensure_host(stamp + 1);
             WC_CUDA(cudaMemsetAsync(stamp_hist.p, 0, 4 * (stamp + 1), st));
-            k_stamp_hist<<<grid_for(slot_alloc, 256), 256, 4 * (size_t)stamp, st>>>(block_of_slot.p, last_used.p,
+            launch_pdl(k_stamp_hist, grid_for(slot_alloc, 256), 256, 4 * (size_t)stamp, st, block_of_slot.p, last_used.p,
                                                                                    ctl, stamp, stamp_hist.p);
             WC_LAUNCH_CHECK();
         }
     }
-    k_cache_plan<<<1, 1, 0, st>>>(ctl, p >= 1 && !hist ? stamp_hist.p : ctl + C_COUNT, stamp, vol->n_blocks,
+    launch_pdl(k_cache_plan, 1, 1, 0, st, ctl, p >= 1 && !hist ? stamp_hist.p : ctl + C_COUNT, stamp, vol->n_blocks,
                                  slot_alloc, nwords, hist);
     WC_LAUNCH_CHECK();
-    k_phys_init<<<grid_for(slot_alloc, 256), 256, 0, st>>>(ctl, block_of_slot.p, last_used.p);
+    launch_pdl(k_phys_init, grid_for(slot_alloc, 256), 256, 0, st, ctl, block_of_slot.p, last_used.p);
     WC_LAUNCH_CHECK();
     if (p >= 1) {  // victims in (last_used, block_id) order: one extraction over the stamp regions
-        k_mark_victims<<<grid_for(slot_alloc, 256), 256, 0, st>>>(block_of_slot.p, last_used.p, ctl, stamp, nwords,
+        launch_pdl(k_mark_victims, grid_for(slot_alloc, 256), 256, 0, st, block_of_slot.p, last_used.p, ctl, stamp, nwords,
                                                                   vict_bm.p, vict_sum.p);
         WC_LAUNCH_CHECK();
         bitmap_extract_listed(vict_bm.p, vict_sum.p, (int64_t)stamp * nwords, slot_alloc, nwords, nullptr, cand_key.p,
                               ctl + C_NCAND, true, word_list.p, ctl + C_NLIST, partials.p, st);  // clears the regions
-        k_blocks_to_slots<<<grid_for(slot_alloc, 256), 256, 0, st>>>(cand_key.p, ctl + C_NEVICT, slot_of_block.p,
+        launch_pdl(k_blocks_to_slots, grid_for(slot_alloc, 256), 256, 0, st, cand_key.p, ctl + C_NEVICT, slot_of_block.p,
                                                                      cand_val.p);
         WC_LAUNCH_CHECK();
-        k_evict<<<grid_for(slot_alloc, 256), 256, 0, st>>>(cand_val.p, ctl + C_NEVICT, block_of_slot.p,
+        launch_pdl(k_evict, grid_for(slot_alloc, 256), 256, 0, st, cand_val.p, ctl + C_NEVICT, block_of_slot.p,
                                                            slot_of_block.p);
         WC_LAUNCH_CHECK();
     }
     // the misses' records decoded straight into their slots (free slots
     // first, then the victims in order, cache.py:97-103)
-    k_decode_insert<<<grid_for(nmax * 32, kDecWarps * 32, 4), kDecWarps * 32, 0, st>>>(vol->payload.p, vol->qbits, vol->stride,
+    launch_pdl(k_decode_insert, grid_for(nmax * 32, kDecWarps * 32, 4), kDecWarps * 32, 0, st, vol->payload.p, vol->qbits, vol->stride,
                                                                  miss_ids.p, ctl, cand_val.p, slot_values.p,
                                                                  block_of_slot.p, last_used.p, slot_of_block.p, stamp);
     WC_LAUNCH_CHECK();
@@ -2116,12 +2147,12 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
         const int64_t n_ent = h_counters.p[C_NENT], nvis = h_counters.p[C_NVIS];
         if (n_ent > 0) {
             radix_sort_pairs(ent_key.p, ent_val.p, n_ent, bits_for((uint64_t)(nvis - 1)), rs, st);
-            k_run_offsets<<<grid_for(n_ent, 256), 256, 0, st>>>(ent_key.p, n_ent, nvis, block_ray_off.p);
+            launch_pdl(k_run_offsets, grid_for(n_ent, 256), 256, 0, st, ent_key.p, n_ent, nvis, block_ray_off.p);
             WC_LAUNCH_CHECK();
         }
     }
     mark(4);
-    k_contrib<<<grid_for(n, 256), 256, 0, st>>>(visible_ids.p, ctl + C_NVIS, slot_of_block.p, vol->bdx, vol->bdy,
+    launch_pdl(k_contrib, grid_for(n, 256), 256, 0, st, visible_ids.p, ctl + C_NVIS, slot_of_block.p, vol->bdx, vol->bdy,
                                                 vol->bdz, contrib.p, ctl + C_ERR, vis_bm.p);
     WC_LAUNCH_CHECK();
     RaytraceArgs ra{};
@@ -2152,27 +2183,27 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
         sa.item_t = item_t.p;
         sa.best = best.p;
         sa.n_items = ctl + C_NITEMS;
-        k_rt_find<<<grid_for(n, 128, 16), 128, 0, st>>>(sa);
+        launch_pdl(k_rt_find, grid_for(n, 128, 16), 128, 0, st, sa);
         WC_LAUNCH_CHECK();
-        k_rt_solve<<<grid_for(sa.item_cap, 128, WC_RAYTRACE_MIN_CTAS), 128, 0, st>>>(sa);
+        launch_pdl(k_rt_solve, grid_for(sa.item_cap, 128, WC_RAYTRACE_MIN_CTAS), 128, 0, st, sa);
         WC_LAUNCH_CHECK();
-        k_rt_shade<<<grid_for(n, 128, 16), 128, 0, st>>>(sa);
+        launch_pdl(k_rt_shade, grid_for(n, 128, 16), 128, 0, st, sa);
         WC_LAUNCH_CHECK();
     } else {
-        k_raytrace<<<grid_for(n, 128, 16), 128, 0, st>>>(ra);
+        launch_pdl(k_raytrace, grid_for(n, 128, 16), 128, 0, st, ra);
         WC_LAUNCH_CHECK();
     }
     mark(5);
     // composite + compaction of the surviving rays (next pass's O_Act)
     if (speculation && n / std::max<int64_t>(1, nact_guess) >= 8)  // n_spec >= 8: a warp per ray
-        k_composite_warp<<<grid_for(n * 32, 256), 256, 0, st>>>(ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p,
+        launch_pdl(k_composite_warp, grid_for(n * 32, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p,
                                                                 status.p, rgba.p, depth.p, keep.p);
     else
-        k_composite<<<grid_for(n, 256), 256, 0, st>>>(ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p, status.p,
+        launch_pdl(k_composite, grid_for(n, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p, status.p,
                                                       rgba.p, depth.p, keep.p);
     WC_LAUNCH_CHECK();
     compact_dev(LoadU32{keep.p}, alist, ctl + C_NACT, n, act_list[(p + 1) & 1].p, ctl + C_NACT_NEXT, partials.p, st);
-    k_pass_end<<<1, 1, 0, st>>>(ctl, plog.p + std::min<int64_t>(p, kMaxPassLog - 1) * L_COUNT, n, speculation,
+    launch_pdl(k_pass_end, 1, 1, 0, st, ctl, plog.p + std::min<int64_t>(p, kMaxPassLog - 1) * L_COUNT, n, speculation,
                                 max_spec, nwords);
     WC_LAUNCH_CHECK();
     mark(6);
@@ -2341,7 +2372,7 @@ void Session::enqueue_fb_snapshot(int64_t p) {
         snap_list.alloc(n);
         patch.alloc(n);
     }
-    k_snapshot_list<<<grid_for(n, 256), 256, 0, st>>>(counters.p, act_list[(p + 1) & 1].p, snap_list.p);
+    launch_pdl(k_snapshot_list, grid_for(n, 256), 256, 0, st, counters.p, act_list[(p + 1) & 1].p, snap_list.p);
     WC_LAUNCH_CHECK();
     WC_CUDA(cudaEventRecord(ev_fb, st));
     WC_CUDA(cudaStreamWaitEvent(st_copy, ev_fb, 0));
@@ -2391,7 +2422,7 @@ int64_t Session::render_to_host(const CameraParams *cam, double iso_, PassStatsC
     }
     const int64_t nsnap = h_counters.p[C_NSNAP];  // read with the frame's last counters
     if (nsnap > 0) {
-        k_gather_patch<<<grid_for(nsnap, 256), 256, 0, st>>>(counters.p, snap_list.p, rgba.p, depth.p, patch.p);
+        launch_pdl(k_gather_patch, grid_for(nsnap, 256), 256, 0, st, counters.p, snap_list.p, rgba.p, depth.p, patch.p);
         WC_LAUNCH_CHECK();
         h_patch.ensure_host(nsnap);
         WC_CUDA(cudaMemcpyAsync(h_patch.p, patch.p, sizeof(uint4) * nsnap, cudaMemcpyDeviceToHost, st));

@@ -7,6 +7,7 @@ namespace wc {
 
 __global__ void __launch_bounds__(kSortThreads)
     k_radix_hist(const uint32_t *keys, int64_t n, int shift, uint32_t mask, uint32_t *hist, int64_t ntiles) {
+    pdl_wait();
     __shared__ uint32_t h[kSortBins];
     h[threadIdx.x] = 0;
     __syncthreads();
@@ -26,6 +27,7 @@ __global__ void __launch_bounds__(kSortThreads)
 __global__ void __launch_bounds__(kSortThreads)
     k_radix_scatter(const uint32_t *keys, const uint32_t *vals, uint32_t *keys_out, uint32_t *vals_out,
                     int64_t n, int shift, uint32_t mask, const uint32_t *hist_off, int64_t ntiles) {
+    pdl_wait();
     constexpr int kWarps = kSortThreads / 32;
     __shared__ uint32_t wh[kWarps][kSortBins];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -98,11 +100,11 @@ void radix_sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int nbits, Radi
     for (int shift = 0; shift < nbits; shift += 8) {
         const int bits = (nbits - shift) < 8 ? (nbits - shift) : 8;
         const uint32_t mask = (1u << bits) - 1u;
-        k_radix_hist<<<(unsigned)nt, kSortThreads, 0, st>>>(ka, n, shift, mask, scratch.hist.p, nt);
+        launch_pdl(k_radix_hist, (unsigned)nt, kSortThreads, 0, st, ka, n, shift, mask, scratch.hist.p, nt);
         WC_LAUNCH_CHECK();
         const int64_t hn = nt * kSortBins;
         scan_exclusive(LoadU32{scratch.hist.p}, hn, scratch.hist.p, scratch.total.p, scratch.hist_partials.p, st);
-        k_radix_scatter<<<(unsigned)nt, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, mask, scratch.hist.p, nt);
+        launch_pdl(k_radix_scatter, (unsigned)nt, kSortThreads, 0, st, ka, va, kb, vb, n, shift, mask, scratch.hist.p, nt);
         WC_LAUNCH_CHECK();
         uint32_t *t = ka;
         ka = kb;
@@ -127,6 +129,7 @@ template <bool kClear>
 __global__ void __launch_bounds__(256) k_bitmap_dense(uint32_t *__restrict__ bm, int64_t nwords, int q16,
                                                       uint32_t *__restrict__ word_offsets, uint32_t *__restrict__ ids,
                                                       uint64_t *status, ScanEpoch ep, uint32_t *d_count) {
+    pdl_wait();
     __shared__ uint32_t sw[32];
     __shared__ uint32_t s_excl;
     const uint32_t epoch = resolve_epoch(ep);
@@ -194,10 +197,10 @@ void bitmap_extract_dense(uint32_t *bm, int64_t nwords, uint32_t *word_offsets, 
     const int64_t q16 = std::min<int64_t>(kDenseQ16, std::max<int64_t>(1, ceil_div(nwords, (int64_t)kNumSMs * 4 * 256 * 4)));
     const unsigned grid = (unsigned)ceil_div(nwords, 256 * 4 * q16);
     if (clear)
-        k_bitmap_dense<true><<<grid, 256, 0, st>>>(bm, nwords, (int)q16, word_offsets, ids,
+        launch_pdl(k_bitmap_dense<true>, grid, 256, 0, st, bm, nwords, (int)q16, word_offsets, ids,
                                                   reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
     else
-        k_bitmap_dense<false><<<grid, 256, 0, st>>>(bm, nwords, (int)q16, word_offsets, ids,
+        launch_pdl(k_bitmap_dense<false>, grid, 256, 0, st, bm, nwords, (int)q16, word_offsets, ids,
                                                    reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
     WC_LAUNCH_CHECK();
 }
@@ -249,11 +252,11 @@ void bitmap_extract_listed(uint32_t *bm, uint32_t *summary, int64_t nwords_max, 
         WC_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st));
         return;
     }
-    k_scan_onepass<LoadPopc, SinkList><<<scan_grid(ns), kScanThreads, 0, st>>>(
+    launch_pdl(k_scan_onepass<LoadPopc, SinkList>, scan_grid(ns), kScanThreads, 0, st, 
         LoadPopc{summary}, SinkList{summary, word_list}, ns, nullptr, reinterpret_cast<uint64_t *>(partials),
         scan_epoch(), d_nlist);
     WC_LAUNCH_CHECK();
-    k_scan_onepass<LoadPopcIdx, SinkBitsIdx><<<scan_grid(nlist_max), kScanThreads, 0, st>>>(
+    launch_pdl(k_scan_onepass<LoadPopcIdx, SinkBitsIdx>, scan_grid(nlist_max), kScanThreads, 0, st, 
         LoadPopcIdx{bm, word_list}, SinkBitsIdx{bm, word_list, word_offsets, ids, id_mod, clear}, nlist_max, d_nlist,
         reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
     WC_LAUNCH_CHECK();

@@ -188,6 +188,7 @@ template <class Load, class Sink>
 __global__ void __launch_bounds__(kScanThreads)
     k_scan_onepass(Load ld, Sink sink, int64_t n_max, const uint32_t *d_n, uint64_t *status, ScanEpoch ep,
                    uint32_t *d_total) {
+    pdl_wait();
     __shared__ uint32_t sw[32];
     __shared__ uint32_t tile[kScanTile];
     __shared__ uint32_t s_excl;
@@ -265,7 +266,7 @@ void scan_exclusive(Load ld, int64_t n, uint32_t *out, uint32_t *d_total, uint32
         WC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
         return;
     }
-    k_scan_onepass<Load, SinkStore><<<scan_grid(n), kScanThreads, 0, st>>>(
+    launch_pdl(k_scan_onepass<Load, SinkStore>, scan_grid(n), kScanThreads, 0, st, 
         ld, SinkStore{out}, n, nullptr, reinterpret_cast<uint64_t *>(scratch), scan_epoch(), d_total);
     WC_LAUNCH_CHECK();
 }
@@ -278,7 +279,7 @@ void scan_exclusive_dev(Load ld, const uint32_t *d_n, int64_t n_max, uint32_t *o
         WC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
         return;
     }
-    k_scan_onepass<Load, SinkStore><<<scan_grid(n_max), kScanThreads, 0, st>>>(
+    launch_pdl(k_scan_onepass<Load, SinkStore>, scan_grid(n_max), kScanThreads, 0, st, 
         ld, SinkStore{out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), scan_epoch(), d_total);
     WC_LAUNCH_CHECK();
 }
@@ -292,7 +293,7 @@ void compact_dev(Pred pred, const uint32_t *ids, const uint32_t *d_n, int64_t n_
         WC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
         return;
     }
-    k_scan_onepass<Pred, SinkCompact<Pred>><<<scan_grid(n_max), kScanThreads, 0, st>>>(
+    launch_pdl(k_scan_onepass<Pred, SinkCompact<Pred>>, scan_grid(n_max), kScanThreads, 0, st, 
         pred, SinkCompact<Pred>{pred, ids, out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), scan_epoch(),
         d_total);
     WC_LAUNCH_CHECK();
