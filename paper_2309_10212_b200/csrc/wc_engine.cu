@@ -965,13 +965,6 @@ __global__ void k_mark_victims(const int32_t *block_of_slot, const int32_t *last
     }
 }
 
-__global__ void k_blocks_to_slots(const uint32_t *blocks, const uint32_t *d_n, const int32_t *slot_of_block,
-                                  uint32_t *slots) {
-    pdl_wait();
-    const int64_t n = *d_n;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        slots[i] = (uint32_t)slot_of_block[blocks[i]];
-}
 
 // BlockCache reset: forget every resident block of the previous frame
 __global__ void k_cache_unmap(const int32_t *block_of_slot, const uint32_t *d_phys, int32_t *slot_of_block) {
@@ -985,13 +978,15 @@ __global__ void k_cache_unmap(const int32_t *block_of_slot, const uint32_t *d_ph
 
 // cache.py:90-95: unmap the first n_evict candidates (they become the
 // slots of the last n_evict misses, cache.py:96-97)
-__global__ void k_evict(const uint32_t *victims, const uint32_t *d_n_evict, int32_t *block_of_slot,
-                        int32_t *slot_of_block) {
+__global__ void k_evict(const uint32_t *victims, const uint32_t *d_n_evict, int32_t *slot_of_block,
+                        int32_t *block_of_slot, uint32_t *victim_slots) {
     pdl_wait();
     const int64_t n_evict = *d_n_evict;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_evict; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = victims[i];
-        slot_of_block[block_of_slot[s]] = -1;
+        const uint32_t b = victims[i];
+        const int32_t s = slot_of_block[b];
+        victim_slots[i] = (uint32_t)s;  // the slot of the i-th last miss
+        slot_of_block[b] = -1;
         block_of_slot[s] = -1;
     }
 }
@@ -1016,6 +1011,14 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4)
     uint32_t(*sw)[kDecWords] = stage[threadIdx.x >> 5];
     const int64_t n_miss = ctl[C_NMISS], hw = ctl[C_HW], n_free = ctl[C_NFREE], cap = ctl[C_CAP];
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl[C_HW_NEXT] = (uint32_t)(n_miss <= n_free ? hw + n_miss : cap);
+    {  // maps of the slots this pass's growth brought into use (cache.py:42-53) that no miss takes
+        const int64_t lo = max((int64_t)ctl[C_PHYS_OLD], hw + min(n_miss, n_free)), hi = ctl[C_PHYS];
+        for (int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < hi;
+             s += (int64_t)gridDim.x * blockDim.x) {
+            block_of_slot[s] = -1;
+            last_used[s] = 0;
+        }
+    }
     const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int n_words = stride >> 2;
@@ -1550,9 +1553,8 @@ __global__ void k_frame_start(uint32_t *ctl, int64_t n, int speculation, int max
 // cache.py:66-96 decisions of ensure_resident once the hits are stamped and
 // the misses listed: growth to ceil(1.5 * needed), free suffix, number of
 // victims and the last stamp bucket they reach (from the stamp histogram)
-__global__ void k_cache_plan(uint32_t *ctl, uint32_t *hist, int32_t pass_no, int64_t n_blocks, int64_t slot_alloc,
-                             int64_t nwords, bool maintain) {
-    pdl_wait();
+__device__ __forceinline__ void cache_plan(uint32_t *ctl, uint32_t *hist, int32_t pass_no, int64_t n_blocks,
+                                           int64_t slot_alloc, bool maintain) {
     const int64_t nactb = ctl[C_NACTB], n_miss = ctl[C_NMISS], hw = ctl[C_HW];
     int64_t cap = ctl[C_CAP], phys = ctl[C_PHYS];
     ctl[C_PHYS_OLD] = (uint32_t)phys;
@@ -1592,16 +1594,25 @@ __global__ void k_cache_plan(uint32_t *ctl, uint32_t *hist, int32_t pass_no, int
         hist[pass_no] += (uint32_t)n_miss;
     }
 }
+__global__ void k_cache_plan(uint32_t *ctl, uint32_t *hist, int32_t pass_no, int64_t n_blocks, int64_t slot_alloc,
+                             bool maintain) {
+    pdl_wait();
+    cache_plan(ctl, hist, pass_no, n_blocks, slot_alloc, maintain);
+}
+
+// the same decisions as the epilogue of the miss compaction (its count is
+// the n_miss they need), saving a launch per pass
+struct CachePlanEpilogue {
+    uint32_t *ctl, *hist;
+    int32_t pass_no;
+    int64_t n_blocks, slot_alloc;
+    __device__ __forceinline__ void operator()(uint32_t n_miss) const {
+        ctl[C_NMISS] = n_miss;
+        cache_plan(ctl, hist, pass_no, n_blocks, slot_alloc, true);
+    }
+};
 
 // maps of the slots the growth just brought into use (cache.py:42-53)
-__global__ void k_phys_init(const uint32_t *ctl, int32_t *block_of_slot, int32_t *last_used) {
-    pdl_wait();
-    const int64_t lo = ctl[C_PHYS_OLD], hi = ctl[C_PHYS];
-    for (int64_t s = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < hi; s += (int64_t)gridDim.x * blockDim.x) {
-        block_of_slot[s] = -1;
-        last_used[s] = 0;
-    }
-}
 
 // end of pass: the PassStats record, then the next pass's n_act / n_spec
 // (engine.py:331-333, slot budget engine.py:341)
@@ -1620,6 +1631,8 @@ __global__ void k_pass_end(uint32_t *ctl, uint32_t *row, int64_t n, int speculat
     row[L_NITEMS] = ctl[C_NITEMS];
     row[L_PHYS] = ctl[C_PHYS];
     row[L_HW] = ctl[C_HW_NEXT];
+    ctl[C_WORK] = 0;  // the next pass's traversal work counter and raytrace list start empty
+    ctl[C_NITEMS] = 0;
     if (n_act == 0) return;  // an enqueued pass after the last one: no state change
     ctl[C_HW] = ctl[C_HW_NEXT];
     const int64_t n_spec = n_spec_of(n, n_after, speculation, max_spec);
@@ -2066,8 +2079,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     ta.vis_bm = vis_bm.p;
     ta.work = ctl + C_WORK;
     ta.ctl = ctl;
-    WC_CUDA(cudaMemsetAsync(ctl + C_WORK, 0, 4, st));
-    WC_CUDA(cudaMemsetAsync(ctl + C_NITEMS, 0, 4, st));
+    // C_WORK and C_NITEMS are zero here (reset, or the last k_pass_end)
     if (nact_guess <= WC_WARP_TRAVERSE_MAX)  // few (long) rays: warp-cooperative DDA per ray
         launch_pdl(k_traverse_warp, grid_for(std::max<int64_t>(1, nact_guess) * 32, 128, 16), 128, 0, st, ta);
     else
@@ -2098,44 +2110,45 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     launch_pdl(k_cache_stamp, grid_for(nmax, 256), 256, 0, st, active_ids.p, ctl + C_NACTB, nmax, slot_of_block.p, last_used.p,
                                                       stamp, ctl + C_COUNT);
     WC_LAUNCH_CHECK();
-    // misses in ascending id order (cache.py:76-78), scan and compaction in one pass
-    compact_dev(PredMiss{active_ids.p, slot_of_block.p}, active_ids.p, ctl + C_NACTB, nmax, miss_ids.p,
-                ctl + C_NMISS, partials.p, st);
+    // misses in ascending id order (cache.py:76-78), scan and compaction in
+    // one pass; the growth / eviction decisions (k_cache_plan) run as its
+    // epilogue when the stamp histogram is kept on the device
+    if (hist)
+        compact_dev(PredMiss{active_ids.p, slot_of_block.p}, active_ids.p, ctl + C_NACTB, nmax, miss_ids.p,
+                    ctl + C_NMISS, partials.p, st, CachePlanEpilogue{ctl, ctl + C_COUNT, stamp, vol->n_blocks, slot_alloc});
+    else
+        compact_dev(PredMiss{active_ids.p, slot_of_block.p}, active_ids.p, ctl + C_NACTB, nmax, miss_ids.p,
+                    ctl + C_NMISS, partials.p, st);
     mark(2);
-    if (p >= 1 && !hist) {  // > kHistBins passes: histogram over all stamps through the host (rare)
+    if (!hist) {  // > kHistBins passes: histogram over all stamps through the host (rare)
         read_counters(0, C_COUNT);
         if (h_counters.p[C_NACT]) {
             stamp_hist.ensure(stamp + 1);
             h_stamp_hist.ensure_host(stamp + 1);
             WC_CUDA(cudaMemsetAsync(stamp_hist.p, 0, 4 * (stamp + 1), st));
-            launch_pdl(k_stamp_hist, grid_for(slot_alloc, 256), 256, 4 * (size_t)stamp, st, block_of_slot.p, last_used.p,
-                                                                                   ctl, stamp, stamp_hist.p);
+            launch_pdl(k_stamp_hist, grid_for(slot_alloc, 256), 256, 4 * (size_t)stamp, st, block_of_slot.p,
+                       last_used.p, ctl, stamp, stamp_hist.p);
             WC_LAUNCH_CHECK();
         }
+        launch_pdl(k_cache_plan, 1, 1, 0, st, ctl, stamp_hist.p, stamp, vol->n_blocks, slot_alloc, false);
+        WC_LAUNCH_CHECK();
     }
-    launch_pdl(k_cache_plan, 1, 1, 0, st, ctl, p >= 1 && !hist ? stamp_hist.p : ctl + C_COUNT, stamp, vol->n_blocks,
-                                 slot_alloc, nwords, hist);
-    WC_LAUNCH_CHECK();
-    launch_pdl(k_phys_init, grid_for(slot_alloc, 256), 256, 0, st, ctl, block_of_slot.p, last_used.p);
-    WC_LAUNCH_CHECK();
     if (p >= 1) {  // victims in (last_used, block_id) order: one extraction over the stamp regions
-        launch_pdl(k_mark_victims, grid_for(slot_alloc, 256), 256, 0, st, block_of_slot.p, last_used.p, ctl, stamp, nwords,
-                                                                  vict_bm.p, vict_sum.p);
+        launch_pdl(k_mark_victims, grid_for(slot_alloc, 256), 256, 0, st, block_of_slot.p, last_used.p, ctl, stamp,
+                   nwords, vict_bm.p, vict_sum.p);
         WC_LAUNCH_CHECK();
         bitmap_extract_listed(vict_bm.p, vict_sum.p, (int64_t)stamp * nwords, slot_alloc, nwords, nullptr, cand_key.p,
                               ctl + C_NCAND, true, word_list.p, ctl + C_NLIST, partials.p, st);  // clears the regions
-        launch_pdl(k_blocks_to_slots, grid_for(slot_alloc, 256), 256, 0, st, cand_key.p, ctl + C_NEVICT, slot_of_block.p,
-                                                                     cand_val.p);
-        WC_LAUNCH_CHECK();
-        launch_pdl(k_evict, grid_for(slot_alloc, 256), 256, 0, st, cand_val.p, ctl + C_NEVICT, block_of_slot.p,
-                                                           slot_of_block.p);
+        launch_pdl(k_evict, grid_for(slot_alloc, 256), 256, 0, st, cand_key.p, ctl + C_NEVICT, slot_of_block.p,
+                   block_of_slot.p, cand_val.p);
         WC_LAUNCH_CHECK();
     }
     // the misses' records decoded straight into their slots (free slots
-    // first, then the victims in order, cache.py:97-103)
-    launch_pdl(k_decode_insert, grid_for(nmax * 32, kDecWarps * 32, 4), kDecWarps * 32, 0, st, vol->payload.p, vol->qbits, vol->stride,
-                                                                 miss_ids.p, ctl, cand_val.p, slot_values.p,
-                                                                 block_of_slot.p, last_used.p, slot_of_block.p, stamp);
+    // first, then the victims in order, cache.py:97-103); the kernel also
+    // initialises the slots this pass's growth brought into use
+    launch_pdl(k_decode_insert, grid_for(nmax * 32, kDecWarps * 32, 4), kDecWarps * 32, 0, st, vol->payload.p,
+               vol->qbits, vol->stride, miss_ids.p, ctl, cand_val.p, slot_values.p, block_of_slot.p, last_used.p,
+               slot_of_block.p, stamp);
     WC_LAUNCH_CHECK();
     if (corrupt) WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * slot_alloc, st));  // engine.py:338-339
     mark(3);

@@ -254,11 +254,11 @@ void bitmap_extract_listed(uint32_t *bm, uint32_t *summary, int64_t nwords_max, 
     }
     launch_pdl(k_scan_onepass<LoadPopc, SinkList>, scan_grid(ns), kScanThreads, 0, st, 
         LoadPopc{summary}, SinkList{summary, word_list}, ns, nullptr, reinterpret_cast<uint64_t *>(partials),
-        scan_epoch(), d_nlist);
+        scan_epoch(), d_nlist, NoEpilogue{});
     WC_LAUNCH_CHECK();
     launch_pdl(k_scan_onepass<LoadPopcIdx, SinkBitsIdx>, scan_grid(nlist_max), kScanThreads, 0, st, 
         LoadPopcIdx{bm, word_list}, SinkBitsIdx{bm, word_list, word_offsets, ids, id_mod, clear}, nlist_max, d_nlist,
-        reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count);
+        reinterpret_cast<uint64_t *>(partials), scan_epoch(), d_count, NoEpilogue{});
     WC_LAUNCH_CHECK();
 }
 

@@ -184,10 +184,17 @@ __device__ __forceinline__ uint32_t tile_lookback(int64_t t, uint32_t agg, uint6
 constexpr int kScanMaxCtas = kNumSMs * 8;
 inline unsigned scan_grid(int64_t n_max) { return (unsigned)std::min<int64_t>(scan_tiles(n_max), kScanMaxCtas); }
 
-template <class Load, class Sink>
+// Epilogue of a scan: run by one thread of the last tile once the total is
+// known (a control decision that would otherwise be a one-thread kernel).
+// It must not change the element count *d_n the other tiles read.
+struct NoEpilogue {
+    __device__ __forceinline__ void operator()(uint32_t) const {}
+};
+
+template <class Load, class Sink, class Epi = NoEpilogue>
 __global__ void __launch_bounds__(kScanThreads)
     k_scan_onepass(Load ld, Sink sink, int64_t n_max, const uint32_t *d_n, uint64_t *status, ScanEpoch ep,
-                   uint32_t *d_total) {
+                   uint32_t *d_total, Epi epi = Epi{}) {
     pdl_wait();
     __shared__ uint32_t sw[32];
     __shared__ uint32_t tile[kScanTile];
@@ -209,7 +216,10 @@ __global__ void __launch_bounds__(kScanThreads)
             const uint32_t excl = tile_lookback(t, agg, status, epoch);
             if (threadIdx.x == 0) {
                 s_excl = excl;
-                if (t == last && d_total) *d_total = excl + agg;
+                if (t == last) {
+                    if (d_total) *d_total = excl + agg;
+                    epi(excl + agg);
+                }
             }
         }
         __syncthreads();
@@ -236,7 +246,11 @@ __global__ void __launch_bounds__(kScanThreads)
             const uint32_t excl = tile_lookback(t, agg, status, epoch);
             if (threadIdx.x == 0) {
                 s_excl = excl;
-                if (t == last && d_total) *d_total = n > 0 ? excl + agg : 0u;
+                if (t == last) {
+                    const uint32_t total = n > 0 ? excl + agg : 0u;
+                    if (d_total) *d_total = total;
+                    epi(total);
+                }
             }
         }
         __syncthreads();
@@ -267,7 +281,7 @@ void scan_exclusive(Load ld, int64_t n, uint32_t *out, uint32_t *d_total, uint32
         return;
     }
     launch_pdl(k_scan_onepass<Load, SinkStore>, scan_grid(n), kScanThreads, 0, st, 
-        ld, SinkStore{out}, n, nullptr, reinterpret_cast<uint64_t *>(scratch), scan_epoch(), d_total);
+        ld, SinkStore{out}, n, nullptr, reinterpret_cast<uint64_t *>(scratch), scan_epoch(), d_total, NoEpilogue{});
     WC_LAUNCH_CHECK();
 }
 
@@ -280,22 +294,23 @@ void scan_exclusive_dev(Load ld, const uint32_t *d_n, int64_t n_max, uint32_t *o
         return;
     }
     launch_pdl(k_scan_onepass<Load, SinkStore>, scan_grid(n_max), kScanThreads, 0, st, 
-        ld, SinkStore{out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), scan_epoch(), d_total);
+        ld, SinkStore{out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), scan_epoch(), d_total, NoEpilogue{});
     WC_LAUNCH_CHECK();
 }
 
 // Stable compaction of ids[i] for pred(i), i < *d_n (<= n_max), in one
 // pass: out[...] in input order, count -> *d_total.
-template <class Pred>
+// (epi: optional epilogue run with the count, see NoEpilogue; n_max > 0)
+template <class Pred, class Epi = NoEpilogue>
 void compact_dev(Pred pred, const uint32_t *ids, const uint32_t *d_n, int64_t n_max, uint32_t *out,
-                 uint32_t *d_total, uint32_t *scratch, cudaStream_t st) {
+                 uint32_t *d_total, uint32_t *scratch, cudaStream_t st, Epi epi = Epi{}) {
     if (n_max <= 0) {
         WC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
         return;
     }
-    launch_pdl(k_scan_onepass<Pred, SinkCompact<Pred>>, scan_grid(n_max), kScanThreads, 0, st, 
-        pred, SinkCompact<Pred>{pred, ids, out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), scan_epoch(),
-        d_total);
+    launch_pdl(k_scan_onepass<Pred, SinkCompact<Pred>, Epi>, scan_grid(n_max), kScanThreads, 0, st, pred,
+               SinkCompact<Pred>{pred, ids, out}, n_max, d_n, reinterpret_cast<uint64_t *>(scratch), scan_epoch(),
+               d_total, epi);
     WC_LAUNCH_CHECK();
 }
 
