@@ -1616,8 +1616,7 @@ struct CachePlanEpilogue {
 
 // end of pass: the PassStats record, then the next pass's n_act / n_spec
 // (engine.py:331-333, slot budget engine.py:341)
-__global__ void k_pass_end(uint32_t *ctl, uint32_t *row, int64_t n, int speculation, int max_spec, int64_t nwords) {
-    pdl_wait();
+__device__ __forceinline__ void pass_end(uint32_t *ctl, uint32_t *row, int64_t n, int speculation, int max_spec) {
     const int64_t n_act = ctl[C_NACT], n_after = ctl[C_NACT_NEXT];
     row[L_NACT] = (uint32_t)n_act;
     row[L_NSPEC] = ctl[C_NSPEC];
@@ -1640,6 +1639,20 @@ __global__ void k_pass_end(uint32_t *ctl, uint32_t *row, int64_t n, int speculat
     ctl[C_NACT] = (uint32_t)n_after;
     ctl[C_NSPEC] = (uint32_t)n_spec;
 }
+
+// pass_end as the epilogue of the compaction of the surviving rays (its
+// count is n_after).  It rewrites the count that compaction reads
+// (ctl[C_NACT]) with n_after <= n_act, so a CTA reading it late still finds
+// no tile of its own.
+struct PassEndEpilogue {
+    uint32_t *ctl, *row;
+    int64_t n;
+    int speculation, max_spec;
+    __device__ __forceinline__ void operator()(uint32_t n_after) const {
+        ctl[C_NACT_NEXT] = n_after;
+        pass_end(ctl, row, n, speculation, max_spec);
+    }
+};
 
 // ---------------------------------------------------- framebuffer read-back
 
@@ -2079,7 +2092,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     ta.vis_bm = vis_bm.p;
     ta.work = ctl + C_WORK;
     ta.ctl = ctl;
-    // C_WORK and C_NITEMS are zero here (reset, or the last k_pass_end)
+    // C_WORK and C_NITEMS are zero here (reset, or the last pass_end)
     if (nact_guess <= WC_WARP_TRAVERSE_MAX)  // few (long) rays: warp-cooperative DDA per ray
         launch_pdl(k_traverse_warp, grid_for(std::max<int64_t>(1, nact_guess) * 32, 128, 16), 128, 0, st, ta);
     else
@@ -2215,10 +2228,11 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
         launch_pdl(k_composite, grid_for(n, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p, status.p,
                                                       rgba.p, depth.p, keep.p);
     WC_LAUNCH_CHECK();
-    compact_dev(LoadU32{keep.p}, alist, ctl + C_NACT, n, act_list[(p + 1) & 1].p, ctl + C_NACT_NEXT, partials.p, st);
-    launch_pdl(k_pass_end, 1, 1, 0, st, ctl, plog.p + std::min<int64_t>(p, kMaxPassLog - 1) * L_COUNT, n, speculation,
-                                max_spec, nwords);
-    WC_LAUNCH_CHECK();
+    // next pass's active list; the pass record and the next pass's counts
+    // (pass_end) as its epilogue
+    compact_dev(LoadU32{keep.p}, alist, ctl + C_NACT, n, act_list[(p + 1) & 1].p, ctl + C_NACT_NEXT, partials.p, st,
+                PassEndEpilogue{ctl, plog.p + std::min<int64_t>(p, kMaxPassLog - 1) * L_COUNT, n, speculation,
+                                max_spec});
     mark(6);
 }
 

@@ -54,7 +54,7 @@ enum Counter : int {
     C_COUNT
 };
 
-// Per-pass record written on the device by k_pass_end (PassStats fields).
+// Per-pass record written on the device by pass_end (PassStats fields).
 enum PassLog : int {
     L_NACT = 0, L_NSPEC, L_NVIS, L_NACTB, L_NMISS, L_NEVICT, L_CAP, L_NENT, L_NAFTER, L_NITEMS, L_PHYS, L_HW,
     L_COUNT

@@ -18,11 +18,11 @@ STAGE_OF = [
     ("k_traverse", "traverse"),
     ("k_rt_", "raytrace"), ("k_raytrace", "raytrace"), ("k_contrib", "raytrace"),
     ("k_decode_insert", "cache_decode"), ("k_evict", "cache_decode"), ("k_stamp_hist", "cache_decode"),
-    ("k_mark_stamp", "cache_decode"), ("k_blocks_to_slots", "cache_decode"), ("k_gather_last_used", "cache_decode"),
-    ("k_compact_cand", "cache_decode"),
+    ("k_mark_victims", "cache_decode"), ("SinkList", "cache_decode"), ("SinkBitsIdx", "cache_decode"),
+    ("k_cache_plan", "cache_decode"),
     ("k_iso_bitmap", "reset"), ("k_iso_cell_mask", "reset"), ("k_init_rays", "reset"), ("k_cache_unmap", "reset"),
-    ("k_stamp_hist", "cache_decode"),
-    ("k_composite", "composite"), ("k_compact_keep", "composite"),
+    ("PredActive", "reset"), ("k_frame_start", "reset"),
+    ("k_composite", "composite"), ("SinkCompact<wc::LoadU32>", "composite"),
     ("k_radix", "group"), ("k_run_offsets", "group"),
 ]
 SETUP = ("k_compress", "k_widen", "k_octant_union", "k_group4", "k_range_extent", "k_range_quantize")
