@@ -183,6 +183,27 @@ def test_arbitrary_rays_lockstep(wc):
              max_spec=4)
 
 
+def test_more_passes_than_histogram_bins(wc):
+    """Speculation off on rays that graze a long slab of candidate blocks: one
+    pass per block (> 64 passes, past the device-kept stamp histogram, so the
+    later passes take the host-recount path), with a small cache that evicts
+    every pass.  Every pass's buffers and cache state are compared."""
+    nx, ny, nz = 448, 16, 12
+    y = np.arange(ny, dtype=np.float64)
+    f = np.sin(2 * np.pi * y / 8.0).astype(np.float32)  # varies in y only
+    vol = wc.volume.make_volume((nx, ny, nz), np.broadcast_to(f[None, :, None], (nz, ny, nx)))
+    cv = wc.compress_volume(vol, 12)
+    rng = np.random.default_rng(11)
+    n = 48
+    origins = np.stack([np.full(n, -5.0), rng.uniform(2.1, 2.9, n), rng.uniform(0.5, nz - 1.5, n)], 1)
+    origins[: n // 3, 1] = rng.uniform(0.2, 15.0, n // 3)  # these rays cross the surface early
+    d = np.stack([np.ones(n), rng.uniform(-2e-4, 2e-4, n), rng.uniform(-1e-3, 1e-3, n)], 1)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    stats, _, _ = lockstep(wc, cv, oracle_volume(cv), None, n, 1, 0.5, origins=origins, dirs=d,
+                           speculation=False, cache_capacity=40)
+    assert len(stats) > 70, len(stats)
+
+
 def test_corrupt_cache_hook_breaks_parity(wc):
     vol = host_volume("sphere", 64)
     cv = wc.compress_volume(vol, 16)
