@@ -1347,33 +1347,62 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArg
 }
 
 // phase 3: shade each entry's winning cell (or record the miss)
+// phase 3: shade each entry's earliest root.  Entries without one only
+// write their miss value; the hits of a warp's successive 32-entry rounds
+// are queued in shared memory and shaded 32 at a time, so every lane of a
+// shading round has a hit (most entries of a pass have none).
+__device__ __forceinline__ void shade_entry(const SplitArgs &s, const RayView &rv, uint32_t k, uint32_t bst) {
+    const RaytraceArgs &a = s.a;
+    const uint32_t i = bst & ((1u << 27) - 1u);
+    const uint4 info = s.item_info[i];
+    const float4 c0 = s.item_corners[2 * (int64_t)i], c1 = s.item_corners[2 * (int64_t)i + 1];
+    const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const uint32_t r = info.y, b = info.z, code = info.w;
+    const int lx = code & 7, ly = (code >> 3) & 7, lz = (code >> 6) & 7;
+    const int bx = (int)(b % (uint32_t)a.bdx), by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy),
+              bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
+    double o[3], d[3];
+    rv.load(r, o, d);
+    float rgb[3];
+    const double th = s.item_t[i];
+    shade_hit(c, o, d, 4 * bx + lx, 4 * by + ly, 4 * bz + lz, th, a.fp[4], a.fp[5], a.fp[6], rgb);
+    a.rgbz[k] = make_float4(rgb[0], rgb[1], rgb[2], (float)th);
+}
+
 __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
     pdl_wait();
     const RaytraceArgs &a = s.a;
     RayView rv = a.rays;
     rv.bind();
+    __shared__ uint2 queue[4][64];  // per warp: (entry, best) of the hits not yet shaded
+    uint2 *q = queue[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    int nq = 0;  // warp-uniform
     const int64_t n_ent = *a.d_n_ent;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_ent; j += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t k = a.identity ? (uint32_t)j : a.ent_val[j];
-        const uint32_t bst = s.best[k];
-        if (bst == WC_UINT_MAX) {
-            a.rgbz[k] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
-            continue;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); j0 < n_ent; j0 += stride) {
+        const int64_t j = j0 + lane;
+        uint32_t k = 0, bst = WC_UINT_MAX;
+        if (j < n_ent) {
+            k = a.identity ? (uint32_t)j : a.ent_val[j];
+            bst = s.best[k];
+            if (bst == WC_UINT_MAX) a.rgbz[k] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
         }
-        const uint32_t i = bst & ((1u << 27) - 1u);
-        const uint4 info = s.item_info[i];
-        const float4 c0 = s.item_corners[2 * (int64_t)i], c1 = s.item_corners[2 * (int64_t)i + 1];
-        const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-        const uint32_t r = info.y, b = info.z, code = info.w;
-        const int lx = code & 7, ly = (code >> 3) & 7, lz = (code >> 6) & 7;
-        const int bx = (int)(b % (uint32_t)a.bdx), by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy),
-                  bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
-        double o[3], d[3];
-        rv.load(r, o, d);
-        float rgb[3];
-        const double th = s.item_t[i];
-        shade_hit(c, o, d, 4 * bx + lx, 4 * by + ly, 4 * bz + lz, th, a.fp[4], a.fp[5], a.fp[6], rgb);
-        a.rgbz[k] = make_float4(rgb[0], rgb[1], rgb[2], (float)th);
+        const uint32_t hits = __ballot_sync(0xffffffffu, bst != WC_UINT_MAX);
+        if (bst != WC_UINT_MAX) q[nq + __popc(hits & ((1u << lane) - 1u))] = make_uint2(k, bst);
+        nq += __popc(hits);
+        __syncwarp();
+        if (nq >= 32) {  // a full round of hits
+            const uint2 e = q[nq - 32 + lane];
+            __syncwarp();
+            nq -= 32;
+            shade_entry(s, rv, e.x, e.y);
+        }
+    }
+    __syncwarp();
+    if (lane < nq) {
+        const uint2 e = q[lane];
+        shade_entry(s, rv, e.x, e.y);
     }
 }
 
