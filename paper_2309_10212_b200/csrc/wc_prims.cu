@@ -122,11 +122,20 @@ void radix_sort_pairs(uint32_t *keys, uint32_t *vals, int64_t n, int nbits, Radi
 
 // ----------------------------------------------------------- bitmap extract
 
-// A thread owns kDenseQ16 16-byte groups (up to 32 words): all loads are
+// A thread owns kDenseQ16 16-byte groups (up to 16 words): all loads are
 // issued before any is used and the words stay in registers for the id pass.
-constexpr int kDenseQ16 = 8;
+#ifndef WC_DENSE_Q16
+#define WC_DENSE_Q16 4
+#endif
+#ifndef WC_DENSE_MIN_CTAS
+#define WC_DENSE_MIN_CTAS 1
+#endif
+#ifndef WC_DENSE_CTAS_PER_SM
+#define WC_DENSE_CTAS_PER_SM 8
+#endif
+constexpr int kDenseQ16 = WC_DENSE_Q16;
 template <bool kClear>
-__global__ void __launch_bounds__(256) k_bitmap_dense(uint32_t *__restrict__ bm, int64_t nwords, int q16,
+__global__ void __launch_bounds__(256, WC_DENSE_MIN_CTAS) k_bitmap_dense(uint32_t *__restrict__ bm, int64_t nwords, int q16,
                                                       uint32_t *__restrict__ word_offsets, uint32_t *__restrict__ ids,
                                                       uint64_t *status, ScanEpoch ep, uint32_t *d_count) {
     pdl_wait();
@@ -192,9 +201,10 @@ void bitmap_extract_dense(uint32_t *bm, int64_t nwords, uint32_t *word_offsets, 
         WC_CUDA(cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st));
         return;
     }
-    // about one wave of 4 CTAs per SM, 1..kDenseQ16 16-byte groups per thread
+    // about one wave of WC_DENSE_CTAS_PER_SM CTAs per SM, 1..kDenseQ16 16-byte groups per
+    // thread (measured at C3: 8 x 4 beats 4 x 8, 2 x 16 and 8 x 1..3)
     // (larger bitmaps launch more waves)
-    const int64_t q16 = std::min<int64_t>(kDenseQ16, std::max<int64_t>(1, ceil_div(nwords, (int64_t)kNumSMs * 4 * 256 * 4)));
+    const int64_t q16 = std::min<int64_t>(kDenseQ16, std::max<int64_t>(1, ceil_div(nwords, (int64_t)kNumSMs * WC_DENSE_CTAS_PER_SM * 256 * 4)));
     const unsigned grid = (unsigned)ceil_div(nwords, 256 * 4 * q16);
     if (clear)
         launch_pdl(k_bitmap_dense<true>, grid, 256, 0, st, bm, nwords, (int)q16, word_offsets, ids,
