@@ -31,6 +31,20 @@
 #ifndef WC_WARP_TRAVERSE_MAX
 #define WC_WARP_TRAVERSE_MAX 16384
 #endif
+// k_iso_cell_mask: coarse cells per half-warp in flight
+#ifndef WC_ISO_KU
+#define WC_ISO_KU 4
+#endif
+// k_decode_insert: warps per CTA, records staged per warp, CTAs per SM
+#ifndef WC_DEC_WARPS
+#define WC_DEC_WARPS 8
+#endif
+#ifndef WC_DEC_REC
+#define WC_DEC_REC 16
+#endif
+#ifndef WC_DEC_CTAS
+#define WC_DEC_CTAS 4
+#endif
 #ifndef WC_RAYTRACE_MIN_CTAS
 #define WC_RAYTRACE_MIN_CTAS 6
 #endif
@@ -761,7 +775,7 @@ __global__ void k_iso_cell_mask(const ushort2 *__restrict__ q, const double2 *__
     // 256 B (lane: 4 fine cells = one x-row), 4 cells per lane in flight.
     // One ballot per x position collects the 16 rows of both half-warps'
     // cells: bits [16x, 16x + 16) of a cell's mask.
-    constexpr int kU = 4;
+    constexpr int kU = WC_ISO_KU;
     const int64_t n_coarse = min((int64_t)cdx * cdy * cdz, c_end);  // cells [c_begin, c_end): c_begin % 8 == 0
     const bool iso_nan = iso != iso;
     const uint32_t qi = iso_nan ? 0u : range_q(iso, base, inv);
@@ -1000,8 +1014,8 @@ __global__ void k_evict(const uint32_t *victims, const uint32_t *d_n_evict, int3
 // memory: kDecRec records are requested with cp.async (no registers held per
 // request, so many random 132 B records are in flight per SM), then decoded
 // from shared memory straight into the slots.
-constexpr int kDecWarps = 8, kDecRec = 16, kDecWords = 64;  // words: the largest record (qbits 31)
-__global__ void __launch_bounds__(kDecWarps * 32, 4)
+constexpr int kDecWarps = WC_DEC_WARPS, kDecRec = WC_DEC_REC, kDecWords = 64;  // words: the largest record (qbits 31)
+__global__ void __launch_bounds__(kDecWarps * 32, WC_DEC_CTAS)
     k_decode_insert(const uint8_t *__restrict__ payload, int qbits, int stride, const uint32_t *__restrict__ miss_ids,
                     uint32_t *ctl, const uint32_t *__restrict__ victims, float *__restrict__ slot_values,
                     int32_t *block_of_slot, int32_t *last_used, int32_t *slot_of_block, int32_t pass_no) {
@@ -2188,7 +2202,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     // the misses' records decoded straight into their slots (free slots
     // first, then the victims in order, cache.py:97-103); the kernel also
     // initialises the slots this pass's growth brought into use
-    launch_pdl(k_decode_insert, grid_for(nmax * 32, kDecWarps * 32, 4), kDecWarps * 32, 0, st, vol->payload.p,
+    launch_pdl(k_decode_insert, grid_for(nmax * 32, kDecWarps * 32, WC_DEC_CTAS), kDecWarps * 32, 0, st, vol->payload.p,
                vol->qbits, vol->stride, miss_ids.p, ctl, cand_val.p, slot_values.p, block_of_slot.p, last_used.p,
                slot_of_block.p, stamp);
     WC_LAUNCH_CHECK();
