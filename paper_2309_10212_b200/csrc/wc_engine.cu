@@ -45,6 +45,10 @@
 #ifndef WC_DEC_CTAS
 #define WC_DEC_CTAS 4
 #endif
+// k_traverse: idle lanes that trigger a refill of the warp
+#ifndef WC_REFILL_MIN
+#define WC_REFILL_MIN 8
+#endif
 #ifndef WC_RAYTRACE_MIN_CTAS
 #define WC_RAYTRACE_MIN_CTAS 6
 #endif
@@ -347,7 +351,9 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
     for (;;) {
         if (!exhausted) {  // refill idle lanes (warp-uniform branch)
             const uint32_t need = __ballot_sync(0xffffffffu, !have);
-            if (need) {
+            // batched: the refill path (ray loads, FP64 deltas) runs for at
+            // least WC_REFILL_MIN lanes at once, unless the warp is all idle
+            if (need && (__popc(need) >= WC_REFILL_MIN || need == 0xffffffffu)) {
                 const int leader = __ffs(need) - 1;
                 uint32_t first = 0;
                 if (lane == leader) first = atomicAdd(a.work, (uint32_t)__popc(need));
