@@ -1317,25 +1317,43 @@ __global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        uint32_t first = 0;
-        if (lane == 31 && incl) first = atomicAdd(s.n_items, incl);
-        first = __shfl_sync(0xffffffffu, first, 31) + incl - (uint32_t)found;
-        if (found) {
-            // the corners were just walked: these loads hit L1
-            for (int q = 0; q < found; q++) {
-                const uint32_t it = first + q;
-                if (it < s.item_cap) {
-                    const uint32_t lc = (uint32_t)(codes >> (6 * q)) & 63u;
-                    const int lx = lc & 3, ly = (lc >> 2) & 3, lz = lc >> 4;
-                    float c[8];
-                    sf.corners(lx, ly, lz, c);
-                    s.item_info[it] = make_uint4(ek, er, eb,
-                                                 (uint32_t)(lx | (ly << 3) | (lz << 6)) | ((uint32_t)q << 9));
-                    s.item_corners[2 * (int64_t)it] = make_float4(c[0], c[1], c[2], c[3]);
-                    s.item_corners[2 * (int64_t)it + 1] = make_float4(c[4], c[5], c[6], c[7]);
-                }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t base_it = 0;
+        if (lane == 31 && total) base_it = atomicAdd(s.n_items, total);
+        base_it = __shfl_sync(0xffffffffu, base_it, 31);
+        // The warp's items are written cooperatively, item t by lane t % 32
+        // (the owning entry's lane is found by a search over the prefix
+        // sums), instead of each lane looping over its own <= 10 items.  The
+        // corners were just walked by the owner: these loads hit L1, through
+        // the owner's row pointers in shared memory.
+        const unsigned long long codes_lane = codes;
+        for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            int owner = 0;  // smallest lane whose inclusive prefix exceeds t
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, incl, owner + step - 1);
+                if (v <= t) owner += step;
+            }
+            const uint32_t o_incl = __shfl_sync(0xffffffffu, incl, owner);
+            const uint32_t o_found = (uint32_t)__shfl_sync(0xffffffffu, found, owner);
+            const unsigned long long o_codes = __shfl_sync(0xffffffffu, codes_lane, owner);
+            const uint32_t o_ek = __shfl_sync(0xffffffffu, ek, owner), o_er = __shfl_sync(0xffffffffu, er, owner),
+                           o_eb = __shfl_sync(0xffffffffu, eb, owner);
+            const uint32_t it = base_it + t;
+            if (t < total && it < s.item_cap) {
+                const uint32_t q = t - (o_incl - o_found);
+                const uint32_t lc = (uint32_t)(o_codes >> (6 * q)) & 63u;
+                const int lx = lc & 3, ly = (lc >> 2) & 3, lz = lc >> 4;
+                const SlotFieldSmem<128> of{&rowtab[0][(threadIdx.x & ~31) + owner]};
+                float c[8];
+                of.corners(lx, ly, lz, c);
+                s.item_info[it] = make_uint4(o_ek, o_er, o_eb, (uint32_t)(lx | (ly << 3) | (lz << 6)) | (q << 9));
+                s.item_corners[2 * (int64_t)it] = make_float4(c[0], c[1], c[2], c[3]);
+                s.item_corners[2 * (int64_t)it + 1] = make_float4(c[4], c[5], c[6], c[7]);
             }
         }
+        __syncwarp();  // the row pointers are refilled by the next entries
     }
 }
 
