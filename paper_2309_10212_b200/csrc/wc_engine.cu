@@ -21,7 +21,7 @@
 // float64-heavy kernels; trades registers for latency hiding (tuned on B200
 // with scripts/gpu_variants.sh).
 #ifndef WC_TRAVERSE_MIN_CTAS
-#define WC_TRAVERSE_MIN_CTAS 6
+#define WC_TRAVERSE_MIN_CTAS 5
 #endif
 // 1: two-phase raytrace (k_rt_find / k_rt_solve / k_rt_shade); 0: fused k_raytrace.
 #ifndef WC_SPLIT_RAYTRACE
