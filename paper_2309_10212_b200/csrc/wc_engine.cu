@@ -49,6 +49,9 @@
 #ifndef WC_REFILL_MIN
 #define WC_REFILL_MIN 8
 #endif
+#ifndef WC_RTFIND_MIN_CTAS
+#define WC_RTFIND_MIN_CTAS 8
+#endif
 #ifndef WC_RAYTRACE_MIN_CTAS
 #define WC_RAYTRACE_MIN_CTAS 6
 #endif
@@ -1272,7 +1275,7 @@ __device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, const RayVi
 }
 
 // phase 1: walk each entry's dual cells, list the bracketing ones
-__global__ void __launch_bounds__(128) k_rt_find(SplitArgs s) {
+__global__ void __launch_bounds__(128, WC_RTFIND_MIN_CTAS) k_rt_find(SplitArgs s) {
     pdl_wait();
     const RaytraceArgs &a = s.a;
     RayView rv = a.rays;
