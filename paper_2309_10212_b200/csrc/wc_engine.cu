@@ -52,6 +52,9 @@
 #ifndef WC_RTFIND_MIN_CTAS
 #define WC_RTFIND_MIN_CTAS 8
 #endif
+#ifndef WC_ISO_MIN_CTAS
+#define WC_ISO_MIN_CTAS 1
+#endif
 #ifndef WC_RAYTRACE_MIN_CTAS
 #define WC_RAYTRACE_MIN_CTAS 6
 #endif
@@ -775,7 +778,7 @@ __device__ __forceinline__ bool iso_in_q(const ushort2 v, uint32_t qi, const dou
 // Only coarse cells whose own range test passes are filled: the traversal
 // reads a cell's mask only after descending into it (traversal.py:357), so
 // the others are left 0.
-__global__ void k_iso_cell_mask(const ushort2 *__restrict__ q, const double2 *__restrict__ mm,
+__global__ void __launch_bounds__(256, WC_ISO_MIN_CTAS) k_iso_cell_mask(const ushort2 *__restrict__ q, const double2 *__restrict__ mm,
                                 const uint32_t *__restrict__ coarse_bm, int fdx, int fdy, int fdz, int cdx, int cdy,
                                 int cdz, double iso, double base, double inv,
                                 unsigned long long *__restrict__ cell_mask, int64_t c_begin, int64_t c_end) {
