@@ -386,7 +386,7 @@ def run_b200(args):
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"], line["parity"] = cpu_baseline(args, wl, cv, iso, fb)
-    print(json.dumps(line), flush=True)
+    emit(line)
     sess.close()
     if sharded:
         torch.distributed.destroy_process_group()
@@ -471,7 +471,7 @@ def run_reference(args):
         "note": "reference is pure Python+numba (no C/C++ to compile); its CPU path is timed through oracle/, "
                 "the bit-exact C port pinned to the reference's golden vectors",
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_c5(args):
@@ -522,10 +522,30 @@ def run_c5(args):
         "clocks": clk.summary(),
         "setup_s": round(setup_s, 2),
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+# The JSON line is the only thing bench.py writes to stdout: native
+# libraries print banners on file descriptor 1 (NCCL prints its version at
+# communicator init), so fd 1 is pointed at stderr for the run and the line
+# goes to the original stdout.
+_JSON_FD = None
+
+
+def emit(line):
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
 
 
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         run_reference(args)
