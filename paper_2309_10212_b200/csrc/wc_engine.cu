@@ -55,6 +55,12 @@
 #ifndef WC_ISO_MIN_CTAS
 #define WC_ISO_MIN_CTAS 1
 #endif
+#ifndef WC_RTFIND_GRID
+#define WC_RTFIND_GRID 64
+#endif
+#ifndef WC_RTSHADE_GRID
+#define WC_RTSHADE_GRID 16
+#endif
 #ifndef WC_RAYTRACE_MIN_CTAS
 #define WC_RAYTRACE_MIN_CTAS 6
 #endif
@@ -2282,11 +2288,11 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
         sa.item_t = item_t.p;
         sa.best = best.p;
         sa.n_items = ctl + C_NITEMS;
-        launch_pdl(k_rt_find, grid_for(n, 128, 16), 128, 0, st, sa);
+        launch_pdl(k_rt_find, grid_for(n, 128, WC_RTFIND_GRID), 128, 0, st, sa);
         WC_LAUNCH_CHECK();
         launch_pdl(k_rt_solve, grid_for(sa.item_cap, 128, WC_RAYTRACE_MIN_CTAS), 128, 0, st, sa);
         WC_LAUNCH_CHECK();
-        launch_pdl(k_rt_shade, grid_for(n, 128, 16), 128, 0, st, sa);
+        launch_pdl(k_rt_shade, grid_for(n, 128, WC_RTSHADE_GRID), 128, 0, st, sa);
         WC_LAUNCH_CHECK();
     } else {
         launch_pdl(k_raytrace, grid_for(n, 128, 16), 128, 0, st, ra);
