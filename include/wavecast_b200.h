@@ -26,6 +26,7 @@ extern "C" {
 
 typedef struct wc_volume wc_volume;
 typedef struct wc_session wc_session;
+typedef struct wc_cache wc_cache;
 
 /* engine.py:66-77 PassStats (+ evicted, n_entries, n_active_after) */
 typedef struct {
@@ -216,6 +217,78 @@ int wc_reference_render_dense(const float *values, int nx, int ny, int nz, const
 /* prims.py:13-40 on the device (host arrays in/out) */
 int wc_exclusive_scan(const uint32_t *values, int64_t n, uint32_t *out, uint64_t *total);
 int wc_sort_by_key(uint32_t *keys, uint32_t *values, int64_t n);
+/* compact (prims.py:26-31): indices i < n with mask[i] != 0, ascending */
+int wc_compact_indices(const uint8_t *mask, int64_t n, uint32_t *out, uint64_t *total);
+
+/* ---- stage-level entry points: the reference's lower-level API
+ * (wavecast/__init__.py:3-56), each one stage on the device with host
+ * arrays in and out, for callers and tests that drive the stages one at a
+ * time.  The render session above fuses the same stages into one pipeline. */
+
+/* traverse_to_next_blocks (traversal.py:406-452): advance every active ray
+ * (status == 0) to its next <= n_spec candidate blocks.  Grids from `v`
+ * (its device copy) or, when v is NULL, from the four float64 arrays
+ * (MacrocellGrids, grids.py:32-45).  RaySoA fields in/out as in
+ * traversal.py:76-91; block_slots / ray_slots (n) are overwritten.
+ * active_offsets (n, int64) must number the active rays 0..n_active-1.
+ * variant: 0 as the session picks, 1 thread per ray, 2 warp per ray.
+ * Slot budget (n_active * n_spec <= n, traversal.py:420) -> WC_E_INVARIANT. */
+int wc_traverse(const wc_volume *v, const double *fine_min, const double *fine_max, const double *coarse_min,
+                const double *coarse_max, const int *fine_dims, const int *coarse_dims, int64_t n,
+                const double *origin, const double *dir, const double *t_exit, const uint8_t *status, uint8_t *exited,
+                uint32_t *coarse_cell, double *coarse_tmax, uint32_t *fine_cell, double *fine_tmax,
+                uint32_t *block_slots, uint32_t *ray_slots, const int64_t *active_offsets, double iso, int n_spec,
+                int variant);
+/* mark_blocks (engine.py:97-118): visible / active block sets as bitmaps
+ * (bit b of word b / 32), ceil(bdx*bdy*bdz / 32) words each. */
+int wc_mark_blocks(const uint32_t *block_slots, int64_t n, int bdx, int bdy, int bdz, uint32_t *visible_words,
+                   uint32_t *active_words);
+/* build_rt_inputs (engine.py:121-149).  visible_words: the visible mask as a
+ * bitmap.  Output capacities: visible_ids / rays_per_block /
+ * block_ray_offsets n_blocks + 1, sorted_* n, valid_prefix n.
+ * sizes[3] = n_entries, n_visible, len(rays_per_block). */
+int wc_build_rt_inputs(const uint32_t *block_slots, const uint32_t *ray_slots, int64_t n,
+                       const uint32_t *visible_words, int64_t n_blocks, uint32_t *visible_ids,
+                       uint32_t *rays_per_block, uint32_t *block_ray_offsets, uint32_t *sorted_ray_ids,
+                       uint32_t *sorted_hit_slots, uint32_t *valid_prefix, int64_t *sizes);
+/* composite (engine.py:222-283): rgbz (n_rgbz x 3 float32 + n_rgbz float32),
+ * ray status (in/out) / exited (n), slot buffers (n_slots), framebuffer
+ * RGBA8 (n x 4, in/out) and depth (n, in/out). */
+int wc_composite(const float *rgbz_rgb, const float *rgbz_z, int64_t n_rgbz, int64_t n, uint8_t *status,
+                 const uint8_t *exited, const int64_t *active_offsets, int n_spec, const uint32_t *block_slots,
+                 int64_t n_slots, const uint32_t *valid_prefix, uint8_t *rgba, float *depth);
+
+/* BlockCache (cache.py:21-111) on the device: the session's cache update
+ * (stamp, miss list, growth to ceil(1.5 needed), (last_used, id) victims,
+ * decode straight into the slots) one ensure_resident at a time. */
+int wc_cache_create(int64_t capacity_slots, wc_cache **out);
+int wc_cache_destroy(wc_cache *c);
+/* active_words: the active mask as a bitmap over n_blocks (== the volume's);
+ * needed = its popcount.  Returns CacheUpdateStats (cache.py:20-24). */
+int wc_cache_ensure_resident(wc_cache *c, const wc_volume *v, const uint32_t *active_words, int64_t n_blocks,
+                             int64_t needed, int64_t *new_decompressed, int64_t *evicted, int64_t *grown_to);
+/* logical capacity, physical (initialised) slots, pass counter, block count */
+int wc_cache_info(const wc_cache *c, int64_t *capacity, int64_t *physical, int64_t *current_pass, int64_t *n_blocks);
+/* lookup (cache.py:55-60): slot of a resident block or -1 */
+int wc_cache_lookup(wc_cache *c, int64_t block_id, int64_t *slot);
+/* slot_values (physical x 64), block_of_slot / last_used (physical),
+ * slot_of_block (n_blocks); each nullable */
+int wc_cache_state(wc_cache *c, float *slot_values, int32_t *block_of_slot, int32_t *last_used, int32_t *slot_of_block);
+/* assemble_dual_grid (blocktrace.py:113-123): the 5^3 dual grid ([z][y][x])
+ * of a resident block from its +octant contributors */
+int wc_cache_dual_grid(wc_cache *c, int64_t block_id, float *values125);
+
+/* blocktrace.py, batched over n cells / rays:
+ * intersect_cell (:452-472): smallest root in [t0, t1] or +inf;
+ * _cell_overlap (:126-158); shade (:475-488) of a gradient;
+ * raytrace_block (:491-530): trace the block's dual cells per ray. */
+int wc_intersect_cells(int64_t n, const float *corners, const double *origin, const double *dir, const double *cell,
+                       const double *t0, const double *t1, double iso, double *t_out);
+int wc_cell_overlaps(int64_t n, const double *origin, const double *dir, const double *cell, double *t0, double *t1);
+int wc_shade(int64_t n, const double *grad, const double *dir, const double *base_color, double *rgb);
+int wc_raytrace_block(const float *values125, const int *block_origin, const int *cells_per_axis, int64_t n,
+                      const double *origin, const double *dir, const double *t_enter, double iso,
+                      const double *base_color, float *rgb, float *z, uint8_t *hit);
 
 #ifdef __cplusplus
 }

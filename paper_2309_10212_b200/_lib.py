@@ -121,8 +121,24 @@ _SIGS = {
     "wc_init_rays": (_i32, [_vp, _vp, _i64, _vp, _vp, _i32, _i32, _i32] + [_vp] * 9),
     "wc_reference_render": (_i32, [_vp, _vp, _vp, _i64, _dbl, _dbl, _dbl, _dbl, _vp, _vp]),
     "wc_reference_render_dense": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, _i64, _dbl, _dbl, _dbl, _dbl, _vp, _vp]),
+    "wc_traverse": (_i32, [_vp] * 7 + [_i64] + [_vp] * 12 + [_dbl, _i32, _i32]),
+    "wc_mark_blocks": (_i32, [_vp, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "wc_build_rt_inputs": (_i32, [_vp, _vp, _i64, _vp, _i64] + [_vp] * 7),
+    "wc_composite": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp, _i64, _vp, _vp, _vp]),
+    "wc_cache_create": (_i32, [_i64, _vp]),
+    "wc_cache_destroy": (_i32, [_vp]),
+    "wc_cache_ensure_resident": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "wc_cache_info": (_i32, [_vp] * 5),
+    "wc_cache_lookup": (_i32, [_vp, _i64, _vp]),
+    "wc_cache_state": (_i32, [_vp] * 5),
+    "wc_cache_dual_grid": (_i32, [_vp, _i64, _vp]),
+    "wc_intersect_cells": (_i32, [_i64] + [_vp] * 6 + [_dbl, _vp]),
+    "wc_cell_overlaps": (_i32, [_i64] + [_vp] * 5),
+    "wc_shade": (_i32, [_i64] + [_vp] * 4),
+    "wc_raytrace_block": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _dbl, _vp, _vp, _vp, _vp]),
     "wc_exclusive_scan": (_i32, [_vp, _i64, _vp, _vp]),
     "wc_sort_by_key": (_i32, [_vp, _vp, _i64]),
+    "wc_compact_indices": (_i32, [_vp, _i64, _vp, _vp]),
 }
 
 _lib = None

@@ -9,6 +9,7 @@
 
 #include "../../include/wavecast_b200.h"
 #include "wc_engine.cuh"
+#include "wc_stage.cuh"
 
 struct wc_volume {
     wc::Volume v;
@@ -16,6 +17,9 @@ struct wc_volume {
 struct wc_session {
     wc::Session *s = nullptr;
     wc_volume *vol = nullptr;
+};
+struct wc_cache {
+    wc::StageCache *c = nullptr;
 };
 
 static thread_local std::string g_err;
@@ -785,6 +789,46 @@ int wc_exclusive_scan(const uint32_t *values, int64_t n, uint32_t *out, uint64_t
     WC_API_END
 }
 
+namespace {
+struct PredMaskU8 {
+    const uint8_t *m;
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const { return m[i] != 0; }
+};
+__global__ void k_iota(uint32_t *p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (uint32_t)i;
+}
+}  // namespace
+
+int wc_compact_indices(const uint8_t *mask, int64_t n, uint32_t *out, uint64_t *total) {
+    WC_API_BEGIN
+    if (n <= 0) {
+        if (total) *total = 0;
+        return WC_OK;
+    }
+    cudaStream_t st;
+    WC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    wc::DevBuf<uint8_t> d_m;
+    wc::DevBuf<uint32_t> d_idx, d_out, d_part, d_tot;
+    upload(d_m, mask, n, st);
+    d_idx.alloc(n);
+    k_iota<<<wc::grid_for(n, 256), 256, 0, st>>>(d_idx.p, n);
+    WC_LAUNCH_CHECK();
+    d_out.alloc(n);
+    d_part.alloc(wc::scan_scratch_words(n));
+    WC_CUDA(cudaMemsetAsync(d_part.p, 0, 4 * d_part.n, st));
+    d_tot.alloc(1);
+    wc::compact_dev(PredMaskU8{d_m.p}, d_idx.p, nullptr, n, d_out.p, d_tot.p, d_part.p, st);
+    uint32_t t = 0;
+    download(&t, d_tot.p, 1, st);
+    WC_CUDA(cudaStreamSynchronize(st));
+    download(out, d_out.p, t, st);
+    WC_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    if (total) *total = t;
+    WC_API_END
+}
+
 int wc_sort_by_key(uint32_t *keys, uint32_t *values, int64_t n) {
     WC_API_BEGIN
     if (n <= 1) return WC_OK;
@@ -799,6 +843,143 @@ int wc_sort_by_key(uint32_t *keys, uint32_t *values, int64_t n) {
     download(values, dv.p, n, st);
     WC_CUDA(cudaStreamSynchronize(st));
     cudaStreamDestroy(st);
+    WC_API_END
+}
+
+/* ---- stage-level entry points (wc_stage.cu) */
+
+int wc_traverse(const wc_volume *v, const double *fine_min, const double *fine_max, const double *coarse_min,
+                const double *coarse_max, const int *fine_dims, const int *coarse_dims, int64_t n,
+                const double *origin, const double *dir, const double *t_exit, const uint8_t *status, uint8_t *exited,
+                uint32_t *coarse_cell, double *coarse_tmax, uint32_t *fine_cell, double *fine_tmax,
+                uint32_t *block_slots, uint32_t *ray_slots, const int64_t *active_offsets, double iso, int n_spec,
+                int variant) {
+    WC_API_BEGIN
+    WC_REQUIRE(n >= 0, wc::UsageError, "negative ray count");
+    WC_REQUIRE(v || (fine_min && fine_max && coarse_min && coarse_max), wc::UsageError, "no grids");
+    wc::stage_traverse(v ? &v->v : nullptr, fine_min, fine_max, coarse_min, coarse_max, fine_dims, coarse_dims, n,
+                       origin, dir, t_exit, status, exited, coarse_cell, coarse_tmax, fine_cell, fine_tmax,
+                       block_slots, ray_slots, active_offsets, iso, n_spec, variant);
+    WC_API_END
+}
+
+int wc_mark_blocks(const uint32_t *block_slots, int64_t n, int bdx, int bdy, int bdz, uint32_t *visible_words,
+                   uint32_t *active_words) {
+    WC_API_BEGIN
+    WC_REQUIRE(bdx > 0 && bdy > 0 && bdz > 0, wc::UsageError, "block dims must be positive");
+    wc::stage_mark_blocks(block_slots, n, bdx, bdy, bdz, visible_words, active_words);
+    WC_API_END
+}
+
+int wc_build_rt_inputs(const uint32_t *block_slots, const uint32_t *ray_slots, int64_t n,
+                       const uint32_t *visible_words, int64_t n_blocks, uint32_t *visible_ids,
+                       uint32_t *rays_per_block, uint32_t *block_ray_offsets, uint32_t *sorted_ray_ids,
+                       uint32_t *sorted_hit_slots, uint32_t *valid_prefix, int64_t *sizes) {
+    WC_API_BEGIN
+    WC_REQUIRE(n >= 0 && n_blocks >= 0, wc::UsageError, "negative size");
+    wc::stage_build_rt_inputs(block_slots, ray_slots, n, visible_words, n_blocks, visible_ids, rays_per_block,
+                              block_ray_offsets, sorted_ray_ids, sorted_hit_slots, valid_prefix, sizes);
+    WC_API_END
+}
+
+int wc_composite(const float *rgbz_rgb, const float *rgbz_z, int64_t n_rgbz, int64_t n, uint8_t *status,
+                 const uint8_t *exited, const int64_t *active_offsets, int n_spec, const uint32_t *block_slots,
+                 int64_t n_slots, const uint32_t *valid_prefix, uint8_t *rgba, float *depth) {
+    WC_API_BEGIN
+    WC_REQUIRE(n_spec >= 1, wc::UsageError, "n_spec must be >= 1");
+    wc::stage_composite(rgbz_rgb, rgbz_z, n_rgbz, n, status, exited, active_offsets, n_spec, block_slots, n_slots,
+                        valid_prefix, rgba, depth);
+    WC_API_END
+}
+
+int wc_cache_create(int64_t capacity_slots, wc_cache **out) {
+    WC_API_BEGIN
+    auto *h = new wc_cache();
+    try {
+        h->c = new wc::StageCache(capacity_slots);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    WC_API_END
+}
+
+int wc_cache_destroy(wc_cache *c) {
+    WC_API_BEGIN
+    if (c) {
+        delete c->c;
+        delete c;
+    }
+    WC_API_END
+}
+
+int wc_cache_ensure_resident(wc_cache *c, const wc_volume *v, const uint32_t *active_words, int64_t n_blocks,
+                             int64_t needed, int64_t *new_decompressed, int64_t *evicted, int64_t *grown_to) {
+    WC_API_BEGIN
+    WC_REQUIRE(c && v, wc::UsageError, "null handle");
+    WC_REQUIRE(n_blocks == v->v.n_blocks, wc::UsageError, "active mask length differs from the block count");
+    c->c->ensure_resident(&v->v, active_words, needed, new_decompressed, evicted, grown_to);
+    WC_API_END
+}
+
+int wc_cache_info(const wc_cache *c, int64_t *capacity, int64_t *physical, int64_t *current_pass, int64_t *n_blocks) {
+    WC_API_BEGIN
+    WC_REQUIRE(c, wc::UsageError, "null handle");
+    if (capacity) *capacity = c->c->cap;
+    if (physical) *physical = c->c->vol ? c->c->phys : 0;
+    if (current_pass) *current_pass = c->c->current_pass;
+    if (n_blocks) *n_blocks = c->c->n_blocks;
+    WC_API_END
+}
+
+int wc_cache_lookup(wc_cache *c, int64_t block_id, int64_t *slot) {
+    WC_API_BEGIN
+    WC_REQUIRE(c, wc::UsageError, "null handle");
+    *slot = c->c->lookup(block_id);
+    WC_API_END
+}
+
+int wc_cache_state(wc_cache *c, float *slot_values, int32_t *block_of_slot, int32_t *last_used,
+                   int32_t *slot_of_block) {
+    WC_API_BEGIN
+    WC_REQUIRE(c, wc::UsageError, "null handle");
+    c->c->download(slot_values, block_of_slot, last_used, slot_of_block);
+    WC_API_END
+}
+
+int wc_cache_dual_grid(wc_cache *c, int64_t block_id, float *values125) {
+    WC_API_BEGIN
+    WC_REQUIRE(c, wc::UsageError, "null handle");
+    c->c->dual_grid(block_id, values125);
+    WC_API_END
+}
+
+int wc_intersect_cells(int64_t n, const float *corners, const double *origin, const double *dir, const double *cell,
+                       const double *t0, const double *t1, double iso, double *t_out) {
+    WC_API_BEGIN
+    wc::stage_intersect_cells(n, corners, origin, dir, cell, t0, t1, iso, t_out);
+    WC_API_END
+}
+
+int wc_cell_overlaps(int64_t n, const double *origin, const double *dir, const double *cell, double *t0, double *t1) {
+    WC_API_BEGIN
+    wc::stage_cell_overlaps(n, origin, dir, cell, t0, t1);
+    WC_API_END
+}
+
+int wc_shade(int64_t n, const double *grad, const double *dir, const double *base_color, double *rgb) {
+    WC_API_BEGIN
+    wc::stage_shade(n, grad, dir, base_color, rgb);
+    WC_API_END
+}
+
+int wc_raytrace_block(const float *values125, const int *block_origin, const int *cells_per_axis, int64_t n,
+                      const double *origin, const double *dir, const double *t_enter, double iso,
+                      const double *base_color, float *rgb, float *z, uint8_t *hit) {
+    WC_API_BEGIN
+    wc::stage_raytrace_block(values125, block_origin, cells_per_axis, n, origin, dir, t_enter, iso, base_color, rgb, z,
+                             hit);
     WC_API_END
 }
 

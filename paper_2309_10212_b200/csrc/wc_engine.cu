@@ -215,52 +215,6 @@ __global__ void k_compact_index(Pred pred, int64_t n, const uint32_t *off, uint3
 
 // --------------------------------------------------------------- traverse
 
-struct RayView {
-    const double *origin;  // nullable -> eye
-    const double *dir, *t_enter;
-    const double *eye;  // FrameParams (device): the camera eye of this frame
-    double ex = 0.0, ey = 0.0, ez = 0.0;
-    __device__ __forceinline__ void bind() {  // once per kernel: the eye into registers
-        if (!origin) {
-            ex = eye[0];
-            ey = eye[1];
-            ez = eye[2];
-        }
-    }
-    __device__ __forceinline__ void load(int64_t r, double o[3], double d[3]) const {
-        if (origin) {
-            o[0] = origin[3 * r];
-            o[1] = origin[3 * r + 1];
-            o[2] = origin[3 * r + 2];
-        } else {
-            o[0] = ex;
-            o[1] = ey;
-            o[2] = ez;
-        }
-        d[0] = dir[3 * r];
-        d[1] = dir[3 * r + 1];
-        d[2] = dir[3 * r + 2];
-    }
-};
-
-struct TraverseArgs {
-    RayView rays;
-    const double *t_exit;
-    uint8_t *exited;
-    uint32_t *coarse_cell, *fine_cell;
-    double *coarse_tmax, *fine_tmax;
-    const uint32_t *act_list;
-    int64_t n_act;
-    int n_spec;
-    const uint32_t *coarse_bm;                // per-iso coarse range-test bitmap (k_iso_bitmap)
-    const unsigned long long *cell_mask;  // per-iso fine tests, one word per coarse cell (k_iso_cell_mask)
-    int fdx, fdy, fdz, cdx, cdy, cdz;
-    double iso;
-    uint32_t *block_slots, *ray_slots, *emitted, *vis_bm;
-    uint32_t *work;        // persistent-kernel ray counter (zeroed per pass)
-    const uint32_t *ctl;   // control block: n_act and n_spec of the pass (Counter)
-};
-
 // Mark block b visible: one RED.OR per distinct block among the lanes that
 // emit together (warp match), traversal emission fused with mark_blocks
 // (engine.py:97-106).
@@ -884,6 +838,30 @@ __global__ void k_mark_active_words(const uint32_t *visible_ids, const uint32_t 
     }
 }
 
+void launch_traverse(const TraverseArgs &ta, int64_t n_grid, int64_t nact_guess, int variant, cudaStream_t st) {
+    if (variant == 2 || (variant == 0 && nact_guess <= WC_WARP_TRAVERSE_MAX))  // few (long) rays: warp-cooperative DDA
+        launch_pdl(k_traverse_warp, grid_for(std::max<int64_t>(1, nact_guess) * 32, 128, 16), 128, 0, st, ta);
+    else
+        launch_pdl(k_traverse<WC_COARSE_AHEAD>, grid_for(n_grid, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st, ta);
+    WC_LAUNCH_CHECK();
+}
+
+void launch_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvis, const uint32_t *vis_bm, int bdx, int bdy,
+                        int bdz, int64_t n_max, uint32_t *act_bm, cudaStream_t st) {
+    if (bdx % 32 == 0)
+        launch_pdl(k_mark_active_words, grid_for(n_max, 256), 256, 0, st, visible_ids, d_nvis, vis_bm, bdx / 32, bdy, bdz,
+                   act_bm);
+    else
+        launch_pdl(k_mark_active, grid_for(8 * n_max, 256), 256, 0, st, visible_ids, d_nvis, bdx, bdy, bdz, act_bm);
+    WC_LAUNCH_CHECK();
+}
+
+void launch_iso_bitmap(const double2 *mm, int64_t n, double iso, uint32_t *bm, cudaStream_t st) {
+    const int64_t nw = ceil_div(n, 32);
+    launch_pdl(k_iso_bitmap, grid_for(nw * 32, 256, 8), 256, 0, st, mm, n, iso, bm, (int64_t)0, nw);
+    WC_LAUNCH_CHECK();
+}
+
 // Entries of active ray i: k = entry_off[i] + j for its j-th emitted slot
 // (== valid_prefix of the slot, engine.py:124-128).  Key = rank of the block
 // among visible ids (bitmap rank), value = k.
@@ -1245,11 +1223,13 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_raytrace(Raytrace
 // start from one coalesced read instead of the entry -> ray -> block -> slot
 // chain: info = (entry k, ray r, block b, lx | ly << 3 | lz << 6 | seq << 9)
 // and the cell's 8 float corners (corner order idx = dx + 2 dy + 4 dz).
+constexpr unsigned long long kNoRoot = ~0ull;
 struct SplitArgs {
     RaytraceArgs a;
     uint4 *item_info;
     float4 *item_corners;  // 2 per item
-    uint32_t *n_items, *best;
+    uint32_t *n_items;
+    unsigned long long *best;  // per entry: (seq << 32 | item) of its earliest root
     double *item_t;
     int64_t item_cap;
 };
@@ -1309,7 +1289,7 @@ __global__ void __launch_bounds__(128, WC_RTFIND_MIN_CTAS) k_rt_find(SplitArgs s
             er = (uint32_t)e.r;
             eb = (uint32_t)(e.bx + a.bdx * (e.by + a.bdy * e.bz));
             ef = e.field;
-            s.best[e.k] = WC_UINT_MAX;
+            s.best[e.k] = kNoRoot;
             const int sl[8] = {ef.s0, ef.s1, ef.s2, ef.s3, ef.s4, ef.s5, ef.s6, ef.s7};
             SlotFieldSmem<128>::fill(&rowtab[0][threadIdx.x], a.slot_values, sl);
             walk_bracketing_cells(sf, 4 * e.bx, 4 * e.by, 4 * e.bz, 4 * e.bx, 4 * e.by, 4 * e.bz, e.cx, e.cy,
@@ -1321,6 +1301,7 @@ __global__ void __launch_bounds__(128, WC_RTFIND_MIN_CTAS) k_rt_find(SplitArgs s
                                   });
             if (!found) a.rgbz[e.k] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
         }
+        __syncwarp();  // the owners' row pointers (shared memory) are read across the warp below
         // one list append per warp (a per-cell atomic on the shared counter
         // serialises at L2)
         uint32_t incl = (uint32_t)found;
@@ -1391,7 +1372,7 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArg
         const double th = solve_cell(c, o, d, 4 * bx + lx, 4 * by + ly, 4 * bz + lz, rv.t_enter[r], iso);
         if (th != CUDART_INF) {
             s.item_t[i] = th;
-            atomicMin(&s.best[k], ((uint32_t)seq << 27) | (uint32_t)i);
+            atomicMin(&s.best[k], ((unsigned long long)seq << 32) | (unsigned long long)i);
         }
     }
 }
@@ -1401,9 +1382,8 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArg
 // write their miss value; the hits of a warp's successive 32-entry rounds
 // are queued in shared memory and shaded 32 at a time, so every lane of a
 // shading round has a hit (most entries of a pass have none).
-__device__ __forceinline__ void shade_entry(const SplitArgs &s, const RayView &rv, uint32_t k, uint32_t bst) {
+__device__ __forceinline__ void shade_entry(const SplitArgs &s, const RayView &rv, uint32_t k, uint32_t i) {
     const RaytraceArgs &a = s.a;
-    const uint32_t i = bst & ((1u << 27) - 1u);
     const uint4 info = s.item_info[i];
     const float4 c0 = s.item_corners[2 * (int64_t)i], c1 = s.item_corners[2 * (int64_t)i + 1];
     const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
@@ -1424,7 +1404,7 @@ __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
     const RaytraceArgs &a = s.a;
     RayView rv = a.rays;
     rv.bind();
-    __shared__ uint2 queue[4][64];  // per warp: (entry, best) of the hits not yet shaded
+    __shared__ uint2 queue[4][64];  // per warp: (entry, winning item) of the hits not yet shaded
     uint2 *q = queue[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     int nq = 0;  // warp-uniform
@@ -1432,14 +1412,15 @@ __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); j0 < n_ent; j0 += stride) {
         const int64_t j = j0 + lane;
-        uint32_t k = 0, bst = WC_UINT_MAX;
+        uint32_t k = 0;
+        unsigned long long bst = kNoRoot;
         if (j < n_ent) {
             k = a.identity ? (uint32_t)j : a.ent_val[j];
             bst = s.best[k];
-            if (bst == WC_UINT_MAX) a.rgbz[k] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
+            if (bst == kNoRoot) a.rgbz[k] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
         }
-        const uint32_t hits = __ballot_sync(0xffffffffu, bst != WC_UINT_MAX);
-        if (bst != WC_UINT_MAX) q[nq + __popc(hits & ((1u << lane) - 1u))] = make_uint2(k, bst);
+        const uint32_t hits = __ballot_sync(0xffffffffu, bst != kNoRoot);
+        if (bst != kNoRoot) q[nq + __popc(hits & ((1u << lane) - 1u))] = make_uint2(k, (uint32_t)bst);
         nq += __popc(hits);
         __syncwarp();
         if (nq >= 32) {  // a full round of hits
@@ -1721,8 +1702,8 @@ __device__ __forceinline__ void pass_end(uint32_t *ctl, uint32_t *row, int64_t n
 
 // pass_end as the epilogue of the compaction of the surviving rays (its
 // count is n_after).  It rewrites the count that compaction reads
-// (ctl[C_NACT]) with n_after <= n_act, so a CTA reading it late still finds
-// no tile of its own.
+// (ctl[C_NACT]); a scan epilogue runs in the CTA that finishes last, after
+// every CTA of the scan has read the count (k_scan_onepass).
 struct PassEndEpilogue {
     uint32_t *ctl, *row;
     int64_t n;
@@ -2004,19 +1985,93 @@ void Session::read_counters(int first, int count) {
 void Session::reserve_slots(int64_t need) {
     if (need <= slot_alloc) return;
     drop_graphs();  // they hold the old buffers
+    reserve_store(need, std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n}), partials, st);
+}
+
+bool CacheStore::reserve_store(int64_t need, int64_t scan_n, DevBuf<uint32_t> &partials, cudaStream_t st) {
+    if (need <= slot_alloc) return false;
     slot_values.grow(need * 64, st);
     block_of_slot.grow(need, st);
     last_used.grow(need, st);
     cand_key.alloc(need);
     cand_val.alloc(need);
     word_list.ensure(need);  // victim words <= resident slots
-    const int64_t words =
-        scan_scratch_words(std::max<int64_t>({n, ceil_div(vol->n_blocks, 32), active_ids.n, need}));
+    const int64_t words = scan_scratch_words(std::max<int64_t>(scan_n, need));
     if (partials.n < words) {
         partials.ensure(words);
         WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
     }
     slot_alloc = need;
+    return true;
+}
+
+bool CacheStore::prepare_regions(int64_t stamp, int64_t n_blocks, DevBuf<uint32_t> &partials, cudaStream_t st) {
+    if (vict_regions >= stamp) return false;
+    const int64_t nwords = ceil_div(n_blocks, 32);
+    const int64_t r = std::max<int64_t>(stamp, std::max<int64_t>(8, 2 * vict_regions));
+    vict_bm.alloc(r * nwords);
+    WC_CUDA(cudaMemsetAsync(vict_bm.p, 0, 4 * r * nwords, st));
+    vict_regions = r;
+    vict_sum.alloc(ceil_div(r * nwords, 32));
+    WC_CUDA(cudaMemsetAsync(vict_sum.p, 0, 4 * vict_sum.n, st));
+    const int64_t words = scan_scratch_words(r * nwords);
+    if (partials.n < words) {
+        partials.ensure(words);
+        WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
+    }
+    return true;
+}
+
+// cache.ensure_resident (cache.py:66-111): stamp hits, list misses
+// (ascending), then growth / victims / decode, all sized on the device
+void CacheStore::enqueue_lookup(uint32_t *ctl, const uint32_t *active_ids, int64_t nmax, int32_t stamp,
+                                int64_t n_blocks, uint32_t *partials, cudaStream_t st) {
+    launch_pdl(k_cache_stamp, grid_for(nmax, 256), 256, 0, st, active_ids, ctl + C_NACTB, nmax, slot_of_block.p,
+               last_used.p, stamp, ctl + C_COUNT);
+    WC_LAUNCH_CHECK();
+    // misses in ascending id order (cache.py:76-78), scan and compaction in
+    // one pass; the growth / eviction decisions (k_cache_plan) run as its
+    // epilogue while the stamp histogram is kept on the device
+    if (stamp < kHistBins)
+        compact_dev(PredMiss{active_ids, slot_of_block.p}, active_ids, ctl + C_NACTB, nmax, miss_ids.p, ctl + C_NMISS,
+                    partials, st, CachePlanEpilogue{ctl, ctl + C_COUNT, stamp, n_blocks, slot_alloc});
+    else
+        compact_dev(PredMiss{active_ids, slot_of_block.p}, active_ids, ctl + C_NACTB, nmax, miss_ids.p, ctl + C_NMISS,
+                    partials, st);
+}
+
+void CacheStore::enqueue_slow_plan(uint32_t *ctl, int32_t stamp, bool any_active, int64_t n_blocks, cudaStream_t st) {
+    stamp_hist.ensure(stamp + 1);
+    WC_CUDA(cudaMemsetAsync(stamp_hist.p, 0, 4 * (stamp + 1), st));
+    if (any_active) {
+        launch_pdl(k_stamp_hist, grid_for(slot_alloc, 256), 256, 4 * (size_t)stamp, st, block_of_slot.p, last_used.p,
+                   ctl, stamp, stamp_hist.p);
+        WC_LAUNCH_CHECK();
+    }
+    launch_pdl(k_cache_plan, 1, 1, 0, st, ctl, stamp_hist.p, stamp, n_blocks, slot_alloc, false);
+    WC_LAUNCH_CHECK();
+}
+
+void CacheStore::enqueue_insert(uint32_t *ctl, int64_t nmax, int32_t stamp, const Volume *vol, uint32_t *partials,
+                                cudaStream_t st) {
+    const int64_t nwords = ceil_div(vol->n_blocks, 32);
+    if (stamp >= 2) {  // victims in (last_used, block_id) order: one extraction over the stamp regions
+        launch_pdl(k_mark_victims, grid_for(slot_alloc, 256), 256, 0, st, block_of_slot.p, last_used.p, ctl, stamp,
+                   nwords, vict_bm.p, vict_sum.p);
+        WC_LAUNCH_CHECK();
+        bitmap_extract_listed(vict_bm.p, vict_sum.p, (int64_t)stamp * nwords, slot_alloc, nwords, nullptr, cand_key.p,
+                              ctl + C_NCAND, true, word_list.p, ctl + C_NLIST, partials, st);  // clears the regions
+        launch_pdl(k_evict, grid_for(slot_alloc, 256), 256, 0, st, cand_key.p, ctl + C_NEVICT, slot_of_block.p,
+                   block_of_slot.p, cand_val.p);
+        WC_LAUNCH_CHECK();
+    }
+    // the misses' records decoded straight into their slots (free slots
+    // first, then the victims in order, cache.py:97-103); the kernel also
+    // initialises the slots this pass's growth brought into use
+    launch_pdl(k_decode_insert, grid_for(nmax * 32, kDecWarps * 32, WC_DEC_CTAS), kDecWarps * 32, 0, st,
+               vol->payload.p, vol->qbits, vol->stride, miss_ids.p, ctl, cand_val.p, slot_values.p, block_of_slot.p,
+               last_used.p, slot_of_block.p, stamp);
+    WC_LAUNCH_CHECK();
 }
 
 cudaEvent_t *Session::pass_events(int64_t p) {
@@ -2030,23 +2085,8 @@ cudaEvent_t *Session::pass_events(int64_t p) {
 // captured pass): the victim regions must hold one bitmap per stamp a
 // candidate can carry.  Reallocation invalidates the captured pass graphs.
 void Session::prepare_pass(int64_t p) {
-    const int64_t nwords = ceil_div(vol->n_blocks, 32);
-    const int64_t stamp = p + 1;
     pass_events(p);
-    if (vict_regions < stamp) {
-        const int64_t r = std::max<int64_t>(stamp, std::max<int64_t>(8, 2 * vict_regions));
-        vict_bm.alloc(r * nwords);
-        WC_CUDA(cudaMemsetAsync(vict_bm.p, 0, 4 * r * nwords, st));
-        vict_regions = r;
-        vict_sum.alloc(ceil_div(r * nwords, 32));
-        WC_CUDA(cudaMemsetAsync(vict_sum.p, 0, 4 * vict_sum.n, st));
-        const int64_t words = scan_scratch_words(r * nwords);
-        if (partials.n < words) {
-            partials.ensure(words);
-            WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
-        }
-        drop_graphs();
-    }
+    if (prepare_regions(p + 1, vol->n_blocks, partials, st)) drop_graphs();
 }
 
 void Session::drop_graphs() {
@@ -2172,76 +2212,28 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     ta.work = ctl + C_WORK;
     ta.ctl = ctl;
     // C_WORK and C_NITEMS are zero here (reset, or the last pass_end)
-    if (nact_guess <= WC_WARP_TRAVERSE_MAX)  // few (long) rays: warp-cooperative DDA per ray
-        launch_pdl(k_traverse_warp, grid_for(std::max<int64_t>(1, nact_guess) * 32, 128, 16), 128, 0, st, ta);
-    else
-        launch_pdl(k_traverse<WC_COARSE_AHEAD>, grid_for(n, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st, ta);
-    WC_LAUNCH_CHECK();
+    launch_traverse(ta, n, nact_guess, 0, st);
     mark(1);
     // entry compaction: exclusive scan of per-ray emitted counts
     scan_exclusive_dev(LoadU32{emitted.p}, ctl + C_NACT, n, entry_off.p, ctl + C_NENT, partials.p, st);
     // visible ids (ascending) + active marking, from the maintained
     // summaries: the cost follows the non-zero bitmap words
     bitmap_extract_dense(vis_bm.p, nwords, vis_word_off.p, visible_ids.p, ctl + C_NVIS, false, partials.p, st);
-    if (vol->bdx % 32 == 0)
-        launch_pdl(k_mark_active_words, grid_for(n, 256), 256, 0, st, visible_ids.p, ctl + C_NVIS, vis_bm.p, vol->bdx / 32,
-                                                              vol->bdy, vol->bdz, act_bm.p);
-    else
-        launch_pdl(k_mark_active, grid_for((int64_t)8 * n, 256), 256, 0, st, visible_ids.p, ctl + C_NVIS, vol->bdx, vol->bdy,
-                                                                     vol->bdz, act_bm.p);
-    WC_LAUNCH_CHECK();
+    launch_mark_active(visible_ids.p, ctl + C_NVIS, vis_bm.p, vol->bdx, vol->bdy, vol->bdz, n, act_bm.p, st);
     bitmap_extract_dense(act_bm.p, nwords, nullptr, active_ids.p, ctl + C_NACTB, true, partials.p, st);  // clears act_bm
     launch_pdl(k_build_entries, grid_for(n, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p,
                                                       vis_word_off.p, ent_key.p, ent_val.p, ent_ray.p, ent_blk.p);
     WC_LAUNCH_CHECK();  // vis_bm is cleared by k_contrib
 
-    // cache.ensure_resident (cache.py:66-111): stamp hits, list misses
-    // (ascending), then growth / victims / decode, all sized on the device
+    // cache.ensure_resident (cache.py:66-111), sized on the device
     const int64_t nmax = active_ids.n - 1;  // upper bound of the active-block count
-    const bool hist = stamp < kHistBins;  // the histogram after the counters is kept current by the passes
-    launch_pdl(k_cache_stamp, grid_for(nmax, 256), 256, 0, st, active_ids.p, ctl + C_NACTB, nmax, slot_of_block.p, last_used.p,
-                                                      stamp, ctl + C_COUNT);
-    WC_LAUNCH_CHECK();
-    // misses in ascending id order (cache.py:76-78), scan and compaction in
-    // one pass; the growth / eviction decisions (k_cache_plan) run as its
-    // epilogue when the stamp histogram is kept on the device
-    if (hist)
-        compact_dev(PredMiss{active_ids.p, slot_of_block.p}, active_ids.p, ctl + C_NACTB, nmax, miss_ids.p,
-                    ctl + C_NMISS, partials.p, st, CachePlanEpilogue{ctl, ctl + C_COUNT, stamp, vol->n_blocks, slot_alloc});
-    else
-        compact_dev(PredMiss{active_ids.p, slot_of_block.p}, active_ids.p, ctl + C_NACTB, nmax, miss_ids.p,
-                    ctl + C_NMISS, partials.p, st);
+    enqueue_lookup(ctl, active_ids.p, nmax, stamp, vol->n_blocks, partials.p, st);
     mark(2);
-    if (!hist) {  // > kHistBins passes: histogram over all stamps through the host (rare)
+    if (stamp >= kHistBins) {  // > kHistBins passes: histogram over all stamps through the host (rare)
         read_counters(0, C_COUNT);
-        if (h_counters.p[C_NACT]) {
-            stamp_hist.ensure(stamp + 1);
-            h_stamp_hist.ensure_host(stamp + 1);
-            WC_CUDA(cudaMemsetAsync(stamp_hist.p, 0, 4 * (stamp + 1), st));
-            launch_pdl(k_stamp_hist, grid_for(slot_alloc, 256), 256, 4 * (size_t)stamp, st, block_of_slot.p,
-                       last_used.p, ctl, stamp, stamp_hist.p);
-            WC_LAUNCH_CHECK();
-        }
-        launch_pdl(k_cache_plan, 1, 1, 0, st, ctl, stamp_hist.p, stamp, vol->n_blocks, slot_alloc, false);
-        WC_LAUNCH_CHECK();
+        enqueue_slow_plan(ctl, stamp, h_counters.p[C_NACT] != 0, vol->n_blocks, st);
     }
-    if (p >= 1) {  // victims in (last_used, block_id) order: one extraction over the stamp regions
-        launch_pdl(k_mark_victims, grid_for(slot_alloc, 256), 256, 0, st, block_of_slot.p, last_used.p, ctl, stamp,
-                   nwords, vict_bm.p, vict_sum.p);
-        WC_LAUNCH_CHECK();
-        bitmap_extract_listed(vict_bm.p, vict_sum.p, (int64_t)stamp * nwords, slot_alloc, nwords, nullptr, cand_key.p,
-                              ctl + C_NCAND, true, word_list.p, ctl + C_NLIST, partials.p, st);  // clears the regions
-        launch_pdl(k_evict, grid_for(slot_alloc, 256), 256, 0, st, cand_key.p, ctl + C_NEVICT, slot_of_block.p,
-                   block_of_slot.p, cand_val.p);
-        WC_LAUNCH_CHECK();
-    }
-    // the misses' records decoded straight into their slots (free slots
-    // first, then the victims in order, cache.py:97-103); the kernel also
-    // initialises the slots this pass's growth brought into use
-    launch_pdl(k_decode_insert, grid_for(nmax * 32, kDecWarps * 32, WC_DEC_CTAS), kDecWarps * 32, 0, st, vol->payload.p,
-               vol->qbits, vol->stride, miss_ids.p, ctl, cand_val.p, slot_values.p, block_of_slot.p, last_used.p,
-               slot_of_block.p, stamp);
-    WC_LAUNCH_CHECK();
+    enqueue_insert(ctl, nmax, stamp, vol, partials.p, st);
     if (corrupt) WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * slot_alloc, st));  // engine.py:338-339
     mark(3);
 

@@ -60,6 +60,95 @@ enum PassLog : int {
     L_COUNT
 };
 
+// Ray state as the kernels read it (origin per ray, or the shared eye).
+struct RayView {
+    const double *origin;  // nullable -> eye
+    const double *dir, *t_enter;
+    const double *eye;  // FrameParams (device): the camera eye of this frame
+    double ex = 0.0, ey = 0.0, ez = 0.0;
+    __device__ __forceinline__ void bind() {  // once per kernel: the eye into registers
+        if (!origin) {
+            ex = eye[0];
+            ey = eye[1];
+            ez = eye[2];
+        }
+    }
+    __device__ __forceinline__ void load(int64_t r, double o[3], double d[3]) const {
+        if (origin) {
+            o[0] = origin[3 * r];
+            o[1] = origin[3 * r + 1];
+            o[2] = origin[3 * r + 2];
+        } else {
+            o[0] = ex;
+            o[1] = ey;
+            o[2] = ez;
+        }
+        d[0] = dir[3 * r];
+        d[1] = dir[3 * r + 1];
+        d[2] = dir[3 * r + 2];
+    }
+};
+
+struct TraverseArgs {
+    RayView rays;
+    const double *t_exit;
+    uint8_t *exited;
+    uint32_t *coarse_cell, *fine_cell;
+    double *coarse_tmax, *fine_tmax;
+    const uint32_t *act_list;
+    int64_t n_act;
+    int n_spec;
+    const uint32_t *coarse_bm;                // per-iso coarse range-test bitmap (k_iso_bitmap)
+    const unsigned long long *cell_mask;  // per-iso fine tests, one word per coarse cell (k_iso_cell_mask)
+    int fdx, fdy, fdz, cdx, cdy, cdz;
+    double iso;
+    uint32_t *block_slots, *ray_slots, *emitted, *vis_bm;
+    uint32_t *work;        // persistent-kernel ray counter (zeroed per pass)
+    const uint32_t *ctl;   // control block: n_act and n_spec of the pass (Counter)
+};
+
+// Traversal kernel launch (k_traverse / k_traverse_warp by the active-ray
+// count guess; variant 1 / 2 forces one of them).
+void launch_traverse(const TraverseArgs &ta, int64_t n_grid, int64_t nact_guess, int variant, cudaStream_t st);
+// +octant active marking from the visible ids (engine.py:107-117)
+void launch_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvis, const uint32_t *vis_bm, int bdx, int bdy,
+                        int bdz, int64_t n_max, uint32_t *act_bm, cudaStream_t st);
+// per-iso coarse range-test bitmap (traversal.py:357)
+void launch_iso_bitmap(const double2 *mm, int64_t n, double iso, uint32_t *bm, cudaStream_t st);
+
+// BlockCache device state (cache.py:21-111): the slot pool, both maps, the
+// miss / victim lists and the per-stamp victim regions, with the launches of
+// one ensure_resident.  Used by the render session (one update per pass,
+// control block shared with the pass) and by the standalone stage-level
+// BlockCache (wc_cache_*).  Sizes live in the control block `ctl`.
+struct CacheStore {
+    int64_t slot_alloc = 0;  // allocated slots (the session reserves its largest capacity up front)
+    DevBuf<float> slot_values;
+    DevBuf<int32_t> block_of_slot, last_used, slot_of_block;
+    DevBuf<uint32_t> miss_ids, cand_key, cand_val;
+    DevBuf<uint32_t> vict_bm;    // per-stamp block bitmaps for victim selection
+    DevBuf<uint32_t> vict_sum;   // summary of the victim regions
+    DevBuf<uint32_t> word_list;  // non-zero words listed by bitmap_extract_listed
+    int64_t vict_regions = 0;
+    DevBuf<uint32_t> stamp_hist;  // > kHistBins passes only
+
+    // slot storage for `need` slots (contents kept); scan scratch grown for
+    // scans over `scan_n` elements.  True when buffers moved.
+    bool reserve_store(int64_t need, int64_t scan_n, DevBuf<uint32_t> &partials, cudaStream_t st);
+    // victim regions for stamps [0, stamp]; true when reallocated
+    bool prepare_regions(int64_t stamp, int64_t n_blocks, DevBuf<uint32_t> &partials, cudaStream_t st);
+    // stamp the hits, list the misses (ascending); with stamp < kHistBins the
+    // growth / eviction plan runs as the epilogue of the miss compaction
+    void enqueue_lookup(uint32_t *ctl, const uint32_t *active_ids, int64_t nmax, int32_t stamp, int64_t n_blocks,
+                        uint32_t *partials, cudaStream_t st);
+    // stamp >= kHistBins: the plan from a full recount of the stamps
+    // (any_active: the pass has work; read on the host by the caller)
+    void enqueue_slow_plan(uint32_t *ctl, int32_t stamp, bool any_active, int64_t n_blocks, cudaStream_t st);
+    // victims in (last_used, block_id) order, eviction, decode into the slots
+    void enqueue_insert(uint32_t *ctl, int64_t nmax, int32_t stamp, const Volume *vol, uint32_t *partials,
+                        cudaStream_t st);
+};
+
 // Per-session device state.  Layout (N = rays in this session):
 //   ray SoA: dir f64[N*3] (origin f64[N*3] only for arbitrary rays; camera
 //   rays share `eye`), t_enter/t_exit f64[N], status/exited u8[N],
@@ -71,7 +160,7 @@ enum PassLog : int {
 //   cache: slot_values f32[phys*64], block_of_slot/last_used i32[phys],
 //          slot_of_block i32[n_blocks]
 //   framebuffer: rgba u32[N] (packed RGBA8), depth f32[N]
-struct Session {
+struct Session : CacheStore {
     Volume *vol = nullptr;
     cudaStream_t st = nullptr;
     int64_t n = 0;
@@ -97,7 +186,7 @@ struct Session {
     DevBuf<int4> contrib;  // 8 contributor slots per visible block
     DevBuf<uint4> item_info;  // two-phase raytrace work list (SplitArgs)
     DevBuf<float4> item_corners;
-    DevBuf<uint32_t> best;
+    DevBuf<unsigned long long> best;
     DevBuf<double> item_t;
     DevBuf<uint32_t> vis_bm, act_bm, vis_word_off;
     DevBuf<uint32_t> coarse_bm;            // per-iso coarse range-test bitmap, rebuilt at every reset
@@ -107,11 +196,7 @@ struct Session {
     DevBuf<float> depth;
     // cache (cache.py)
     int64_t cap = 0, phys = 0, hw = 0;
-    int64_t slot_alloc = 0;  // allocated slots (>= phys, grown geometrically)
     int32_t pass_no = 0;
-    DevBuf<float> slot_values;
-    DevBuf<int32_t> block_of_slot, last_used, slot_of_block;
-    DevBuf<uint32_t> miss_ids, cand_key, cand_val;
     // scratch
     DevBuf<uint32_t> counters, partials;
     PinnedBuf<uint32_t> h_counters;
@@ -136,12 +221,8 @@ struct Session {
     double pass_ms_hist[kMaxPassLog] = {};  // device ms per pass of the last frame (read-back scheduling)
     DevBuf<uint32_t> plog;          // kMaxPassLog x L_COUNT per-pass records (device)
     PinnedBuf<uint32_t> h_plog;
-    DevBuf<uint32_t> vict_bm;       // per-stamp block bitmaps for victim selection
     DevBuf<double> fparams;         // FrameParams: eye[3], iso, base colour[3] (written by k_frame_start)
     uint32_t frame_no = 0;
-    DevBuf<uint32_t> vict_sum;   // summary of the victim regions
-    DevBuf<uint32_t> word_list;  // non-zero words listed by bitmap_extract_listed
-    int64_t vict_regions = 0;
     int64_t last_slots_used = 0, last_nvis = 0, last_nactb = 0, last_nent = 0;
     int64_t last_n_spec = 1;
     float last_kernel_ms = 0.0f;
@@ -202,8 +283,6 @@ struct Session {
     DevBuf<uint32_t> snap_list;
     DevBuf<uint4> patch;
     PinnedBuf<uint4> h_patch;
-    DevBuf<uint32_t> stamp_hist;          // > kHistBins passes only
-    PinnedBuf<uint32_t> h_stamp_hist;
 };
 
 // Brute-force oracle on the device (oracle.py:42-122): every ray marches all

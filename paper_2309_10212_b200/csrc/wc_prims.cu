@@ -140,34 +140,44 @@ __global__ void __launch_bounds__(256, WC_DENSE_MIN_CTAS) k_bitmap_dense(uint32_
                                                       uint64_t *status, ScanEpoch ep, uint32_t *d_count) {
     pdl_wait();
     __shared__ uint32_t sw[32];
-    __shared__ uint32_t s_excl;
+    __shared__ uint32_t s_excl, s_ticket;
     const uint32_t epoch = resolve_epoch(ep);
     const int64_t chunk = 256LL * 4 * q16;
-    const int64_t t = blockIdx.x;
     const int64_t last = (nwords - 1) / chunk;
-    const int64_t w0 = t * chunk + (int64_t)threadIdx.x * 4 * q16;
+    bool lt = false;
+    uint32_t tk = 0;
+    if (threadIdx.x == 0) tk = take_ticket(status, lt);  // dynamic tile id (see k_scan_onepass)
     uint4 q[kDenseQ16];
-    uint32_t cnt = 0;
+    auto load = [&](int64_t tt) {
+        const int64_t w0 = tt * chunk + (int64_t)threadIdx.x * 4 * q16;
 #pragma unroll
-    for (int j = 0; j < kDenseQ16; j++) {
-        const int64_t w = w0 + 4 * j;
-        q[j] = make_uint4(0u, 0u, 0u, 0u);
-        if (j < q16) {
-            if (w + 4 <= nwords) {
-                q[j] = *reinterpret_cast<const uint4 *>(bm + w);
-            } else {
-                if (w < nwords) q[j].x = bm[w];
-                if (w + 1 < nwords) q[j].y = bm[w + 1];
-                if (w + 2 < nwords) q[j].z = bm[w + 2];
+        for (int j = 0; j < kDenseQ16; j++) {
+            const int64_t w = w0 + 4 * j;
+            q[j] = make_uint4(0u, 0u, 0u, 0u);
+            if (j < q16) {
+                if (w + 4 <= nwords) {
+                    q[j] = *reinterpret_cast<const uint4 *>(bm + w);
+                } else {
+                    if (w < nwords) q[j].x = bm[w];
+                    if (w + 1 < nwords) q[j].y = bm[w + 1];
+                    if (w + 2 < nwords) q[j].z = bm[w + 2];
+                }
             }
         }
-    }
+    };
+    load(blockIdx.x);  // speculative: the tile of blockIdx.x while the ticket is in flight
+    if (threadIdx.x == 0) s_ticket = tk;
+    __syncthreads();
+    const int64_t t = s_ticket;
+    if (t != (int64_t)blockIdx.x) load(t);
+    const int64_t w0 = t * chunk + (int64_t)threadIdx.x * 4 * q16;
+    uint32_t cnt = 0;
 #pragma unroll
     for (int j = 0; j < kDenseQ16; j++) cnt += __popc(q[j].x) + __popc(q[j].y) + __popc(q[j].z) + __popc(q[j].w);
     uint32_t agg;
     uint32_t pre = block_exclusive_scan(cnt, sw, &agg);
     if (threadIdx.x < 32) {
-        const uint32_t excl = tile_lookback(t, agg, status, epoch);
+        const uint32_t excl = tile_lookback(t, agg, tile_status(status), epoch);
         if (threadIdx.x == 0) {
             s_excl = excl;
             if (t == last) *d_count = excl + agg;
@@ -204,7 +214,7 @@ void bitmap_extract_dense(uint32_t *bm, int64_t nwords, uint32_t *word_offsets, 
     // about one wave of WC_DENSE_CTAS_PER_SM CTAs per SM, 1..kDenseQ16 16-byte groups per
     // thread (measured at C3: 8 x 4 beats 4 x 8, 2 x 16 and 8 x 1..3)
     // (larger bitmaps launch more waves)
-    const int64_t q16 = std::min<int64_t>(kDenseQ16, std::max<int64_t>(1, ceil_div(nwords, (int64_t)kNumSMs * WC_DENSE_CTAS_PER_SM * 256 * 4)));
+    const int64_t q16 = std::min<int64_t>(kDenseQ16, std::max<int64_t>(1, ceil_div(nwords, (int64_t)num_sms() * WC_DENSE_CTAS_PER_SM * 256 * 4)));
     const unsigned grid = (unsigned)ceil_div(nwords, 256 * 4 * q16);
     if (clear)
         launch_pdl(k_bitmap_dense<true>, grid, 256, 0, st, bm, nwords, (int)q16, word_offsets, ids,

@@ -76,8 +76,15 @@ __device__ __forceinline__ int64_t scan_count(int64_t n, const uint32_t *d_n) {
 // Each tile publishes its aggregate, then its inclusive prefix, in one
 // 64-bit status word [epoch:30 | flag:2 | value:32]; successors look back
 // over the status words with a warp.  The epoch tags every scan call, so
-// the status array never needs clearing.  Tiles only wait on lower-numbered
-// tiles, which the hardware dispatches first.  One launch per scan.
+// the status array never needs clearing.  One launch per scan.
+//
+// Tile ids are dynamic tickets (an atomic counter in the scratch header), so
+// a tile only ever waits on tiles whose CTAs are already running: forward
+// progress does not depend on the hardware dispatching CTAs in blockIdx
+// order, on how many CTAs fit per SM, or on other kernels sharing the GPU.
+// Every CTA reads the element count before it takes its ticket, and the
+// epilogue runs only once the last ticket is taken and the total is known,
+// so an epilogue may rewrite the count the scan itself read.
 constexpr uint32_t kFlagAggregate = 1, kFlagPrefix = 2;
 
 // Host-issued epochs have bit 29 set; epochs derived on the device (below)
@@ -107,8 +114,52 @@ __device__ __forceinline__ uint32_t resolve_epoch(const ScanEpoch e) {
     return v ? v : 0x1FFFFFFFu;
 }
 
-// scratch words (uint32) a scan over n elements needs
+// scratch words (uint32) a scan over n elements needs: a 64-bit header
+// (ticket and done counters, zero between scans) + one status word per tile
 inline int64_t scan_scratch_words(int64_t n) { return 2 * scan_tiles(n) + 8; }
+
+// Scratch header: word 0 = ticket counter, word 1 = epilogue arrivals; both
+// are zero between scans.
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t *p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+// Thread 0: this CTA's ticket (tile id), taken after the CTA has read its
+// inputs' count.  The CTA holding the last ticket resets the counter for the
+// next scan on this scratch (every ticket of the launch has been taken).
+#ifndef WC_SCAN_TICKETS
+#define WC_SCAN_TICKETS 1
+#endif
+// Thread 0: this CTA's ticket (tile id), taken after the CTA has read (and
+// used) its inputs' count.  The CTA holding the last ticket resets the
+// counter for the next scan on this scratch (every ticket of the launch has
+// been taken).  A CTA loads the data of tile blockIdx.x while its ticket is in
+// flight and reloads only when the ticket differs (dispatch out of blockIdx
+// order), so the atomic's latency stays off the critical path.
+__device__ __forceinline__ uint32_t take_ticket(uint64_t *scratch, bool &last_ticket) {
+#if !WC_SCAN_TICKETS  // timing experiment only: tile id = blockIdx.x (assumes in-order dispatch)
+    last_ticket = blockIdx.x == gridDim.x - 1;
+    return blockIdx.x;
+#endif
+    uint32_t *c = reinterpret_cast<uint32_t *>(scratch);
+    const uint32_t t = atomicAdd(c, 1u);
+    last_ticket = t == gridDim.x - 1;
+    if (last_ticket) *reinterpret_cast<volatile uint32_t *>(c) = 0u;
+    return t;
+}
+// Thread 0: the epilogue runs once both the scan total is known (the last
+// tile) and every CTA has read the count (the last ticket): the second of
+// those two arrivals runs it and clears the arrival word.
+__device__ __forceinline__ bool epilogue_arrive(uint64_t *scratch, uint32_t arrivals) {
+    uint32_t *c = reinterpret_cast<uint32_t *>(scratch) + 1;
+    if (!arrivals) return false;
+    if (atom_add_acq_rel(c, arrivals) + arrivals != 2u) return false;
+    *reinterpret_cast<volatile uint32_t *>(c) = 0u;
+    return true;
+}
+// the per-tile status words follow the header
+__device__ __forceinline__ uint64_t *tile_status(uint64_t *scratch) { return scratch + 1; }
 
 __device__ __forceinline__ void store_status(uint64_t *p, uint32_t epoch, uint32_t flag, uint32_t v) {
     atomicExch(reinterpret_cast<unsigned long long *>(p),
@@ -177,62 +228,107 @@ __device__ __forceinline__ uint32_t tile_lookback(int64_t t, uint32_t agg, uint6
     return excl;
 }
 
-// The grid is capped (kScanMaxCtas) so that a scan sized for a large upper
+// The grid is capped (scan_max_ctas) so that a scan sized for a large upper
 // bound does not launch thousands of CTAs that find no work: with more tiles
 // than CTAs, each CTA owns m consecutive tiles, publishes their total through
 // the look-back, then scans them in order (loading each twice).
-constexpr int kScanMaxCtas = kNumSMs * 8;
-inline unsigned scan_grid(int64_t n_max) { return (unsigned)std::min<int64_t>(scan_tiles(n_max), kScanMaxCtas); }
+inline int64_t scan_max_ctas() { return (int64_t)num_sms() * 8; }
+inline unsigned scan_grid(int64_t n_max) { return (unsigned)std::min<int64_t>(scan_tiles(n_max), scan_max_ctas()); }
 
-// Epilogue of a scan: run by one thread of the last tile once the total is
-// known (a control decision that would otherwise be a one-thread kernel).
-// It must not change the element count *d_n the other tiles read.
+// Epilogue of a scan: run once with the total, after every CTA has read the
+// count (a control decision that would otherwise be a one-thread kernel).
 struct NoEpilogue {
     __device__ __forceinline__ void operator()(uint32_t) const {}
+};
+template <class Epi>
+struct EpiTraits {
+    static constexpr bool none = false;
+};
+template <>
+struct EpiTraits<NoEpilogue> {
+    static constexpr bool none = true;
 };
 
 template <class Load, class Sink, class Epi = NoEpilogue>
 __global__ void __launch_bounds__(kScanThreads)
-    k_scan_onepass(Load ld, Sink sink, int64_t n_max, const uint32_t *d_n, uint64_t *status, ScanEpoch ep,
+    k_scan_onepass(Load ld, Sink sink, int64_t n_max, const uint32_t *d_n, uint64_t *scratch, ScanEpoch ep,
                    uint32_t *d_total, Epi epi = Epi{}) {
     pdl_wait();
     __shared__ uint32_t sw[32];
     __shared__ uint32_t tile[kScanTile];
-    __shared__ uint32_t s_excl;
+    __shared__ uint32_t s_excl, s_ticket, s_n, s_last_ticket;
+    uint64_t *status = tile_status(scratch);
     const uint32_t epoch = resolve_epoch(ep);
-    const int64_t n = scan_count(n_max, d_n);
+    if (threadIdx.x == 0) s_n = (uint32_t)scan_count(n_max, d_n);
+    __syncthreads();  // every CTA has read the count before it takes a ticket
+    const int64_t n = s_n;
     const int64_t ntiles = n > 0 ? (n - 1) / kScanTile + 1 : 1;
     const int64_t m = (ntiles + gridDim.x - 1) / gridDim.x;  // tiles per CTA
-    const int64_t t = blockIdx.x;
     const int64_t last = (ntiles - 1) / m;
-    if (t > last) return;
-    const int64_t base = t * m * kScanTile;
-    if (m > 1) {  // the chunk's total first, so successors can look back early
-        uint32_t s = 0;
-        for (int64_t i = base + threadIdx.x; i < min(n, base + m * kScanTile); i += kScanThreads) s += ld(i);
-        uint32_t agg;
-        block_exclusive_scan(s, sw, &agg);
-        if (threadIdx.x < 32) {
-            const uint32_t excl = tile_lookback(t, agg, status, epoch);
-            if (threadIdx.x == 0) {
-                s_excl = excl;
-                if (t == last) {
-                    if (d_total) *d_total = excl + agg;
-                    epi(excl + agg);
-                }
-            }
-        }
-        __syncthreads();
-    }
-    uint32_t running = 0;
-    for (int64_t sub = 0; sub < m; sub++) {
-        const int64_t tb = base + sub * kScanTile;
+    bool lt = false;
+    uint32_t tk = 0;
+    if (threadIdx.x == 0) tk = take_ticket(scratch, lt);
+    // speculative load of tile blockIdx.x while the ticket is in flight
+    auto chunk_sum = [&](int64_t tt) {
+        uint32_t acc = 0;
+        const int64_t b0 = tt * m * kScanTile;
+        for (int64_t i = b0 + threadIdx.x; i < min(n, b0 + m * kScanTile); i += kScanThreads) acc += ld(i);
+        return acc;
+    };
+    auto load_tile = [&](int64_t tb) {
 #pragma unroll
         for (int k = 0; k < kScanIPT; k++) {
             const int idx = k * kScanThreads + threadIdx.x;
             const int64_t i = tb + idx;
             tile[idx] = i < n ? ld(i) : 0;
         }
+    };
+    const int64_t ts = blockIdx.x;
+    uint32_t csum = 0;
+    if (ts <= last) {
+        if (m > 1)
+            csum = chunk_sum(ts);
+        else
+            load_tile(ts * kScanTile);
+    }
+    if (threadIdx.x == 0) {
+        s_ticket = tk;
+        s_last_ticket = lt;
+        // the holder of the last ticket arrives now unless it also holds the
+        // last tile (which arrives once the total is known)
+        if (!EpiTraits<Epi>::none && lt && (int64_t)tk != last && epilogue_arrive(scratch, 1u))
+            epi(*reinterpret_cast<volatile uint32_t *>(d_total));
+    }
+    __syncthreads();
+    const int64_t t = s_ticket;
+    if (t > last) return;
+    if (t != ts) {  // dispatched out of order: the data of the ticket's tile
+        if (m > 1)
+            csum = chunk_sum(t);
+        else
+            load_tile(t * kScanTile);
+    }
+    const int64_t base = t * m * kScanTile;
+    if (m > 1) {  // the chunk's total first, so successors can look back early
+        uint32_t agg;
+        block_exclusive_scan(csum, sw, &agg);
+        if (threadIdx.x < 32) {
+            const uint32_t excl = tile_lookback(t, agg, status, epoch);
+            if (threadIdx.x == 0) {
+                s_excl = excl;
+                if (t == last) {
+                    *d_total = excl + agg;
+                    if (!EpiTraits<Epi>::none && epilogue_arrive(scratch, 1u + s_last_ticket)) epi(excl + agg);
+                }
+            }
+        }
+        __syncthreads();
+        load_tile(base);  // the chunk's first tile
+    }
+    uint32_t running = 0;
+    for (int64_t sub = 0; sub < m; sub++) {
+        const int64_t tb = base + sub * kScanTile;
+        if (sub > 0) load_tile(tb);  // sub-tile 0 is loaded above
         __syncthreads();
         uint32_t v[kScanIPT], s = 0;
 #pragma unroll
@@ -248,8 +344,8 @@ __global__ void __launch_bounds__(kScanThreads)
                 s_excl = excl;
                 if (t == last) {
                     const uint32_t total = n > 0 ? excl + agg : 0u;
-                    if (d_total) *d_total = total;
-                    epi(total);
+                    *d_total = total;
+                    if (!EpiTraits<Epi>::none && epilogue_arrive(scratch, 1u + s_last_ticket)) epi(total);
                 }
             }
         }

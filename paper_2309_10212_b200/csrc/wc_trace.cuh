@@ -52,7 +52,7 @@ __device__ __forceinline__ double poly_eval(double A, double B, double C, double
 }
 
 // blocktrace.py:198-233 _refine_root (Illinois regula falsi, bisection fallback)
-__device__ __noinline__ double refine_root(double A, double B, double C, double D, double lo, double hi,
+static __device__ __noinline__ double refine_root(double A, double B, double C, double D, double lo, double hi,
                                            double g_lo, double g_hi) {
     const double tol = 1e-9 * (hi - lo);
     int side = 0;
@@ -168,6 +168,22 @@ __device__ __forceinline__ void grad_shade(const float c[8], double ux, double u
     rgb[0] = (float)(br * inten);
     rgb[1] = (float)(bg * inten);
     rgb[2] = (float)(bb * inten);
+}
+
+// blocktrace.py:306-314 _shade on its own (the reference's `shade` API).
+__device__ __forceinline__ void shade_grad(double gx, double gy, double gz, const double d[3], double br, double bg,
+                                           double bb, double rgb[3]) {
+    const double gl = sqrt((gx * gx + gy * gy) + gz * gz);
+    double inten;
+    if (gl == 0.0) {
+        inten = kAmbient;
+    } else {
+        const double cos_t = fabs((gx * d[0] + gy * d[1]) + gz * d[2]) / gl;
+        inten = cos_t > kAmbient ? cos_t : kAmbient;
+    }
+    rgb[0] = br * inten;
+    rgb[1] = bg * inten;
+    rgb[2] = bb * inten;
 }
 
 // Same, returning float64 colour (oracle.py:88-90 quantises the f64 value).

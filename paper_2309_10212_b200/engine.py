@@ -17,6 +17,7 @@ from typing import Iterator
 import numpy as np
 
 from . import _lib
+from .bitmaps import mask_to_words, n_words, words_to_mask
 from .codec import CompressedVolume
 from .grids import MacrocellGrids
 from .traversal import Camera
@@ -92,6 +93,70 @@ def compute_n_spec(n_act: int, w: int, h: int, max_spec: int = MAX_SPEC_DEFAULT)
     """Free slots shared evenly, clamped to [1, max_spec] (engine.py:91-94)."""
     assert n_act >= 1
     return min(max_spec, max(1, (w * h) // n_act))
+
+
+UINT_MAX = 0xFFFFFFFF
+
+
+def mark_blocks(block_slots: np.ndarray, block_dims) -> tuple[np.ndarray, np.ndarray]:
+    """engine.py:97-118 on the device: visible = referenced by a slot; active
+    adds each visible block's existing +octant neighbours.  The session's
+    marking kernels (bitmap extraction + word/bit dilation, csrc/wc_stage.cu)."""
+    bdx, bdy, bdz = (int(v) for v in block_dims)
+    n_blocks = bdx * bdy * bdz
+    slots = np.ascontiguousarray(np.asarray(block_slots).reshape(-1), dtype=np.uint32)
+    vis = np.zeros(n_words(n_blocks), dtype=np.uint32)
+    act = np.zeros_like(vis)
+    _lib.call("wc_mark_blocks", _lib.ptr(slots), len(slots), bdx, bdy, bdz, _lib.ptr(vis), _lib.ptr(act))
+    return words_to_mask(vis, n_blocks), words_to_mask(act, n_blocks)
+
+
+def build_rt_inputs(block_slots: np.ndarray, ray_slots: np.ndarray, visible_mask: np.ndarray) -> PassBuffers:
+    """engine.py:121-149 on the device: scan of slot validity, compaction,
+    stable radix sort of the entries by block, per-block counts by visible
+    rank (csrc/wc_stage.cu)."""
+    bs = np.ascontiguousarray(np.asarray(block_slots).reshape(-1), dtype=np.uint32)
+    rs = np.ascontiguousarray(np.asarray(ray_slots).reshape(-1), dtype=np.uint32)
+    assert bs.shape == rs.shape, "slot buffers differ in length"
+    vm = np.asarray(visible_mask, dtype=bool).reshape(-1)
+    n, nb = len(bs), len(vm)
+    words = mask_to_words(vm)
+    vis = np.empty(nb + 1, dtype=np.uint32)
+    counts = np.empty(nb + 1, dtype=np.uint32)
+    offs = np.empty(nb + 1, dtype=np.uint32)
+    sr = np.empty(n, dtype=np.uint32)
+    sh = np.empty(n, dtype=np.uint32)
+    vp = np.empty(n, dtype=np.uint32)
+    sizes = np.zeros(3, dtype=np.int64)
+    _lib.call("wc_build_rt_inputs", _lib.ptr(bs), _lib.ptr(rs), n, _lib.ptr(words), nb, _lib.ptr(vis),
+              _lib.ptr(counts), _lib.ptr(offs), _lib.ptr(sr), _lib.ptr(sh), _lib.ptr(vp), _lib.ptr(sizes))
+    ne, nv, nc = (int(x) for x in sizes)
+    return PassBuffers(visible_ids=vis[:nv].copy(), rays_per_block=counts[:nc].copy(),
+                       block_ray_offsets=offs[:nc].copy(), sorted_ray_ids=sr[:ne].copy(),
+                       sorted_hit_slots=sh[:ne].copy(), valid_prefix=vp, n_entries=ne)
+
+
+def composite(rgbz_rgb: np.ndarray, rgbz_z: np.ndarray, rays, n_spec: int, active_offsets: np.ndarray,
+              valid_prefix: np.ndarray, fb: Framebuffer) -> None:
+    """engine.py:261-283 on the device: each active ray's closest speculated
+    hit (strict <, earliest slot wins); finished rays terminate."""
+    rgb = np.ascontiguousarray(rgbz_rgb, dtype=np.float32).reshape(-1, 3)
+    z = np.ascontiguousarray(rgbz_z, dtype=np.float32).reshape(-1)
+    assert len(rgb) == len(z), "rgbz buffers differ in length"
+    status = np.ascontiguousarray(rays.status, dtype=np.uint8)
+    exited = np.ascontiguousarray(rays.exited, dtype=np.uint8)
+    offs = np.ascontiguousarray(active_offsets, dtype=np.int64)
+    bs = np.ascontiguousarray(rays.block_slots, dtype=np.uint32)
+    vp = np.ascontiguousarray(valid_prefix, dtype=np.uint32)
+    rgba = np.ascontiguousarray(fb.rgba.reshape(-1, 4))
+    depth = np.ascontiguousarray(fb.depth.reshape(-1))
+    n = len(status)
+    _lib.call("wc_composite", _lib.ptr(rgb), _lib.ptr(z), len(z), n, _lib.ptr(status), _lib.ptr(exited),
+              _lib.ptr(offs), int(n_spec), _lib.ptr(bs), len(bs), _lib.ptr(vp), _lib.ptr(rgba), _lib.ptr(depth))
+    rays.status[:] = status
+    fb.rgba.reshape(-1, 4)[:] = rgba
+    fb.depth.reshape(-1)[:] = depth
+    fb.completeness = float(rays.n - rays.n_active) / rays.n
 
 
 def _stats_from_c(s: _lib.PassStatsC) -> PassStats:

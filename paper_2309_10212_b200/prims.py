@@ -27,15 +27,15 @@ def exclusive_scan(values) -> tuple[np.ndarray, int]:
 
 def compact(values, mask) -> np.ndarray:
     """Keep values[i] where mask[i] != 0, order preserved (prims.py:26-31):
-    device scan of the mask gives each kept element its output slot."""
+    the kept indices come from the device's single-pass scan + compaction."""
     values = np.asarray(values)
     mask = np.asarray(mask)
     assert values.shape[0] == mask.shape[0], "compact: length mismatch"
-    offsets, total = exclusive_scan(mask.astype(bool).astype(np.uint32))
-    out = np.empty((total,) + values.shape[1:], dtype=values.dtype)
-    keep = mask.astype(bool)
-    out[offsets[keep]] = values[keep]
-    return out
+    m = np.ascontiguousarray(mask.astype(bool).astype(np.uint8))
+    idx = np.empty(len(m), dtype=np.uint32)
+    tot = C.c_uint64()
+    _lib.call("wc_compact_indices", _lib.ptr(m), len(m), _lib.ptr(idx), C.byref(tot))
+    return values[idx[:tot.value]]
 
 
 def sort_by_key(keys, values) -> tuple[np.ndarray, np.ndarray]:

@@ -148,6 +148,45 @@ def init_rays(cam: Camera, w: int, h: int, dims) -> RaySoA:
     return RaySoA.from_camera(cam, w, h, dims)
 
 
+def traverse_to_next_blocks(rays: RaySoA, grids, iso: float, n_spec: int, active_offsets: np.ndarray,
+                            variant: int = 0) -> None:
+    """Advance every active ray to its next up-to-n_spec candidate blocks
+    (traversal.py:406-452) with the session's traversal kernels
+    (k_traverse / k_traverse_warp; ``variant`` 1 or 2 forces one).
+
+    Candidate block ids land in rays.block_slots (owning ray in
+    rays.ray_slots) at offset active_offsets[ray] * n_spec; unfilled slots
+    stay UINT_MAX.  Iterator state is saved past the last emitted block;
+    rays that run out of volume get their exited flag set."""
+    assert n_spec >= 1
+    n = rays.n
+    fd = np.asarray(grids.fine_dims, dtype=np.int32)
+    cd = np.asarray(grids.coarse_dims, dtype=np.int32)
+    vol = grids.bound_volume
+    if vol is not None:
+        arrs = (None, None, None, None)
+        vh = vol.device_handle()
+    else:
+        arrs = tuple(np.ascontiguousarray(a, dtype=np.float64) for a in
+                     (grids.fine_min, grids.fine_max, grids.coarse_min, grids.coarse_max))
+        vh = None
+    fields = {}
+    for name, dt in (("origin", np.float64), ("direction", np.float64), ("t_exit", np.float64),
+                     ("status", np.uint8), ("exited", np.uint8), ("coarse_cell", np.uint32),
+                     ("coarse_tmax", np.float64), ("fine_cell", np.uint32), ("fine_tmax", np.float64),
+                     ("block_slots", np.uint32), ("ray_slots", np.uint32)):
+        a = getattr(rays, name)
+        if a.dtype != dt or not a.flags["C_CONTIGUOUS"]:
+            a = np.ascontiguousarray(a, dtype=dt)
+            setattr(rays, name, a)
+        fields[name] = a
+    offs = np.ascontiguousarray(active_offsets, dtype=np.int64)
+    _lib.call("wc_traverse", vh, *[_lib.ptr(a) for a in arrs], _lib.ptr(fd), _lib.ptr(cd), n,
+              *[_lib.ptr(fields[k]) for k in ("origin", "direction", "t_exit", "status", "exited", "coarse_cell",
+                                              "coarse_tmax", "fine_cell", "fine_tmax", "block_slots", "ray_slots")],
+              _lib.ptr(offs), float(iso), int(n_spec), int(variant))
+
+
 def dda_step(cell, tmax, direction, grid_dims, cell_size):
     """One Amanatides-Woo step (traversal.py:195-214); ties step x, then y, then z."""
     cell = [int(c) for c in cell]

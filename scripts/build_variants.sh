@@ -9,7 +9,7 @@ while [ $# -gt 0 ]; do
   name=$1; flags=$2; shift 2
   rm -rf build_var/$name; mkdir -p build_var/$name
   pids=()
-  for f in wc_prims wc_volume wc_engine wc_capi; do
+  for f in wc_prims wc_volume wc_engine wc_stage wc_capi; do
     nvcc $ARCH -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $flags \
       -c $f.cu -o build_var/$name/$f.o &
     pids+=($!)
