@@ -187,3 +187,53 @@ def test_intersection_kats():
     # test_blocktrace.py:85-90: linear field -> exactly 0.5
     corners = np.array([-1, 1, -1, 1, -1, 1, -1, 1], np.float32)
     assert orc.intersect_cell(corners, (0.0, 0.5, 0.5), (1.0, 0.0, 0.0), (0, 0, 0), 0.0, 1.0, 0.0) == 0.5
+
+
+def _ragged(z, name):
+    flat, lens = z[f"{name}_flat"], z[f"{name}_len"]
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    return [flat[offs[i]:offs[i + 1]] for i in range(len(lens))]
+
+
+@pytest.mark.parametrize("cap", [4, 16])
+def test_stage_cache_traces_pin_the_oracle_cache(cap):
+    """tests/golden/stage_kats.npz (make_stage_golden.py, the reference
+    BlockCache with growth from capacity 4 / 16): the oracle's cache."""
+    z = load("stage_kats.npz")
+    import paper_2309_10212_b200.volume as V
+
+    vol = V.synthesize("value_noise", (16, 16, 16), seed=5)
+    ov = orc.volume_from_values(vol.values, vol.dims, 12)
+    c = orc.Cache(cap, ov)
+    act, bos, lu = _ragged(z, f"cache{cap}_active"), _ragged(z, f"cache{cap}_block_of_slot"), \
+        _ragged(z, f"cache{cap}_last_used")
+    for i, ids in enumerate(act):
+        s = c.ensure_resident(ids.astype(np.int64))
+        assert [s["new_decompressed"], s["evicted"], s["grown_to"]] == list(z[f"cache{cap}_stats"][i]), i
+        b, l_, sv = c.state()
+        assert np.array_equal(b, bos[i]) and np.array_equal(l_, lu[i]), i
+    assert np.array_equal(sv.view(np.uint32), z[f"cache{cap}_final_values"].view(np.uint32))
+
+
+def test_stage_intersections_pin_the_oracle():
+    z = load("stage_kats.npz")
+    t01 = z["isec_t01"]
+    for i in range(len(t01)):
+        if t01[i, 0] > t01[i, 1]:
+            continue
+        got = orc.intersect_cell(z["isec_corners"][i], z["isec_o"][i], z["isec_d"][i], (0, 0, 0), t01[i, 0],
+                                 t01[i, 1], z["isec_iso"][i])
+        assert (got is None and z["isec_t"][i] == np.inf) or got == z["isec_t"][i], i
+
+
+def test_bitmap_helpers_round_trip():
+    from paper_2309_10212_b200.bitmaps import mask_to_words, n_words, words_to_mask
+
+    rng = np.random.default_rng(3)
+    for n in (0, 1, 31, 32, 33, 64, 1000):
+        m = rng.random(n) < 0.3
+        w = mask_to_words(m)
+        assert w.dtype == np.uint32 and len(w) == n_words(n)
+        assert np.array_equal(words_to_mask(w, n), m)
+        for b in np.nonzero(m)[0]:
+            assert (int(w[b >> 5]) >> int(b & 31)) & 1
