@@ -137,7 +137,7 @@ int wc_session_set_grouping(wc_session *s, int group_entries);
  * (wc_session_run).  wc_session_sync waits for the session's stream. */
 int wc_session_reset_part(wc_session *s, const wc_camera *cam, double iso, int64_t part, int64_t parts);
 int wc_session_mask_buffers(wc_session *s, int64_t parts, void **coarse_bm, void **cell_mask, int64_t *chunk_words);
-int wc_session_sync(wc_session *s);
+int wc_session_sync(wc_session *s);  /* waits for the session's stream and its copies */
 /* Replay passes as captured CUDA graphs (default on; WAVECAST_NO_GRAPHS=1 in
  * the environment turns it off).  Off = plain launches with per-stage
  * timing (wc_session_stage_ms); on = the pass timed as a whole. */
@@ -160,6 +160,14 @@ int wc_session_render_host(wc_session *s, const wc_camera *cam, double iso, wc_p
 int wc_session_n_active(const wc_session *s, int64_t *n_active);
 /* Framebuffer.snapshot (engine.py:62-63): RGBA8 (n x 4) + float32 depth (n). */
 int wc_session_framebuffer(wc_session *s, uint8_t *rgba, float *depth);
+/* Streamed snapshot of the current framebuffer (render_passes yields one per
+ * pass, engine.py:62-63, :380-382): copied on the device into a ring slot
+ * (session stream), then to the caller's host buffers (n RGBA8 words + n
+ * float32, page-locked for full speed) on a copy stream, overlapped with the
+ * passes that follow.  The buffers must stay valid until
+ * wc_session_snapshot_wait(ticket) returns (or wc_session_sync). */
+int wc_session_snapshot(wc_session *s, uint32_t *rgba_host, float *depth_host, int64_t *ticket);
+int wc_session_snapshot_wait(wc_session *s, int64_t ticket);
 /* Same into caller-owned DEVICE buffers (for NCCL tile gathers). */
 int wc_session_framebuffer_device(wc_session *s, void *rgba_dev, void *depth_dev);
 /* Device time of the last pass (CUDA events on the session stream). */

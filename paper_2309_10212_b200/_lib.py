@@ -105,6 +105,8 @@ _SIGS = {
     "wc_session_render": (_i32, [_vp, _vp, _dbl, _vp, _i64, _vp]),
     "wc_session_framebuffer": (_i32, [_vp, _vp, _vp]),
     "wc_session_framebuffer_device": (_i32, [_vp, _vp, _vp]),
+    "wc_session_snapshot": (_i32, [_vp, _vp, _vp, _vp]),
+    "wc_session_snapshot_wait": (_i32, [_vp, _i64]),
     "wc_session_last_pass_ms": (_i32, [_vp, _vp]),
     "wc_session_destroy": (_i32, [_vp]),
     "wc_session_sizes": (_i32, [_vp, _vp]),

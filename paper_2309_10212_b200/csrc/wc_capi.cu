@@ -564,7 +564,20 @@ int wc_session_mask_buffers(wc_session *s, int64_t parts, void **coarse_bm, void
 
 int wc_session_sync(wc_session *s) {
     WC_API_BEGIN
-    WC_CUDA(cudaStreamSynchronize(s->s->st));
+    s->s->sync_all();
+    WC_API_END
+}
+
+int wc_session_snapshot(wc_session *s, uint32_t *rgba_host, float *depth_host, int64_t *ticket) {
+    WC_API_BEGIN
+    WC_REQUIRE(rgba_host && depth_host, wc::UsageError, "snapshot needs host buffers");
+    *ticket = s->s->snapshot_async(rgba_host, depth_host);
+    WC_API_END
+}
+
+int wc_session_snapshot_wait(wc_session *s, int64_t ticket) {
+    WC_API_BEGIN
+    s->s->snapshot_wait(ticket);
     WC_API_END
 }
 

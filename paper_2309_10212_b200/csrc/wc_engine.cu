@@ -1963,6 +1963,10 @@ Session::~Session() {
         cudaStreamSynchronize(st_copy);
         cudaStreamDestroy(st_copy);
     }
+    for (int k = 0; k < kSnapRing; k++) {
+        if (snap_ready[k]) cudaEventDestroy(snap_ready[k]);
+        if (snap_done[k]) cudaEventDestroy(snap_done[k]);
+    }
     if (ev_fb) cudaEventDestroy(ev_fb);
     if (ev_fb_done) cudaEventDestroy(ev_fb_done);
     if (ev_frame0) cudaEventDestroy(ev_frame0);
@@ -2462,11 +2466,16 @@ float Session::frame_ms() {
 // After pass p: remember the rays still active (only their pixels can
 // change from here on) and start copying the whole framebuffer to the host on
 // a second stream while the remaining passes run.
+void Session::ensure_copy_stream() {
+    if (st_copy) return;
+    WC_CUDA(cudaStreamCreateWithFlags(&st_copy, cudaStreamNonBlocking));
+    WC_CUDA(cudaEventCreate(&ev_fb));
+    WC_CUDA(cudaEventCreate(&ev_fb_done));
+}
+
 void Session::enqueue_fb_snapshot(int64_t p) {
-    if (!st_copy) {
-        WC_CUDA(cudaStreamCreateWithFlags(&st_copy, cudaStreamNonBlocking));
-        WC_CUDA(cudaEventCreate(&ev_fb));
-        WC_CUDA(cudaEventCreate(&ev_fb_done));
+    ensure_copy_stream();
+    if (!snap_list.p) {
         snap_list.alloc(n);
         patch.alloc(n);
     }
@@ -2544,6 +2553,38 @@ int64_t Session::render_to_host(const CameraParams *cam, double iso_, PassStatsC
                 std::chrono::duration<double>(t3 - t2).count() * 1e3);
     }
     return k;
+}
+
+int64_t Session::snapshot_async(uint32_t *rgba_host, float *depth_host) {
+    ensure_copy_stream();
+    const int k = (int)(snap_seq % kSnapRing);
+    if (!snap_ring[k].p) {
+        snap_ring[k].alloc(2 * n);
+        WC_CUDA(cudaEventCreateWithFlags(&snap_ready[k], cudaEventDisableTiming));
+        WC_CUDA(cudaEventCreateWithFlags(&snap_done[k], cudaEventDisableTiming));
+    } else {
+        WC_CUDA(cudaStreamWaitEvent(st, snap_done[k], 0));  // the slot's previous host copy has landed
+    }
+    WC_CUDA(cudaMemcpyAsync(snap_ring[k].p, rgba.p, 4 * n, cudaMemcpyDeviceToDevice, st));
+    WC_CUDA(cudaMemcpyAsync(snap_ring[k].p + n, depth.p, 4 * n, cudaMemcpyDeviceToDevice, st));
+    WC_CUDA(cudaEventRecord(snap_ready[k], st));
+    WC_CUDA(cudaStreamWaitEvent(st_copy, snap_ready[k], 0));
+    WC_CUDA(cudaMemcpyAsync(rgba_host, snap_ring[k].p, 4 * n, cudaMemcpyDeviceToHost, st_copy));
+    WC_CUDA(cudaMemcpyAsync(depth_host, snap_ring[k].p + n, 4 * n, cudaMemcpyDeviceToHost, st_copy));
+    WC_CUDA(cudaEventRecord(snap_done[k], st_copy));
+    return snap_seq++;
+}
+
+// The slot's event may since have been recorded for a later snapshot: the
+// copy stream is in order, so that one completing implies this one did.
+void Session::snapshot_wait(int64_t ticket) {
+    if (ticket < 0 || ticket >= snap_seq) throw UsageError("no such snapshot");
+    WC_CUDA(cudaEventSynchronize(snap_done[ticket % kSnapRing]));
+}
+
+void Session::sync_all() {
+    WC_CUDA(cudaStreamSynchronize(st));
+    if (st_copy) WC_CUDA(cudaStreamSynchronize(st_copy));
 }
 
 void Session::download_framebuffer(uint8_t *rgba_host, float *depth_host) {

@@ -245,6 +245,14 @@ struct Session : CacheStore {
     void mask_buffers(int64_t parts, int64_t &chunk_words);  // sized for `parts` slices of chunk_words
     float frame_ms();  // device time from the last reset to the end of the last pass
     void download_framebuffer(uint8_t *rgba_host, float *depth_host);
+    // Streamed per-pass snapshots (render_passes, Framebuffer.snapshot,
+    // engine.py:62-63): a device-to-device copy of the framebuffer into a
+    // ring slot on the session stream, then its copy to the caller's host
+    // buffers on the copy stream, overlapped with the passes that follow.
+    // Returns a ticket; snapshot_wait(ticket) blocks until that copy landed.
+    int64_t snapshot_async(uint32_t *rgba_host, float *depth_host);
+    void snapshot_wait(int64_t ticket);
+    void sync_all();  // session and copy streams
     void copy_framebuffer_device(void *rgba_dst, void *depth_dst);
 
     double reset_device_ms();  // device time of the last reset, once it has run
@@ -281,6 +289,11 @@ struct Session : CacheStore {
     uint32_t *fb_rgba = nullptr;
     float *fb_depth = nullptr;
     DevBuf<uint32_t> snap_list;
+    static constexpr int kSnapRing = 3;
+    DevBuf<uint32_t> snap_ring[kSnapRing];  // rgba words (n) + depth bits (n) per slot
+    cudaEvent_t snap_ready[kSnapRing] = {}, snap_done[kSnapRing] = {};
+    int64_t snap_seq = 0;
+    void ensure_copy_stream();
     DevBuf<uint4> patch;
     PinnedBuf<uint4> h_patch;
 };

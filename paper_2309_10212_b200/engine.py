@@ -19,6 +19,7 @@ import numpy as np
 from . import _lib
 from .bitmaps import mask_to_words, n_words, words_to_mask
 from .codec import CompressedVolume
+from .errors import UsageError
 from .grids import MacrocellGrids
 from .traversal import Camera
 
@@ -61,6 +62,44 @@ class Framebuffer:
         return cls(w, h, rgba, np.full((h, w), np.inf, dtype=np.float32), 0.0)
 
     def snapshot(self) -> "Framebuffer":
+        return Framebuffer(self.w, self.h, self.rgba.copy(), self.depth.copy(), self.completeness)
+
+
+class StreamedFramebuffer:
+    """A per-pass framebuffer snapshot (engine.py:62-63) whose pixels are
+    still in flight: the session copied its framebuffer on the device and is
+    moving the copy to page-locked host memory on a copy stream while the
+    next passes run (wc_session_snapshot).  ``rgba`` / ``depth`` wait for that
+    copy on first access, so a consumer that looks at every frame sees the
+    copy overlapped with rendering, and one that skips frames never waits."""
+
+    def __init__(self, session: "RenderSession", ticket: int, base: np.ndarray, completeness: float):
+        self.w, self.h = session.w, session.h
+        self.completeness = completeness
+        n = session.n
+        self._rgba = base[:4 * n].reshape(self.h, self.w, 4)
+        self._depth = base[4 * n:8 * n].view(np.float32).reshape(self.h, self.w)
+        self._session = session
+        self._ticket = ticket
+
+    def _land(self):
+        s = self._session
+        if s is not None:
+            self._session = None
+            if s._h is not None:
+                _lib.call("wc_session_snapshot_wait", s._h, self._ticket)
+
+    @property
+    def rgba(self) -> np.ndarray:
+        self._land()
+        return self._rgba
+
+    @property
+    def depth(self) -> np.ndarray:
+        self._land()
+        return self._depth
+
+    def snapshot(self) -> Framebuffer:
         return Framebuffer(self.w, self.h, self.rgba.copy(), self.depth.copy(), self.completeness)
 
 
@@ -203,8 +242,40 @@ class RenderSession:
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.lib().wc_session_sync(self._h)  # streamed snapshots have landed
+            for ref in getattr(self, "_streamed", ()):
+                fb = ref()
+                if fb is not None:
+                    fb._session = None
             _lib.lib().wc_session_destroy(self._h)
             self._h = None
+
+    def snapshot(self, completeness: float) -> StreamedFramebuffer:
+        """This pass's framebuffer, copied to host memory in the background
+        (see StreamedFramebuffer); whole-image sessions only."""
+        import weakref
+
+        if self._pix is not None or self.n != self.w * self.h:
+            raise UsageError("streamed snapshots need a whole-image camera session")
+        base = _lib.pinned_pool.get(8 * self.n)
+        t = C.c_int64()
+        rgba = base[:4 * self.n]
+        depth = base[4 * self.n:8 * self.n]
+        _lib.call("wc_session_snapshot", self._h, _lib.ptr(rgba), _lib.ptr(depth), C.byref(t))
+        fb = StreamedFramebuffer(self, int(t.value), base, completeness)
+        # A pinned buffer must not be handed out again while a copy into it
+        # is in flight, even if the consumer dropped its frame: the copy of
+        # snapshot k has landed once the session stream has passed snapshot
+        # k + 3's ring-slot wait (three ring slots, one sync per step).
+        if not hasattr(self, "_streamed"):
+            import collections
+
+            self._streamed = []
+            self._inflight = collections.deque(maxlen=4)
+        self._inflight.append(base)
+        self._streamed = [r for r in self._streamed if r() is not None and r()._session is not None]
+        self._streamed.append(weakref.ref(fb))
+        return fb
 
     __del__ = close
 
@@ -333,13 +404,18 @@ class RenderSession:
 
 def render_passes(cv: CompressedVolume, grids: MacrocellGrids, cam: Camera, iso: float,
                   opts: RenderOptions) -> Iterator[tuple[Framebuffer, PassStats]]:
-    """engine.py:308-382: yield a framebuffer snapshot + stats per pass."""
+    """engine.py:308-382: yield a framebuffer snapshot + stats per pass.
+
+    Each snapshot is streamed (StreamedFramebuffer): copied on the device
+    after its pass and moved to host memory on a copy stream while the next
+    passes run; its pixels are waited for only when the consumer reads them
+    (the reference copies the whole framebuffer every pass, engine.py:62-63)."""
     with RenderSession(cv, grids, cam, iso, opts) as s:
         while True:
             ps = s.step()
             if ps is None:
                 break
-            yield s.framebuffer(ps.completeness), ps
+            yield s.snapshot(ps.completeness), ps
 
 
 class _SessionPool:

@@ -427,3 +427,27 @@ def test_split_range_tests_assemble_to_the_whole(wc):
     assert [x.n_active_before for x in stats] == [x.n_active_before for x in ref]
     assert np.array_equal(rgba0, rgba1) and np.array_equal(depth0, depth1)
     s.close()
+
+
+# The product path per pass: ray-ordered entries (no grouping) with every pass
+# replayed as a captured CUDA graph, over two frames on one session (the
+# second frame replays the graphs the first captured).
+GRAPH_SCENES = [
+    ("marschner_lobb", 64, 16, 256, 256, 0.5, 0.0, False, 64, None),
+    ("value_noise", 64, 16, 64, 64, 0.5, 0.4, True, 64, None),
+    ("value_noise", 48, 12, 120, 90, 0.35, 0.7, True, 64, 40),
+    ("turbulence", (256, 40, 36), 16, 120, 90, 0.5, 0.2, True, 64, None),
+    ("value_noise", 128, 12, 12, 12, 0.5, 0.2, True, 64, None),
+]
+
+
+@pytest.mark.parametrize("scene", GRAPH_SCENES, ids=[f"{s[0]}-{s[3]}x{s[4]}-spec{int(s[7])}" for s in GRAPH_SCENES])
+def test_graph_replay_ungrouped_lockstep(wc, scene):
+    kind, n, qbits, w, h, isof, camf, spec, max_spec, cache = scene
+    vol = host_volume(kind, n, seed=1 if kind == "turbulence" else (0 if kind == "gaussians" else 3))
+    cv = wc.compress_volume(vol, qbits)
+    ov = oracle_volume(cv)
+    lockstep(wc, cv, ov, orbit(cv.dims, camf), w, h, iso_at(vol, isof), speculation=spec, max_spec=max_spec,
+             cache_capacity=cache, group=False,
+             frames=[(orbit(cv.dims, camf + 0.31), iso_at(vol, isof * 0.9 + 0.05)),
+                     (orbit(cv.dims, camf), iso_at(vol, isof))])
