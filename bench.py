@@ -209,6 +209,69 @@ def stage_bytes(stage, stats, n_rays, stride):
     return 0
 
 
+# Algorithmic bytes of one kernel over a frame, from the per-pass PassStats
+# (A active rays, E entries, V visible blocks, D decoded blocks, A' the next
+# pass's active rays): the SURVEY.md §8(d) per-unit figures of the stage the
+# kernel implements (DESIGN.md §5 lists them).
+def kernel_bytes(name, stats, n_rays, stride, passes=None):
+    tot = 0
+    for i, s in enumerate(stats):
+        if passes is not None and i not in passes:
+            continue
+        a = s.n_active_before
+        e = round(s.utilization * n_rays)
+        a_next = stats[i + 1].n_active_before if i + 1 < len(stats) else 0
+        if name.startswith("k_traverse"):        # O_Act 4 + dir 24 + t_exit 8 + iterators 2x28 r+w + exited 1; R_BID/R_ID 8
+            tot += 149 * a + 8 * e
+        elif name.startswith("k_decode_insert"):  # compressed record read + f32[64] slot write
+            tot += (stride + 256) * s.new_decompressed
+        elif name.startswith("k_rt_find"):        # 5^3 f32 dual grid per visible block; entry ids 8 + ray 56
+            tot += 500 * s.visible_blocks + 64 * e
+        elif name.startswith("k_rt_shade"):       # winning rgbz 16 per entry
+            tot += 16 * e
+        elif "PassEndEpilogue" in name:           # surviving-ray compaction: keep flag 4 + id 4 read, id 4 written
+            tot += 8 * a + 4 * a_next
+        elif name.startswith("k_composite"):      # slot id 4 + prefix 4 + z 4 per entry; winner rgbz 16 + fb 8 + status 1
+            tot += 12 * e + 25 * (a - a_next)
+        else:
+            return None
+    return tot
+
+
+def kernel_table(rows, steps, stats, n_rays, stride, peak):
+    """Per-kernel device ms per frame (CUDA events around every launch of the
+    staged frames) with algorithmic GB/s where §8(d) assigns bytes."""
+    agg = {}
+    for r in rows:
+        k = agg.setdefault(r["kernel"], {"ms": 0.0, "launches": 0, "passes": set()})
+        k["ms"] += r["ms"]
+        k["launches"] += r["launches"]
+        k["passes"].add(r["pass"])
+    out = []
+    for name, k in agg.items():
+        ms = k["ms"] / steps
+        b = kernel_bytes(name, stats, n_rays, stride, k["passes"])
+        gbs = b / (ms * 1e-3) / 1e9 if (b and ms > 0) else None
+        out.append({"kernel": name, "ms_per_frame": round(ms, 4), "launches_per_frame": round(k["launches"] / steps, 2),
+                    "algorithmic_bytes": b, "gbs": round(gbs, 1) if gbs else None,
+                    "frac": round(gbs / peak, 4) if gbs else None})
+    out.sort(key=lambda x: -x["ms_per_frame"])
+    return out
+
+
+NCU_TRAVERSE = "profiles/r02_k_traverse_ncu.json"
+
+
+def ncu_summary(path):
+    """Committed ncu --set full summary of a kernel of this code (warp-exec
+    efficiency, L2 hit rate, DRAM bytes), or None."""
+    try:
+        with open(os.path.join(ROOT, path)) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
 # ------------------------------------------------------------------ B200 arm
 def run_b200(args):
     import torch
@@ -259,8 +322,8 @@ def run_b200(args):
         torch.cuda.synchronize()
 
     def frame():  # multi-GPU: the per-iso range tests are split across the ranks and all-gathered
-        if sharded:
-            return wdist.render_frame_split(sess, cam, iso)
+        if sharded:  # --force-shard on one GPU: the split range tests and their all-gathers still run
+            return wdist.render_frame_split(sess, cam, iso, split=True if args.force_shard else None)
         if args.rank_share > 1:  # rank 0's share incl. its slice of the range tests (the all-gather not timed)
             sess.reset_part(cam, iso, 0, args.rank_share)
             return sess.run()
@@ -289,6 +352,7 @@ def run_b200(args):
     stage_tot = {}
     staged_ms = []
     sess.set_graphs(False)
+    sess.set_kernel_profile(True)
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -296,7 +360,10 @@ def run_b200(args):
         staged_ms.append(sess.frame_ms())
         for k, v in sess.stage_ms().items():
             stage_tot[k] = stage_tot.get(k, 0.0) + v
+    kprof = sess.kernel_profile()
+    sess.set_kernel_profile(False)
     sess.set_graphs(True)
+    c_stats = list(getattr(sess, "last_frame_c", []))
     total_ms = float(np.sum(frame_ms))
     if sharded:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
@@ -315,7 +382,8 @@ def run_b200(args):
         barrier()
         t = time.perf_counter()
         if sharded:
-            fb, _ = wdist.render_sharded(cv, grids, cam, iso, opts, tile=args.tile)
+            fb, _ = wdist.render_sharded(cv, grids, cam, iso, opts, tile=args.tile,
+                                         split=True if args.force_shard else None)
         else:
             fb, _ = wc.render(cv, grids, cam, iso, opts)
         barrier()
@@ -327,7 +395,7 @@ def run_b200(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_frame = float(t.item())
 
-    # ---- roofline of the dominant stage (per-frame algorithmic bytes / stage time)
+    # ---- roofline of the dominant kernel (per-frame algorithmic bytes / its device time)
     pk = peaks()
     stage_frame = {k: v / args.steps for k, v in stage_tot.items()}
     kernel_stages = {k: v for k, v in stage_frame.items() if k != "reset"}
@@ -335,6 +403,12 @@ def run_b200(args):
     tb = stage_bytes(top, stats, n_local, stride)
     achieved = tb / (stage_frame[top] * 1e-3) / 1e9 if stage_frame[top] > 0 else 0.0
     fbytes = frame_bytes(stats, n_local, stride)
+    ktab = kernel_table(kprof, args.steps, stats, n_local, stride, pk["hbm_gbs"])
+    top_k = next((k for k in ktab if k["algorithmic_bytes"]), ktab[0] if ktab else None)
+    ncu_trav = ncu_summary(NCU_TRAVERSE)
+    dec = next((k for k in ktab if k["kernel"].startswith("k_decode_insert")), None)
+    comp = next((k for k in ktab if "PassEndEpilogue" in k["kernel"]), None)
+    trav = [k for k in ktab if k["kernel"].startswith("k_traverse")]
 
     if rank != 0:
         if sharded:
@@ -373,28 +447,68 @@ def run_b200(args):
                                          for p in range(min(len(stats), 128))],
         "frame_ms_all": [round(x, 3) for x in frame_ms],
         "wall_s_timed_region": round(wall_s, 3),
-        "roofline": {"bound": "hbm", "kernel": top, "achieved": round(achieved, 2), "peak": pk["hbm_gbs"],
-                     "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 5),
-                     "traffic": traffic_of(top, args.config),
-                     "traffic_source": TRAFFIC_FILE if traffic_of(top, args.config) is not None else None,
+        "roofline": {"bound": "hbm", "kernel": top_k["kernel"] if top_k else None,
+                     "achieved": top_k["gbs"] if top_k else None, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": top_k["frac"] if top_k else None,
+                     "kernel_ms_per_frame": top_k["ms_per_frame"] if top_k else None,
+                     "kernel_algorithmic_bytes_per_frame": top_k["algorithmic_bytes"] if top_k else None,
+                     "traffic": (ncu_trav or {}).get("dram_bytes_per_launch") if top_k and
+                     top_k["kernel"].startswith("k_traverse") else None,
+                     "traffic_source": NCU_TRAVERSE if ncu_trav else None,
+                     "achieved_note": "algorithmic bytes per frame (SURVEY §8(d) per-unit figures x the frame's "
+                                      "PassStats) / the kernel's device ms per frame, CUDA events around each "
+                                      "launch on the session stream in the staged (kernel-by-kernel) frames",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "_fallback" not in pk
                      else "fallback 6650 GB/s (B200_PROFILING.md)",
+                     "stage": top, "stage_achieved": round(achieved, 2),
+                     "stage_frac": round(achieved / pk["hbm_gbs"], 5),
                      "frame_algorithmic_bytes": int(fbytes),
                      "frame_frac": round(fbytes / (ms_per_frame * 1e-3) / 1e9 / pk["hbm_gbs"], 5)},
+        "kernels": ktab[:16],
+        "decode": {"gbs": dec["gbs"], "frac": dec["frac"], "ms_per_frame": dec["ms_per_frame"],
+                   "blocks_per_frame": sum(s.new_decompressed for s in stats)} if dec else None,
+        "compaction": {"kernel": comp["kernel"], "gbs": comp["gbs"], "frac": comp["frac"],
+                       "ms_per_frame": comp["ms_per_frame"]} if comp else None,
+        "traversal": {"ms_per_frame": round(sum(k["ms_per_frame"] for k in trav), 4),
+                      "ncu": {k: ncu_trav.get(k) for k in ("warp_exec_threads_per_instr", "warp_exec_efficiency",
+                                                          "l2_hit_rate", "dram_gbs", "duration_us", "commit")}
+                      if ncu_trav else None, "ncu_source": NCU_TRAVERSE if ncu_trav else None},
+        "time_to_first_pass_ms": round(stage_frame.get("reset", 0.0) + stats[0].duration * 1e3, 4) if stats else None,
+        "evicted_per_pass": [int(c["evicted"]) for c in c_stats],
         "clocks": clocks,
         "setup_s": round(setup_s, 2),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"], line["parity"] = cpu_baseline(args, wl, cv, iso, fb)
+        line["cpu_baseline"], line["parity"] = cpu_baseline(args, wl, cv, iso, fb, stats, c_stats, cache)
     emit(line)
     sess.close()
     if sharded:
         torch.distributed.destroy_process_group()
 
 
-def cpu_baseline(args, wl, cv, iso, fb):
-    """Oracle (C port of the reference path) on one host core over a sample of
-    image tiles; the same pixels are checked against the GPU frame."""
+STAT_KEYS = ("n_active_before", "n_spec", "visible_blocks", "active_blocks", "new_decompressed", "cache_slots",
+             "utilization", "completeness")
+
+
+def stats_mismatches(gpu_stats, gpu_c, ora_stats):
+    """Per-pass PassStats fields (+ evicted) that differ from the oracle's."""
+    bad = []
+    if len(gpu_stats) != len(ora_stats):
+        return [f"passes {len(gpu_stats)} vs {len(ora_stats)}"]
+    for i, (g, o) in enumerate(zip(gpu_stats, ora_stats)):
+        for k in STAT_KEYS:
+            if getattr(g, k) != o[k]:
+                bad.append(f"pass {i} {k}")
+        if gpu_c and int(gpu_c[i]["evicted"]) != o["evicted"]:
+            bad.append(f"pass {i} evicted")
+    return bad
+
+
+def cpu_baseline(args, wl, cv, iso, fb, gpu_stats, gpu_c, cache):
+    """The oracle (C port of the reference path, oracle/) renders the same
+    full frame on one host core as ONE session with the GPU session's slot
+    budget and cache capacity: that time is cpu_baseline, and its framebuffer
+    and per-pass PassStats (incl. evictions) are the parity check."""
     from oracle import oracle as orc
 
     threads = os.cpu_count() or 1
@@ -406,25 +520,23 @@ def cpu_baseline(args, wl, cv, iso, fb):
     ov = orc.volume_from_payload(wl["dims"], wl["qbits"], pay, rng)
     w, h = wl["w"], wl["h"]
     cam = orbit(wl["dims"])
-    # sample: every k-th 32x32 tile (interleaved), one thread
-    tiles_total = -(w // -32) * -(h // -32)
-    n_tiles = args.cpu_sample_tiles or tiles_total  # default: the whole frame (~7 s on one core at C3)
-    world = max(1, tiles_total // n_tiles)
-    pix = orc.tile_pixels(w, h, 0, world, 32)
-    o, d = orc.camera_rays(cam, w, h, pix)
+    o, d = orc.camera_rays(cam, w, h)
     t = time.perf_counter()
-    rgba, depth, st = orc.render(ov, o, d, len(pix), 1, iso, max_spec=args.max_spec)  # budget = sample rays
+    rgba, depth, st = orc.render(ov, o, d, w, h, iso, max_spec=args.max_spec, cache_capacity=cache or 0)
     cpu_s = time.perf_counter() - t
     mism = None
     if fb is not None:
-        g_rgba = fb.rgba.reshape(-1, 4)[pix]
-        g_depth = fb.depth.reshape(-1)[pix]
+        g_rgba = fb.rgba.reshape(-1, 4)
+        g_depth = fb.depth.reshape(-1)
         mism = int(np.count_nonzero((g_rgba != rgba).any(1) | (g_depth.view(np.uint32) != depth.view(np.uint32))))
-    base = {"value": round(len(pix) / cpu_s / 1e6, 5), "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{len(pix)} rays = every {world}th 32x32 tile of the 1080p frame, full pass loop, 1 thread "
+    base = {"value": round(w * h / cpu_s / 1e6, 5), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"the full {w}x{h} frame ({w * h} rays), one session, full pass loop, 1 thread "
                       f"({cpu_s:.1f} s, {len(st)} passes)", "seconds": round(cpu_s, 2)}
+    bad = stats_mismatches(gpu_stats, gpu_c, st)
     parity = {"cpu_volume_synth_bit_exact": volume_bit_exact, "cpu_synth_s": round(synth_s, 1),
-              "pixels_checked": int(len(pix)), "pixel_mismatches": mism}
+              "pixels_checked": int(w * h), "pixel_mismatches": mism, "passes": len(st),
+              "pass_stats_checked": list(STAT_KEYS) + ["evicted"], "pass_stat_mismatches": bad[:20],
+              "oracle_evicted_per_pass": [int(x["evicted"]) for x in st]}
     return base, parity
 
 
@@ -500,6 +612,26 @@ def run_c5(args):
                                 width=w, height=h, max_spec=args.max_spec, volume="C3 (device-synthesised)")
     ms = tim["mean_frame_ms"]
     wall = float(np.mean(tim["wall_ms"]))
+    n_rays = w * h
+    per_render = []
+    for (iso, cam), st, fms in zip(tim["views"], tim["stats"], tim["frame_ms"]):
+        per_render.append({"iso_fraction": round((iso - tim["value_range"][0]) /
+                                                 (tim["value_range"][1] - tim["value_range"][0]), 4),
+                           "eye": [round(v, 2) for v in cam.eye], "frame_ms": round(fms, 3), "passes": len(st),
+                           "n_active": [s.n_active_before for s in st], "visible": [s.visible_blocks for s in st],
+                           "decoded": [s.new_decompressed for s in st],
+                           "first_pass_completeness": round(st[0].completeness, 4) if st else 1.0,
+                           "algorithmic_gb": round(frame_bytes(st, n_rays, cv.block_stride_bytes) / 1e9, 3)})
+    # low -> high occlusion: renders grouped by isovalue (ascending), the
+    # share of rays the first pass terminates as the occlusion measure
+    by_iso = {}
+    for r in per_render:
+        by_iso.setdefault(r["iso_fraction"], []).append(r)
+    occlusion = [{"iso_fraction": k, "mean_frame_ms": round(float(np.mean([r["frame_ms"] for r in v])), 3),
+                  "mean_passes": round(float(np.mean([r["passes"] for r in v])), 2),
+                  "mean_first_pass_completeness": round(float(np.mean([r["first_pass_completeness"] for r in v])), 4)}
+                 for k, v in sorted(by_iso.items())]
+    parity = None if args.no_cpu_baseline else c5_parity(args, wl, cv, grids, tim)
     line = {
         "metric": METRIC, "value": round((w * h) / (ms * 1e-3) / 1e6, 3), "unit": UNIT, "n_gpus": 1,
         "steps": rep["n_renders"], "warmup": max(1, args.warmup), "ms_per_step": round(ms, 4),
@@ -517,12 +649,59 @@ def run_c5(args):
         "frame_ms": {"mean": round(ms, 4), "median": round(tim["median_frame_ms"], 4),
                      "max": round(tim["max_frame_ms"], 4), "all": [round(x, 3) for x in tim["frame_ms"]]},
         "passes_all": tim["passes"],
+        "occlusion_by_iso": occlusion,
+        "renders": per_render,
+        "parity": parity,
         "report": rep,
         "value_range": tim["value_range"],
         "clocks": clk.summary(),
         "setup_s": round(setup_s, 2),
     }
     emit(line)
+
+
+def c5_parity(args, wl, cv, grids, tim):
+    """Every protocol render again through render() (framebuffer to host) and
+    through the oracle as one full-frame session on a host thread each
+    (renders spread over the host's cores): pixels and per-pass PassStats."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import paper_2309_10212_b200 as wc
+    from oracle import oracle as orc
+
+    threads = os.cpu_count() or 1
+    field = wc.volume.separable_field(wl["kind"], wl["dims"], wl["seed"])
+    t = time.perf_counter()
+    pay, rng = orc.compress_separable(field.amp, field.fx, field.fy, field.fz, wl["dims"], wl["qbits"], threads)
+    synth_s = time.perf_counter() - t
+    ov = orc.volume_from_payload(wl["dims"], wl["qbits"], pay, rng)
+    w, h = wl["w"], wl["h"]
+    opts = wc.RenderOptions(width=w, height=h, max_spec=args.max_spec)
+    gpu = []
+    for iso, cam in tim["views"]:
+        fb, st = wc.render(cv, grids, cam, iso, opts)
+        sess = wc.engine.session_pool.items[-1][1]
+        gpu.append((fb.rgba.reshape(-1, 4).copy(), fb.depth.reshape(-1).copy(), st, list(sess.last_frame_c)))
+
+    def oracle_view(i):
+        iso, cam = tim["views"][i]
+        c = (tuple(cam.eye), tuple(cam.look_dir), tuple(cam.up), cam.fov_y)
+        o, d = orc.camera_rays(c, w, h)
+        return orc.render(ov, o, d, w, h, iso, max_spec=args.max_spec)
+
+    t = time.perf_counter()
+    pix_bad, stat_bad = 0, []
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        for i, (rgba, depth, st) in enumerate(ex.map(oracle_view, range(len(gpu)))):
+            g_rgba, g_depth, g_st, g_c = gpu[i]
+            pix_bad += int(np.count_nonzero((g_rgba != rgba).any(1) | (g_depth.view(np.uint32) !=
+                                                                        depth.view(np.uint32))))
+            stat_bad += [f"render {i}: {m}" for m in stats_mismatches(g_st, g_c, st)]
+    return {"renders_checked": len(gpu), "pixels_checked": int(len(gpu) * w * h), "pixel_mismatches": pix_bad,
+            "pass_stat_mismatches": stat_bad[:20], "pass_stats_checked": list(STAT_KEYS) + ["evicted"],
+            "oracle": f"one full-frame session per render, {threads} renders at a time on host threads "
+                      f"({time.perf_counter() - t:.0f} s)", "cpu_synth_s": round(synth_s, 1),
+            "cpu_volume_synth_bit_exact": bool(np.array_equal(pay, cv.payload))}
 
 
 # The JSON line is the only thing bench.py writes to stdout: native

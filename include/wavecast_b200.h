@@ -168,6 +168,20 @@ int wc_session_framebuffer(wc_session *s, uint8_t *rgba, float *depth);
  * wc_session_snapshot_wait(ticket) returns (or wc_session_sync). */
 int wc_session_snapshot(wc_session *s, uint32_t *rgba_host, float *depth_host, int64_t *ticket);
 int wc_session_snapshot_wait(wc_session *s, int64_t ticket);
+/* The session's CUDA stream (cudaStream_t), so a caller can order its own
+ * device work -- e.g. NCCL collectives over the session's buffers -- on it
+ * without host synchronisation. */
+int wc_session_stream(const wc_session *s, void **stream);
+/* The framebuffer packed into a caller DEVICE buffer: RGBA8 words at
+ * [0, n), depth bits at [stride, stride + n) (stride >= n), ordered on the
+ * session stream: a tile gather's send buffer. */
+int wc_session_framebuffer_packed(wc_session *s, void *dst_dev, int64_t stride_words);
+/* Multi-GPU frame assembly: packed holds n / stride blocks of
+ * [stride RGBA8 words | stride depth bits] (one per rank, a gather's receive
+ * buffer); pixel_ids (int64, n; < 0 = padding) maps block b's entry i to its
+ * pixel.  Writes frame rgba / depth (DEVICE, u32 per pixel) on `stream`. */
+int wc_scatter_pixels(const void *packed_dev, int64_t stride_words, const void *pixel_ids_dev, int64_t n,
+                      void *rgba_dev, void *depth_dev, void *stream);
 /* Same into caller-owned DEVICE buffers (for NCCL tile gathers). */
 int wc_session_framebuffer_device(wc_session *s, void *rgba_dev, void *depth_dev);
 /* Device time of the last pass (CUDA events on the session stream). */
@@ -185,6 +199,13 @@ int wc_session_frame_ms(wc_session *s, double *ms);
 int wc_session_stage_ms(const wc_session *s, double *ms6);
 /* The same split for one pass (pass_index < 128) of the current frame. */
 int wc_session_pass_stage_ms(const wc_session *s, int64_t pass_index, double *ms6);
+
+/* Per-kernel device time of the passes launched kernel by kernel (graphs
+ * off, wc_session_set_graphs(s, 0)) while profiling is on: CUDA events on the
+ * session stream around every launch.  The text has one row per (pass,
+ * kernel): "pass<TAB>kernel<TAB>launches<TAB>ms".  *len = its length. */
+int wc_session_set_kernel_profile(wc_session *s, int on); /* also clears */
+int wc_session_kernel_profile(const wc_session *s, char *buf, int64_t cap, int64_t *len);
 
 /* ---- per-stage views of the last pass (parity tests) */
 /* sizes[8] = slots_used, n_visible, n_active_blocks, n_entries, n_spec,

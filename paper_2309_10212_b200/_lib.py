@@ -106,6 +106,11 @@ _SIGS = {
     "wc_session_framebuffer": (_i32, [_vp, _vp, _vp]),
     "wc_session_framebuffer_device": (_i32, [_vp, _vp, _vp]),
     "wc_session_snapshot": (_i32, [_vp, _vp, _vp, _vp]),
+    "wc_session_set_kernel_profile": (_i32, [_vp, _i32]),
+    "wc_session_stream": (_i32, [_vp, _vp]),
+    "wc_session_framebuffer_packed": (_i32, [_vp, _vp, _i64]),
+    "wc_scatter_pixels": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),
+    "wc_session_kernel_profile": (_i32, [_vp, _vp, _i64, _vp]),
     "wc_session_snapshot_wait": (_i32, [_vp, _i64]),
     "wc_session_last_pass_ms": (_i32, [_vp, _vp]),
     "wc_session_destroy": (_i32, [_vp]),

@@ -67,13 +67,15 @@ def bench_report(cv, grids, *, isovalues: int = 100, orbit_steps: int = 10, seed
     pass_counts, visible_fracs, spec_counts, utilizations = [], [], [], []
     completeness_curves, new_per_pass = [], []
     max_slots = 0
-    frame_ms, wall_ms = [], []
+    frame_ms, wall_ms, views, all_stats = [], [], [], []
     for iso, cam in bench_scenes(cv.dims, value_range, isovalues, orbit_steps, seed, iso_range):
         t0 = time.perf_counter()
         sess = session_pool.get(cv, grids, opts, cam)
         stats = sess.render_frame(cam, iso)
         wall_ms.append((time.perf_counter() - t0) * 1e3)
         frame_ms.append(sess.frame_ms())
+        views.append((iso, cam))
+        all_stats.append(stats)
         pass_counts.append(len(stats))
         if stats:
             visible_fracs.append(float(np.mean([s.visible_blocks for s in stats])) / cv.block_count)
@@ -117,5 +119,7 @@ def bench_report(cv, grids, *, isovalues: int = 100, orbit_steps: int = 10, seed
         "max_frame_ms": float(np.max(frame_ms)) if frame_ms else 0.0,
         "passes": pass_counts,
         "value_range": list(value_range),
+        "views": views,          # (iso, Camera) of every render, in order
+        "stats": all_stats,      # its PassStats
     }
     return report, timings

@@ -568,6 +568,47 @@ int wc_session_sync(wc_session *s) {
     WC_API_END
 }
 
+int wc_session_stream(const wc_session *s, void **stream) {
+    WC_API_BEGIN
+    *stream = (void *)s->s->st;
+    WC_API_END
+}
+
+int wc_session_framebuffer_packed(wc_session *s, void *dst_dev, int64_t stride_words) {
+    WC_API_BEGIN
+    WC_REQUIRE(stride_words >= s->s->n, wc::UsageError, "packed stride below the session's pixel count");
+    s->s->pack_framebuffer(static_cast<uint32_t *>(dst_dev), stride_words);
+    WC_API_END
+}
+
+int wc_scatter_pixels(const void *packed_dev, int64_t stride_words, const void *pixel_ids_dev, int64_t n,
+                      void *rgba_dev, void *depth_dev, void *stream) {
+    WC_API_BEGIN
+    wc::scatter_pixels(static_cast<const uint32_t *>(packed_dev), stride_words,
+                       static_cast<const int64_t *>(pixel_ids_dev), n, static_cast<uint32_t *>(rgba_dev),
+                       static_cast<uint32_t *>(depth_dev), static_cast<cudaStream_t>(stream));
+    WC_API_END
+}
+
+int wc_session_set_kernel_profile(wc_session *s, int on) {
+    WC_API_BEGIN
+    s->s->kernel_profile = on != 0;
+    s->s->kstats.clear();
+    WC_API_END
+}
+
+int wc_session_kernel_profile(const wc_session *s, char *buf, int64_t cap, int64_t *len) {
+    WC_API_BEGIN
+    const std::string t = s->s->kernel_profile_text();
+    *len = (int64_t)t.size();
+    if (buf && cap > 0) {
+        const size_t k = std::min<size_t>((size_t)cap - 1, t.size());
+        memcpy(buf, t.data(), k);
+        buf[k] = 0;
+    }
+    WC_API_END
+}
+
 int wc_session_snapshot(wc_session *s, uint32_t *rgba_host, float *depth_host, int64_t *ticket) {
     WC_API_BEGIN
     WC_REQUIRE(rgba_host && depth_host, wc::UsageError, "snapshot needs host buffers");

@@ -13,6 +13,7 @@
 #include <cstring>
 
 #include <cstdlib>
+#include <cxxabi.h>
 
 #include "wc_engine.cuh"
 #include "wc_trace.cuh"
@@ -2183,7 +2184,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
             t_ktime_stream = nullptr;
             t_ktime = nullptr;
         }
-    } kscope(ktime_on && !capturing, st, &ktime, p);
+    } kscope((ktime_on || kernel_profile) && !capturing, st, &ktime, p);
     auto mark = [&](int k) {
         if (ev && !capturing) WC_CUDA(cudaEventRecord(ev[k], st));
     };
@@ -2313,8 +2314,35 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
 
 // WAVECAST_KTIME: device time of every launch since the last report, by
 // pass and launch site (the stream has been synchronised by the caller).
+// Readable kernel name: the demangled symbol without its return type,
+// namespace and parameter list (template arguments kept).
+static std::string kernel_name(const void *func) {
+    if (!func) return "?";
+    const char *raw = nullptr;
+    if (cudaFuncGetName(&raw, func) != cudaSuccess || !raw) return "?";
+    std::string s = raw;
+    int status = 0;
+    if (char *dm = abi::__cxa_demangle(raw, nullptr, nullptr, &status)) {
+        if (status == 0) s = dm;
+        free(dm);
+    }
+    if (s.rfind("void ", 0) == 0) s = s.substr(5);
+    int depth = 0;
+    for (size_t i = 0; i < s.size(); i++) {  // cut the parameter list (the first '(' outside <>)
+        if (s[i] == '<') depth++;
+        if (s[i] == '>') depth--;
+        if (s[i] == '(' && depth == 0) {
+            s = s.substr(0, i);
+            break;
+        }
+    }
+    for (size_t q; (q = s.find("wc::")) != std::string::npos;) s.erase(q, 4);
+    return s;
+}
+
 void Session::ktime_report() {
     if (ktime.empty()) return;
+    static const bool print = getenv("WAVECAST_KTIME") != nullptr;
     int pass = -1, k = 0;
     for (size_t i = 0; i < ktime.size(); i++) {
         const KTime &t = ktime[i];
@@ -2326,11 +2354,32 @@ void Session::ktime_report() {
         float ms = 0.0f;
         if (i > 0) cudaEventElapsedTime(&ms, ktime[i - 1].ev, t.ev);
         const char *base = strrchr(t.file, '/');
-        fprintf(stderr, "[ktime] pass %d #%02d %s:%d %.1f us\n", pass, k++, base ? base + 1 : t.file, t.line,
-                ms * 1e3f);
+        if (print)
+            fprintf(stderr, "[ktime] pass %d #%02d %s:%d %.1f us\n", pass, k++, base ? base + 1 : t.file, t.line,
+                    ms * 1e3f);
+        if (kernel_profile) {
+            const std::string key = std::to_string(pass) + "\t" + kernel_name(t.func);
+            auto it = std::find_if(kstats.begin(), kstats.end(), [&](const auto &e) { return e.first == key; });
+            if (it == kstats.end()) {
+                kstats.push_back({key, KStat{}});
+                it = kstats.end() - 1;
+            }
+            it->second.calls++;
+            it->second.ms += ms;
+        }
     }
     for (auto &t : ktime) cudaEventDestroy(t.ev);
     ktime.clear();
+}
+
+std::string Session::kernel_profile_text() const {
+    std::string out;
+    char buf[64];
+    for (const auto &e : kstats) {
+        snprintf(buf, sizeof(buf), "\t%lld\t%.6f\n", (long long)e.second.calls, e.second.ms);
+        out += e.first + buf;
+    }
+    return out;
 }
 
 void Session::check_device_errors() {
@@ -2405,6 +2454,7 @@ bool Session::pass(PassStatsC &stats) {
     WC_CUDA(cudaMemcpyAsync(h_plog.p, plog.p, 4 * L_COUNT * std::min<int64_t>(pass_index + 1, kMaxPassLog),
                             cudaMemcpyDeviceToHost, st));
     read_counters(0, C_COUNT);
+    ktime_report();
     check_device_errors();
     collect_pass(pass_index, stats);
     pass_index++;
@@ -2591,6 +2641,30 @@ void Session::download_framebuffer(uint8_t *rgba_host, float *depth_host) {
     if (rgba_host) WC_CUDA(cudaMemcpyAsync(rgba_host, rgba.p, 4 * n, cudaMemcpyDeviceToHost, st));
     if (depth_host) WC_CUDA(cudaMemcpyAsync(depth_host, depth.p, 4 * n, cudaMemcpyDeviceToHost, st));
     WC_CUDA(cudaStreamSynchronize(st));
+}
+
+void Session::pack_framebuffer(uint32_t *dst, int64_t stride) {
+    WC_CUDA(cudaMemcpyAsync(dst, rgba.p, 4 * n, cudaMemcpyDeviceToDevice, st));
+    WC_CUDA(cudaMemcpyAsync(dst + stride, depth.p, 4 * n, cudaMemcpyDeviceToDevice, st));
+}
+
+__global__ void k_scatter_pixels(const uint32_t *packed, int64_t stride, const int64_t *ids, int64_t n, uint32_t *rgba,
+                                 uint32_t *depth) {
+    pdl_wait();
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = ids[j];
+        if (p < 0) continue;
+        const int64_t b = j / stride, i = j - b * stride;
+        rgba[p] = packed[2 * stride * b + i];
+        depth[p] = packed[2 * stride * b + stride + i];
+    }
+}
+
+void scatter_pixels(const uint32_t *packed, int64_t stride, const int64_t *ids, int64_t n, uint32_t *rgba,
+                    uint32_t *depth, cudaStream_t st) {
+    if (n <= 0) return;
+    launch_pdl(k_scatter_pixels, grid_for(n, 256), 256, 0, st, packed, stride, ids, n, rgba, depth);
+    WC_LAUNCH_CHECK();
 }
 
 void Session::copy_framebuffer_device(void *rgba_dst, void *depth_dst) {

@@ -1,6 +1,7 @@
 // wc_engine.cuh -- the per-pass wavefront session (engine.py:308-382).
 #pragma once
 
+#include <string>
 #include <vector>
 
 #include "wc_common.cuh"
@@ -228,6 +229,15 @@ struct Session : CacheStore {
     float last_kernel_ms = 0.0f;
     std::vector<KTime> ktime;  // WAVECAST_KTIME: per-launch events of the directly enqueued passes
     void ktime_report();
+    // per-kernel device time of the directly enqueued passes (graphs off),
+    // accumulated while kernel_profile is on: "pass\tkernel\tcalls\tms" rows
+    bool kernel_profile = false;
+    struct KStat {
+        int64_t calls = 0;
+        double ms = 0.0;
+    };
+    std::vector<std::pair<std::string, KStat>> kstats;  // key "pass\tkernel"
+    std::string kernel_profile_text() const;
 
     Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, int64_t n_rays, const double *origins,
             const double *dirs, double iso, int speculation, int max_spec, int64_t cache_capacity, int corrupt);
@@ -254,6 +264,10 @@ struct Session : CacheStore {
     void snapshot_wait(int64_t ticket);
     void sync_all();  // session and copy streams
     void copy_framebuffer_device(void *rgba_dst, void *depth_dst);
+    // rgba words at dst[0, n), depth bits at dst[stride, stride + n) (stride
+    // >= n), stream-ordered on the session stream (no host sync): the send
+    // buffer of a tile gather
+    void pack_framebuffer(uint32_t *dst, int64_t stride);
 
     double reset_device_ms();  // device time of the last reset, once it has run
     int64_t active_count();    // active rays now (read from the device after a reset)
@@ -297,6 +311,13 @@ struct Session : CacheStore {
     DevBuf<uint4> patch;
     PinnedBuf<uint4> h_patch;
 };
+
+// Finished tiles into the frame (multi-GPU gather): for every
+// source b in [0, n / stride) and i < stride, pixel ids[b*stride + i] (< 0:
+// padding) gets packed[2*stride*b + i] (RGBA8 word) and
+// packed[2*stride*b + stride + i] (depth bits).
+void scatter_pixels(const uint32_t *packed, int64_t stride, const int64_t *ids, int64_t n, uint32_t *rgba,
+                    uint32_t *depth, cudaStream_t st);
 
 // Brute-force oracle on the device (oracle.py:42-122): every ray marches all
 // dual cells of the fully decoded volume.  d_values dense float32 x-fastest.

@@ -4,9 +4,13 @@ Each rank holds the full compressed volume and its own LRU cache and renders
 an interleaved subset of square tiles as one device session (its own pass
 loop, n_act and n_spec).  Because speculation never changes final pixels
 (engine.py:1-9), the stitched frame equals the single-GPU frame bit for bit.
-The only exchange step is the final tile gather: every rank's RGBA8+depth
-(8 B/pixel) goes to rank 0 with one NCCL collective over NVLink
-(``torch.distributed``; gloo on CPU for tests).
+The exchange steps are the per-iso range tests (each rank computes a slice,
+two in-place all-gathers assemble them) and the final tile gather: every
+rank's RGBA8+depth (8 B/pixel) goes to rank 0 alone with one NCCL gather
+over NVLink, scattered into the frame on rank 0's GPU (wc_scatter_pixels).
+All of it is ordered on the session's CUDA stream, so a frame has no host
+synchronisation besides the pass loop's own (``torch.distributed``; gloo on
+CPU for tests).
 """
 
 from __future__ import annotations
@@ -38,8 +42,9 @@ _GATHER_CACHE: dict = {}
 
 def _gather_plan(w, h, world, tile, dev):
     """Per (image, world, tile): every rank's pixel list is a pure function of
-    (w, h, rank, world, tile), so no pixel ids travel -- rank 0 scatters each
-    rank's block of words with a precomputed index (padding -> dummy slot w*h)."""
+    (w, h, rank, world, tile), so no pixel ids travel.  Each rank sends one
+    block of [RGBA words | depth bits] padded to n_max pixels; the pixel id of
+    every received word is precomputed (-1 = padding)."""
     import torch
 
     key = (w, h, world, tile, str(dev))
@@ -47,71 +52,132 @@ def _gather_plan(w, h, world, tile, dev):
     if plan is None:
         pix = [tile_pixels(w, h, r, world, tile) for r in range(world)]
         n_max = max(1, max(len(p) for p in pix))
-        index = np.full((world, n_max), w * h, dtype=np.int64)
+        index = np.full((world, n_max), -1, dtype=np.int64)
         for r, p in enumerate(pix):
             index[r, :len(p)] = p
         plan = {
             "n_max": n_max,
+            "index_np": index,
             "index": torch.from_numpy(index.reshape(-1)).to(dev),
-            "send": torch.zeros((2, n_max), dtype=torch.int32, device=dev),
-            "recv": torch.empty((world, 2, n_max), dtype=torch.int32, device=dev),
-            "frame": torch.zeros((2, w * h + 1), dtype=torch.int32, device=dev),
+            "send": torch.zeros(2 * n_max, dtype=torch.int32, device=dev),
+            "recv": torch.zeros((world, 2 * n_max), dtype=torch.int32, device=dev),
+            "frame": torch.zeros((2, w * h), dtype=torch.int32, device=dev),
         }
         _GATHER_CACHE.clear()
         _GATHER_CACHE[key] = plan
     return plan
 
 
+def check_tiles(w: int, h: int, world: int, tile: int) -> None:
+    """Every rank must own at least one tile: the frame's collectives (range
+    tests, tile gather) need all ranks (UsageError otherwise)."""
+    from .errors import UsageError
+
+    n_tiles = (-(w // -tile)) * (-(h // -tile))
+    if n_tiles < world:
+        raise UsageError(f"{w}x{h} in {tile}x{tile} tiles gives {n_tiles} tiles for {world} ranks: "
+                         "use smaller tiles or fewer ranks")
+
+
+def _to_frame(plan, w, h, dev, stream=None):
+    """Rank 0: the scattered frame -> (rgba (h,w,4) u8, depth (h,w) f32) in host memory."""
+    import torch
+
+    frame = plan["frame"]
+    if dev.type == "cuda":  # read back into a recycled page-locked buffer (full-speed D2H)
+        from . import _lib
+
+        base = _lib.pinned_pool.get(8 * w * h)
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            torch.from_numpy(base.view(np.int32)).view(2, w * h).copy_(frame, non_blocking=True)
+        (stream or torch.cuda.current_stream(dev)).synchronize()
+    else:
+        base = frame.contiguous().numpy().view(np.uint8).reshape(-1)
+    return base[:4 * w * h].reshape(h, w, 4), base[4 * w * h:].view(np.float32).reshape(h, w)
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def gather_tiles(rgba_local, depth_local, w: int, h: int, tile: int = 32, group=None):
     """The finished tiles -> rank 0 (the pass loop's only exchange step):
-    one all_gather_into_tensor of every rank's [RGBA words | depth bits]
-    (8 B per pixel, over NCCL/NVLink; gloo on CPU), then one scatter into the
-    frame on rank 0.  Inputs are the rank's (n,4) uint8 and (n,) float32
-    torch tensors in tile_pixels order.  Returns (rgba (h,w,4) uint8,
-    depth (h,w) float32) numpy on rank 0, None elsewhere."""
-    import torch
+    one gather of every rank's [RGBA words | depth bits] (8 B per pixel, over
+    NCCL/NVLink; gloo on CPU) to rank 0 alone, then the scatter into the frame
+    (wc_scatter_pixels on the device).  Inputs are the rank's (n,4) uint8 and
+    (n,) float32 torch tensors in tile_pixels order.  Returns (rgba (h,w,4)
+    uint8, depth (h,w) float32) numpy on rank 0, None elsewhere."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = rgba_local.device
+    check_tiles(w, h, world, tile)
     plan = _gather_plan(w, h, world, tile, dev)
     k = rgba_local.shape[0]
+    n_max = plan["n_max"]
     send = plan["send"]
-    if k:
-        send[0, :k] = rgba_local.reshape(-1).view(torch.int32)
-        send[1, :k] = depth_local.view(torch.int32)
-    dist.all_gather_into_tensor(plan["recv"].view(-1), send.view(-1), group=group)
+    send[:k] = rgba_local.reshape(-1).view(dtype=__import__("torch").int32)
+    send[n_max:n_max + k] = depth_local.view(dtype=__import__("torch").int32)
+    return _gather_and_scatter(plan, rank, world, w, h, dev, group, None)
+
+
+def _gather_and_scatter(plan, rank, world, w, h, dev, group, stream):
+    import torch.distributed as dist
+
+    recv = plan["recv"]
+    dist.gather(plan["send"], list(recv.unbind(0)) if rank == 0 else None, dst=0, group=group)
     if rank != 0:
         return None
     frame = plan["frame"]
-    idx = plan["index"]
-    frame[0].index_copy_(0, idx, plan["recv"][:, 0, :].reshape(-1))
-    frame[1].index_copy_(0, idx, plan["recv"][:, 1, :].reshape(-1))
-    frame = frame[:, : w * h]  # [rgba words | depth bits], dummy slot dropped
-    if dev.type == "cuda":  # read back into a recycled page-locked buffer (full-speed D2H)
+    n_max = plan["n_max"]
+    if dev.type == "cuda":
         from . import _lib
 
-        base = _lib.pinned_pool.get(8 * w * h)
-        torch.from_numpy(base.view(np.int32)).view(2, w * h).copy_(frame)
-    else:
-        base = frame.contiguous().numpy().view(np.uint8).reshape(-1)
-    rgba_np = base[:4 * w * h].reshape(h, w, 4)
-    depth_np = base[4 * w * h:].view(np.float32).reshape(h, w)
-    return rgba_np, depth_np
+        _lib.call("wc_scatter_pixels", recv.data_ptr(), n_max, plan["index"].data_ptr(), world * n_max,
+                  frame[0].data_ptr(), frame[1].data_ptr(), stream.cuda_stream if stream is not None else
+                  __import__("torch").cuda.current_stream(dev).cuda_stream)
+    else:  # gloo (CPU tests): the same scatter on the host
+        idx = plan["index_np"]
+        r = recv.numpy().reshape(world, 2, n_max)
+        f = frame.numpy()
+        ok = idx >= 0
+        f[0][idx[ok]] = r[:, 0, :][ok]
+        f[1][idx[ok]] = r[:, 1, :][ok]
+    return _to_frame(plan, w, h, dev, stream)
 
 
-def render_frame_split(sess, cam, iso, group=None):
+def session_stream(sess):
+    """The session's CUDA stream as a torch stream (collectives on the session's
+    buffers are ordered on it: no host synchronisation around them)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+
+    p = C.c_void_p()
+    _lib.call("wc_session_stream", sess.handle, C.byref(p))
+    return torch.cuda.ExternalStream(p.value, device=torch.device("cuda", torch.cuda.current_device()))
+
+
+def render_frame_split(sess, cam, iso, group=None, split=None):
     """One frame of a rank's tile session with the per-iso range tests split
     across the ranks (the exchange step of a multi-GPU frame besides the tile
     gather): each rank computes its slice of coarse cells (coarse bitmap
-    words and 64-bit fine masks) during reset, one all-gather per buffer over
-    NCCL assembles them in place, then the passes run.  Returns the stats."""
+    words and 64-bit fine masks) during reset, two all-gathers over NCCL
+    assemble them in place -- enqueued on the session's stream, after the
+    reset and before the passes, with no host synchronisation -- then the
+    passes run.  Returns the stats."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    if world == 1:
+    if not (world > 1 if split is None else split):  # one rank: nothing to exchange
         return sess.render_frame(cam, iso)
     rank = dist.get_rank(group)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -119,29 +185,29 @@ def render_frame_split(sess, cam, iso, group=None):
     cb, cm, chunk = sess.mask_buffers(world)
     bits = torch.as_tensor(_DeviceBytes(cb, 4 * chunk * world), device=dev)
     masks = torch.as_tensor(_DeviceBytes(cm, 8 * 32 * chunk * world), device=dev)
-    sess.sync()  # the slice is written (session stream) before NCCL reads it
-    for buf, per in ((bits, 4 * chunk), (masks, 8 * 32 * chunk)):
-        dist.all_gather_into_tensor(buf, buf[rank * per:(rank + 1) * per], group=group)
-    torch.cuda.current_stream(dev).synchronize()  # gathered before the passes read them
+    with torch.cuda.stream(session_stream(sess)):
+        for buf, per in ((bits, 4 * chunk), (masks, 8 * 32 * chunk)):
+            dist.all_gather_into_tensor(buf, buf[rank * per:(rank + 1) * per], group=group)
     return sess.run()
 
 
 _SHARD_SESSIONS: dict = {}
 
 
-def render_sharded(cv, grids, cam, iso, opts, tile: int = 32, group=None):
+def render_sharded(cv, grids, cam, iso, opts, tile: int = 32, group=None, split=None):
     """Render this rank's tiles on its GPU, gather the frame to rank 0.
-    Returns (framebuffer or None, local PassStats list, session device ms)."""
+    Returns (framebuffer or None, local PassStats list).  The framebuffer
+    pack, the gather and the scatter are ordered on the session's stream."""
     import torch
     import torch.distributed as dist
 
-    from .engine import Framebuffer, RenderSession
-
     from . import _lib
+    from .engine import Framebuffer, RenderSession
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = torch.device("cuda", torch.cuda.current_device())
+    check_tiles(opts.width, opts.height, world, tile)
     # one pooled session (and tile set) per (volume, image, options, world):
     # later frames reuse its HBM allocations through wc_session_render
     key = (id(cv), opts.width, opts.height, opts.speculation, opts.max_spec, opts.cache_capacity,
@@ -149,19 +215,17 @@ def render_sharded(cv, grids, cam, iso, opts, tile: int = 32, group=None):
     ent = _SHARD_SESSIONS.get(key)
     if ent is None or ent[0].cv is not cv:
         pix = tile_pixels(opts.width, opts.height, rank, world, tile)
-        s = RenderSession(cv, grids, cam, iso, opts, pixel_ids=pix) if len(pix) else None
+        s = RenderSession(cv, grids, cam, iso, opts, pixel_ids=pix)
         ent = (s, pix)
         _SHARD_SESSIONS.clear()
         _SHARD_SESSIONS[key] = ent
     s, pix = ent
-    n = len(pix)
-    rgba_t = torch.empty((n, 4), dtype=torch.uint8, device=dev)
-    depth_t = torch.empty(n, dtype=torch.float32, device=dev)
-    stats = []
-    if n:
-        stats = render_frame_split(s, cam, iso, group)
-        _lib.call("wc_session_framebuffer_device", s.handle, rgba_t.data_ptr(), depth_t.data_ptr())
-    out = gather_tiles(rgba_t, depth_t, opts.width, opts.height, tile, group)
+    stats = render_frame_split(s, cam, iso, group, split)
+    plan = _gather_plan(opts.width, opts.height, world, tile, dev)
+    stream = session_stream(s)
+    _lib.call("wc_session_framebuffer_packed", s.handle, plan["send"].data_ptr(), plan["n_max"])
+    with torch.cuda.stream(stream):
+        out = _gather_and_scatter(plan, rank, world, opts.width, opts.height, dev, group, stream)
     if out is None:
         return None, stats
     rgba, depth = out

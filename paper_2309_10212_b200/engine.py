@@ -310,7 +310,13 @@ class RenderSession:
         buf = (_lib.PassStatsC * self._MAX_STATS)()
         k = C.c_int64()
         _lib.call("wc_session_run", self._h, buf, self._MAX_STATS, C.byref(k))
-        return [_stats_from_c(buf[i]) for i in range(min(k.value, self._MAX_STATS))]
+        return self._frame_stats(buf, k.value)
+
+    def _frame_stats(self, buf, k: int) -> list[PassStats]:
+        """PassStats of a frame; the C records (with evicted / n_entries) stay in last_frame_c."""
+        k = min(int(k), self._MAX_STATS)
+        self.last_frame_c = [{f: getattr(buf[i], f) for f, _ in _lib.PassStatsC._fields_} for i in range(k)]
+        return [_stats_from_c(buf[i]) for i in range(k)]
 
     def render_frame(self, cam: Camera | None, iso: float) -> list[PassStats]:
         """reset(cam, iso) + run() in a single C call (no Python inside the frame)."""
@@ -319,7 +325,7 @@ class RenderSession:
         k = C.c_int64()
         _lib.call("wc_session_render", self._h, None if cam_c is None else C.byref(cam_c), float(iso), buf,
                   self._MAX_STATS, C.byref(k))
-        return [_stats_from_c(buf[i]) for i in range(min(k.value, self._MAX_STATS))]
+        return self._frame_stats(buf, k.value)
 
     def reset_part(self, cam: Camera | None, iso: float, part: int, parts: int) -> None:
         """reset with the per-iso range tests computed for coarse-cell slice
@@ -353,7 +359,7 @@ class RenderSession:
         depth = base[4 * self.n:8 * self.n].view(np.float32)
         _lib.call("wc_session_render_host", self._h, None if cam_c is None else C.byref(cam_c), float(iso), buf,
                   self._MAX_STATS, C.byref(k), _lib.ptr(rgba), _lib.ptr(depth))
-        return [_stats_from_c(buf[i]) for i in range(min(k.value, self._MAX_STATS))], rgba, depth
+        return self._frame_stats(buf, k.value), rgba, depth
 
     def reset(self, cam: Camera | None, iso: float) -> None:
         """New frame on the same allocations (fresh rays, framebuffer, cache)."""
@@ -377,6 +383,23 @@ class RenderSession:
         a = (C.c_double * 6)()
         _lib.call("wc_session_pass_stage_ms", self._h, int(pass_index), a)
         return dict(zip(STAGES, [float(x) for x in a]))
+
+    def set_kernel_profile(self, on: bool) -> None:
+        """Collect per-kernel device times of passes launched kernel by
+        kernel (set_graphs(False)); clears the previous collection."""
+        _lib.call("wc_session_set_kernel_profile", self._h, int(bool(on)))
+
+    def kernel_profile(self) -> list[dict]:
+        """[{pass, kernel, launches, ms}] accumulated since set_kernel_profile(True)."""
+        n = C.c_int64()
+        _lib.call("wc_session_kernel_profile", self._h, None, 0, C.byref(n))
+        buf = C.create_string_buffer(int(n.value) + 1)
+        _lib.call("wc_session_kernel_profile", self._h, buf, int(n.value) + 1, C.byref(n))
+        rows = []
+        for line in buf.value.decode().splitlines():
+            p, k, c, ms = line.split("\t")
+            rows.append({"pass": int(p), "kernel": k, "launches": int(c), "ms": float(ms)})
+        return rows
 
     def last_pass_ms(self) -> float:
         v = C.c_double()

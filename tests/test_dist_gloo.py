@@ -107,3 +107,14 @@ def test_gloo_volume_broadcast():
         p.join(timeout=120)
         assert p.exitcode == 0
     assert res == {0: True, 1: True}
+
+
+def test_sharding_rejects_fewer_tiles_than_ranks():
+    # every rank takes part in the frame's collectives, so each must own a tile
+    from paper_2309_10212_b200 import dist as wdist
+    from paper_2309_10212_b200.errors import UsageError
+
+    with pytest.raises(UsageError, match="tiles"):
+        wdist.check_tiles(64, 64, 8, 32)
+    wdist.check_tiles(64, 64, 4, 32)
+    assert sum(len(wdist.tile_pixels(64, 64, r, 4, 32)) for r in range(4)) == 64 * 64
