@@ -207,6 +207,53 @@ struct PredMiss {  // active block not resident (cache.py:69-72)
     __device__ __forceinline__ uint32_t operator()(int64_t i) const { return slot_of_block[ids[i]] < 0; }
 };
 
+// cache.py:69-78 in one pass over the active ids: a resident block's slot is
+// stamped with this pass (its last_used moves from bin `old` to bin pass_no
+// of the stamp histogram kept after the counters, via per-CTA bins), a
+// non-resident block is a miss (the scan's value 1, compacted in ascending
+// id order).  The scan runs this loader only in the tile's owner, at most
+// twice per element and by the same thread, so a plain read-modify-write
+// moves each hit's histogram count once.
+__device__ __forceinline__ int32_t *stamp_bins() {
+    __shared__ int32_t bins[kHistBins + 1];  // [kHistBins]: hits moved into this pass's bin
+    return bins;
+}
+struct LookupStamp {
+    const uint32_t *ids;
+    const int32_t *slot_of_block;
+    int32_t *last_used;
+    int32_t pass_no;
+    uint32_t *hist;  // nullptr: no histogram upkeep (passes past kHistBins)
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const {
+        const int32_t s = slot_of_block[ids[i]];
+        if (s < 0) return 1u;
+        const int32_t old = last_used[s];
+        if (old != pass_no) {  // (a second load of the element by its thread finds it stamped)
+            last_used[s] = pass_no;
+            if (hist) {
+                atomicSub(&stamp_bins()[old], 1);
+                atomicAdd(&stamp_bins()[kHistBins], 1);
+            }
+        }
+        return 0u;
+    }
+    __device__ __forceinline__ void cta_begin() const {
+        if (hist)
+            for (int b = threadIdx.x; b <= kHistBins; b += blockDim.x) stamp_bins()[b] = 0;
+    }
+    __device__ __forceinline__ void cta_end() const {
+        if (!hist) return;
+        __syncthreads();
+        for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
+            const int32_t v = stamp_bins()[b];
+            if (v) atomicAdd(&hist[b], (uint32_t)v);  // two's complement: subtracts
+        }
+        if (threadIdx.x == 0 && stamp_bins()[kHistBins]) atomicAdd(&hist[pass_no], (uint32_t)stamp_bins()[kHistBins]);
+        __threadfence();  // performed before the CTA's end arrival (the cache plan reads the histogram)
+        __syncthreads();
+    }
+};
+
 template <class Pred>
 __global__ void k_compact_index(Pred pred, int64_t n, const uint32_t *off, uint32_t *out) {
     pdl_wait();
@@ -282,6 +329,24 @@ constexpr int kFineRun = 10;  // a monotone ray visits at most 4+4+4-2 fine cell
 // bit of fine cell f in its coarse cell's iso mask (k_iso_cell_mask)
 __device__ __forceinline__ int fine_local(const Dda &f) { return 16 * (f.cx & 3) + (f.cy & 3) + 4 * (f.cz & 3); }
 
+#ifndef WC_TRAV_AXIS
+#define WC_TRAV_AXIS 0  // per-axis exit tests (measured slower at C3: 0.88 vs 0.80 ms)
+#endif
+// dda_step that also reports the axis it stepped (0, 1, 2) and that axis'
+// new cell coordinate: only that coordinate changed, so the grid-exit and
+// leave-the-coarse-cell tests of the reference (traversal.py:315-355) reduce
+// to tests on it (the other two were inside before the step and still are).
+__device__ __forceinline__ double dda_step_ax(Dda &s, int sx, int sy, int sz, double dlx, double dly, double dlz,
+                                              int &ax, int &v) {
+    const bool mx = s.tx <= s.ty && s.tx <= s.tz;
+    const bool my = !mx && s.ty <= s.tz;
+    const double t = dda_step(s, sx, sy, sz, dlx, dly, dlz);
+    ax = mx ? 0 : (my ? 1 : 2);
+    v = mx ? s.cx : (my ? s.cy : s.cz);
+    return t;
+}
+__device__ __forceinline__ int pick3(int ax, int a, int b, int c) { return ax == 0 ? a : (ax == 1 ? b : c); }
+
 // traversal.py:217-403 _traverse_kernel, restructured for latency on B200:
 //  * persistent: a lane that finishes its ray fetches the next active ray
 //    from a warp-aggregated work counter, so divergent per-ray step counts do
@@ -301,6 +366,7 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
     pdl_wait();
     TraverseArgs a = a_in;
     a.n_act = a.ctl[C_NACT];
+    if (a.n_act <= (int64_t)a.warp_max) return;  // k_traverse_warp's pass
     a.n_spec = (int)a.ctl[C_NSPEC];
     a.rays.bind();
     const int lane = threadIdx.x & 31;
@@ -309,7 +375,7 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
     bool have = false, exhausted = false;
     uint32_t i = 0, r = 0;
     double ox = 0, oy = 0, oz = 0, dx = 0, dy = 0, dz = 0, te = 0;
-    double fdel_x = 0, fdel_y = 0, fdel_z = 0, cdel_x = 0, cdel_y = 0, cdel_z = 0;
+    double fdel_x = 0, fdel_y = 0, fdel_z = 0;  // coarse deltas: 4 * fdel (16/|d| == 4 * RN(4/|d|) exactly)
     int sx = 0, sy = 0, sz = 0, emitted = 0;
     Dda f{0, 0, 0, 0, 0, 0}, c{0, 0, 0, 0, 0, 0};
     bool in_fine_run = false;
@@ -341,9 +407,6 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
                     fdel_x = dx != 0.0 ? 4.0 / fabs(dx) : CUDART_INF;
                     fdel_y = dy != 0.0 ? 4.0 / fabs(dy) : CUDART_INF;
                     fdel_z = dz != 0.0 ? 4.0 / fabs(dz) : CUDART_INF;
-                    cdel_x = dx != 0.0 ? 16.0 / fabs(dx) : CUDART_INF;
-                    cdel_y = dy != 0.0 ? 16.0 / fabs(dy) : CUDART_INF;
-                    cdel_z = dz != 0.0 ? 16.0 / fabs(dz) : CUDART_INF;
                     const uint32_t cc = a.coarse_cell[r];
                     c.cx = (int)(cc % (uint32_t)cdx);
                     c.cy = (int)((cc / (uint32_t)cdx) % (uint32_t)cdy);
@@ -393,7 +456,7 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
         };
         if (!in_fine_run) {
             if (CA == 1) {  // one coarse step (traversal.py:332-386)
-                const double t = dda_step(c, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+                const double t = dda_step(c, sx, sy, sz, 4.0 * fdel_x, 4.0 * fdel_y, 4.0 * fdel_z);
                 if (t > te || c.cx < 0 || c.cx >= cdx || c.cy < 0 || c.cy >= cdy || c.cz < 0 || c.cz >= cdz) {
                     ray_done = true;
                     finished = true;
@@ -414,9 +477,15 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
 #pragma unroll
                 for (int j = 0; j < CA; j++) {
                     if (!done) {
-                        const double t = dda_step(g, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+#if WC_TRAV_AXIS
+                        int ax, v;
+                        const double t = dda_step_ax(g, sx, sy, sz, 4.0 * fdel_x, 4.0 * fdel_y, 4.0 * fdel_z, ax, v);
+                        if (t > te || (unsigned)v >= (unsigned)pick3(ax, cdx, cdy, cdz)) {
+#else
+                        const double t = dda_step(g, sx, sy, sz, 4.0 * fdel_x, 4.0 * fdel_y, 4.0 * fdel_z);
                         if (t > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 ||
                             g.cz >= cdz) {
+#endif
                             done = true;
                         } else {
                             cell[j] = (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz));
@@ -431,7 +500,7 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
                 if (bits) {
                     const int js = __ffs(bits) - 1;
                     double t_cross = 0.0;
-                    for (int j = 0; j <= js; j++) t_cross = dda_step(c, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+                    for (int j = 0; j <= js; j++) t_cross = dda_step(c, sx, sy, sz, 4.0 * fdel_x, 4.0 * fdel_y, 4.0 * fdel_z);
                     descend(t_cross);
                     fm = __ldg(a.cell_mask + (c.cx + cdx * (c.cy + cdy * c.cz)));
                 } else {
@@ -444,14 +513,39 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
             }
         }
         if (in_fine_run) {  // the rest of the run, from the register mask (traversal.py:295-331)
+            // the fine cell stays inside coarse cell c during a run: a step
+            // leaves c exactly when the stepped coordinate crosses a multiple
+            // of 4, and moves the cell's mask bit by 16 (x), 1 (y) or 4 (z)
+#if WC_TRAV_AXIS
+            int lb = fine_local(f);
+#endif
             for (int k = 0; k < kFineRun; k++) {
+#if WC_TRAV_AXIS
+                if ((fm >> lb) & 1ull) {
+#else
                 if ((fm >> fine_local(f)) & 1ull) {
+#endif
                     const uint32_t f_lin = (uint32_t)(f.cx + fdx * (f.cy + fdy * f.cz));
                     a.block_slots[base + emitted] = f_lin;
                     a.ray_slots[base + emitted] = r;
                     emitted++;
                     mark_visible(a.vis_bm, f_lin);
                 }
+#if WC_TRAV_AXIS
+                int ax, v;
+                const double t = dda_step_ax(f, sx, sy, sz, fdel_x, fdel_y, fdel_z, ax, v);
+                if (t > te || (unsigned)v >= (unsigned)pick3(ax, fdx, fdy, fdz)) {
+                    in_fine_run = false;
+                    ray_done = true;
+                    break;
+                }
+                const int st = pick3(ax, sx, sy, sz);
+                if ((v & 3) == (st > 0 ? 0 : 3)) {
+                    in_fine_run = false;
+                    break;
+                }
+                lb += st * pick3(ax, 16, 1, 4);
+#else
                 const double t = dda_step(f, sx, sy, sz, fdel_x, fdel_y, fdel_z);
                 if (t > te || f.cx < 0 || f.cx >= fdx || f.cy < 0 || f.cy >= fdy || f.cz < 0 || f.cz >= fdz) {
                     in_fine_run = false;
@@ -462,6 +556,7 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
                     in_fine_run = false;
                     break;
                 }
+#endif
                 if (emitted == a.n_spec) break;
             }
             finished = emitted == a.n_spec || ray_done;
@@ -515,6 +610,7 @@ __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a_in) {
     pdl_wait();
     TraverseArgs a = a_in;
     a.n_act = a.ctl[C_NACT];
+    if (a.n_act > (int64_t)a.warp_max) return;  // k_traverse's pass
     a.n_spec = (int)a.ctl[C_NSPEC];
     a.rays.bind();
     const int lane = threadIdx.x & 31;
@@ -839,12 +935,17 @@ __global__ void k_mark_active_words(const uint32_t *visible_ids, const uint32_t 
     }
 }
 
-void launch_traverse(const TraverseArgs &ta, int64_t n_grid, int64_t nact_guess, int variant, cudaStream_t st) {
-    if (variant == 2 || (variant == 0 && nact_guess <= WC_WARP_TRAVERSE_MAX))  // few (long) rays: warp-cooperative DDA
-        launch_pdl(k_traverse_warp, grid_for(std::max<int64_t>(1, nact_guess) * 32, 128, 16), 128, 0, st, ta);
-    else
+void launch_traverse(TraverseArgs ta, int64_t n_grid, int variant, cudaStream_t st) {
+    ta.warp_max = variant == 1 ? 0u : (variant == 2 ? 0xFFFFFFFFu : (uint32_t)WC_WARP_TRAVERSE_MAX);
+    if (variant != 2) {  // many rays: thread per ray, persistent
         launch_pdl(k_traverse<WC_COARSE_AHEAD>, grid_for(n_grid, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st, ta);
-    WC_LAUNCH_CHECK();
+        WC_LAUNCH_CHECK();
+    }
+    if (variant != 1) {  // few (long) rays: warp-cooperative DDA per ray
+        const int64_t most = variant == 2 ? n_grid : std::min<int64_t>(n_grid, WC_WARP_TRAVERSE_MAX);
+        launch_pdl(k_traverse_warp, grid_for(std::max<int64_t>(1, most) * 32, 128, 16), 128, 0, st, ta);
+        WC_LAUNCH_CHECK();
+    }
 }
 
 void launch_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvis, const uint32_t *vis_bm, int bdx, int bdy,
@@ -898,39 +999,6 @@ __global__ void k_run_offsets(const uint32_t *key, int64_t n, int64_t nvis, uint
 }
 
 // ---------------------------------------------------------------- cache
-
-// Stamp the hits (cache.py:73-74) and keep the stamp histogram (resident
-// slots per last_used value, after the counters) current: a hit moves its
-// slot from bin old to bin pass_no.  Per-CTA shared-memory bins, one global
-// update per touched bin.  Passes past kHistBins use the full recount.
-__global__ void k_cache_stamp(const uint32_t *ids, const uint32_t *d_n, int64_t n_max, const int32_t *slot_of_block,
-                              int32_t *last_used, int32_t pass_no, uint32_t *hist) {
-    pdl_wait();
-    __shared__ int32_t sh[kHistBins];
-    const bool keep = pass_no < kHistBins;
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) sh[b] = 0;
-    __syncthreads();
-    const int64_t n = min(n_max, (int64_t)*d_n);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t s = slot_of_block[ids[i]];
-        if (s < 0) continue;
-        const int32_t old = last_used[s];
-        if (old == pass_no) continue;
-        last_used[s] = pass_no;
-        if (keep) atomicSub(&sh[old], 1);
-    }
-    __syncthreads();
-    if (!keep) return;
-    int32_t moved = 0;
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x)
-        if (sh[b]) {
-            atomicAdd(&hist[b], (uint32_t)sh[b]);  // two's complement: subtracts
-            moved -= sh[b];
-        }
-    // hits moved into bin pass_no (block-wide sum of the subtractions)
-    for (int o = 16; o > 0; o >>= 1) moved += __shfl_xor_sync(0xffffffffu, moved, o);
-    if ((threadIdx.x & 31) == 0 && moved) atomicAdd(&hist[pass_no], (uint32_t)moved);
-}
 
 // eviction candidates (resident, stamp < pass_no) per stamp value
 // (few distinct stamps: per-CTA shared-memory bins, one global add per bin)
@@ -1186,6 +1254,7 @@ struct RaytraceArgs {
     const uint32_t *d_n_ent;  // entry count on the device (Counter C_NENT)
 };
 
+#if !WC_SPLIT_RAYTRACE  // the fused single-kernel raytrace (measured slower; kept for comparison builds)
 // engine.py:161-219 _raytrace_visible_kernel, one thread per ray-block entry
 // of the grouped (sorted-by-block) list, so neighbouring lanes trace the
 // same block and share its slot lines in L1.  Each entry runs the region
@@ -1216,6 +1285,8 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_raytrace(Raytrace
                                     : make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
     }
 }
+
+#endif
 
 // ---- two-phase raytrace: the same per-entry result as k_raytrace, with the
 // float64 cubic solves run as a dense work list so that the divergent DDA
@@ -1442,10 +1513,13 @@ __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
 
 // engine.py:222-258 _composite_kernel: closest speculated hit per active
 // ray (strict <, earliest entry wins ties), then terminate or keep.
+constexpr uint32_t kWarpCompositeSpec = 8;  // n_spec from which a warp composites one ray
+
 __global__ void k_composite(const uint32_t *ctl, const uint32_t *act_list, const uint32_t *emitted,
                             const uint32_t *entry_off, const float4 *rgbz, const uint8_t *exited, uint8_t *status,
                             uint32_t *rgba, float *depth, uint32_t *keep) {
     pdl_wait();
+    if (ctl[C_NSPEC] >= kWarpCompositeSpec) return;  // k_composite_warp's pass
     const int64_t n_act = ctl[C_NACT];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_act; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t r = act_list[i], ne = emitted[i], eo = entry_off[i];
@@ -1479,6 +1553,7 @@ __global__ void k_composite_warp(const uint32_t *ctl, const uint32_t *act_list, 
                                  const uint32_t *entry_off, const float4 *rgbz, const uint8_t *exited, uint8_t *status,
                                  uint32_t *rgba, float *depth, uint32_t *keep) {
     pdl_wait();
+    if (ctl[C_NSPEC] < kWarpCompositeSpec) return;  // k_composite's pass
     const int64_t n_act = ctl[C_NACT];
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -2031,18 +2106,17 @@ bool CacheStore::prepare_regions(int64_t stamp, int64_t n_blocks, DevBuf<uint32_
 // (ascending), then growth / victims / decode, all sized on the device
 void CacheStore::enqueue_lookup(uint32_t *ctl, const uint32_t *active_ids, int64_t nmax, int32_t stamp,
                                 int64_t n_blocks, uint32_t *partials, cudaStream_t st) {
-    launch_pdl(k_cache_stamp, grid_for(nmax, 256), 256, 0, st, active_ids, ctl + C_NACTB, nmax, slot_of_block.p,
-               last_used.p, stamp, ctl + C_COUNT);
-    WC_LAUNCH_CHECK();
-    // misses in ascending id order (cache.py:76-78), scan and compaction in
-    // one pass; the growth / eviction decisions (k_cache_plan) run as its
-    // epilogue while the stamp histogram is kept on the device
+    // hits stamped and misses listed in ascending id order (cache.py:69-78)
+    // in one scan + compaction pass; the growth / eviction decisions
+    // (k_cache_plan) run as its epilogue while the stamp histogram is kept on
+    // the device
     if (stamp < kHistBins)
-        compact_dev(PredMiss{active_ids, slot_of_block.p}, active_ids, ctl + C_NACTB, nmax, miss_ids.p, ctl + C_NMISS,
-                    partials, st, CachePlanEpilogue{ctl, ctl + C_COUNT, stamp, n_blocks, slot_alloc});
+        compact_dev(LookupStamp{active_ids, slot_of_block.p, last_used.p, stamp, ctl + C_COUNT}, active_ids,
+                    ctl + C_NACTB, nmax, miss_ids.p, ctl + C_NMISS, partials, st,
+                    CachePlanEpilogue{ctl, ctl + C_COUNT, stamp, n_blocks, slot_alloc});
     else
-        compact_dev(PredMiss{active_ids, slot_of_block.p}, active_ids, ctl + C_NACTB, nmax, miss_ids.p, ctl + C_NMISS,
-                    partials, st);
+        compact_dev(LookupStamp{active_ids, slot_of_block.p, last_used.p, stamp, nullptr}, active_ids, ctl + C_NACTB,
+                    nmax, miss_ids.p, ctl + C_NMISS, partials, st);
 }
 
 void CacheStore::enqueue_slow_plan(uint32_t *ctl, int32_t stamp, bool any_active, int64_t n_blocks, cudaStream_t st) {
@@ -2104,30 +2178,28 @@ void Session::drop_graphs() {
 // the device (control block, FrameParams, device-derived scan epochs), so a
 // replay is exactly the enqueued pass.  Modes with host reads inside a pass
 // (entry grouping, more passes than histogram bins) are enqueued directly.
-void Session::launch_pass(int64_t p, int64_t nact_guess) {
-    const bool warp_trav = nact_guess <= WC_WARP_TRAVERSE_MAX;
-    const bool warp_comp = speculation && n / std::max<int64_t>(1, nact_guess) >= 8;
+void Session::launch_pass(int64_t p) {
     if (!use_graphs || group_entries || p + 2 > kHistBins || p >= kMaxPassLog) {
-        enqueue_pass(p, nact_guess);
+        enqueue_pass(p);
         return;
     }
     prepare_pass(p);
     PassGraph *g = nullptr;
     for (auto &x : graphs)
-        if (x.p == p && x.warp_trav == warp_trav && x.warp_comp == warp_comp) g = &x;
+        if (x.p == p) g = &x;
     if (!g) {
         const long long launches0 = g_launches.load();
         cudaGraph_t graph = nullptr;
         WC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         try {
-            enqueue_pass(p, nact_guess);
+            enqueue_pass(p);
         } catch (...) {
             cudaStreamEndCapture(st, &graph);
             if (graph) cudaGraphDestroy(graph);
             throw;
         }
         WC_CUDA(cudaStreamEndCapture(st, &graph));
-        PassGraph pg{p, warp_trav, warp_comp, nullptr, g_launches.load() - launches0};
+        PassGraph pg{p, nullptr, g_launches.load() - launches0};
         g_launches -= pg.kernels;  // captured, not launched
         const cudaError_t e = cudaGraphInstantiate(&pg.exec, graph, 0);
         cudaGraphDestroy(graph);
@@ -2158,7 +2230,7 @@ struct DeviceEpochs {
 };
 }  // namespace
 
-void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
+void Session::enqueue_pass(int64_t p) {
     const int64_t nwords = ceil_div(vol->n_blocks, 32);
     const int32_t stamp = (int32_t)(p + 1);
     pass_no = stamp;
@@ -2217,7 +2289,7 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
     ta.work = ctl + C_WORK;
     ta.ctl = ctl;
     // C_WORK and C_NITEMS are zero here (reset, or the last pass_end)
-    launch_traverse(ta, n, nact_guess, 0, st);
+    launch_traverse(ta, n, 0, st);
     mark(1);
     // entry compaction: exclusive scan of per-ray emitted counts
     scan_exclusive_dev(LoadU32{emitted.p}, ctl + C_NACT, n, entry_off.p, ctl + C_NENT, partials.p, st);
@@ -2292,18 +2364,22 @@ void Session::enqueue_pass(int64_t p, int64_t nact_guess) {
         launch_pdl(k_rt_shade, grid_for(n, 128, WC_RTSHADE_GRID), 128, 0, st, sa);
         WC_LAUNCH_CHECK();
     } else {
+#if !WC_SPLIT_RAYTRACE
         launch_pdl(k_raytrace, grid_for(n, 128, 16), 128, 0, st, ra);
         WC_LAUNCH_CHECK();
+#endif
     }
     mark(5);
-    // composite + compaction of the surviving rays (next pass's O_Act)
-    if (speculation && n / std::max<int64_t>(1, nact_guess) >= 8)  // n_spec >= 8: a warp per ray
-        launch_pdl(k_composite_warp, grid_for(n * 32, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p,
-                                                                status.p, rgba.p, depth.p, keep.p);
-    else
-        launch_pdl(k_composite, grid_for(n, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p, status.p,
-                                                      rgba.p, depth.p, keep.p);
+    // composite + compaction of the surviving rays (next pass's O_Act); the
+    // device picks thread or warp per ray by the pass's n_spec
+    launch_pdl(k_composite, grid_for(n, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p, status.p,
+               rgba.p, depth.p, keep.p);
     WC_LAUNCH_CHECK();
+    if (speculation && max_spec >= (int)kWarpCompositeSpec) {
+        launch_pdl(k_composite_warp, grid_for(n * 32, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, rgbz.p,
+                   exited.p, status.p, rgba.p, depth.p, keep.p);
+        WC_LAUNCH_CHECK();
+    }
     // next pass's active list; the pass record and the next pass's counts
     // (pass_end) as its epilogue
     compact_dev(LoadU32{keep.p}, alist, ctl + C_NACT, n, act_list[(p + 1) & 1].p, ctl + C_NACT_NEXT, partials.p, st,
@@ -2450,7 +2526,7 @@ bool Session::pass(PassStatsC &stats) {
         n_act = h_counters.p[C_NACT];
     }
     if (n_act == 0) return false;
-    launch_pass(pass_index, n_act);
+    launch_pass(pass_index);
     WC_CUDA(cudaMemcpyAsync(h_plog.p, plog.p, 4 * L_COUNT * std::min<int64_t>(pass_index + 1, kMaxPassLog),
                             cudaMemcpyDeviceToHost, st));
     read_counters(0, C_COUNT);
@@ -2467,13 +2543,12 @@ bool Session::pass(PassStatsC &stats) {
 int64_t Session::run_frame(PassStatsC *out, int64_t max_out) {
     int64_t k = 0;
     int64_t batch = std::max<int64_t>(1, frame_passes_hint);
-    if (n_act < 0 && nact_hist[0] == 0) active_count();  // first frame: no history to guess from
     for (;;) {
         const int64_t p0 = pass_index;
         batch = p0 < kMaxPassLog ? std::min<int64_t>(batch, kMaxPassLog - p0) : 1;  // one log row per pass
-        for (int64_t b = 0; b < batch; b++) {  // active-count guesses: exact for the first, last frame's after
+        for (int64_t b = 0; b < batch; b++) {
             const int64_t p = p0 + b;
-            launch_pass(p, b == 0 && n_act >= 0 ? n_act : (p < kMaxPassLog ? nact_hist[p] : 1));
+            launch_pass(p);
             if (p == fb_snap_pass && fb_rgba) enqueue_fb_snapshot(p);
         }
         WC_CUDA(cudaMemcpyAsync(h_plog.p, plog.p, 4 * L_COUNT * std::min<int64_t>(p0 + batch, kMaxPassLog),

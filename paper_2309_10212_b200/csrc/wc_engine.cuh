@@ -106,11 +106,15 @@ struct TraverseArgs {
     uint32_t *block_slots, *ray_slots, *emitted, *vis_bm;
     uint32_t *work;        // persistent-kernel ray counter (zeroed per pass)
     const uint32_t *ctl;   // control block: n_act and n_spec of the pass (Counter)
+    // the kernel variant is chosen on the device from the pass's n_act:
+    // warp per ray when n_act <= warp_max, thread per ray otherwise (both
+    // kernels are launched; the other one returns at once)
+    uint32_t warp_max;
 };
 
-// Traversal kernel launch (k_traverse / k_traverse_warp by the active-ray
-// count guess; variant 1 / 2 forces one of them).
-void launch_traverse(const TraverseArgs &ta, int64_t n_grid, int64_t nact_guess, int variant, cudaStream_t st);
+// Traversal kernel launch: both variants, the device picks by its n_act
+// (variant 0); variant 1 / 2 forces thread-per-ray / warp-per-ray.
+void launch_traverse(TraverseArgs ta, int64_t n_grid, int variant, cudaStream_t st);
 // +octant active marking from the visible ids (engine.py:107-117)
 void launch_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvis, const uint32_t *vis_bm, int bdx, int bdy,
                         int bdz, int64_t n_max, uint32_t *act_bm, cudaStream_t st);
@@ -274,15 +278,12 @@ struct Session : CacheStore {
 
    private:
     void read_counters(int first, int count);
-    // nact_guess picks the traversal / composite kernel variants (each is
-    // exact for any count; the guess only matters for speed)
-    void enqueue_pass(int64_t p, int64_t nact_guess);
+    void enqueue_pass(int64_t p);
     void prepare_pass(int64_t p);
-    void launch_pass(int64_t p, int64_t nact_guess);  // enqueue_pass through a cached CUDA graph
+    void launch_pass(int64_t p);  // enqueue_pass through a cached CUDA graph
     void drop_graphs();
     struct PassGraph {
         int64_t p;
-        bool warp_trav, warp_comp;
         cudaGraphExec_t exec;
         long long kernels;  // kernels per replay (the launch counter)
     };

@@ -229,7 +229,7 @@ void bitmap_extract_dense(uint32_t *bm, int64_t nwords, uint32_t *word_offsets, 
 // the bitmap), clearing the summary word
 struct SinkList {
     uint32_t *summary, *list;
-    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const {
+    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix, uint32_t) const {
         uint32_t v = summary[i];
         if (v) summary[i] = 0u;
         while (v) {
@@ -250,7 +250,7 @@ struct SinkBitsIdx {
     uint32_t *word_offsets, *ids;
     int64_t id_mod;
     bool clear;
-    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const {
+    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix, uint32_t) const {
         const uint32_t w = idx[i];
         uint32_t v = bm[w];
         if (word_offsets) word_offsets[w] = prefix;

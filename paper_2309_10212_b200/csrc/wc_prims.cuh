@@ -8,6 +8,8 @@
 //                    a summary maintained by the kernels that set them)
 #pragma once
 
+#include <type_traits>
+
 #include "wc_common.cuh"
 
 namespace wc {
@@ -151,10 +153,10 @@ __device__ __forceinline__ uint32_t take_ticket(uint64_t *scratch, bool &last_ti
 // Thread 0: the epilogue runs once both the scan total is known (the last
 // tile) and every CTA has read the count (the last ticket): the second of
 // those two arrivals runs it and clears the arrival word.
-__device__ __forceinline__ bool epilogue_arrive(uint64_t *scratch, uint32_t arrivals) {
+__device__ __forceinline__ bool epilogue_arrive(uint64_t *scratch, uint32_t arrivals, uint32_t target = 2u) {
     uint32_t *c = reinterpret_cast<uint32_t *>(scratch) + 1;
     if (!arrivals) return false;
-    if (atom_add_acq_rel(c, arrivals) + arrivals != 2u) return false;
+    if (atom_add_acq_rel(c, arrivals) + arrivals != target) return false;
     *reinterpret_cast<volatile uint32_t *>(c) = 0u;
     return true;
 }
@@ -166,14 +168,15 @@ __device__ __forceinline__ void store_status(uint64_t *p, uint32_t epoch, uint32
                ((unsigned long long)epoch << 34) | ((unsigned long long)flag << 32) | v);
 }
 
+// Sinks receive (element, its exclusive prefix, its loaded value).
 struct SinkStore {  // out[i] = exclusive prefix
     uint32_t *out;
-    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const { out[i] = prefix; }
+    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix, uint32_t) const { out[i] = prefix; }
 };
 struct SinkBits {  // word offsets + ascending ids of the set bits of bm
     const uint32_t *bm;
     uint32_t *word_offsets, *ids;
-    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const {
+    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix, uint32_t) const {
         word_offsets[i] = prefix;
         uint32_t v = bm[i];
         while (v) {
@@ -183,16 +186,28 @@ struct SinkBits {  // word offsets + ascending ids of the set bits of bm
     }
 };
 
-// exclusive-scan consumer that compacts the ids whose predicate holds
+// exclusive-scan consumer that compacts the ids whose predicate (the scan's
+// 0/1 loaded value) holds
 template <class Pred>
 struct SinkCompact {
     Pred pred;
     const uint32_t *ids;
     uint32_t *out;
-    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix) const {
-        if (pred(i)) out[prefix] = ids[i];
+    __device__ __forceinline__ void operator()(int64_t i, uint32_t prefix, uint32_t v) const {
+        if (v) out[prefix] = ids[i];
     }
 };
+
+// Loaders with per-CTA state (e.g. shared-memory bins) define cta_begin()
+// (all threads, before the first load; the scan synchronises after it) and
+// cta_end() (all threads, on every exit path, after the last load).  Such a
+// loader runs only on the CTA's own tiles (no speculative load), but may be
+// called twice per element by the same thread (chunk totals, then the tile):
+// its side effects must be idempotent.
+template <class L, class = void>
+struct HasCtaHooks : std::false_type {};
+template <class L>
+struct HasCtaHooks<L, std::void_t<decltype(&L::cta_begin)>> : std::true_type {};
 
 // Decoupled look-back of tile t (called by warp 0 of its CTA): publishes the
 // tile's aggregate, sums predecessors back to the nearest published prefix,
@@ -255,11 +270,16 @@ __global__ void __launch_bounds__(kScanThreads)
                    uint32_t *d_total, Epi epi = Epi{}) {
     pdl_wait();
     __shared__ uint32_t sw[32];
-    __shared__ uint32_t tile[kScanTile];
+    __shared__ uint32_t tile[kScanTile + 1];
     __shared__ uint32_t s_excl, s_ticket, s_n, s_last_ticket;
     uint64_t *status = tile_status(scratch);
     const uint32_t epoch = resolve_epoch(ep);
+    // A loader with per-CTA state flushes it at the CTA's end, and the
+    // epilogue may read what it flushed: then every CTA arrives at its end
+    // and the last of the gridDim.x arrivals runs the epilogue.
+    constexpr bool kEndArrive = HasCtaHooks<Load>::value && !EpiTraits<Epi>::none;
     if (threadIdx.x == 0) s_n = (uint32_t)scan_count(n_max, d_n);
+    if constexpr (HasCtaHooks<Load>::value) ld.cta_begin();
     __syncthreads();  // every CTA has read the count before it takes a ticket
     const int64_t n = s_n;
     const int64_t ntiles = n > 0 ? (n - 1) / kScanTile + 1 : 1;
@@ -283,9 +303,11 @@ __global__ void __launch_bounds__(kScanThreads)
             tile[idx] = i < n ? ld(i) : 0;
         }
     };
-    const int64_t ts = blockIdx.x;
+    // (loaders with per-CTA state are not run speculatively: their side
+    // effects then happen only in the tile's owner)
+    const int64_t ts = HasCtaHooks<Load>::value ? -1 : (int64_t)blockIdx.x;
     uint32_t csum = 0;
-    if (ts <= last) {
+    if (ts >= 0 && ts <= last) {
         if (m > 1)
             csum = chunk_sum(ts);
         else
@@ -296,12 +318,20 @@ __global__ void __launch_bounds__(kScanThreads)
         s_last_ticket = lt;
         // the holder of the last ticket arrives now unless it also holds the
         // last tile (which arrives once the total is known)
-        if (!EpiTraits<Epi>::none && lt && (int64_t)tk != last && epilogue_arrive(scratch, 1u))
+        if (!kEndArrive && !EpiTraits<Epi>::none && lt && (int64_t)tk != last && epilogue_arrive(scratch, 1u))
             epi(*reinterpret_cast<volatile uint32_t *>(d_total));
     }
+    auto end_arrive = [&](bool total_known) {  // kEndArrive: after cta_end
+        if (threadIdx.x == 0 && epilogue_arrive(scratch, 1u, gridDim.x)) epi(*reinterpret_cast<volatile uint32_t *>(d_total));
+        (void)total_known;
+    };
     __syncthreads();
     const int64_t t = s_ticket;
-    if (t > last) return;
+    if (t > last) {
+        if constexpr (HasCtaHooks<Load>::value) ld.cta_end();  // the speculative loads' side effects
+        if constexpr (kEndArrive) end_arrive(false);
+        return;
+    }
     if (t != ts) {  // dispatched out of order: the data of the ticket's tile
         if (m > 1)
             csum = chunk_sum(t);
@@ -318,7 +348,8 @@ __global__ void __launch_bounds__(kScanThreads)
                 s_excl = excl;
                 if (t == last) {
                     *d_total = excl + agg;
-                    if (!EpiTraits<Epi>::none && epilogue_arrive(scratch, 1u + s_last_ticket)) epi(excl + agg);
+                    if (!kEndArrive && !EpiTraits<Epi>::none && epilogue_arrive(scratch, 1u + s_last_ticket))
+                        epi(excl + agg);
                 }
             }
         }
@@ -345,7 +376,8 @@ __global__ void __launch_bounds__(kScanThreads)
                 if (t == last) {
                     const uint32_t total = n > 0 ? excl + agg : 0u;
                     *d_total = total;
-                    if (!EpiTraits<Epi>::none && epilogue_arrive(scratch, 1u + s_last_ticket)) epi(total);
+                    if (!kEndArrive && !EpiTraits<Epi>::none && epilogue_arrive(scratch, 1u + s_last_ticket))
+                        epi(total);
                 }
             }
         }
@@ -356,16 +388,19 @@ __global__ void __launch_bounds__(kScanThreads)
             tile[threadIdx.x * kScanIPT + k] = pre;
             pre += v[k];
         }
+        if (threadIdx.x == kScanThreads - 1) tile[kScanTile] = pre;  // the tile's inclusive end
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < kScanIPT; k++) {
             const int idx = k * kScanThreads + threadIdx.x;
             const int64_t i = tb + idx;
-            if (i < n) sink(i, tile[idx]);
+            if (i < n) sink(i, tile[idx], tile[idx + 1] - tile[idx]);
         }
         running += agg;
         __syncthreads();  // tile and sw are reused by the next tile
     }
+    if constexpr (HasCtaHooks<Load>::value) ld.cta_end();
+    if constexpr (kEndArrive) end_arrive(true);
 }
 
 // Exclusive scan of ld(0..n) into out[0..n); grand total into *d_total.

@@ -176,7 +176,7 @@ void stage_traverse(const Volume *vol, const double *fine_min, const double *fin
         ta.vis_bm = vis_bm.p;
         ta.work = ctl.p + C_WORK;
         ta.ctl = ctl.p;
-        launch_traverse(ta, n_act, n_act, variant, st);
+        launch_traverse(ta, n_act, variant, st);
     }
     to_host(exited, d_ex.p, n, st);
     to_host(coarse_cell, d_cc.p, n, st);
