@@ -24,6 +24,12 @@
 #ifndef WC_TRAVERSE_MIN_CTAS
 #define WC_TRAVERSE_MIN_CTAS 5
 #endif
+// 1: one kernel with warp phases (k_rt_fused; measured slower at C3: raytrace
+// 1.15 vs 0.96 ms/frame, the solves' divergence and 96 registers); 0: the
+// work-list version below
+#ifndef WC_RT_FUSED
+#define WC_RT_FUSED 0
+#endif
 // 1: two-phase raytrace (k_rt_find / k_rt_solve / k_rt_shade); 0: fused k_raytrace.
 #ifndef WC_SPLIT_RAYTRACE
 #define WC_SPLIT_RAYTRACE 1
@@ -1509,6 +1515,111 @@ __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
     }
 }
 
+#if WC_RT_FUSED
+// ---- one-kernel raytrace with warp phases (WC_RT_FUSED): the same
+// per-entry result as k_rt_find + k_rt_solve + k_rt_shade without the global
+// work list.  A warp walks 32 entries' dual cells (lane = entry), lists the
+// bracketing cells in registers (6-bit codes, DDA order), then solves them in
+// rounds of 32 with lane = cell (the owner found by a search over the warp's
+// prefix sums, corners through the owner's row pointers); the first cell of
+// an entry with a root (blocktrace.py:420-433) shades it in place.
+#ifndef WC_RTFUSED_MIN_CTAS
+#define WC_RTFUSED_MIN_CTAS 5
+#endif
+__global__ void __launch_bounds__(128, WC_RTFUSED_MIN_CTAS) k_rt_fused(SplitArgs s) {
+    pdl_wait();
+    const RaytraceArgs &a = s.a;
+    RayView rv = a.rays;
+    rv.bind();
+    const int lane = threadIdx.x & 31;
+    __shared__ const float *rowtab[8][128];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_ent = *a.d_n_ent;
+    const double iso = a.fp[3], br = a.fp[4], bg = a.fp[5], bb = a.fp[6];
+    for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); j0 < n_ent; j0 += stride) {
+        const int64_t j = j0 + lane;
+        int found = 0;
+        unsigned long long codes = 0;
+        uint32_t ek = 0, er = 0;
+        int ebx = 0, eby = 0, ebz = 0;
+        if (j < n_ent) {
+            const EntryCtx e = entry_ctx(a, rv, j);
+            ek = e.k;
+            er = (uint32_t)e.r;
+            ebx = e.bx;
+            eby = e.by;
+            ebz = e.bz;
+            const int sl[8] = {e.field.s0, e.field.s1, e.field.s2, e.field.s3, e.field.s4, e.field.s5, e.field.s6,
+                               e.field.s7};
+            SlotFieldSmem<128>::fill(&rowtab[0][threadIdx.x], a.slot_values, sl);
+            const SlotFieldSmem<128> sf{&rowtab[0][threadIdx.x]};
+            walk_bracketing_cells(sf, 4 * e.bx, 4 * e.by, 4 * e.bz, 4 * e.bx, 4 * e.by, 4 * e.bz, e.cx, e.cy, e.cz,
+                                  e.o, e.d, e.te, iso, [&](int cx, int cy, int cz, int seq) {
+                                      const uint32_t lc = (uint32_t)((cx - 4 * e.bx) | ((cy - 4 * e.by) << 2) |
+                                                                     ((cz - 4 * e.bz) << 4));
+                                      codes |= (unsigned long long)lc << (6 * seq);
+                                      found++;
+                                  });
+        }
+        __syncwarp();  // the owners' row pointers are read across the warp below
+        uint32_t incl = (uint32_t)found;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t won = 0;  // owner lanes whose entry has its root (warp-uniform)
+        for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            int owner = 0;  // smallest lane whose inclusive prefix exceeds t
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, incl, owner + step - 1);
+                if (v <= t) owner += step;
+            }
+            const uint32_t o_incl = __shfl_sync(0xffffffffu, incl, owner);
+            const uint32_t o_found = (uint32_t)__shfl_sync(0xffffffffu, found, owner);
+            const unsigned long long o_codes = __shfl_sync(0xffffffffu, codes, owner);
+            const uint32_t o_ek = __shfl_sync(0xffffffffu, ek, owner), o_er = __shfl_sync(0xffffffffu, er, owner);
+            const int o_bx = __shfl_sync(0xffffffffu, ebx, owner), o_by = __shfl_sync(0xffffffffu, eby, owner),
+                      o_bz = __shfl_sync(0xffffffffu, ebz, owner);
+            const bool live = t < total && !((won >> owner) & 1u);
+            double th = CUDART_INF;
+            float c[8];
+            int cx = 0, cy = 0, cz = 0;
+            double o[3], d[3];
+            if (live) {
+                const uint32_t q = t - (o_incl - o_found);
+                const uint32_t lc = (uint32_t)(o_codes >> (6 * q)) & 63u;
+                const int lx = lc & 3, ly = (lc >> 2) & 3, lz = lc >> 4;
+                const SlotFieldSmem<128> of{&rowtab[0][(threadIdx.x & ~31) + owner]};
+                of.corners(lx, ly, lz, c);
+                cx = 4 * o_bx + lx;
+                cy = 4 * o_by + ly;
+                cz = 4 * o_bz + lz;
+                rv.load(o_er, o, d);
+                th = solve_cell(c, o, d, cx, cy, cz, rv.t_enter[o_er], iso);
+            }
+            // the owner's first cell (in DDA order) with a root wins: the
+            // cells of an owner are consecutive lanes in seq order
+            const uint32_t roots = __ballot_sync(0xffffffffu, th != CUDART_INF);
+            const uint32_t same = __match_any_sync(0xffffffffu, owner);
+            const uint32_t first = roots & same;
+            const bool winner = th != CUDART_INF && (first & ((1u << lane) - 1u)) == 0u;
+            if (winner) {
+                float rgb[3];
+                shade_hit(c, o, d, cx, cy, cz, th, br, bg, bb, rgb);
+                a.rgbz[o_ek] = make_float4(rgb[0], rgb[1], rgb[2], (float)th);
+            }
+            won |= __reduce_or_sync(0xffffffffu, winner ? (1u << owner) : 0u);
+        }
+        if (j < n_ent && !((won >> lane) & 1u)) a.rgbz[ek] = make_float4(0.0f, 0.0f, 0.0f, CUDART_INF_F);
+        __syncwarp();  // the row pointers are refilled by the next entries
+    }
+}
+#endif
+
 // ------------------------------------------------------------- composite
 
 // engine.py:222-258 _composite_kernel: closest speculated hit per active
@@ -2348,6 +2459,14 @@ void Session::enqueue_pass(int64_t p) {
     ra.rays = ta.rays;
     ra.fp = fparams.p;
     ra.rgbz = rgbz.p;
+#if WC_RT_FUSED
+    if (true) {
+        SplitArgs sa{};
+        sa.a = ra;
+        launch_pdl(k_rt_fused, grid_for(n, 128, WC_RTFIND_GRID), 128, 0, st, sa);
+        WC_LAUNCH_CHECK();
+    } else
+#endif
     if (WC_SPLIT_RAYTRACE) {
         SplitArgs sa{};
         sa.a = ra;
