@@ -34,6 +34,10 @@
 #ifndef WC_SPLIT_RAYTRACE
 #define WC_SPLIT_RAYTRACE 1
 #endif
+// 1: the thread-per-ray traversal queues its descents (k_traverse_q)
+#ifndef WC_TRAVERSE_Q
+#define WC_TRAVERSE_Q 0  // measured neutral at C3 (0.93 vs 0.91 ms/frame traverse): kept for comparison builds
+#endif
 // Passes with at most this many active rays use the warp-per-ray traversal.
 #ifndef WC_WARP_TRAVERSE_MAX
 #define WC_WARP_TRAVERSE_MAX 16384
@@ -603,6 +607,257 @@ __device__ __forceinline__ Dda shfl_dda(const Dda &s, int src) {
     return o;
 }
 
+// ---- traversal with deferred fine runs (k_traverse_q) ----------------------
+// The same per-ray walk as k_traverse, scheduled for SIMT efficiency.  A
+// lane walking its ray's coarse grid does not run the fine run of a coarse
+// cell whose range brackets iso right away: it queues the descent (the coarse
+// state after stepping into the cell, and the crossing that seeds the fine
+// iterator) in its own two-slot FIFO in shared memory and walks on (the
+// coarse walk never depends on the fine runs).  The warp alternates between
+// walking (lanes with room in their FIFO) and running fine runs (every lane
+// with a queued descent runs its oldest one, at most 10 steps from the cell's
+// 64-bit iso mask), so the two kinds of steps no longer share warp
+// instructions.  A run that fills the ray's n_spec slots or leaves the volume
+// ends the ray with the queued descent's coarse state; queued descents past
+// that point are dropped (the walk ran ahead); a ray whose walk left the
+// volume ends with its last run.  Every slot, iterator and exit flag is the
+// reference's, bit for bit (traversal.py:217-403).
+#ifndef WC_TQ_MINWALK
+#define WC_TQ_MINWALK 8  // below this many walking lanes, the queued runs go first
+#endif
+#ifndef WC_TQ_MINRUN
+#define WC_TQ_MINRUN 24  // runs start once this many lanes have one queued
+#endif
+#ifndef WC_TQ_MIN_CTAS
+#define WC_TQ_MIN_CTAS 5
+#endif
+#ifndef WC_TQ_DEPTH
+#define WC_TQ_DEPTH 2
+#endif
+constexpr int kTqDepth = WC_TQ_DEPTH, kTqWarps = 4;
+static_assert((kTqDepth & (kTqDepth - 1)) == 0, "FIFO depth: a power of 2");
+struct TqSlots {  // per warp, per lane: its queued descents (FIFO of kTqDepth)
+    uint32_t cxyz[kTqDepth][32];  // coarse cell coordinates, 10 bits each
+    uint32_t fcell[kTqDepth][32]; // UINT_MAX: seed from tc; else the ray's saved fine cell (resumed run)
+    double ctx[kTqDepth][32], cty[kTqDepth][32], ctz[kTqDepth][32];  // coarse tmax after stepping into it
+    double s0[kTqDepth][32], s1[kTqDepth][32], s2[kTqDepth][32];     // tc, or the saved fine tmax
+};
+
+template <int CA>
+__global__ void __launch_bounds__(128, WC_TQ_MIN_CTAS) k_traverse_q(TraverseArgs a_in) {
+    pdl_wait();
+    TraverseArgs a = a_in;
+    a.n_act = a.ctl[C_NACT];
+    if (a.n_act <= (int64_t)a.warp_max) return;  // k_traverse_warp's pass
+    a.n_spec = (int)a.ctl[C_NSPEC];
+    a.rays.bind();
+    __shared__ TqSlots slots_all[kTqWarps];
+    TqSlots &S = slots_all[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
+    bool have = false, exhausted = false, walk_done = false;
+    uint32_t i = 0, r = 0;
+    double ox = 0, oy = 0, oz = 0, dx = 0, dy = 0, dz = 0, te = 0;
+    double fdel_x = 0, fdel_y = 0, fdel_z = 0;  // coarse deltas: 4 * fdel (16/|d| == 4 * RN(4/|d|) exactly)
+    int sx = 0, sy = 0, sz = 0, emitted = 0, pending = 0, qhead = 0;
+    Dda c{0, 0, 0, 0, 0, 0};
+    double lfx = 0, lfy = 0, lfz = 0;  // fine tmax after the last run (saved if the ray ends in the walk)
+    int64_t base = 0;
+
+    auto finish = [&](bool ray_done, uint32_t c_lin, double ctx, double cty, double ctz, bool in_fine, uint32_t f_lin,
+                      double ftx, double fty, double ftz) {
+        for (int k = emitted; k < a.n_spec; k++) {  // traversal.py:423-424 sentinels
+            a.block_slots[base + k] = WC_UINT_MAX;
+            a.ray_slots[base + k] = WC_UINT_MAX;
+        }
+        a.emitted[i] = (uint32_t)emitted;
+        if (ray_done) {
+            a.exited[r] = 1;
+            a.coarse_cell[r] = WC_UINT_MAX;
+            a.fine_cell[r] = WC_UINT_MAX;
+        } else {
+            a.coarse_cell[r] = c_lin;
+            a.fine_cell[r] = in_fine ? f_lin : WC_UINT_MAX;
+        }
+        a.coarse_tmax[3 * (int64_t)r] = ctx;
+        a.coarse_tmax[3 * (int64_t)r + 1] = cty;
+        a.coarse_tmax[3 * (int64_t)r + 2] = ctz;
+        a.fine_tmax[3 * (int64_t)r] = ftx;
+        a.fine_tmax[3 * (int64_t)r + 1] = fty;
+        a.fine_tmax[3 * (int64_t)r + 2] = ftz;
+        have = false;
+        pending = 0;
+    };
+    auto push = [&](const Dda &cs, uint32_t fcell, double v0, double v1, double v2) {
+        const int q = (qhead + pending) & (kTqDepth - 1);
+        S.cxyz[q][lane] = (uint32_t)cs.cx | ((uint32_t)cs.cy << 10) | ((uint32_t)cs.cz << 20);
+        S.fcell[q][lane] = fcell;
+        S.ctx[q][lane] = cs.tx;
+        S.cty[q][lane] = cs.ty;
+        S.ctz[q][lane] = cs.tz;
+        S.s0[q][lane] = v0;
+        S.s1[q][lane] = v1;
+        S.s2[q][lane] = v2;
+        pending++;
+    };
+
+    for (;;) {
+        if (!exhausted) {  // refill idle lanes (warp-uniform branch), as k_traverse
+            const uint32_t need = __ballot_sync(0xffffffffu, !have);
+            if (need && (__popc(need) >= WC_REFILL_MIN || need == 0xffffffffu)) {
+                const int leader = __ffs(need) - 1;
+                uint32_t first = 0;
+                if (lane == leader) first = atomicAdd(a.work, (uint32_t)__popc(need));
+                first = __shfl_sync(0xffffffffu, first, leader);
+                if (first + __popc(need) >= a.n_act) exhausted = true;
+                const uint32_t mine = first + __popc(need & lt);
+                if (!have && mine < a.n_act) {
+                    have = true;
+                    walk_done = false;
+                    pending = 0;
+                    qhead = 0;
+                    i = mine;
+                    r = a.act_list[i];
+                    double o[3], d[3];
+                    a.rays.load(r, o, d);
+                    ox = o[0], oy = o[1], oz = o[2], dx = d[0], dy = d[1], dz = d[2];
+                    te = a.t_exit[r];
+                    sx = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
+                    sy = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
+                    sz = dz > 0.0 ? 1 : (dz < 0.0 ? -1 : 0);
+                    fdel_x = dx != 0.0 ? 4.0 / fabs(dx) : CUDART_INF;
+                    fdel_y = dy != 0.0 ? 4.0 / fabs(dy) : CUDART_INF;
+                    fdel_z = dz != 0.0 ? 4.0 / fabs(dz) : CUDART_INF;
+                    const uint32_t cc = a.coarse_cell[r];
+                    c.cx = (int)(cc % (uint32_t)cdx);
+                    c.cy = (int)((cc / (uint32_t)cdx) % (uint32_t)cdy);
+                    c.cz = (int)(cc / ((uint32_t)cdx * (uint32_t)cdy));
+                    c.tx = a.coarse_tmax[3 * (int64_t)r];
+                    c.ty = a.coarse_tmax[3 * (int64_t)r + 1];
+                    c.tz = a.coarse_tmax[3 * (int64_t)r + 2];
+                    lfx = a.fine_tmax[3 * (int64_t)r];
+                    lfy = a.fine_tmax[3 * (int64_t)r + 1];
+                    lfz = a.fine_tmax[3 * (int64_t)r + 2];
+                    const uint32_t fc = a.fine_cell[r];
+                    if (fc != WC_UINT_MAX) push(c, fc, lfx, lfy, lfz);  // the saved fine run goes first
+                    base = (int64_t)i * a.n_spec;
+                    emitted = 0;
+                }
+            }
+        }
+        const uint32_t walkers = __ballot_sync(0xffffffffu, have && !walk_done && pending < kTqDepth);
+        const uint32_t runners = __ballot_sync(0xffffffffu, have && pending > 0);
+        if (!walkers && !runners) {
+            if (exhausted) break;
+            continue;
+        }
+        if (walkers && (!runners || (__popc(walkers) >= WC_TQ_MINWALK && __popc(runners) < WC_TQ_MINRUN))) {
+            // ---- walk: CA coarse steps simulated, their range bits fetched together
+            if ((walkers >> lane) & 1u) {
+                Dda g = c;
+                uint32_t cell[CA];
+                int J = 0;
+                bool done = false;
+#pragma unroll
+                for (int j = 0; j < CA; j++) {
+                    if (!done) {
+                        const double t = dda_step(g, sx, sy, sz, 4.0 * fdel_x, 4.0 * fdel_y, 4.0 * fdel_z);
+                        if (t > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 ||
+                            g.cz >= cdz) {
+                            done = true;
+                        } else {
+                            cell[j] = (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz));
+                            J = j + 1;
+                        }
+                    }
+                }
+                uint32_t bits = 0;
+#pragma unroll
+                for (int j = 0; j < CA; j++)
+                    if (j < J) bits |= ((__ldg(a.coarse_bm + (cell[j] >> 5)) >> (cell[j] & 31)) & 1u) << j;
+                if (bits) {  // queue the descent at the first hit
+                    const int js = __ffs(bits) - 1;
+                    double t_cross = 0.0;
+                    for (int j = 0; j <= js; j++)
+                        t_cross = dda_step(c, sx, sy, sz, 4.0 * fdel_x, 4.0 * fdel_y, 4.0 * fdel_z);
+                    push(c, WC_UINT_MAX, t_cross, 0.0, 0.0);
+                } else {
+                    c = g;  // includes the exiting step when done (traversal.py:333-355)
+                    walk_done = done;
+                    if (done && pending == 0)  // left the volume with no run outstanding
+                        finish(true, 0u, c.tx, c.ty, c.tz, false, 0u, lfx, lfy, lfz);
+                }
+            }
+        } else if ((runners >> lane) & 1u) {
+            // ---- the oldest queued fine run of every lane that has one (traversal.py:295-331)
+            const int q = qhead;
+            const uint32_t cxyz = S.cxyz[q][lane], fc0 = S.fcell[q][lane];
+            const int ccx = (int)(cxyz & 1023u), ccy = (int)((cxyz >> 10) & 1023u), ccz = (int)(cxyz >> 20);
+            Dda f;
+            if (fc0 != WC_UINT_MAX) {  // resumed run: the saved fine iterator
+                f.cx = (int)(fc0 % (uint32_t)fdx);
+                f.cy = (int)((fc0 / (uint32_t)fdx) % (uint32_t)fdy);
+                f.cz = (int)(fc0 / ((uint32_t)fdx * (uint32_t)fdy));
+                f.tx = S.s0[q][lane];
+                f.ty = S.s1[q][lane];
+                f.tz = S.s2[q][lane];
+            } else {  // traversal.py:357-386: seed where the ray entered the coarse cell
+                const double t_cross = S.s0[q][lane];
+                const double px = ox + dx * t_cross, py = oy + dy * t_cross, pz = oz + dz * t_cross;
+                const int lo_x = 4 * ccx, lo_y = 4 * ccy, lo_z = 4 * ccz;
+                const int hi_x = min(lo_x + 3, fdx - 1), hi_y = min(lo_y + 3, fdy - 1), hi_z = min(lo_z + 3, fdz - 1);
+                f.cx = (int)floor(px / 4.0);
+                f.cy = (int)floor(py / 4.0);
+                f.cz = (int)floor(pz / 4.0);
+                f.cx = f.cx < lo_x ? lo_x : (f.cx > hi_x ? hi_x : f.cx);
+                f.cy = f.cy < lo_y ? lo_y : (f.cy > hi_y ? hi_y : f.cy);
+                f.cz = f.cz < lo_z ? lo_z : (f.cz > hi_z ? hi_z : f.cz);
+                f.tx = dx > 0.0 ? ((double)(f.cx + 1) * 4.0 - ox) / dx
+                                : (dx < 0.0 ? ((double)f.cx * 4.0 - ox) / dx : CUDART_INF);
+                f.ty = dy > 0.0 ? ((double)(f.cy + 1) * 4.0 - oy) / dy
+                                : (dy < 0.0 ? ((double)f.cy * 4.0 - oy) / dy : CUDART_INF);
+                f.tz = dz > 0.0 ? ((double)(f.cz + 1) * 4.0 - oz) / dz
+                                : (dz < 0.0 ? ((double)f.cz * 4.0 - oz) / dz : CUDART_INF);
+            }
+            const unsigned long long fm = __ldg(a.cell_mask + (ccx + cdx * (ccy + cdy * ccz)));
+            bool ray_done = false, in_run = true;
+            for (int k = 0; k < kFineRun; k++) {
+                if ((fm >> fine_local(f)) & 1ull) {
+                    const uint32_t f_lin = (uint32_t)(f.cx + fdx * (f.cy + fdy * f.cz));
+                    a.block_slots[base + emitted] = f_lin;
+                    a.ray_slots[base + emitted] = r;
+                    emitted++;
+                    mark_visible(a.vis_bm, f_lin);
+                }
+                const double t = dda_step(f, sx, sy, sz, fdel_x, fdel_y, fdel_z);
+                if (t > te || f.cx < 0 || f.cx >= fdx || f.cy < 0 || f.cy >= fdy || f.cz < 0 || f.cz >= fdz) {
+                    in_run = false;
+                    ray_done = true;
+                    break;
+                }
+                if ((f.cx >> 2) != ccx || (f.cy >> 2) != ccy || (f.cz >> 2) != ccz) {
+                    in_run = false;
+                    break;
+                }
+                if (emitted == a.n_spec) break;
+            }
+            if (emitted == a.n_spec || ray_done) {  // the ray's pass ends in this run
+                finish(ray_done, (uint32_t)(ccx + cdx * (ccy + cdy * ccz)), S.ctx[q][lane], S.cty[q][lane],
+                       S.ctz[q][lane], in_run, (uint32_t)(f.cx + fdx * (f.cy + fdy * f.cz)), f.tx, f.ty, f.tz);
+            } else {  // left the coarse cell: on to the next queued run or the walk
+                lfx = f.tx;
+                lfy = f.ty;
+                lfz = f.tz;
+                qhead = (qhead + 1) & (kTqDepth - 1);
+                pending--;
+                if (pending == 0 && walk_done)  // the walk had left the volume after this run
+                    finish(true, 0u, c.tx, c.ty, c.tz, false, 0u, lfx, lfy, lfz);
+            }
+        }
+    }
+}
+
 // traversal.py:217-403 for passes with few active rays (the long rays of the
 // last passes, where one ray's serial DDA is the critical path): one warp
 // per ray.  The DDA never depends on grid values, so lane k simulates the
@@ -944,7 +1199,10 @@ __global__ void k_mark_active_words(const uint32_t *visible_ids, const uint32_t 
 void launch_traverse(TraverseArgs ta, int64_t n_grid, int variant, cudaStream_t st) {
     ta.warp_max = variant == 1 ? 0u : (variant == 2 ? 0xFFFFFFFFu : (uint32_t)WC_WARP_TRAVERSE_MAX);
     if (variant != 2) {  // many rays: thread per ray, persistent
-        launch_pdl(k_traverse<WC_COARSE_AHEAD>, grid_for(n_grid, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st, ta);
+        if (WC_TRAVERSE_Q)
+            launch_pdl(k_traverse_q<WC_COARSE_AHEAD>, grid_for(n_grid, 128, WC_TQ_MIN_CTAS), 128, 0, st, ta);
+        else
+            launch_pdl(k_traverse<WC_COARSE_AHEAD>, grid_for(n_grid, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st, ta);
         WC_LAUNCH_CHECK();
     }
     if (variant != 1) {  // few (long) rays: warp-cooperative DDA per ray
