@@ -74,6 +74,7 @@ def parse():
     p.add_argument("--isovalues", type=int, default=9, help="c5: random isovalues (cli.py bench protocol)")
     p.add_argument("--orbit-steps", type=int, default=10, help="c5: cameras per isovalue")
     p.add_argument("--seed", type=int, default=0, help="c5: isovalue seed")
+    p.add_argument("--dump-kernels", action="store_true", help="add every (pass, kernel) device time to the line")
     return p.parse_args()
 
 
@@ -200,8 +201,8 @@ def stage_bytes(stage, stats, n_rays, stride):
         return 500 * V + 80 * E
     if stage == "cache_decode":  # compressed record read + f32[64] slot write per decoded block
         return (stride + 256) * D
-    if stage == "group":         # sort keys/values read+write per entry (one digit pass)
-        return 16 * E
+    if stage == "rt_inputs":     # entries: slot 4 + prefix 4 read, key/val/ray/block 16 written; contributor rows
+        return 24 * E
     if stage == "composite":     # slot id 4 + prefix 4 + z 4 per entry; winner rgbz 16 + fb 8 + status 1
         return 12 * E + 25 * A
     if stage == "mark":
@@ -481,7 +482,7 @@ def run_b200(args):
                      "stage_frac": round(achieved / pk["hbm_gbs"], 5),
                      "frame_algorithmic_bytes": int(fbytes),
                      "frame_frac": round(fbytes / (ms_per_frame * 1e-3) / 1e9 / pk["hbm_gbs"], 5)},
-        "kernels": ktab[:16],
+        "kernels": ktab[:24],
         "decode": {"gbs": dec["gbs"], "frac": dec["frac"], "ms_per_frame": dec["ms_per_frame"],
                    "blocks_per_frame": sum(s.new_decompressed for s in stats)} if dec else None,
         "compaction": {"kernel": comp["kernel"], "gbs": comp["gbs"], "frac": comp["frac"],
@@ -495,6 +496,8 @@ def run_b200(args):
         "clocks": clocks,
         "setup_s": round(setup_s, 2),
     }
+    if args.dump_kernels:
+        line["kernel_profile_rows"] = [dict(r, ms=round(r["ms"] / args.steps, 5)) for r in kprof]
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"], line["parity"] = cpu_baseline(args, wl, cv, iso, fb, stats, c_stats, cache)
     emit(line)

@@ -195,7 +195,8 @@ int wc_session_reset(wc_session *s, const wc_camera *cam, double iso);
  * create/reset to the end of the last pass. */
 int wc_session_frame_ms(wc_session *s, double *ms);
 /* Accumulated device ms per stage since the last reset, then the reset itself:
- * [traverse, mark+extract, cache+decode, group(sort), raytrace, composite, reset] (7 doubles) */
+ * [traverse, mark+extract, cache+decode, raytrace inputs (+ grouping sort), raytrace, composite, reset]
+ * (7 doubles) */
 int wc_session_stage_ms(const wc_session *s, double *ms6);
 /* The same split for one pass (pass_index < 128) of the current frame. */
 int wc_session_pass_stage_ms(const wc_session *s, int64_t pass_index, double *ms6);

@@ -372,13 +372,7 @@ __device__ __forceinline__ int pick3(int ax, int a, int b, int c) { return ax ==
 // Every emitted slot, saved iterator and exit flag is the reference's, bit
 // for bit.
 template <int CA>
-__global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(TraverseArgs a_in) {
-    pdl_wait();
-    TraverseArgs a = a_in;
-    a.n_act = a.ctl[C_NACT];
-    if (a.n_act <= (int64_t)a.warp_max) return;  // k_traverse_warp's pass
-    a.n_spec = (int)a.ctl[C_NSPEC];
-    a.rays.bind();
+__device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
@@ -867,13 +861,7 @@ __global__ void __launch_bounds__(128, WC_TQ_MIN_CTAS) k_traverse_q(TraverseArgs
 // which cells emit, where the n_spec-th emit or the descent happens, and
 // where the ray leaves.  The lane that simulated exactly that many steps
 // holds the reference's iterator state and shuffles it to the warp.
-__global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a_in) {
-    pdl_wait();
-    TraverseArgs a = a_in;
-    a.n_act = a.ctl[C_NACT];
-    if (a.n_act > (int64_t)a.warp_max) return;  // k_traverse's pass
-    a.n_spec = (int)a.ctl[C_NSPEC];
-    a.rays.bind();
+__device__ __forceinline__ void traverse_rays_warp(TraverseArgs a) {
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
@@ -1056,6 +1044,24 @@ __global__ void __launch_bounds__(128) k_traverse_warp(TraverseArgs a_in) {
     }
 }
 
+// One launch per pass: thread per ray (persistent, refilled from a work
+// counter) when the pass has many rays, warp per ray when it has at most
+// warp_max -- chosen on the device from the pass's n_act, so a captured pass
+// graph fits any frame.
+template <int CA>
+__global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(TraverseArgs a_in) {
+    pdl_wait();
+    TraverseArgs a = a_in;
+    a.n_act = a.ctl[C_NACT];
+    a.n_spec = (int)a.ctl[C_NSPEC];
+    a.rays.bind();
+    if (a.n_act > (int64_t)a.warp_max) {
+        if (!a.warp_only) traverse_rays_thread<CA>(a);
+    } else {
+        traverse_rays_warp(a);
+    }
+}
+
 // The traversal's range tests for one isovalue, precomputed: bit c of the
 // fine (coarse) bitmap is `min[c] <= iso && iso <= max[c]` evaluated in
 // float64 exactly as traversal.py:297 (:357) does.  The 15.7 MB fine bitmap
@@ -1198,18 +1204,20 @@ __global__ void k_mark_active_words(const uint32_t *visible_ids, const uint32_t 
 
 void launch_traverse(TraverseArgs ta, int64_t n_grid, int variant, cudaStream_t st) {
     ta.warp_max = variant == 1 ? 0u : (variant == 2 ? 0xFFFFFFFFu : (uint32_t)WC_WARP_TRAVERSE_MAX);
-    if (variant != 2) {  // many rays: thread per ray, persistent
-        if (WC_TRAVERSE_Q)
-            launch_pdl(k_traverse_q<WC_COARSE_AHEAD>, grid_for(n_grid, 128, WC_TQ_MIN_CTAS), 128, 0, st, ta);
-        else
-            launch_pdl(k_traverse<WC_COARSE_AHEAD>, grid_for(n_grid, 128, WC_TRAVERSE_MIN_CTAS), 128, 0, st, ta);
+#if WC_TRAVERSE_Q
+    if (variant != 2) {
+        launch_pdl(k_traverse_q<WC_COARSE_AHEAD>, grid_for(n_grid, 128, WC_TQ_MIN_CTAS), 128, 0, st, ta);
         WC_LAUNCH_CHECK();
     }
-    if (variant != 1) {  // few (long) rays: warp-cooperative DDA per ray
-        const int64_t most = variant == 2 ? n_grid : std::min<int64_t>(n_grid, WC_WARP_TRAVERSE_MAX);
-        launch_pdl(k_traverse_warp, grid_for(std::max<int64_t>(1, most) * 32, 128, 16), 128, 0, st, ta);
-        WC_LAUNCH_CHECK();
-    }
+    if (variant == 1) return;
+    ta.warp_only = true;
+#endif
+    // enough CTAs for a warp per ray up to warp_max rays; the thread-per-ray
+    // path keeps what fits resident busy and the rest find no work
+    const int64_t warps = std::min<int64_t>(n_grid, variant == 1 ? 0 : (variant == 2 ? n_grid : WC_WARP_TRAVERSE_MAX));
+    const unsigned grid = std::max(grid_for(n_grid, 128, WC_TRAVERSE_MIN_CTAS), grid_for(std::max<int64_t>(1, warps) * 32, 128, 16));
+    launch_pdl(k_traverse<WC_COARSE_AHEAD>, grid, 128, 0, st, ta);
+    WC_LAUNCH_CHECK();
 }
 
 void launch_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvis, const uint32_t *vis_bm, int bdx, int bdy,
@@ -1226,31 +1234,6 @@ void launch_iso_bitmap(const double2 *mm, int64_t n, double iso, uint32_t *bm, c
     const int64_t nw = ceil_div(n, 32);
     launch_pdl(k_iso_bitmap, grid_for(nw * 32, 256, 8), 256, 0, st, mm, n, iso, bm, (int64_t)0, nw);
     WC_LAUNCH_CHECK();
-}
-
-// Entries of active ray i: k = entry_off[i] + j for its j-th emitted slot
-// (== valid_prefix of the slot, engine.py:124-128).  Key = rank of the block
-// among visible ids (bitmap rank), value = k.
-__global__ void k_build_entries(const uint32_t *ctl, const uint32_t *act_list, const uint32_t *emitted,
-                                const uint32_t *entry_off, const uint32_t *block_slots, const uint32_t *vis_bm,
-                                const uint32_t *vis_word_off, uint32_t *ent_key, uint32_t *ent_val, uint32_t *ent_ray,
-                                uint32_t *ent_blk) {
-    pdl_wait();
-    // thread per slot (i, j): no per-ray serial chain of rank lookups
-    const int64_t n_act = ctl[C_NACT], n_spec = ctl[C_NSPEC];
-    const int64_t n_slots = n_act * n_spec;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_slots; t += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t i = (uint32_t)t / (uint32_t)n_spec;  // slots <= rays < 2^32
-        const uint32_t j = (uint32_t)t - i * (uint32_t)n_spec;
-        if (j >= emitted[i]) continue;
-        const uint32_t eo = entry_off[i] + j;
-        const uint32_t b = block_slots[t];
-        const uint32_t w = b >> 5;
-        ent_key[eo] = vis_word_off[w] + __popc(vis_bm[w] & ((1u << (b & 31)) - 1u));
-        ent_val[eo] = eo;
-        ent_ray[eo] = act_list[i];
-        ent_blk[eo] = b;
-    }
 }
 
 // Run starts of the sorted keys -> block_ray_offsets (engine.py:133-139).
@@ -1482,13 +1465,10 @@ struct DenseFieldView {  // fully decoded volume, x-fastest
 // and its 7 +octant neighbours (-1 outside the volume), 32 B per block.
 // Also clears the visibility bitmap for the next pass (its ranks were last
 // read by k_build_entries): every visible id zeroes its word.
-__global__ void k_contrib(const uint32_t *visible_ids, const uint32_t *d_nvis, const int32_t *slot_of_block, int bdx,
-                          int bdy, int bdz, int4 *contrib, uint32_t *err, uint32_t *vis_bm) {
-    pdl_wait();
-    const int64_t nvis = *d_nvis;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvis; v += (int64_t)gridDim.x * blockDim.x) {
+__device__ __forceinline__ void contrib_row(int64_t v, const uint32_t *visible_ids, const int32_t *slot_of_block,
+                                            int bdx, int bdy, int bdz, int4 *contrib, uint32_t *err) {
+    {
         const uint32_t b = visible_ids[v];
-        vis_bm[b >> 5] = 0u;
         const int bx = (int)(b % (uint32_t)bdx), by = (int)((b / (uint32_t)bdx) % (uint32_t)bdy),
                   bz = (int)(b / ((uint32_t)bdx * (uint32_t)bdy));
         int s[8];
@@ -1505,8 +1485,51 @@ __global__ void k_contrib(const uint32_t *visible_ids, const uint32_t *d_nvis, c
     }
 }
 
+// The raytrace's inputs in one launch, after the cache update: the entries
+// (k_build_entries' work, a thread per ray slot) and the contributor rows (a
+// thread per visible block).  The visibility bitmap the entries rank against
+// is cleared later, by k_rt_find.
+struct BuildEntriesArgs {
+    const uint32_t *ctl, *act_list, *emitted, *entry_off, *block_slots, *vis_bm, *vis_word_off;
+    uint32_t *ent_key, *ent_val, *ent_ray, *ent_blk;
+};
+__global__ void k_rt_prep(BuildEntriesArgs be, const uint32_t *visible_ids, const uint32_t *d_nvis,
+                          const int32_t *slot_of_block, int bdx, int bdy, int bdz, int4 *contrib, uint32_t *err) {
+    pdl_wait();
+    const int64_t n_act = be.ctl[C_NACT], n_spec = be.ctl[C_NSPEC];
+    const int64_t n_slots = n_act * n_spec, nvis = *d_nvis;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_slots + nvis;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        if (t >= n_slots) {
+            contrib_row(t - n_slots, visible_ids, slot_of_block, bdx, bdy, bdz, contrib, err);
+            continue;
+        }
+        const uint32_t i = (uint32_t)t / (uint32_t)n_spec;  // slots <= rays < 2^32
+        const uint32_t j = (uint32_t)t - i * (uint32_t)n_spec;
+        if (j >= be.emitted[i]) continue;
+        const uint32_t eo = be.entry_off[i] + j;
+        const uint32_t b = be.block_slots[t];
+        const uint32_t w = b >> 5;
+        be.ent_key[eo] = be.vis_word_off[w] + __popc(be.vis_bm[w] & ((1u << (b & 31)) - 1u));
+        be.ent_val[eo] = eo;
+        be.ent_ray[eo] = be.act_list[i];
+        be.ent_blk[eo] = b;
+    }
+}
+
+// every visible id zeroes its word of the visibility bitmap (its ranks were
+// read by k_rt_prep), ready for the next pass's traversal
+__device__ __forceinline__ void clear_visible_words(const uint32_t *visible_ids, const uint32_t *d_nvis,
+                                                    uint32_t *vis_bm) {
+    const int64_t nvis = *d_nvis;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvis; v += (int64_t)gridDim.x * blockDim.x)
+        vis_bm[visible_ids[v] >> 5] = 0u;
+}
+
 struct RaytraceArgs {
     const uint32_t *visible_ids, *ent_key, *ent_val, *ent_ray, *ent_blk;
+    uint32_t *vis_bm;         // cleared by k_rt_find (clear_visible_words)
+    const uint32_t *d_nvis;
     bool identity;  // entries in their build order (not grouped): entry k at position k
     int64_t n_ent;
     const int4 *contrib;
@@ -1526,6 +1549,7 @@ struct RaytraceArgs {
 // writes (rgb, z) -- or (0, 0, 0, +inf) on a miss -- at its entry id.
 __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_raytrace(RaytraceArgs a) {
     pdl_wait();
+    clear_visible_words(a.visible_ids, a.d_nvis, a.vis_bm);
     a.rays.bind();
     const int64_t n_ent = *a.d_n_ent;
     const double iso = a.fp[3], br = a.fp[4], bg = a.fp[5], bb = a.fp[6];
@@ -1603,6 +1627,7 @@ __device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, const RayVi
 __global__ void __launch_bounds__(128, WC_RTFIND_MIN_CTAS) k_rt_find(SplitArgs s) {
     pdl_wait();
     const RaytraceArgs &a = s.a;
+    clear_visible_words(a.visible_ids, a.d_nvis, a.vis_bm);
     RayView rv = a.rays;
     rv.bind();
     const int lane = threadIdx.x & 31;
@@ -1787,6 +1812,7 @@ __global__ void __launch_bounds__(128) k_rt_shade(SplitArgs s) {
 __global__ void __launch_bounds__(128, WC_RTFUSED_MIN_CTAS) k_rt_fused(SplitArgs s) {
     pdl_wait();
     const RaytraceArgs &a = s.a;
+    clear_visible_words(a.visible_ids, a.d_nvis, a.vis_bm);
     RayView rv = a.rays;
     rv.bind();
     const int lane = threadIdx.x & 31;
@@ -1884,46 +1910,50 @@ __global__ void __launch_bounds__(128, WC_RTFUSED_MIN_CTAS) k_rt_fused(SplitArgs
 // ray (strict <, earliest entry wins ties), then terminate or keep.
 constexpr uint32_t kWarpCompositeSpec = 8;  // n_spec from which a warp composites one ray
 
+// engine.py:222-258 for active ray i: the closest speculated hit (strict <,
+// earliest entry wins ties), then terminate (hit / exited) or keep.
+__device__ __forceinline__ void composite_ray(int64_t i, uint32_t r, float best, int64_t bk, const float4 *rgbz,
+                                              const uint8_t *exited, uint8_t *status, uint32_t *rgba, float *depth,
+                                              uint32_t *keep) {
+    uint32_t kp = 0;
+    if (bk >= 0) {
+        const float4 c = rgbz[bk];
+        depth[r] = best;
+        rgba[r] = rgb_u8((double)c.x) | (rgb_u8((double)c.y) << 8) | (rgb_u8((double)c.z) << 16) | 0xFF000000u;
+        status[r] = 1;
+    } else if (exited[r] == 1) {
+        status[r] = 2;
+    } else {
+        kp = 1;
+    }
+    keep[i] = kp;
+}
+
+// Thread per ray, or (n_spec >= kWarpCompositeSpec, read on the device) a
+// warp per ray: the lexicographic (depth, entry) minimum over the lanes is
+// the first strict minimum in order.
 __global__ void k_composite(const uint32_t *ctl, const uint32_t *act_list, const uint32_t *emitted,
                             const uint32_t *entry_off, const float4 *rgbz, const uint8_t *exited, uint8_t *status,
                             uint32_t *rgba, float *depth, uint32_t *keep) {
     pdl_wait();
-    if (ctl[C_NSPEC] >= kWarpCompositeSpec) return;  // k_composite_warp's pass
     const int64_t n_act = ctl[C_NACT];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_act; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t r = act_list[i], ne = emitted[i], eo = entry_off[i];
-        float best = CUDART_INF_F;
-        int64_t bk = -1;
-        for (uint32_t j = 0; j < ne; j++) {
-            const float z = rgbz[eo + j].w;
-            if (z < best) {
-                best = z;
-                bk = eo + j;
+    if (ctl[C_NSPEC] < kWarpCompositeSpec) {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_act;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const uint32_t r = act_list[i], ne = emitted[i], eo = entry_off[i];
+            float best = CUDART_INF_F;
+            int64_t bk = -1;
+            for (uint32_t j = 0; j < ne; j++) {
+                const float z = rgbz[eo + j].w;
+                if (z < best) {
+                    best = z;
+                    bk = eo + j;
+                }
             }
+            composite_ray(i, r, best, bk, rgbz, exited, status, rgba, depth, keep);
         }
-        uint32_t kp = 0;
-        if (bk >= 0) {
-            const float4 c = rgbz[bk];
-            depth[r] = best;
-            rgba[r] = rgb_u8((double)c.x) | (rgb_u8((double)c.y) << 8) | (rgb_u8((double)c.z) << 16) | 0xFF000000u;
-            status[r] = 1;
-        } else if (exited[r] == 1) {
-            status[r] = 2;
-        } else {
-            kp = 1;
-        }
-        keep[i] = kp;
+        return;
     }
-}
-
-// Same with a warp per ray, for speculative passes (n_spec entries per ray):
-// lexicographic (depth, entry) minimum == the first strict minimum in order.
-__global__ void k_composite_warp(const uint32_t *ctl, const uint32_t *act_list, const uint32_t *emitted,
-                                 const uint32_t *entry_off, const float4 *rgbz, const uint8_t *exited, uint8_t *status,
-                                 uint32_t *rgba, float *depth, uint32_t *keep) {
-    pdl_wait();
-    if (ctl[C_NSPEC] < kWarpCompositeSpec) return;  // k_composite's pass
-    const int64_t n_act = ctl[C_NACT];
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1947,20 +1977,8 @@ __global__ void k_composite_warp(const uint32_t *ctl, const uint32_t *act_list, 
                 bj = jb;
             }
         }
-        if (lane == 0) {
-            uint32_t kp = 0;
-            if (bj != 0xFFFFFFFFu) {
-                const float4 c = rgbz[eo + bj];
-                depth[r] = best;
-                rgba[r] = rgb_u8((double)c.x) | (rgb_u8((double)c.y) << 8) | (rgb_u8((double)c.z) << 16) | 0xFF000000u;
-                status[r] = 1;
-            } else if (exited[r] == 1) {
-                status[r] = 2;
-            } else {
-                kp = 1;
-            }
-            keep[i] = kp;
-        }
+        if (lane == 0) composite_ray(i, r, best, bj != 0xFFFFFFFFu ? (int64_t)eo + bj : -1, rgbz, exited, status, rgba,
+                                     depth, keep);
     }
 }
 
@@ -2089,6 +2107,9 @@ __device__ __forceinline__ void cache_plan(uint32_t *ctl, uint32_t *hist, int32_
     }
     ctl[C_NEVICT] = (uint32_t)n_evict;
     ctl[C_LSTAR] = lstar;
+    // the victims' regions are stamps 0..L*: their summary words are the
+    // only ones k_mark_victims can set
+    ctl[C_VSUM] = n_evict ? (uint32_t)(((int64_t)lstar + 1) * ceil_div(n_blocks, 32) / 32 + 1) : 0u;
     if (maintain) {  // the victims leave their bins (in (last_used, id) order), the misses enter bin pass_no
         int64_t left = n_evict;
         for (int L = 0; L < pass_no && left > 0; L++) {
@@ -2508,7 +2529,8 @@ void CacheStore::enqueue_insert(uint32_t *ctl, int64_t nmax, int32_t stamp, cons
                    nwords, vict_bm.p, vict_sum.p);
         WC_LAUNCH_CHECK();
         bitmap_extract_listed(vict_bm.p, vict_sum.p, (int64_t)stamp * nwords, slot_alloc, nwords, nullptr, cand_key.p,
-                              ctl + C_NCAND, true, word_list.p, ctl + C_NLIST, partials, st);  // clears the regions
+                              ctl + C_NCAND, true, word_list.p, ctl + C_NLIST, partials, st,
+                              ctl + C_VSUM);  // clears the regions
         launch_pdl(k_evict, grid_for(slot_alloc, 256), 256, 0, st, cand_key.p, ctl + C_NEVICT, slot_of_block.p,
                    block_of_slot.p, cand_val.p);
         WC_LAUNCH_CHECK();
@@ -2667,10 +2689,6 @@ void Session::enqueue_pass(int64_t p) {
     bitmap_extract_dense(vis_bm.p, nwords, vis_word_off.p, visible_ids.p, ctl + C_NVIS, false, partials.p, st);
     launch_mark_active(visible_ids.p, ctl + C_NVIS, vis_bm.p, vol->bdx, vol->bdy, vol->bdz, n, act_bm.p, st);
     bitmap_extract_dense(act_bm.p, nwords, nullptr, active_ids.p, ctl + C_NACTB, true, partials.p, st);  // clears act_bm
-    launch_pdl(k_build_entries, grid_for(n, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p,
-                                                      vis_word_off.p, ent_key.p, ent_val.p, ent_ray.p, ent_blk.p);
-    WC_LAUNCH_CHECK();  // vis_bm is cleared by k_contrib
-
     // cache.ensure_resident (cache.py:66-111), sized on the device
     const int64_t nmax = active_ids.n - 1;  // upper bound of the active-block count
     enqueue_lookup(ctl, active_ids.p, nmax, stamp, vol->n_blocks, partials.p, st);
@@ -2683,6 +2701,12 @@ void Session::enqueue_pass(int64_t p) {
     if (corrupt) WC_CUDA(cudaMemsetAsync(slot_values.p, 0, 4 * 64 * slot_alloc, st));  // engine.py:338-339
     mark(3);
 
+    // the raytrace's inputs: entries (keyed by visible rank) and contributor rows
+    const BuildEntriesArgs be{ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p, vis_word_off.p,
+                              ent_key.p, ent_val.p, ent_ray.p, ent_blk.p};
+    launch_pdl(k_rt_prep, grid_for(2 * n, 256), 256, 0, st, be, visible_ids.p, ctl + C_NVIS, slot_of_block.p, vol->bdx,
+               vol->bdy, vol->bdz, contrib.p, ctl + C_ERR);
+    WC_LAUNCH_CHECK();
     // build_rt_inputs grouping (debug views only: the raytrace is correct on
     // ray order; the radix sort needs the entry and visible counts on the host)
     if (group_entries) {
@@ -2695,11 +2719,10 @@ void Session::enqueue_pass(int64_t p) {
         }
     }
     mark(4);
-    launch_pdl(k_contrib, grid_for(n, 256), 256, 0, st, visible_ids.p, ctl + C_NVIS, slot_of_block.p, vol->bdx, vol->bdy,
-                                                vol->bdz, contrib.p, ctl + C_ERR, vis_bm.p);
-    WC_LAUNCH_CHECK();
     RaytraceArgs ra{};
     ra.visible_ids = visible_ids.p;
+    ra.vis_bm = vis_bm.p;
+    ra.d_nvis = ctl + C_NVIS;
     ra.ent_key = ent_key.p;
     ra.ent_val = ent_val.p;
     ra.ent_ray = ent_ray.p;
@@ -2749,14 +2772,9 @@ void Session::enqueue_pass(int64_t p) {
     mark(5);
     // composite + compaction of the surviving rays (next pass's O_Act); the
     // device picks thread or warp per ray by the pass's n_spec
-    launch_pdl(k_composite, grid_for(n, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p, status.p,
-               rgba.p, depth.p, keep.p);
+    launch_pdl(k_composite, grid_for((speculation && max_spec >= (int)kWarpCompositeSpec ? 32 : 1) * n, 256), 256, 0, st,
+               ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p, status.p, rgba.p, depth.p, keep.p);
     WC_LAUNCH_CHECK();
-    if (speculation && max_spec >= (int)kWarpCompositeSpec) {
-        launch_pdl(k_composite_warp, grid_for(n * 32, 256), 256, 0, st, ctl, alist, emitted.p, entry_off.p, rgbz.p,
-                   exited.p, status.p, rgba.p, depth.p, keep.p);
-        WC_LAUNCH_CHECK();
-    }
     // next pass's active list; the pass record and the next pass's counts
     // (pass_end) as its epilogue
     compact_dev(LoadU32{keep.p}, alist, ctl + C_NACT, n, act_list[(p + 1) & 1].p, ctl + C_NACT_NEXT, partials.p, st,

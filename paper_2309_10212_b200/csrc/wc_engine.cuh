@@ -52,6 +52,7 @@ enum Counter : int {
     C_NSNAP,      // rays still active when the framebuffer read-back started
     C_NLIST,      // non-zero bitmap words listed by bitmap_extract_listed
     C_FRAME,      // frame counter (device-derived scan epochs)
+    C_VSUM,       // victim-region summary words to list this pass (0: no eviction)
     C_COUNT
 };
 
@@ -110,6 +111,7 @@ struct TraverseArgs {
     // warp per ray when n_act <= warp_max, thread per ray otherwise (both
     // kernels are launched; the other one returns at once)
     uint32_t warp_max;
+    bool warp_only;  // passes with more rays are another kernel's (k_traverse_q builds)
 };
 
 // Traversal kernel launch: both variants, the device picks by its n_act
@@ -209,7 +211,7 @@ struct Session : CacheStore {
     cudaEvent_t ev_frame0 = nullptr, ev_reset_end = nullptr;
     cudaStream_t st_side = nullptr;  // reset: per-iso range tests overlapped with the ray setup
     cudaEvent_t ev_side = nullptr;
-    static constexpr int kStages = 6;  // traverse, mark, cache, group, raytrace, composite
+    static constexpr int kStages = 6;  // traverse, mark, cache, raytrace inputs (+ grouping), raytrace, composite
     double stage_ms[kStages] = {};
     static constexpr int kMaxPassLog = 128;
     double pass_stage_ms[kMaxPassLog][kStages] = {};  // per-pass stage device ms since reset

@@ -265,7 +265,7 @@ struct SinkBitsIdx {
 
 void bitmap_extract_listed(uint32_t *bm, uint32_t *summary, int64_t nwords_max, int64_t nlist_max, int64_t id_mod,
                            uint32_t *word_offsets, uint32_t *ids, uint32_t *d_count, bool clear, uint32_t *word_list,
-                           uint32_t *d_nlist, uint32_t *partials, cudaStream_t st) {
+                           uint32_t *d_nlist, uint32_t *partials, cudaStream_t st, const uint32_t *d_nsummary) {
     const int64_t ns = ceil_div(nwords_max, 32);
     nlist_max = std::min(nlist_max, nwords_max);
     if (ns <= 0 || nlist_max <= 0) {
@@ -273,7 +273,7 @@ void bitmap_extract_listed(uint32_t *bm, uint32_t *summary, int64_t nwords_max, 
         return;
     }
     launch_pdl(k_scan_onepass<LoadPopc, SinkList>, scan_grid(ns), kScanThreads, 0, st, 
-        LoadPopc{summary}, SinkList{summary, word_list}, ns, nullptr, reinterpret_cast<uint64_t *>(partials),
+        LoadPopc{summary}, SinkList{summary, word_list}, ns, d_nsummary, reinterpret_cast<uint64_t *>(partials),
         scan_epoch(), d_nlist, NoEpilogue{});
     WC_LAUNCH_CHECK();
     launch_pdl(k_scan_onepass<LoadPopcIdx, SinkBitsIdx>, scan_grid(nlist_max), kScanThreads, 0, st, 

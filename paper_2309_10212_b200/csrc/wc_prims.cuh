@@ -499,6 +499,7 @@ void bitmap_extract_dense(uint32_t *bm, int64_t nwords, uint32_t *word_offsets, 
 // words, partials >= scan_scratch_words(max(nlist_max, summary words)).
 void bitmap_extract_listed(uint32_t *bm, uint32_t *summary, int64_t nwords_max, int64_t nlist_max, int64_t id_mod,
                            uint32_t *word_offsets, uint32_t *ids, uint32_t *d_count, bool clear, uint32_t *word_list,
-                           uint32_t *d_nlist, uint32_t *partials, cudaStream_t st);
+                           uint32_t *d_nlist, uint32_t *partials, cudaStream_t st,
+                           const uint32_t *d_nsummary = nullptr);  // summary words to scan, on the device (<= bound)
 
 }  // namespace wc

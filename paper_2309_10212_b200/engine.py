@@ -24,7 +24,7 @@ from .grids import MacrocellGrids
 from .traversal import Camera
 
 BACKGROUND_RGBA = (0, 0, 0, 255)
-STAGES = ("traverse", "mark", "cache_decode", "group", "raytrace", "composite")
+STAGES = ("traverse", "mark", "cache_decode", "rt_inputs", "raytrace", "composite")
 MAX_SPEC_DEFAULT = 64
 AMBIENT = 0.2
 BASE_COLOR = (0.85, 0.85, 0.85)
