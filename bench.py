@@ -453,6 +453,8 @@ def run_b200(args):
         "pass_stats": [{"n_active_before": s.n_active_before, "n_spec": s.n_spec, "visible": s.visible_blocks,
                         "active": s.active_blocks, "decoded": s.new_decompressed, "cache_slots": s.cache_slots,
                         "utilization": round(s.utilization, 4)} for s in stats],
+        "pass_ms": [round(s.duration * 1e3, 4) for s in stats],
+        "pass_ms_note": "device ms of each pass of the last timed frame (its captured graph, CUDA events around the launch)",
         "stage_ms_per_frame": {k: round(v, 4) for k, v in stage_frame.items()},
         "frame_ms_outside_stages": round(float(np.mean(staged_ms)) - sum(stage_frame.values()), 4),
         "stage_split_note": "stage_ms_* from the same frames launched kernel by kernel with stage events "

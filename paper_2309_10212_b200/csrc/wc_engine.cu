@@ -905,15 +905,8 @@ __device__ __forceinline__ void traverse_rays_warp(TraverseArgs a) {
         const int64_t base = i * (int64_t)a.n_spec;
         int emitted = 0;
         bool ray_done = false, finished = false;
-        // coarse chunk: lane k holds the state after step k+1 from the chunk
-        // start.  The coarse walk never depends on the fine runs, so a chunk
-        // interrupted by a descent resumes at step p after the run.
-        bool chunk_ok = false;
-        int p = 0;
-        uint32_t B = 0, T = 0;
-        Dda g;
-        double tk = 0.0;
-        unsigned long long mk = 0;
+        // Coarse chunks: lane k holds the state after step k+1 from the chunk
+        // start (the coarse walk never depends on the fine runs).
         while (!finished) {
             if (in_fine_run) {
                 // lane k: cell X_k of the run (k steps from f), and the step that leaves it
@@ -967,56 +960,118 @@ __device__ __forceinline__ void traverse_rays_warp(TraverseArgs a) {
                 }
                 finished = emitted == a.n_spec || ray_done;
             } else {
-                if (!chunk_ok) {  // lane k: the (k+1)-th coarse step from c, its range bit and fine mask
-                    g = c;
-                    bool valid = true, term_here = false;
-                    for (int j = 0; j <= lane && valid; j++) {
-                        tk = dda_step(g, sx, sy, sz, cdel_x, cdel_y, cdel_z);
-                        if (tk > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 || g.cz >= cdz) {
-                            valid = false;
-                            term_here = j == lane;
-                        }
+                // lane k: the (k+1)-th coarse step from c, its range bit and fine mask
+                Dda g = c;
+                double tk = 0.0;
+                bool valid = true, term_here = false;
+                for (int j = 0; j <= lane && valid; j++) {
+                    tk = dda_step(g, sx, sy, sz, cdel_x, cdel_y, cdel_z);
+                    if (tk > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 || g.cz >= cdz) {
+                        valid = false;
+                        term_here = j == lane;
                     }
-                    const uint32_t cell = valid ? (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz)) : 0u;
-                    const uint32_t cw = valid ? __ldg(a.coarse_bm + (cell >> 5)) : 0u;
-                    mk = valid ? __ldg(a.cell_mask + cell) : 0ull;  // same round trip as the bit
-                    B = __ballot_sync(0xffffffffu, (cw >> (cell & 31)) & 1u);
-                    T = __ballot_sync(0xffffffffu, term_here);
-                    p = 0;
-                    chunk_ok = true;
                 }
-                const uint32_t rem = p >= 32 ? 0u : ~((1u << p) - 1u);
-                const int first_term = (T & rem) ? __ffs(T & rem) - 1 : 32;
-                const int first_hit = (B & rem) ? __ffs(B & rem) - 1 : 32;
-                if (first_hit < first_term) {  // descend (traversal.py:357-386)
-                    c = shfl_dda(g, first_hit);
-                    const double t_cross = __shfl_sync(0xffffffffu, tk, first_hit);
-                    fm = __shfl_sync(0xffffffffu, mk, first_hit);
-                    const double px = ox + dx * t_cross, py = oy + dy * t_cross, pz = oz + dz * t_cross;
-                    const int lo_x = 4 * c.cx, lo_y = 4 * c.cy, lo_z = 4 * c.cz;
+                const uint32_t cell = valid ? (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz)) : 0u;
+                const uint32_t cw = valid ? __ldg(a.coarse_bm + (cell >> 5)) : 0u;
+                const unsigned long long mk = valid ? __ldg(a.cell_mask + cell) : 0ull;
+                const uint32_t T = __ballot_sync(0xffffffffu, term_here);
+                const int first_term = T ? __ffs(T) - 1 : 32;
+                const bool hit = valid && ((cw >> (cell & 31)) & 1u) && lane < first_term;
+                const uint32_t H = __ballot_sync(0xffffffffu, hit);
+                // Every descent of the chunk runs its fine run at once, lane =
+                // descent (traversal.py:357-386, 295-331): the runs never depend
+                // on one another, only their order does.
+                Dda fj{0, 0, 0, 0, 0, 0}, f0{0, 0, 0, 0, 0, 0};
+                unsigned long long codes = 0;
+                int cnt = 0;
+                bool exits = false;
+                if (hit) {
+                    const double px = ox + dx * tk, py = oy + dy * tk, pz = oz + dz * tk;
+                    const int lo_x = 4 * g.cx, lo_y = 4 * g.cy, lo_z = 4 * g.cz;
                     const int hi_x = min(lo_x + 3, fdx - 1), hi_y = min(lo_y + 3, fdy - 1),
                               hi_z = min(lo_z + 3, fdz - 1);
-                    f.cx = (int)floor(px / 4.0);
-                    f.cy = (int)floor(py / 4.0);
-                    f.cz = (int)floor(pz / 4.0);
-                    f.cx = f.cx < lo_x ? lo_x : (f.cx > hi_x ? hi_x : f.cx);
-                    f.cy = f.cy < lo_y ? lo_y : (f.cy > hi_y ? hi_y : f.cy);
-                    f.cz = f.cz < lo_z ? lo_z : (f.cz > hi_z ? hi_z : f.cz);
-                    f.tx = dx > 0.0 ? ((double)(f.cx + 1) * 4.0 - ox) / dx
-                                    : (dx < 0.0 ? ((double)f.cx * 4.0 - ox) / dx : CUDART_INF);
-                    f.ty = dy > 0.0 ? ((double)(f.cy + 1) * 4.0 - oy) / dy
-                                    : (dy < 0.0 ? ((double)f.cy * 4.0 - oy) / dy : CUDART_INF);
-                    f.tz = dz > 0.0 ? ((double)(f.cz + 1) * 4.0 - oz) / dz
-                                    : (dz < 0.0 ? ((double)f.cz * 4.0 - oz) / dz : CUDART_INF);
-                    in_fine_run = true;
-                    p = first_hit + 1;
-                } else if (first_term < 32) {  // left the volume / passed t_exit
-                    c = shfl_dda(g, first_term);
-                    ray_done = true;
+                    f0.cx = (int)floor(px / 4.0);
+                    f0.cy = (int)floor(py / 4.0);
+                    f0.cz = (int)floor(pz / 4.0);
+                    f0.cx = f0.cx < lo_x ? lo_x : (f0.cx > hi_x ? hi_x : f0.cx);
+                    f0.cy = f0.cy < lo_y ? lo_y : (f0.cy > hi_y ? hi_y : f0.cy);
+                    f0.cz = f0.cz < lo_z ? lo_z : (f0.cz > hi_z ? hi_z : f0.cz);
+                    f0.tx = dx > 0.0 ? ((double)(f0.cx + 1) * 4.0 - ox) / dx
+                                     : (dx < 0.0 ? ((double)f0.cx * 4.0 - ox) / dx : CUDART_INF);
+                    f0.ty = dy > 0.0 ? ((double)(f0.cy + 1) * 4.0 - oy) / dy
+                                     : (dy < 0.0 ? ((double)f0.cy * 4.0 - oy) / dy : CUDART_INF);
+                    f0.tz = dz > 0.0 ? ((double)(f0.cz + 1) * 4.0 - oz) / dz
+                                     : (dz < 0.0 ? ((double)f0.cz * 4.0 - oz) / dz : CUDART_INF);
+                    fj = f0;
+                    for (int k = 0; k < kFineRun; k++) {
+                        if ((mk >> fine_local(fj)) & 1ull) {
+                            codes |= (unsigned long long)((fj.cx & 3) | ((fj.cy & 3) << 2) | ((fj.cz & 3) << 4))
+                                     << (6 * cnt);
+                            cnt++;
+                        }
+                        const double t = dda_step(fj, sx, sy, sz, fdel_x, fdel_y, fdel_z);
+                        if (t > te || fj.cx < 0 || fj.cx >= fdx || fj.cy < 0 || fj.cy >= fdy || fj.cz < 0 ||
+                            fj.cz >= fdz) {
+                            exits = true;
+                            break;
+                        }
+                        if ((fj.cx >> 2) != g.cx || (fj.cy >> 2) != g.cy || (fj.cz >> 2) != g.cz) break;
+                    }
+                }
+                // the runs' emits in chunk order, until the n_spec-th or a run that exits
+                uint32_t incl = hit ? (uint32_t)cnt : 0u;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const uint32_t excl = incl - (hit ? (uint32_t)cnt : 0u);
+                const uint32_t left = (uint32_t)(a.n_spec - emitted);
+                const uint32_t S = __ballot_sync(0xffffffffu, hit && (incl >= left || exits));
+                const int stop = S ? __ffs(S) - 1 : 32;  // the run the ray's pass ends in
+                if (hit && lane <= stop) {
+                    const uint32_t take = lane == stop ? min((uint32_t)cnt, left - excl) : (uint32_t)cnt;
+                    for (uint32_t q = 0; q < take; q++) {
+                        const uint32_t lc = (uint32_t)(codes >> (6 * q)) & 63u;
+                        const uint32_t f_lin = (uint32_t)((4 * g.cx + (lc & 3)) +
+                                                          fdx * ((4 * g.cy + ((lc >> 2) & 3)) + fdy * (4 * g.cz + (lc >> 4))));
+                        a.block_slots[base + emitted + excl + q] = f_lin;
+                        a.ray_slots[base + emitted + excl + q] = r;
+                        atomicOr(&a.vis_bm[f_lin >> 5], 1u << (f_lin & 31));
+                    }
+                }
+                if (stop < 32) {  // the pass ends in run `stop`
+                    bool ex = exits, lv = false;
+                    Dda fs = fj;
+                    if (lane == stop && incl >= left) {  // the n_spec-th emit: replay to the step after it
+                        fs = f0;
+                        const uint32_t take = left - excl;
+                        uint32_t seen = 0;
+                        for (int k = 0; k < kFineRun; k++) {
+                            seen += (uint32_t)((mk >> fine_local(fs)) & 1ull);
+                            const double t = dda_step(fs, sx, sy, sz, fdel_x, fdel_y, fdel_z);
+                            ex = t > te || fs.cx < 0 || fs.cx >= fdx || fs.cy < 0 || fs.cy >= fdy || fs.cz < 0 ||
+                                 fs.cz >= fdz;
+                            lv = !ex && ((fs.cx >> 2) != g.cx || (fs.cy >> 2) != g.cy || (fs.cz >> 2) != g.cz);
+                            if (seen == take || ex || lv) break;
+                        }
+                    }
+                    c = shfl_dda(g, stop);
+                    f = shfl_dda(fs, stop);
+                    ray_done = __shfl_sync(0xffffffffu, ex, stop);
+                    in_fine_run = !__shfl_sync(0xffffffffu, ex || lv || !(incl >= left), stop);
+                    emitted = min(a.n_spec, emitted + (int)__shfl_sync(0xffffffffu, incl, stop));
                     finished = true;
                 } else {
-                    c = shfl_dda(g, 31);
-                    chunk_ok = false;
+                    emitted += (int)__shfl_sync(0xffffffffu, incl, 31);
+                    if (H) f = shfl_dda(fj, 31 - __clz(H));  // the last run's fine state
+                    if (first_term < 32) {  // left the volume / passed t_exit (traversal.py:345-355)
+                        c = shfl_dda(g, first_term);
+                        ray_done = true;
+                        finished = true;
+                    } else {
+                        c = shfl_dda(g, 31);
+                    }
                 }
             }
         }
