@@ -530,6 +530,7 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
                 if ((fm >> fine_local(f)) & 1ull) {
 #endif
                     const uint32_t f_lin = (uint32_t)(f.cx + fdx * (f.cy + fdy * f.cz));
+                    WC_DEVICE_CHECK(emitted < a.n_spec && (uint64_t)f_lin < (uint64_t)fdx * fdy * fdz);
                     a.block_slots[base + emitted] = f_lin;
                     a.ray_slots[base + emitted] = r;
                     emitted++;
@@ -1035,6 +1036,7 @@ __device__ __forceinline__ void traverse_rays_warp(TraverseArgs a) {
                         const uint32_t lc = (uint32_t)(codes >> (6 * q)) & 63u;
                         const uint32_t f_lin = (uint32_t)((4 * g.cx + (lc & 3)) +
                                                           fdx * ((4 * g.cy + ((lc >> 2) & 3)) + fdy * (4 * g.cz + (lc >> 4))));
+                        WC_DEVICE_CHECK(emitted + (int)(excl + q) < a.n_spec);
                         a.block_slots[base + emitted + excl + q] = f_lin;
                         a.ray_slots[base + emitted + excl + q] = r;
                         atomicOr(&a.vis_bm[f_lin >> 5], 1u << (f_lin & 31));
@@ -1408,6 +1410,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, WC_DEC_CTAS)
         const uint32_t my_b = jl < n_miss ? miss_ids[jl] : 0u;
         const uint32_t my_s = jl < n_miss ? (jl < n_free ? (uint32_t)(hw + jl) : victims[jl - n_free]) : 0u;
         if (jl < n_miss) {  // lane-parallel bookkeeping for the 32 misses
+            WC_DEVICE_CHECK((int64_t)my_s < (int64_t)ctl[C_PHYS] && (int64_t)my_s < cap);
             block_of_slot[my_s] = (int32_t)my_b;
             last_used[my_s] = pass_no;
             slot_of_block[my_b] = (int32_t)my_s;
@@ -1564,6 +1567,7 @@ __global__ void k_rt_prep(BuildEntriesArgs be, const uint32_t *visible_ids, cons
         if (j >= be.emitted[i]) continue;
         const uint32_t eo = be.entry_off[i] + j;
         const uint32_t b = be.block_slots[t];
+        WC_DEVICE_CHECK(eo < be.ctl[C_NENT] && b != WC_UINT_MAX);
         const uint32_t w = b >> 5;
         be.ent_key[eo] = be.vis_word_off[w] + __popc(be.vis_bm[w] & ((1u << (b & 31)) - 1u));
         be.ent_val[eo] = eo;
@@ -1750,6 +1754,7 @@ __global__ void __launch_bounds__(128, WC_RTFIND_MIN_CTAS) k_rt_find(SplitArgs s
             const uint32_t o_ek = __shfl_sync(0xffffffffu, ek, owner), o_er = __shfl_sync(0xffffffffu, er, owner),
                            o_eb = __shfl_sync(0xffffffffu, eb, owner);
             const uint32_t it = base_it + t;
+            WC_DEVICE_CHECK(t >= total || it < s.item_cap);  // 10 dual cells per entry at most
             if (t < total && it < s.item_cap) {
                 const uint32_t q = t - (o_incl - o_found);
                 const uint32_t lc = (uint32_t)(o_codes >> (6 * q)) & 63u;
@@ -1996,6 +2001,7 @@ __global__ void k_composite(const uint32_t *ctl, const uint32_t *act_list, const
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_act;
              i += (int64_t)gridDim.x * blockDim.x) {
             const uint32_t r = act_list[i], ne = emitted[i], eo = entry_off[i];
+            WC_DEVICE_CHECK(eo + ne <= ctl[C_NENT] && ne <= ctl[C_NSPEC]);
             float best = CUDART_INF_F;
             int64_t bk = -1;
             for (uint32_t j = 0; j < ne; j++) {
