@@ -1682,6 +1682,14 @@ __device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, const RayVi
     return e;
 }
 
+#ifndef WC_WALK_PREFETCH
+#define WC_WALK_PREFETCH 0  // the two-phase walk measured slower (raytrace 0.96 vs 0.90 ms/frame)
+#endif
+#if WC_WALK_PREFETCH
+#define WC_WALK walk_bracketing_cells_prefetch
+#else
+#define WC_WALK walk_bracketing_cells
+#endif
 // phase 1: walk each entry's dual cells, list the bracketing ones
 __global__ void __launch_bounds__(128, WC_RTFIND_MIN_CTAS) k_rt_find(SplitArgs s) {
     pdl_wait();
@@ -1712,7 +1720,7 @@ __global__ void __launch_bounds__(128, WC_RTFIND_MIN_CTAS) k_rt_find(SplitArgs s
             s.best[e.k] = kNoRoot;
             const int sl[8] = {ef.s0, ef.s1, ef.s2, ef.s3, ef.s4, ef.s5, ef.s6, ef.s7};
             SlotFieldSmem<128>::fill(&rowtab[0][threadIdx.x], a.slot_values, sl);
-            walk_bracketing_cells(sf, 4 * e.bx, 4 * e.by, 4 * e.bz, 4 * e.bx, 4 * e.by, 4 * e.bz, e.cx, e.cy,
+            WC_WALK(sf, 4 * e.bx, 4 * e.by, 4 * e.bz, 4 * e.bx, 4 * e.by, 4 * e.bz, e.cx, e.cy,
                                   e.cz, e.o, e.d, e.te, iso, [&](int cx, int cy, int cz, int seq) {
                                       const uint32_t lc = (uint32_t)((cx - 4 * e.bx) | ((cy - 4 * e.by) << 2) |
                                                                      ((cz - 4 * e.bz) << 4));
