@@ -2360,6 +2360,7 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     fparams.alloc(8);
     h_plog.alloc((int64_t)kMaxPassLog * L_COUNT);
     reset(cam, iso_);
+    precapture(kPrecapturePasses);
 }
 
 // A new frame on the same allocations: fresh rays for (cam, iso), a blank
@@ -2638,35 +2639,48 @@ void Session::drop_graphs() {
 // the device (control block, FrameParams, device-derived scan epochs), so a
 // replay is exactly the enqueued pass.  Modes with host reads inside a pass
 // (entry grouping, more passes than histogram bins) are enqueued directly.
+Session::PassGraph *Session::graph_for(int64_t p) {
+    for (auto &x : graphs)
+        if (x.p == p) return &x;
+    const long long launches0 = g_launches.load();
+    cudaGraph_t graph = nullptr;
+    WC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+        enqueue_pass(p);
+    } catch (...) {
+        cudaStreamEndCapture(st, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    WC_CUDA(cudaStreamEndCapture(st, &graph));
+    PassGraph pg{p, nullptr, g_launches.load() - launches0};
+    g_launches -= pg.kernels;  // captured, not launched
+    const cudaError_t e = cudaGraphInstantiate(&pg.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    WC_CUDA(e);
+    WC_CUDA(cudaGraphUpload(pg.exec, st));
+    graphs.push_back(pg);
+    return &graphs.back();
+}
+
+// Capture (and upload) the graphs of the first passes ahead of time, so that
+// no frame's device timeline waits for the host to capture a pass it reaches
+// for the first time.
+void Session::precapture(int64_t passes) {
+    if (!use_graphs || group_entries) return;
+    for (int64_t p = 0; p < passes && p + 2 <= kHistBins && p < kMaxPassLog; p++) {
+        prepare_pass(p);
+        graph_for(p);
+    }
+}
+
 void Session::launch_pass(int64_t p) {
     if (!use_graphs || group_entries || p + 2 > kHistBins || p >= kMaxPassLog) {
         enqueue_pass(p);
         return;
     }
     prepare_pass(p);
-    PassGraph *g = nullptr;
-    for (auto &x : graphs)
-        if (x.p == p) g = &x;
-    if (!g) {
-        const long long launches0 = g_launches.load();
-        cudaGraph_t graph = nullptr;
-        WC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        try {
-            enqueue_pass(p);
-        } catch (...) {
-            cudaStreamEndCapture(st, &graph);
-            if (graph) cudaGraphDestroy(graph);
-            throw;
-        }
-        WC_CUDA(cudaStreamEndCapture(st, &graph));
-        PassGraph pg{p, nullptr, g_launches.load() - launches0};
-        g_launches -= pg.kernels;  // captured, not launched
-        const cudaError_t e = cudaGraphInstantiate(&pg.exec, graph, 0);
-        cudaGraphDestroy(graph);
-        WC_CUDA(e);
-        graphs.push_back(pg);
-        g = &graphs.back();
-    }
+    PassGraph *g = graph_for(p);
     cudaEvent_t *ev = pass_events(p);
     WC_CUDA(cudaEventRecord(ev[0], st));
     WC_CUDA(cudaGraphLaunch(g->exec, st));

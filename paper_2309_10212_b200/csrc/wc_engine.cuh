@@ -290,6 +290,9 @@ struct Session : CacheStore {
         long long kernels;  // kernels per replay (the launch counter)
     };
     std::vector<PassGraph> graphs;
+    PassGraph *graph_for(int64_t p);  // captured on first use
+    static constexpr int64_t kPrecapturePasses = 8;
+    void precapture(int64_t passes);
     void collect_pass(int64_t p, PassStatsC &stats);
     void check_device_errors();
     void reserve_slots(int64_t need);

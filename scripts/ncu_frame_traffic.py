@@ -16,9 +16,10 @@ import json
 
 STAGE_OF = [
     ("k_traverse", "traverse"),
-    ("k_rt_", "raytrace"), ("k_raytrace", "raytrace"), ("k_contrib", "raytrace"),
+    ("k_rt_prep", "rt_inputs"), ("k_rt_", "raytrace"), ("k_raytrace", "raytrace"), ("k_contrib", "raytrace"),
     ("k_decode_insert", "cache_decode"), ("k_evict", "cache_decode"), ("k_stamp_hist", "cache_decode"),
     ("k_mark_victims", "cache_decode"), ("SinkList", "cache_decode"), ("SinkBitsIdx", "cache_decode"),
+    ("LookupStamp", "mark"),
     ("k_cache_plan", "cache_decode"),
     ("k_iso_bitmap", "reset"), ("k_iso_cell_mask", "reset"), ("k_init_rays", "reset"), ("k_cache_unmap", "reset"),
     ("PredActive", "reset"), ("k_frame_start", "reset"),
