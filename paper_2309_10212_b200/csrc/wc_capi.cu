@@ -236,7 +236,7 @@ int wc_volume_load_wcz(const char *path, int64_t chunk_bytes, wc_volume **out) {
     try {
         v->v.set_dims(h.nx, h.ny, h.nz, h.qbits);
         v->v.ranges.alloc(h.n_blocks);
-        v->v.payload.alloc(h.n_blocks * h.stride);
+        v->v.payload.alloc(h.n_blocks * h.stride + wc::kPayloadPad);
         const int64_t chunk = chunk_bytes > 0 ? chunk_bytes : (int64_t)64 << 20;
         stream_to_device(f.fd, path, 28, 8 * h.n_blocks, v->v.ranges.p, chunk, v->v.st);
         stream_to_device(f.fd, path, 28 + 8 * h.n_blocks, h.n_blocks * h.stride, v->v.payload.p, chunk, v->v.st);
@@ -257,7 +257,7 @@ int wc_volume_alloc(int nx, int ny, int nz, int qbits, wc_volume **out) {
     try {
         v->v.set_dims(nx, ny, nz, qbits);
         v->v.ranges.alloc(v->v.n_blocks);
-        v->v.payload.alloc(v->v.n_blocks * v->v.stride);
+        v->v.payload.alloc(v->v.n_blocks * v->v.stride + wc::kPayloadPad);
     } catch (...) {
         delete v;
         throw;

@@ -54,7 +54,13 @@
 #define WC_DEC_REC 16
 #endif
 #ifndef WC_DEC_CTAS
-#define WC_DEC_CTAS 4
+#define WC_DEC_CTAS 3
+#endif
+#ifndef WC_DEC_PIPE
+#define WC_DEC_PIPE 2
+#endif
+#ifndef WC_DEC_PREC
+#define WC_DEC_PREC 8
 #endif
 // k_traverse: idle lanes that trigger a refill of the warp
 #ifndef WC_REFILL_MIN
@@ -339,6 +345,12 @@ constexpr int kFineRun = 10;  // a monotone ray visits at most 4+4+4-2 fine cell
 // bit of fine cell f in its coarse cell's iso mask (k_iso_cell_mask)
 __device__ __forceinline__ int fine_local(const Dda &f) { return 16 * (f.cx & 3) + (f.cy & 3) + 4 * (f.cz & 3); }
 
+#ifndef WC_TRAV_PLAIN
+#define WC_TRAV_PLAIN 0  // measured neutral at C3 (0.828 vs 0.824 ms), slower at C4 (2.01 vs 1.95 ms)
+#endif
+#ifndef WC_TRAV_KEEP
+#define WC_TRAV_KEEP 1
+#endif
 #ifndef WC_TRAV_AXIS
 #define WC_TRAV_AXIS 0  // per-axis exit tests (measured slower at C3: 0.88 vs 0.80 ms)
 #endif
@@ -385,6 +397,22 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
     bool in_fine_run = false;
     unsigned long long fm = 0;  // iso mask of the fine cells of coarse cell c
     int64_t base = 0;
+    // A run is plain when no step of it can end the ray: coarse cell c and
+    // its neighbours lie inside the grid (a step out of c lands in the grid)
+    // and c's exit crossing (min of c's tmax: every fine crossing inside c is
+    // earlier, up to a few ulps of accumulated rounding) is below t_exit by a
+    // relative 1e-9.  Then the reference's exit test (traversal.py:315-320)
+    // is false at every step and only the leave-c test remains.
+    bool plain = false;
+    auto plain_cell = [&]() {
+#if WC_TRAV_PLAIN
+        const double tcx = fmin(c.tx, fmin(c.ty, c.tz));
+        return c.cx >= 1 && c.cy >= 1 && c.cz >= 1 && 4 * c.cx + 5 <= fdx && 4 * c.cy + 5 <= fdy &&
+               4 * c.cz + 5 <= fdz && tcx > 0.0 && tcx < te * (1.0 - 1e-9);
+#else
+        return false;
+#endif
+    };
     for (;;) {
         if (!exhausted) {  // refill idle lanes (warp-uniform branch)
             const uint32_t need = __ballot_sync(0xffffffffu, !have);
@@ -426,6 +454,7 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
                         f.cy = (int)((fc / (uint32_t)fdx) % (uint32_t)fdy);
                         f.cz = (int)(fc / ((uint32_t)fdx * (uint32_t)fdy));
                         fm = __ldg(a.cell_mask + cc);
+                        plain = plain_cell();
                     }
                     f.tx = a.fine_tmax[3 * (int64_t)r];
                     f.ty = a.fine_tmax[3 * (int64_t)r + 1];
@@ -457,6 +486,7 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
             f.tz = dz > 0.0 ? ((double)(f.cz + 1) * 4.0 - oz) / dz
                             : (dz < 0.0 ? ((double)f.cz * 4.0 - oz) / dz : CUDART_INF);
             in_fine_run = true;
+            plain = plain_cell();
         };
         if (!in_fine_run) {
             if (CA == 1) {  // one coarse step (traversal.py:332-386)
@@ -476,6 +506,10 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
             } else {  // CA coarse steps: simulate, fetch all range bits, descend at the first hit
                 Dda g = c;
                 uint32_t cell[CA];
+#if WC_TRAV_KEEP
+                Dda gs[CA];  // the state after step j + 1 (no re-stepping at the descent)
+                double ts[CA];
+#endif
                 int J = 0;
                 bool done = false;
 #pragma unroll
@@ -494,6 +528,10 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
                         } else {
                             cell[j] = (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz));
                             J = j + 1;
+#if WC_TRAV_KEEP
+                            gs[j] = g;
+                            ts[j] = t;
+#endif
                         }
                     }
                 }
@@ -504,7 +542,16 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
                 if (bits) {
                     const int js = __ffs(bits) - 1;
                     double t_cross = 0.0;
+#if WC_TRAV_KEEP
+#pragma unroll
+                    for (int j = 0; j < CA; j++)
+                        if (j == js) {
+                            c = gs[j];
+                            t_cross = ts[j];
+                        }
+#else
                     for (int j = 0; j <= js; j++) t_cross = dda_step(c, sx, sy, sz, 4.0 * fdel_x, 4.0 * fdel_y, 4.0 * fdel_z);
+#endif
                     descend(t_cross);
                     fm = __ldg(a.cell_mask + (c.cx + cdx * (c.cy + cdy * c.cz)));
                 } else {
@@ -552,7 +599,8 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
                 lb += st * pick3(ax, 16, 1, 4);
 #else
                 const double t = dda_step(f, sx, sy, sz, fdel_x, fdel_y, fdel_z);
-                if (t > te || f.cx < 0 || f.cx >= fdx || f.cy < 0 || f.cy >= fdy || f.cz < 0 || f.cz >= fdz) {
+                if (!plain &&
+                    (t > te || f.cx < 0 || f.cx >= fdx || f.cy < 0 || f.cy >= fdy || f.cz < 0 || f.cz >= fdz)) {
                     in_fine_run = false;
                     ray_done = true;
                     break;
@@ -1384,14 +1432,21 @@ __global__ void k_evict(const uint32_t *victims, const uint32_t *d_n_evict, int3
 // request, so many random 132 B records are in flight per SM), then decoded
 // from shared memory straight into the slots.
 constexpr int kDecWarps = WC_DEC_WARPS, kDecRec = WC_DEC_REC, kDecWords = 64;  // words: the largest record (qbits 31)
+// pipelined form: records per batch (two batches per warp in flight), words per
+// staged record (the largest record's 16-byte aligned span)
+constexpr int kDecRecP = WC_DEC_PREC, kDecWordsP = 72;
 __global__ void __launch_bounds__(kDecWarps * 32, WC_DEC_CTAS)
     k_decode_insert(const uint8_t *__restrict__ payload, int qbits, int stride, const uint32_t *__restrict__ miss_ids,
                     uint32_t *ctl, const uint32_t *__restrict__ victims, float *__restrict__ slot_values,
                     int32_t *block_of_slot, int32_t *last_used, int32_t *slot_of_block, int32_t pass_no) {
     pdl_wait();
-    __shared__ uint32_t stage[kDecWarps][kDecRec][kDecWords];
     const int lane = threadIdx.x & 31;
+#if WC_DEC_PIPE
+    __shared__ __align__(16) uint32_t stage_p[kDecWarps][2][kDecRecP][kDecWordsP];
+#else
+    __shared__ uint32_t stage[kDecWarps][kDecRec][kDecWords];
     uint32_t(*sw)[kDecWords] = stage[threadIdx.x >> 5];
+#endif
     const int64_t n_miss = ctl[C_NMISS], hw = ctl[C_HW], n_free = ctl[C_NFREE], cap = ctl[C_CAP];
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl[C_HW_NEXT] = (uint32_t)(n_miss <= n_free ? hw + n_miss : cap);
     {  // maps of the slots this pass's growth brought into use (cache.py:42-53) that no miss takes
@@ -1405,6 +1460,135 @@ __global__ void __launch_bounds__(kDecWarps * 32, WC_DEC_CTAS)
     const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int n_words = stride >> 2;
+#if WC_DEC_PIPE
+    // Pipelined: a warp takes groups of 32 misses (strided over the grid) in
+    // batches of kDecRecP records; batch k+1's records are in flight while
+    // batch k is decoded (two stage buffers per warp).
+    //   WC_DEC_PIPE 1: 4-byte cp.async per word (LDGSTS);
+    //   WC_DEC_PIPE 2: one bulk copy (TMA engine) per record of its 16-byte
+    //                  aligned span, completion counted on a per-buffer mbarrier.
+    const int64_t gstride = nwarps * 32;
+    int64_t g = warp0 * 32;
+    if (g >= n_miss) return;  // whole warp (no CTA-wide barrier follows)
+    const int w_in = threadIdx.x >> 5;
+#if WC_DEC_PIPE == 2
+    __shared__ __align__(8) unsigned long long mbar[kDecWarps][2];
+    if (lane == 0) {
+        mbar_init(&mbar[w_in][0], 1);
+        mbar_init(&mbar[w_in][1], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t phase = 0;  // bit b: parity of buffer b's next completion
+    uint32_t offs[2] = {0u, 0u};  // lane u: word offset of record u inside its span, per buffer
+#endif
+    auto group_ids = [&](int64_t gg, uint32_t &b, uint32_t &s) {
+        const int64_t jl = gg + lane;
+        b = jl < n_miss ? miss_ids[jl] : 0u;
+        s = jl < n_miss ? (jl < n_free ? (uint32_t)(hw + jl) : victims[jl - n_free]) : 0u;
+        if (jl < n_miss) {  // lane-parallel bookkeeping for the 32 misses
+            WC_DEVICE_CHECK((int64_t)s < (int64_t)ctl[C_PHYS] && (int64_t)s < cap);
+            block_of_slot[s] = (int32_t)b;
+            last_used[s] = pass_no;
+            slot_of_block[b] = (int32_t)s;
+        }
+    };
+    auto issue = [&](int buf, uint32_t ids, int cnt, int u0) {
+#if WC_DEC_PIPE == 1
+#pragma unroll
+        for (int u = 0; u < kDecRecP; u++) {
+            const uint32_t b = __shfl_sync(0xffffffffu, ids, (u0 + u) & 31);
+            if (u0 + u < cnt) {
+                const uint32_t *rec = reinterpret_cast<const uint32_t *>(payload + (int64_t)b * stride);
+                uint32_t *dst = stage_p[w_in][buf][u];
+                if (lane < n_words) cp_async4(&dst[lane], rec + lane);
+                if (lane + 32 < n_words) cp_async4(&dst[lane + 32], rec + lane + 32);
+            }
+        }
+        cp_async_commit();
+#else
+        const uint32_t b = __shfl_sync(0xffffffffu, ids, (u0 + lane) & 31);
+        const bool mine = lane < kDecRecP && u0 + lane < cnt;
+        const uint64_t a0 = (uint64_t)(payload + (int64_t)b * stride);
+        const uint64_t lo = a0 & ~15ull, hi = (a0 + (uint64_t)stride + 15ull) & ~15ull;
+        const uint32_t bytes = mine ? (uint32_t)(hi - lo) : 0u;
+        offs[buf] = (uint32_t)(a0 - lo) >> 2;
+        const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
+        if (lane == 0) mbar_arrive_expect_tx(&mbar[w_in][buf], total);
+        __syncwarp();
+        if (mine) bulk_g2s(stage_p[w_in][buf][lane], reinterpret_cast<const void *>(lo), bytes, &mbar[w_in][buf]);
+#endif
+    };
+    auto wait_buf = [&](int buf, bool more) {
+#if WC_DEC_PIPE == 1
+        if (more)
+            cp_async_wait_1();
+        else
+            cp_async_wait_0();
+        (void)buf;
+#else
+        (void)more;
+        mbar_wait_parity(&mbar[w_in][buf], (phase >> buf) & 1u);
+        phase ^= 1u << buf;
+#endif
+        __syncwarp();
+    };
+    uint32_t cb, cs;
+    group_ids(g, cb, cs);
+    int ccnt = n_miss - g < 32 ? (int)(n_miss - g) : 32;
+    int buf = 0, u0 = 0;
+    issue(0, cb, ccnt, 0);
+    for (;;) {
+        int64_t g2 = g;
+        int u2 = u0 + kDecRecP, cnt2 = ccnt;
+        const bool next_group = u2 >= ccnt;
+        if (next_group) {
+            g2 = g + gstride;
+            u2 = 0;
+        }
+        const bool more = g2 < n_miss;
+        uint32_t nb = cb, ns = cs;
+        if (more) {
+            if (next_group) {
+                group_ids(g2, nb, ns);
+                cnt2 = n_miss - g2 < 32 ? (int)(n_miss - g2) : 32;
+            }
+            issue(buf ^ 1, nb, cnt2, u2);
+        }
+        wait_buf(buf, more);
+#pragma unroll 4
+        for (int u = 0; u < kDecRecP; u++) {
+            const uint32_t sl = __shfl_sync(0xffffffffu, cs, (u0 + u) & 31);
+            if (u0 + u >= ccnt) break;  // warp-uniform
+#if WC_DEC_PIPE == 2
+            const uint32_t *rw = stage_p[w_in][buf][u] + __shfl_sync(0xffffffffu, offs[buf], u);
+#else
+            const uint32_t *rw = stage_p[w_in][buf][u];
+#endif
+            float *dst = slot_values + (int64_t)sl * 64;
+            if (qbits == 16) {
+                reinterpret_cast<float2 *>(dst)[lane] = decode16_words(rw[lane], rw[lane + 1], rw[0]);
+            } else {
+                const uint32_t wa = lane < n_words ? rw[lane] : 0u;
+                const uint32_t wb = lane + 32 < n_words ? rw[lane + 32] : 0u;
+                float v0, v1;
+                decode_loaded_warp(wa, wb, qbits, lane, v0, v1);
+                dst[lane] = v0;
+                dst[lane + 32] = v1;
+            }
+        }
+        __syncwarp();  // buffer `buf` is refilled by the batch after next
+        if (!more) break;
+        if (next_group) {
+            cb = nb;
+            cs = ns;
+            ccnt = cnt2;
+            g = g2;
+        }
+        u0 = u2;
+        buf ^= 1;
+    }
+#else
     for (int64_t g = warp0 * 32; g < n_miss; g += nwarps * 32) {
         const int64_t jl = g + lane;
         const uint32_t my_b = jl < n_miss ? miss_ids[jl] : 0u;
@@ -1447,6 +1631,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, WC_DEC_CTAS)
             __syncwarp();  // the stage is refilled by the next batch
         }
     }
+#endif
 }
 
 // -------------------------------------------------------------- raytrace

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256, WC_DENSE_MIN_CTAS) k_bitmap_dense(uint32_
                                                       uint32_t *__restrict__ word_offsets, uint32_t *__restrict__ ids,
                                                       uint64_t *status, ScanEpoch ep, uint32_t *d_count) {
     pdl_wait();
-    __shared__ uint32_t sw[32];
+    __shared__ uint32_t sw[32], slb[64];
     __shared__ uint32_t s_excl, s_ticket;
     const uint32_t epoch = resolve_epoch(ep);
     const int64_t chunk = 256LL * 4 * q16;
@@ -176,12 +176,14 @@ __global__ void __launch_bounds__(256, WC_DENSE_MIN_CTAS) k_bitmap_dense(uint32_
     for (int j = 0; j < kDenseQ16; j++) cnt += __popc(q[j].x) + __popc(q[j].y) + __popc(q[j].z) + __popc(q[j].w);
     uint32_t agg;
     uint32_t pre = block_exclusive_scan(cnt, sw, &agg);
-    if (threadIdx.x < 32) {
-        const uint32_t excl = tile_lookback(t, agg, tile_status(status), epoch);
-        if (threadIdx.x == 0) {
-            s_excl = excl;
-            if (t == last) *d_count = excl + agg;
-        }
+    uint32_t excl = 0;
+    if (WC_LOOKBACK_CTA)
+        excl = tile_lookback_cta(t, agg, tile_status(status), epoch, slb);
+    else if (threadIdx.x < 32)
+        excl = tile_lookback(t, agg, tile_status(status), epoch);
+    if (threadIdx.x == 0) {
+        s_excl = excl;
+        if (t == last) *d_count = excl + agg;
     }
     __syncthreads();
     pre += s_excl;

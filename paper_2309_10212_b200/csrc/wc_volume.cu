@@ -166,7 +166,7 @@ void synth_separable_compress(Volume &v, int K, const float *amp, const float *f
     WC_CUDA(cudaMemcpyAsync(d_fx.p, fx, sizeof(float) * K * v.nx, cudaMemcpyHostToDevice, v.st));
     WC_CUDA(cudaMemcpyAsync(d_fy.p, fy, sizeof(float) * K * v.ny, cudaMemcpyHostToDevice, v.st));
     WC_CUDA(cudaMemcpyAsync(d_fz.p, fz, sizeof(float) * K * v.nz, cudaMemcpyHostToDevice, v.st));
-    v.payload.alloc(v.n_blocks * v.stride);
+    v.payload.alloc(v.n_blocks * v.stride + kPayloadPad);
     v.ranges.alloc(v.n_blocks);
     SeparableField f{K, v.nx, v.ny, v.nz, d_amp.p, d_fx.p, d_fy.p, d_fz.p};
     k_compress<<<grid_for(v.n_blocks * 32, 256, 8), 256, 0, v.st>>>(f, v.nx, v.ny, v.nz, v.bdx, v.bdy, v.n_blocks,
@@ -176,7 +176,7 @@ void synth_separable_compress(Volume &v, int K, const float *amp, const float *f
 }
 
 void compress_dense_device(Volume &v, const float *d_values) {
-    v.payload.alloc(v.n_blocks * v.stride);
+    v.payload.alloc(v.n_blocks * v.stride + kPayloadPad);
     v.ranges.alloc(v.n_blocks);
     DenseField f{d_values, v.nx, v.ny};
     k_compress<<<grid_for(v.n_blocks * 32, 256, 8), 256, 0, v.st>>>(f, v.nx, v.ny, v.nz, v.bdx, v.bdy, v.n_blocks,
