@@ -315,6 +315,13 @@ int wc_cache_dual_grid(wc_cache *c, int64_t block_id, float *values125);
 int wc_intersect_cells(int64_t n, const float *corners, const double *origin, const double *dir, const double *cell,
                        const double *t0, const double *t1, double iso, double *t_out);
 int wc_cell_overlaps(int64_t n, const double *origin, const double *dir, const double *cell, double *t0, double *t1);
+
+/* Self-check (no reference counterpart): the kernels divide by a ray's
+ * direction components through a factored float64 division (one reciprocal
+ * refinement per divisor, reused); this compares it with the plain division
+ * over n hashed operand pairs from `seed` and reports the mismatching count
+ * (0 expected) and the last mismatching (a, b) in example[0..1]. */
+int wc_check_fastdiv(int64_t n, uint64_t seed, int64_t *mismatches, double *example);
 int wc_shade(int64_t n, const double *grad, const double *dir, const double *base_color, double *rgb);
 int wc_raytrace_block(const float *values125, const int *block_origin, const int *cells_per_axis, int64_t n,
                       const double *origin, const double *dir, const double *t_enter, double iso,

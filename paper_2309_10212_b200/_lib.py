@@ -141,6 +141,7 @@ _SIGS = {
     "wc_cache_dual_grid": (_i32, [_vp, _i64, _vp]),
     "wc_intersect_cells": (_i32, [_i64] + [_vp] * 6 + [_dbl, _vp]),
     "wc_cell_overlaps": (_i32, [_i64] + [_vp] * 5),
+    "wc_check_fastdiv": (_i32, [_i64, C.c_uint64, _vp, _vp]),
     "wc_shade": (_i32, [_i64] + [_vp] * 4),
     "wc_raytrace_block": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _dbl, _vp, _vp, _vp, _vp]),
     "wc_exclusive_scan": (_i32, [_vp, _i64, _vp, _vp]),

@@ -1022,6 +1022,13 @@ int wc_cell_overlaps(int64_t n, const double *origin, const double *dir, const d
     WC_API_END
 }
 
+int wc_check_fastdiv(int64_t n, uint64_t seed, int64_t *mismatches, double *example) {
+    WC_API_BEGIN
+    const int64_t bad = wc::stage_check_fastdiv(n, seed, example);
+    if (mismatches) *mismatches = bad;
+    WC_API_END
+}
+
 int wc_shade(int64_t n, const double *grad, const double *dir, const double *base_color, double *rgb) {
     WC_API_BEGIN
     wc::stage_shade(n, grad, dir, base_color, rgb);

@@ -580,7 +580,8 @@ __global__ void k_cell_overlaps(int64_t n, const double *o, const double *d, con
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double oo[3] = {o[3 * i], o[3 * i + 1], o[3 * i + 2]}, dd[3] = {d[3 * i], d[3 * i + 1], d[3 * i + 2]};
         const double cc[3] = {cell[3 * i], cell[3 * i + 1], cell[3 * i + 2]};
-        cell_overlap(oo, dd, cc, t0[i], t1[i]);  // blocktrace.py:126-158
+        const Recip rd[3] = {recip_of(dd[0]), recip_of(dd[1]), recip_of(dd[2])};
+        cell_overlap(oo, dd, rd, cc, t0[i], t1[i]);  // blocktrace.py:126-158
     }
 }
 
@@ -643,6 +644,66 @@ void stage_intersect_cells(int64_t n, const float *corners, const double *o, con
     WC_LAUNCH_CHECK();
     to_host(t_out, dt.p, n, S.st);
     S.sync();
+}
+
+// Self-check of the factored division (wc_common.cuh div_by): n operand
+// pairs from a counter-based hash, a mix of the path's own magnitudes (grid
+// coordinates minus ray origins over unit-vector components) and arbitrary
+// bit patterns; counts quotients whose bits differ from a / b.
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    return x ^ (x >> 33);
+}
+__global__ void k_fastdiv_check(uint64_t n, uint64_t seed, unsigned long long *bad, double *example) {
+    unsigned long long local = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t h1 = mix64(seed ^ (2 * i)), h2 = mix64(seed ^ (2 * i + 1));
+        double a, b;
+        switch (h1 & 3) {
+            case 0:  // the path: (grid coordinate - origin) / direction component
+                a = (double)(int)((h1 >> 8) % 9000) - 4500.0 + __longlong_as_double((h2 & 0x000FFFFFFFFFFFFFull) |
+                                                                                    0x3FF0000000000000ull);
+                b = __longlong_as_double(((h2 >> 3) & 0x000FFFFFFFFFFFFFull) |
+                                         ((uint64_t)(1022 - ((h2 >> 58) & 31)) << 52)) *
+                    ((h1 >> 4) & 1 ? -1.0 : 1.0);
+                break;
+            case 1:  // constants over components (4 / d, 16 / d, 1 / d)
+                a = (double)(1u << (2 * ((h1 >> 8) % 3)));
+                b = __longlong_as_double((h2 & 0x000FFFFFFFFFFFFFull) | ((uint64_t)(1023 - ((h2 >> 52) & 63)) << 52)) *
+                    ((h1 >> 4) & 1 ? -1.0 : 1.0);
+                break;
+            default:  // arbitrary bit patterns (incl. subnormals, infinities, NaN)
+                a = __longlong_as_double((long long)h1);
+                b = __longlong_as_double((long long)h2);
+                break;
+        }
+        const double q = div_by(a, recip_of(b)), ref = a / b;
+        const bool same = __double_as_longlong(q) == __double_as_longlong(ref) || (q != q && ref != ref);
+        if (!same) {
+            local++;
+            example[0] = a;
+            example[1] = b;
+        }
+    }
+    if (local) atomicAdd(bad, local);
+}
+
+int64_t stage_check_fastdiv(int64_t n, uint64_t seed, double *example) {
+    DevBuf<unsigned long long> d_bad;
+    DevBuf<double> d_ex;
+    d_bad.alloc(1);
+    d_ex.alloc(2);
+    WC_CUDA(cudaMemset(d_bad.p, 0, sizeof(unsigned long long)));
+    WC_CUDA(cudaMemset(d_ex.p, 0, 2 * sizeof(double)));
+    k_fastdiv_check<<<num_sms() * 8, 256>>>((uint64_t)n, seed, d_bad.p, d_ex.p);
+    WC_LAUNCH_CHECK();
+    unsigned long long bad = 0;
+    WC_CUDA(cudaMemcpy(&bad, d_bad.p, sizeof(bad), cudaMemcpyDeviceToHost));
+    if (example) WC_CUDA(cudaMemcpy(example, d_ex.p, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+    return (int64_t)bad;
 }
 
 void stage_cell_overlaps(int64_t n, const double *o, const double *d, const double *cell, double *t0, double *t1) {

@@ -55,6 +55,7 @@ struct StageCache : CacheStore {
 // blocktrace.py:126-158, 236-280, 306-314, 491-530 (batched)
 void stage_intersect_cells(int64_t n, const float *corners, const double *o, const double *d, const double *cell,
                            const double *t0, const double *t1, double iso, double *t_out);
+int64_t stage_check_fastdiv(int64_t n, uint64_t seed, double *example);
 void stage_cell_overlaps(int64_t n, const double *o, const double *d, const double *cell, double *t0, double *t1);
 void stage_shade(int64_t n, const double *grad, const double *dir, const double base[3], double *rgb);
 void stage_raytrace_block(const float *values125, const int origin[3], const int cells[3], int64_t n, const double *o,

@@ -21,14 +21,15 @@ __device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? 
 __device__ __forceinline__ double py_min(double a, double b) { return (b < a) ? b : a; }
 
 // blocktrace.py:126-158 _cell_overlap
-__device__ __forceinline__ void cell_overlap(const double o[3], const double d[3], const double c[3],
-                                             double &t0o, double &t1o) {
+// (rd: the reciprocals of d, recip_of; the quotients are exactly (x - o) / d)
+__device__ __forceinline__ void cell_overlap(const double o[3], const double d[3], const Recip rd[3],
+                                             const double c[3], double &t0o, double &t1o) {
     double t0 = -CUDART_INF, t1 = CUDART_INF;
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         if (d[a] != 0.0) {
-            double ta = (c[a] - o[a]) / d[a];
-            double tb = (c[a] + 1.0 - o[a]) / d[a];
+            double ta = div_by(c[a] - o[a], rd[a]);
+            double tb = div_by(c[a] + 1.0 - o[a], rd[a]);
             if (ta > tb) {
                 const double t = ta;
                 ta = tb;
@@ -224,11 +225,12 @@ __device__ double trace_region(const Field &field, int fox, int foy, int foz, in
     if (n_x <= 0 || n_y <= 0 || n_z <= 0) return CUDART_INF;
     double t0 = ray_t_enter, t1 = CUDART_INF;
     const int lo[3] = {lo_x, lo_y, lo_z}, nn[3] = {n_x, n_y, n_z};
+    const Recip rd[3] = {recip_of(d[0]), recip_of(d[1]), recip_of(d[2])};
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         if (d[a] != 0.0) {
-            double ta = ((double)lo[a] - o[a]) / d[a];
-            double tb = ((double)(lo[a] + nn[a]) - o[a]) / d[a];
+            double ta = div_by((double)lo[a] - o[a], rd[a]);
+            double tb = div_by((double)(lo[a] + nn[a]) - o[a], rd[a]);
             if (ta > tb) {
                 const double t = ta;
                 ta = tb;
@@ -251,12 +253,13 @@ __device__ double trace_region(const Field &field, int fox, int foy, int foz, in
     const int sx = d[0] > 0.0 ? 1 : (d[0] < 0.0 ? -1 : 0);
     const int sy = d[1] > 0.0 ? 1 : (d[1] < 0.0 ? -1 : 0);
     const int sz = d[2] > 0.0 ? 1 : (d[2] < 0.0 ? -1 : 0);
-    const double del_x = d[0] != 0.0 ? 1.0 / fabs(d[0]) : CUDART_INF;
-    const double del_y = d[1] != 0.0 ? 1.0 / fabs(d[1]) : CUDART_INF;
-    const double del_z = d[2] != 0.0 ? 1.0 / fabs(d[2]) : CUDART_INF;
-    double tmx = d[0] > 0.0 ? ((double)(cx + 1) - o[0]) / d[0] : (d[0] < 0.0 ? ((double)cx - o[0]) / d[0] : CUDART_INF);
-    double tmy = d[1] > 0.0 ? ((double)(cy + 1) - o[1]) / d[1] : (d[1] < 0.0 ? ((double)cy - o[1]) / d[1] : CUDART_INF);
-    double tmz = d[2] > 0.0 ? ((double)(cz + 1) - o[2]) / d[2] : (d[2] < 0.0 ? ((double)cz - o[2]) / d[2] : CUDART_INF);
+    // 1 / |d| == |1 / d| (round to nearest is sign-symmetric)
+    const double del_x = d[0] != 0.0 ? fabs(div_by(1.0, rd[0])) : CUDART_INF;
+    const double del_y = d[1] != 0.0 ? fabs(div_by(1.0, rd[1])) : CUDART_INF;
+    const double del_z = d[2] != 0.0 ? fabs(div_by(1.0, rd[2])) : CUDART_INF;
+    double tmx = d[0] != 0.0 ? div_by((double)(d[0] > 0.0 ? cx + 1 : cx) - o[0], rd[0]) : CUDART_INF;
+    double tmy = d[1] != 0.0 ? div_by((double)(d[1] > 0.0 ? cy + 1 : cy) - o[1], rd[1]) : CUDART_INF;
+    double tmz = d[2] != 0.0 ? div_by((double)(d[2] > 0.0 ? cz + 1 : cz) - o[2], rd[2]) : CUDART_INF;
     float c[8];
     for (;;) {
         field.corners(cx - fox, cy - foy, cz - foz, c);
@@ -269,7 +272,7 @@ __device__ double trace_region(const Field &field, int fox, int foy, int foz, in
         if ((double)cmin <= iso && iso <= (double)cmax) {
             const double cell[3] = {(double)cx, (double)cy, (double)cz};
             double ct0, ct1;
-            cell_overlap(o, d, cell, ct0, ct1);
+            cell_overlap(o, d, rd, cell, ct0, ct1);
             if (ct0 < ray_t_enter) ct0 = ray_t_enter;
             if (ct0 <= ct1) {
                 const double th = intersect_cubic(c, o, d, cell, ct0, ct1, iso);
@@ -529,7 +532,8 @@ __device__ __forceinline__ double solve_cell(const float c[8], const double o[3]
                                              int cz, double ray_t_enter, double iso) {
     const double cell[3] = {(double)cx, (double)cy, (double)cz};
     double ct0, ct1;
-    cell_overlap(o, d, cell, ct0, ct1);
+    const Recip rd[3] = {recip_of(d[0]), recip_of(d[1]), recip_of(d[2])};
+    cell_overlap(o, d, rd, cell, ct0, ct1);
     if (ct0 < ray_t_enter) ct0 = ray_t_enter;
     if (!(ct0 <= ct1)) return CUDART_INF;
     return intersect_cubic(c, o, d, cell, ct0, ct1, iso);
