@@ -42,6 +42,15 @@
 #ifndef WC_WARP_TRAVERSE_MAX
 #define WC_WARP_TRAVERSE_MAX 16384
 #endif
+// ... and passes of long rays (n_spec >= WC_WARP_LONG_SPEC) up to this many
+// (a 4-way split's third pass: 22K rays at n_spec 23, 0.20 -> 0.12 ms; the
+// whole frame's: 60K rays at n_spec 34 stay thread per ray, 0.30 vs 0.38 ms)
+#ifndef WC_WARP_TRAVERSE_MAX_LONG
+#define WC_WARP_TRAVERSE_MAX_LONG 32768
+#endif
+#ifndef WC_WARP_LONG_SPEC
+#define WC_WARP_LONG_SPEC 16
+#endif
 // k_iso_cell_mask: coarse cells per half-warp in flight
 #ifndef WC_ISO_KU
 #define WC_ISO_KU 4
@@ -1160,7 +1169,8 @@ __global__ void __launch_bounds__(128, WC_TRAVERSE_MIN_CTAS) k_traverse(Traverse
     a.n_act = a.ctl[C_NACT];
     a.n_spec = (int)a.ctl[C_NSPEC];
     a.rays.bind();
-    if (a.n_act > (int64_t)a.warp_max) {
+    const bool warp = a.n_act <= (int64_t)a.warp_max || (a.n_spec >= WC_WARP_LONG_SPEC && a.n_act <= (int64_t)a.warp_max_long);
+    if (!warp) {
         if (!a.warp_only) traverse_rays_thread<CA>(a);
     } else {
         traverse_rays_warp(a);
@@ -1309,6 +1319,7 @@ __global__ void k_mark_active_words(const uint32_t *visible_ids, const uint32_t 
 
 void launch_traverse(TraverseArgs ta, int64_t n_grid, int variant, cudaStream_t st) {
     ta.warp_max = variant == 1 ? 0u : (variant == 2 ? 0xFFFFFFFFu : (uint32_t)WC_WARP_TRAVERSE_MAX);
+    ta.warp_max_long = variant == 0 ? (uint32_t)WC_WARP_TRAVERSE_MAX_LONG : ta.warp_max;
 #if WC_TRAVERSE_Q
     if (variant != 2) {
         launch_pdl(k_traverse_q<WC_COARSE_AHEAD>, grid_for(n_grid, 128, WC_TQ_MIN_CTAS), 128, 0, st, ta);
@@ -1319,7 +1330,7 @@ void launch_traverse(TraverseArgs ta, int64_t n_grid, int variant, cudaStream_t 
 #endif
     // enough CTAs for a warp per ray up to warp_max rays; the thread-per-ray
     // path keeps what fits resident busy and the rest find no work
-    const int64_t warps = std::min<int64_t>(n_grid, variant == 1 ? 0 : (variant == 2 ? n_grid : WC_WARP_TRAVERSE_MAX));
+    const int64_t warps = std::min<int64_t>(n_grid, variant == 1 ? 0 : (variant == 2 ? n_grid : WC_WARP_TRAVERSE_MAX));  // (long passes grid-stride)
     const unsigned grid = std::max(grid_for(n_grid, 128, WC_TRAVERSE_MIN_CTAS), grid_for(std::max<int64_t>(1, warps) * 32, 128, 16));
     launch_pdl(k_traverse<WC_COARSE_AHEAD>, grid, 128, 0, st, ta);
     WC_LAUNCH_CHECK();

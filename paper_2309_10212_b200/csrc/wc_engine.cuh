@@ -111,6 +111,7 @@ struct TraverseArgs {
     // warp per ray when n_act <= warp_max, thread per ray otherwise (both
     // kernels are launched; the other one returns at once)
     uint32_t warp_max;
+    uint32_t warp_max_long;  // ... or n_act <= warp_max_long when n_spec >= WC_WARP_LONG_SPEC (long rays)
     bool warp_only;  // passes with more rays are another kernel's (k_traverse_q builds)
 };
 
