@@ -51,6 +51,18 @@
 #ifndef WC_WARP_LONG_SPEC
 #define WC_WARP_LONG_SPEC 16
 #endif
+// long-ray hand-off from the thread-per-ray traversal (k_traverse_long):
+// in mid-size passes (one rank's share of a tile split) the pass time is the
+// few long rays of the last lanes; 8-way share 0.93 -> 0.88 ms
+#ifndef WC_TRAV_DEFER
+#define WC_TRAV_DEFER 1
+#endif
+#ifndef WC_DEFER_ITERS
+#define WC_DEFER_ITERS 12
+#endif
+#ifndef WC_DEFER_MAX_ACT
+#define WC_DEFER_MAX_ACT 150000  // (a 2-way share's second pass, 205K rays: 0.145 -> 0.157 ms handed off)
+#endif
 // k_iso_cell_mask: coarse cells per half-warp in flight
 #ifndef WC_ISO_KU
 #define WC_ISO_KU 4
@@ -412,6 +424,14 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
     // earlier, up to a few ulps of accumulated rounding) is below t_exit by a
     // relative 1e-9.  Then the reference's exit test (traversal.py:315-320)
     // is false at every step and only the leave-c test remains.
+#if WC_TRAV_DEFER
+    int iters = 0;
+    // (passes of short rays only: with n_spec >= WC_WARP_LONG_SPEC most rays
+    // would be handed off -- a whole frame's third pass: 0.29 -> 0.36 ms)
+    const int defer_k = a.long_q && a.n_act <= (int64_t)WC_DEFER_MAX_ACT && a.n_spec < WC_WARP_LONG_SPEC
+                            ? WC_DEFER_ITERS
+                            : 0x7fffffff;
+#endif
     bool plain = false;
     auto plain_cell = [&]() {
 #if WC_TRAV_PLAIN
@@ -436,6 +456,9 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
                 const uint32_t mine = first + __popc(need & lt);
                 if (!have && mine < a.n_act) {
                     have = true;
+#if WC_TRAV_DEFER
+                    iters = 0;
+#endif
                     i = mine;
                     r = a.act_list[i];
                     double o[3], d[3];
@@ -645,6 +668,21 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
             a.fine_tmax[3 * (int64_t)r + 2] = f.tz;
             have = false;
         }
+#if WC_TRAV_DEFER
+        else if (++iters >= defer_k) {  // hand the ray to k_traverse_long (same iterator, same slots)
+            a.emitted[i] = (uint32_t)emitted;
+            a.coarse_cell[r] = (uint32_t)(c.cx + cdx * (c.cy + cdy * c.cz));
+            a.fine_cell[r] = in_fine_run ? (uint32_t)(f.cx + fdx * (f.cy + fdy * f.cz)) : WC_UINT_MAX;
+            a.coarse_tmax[3 * (int64_t)r] = c.tx;
+            a.coarse_tmax[3 * (int64_t)r + 1] = c.ty;
+            a.coarse_tmax[3 * (int64_t)r + 2] = c.tz;
+            a.fine_tmax[3 * (int64_t)r] = f.tx;
+            a.fine_tmax[3 * (int64_t)r + 1] = f.ty;
+            a.fine_tmax[3 * (int64_t)r + 2] = f.tz;
+            a.long_q[atomicAdd(a.n_long, 1u)] = i;
+            have = false;
+        }
+#endif
     }
 }
 
@@ -919,13 +957,13 @@ __global__ void __launch_bounds__(128, WC_TQ_MIN_CTAS) k_traverse_q(TraverseArgs
 // which cells emit, where the n_spec-th emit or the descent happens, and
 // where the ray leaves.  The lane that simulated exactly that many steps
 // holds the reference's iterator state and shuffles it to the warp.
-__device__ __forceinline__ void traverse_rays_warp(TraverseArgs a) {
+// One ray (position i of the active list) by the whole warp, from its saved
+// iterator with emitted0 of its slots already written.
+__device__ __forceinline__ void warp_trace_ray(const TraverseArgs &a, int64_t i, int emitted0) {
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int fdx = a.fdx, fdy = a.fdy, fdz = a.fdz, cdx = a.cdx, cdy = a.cdy, cdz = a.cdz;
-    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp0; i < a.n_act; i += nwarps) {
+    {
         const uint32_t r = a.act_list[i];
         double o[3], d[3];
         a.rays.load(r, o, d);
@@ -961,7 +999,7 @@ __device__ __forceinline__ void traverse_rays_warp(TraverseArgs a) {
         f.tz = a.fine_tmax[3 * (int64_t)r + 2];
         unsigned long long fm = in_fine_run ? __ldg(a.cell_mask + cc) : 0ull;  // warp-uniform
         const int64_t base = i * (int64_t)a.n_spec;
-        int emitted = 0;
+        int emitted = emitted0;
         bool ray_done = false, finished = false;
         // Coarse chunks: lane k holds the state after step k+1 from the chunk
         // start (the coarse walk never depends on the fine runs).
@@ -1158,6 +1196,12 @@ __device__ __forceinline__ void traverse_rays_warp(TraverseArgs a) {
     }
 }
 
+__device__ __forceinline__ void traverse_rays_warp(TraverseArgs a) {
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp0; i < a.n_act; i += nwarps) warp_trace_ray(a, i, 0);
+}
+
 // One launch per pass: thread per ray (persistent, refilled from a work
 // counter) when the pass has many rays, warp per ray when it has at most
 // warp_max -- chosen on the device from the pass's n_act, so a captured pass
@@ -1317,6 +1361,23 @@ __global__ void k_mark_active_words(const uint32_t *visible_ids, const uint32_t 
     }
 }
 
+// The long rays the thread-per-ray pass handed off, warp per ray.
+__global__ void __launch_bounds__(128) k_traverse_long(TraverseArgs a_in) {
+    pdl_wait();
+    TraverseArgs a = a_in;
+    const uint32_t nq = *a.n_long;
+    if (nq == 0) return;
+    a.n_act = a.ctl[C_NACT];
+    a.n_spec = (int)a.ctl[C_NSPEC];
+    a.rays.bind();
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t q = warp0; q < (int64_t)nq; q += nwarps) {
+        const uint32_t i = a.long_q[q];
+        warp_trace_ray(a, i, (int)a.emitted[i]);
+    }
+}
+
 void launch_traverse(TraverseArgs ta, int64_t n_grid, int variant, cudaStream_t st) {
     ta.warp_max = variant == 1 ? 0u : (variant == 2 ? 0xFFFFFFFFu : (uint32_t)WC_WARP_TRAVERSE_MAX);
     ta.warp_max_long = variant == 0 ? (uint32_t)WC_WARP_TRAVERSE_MAX_LONG : ta.warp_max;
@@ -1332,8 +1393,15 @@ void launch_traverse(TraverseArgs ta, int64_t n_grid, int variant, cudaStream_t 
     // path keeps what fits resident busy and the rest find no work
     const int64_t warps = std::min<int64_t>(n_grid, variant == 1 ? 0 : (variant == 2 ? n_grid : WC_WARP_TRAVERSE_MAX));  // (long passes grid-stride)
     const unsigned grid = std::max(grid_for(n_grid, 128, WC_TRAVERSE_MIN_CTAS), grid_for(std::max<int64_t>(1, warps) * 32, 128, 16));
+    if (variant != 0) ta.long_q = nullptr;  // forced variants: no hand-off
     launch_pdl(k_traverse<WC_COARSE_AHEAD>, grid, 128, 0, st, ta);
     WC_LAUNCH_CHECK();
+#if WC_TRAV_DEFER
+    if (ta.long_q) {
+        launch_pdl(k_traverse_long, (unsigned)(num_sms() * 8), 128, 0, st, ta);
+        WC_LAUNCH_CHECK();
+    }
+#endif
 }
 
 void launch_mark_active(const uint32_t *visible_ids, const uint32_t *d_nvis, const uint32_t *vis_bm, int bdx, int bdy,
@@ -2422,6 +2490,7 @@ __device__ __forceinline__ void pass_end(uint32_t *ctl, uint32_t *row, int64_t n
     row[L_PHYS] = ctl[C_PHYS];
     row[L_HW] = ctl[C_HW_NEXT];
     ctl[C_WORK] = 0;  // the next pass's traversal work counter and raytrace list start empty
+    ctl[C_NLONG] = 0;
     ctl[C_NITEMS] = 0;
     if (n_act == 0) return;  // an enqueued pass after the last one: no state change
     ctl[C_HW] = ctl[C_HW_NEXT];
@@ -2500,6 +2569,7 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     act_list[1].alloc(n);
     keep.alloc(n);
     emitted.alloc(n);
+    long_q.alloc(n);
     entry_off.alloc(n);
     block_slots.alloc(n);
     ray_slots.alloc(n);
@@ -2957,8 +3027,10 @@ void Session::enqueue_pass(int64_t p) {
     ta.emitted = emitted.p;
     ta.vis_bm = vis_bm.p;
     ta.work = ctl + C_WORK;
+    ta.long_q = long_q.p;
+    ta.n_long = ctl + C_NLONG;
     ta.ctl = ctl;
-    // C_WORK and C_NITEMS are zero here (reset, or the last pass_end)
+    // C_WORK, C_NLONG and C_NITEMS are zero here (reset, or the last pass_end)
     launch_traverse(ta, n, 0, st);
     mark(1);
     // entry compaction: exclusive scan of per-ray emitted counts

@@ -53,6 +53,7 @@ enum Counter : int {
     C_NLIST,      // non-zero bitmap words listed by bitmap_extract_listed
     C_FRAME,      // frame counter (device-derived scan epochs)
     C_VSUM,       // victim-region summary words to list this pass (0: no eviction)
+    C_NLONG,      // rays handed from the thread-per-ray traversal to k_traverse_long this pass
     C_COUNT
 };
 
@@ -106,6 +107,10 @@ struct TraverseArgs {
     double iso;
     uint32_t *block_slots, *ray_slots, *emitted, *vis_bm;
     uint32_t *work;        // persistent-kernel ray counter (zeroed per pass)
+    // long-ray hand-off (nullable): thread-per-ray lanes still walking after
+    // WC_DEFER_ITERS iterations save their iterator, queue the ray here and
+    // k_traverse_long finishes it warp per ray (passes of <= WC_DEFER_MAX_ACT rays)
+    uint32_t *long_q, *n_long;
     const uint32_t *ctl;   // control block: n_act and n_spec of the pass (Counter)
     // the kernel variant is chosen on the device from the pass's n_act:
     // warp per ray when n_act <= warp_max, thread per ray otherwise (both
@@ -187,7 +192,7 @@ struct Session : CacheStore {
     DevBuf<double> origin, dir, t_enter, t_exit, coarse_tmax, fine_tmax;
     DevBuf<uint8_t> status, exited;
     DevBuf<uint32_t> coarse_cell, fine_cell;
-    DevBuf<uint32_t> act_list[2], keep, emitted, entry_off;
+    DevBuf<uint32_t> act_list[2], keep, emitted, entry_off, long_q;
     DevBuf<uint32_t> block_slots, ray_slots;
     DevBuf<uint32_t> ent_key, ent_val, ent_ray, ent_blk;
     DevBuf<float4> rgbz;
