@@ -9,8 +9,12 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
+#include <thread>
 
 #include <cstdlib>
 #include <cxxabi.h>
@@ -3360,6 +3364,85 @@ void Session::enqueue_fb_snapshot(int64_t p) {
     fb_snapped = true;
 }
 
+// Host patch of the pixels still active when the framebuffer copy started:
+// a few persistent threads share the (ascending) patch list, so a copy
+// started two passes before the end (~60K pixels at C3) is patched in well
+// under its copy time.  Workers sleep on a condition variable between frames.
+namespace {
+struct PatchPool {
+    std::vector<std::thread> workers;
+    std::mutex m;
+    std::condition_variable cv;
+    uint64_t job = 0;
+    bool stop = false;
+    const uint4 *src = nullptr;
+    uint32_t *rgba = nullptr;
+    float *depth = nullptr;
+    int64_t n = 0;
+    int parts = 1;
+    std::atomic<int> left{0};
+
+    static void apply(const uint4 *q, int64_t b, int64_t e, uint32_t *rgba, float *depth) {
+        for (int64_t i = b; i < e; i++) rgba[q[i].x] = q[i].y;
+        for (int64_t i = b; i < e; i++) std::memcpy(depth + q[i].x, &q[i].z, 4);
+    }
+    void part(int k) { apply(src, n * k / parts, n * (k + 1) / parts, rgba, depth); }
+    void run(const uint4 *q, int64_t count, uint32_t *rgba_, float *depth_) {
+        const int want = count < 16384 ? 1 : (int)std::min<int64_t>(8, count / 8192);
+        const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+        const int p = std::max(1, std::min(want, hw / 2));
+        if (p == 1) {
+            apply(q, 0, count, rgba_, depth_);
+            return;
+        }
+        if ((int)workers.size() < p - 1) {
+            for (int k = (int)workers.size(); k < p - 1; k++)
+                workers.emplace_back([this, k] {
+                    uint64_t seen = 0;
+                    for (;;) {
+                        std::unique_lock<std::mutex> lk(m);
+                        cv.wait(lk, [&] { return stop || job != seen; });
+                        if (stop) return;
+                        seen = job;
+                        const bool mine = k + 1 < parts;
+                        lk.unlock();
+                        if (mine) {
+                            part(k + 1);
+                            left.fetch_sub(1, std::memory_order_acq_rel);
+                        }
+                    }
+                });
+        }
+        {
+            std::lock_guard<std::mutex> lk(m);
+            src = q;
+            rgba = rgba_;
+            depth = depth_;
+            n = count;
+            parts = p;
+            left.store(p - 1, std::memory_order_release);
+            job++;
+        }
+        cv.notify_all();
+        part(0);
+        while (left.load(std::memory_order_acquire) > 0) std::this_thread::yield();
+    }
+    ~PatchPool() {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto &t : workers) t.join();
+    }
+};
+PatchPool &patch_pool() {
+    static PatchPool p;
+    return p;
+}
+std::mutex g_patch_mutex;  // one frame's patch at a time (sessions on several host threads)
+}  // namespace
+
 int64_t Session::render_to_host(const CameraParams *cam, double iso_, PassStatsC *out, int64_t max_out,
                                 uint32_t *rgba_host, float *depth_host) {
     reset(cam, iso_);
@@ -3369,17 +3452,22 @@ int64_t Session::render_to_host(const CameraParams *cam, double iso_, PassStatsC
     // frame of a session has no history and copies at the end.
     fb_snap_pass = -1;
     const double copy_ms = fb_copy_ms > 0.0 ? fb_copy_ms : 8.0 * (double)n / 50e6;
+    // host patch cost per still-active pixel (ms): ~7 ns on one thread,
+    // spread over the patch pool's threads for large patches
+    const double patch_ms_per_px = 3e-6;  // (measured at C3: the patch gather, its read-back and the threaded scatter of 60K pixels ~0.2 ms)
     int64_t last = 0;
     while (last < kMaxPassLog && nact_hist[last] > 0) last++;
     double best_cost = copy_ms, tail_ms = 0.0;
     for (int64_t p = last - 2; p >= 0; p--) {
         tail_ms += pass_ms_hist[p + 1];
-        const double cost = std::max(0.0, copy_ms - tail_ms) + 5e-6 * (double)nact_hist[p + 1];
+        const double cost = std::max(0.0, copy_ms - tail_ms) + patch_ms_per_px * (double)nact_hist[p + 1];
         if (cost < best_cost) {
             best_cost = cost;
             fb_snap_pass = p;
         }
     }
+    static const char *force_snap = getenv("WAVECAST_SNAP_PASS");  // diagnostic: copy after this pass
+    if (force_snap && *force_snap) fb_snap_pass = atoi(force_snap);
     fb_rgba = rgba_host;
     fb_depth = depth_host;
     fb_snapped = false;
@@ -3410,10 +3498,9 @@ int64_t Session::render_to_host(const CameraParams *cam, double iso_, PassStatsC
     float cms = 0.0f;
     if (cudaEventElapsedTime(&cms, ev_fb, ev_fb_done) == cudaSuccess && cms > 0.0f) fb_copy_ms = cms;
     const auto t2 = std::chrono::steady_clock::now();
-    for (int64_t i = 0; i < nsnap; i++) {
-        const uint4 q = h_patch.p[i];
-        rgba_host[q.x] = q.y;
-        std::memcpy(depth_host + q.x, &q.z, 4);
+    if (nsnap > 0) {
+        std::lock_guard<std::mutex> lk(g_patch_mutex);
+        patch_pool().run(h_patch.p, nsnap, rgba_host, depth_host);
     }
     static const bool trace = getenv("WAVECAST_TRACE") != nullptr;
     if (trace) {

@@ -305,9 +305,18 @@ class RenderSession:
 
     _MAX_STATS = 4096
 
+    def _stats_buf(self):
+        """The session's PassStatsC records buffer (allocated once: a fresh
+        4096-record array per frame costs ~0.1 ms of host time)."""
+        buf = getattr(self, "_sbuf", None)
+        if buf is None:
+            buf = (_lib.PassStatsC * self._MAX_STATS)()
+            self._sbuf = buf
+        return buf
+
     def run(self) -> list[PassStats]:
         """All remaining passes (render, engine.py:385-401)."""
-        buf = (_lib.PassStatsC * self._MAX_STATS)()
+        buf = self._stats_buf()
         k = C.c_int64()
         _lib.call("wc_session_run", self._h, buf, self._MAX_STATS, C.byref(k))
         return self._frame_stats(buf, k.value)
@@ -315,13 +324,21 @@ class RenderSession:
     def _frame_stats(self, buf, k: int) -> list[PassStats]:
         """PassStats of a frame; the C records (with evicted / n_entries) stay in last_frame_c."""
         k = min(int(k), self._MAX_STATS)
-        self.last_frame_c = [{f: getattr(buf[i], f) for f, _ in _lib.PassStatsC._fields_} for i in range(k)]
-        return [_stats_from_c(buf[i]) for i in range(k)]
+        recs = (_lib.PassStatsC * k)()  # a copy: the records buffer is reused by the next frame
+        C.memmove(recs, buf, C.sizeof(_lib.PassStatsC) * k)
+        self._last_recs = recs
+        return [_stats_from_c(r) for r in recs]
+
+    @property
+    def last_frame_c(self) -> list[dict]:
+        """The last frame's C records as dicts (PassStats fields + evicted / n_entries)."""
+        recs = getattr(self, "_last_recs", None) or []
+        return [{f: getattr(r, f) for f, _ in _lib.PassStatsC._fields_} for r in recs]
 
     def render_frame(self, cam: Camera | None, iso: float) -> list[PassStats]:
         """reset(cam, iso) + run() in a single C call (no Python inside the frame)."""
         cam_c = cam.to_c(self.w, self.h) if cam is not None else None
-        buf = (_lib.PassStatsC * self._MAX_STATS)()
+        buf = self._stats_buf()
         k = C.c_int64()
         _lib.call("wc_session_render", self._h, None if cam_c is None else C.byref(cam_c), float(iso), buf,
                   self._MAX_STATS, C.byref(k))
@@ -352,7 +369,7 @@ class RenderSession:
         """render_frame + the framebuffer in (pinned) host memory, most of the
         copy overlapped with the frame's last passes.  -> (stats, rgba, depth)."""
         cam_c = cam.to_c(self.w, self.h) if cam is not None else None
-        buf = (_lib.PassStatsC * self._MAX_STATS)()
+        buf = self._stats_buf()
         k = C.c_int64()
         base = _lib.pinned_pool.get(8 * self.n)
         rgba = base[:4 * self.n].reshape(self.n, 4)

@@ -11,6 +11,7 @@ per-pixel rays, slab clipping and iterator seeding run on the GPU
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 from dataclasses import dataclass
 
@@ -61,7 +62,11 @@ class Camera:
         return look, right, np.cross(right, look)
 
     def to_c(self, w: int, h: int) -> "_lib.CameraC":
-        """wc_camera for the C ABI: basis + tan_half exactly as the reference."""
+        """wc_camera for the C ABI: basis + tan_half exactly as the reference.
+        (The camera is frozen: its record is built once per image size.)"""
+        return _camera_c(self, int(w), int(h))
+
+    def _to_c(self, w: int, h: int) -> "_lib.CameraC":
         look, right, up_v = self.basis()
         c = _lib.CameraC()
         c.eye[:] = [float(v) for v in self.eye]
@@ -72,6 +77,11 @@ class Camera:
         c.img_w = int(w)
         c.img_h = int(h)
         return c
+
+
+@functools.lru_cache(maxsize=256)
+def _camera_c(cam: Camera, w: int, h: int) -> "_lib.CameraC":
+    return cam._to_c(w, h)
 
 
 def fine_dims(dims):
