@@ -2540,6 +2540,29 @@ __global__ void k_gather_patch(const uint32_t *ctl, const uint32_t *snap, const 
     }
 }
 
+// The same patch written by the GPU straight into the host framebuffer
+// (pinned, device-mapped), after the bulk copy has landed.
+__global__ void k_patch_host(const uint32_t *ctl, const uint32_t *snap, const uint32_t *rgba, const float *depth,
+                             uint32_t *h_rgba, float *h_depth) {
+    pdl_wait();
+    const int64_t n = ctl[C_NSNAP];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = snap[i];
+        h_rgba[r] = rgba[r];
+        h_depth[r] = depth[r];
+    }
+}
+
+// device address of a pinned host buffer (nullptr: pageable / not mapped)
+static void *mapped_device_ptr(void *host) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 // ------------------------------------------------------------------ session
 
 static int bits_for(uint64_t max_value) {
@@ -3454,7 +3477,7 @@ int64_t Session::render_to_host(const CameraParams *cam, double iso_, PassStatsC
     const double copy_ms = fb_copy_ms > 0.0 ? fb_copy_ms : 8.0 * (double)n / 50e6;
     // host patch cost per still-active pixel (ms): ~7 ns on one thread,
     // spread over the patch pool's threads for large patches
-    const double patch_ms_per_px = 3e-6;  // (measured at C3: the patch gather, its read-back and the threaded scatter of 60K pixels ~0.2 ms)
+    const double patch_ms_per_px = zero_copy_patch ? 1e-6 : 3e-6;  // (measured at C3: the patch gather, its read-back and the threaded scatter of 60K pixels ~0.2 ms)
     int64_t last = 0;
     while (last < kMaxPassLog && nact_hist[last] > 0) last++;
     double best_cost = copy_ms, tail_ms = 0.0;
@@ -3487,18 +3510,31 @@ int64_t Session::render_to_host(const CameraParams *cam, double iso_, PassStatsC
         return k;
     }
     const int64_t nsnap = h_counters.p[C_NSNAP];  // read with the frame's last counters
+    // pinned (device-mapped) host buffers: the GPU writes the patch itself
+    // once the bulk copy has landed; else gather, read back, patch on the host
+    uint32_t *d_hrgba = zero_copy_patch ? static_cast<uint32_t *>(mapped_device_ptr(rgba_host)) : nullptr;
+    float *d_hdepth = d_hrgba ? static_cast<float *>(mapped_device_ptr(depth_host)) : nullptr;
+    const bool zc = d_hrgba && d_hdepth;
     if (nsnap > 0) {
-        launch_pdl(k_gather_patch, grid_for(nsnap, 256), 256, 0, st, counters.p, snap_list.p, rgba.p, depth.p, patch.p);
-        WC_LAUNCH_CHECK();
-        h_patch.ensure_host(nsnap);
-        WC_CUDA(cudaMemcpyAsync(h_patch.p, patch.p, sizeof(uint4) * nsnap, cudaMemcpyDeviceToHost, st));
+        if (zc) {
+            WC_CUDA(cudaStreamWaitEvent(st, ev_fb_done, 0));
+            launch_pdl(k_patch_host, grid_for(nsnap, 256), 256, 0, st, counters.p, snap_list.p, rgba.p, depth.p, d_hrgba,
+                       d_hdepth);
+            WC_LAUNCH_CHECK();
+        } else {
+            launch_pdl(k_gather_patch, grid_for(nsnap, 256), 256, 0, st, counters.p, snap_list.p, rgba.p, depth.p,
+                       patch.p);
+            WC_LAUNCH_CHECK();
+            h_patch.ensure_host(nsnap);
+            WC_CUDA(cudaMemcpyAsync(h_patch.p, patch.p, sizeof(uint4) * nsnap, cudaMemcpyDeviceToHost, st));
+        }
     }
     WC_CUDA(cudaStreamSynchronize(st));
     WC_CUDA(cudaEventSynchronize(ev_fb_done));  // the bulk copy has landed before it is patched
     float cms = 0.0f;
     if (cudaEventElapsedTime(&cms, ev_fb, ev_fb_done) == cudaSuccess && cms > 0.0f) fb_copy_ms = cms;
     const auto t2 = std::chrono::steady_clock::now();
-    if (nsnap > 0) {
+    if (nsnap > 0 && !zc) {
         std::lock_guard<std::mutex> lk(g_patch_mutex);
         patch_pool().run(h_patch.p, nsnap, rgba_host, depth_host);
     }

@@ -322,6 +322,9 @@ struct Session : CacheStore {
     void ensure_copy_stream();
     DevBuf<uint4> patch;
     PinnedBuf<uint4> h_patch;
+    // render_to_host patches pinned host framebuffers from the GPU (zero-copy
+    // writes); WAVECAST_HOST_PATCH=1 patches on the host instead
+    bool zero_copy_patch = getenv("WAVECAST_HOST_PATCH") == nullptr;
 };
 
 // Finished tiles into the frame (multi-GPU gather): for every
