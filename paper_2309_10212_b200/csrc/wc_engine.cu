@@ -3324,6 +3324,15 @@ int64_t Session::run_frame(PassStatsC *out, int64_t max_out) {
             launch_pass(p);
             if (p == fb_snap_pass && fb_rgba) enqueue_fb_snapshot(p);
         }
+        // render_to_host's zero-copy patch rides behind every batch (it writes
+        // final values only, so an early one is merely redundant): the batch
+        // that turns out to be the last needs no second round trip
+        if (fb_snapped && fb_patch_rgba) {
+            WC_CUDA(cudaStreamWaitEvent(st, ev_fb_done, 0));
+            launch_pdl(k_patch_host, grid_for(n, 256), 256, 0, st, counters.p, snap_list.p, rgba.p, depth.p,
+                       fb_patch_rgba, fb_patch_depth);
+            WC_LAUNCH_CHECK();
+        }
         WC_CUDA(cudaMemcpyAsync(h_plog.p, plog.p, 4 * L_COUNT * std::min<int64_t>(p0 + batch, kMaxPassLog),
                                 cudaMemcpyDeviceToHost, st));
         read_counters(0, C_COUNT);
@@ -3494,34 +3503,36 @@ int64_t Session::render_to_host(const CameraParams *cam, double iso_, PassStatsC
     fb_rgba = rgba_host;
     fb_depth = depth_host;
     fb_snapped = false;
+    // pinned (device-mapped) host buffers: the GPU writes the patch itself
+    // once the bulk copy has landed; else gather, read back, patch on the host
+    fb_patch_rgba = zero_copy_patch ? static_cast<uint32_t *>(mapped_device_ptr(rgba_host)) : nullptr;
+    fb_patch_depth = fb_patch_rgba ? static_cast<float *>(mapped_device_ptr(depth_host)) : nullptr;
+    if (!fb_patch_depth) fb_patch_rgba = nullptr;
     int64_t k = 0;
     const auto t0 = std::chrono::steady_clock::now();
     try {
         k = run_frame(out, max_out);
     } catch (...) {
         fb_rgba = nullptr;
+        fb_patch_rgba = nullptr;
+        fb_patch_depth = nullptr;
         if (st_copy) cudaStreamSynchronize(st_copy);
         throw;
     }
     fb_rgba = nullptr;
     fb_depth = nullptr;
     if (!fb_snapped) {  // no snapshot this frame: the whole framebuffer now
+        fb_patch_rgba = nullptr;
+        fb_patch_depth = nullptr;
         download_framebuffer(reinterpret_cast<uint8_t *>(rgba_host), depth_host);
         return k;
     }
     const int64_t nsnap = h_counters.p[C_NSNAP];  // read with the frame's last counters
-    // pinned (device-mapped) host buffers: the GPU writes the patch itself
-    // once the bulk copy has landed; else gather, read back, patch on the host
-    uint32_t *d_hrgba = zero_copy_patch ? static_cast<uint32_t *>(mapped_device_ptr(rgba_host)) : nullptr;
-    float *d_hdepth = d_hrgba ? static_cast<float *>(mapped_device_ptr(depth_host)) : nullptr;
-    const bool zc = d_hrgba && d_hdepth;
+    const bool zc = fb_patch_rgba != nullptr;  // patched by the GPU behind the last batch (run_frame)
+    fb_patch_rgba = nullptr;
+    fb_patch_depth = nullptr;
     if (nsnap > 0) {
-        if (zc) {
-            WC_CUDA(cudaStreamWaitEvent(st, ev_fb_done, 0));
-            launch_pdl(k_patch_host, grid_for(nsnap, 256), 256, 0, st, counters.p, snap_list.p, rgba.p, depth.p, d_hrgba,
-                       d_hdepth);
-            WC_LAUNCH_CHECK();
-        } else {
+        if (!zc) {
             launch_pdl(k_gather_patch, grid_for(nsnap, 256), 256, 0, st, counters.p, snap_list.p, rgba.p, depth.p,
                        patch.p);
             WC_LAUNCH_CHECK();

@@ -325,6 +325,8 @@ struct Session : CacheStore {
     // render_to_host patches pinned host framebuffers from the GPU (zero-copy
     // writes); WAVECAST_HOST_PATCH=1 patches on the host instead
     bool zero_copy_patch = getenv("WAVECAST_HOST_PATCH") == nullptr;
+    uint32_t *fb_patch_rgba = nullptr;  // device addresses of this frame's mapped host framebuffer
+    float *fb_patch_depth = nullptr;
 };
 
 // Finished tiles into the frame (multi-GPU gather): for every
