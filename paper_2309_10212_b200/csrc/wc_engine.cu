@@ -61,6 +61,10 @@
 #ifndef WC_TRAV_DEFER
 #define WC_TRAV_DEFER 1
 #endif
+// mark_blocks as one launch (mark_extract) when a bitmap word never straddles an x-row
+#ifndef WC_MARK_FUSED
+#define WC_MARK_FUSED 1
+#endif
 #ifndef WC_DEFER_ITERS
 #define WC_DEFER_ITERS 12
 #endif
@@ -3064,9 +3068,17 @@ void Session::enqueue_pass(int64_t p) {
     scan_exclusive_dev(LoadU32{emitted.p}, ctl + C_NACT, n, entry_off.p, ctl + C_NENT, partials.p, st);
     // visible ids (ascending) + active marking, from the maintained
     // summaries: the cost follows the non-zero bitmap words
-    bitmap_extract_dense(vis_bm.p, nwords, vis_word_off.p, visible_ids.p, ctl + C_NVIS, false, partials.p, st);
-    launch_mark_active(visible_ids.p, ctl + C_NVIS, vis_bm.p, vol->bdx, vol->bdy, vol->bdz, n, act_bm.p, st);
-    bitmap_extract_dense(act_bm.p, nwords, nullptr, active_ids.p, ctl + C_NACTB, true, partials.p, st);  // clears act_bm
+#if WC_MARK_FUSED
+    if (vol->bdx % 32 == 0) {  // one launch: visible ids, ranks and active ids from the visibility bitmap
+        mark_extract(vis_bm.p, nwords, vol->bdx / 32, vol->bdy, vol->bdz, vis_word_off.p, visible_ids.p, ctl + C_NVIS,
+                     active_ids.p, ctl + C_NACTB, partials.p, st);
+    } else
+#endif
+    {
+        bitmap_extract_dense(vis_bm.p, nwords, vis_word_off.p, visible_ids.p, ctl + C_NVIS, false, partials.p, st);
+        launch_mark_active(visible_ids.p, ctl + C_NVIS, vis_bm.p, vol->bdx, vol->bdy, vol->bdz, n, act_bm.p, st);
+        bitmap_extract_dense(act_bm.p, nwords, nullptr, active_ids.p, ctl + C_NACTB, true, partials.p, st);  // clears act_bm
+    }
     // cache.ensure_resident (cache.py:66-111), sized on the device
     const int64_t nmax = active_ids.n - 1;  // upper bound of the active-block count
     enqueue_lookup(ctl, active_ids.p, nmax, stamp, vol->n_blocks, partials.p, st);

@@ -227,6 +227,185 @@ void bitmap_extract_dense(uint32_t *bm, int64_t nwords, uint32_t *word_offsets, 
     WC_LAUNCH_CHECK();
 }
 
+#ifndef WC_MARK_Q16
+#define WC_MARK_Q16 2  // words per thread / 4 (measured: 2 beats 4 and 1 over C3, C2 at max_spec 1 and an 8-way share)
+#endif
+constexpr int kMarkQ16 = WC_MARK_Q16;
+template <int Q>
+__global__ void __launch_bounds__(256, WC_DENSE_MIN_CTAS)
+    k_mark_extract(const uint32_t *__restrict__ vis, int64_t nwords, int q16, int wx_words, int bdy, int bdz,
+                   uint32_t *__restrict__ vis_word_off, uint32_t *__restrict__ vis_ids, uint32_t *d_nvis,
+                   uint32_t *__restrict__ act_ids, uint32_t *d_nact, uint64_t *scratch, ScanEpoch ep) {
+    pdl_wait();
+    __shared__ uint32_t swv[32], swa[32], slb[64];
+    __shared__ uint32_t s_exv, s_exa, s_ticket;
+    const uint32_t epoch = resolve_epoch(ep);
+    const int64_t chunk = 256LL * 4 * q16;
+    const int64_t ntiles = (nwords - 1) / chunk + 1;
+    const int64_t last = ntiles - 1;
+    bool lt = false;
+    uint32_t tk = 0;
+    if (threadIdx.x == 0) tk = take_ticket(scratch, lt);
+    uint32_t V[4 * Q], A[4 * Q];
+    auto load_own = [&](int64_t tt) {
+        const int64_t wb = tt * chunk + (int64_t)threadIdx.x * 4 * q16;
+#pragma unroll
+        for (int j = 0; j < Q; j++) {
+            const int64_t w = wb + 4 * j;
+            uint4 q = make_uint4(0u, 0u, 0u, 0u);
+            if (j < q16) {
+                if (w + 4 <= nwords) {
+                    q = *reinterpret_cast<const uint4 *>(vis + w);
+                } else {
+                    if (w < nwords) q.x = vis[w];
+                    if (w + 1 < nwords) q.y = vis[w + 1];
+                    if (w + 2 < nwords) q.z = vis[w + 2];
+                }
+            }
+            V[4 * j] = q.x, V[4 * j + 1] = q.y, V[4 * j + 2] = q.z, V[4 * j + 3] = q.w;
+        }
+    };
+    load_own(blockIdx.x);  // speculative: the tile of blockIdx.x while the ticket is in flight
+    if (threadIdx.x == 0) s_ticket = tk;
+    __syncthreads();
+    const int64_t t = s_ticket;
+    if (t != (int64_t)blockIdx.x) load_own(t);
+    const int64_t w0 = t * chunk + (int64_t)threadIdx.x * 4 * q16;
+    const int nw = 4 * q16;  // this thread's words [w0, w0 + nw)
+    const int64_t plane = (int64_t)wx_words * bdy;
+    const bool aligned4 = (wx_words & 3) == 0 && (plane & 3) == 0;
+    // row coordinates of each word (bitmasks over the thread's words)
+    uint32_t m_wx = 0, m_by = 0, m_bz = 0;  // bit k: word k has x-word > 0 / y > 0 / z > 0
+    {
+        int64_t wx = w0 % wx_words, row = w0 / wx_words;
+        int64_t by = row % bdy, bz = row / bdy;
+#pragma unroll
+        for (int k = 0; k < 4 * Q; k++) {
+            m_wx |= (uint32_t)(wx > 0) << k;
+            m_by |= (uint32_t)(by > 0) << k;
+            m_bz |= (uint32_t)(bz > 0) << k;
+            if (++wx == wx_words) {  // next x-row
+                wx = 0;
+                if (++by == bdy) {
+                    by = 0;
+                    ++bz;
+                }
+            }
+        }
+    }
+    // x-dilation of a run of words S[1..nw] whose predecessor is S[0]
+    auto load_run = [&](int64_t first, uint32_t S[4 * Q + 1]) {  // S[i] = vis[first - 1 + i]
+        const bool vec = aligned4 && first >= 0 && first + 4 * Q <= nwords;
+        S[0] = (first - 1 >= 0 && first - 1 < nwords) ? __ldg(vis + first - 1) : 0u;
+        if (vec) {
+#pragma unroll
+            for (int j = 0; j < Q; j++) {
+                const uint4 q = j < q16 ? __ldg(reinterpret_cast<const uint4 *>(vis + first + 4 * j)) : make_uint4(0, 0, 0, 0);
+                S[1 + 4 * j] = q.x, S[2 + 4 * j] = q.y, S[3 + 4 * j] = q.z, S[4 + 4 * j] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4 * Q; k++) {
+                const int64_t w = first + k;
+                S[1 + k] = (k < nw && w >= 0 && w < nwords) ? __ldg(vis + w) : 0u;
+            }
+        }
+    };
+    auto dilate = [&](const uint32_t S[4 * Q + 1], uint32_t gate) {
+#pragma unroll
+        for (int k = 0; k < 4 * Q; k++)
+            if ((gate >> k) & 1u) A[k] |= S[k + 1] | (S[k + 1] << 1) | (((m_wx >> k) & 1u) ? S[k] >> 31 : 0u);
+    };
+    {
+        const uint32_t own = (1u << nw) - 1u;
+        uint32_t S[4 * Q + 1];
+        S[0] = (w0 - 1 >= 0 && w0 - 1 < nwords) ? __ldg(vis + w0 - 1) : 0u;
+#pragma unroll
+        for (int k = 0; k < 4 * Q; k++) {
+            S[k + 1] = V[k];
+            A[k] = 0u;
+        }
+        dilate(S, own);
+        if (m_by & own) {
+            load_run(w0 - wx_words, S);
+            dilate(S, m_by & own);
+        }
+        if (m_bz & own) {
+            load_run(w0 - plane, S);
+            dilate(S, m_bz & own);
+            if (m_by & m_bz & own) {
+                load_run(w0 - plane - wx_words, S);
+                dilate(S, m_by & m_bz & own);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4 * Q; k++)
+            if (w0 + k >= nwords) A[k] = 0u;
+    }
+    (void)bdz;
+    uint32_t cv = 0, ca = 0;
+#pragma unroll
+    for (int k = 0; k < 4 * Q; k++) {
+        cv += __popc(V[k]);
+        ca += __popc(A[k]);
+    }
+    uint32_t aggv, agga;
+    uint32_t prev_v = block_exclusive_scan(cv, swv, &aggv);
+    uint32_t prev_a = block_exclusive_scan(ca, swa, &agga);
+    uint64_t *status_v = tile_status(scratch), *status_a = tile_status(scratch) + ntiles;
+    if (threadIdx.x < 32) {
+        const uint32_t e = tile_lookback(t, aggv, status_v, epoch);
+        if (threadIdx.x == 0) {
+            s_exv = e;
+            if (t == last) *d_nvis = e + aggv;
+        }
+    } else if (threadIdx.x < 64) {
+        const uint32_t e = tile_lookback(t, agga, status_a, epoch);
+        if (threadIdx.x == 32) {
+            s_exa = e;
+            if (t == last) *d_nact = e + agga;
+        }
+    }
+    __syncthreads();
+    prev_v += s_exv;
+    prev_a += s_exa;
+#pragma unroll
+    for (int k = 0; k < 4 * Q; k++) {
+        uint32_t v = V[k], a = A[k];
+        const int64_t w = w0 + k;
+        if (v) {
+            vis_word_off[w] = prev_v;
+            const uint32_t base = (uint32_t)(w * 32);
+            while (v) {
+                vis_ids[prev_v++] = base + __ffs(v) - 1;
+                v &= v - 1;
+            }
+        }
+        if (a) {
+            const uint32_t base = (uint32_t)(w * 32);
+            while (a) {
+                act_ids[prev_a++] = base + __ffs(a) - 1;
+                a &= a - 1;
+            }
+        }
+    }
+}
+
+void mark_extract(const uint32_t *vis, int64_t nwords, int wx_words, int bdy, int bdz, uint32_t *vis_word_off,
+                  uint32_t *vis_ids, uint32_t *d_nvis, uint32_t *act_ids, uint32_t *d_nact, uint32_t *partials,
+                  cudaStream_t st) {
+    if (nwords <= 0) {
+        WC_CUDA(cudaMemsetAsync(d_nvis, 0, sizeof(uint32_t), st));
+        WC_CUDA(cudaMemsetAsync(d_nact, 0, sizeof(uint32_t), st));
+        return;
+    }
+    const int64_t q16 = std::min<int64_t>(kMarkQ16, std::max<int64_t>(1, ceil_div(nwords, (int64_t)num_sms() * WC_DENSE_CTAS_PER_SM * 256 * 4)));
+    const unsigned grid = (unsigned)ceil_div(nwords, 256 * 4 * q16);
+    launch_pdl(k_mark_extract<kMarkQ16>, grid, 256, 0, st, vis, nwords, (int)q16, wx_words, bdy, bdz, vis_word_off,
+               vis_ids, d_nvis, act_ids, d_nact, reinterpret_cast<uint64_t *>(partials), scan_epoch());
+    WC_LAUNCH_CHECK();
+}
+
 // summary word i -> ascending indices of its set bits (the non-zero words of
 // the bitmap), clearing the summary word
 struct SinkList {

@@ -555,6 +555,17 @@ __device__ __forceinline__ void bitmap_set(uint32_t *bm, uint32_t *summary, uint
 void bitmap_extract_dense(uint32_t *bm, int64_t nwords, uint32_t *word_offsets, uint32_t *ids, uint32_t *d_count,
                           bool clear, uint32_t *partials, cudaStream_t st);
 
+// mark_blocks in one launch (engine.py:97-118): from the visibility bitmap
+// vis (bdx % 32 == 0: a word never straddles an x-row), the ascending
+// visible ids + the rank table vis_word_off, and the ascending ids of the
+// active set -- the visible blocks and their existing +octant neighbours --
+// computed word by word from vis itself (a block is active when it or its
+// -x / -y / -z / ... neighbour is visible), so no active bitmap is built.
+// Two look-backs (visible, active) run side by side; vis is left intact.
+void mark_extract(const uint32_t *vis, int64_t nwords, int wx_words, int bdy, int bdz, uint32_t *vis_word_off,
+                  uint32_t *vis_ids, uint32_t *d_nvis, uint32_t *act_ids, uint32_t *d_nact, uint32_t *partials,
+                  cudaStream_t st);
+
 // Ascending ids of the set bits of bm -> ids, count -> *d_count, from its
 // summary (summary words [0, ceil(nwords_max / 32))):
 //   1. a scan of the summary's popcounts lists the non-zero words in order
