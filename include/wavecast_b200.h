@@ -209,8 +209,9 @@ int wc_session_set_kernel_profile(wc_session *s, int on); /* also clears */
 int wc_session_kernel_profile(const wc_session *s, char *buf, int64_t cap, int64_t *len);
 
 /* ---- per-stage views of the last pass (parity tests) */
-/* sizes[8] = slots_used, n_visible, n_active_blocks, n_entries, n_spec,
- *            n_active_before, cache_capacity, cache_physical */
+/* sizes[9] = slots_used, n_visible, n_active_blocks, n_entries, n_spec,
+ *            n_active_before, cache_capacity, cache_physical,
+ *            rays the traversal handed to its warp-per-ray long-ray pass */
 int wc_session_sizes(const wc_session *s, int64_t *sizes);
 /* RaySoA fields (traversal.py:76-91), each nullable */
 int wc_session_rays(const wc_session *s, double *dir, double *t_enter, double *t_exit, uint8_t *status,

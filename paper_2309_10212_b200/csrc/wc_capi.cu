@@ -653,6 +653,7 @@ int wc_session_sizes(const wc_session *s, int64_t *sizes) {
     sizes[5] = S.last_slots_used / (S.last_n_spec ? S.last_n_spec : 1);
     sizes[6] = S.cap;
     sizes[7] = S.phys;
+    sizes[8] = S.last_nlong;
     WC_API_END
 }
 

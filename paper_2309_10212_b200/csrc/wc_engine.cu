@@ -2497,6 +2497,7 @@ __device__ __forceinline__ void pass_end(uint32_t *ctl, uint32_t *row, int64_t n
     row[L_NITEMS] = ctl[C_NITEMS];
     row[L_PHYS] = ctl[C_PHYS];
     row[L_HW] = ctl[C_HW_NEXT];
+    row[L_NLONG] = ctl[C_NLONG];
     ctl[C_WORK] = 0;  // the next pass's traversal work counter and raytrace list start empty
     ctl[C_NLONG] = 0;
     ctl[C_NITEMS] = 0;
@@ -3292,6 +3293,7 @@ void Session::collect_pass(int64_t p, PassStatsC &stats) {
     last_nvis = r[L_NVIS];
     last_nactb = r[L_NACTB];
     last_nent = r[L_NENT];
+    last_nlong = r[L_NLONG];
     cap = r[L_CAP];
     phys = r[L_PHYS];
     hw = r[L_HW];

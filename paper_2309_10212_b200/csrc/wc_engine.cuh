@@ -60,6 +60,7 @@ enum Counter : int {
 // Per-pass record written on the device by pass_end (PassStats fields).
 enum PassLog : int {
     L_NACT = 0, L_NSPEC, L_NVIS, L_NACTB, L_NMISS, L_NEVICT, L_CAP, L_NENT, L_NAFTER, L_NITEMS, L_PHYS, L_HW,
+    L_NLONG,  // rays the thread-per-ray traversal handed to k_traverse_long
     L_COUNT
 };
 
@@ -236,7 +237,7 @@ struct Session : CacheStore {
     PinnedBuf<uint32_t> h_plog;
     DevBuf<double> fparams;         // FrameParams: eye[3], iso, base colour[3] (written by k_frame_start)
     uint32_t frame_no = 0;
-    int64_t last_slots_used = 0, last_nvis = 0, last_nactb = 0, last_nent = 0;
+    int64_t last_slots_used = 0, last_nvis = 0, last_nactb = 0, last_nent = 0, last_nlong = 0;
     int64_t last_n_spec = 1;
     float last_kernel_ms = 0.0f;
     std::vector<KTime> ktime;  // WAVECAST_KTIME: per-launch events of the directly enqueued passes

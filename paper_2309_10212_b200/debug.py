@@ -18,10 +18,10 @@ UINT_MAX = 0xFFFFFFFF
 
 
 def sizes(sess: RenderSession) -> dict:
-    s = np.empty(8, dtype=np.int64)
+    s = np.empty(9, dtype=np.int64)
     _lib.call("wc_session_sizes", sess.handle, _lib.ptr(s))
     keys = ("slots_used", "n_visible", "n_active_blocks", "n_entries", "n_spec", "n_active_before", "cache_capacity",
-            "cache_physical")
+            "cache_physical", "n_handed_off")
     return {k: int(v) for k, v in zip(keys, s)}
 
 

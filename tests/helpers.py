@@ -41,7 +41,8 @@ def iso_at(vol, frac):
 
 
 def lockstep(wc, cv, ov, cam_tuple, w, h, iso, *, speculation=True, max_spec=64, cache_capacity=None,
-             pixel_ids=None, origins=None, dirs=None, internals=True, corrupt=False, group=None, frames=None):
+             pixel_ids=None, origins=None, dirs=None, internals=True, corrupt=False, group=None, frames=None,
+             probe=None):
     """Run the GPU session and the oracle session pass by pass; assert every
     per-pass stat, per-stage buffer and the final framebuffer are identical.
 
@@ -51,7 +52,8 @@ def lockstep(wc, cv, ov, cam_tuple, w, h, iso, *, speculation=True, max_spec=64,
     grouped ones are compared (rgbz per entry id is order-independent).
     frames: extra [(cam_tuple, iso)] rendered after the first on the same
     session (wc_session_reset: the pass graphs captured by the first frame are
-    replayed), each against a fresh oracle session."""
+    replayed), each against a fresh oracle session.
+    probe: called as probe(session, pass_index) after each compared pass."""
     if group is None:
         group = internals
     cam = wc_camera(wc, cam_tuple) if cam_tuple is not None else None
@@ -91,6 +93,8 @@ def lockstep(wc, cv, ov, cam_tuple, w, h, iso, *, speculation=True, max_spec=64,
             assert sess.last_c_stats.evicted == rs["evicted"], f"frame {fi} pass {n_pass} evicted"
             if internals:
                 compare_pass(sess, os_, n_pass, grouped=group)
+            if probe is not None:
+                probe(sess, n_pass)
             stats.append(gs)
             n_pass += 1
         rgba, depth = sess.read()

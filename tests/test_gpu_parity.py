@@ -110,6 +110,22 @@ def test_render_lockstep_vs_oracle(wc, scene):
              cache_capacity=cache)
 
 
+def test_long_ray_handoff_lockstep(wc):
+    """Passes of <= 150K short rays (n_spec < 16) hand rays still walking
+    after 12 iterations to the warp-per-ray k_traverse_long: an isovalue near
+    the top of the range leaves long empty walks, so the hand-off runs, and
+    every pass still equals the oracle's bit for bit."""
+    from paper_2309_10212_b200 import debug
+
+    vol = host_volume("value_noise", 256, seed=3)
+    cv = wc.compress_volume(vol, 12)
+    ov = oracle_volume(cv)
+    handed = []
+    lockstep(wc, cv, ov, orbit(cv.dims, 0.15), 256, 256, iso_at(vol, 0.93), max_spec=8,
+             probe=lambda sess, p: handed.append(debug.sizes(sess)["n_handed_off"]))
+    assert sum(handed) > 0, f"no ray was handed off ({handed})"
+
+
 @pytest.mark.parametrize("bound", ["fine_min", "fine_max"])
 def test_iso_on_a_grid_bound(wc, bound):
     # iso exactly equal to a float64 grid bound: the 16-bit screening bitmap
