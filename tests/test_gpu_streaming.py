@@ -79,3 +79,34 @@ def test_streamed_snapshots_many_passes_held(wc):
         assert np.array_equal(fb.depth.reshape(-1).view(np.uint32), ref[k][1].view(np.uint32)), k
         snap = fb.snapshot()
         assert np.array_equal(snap.rgba, fb.rgba) and snap.completeness == fb.completeness
+
+
+@pytest.mark.parametrize("host_patch", [False, True])
+def test_render_host_readback_equals_oracle(wc, monkeypatch, host_patch):
+    """render()'s read-back: the bulk copy starts before the last passes and
+    the pixels still active then are patched -- by the GPU straight into the
+    pinned host framebuffer, or (WAVECAST_HOST_PATCH=1, and for pageable
+    buffers) on the host.  Frames after the first (which choose the copy's
+    pass from the previous frame's pass times) equal the oracle's."""
+    if host_patch:
+        monkeypatch.setenv("WAVECAST_HOST_PATCH", "1")
+    else:
+        monkeypatch.delenv("WAVECAST_HOST_PATCH", raising=False)
+    vol = host_volume("value_noise", 96, seed=4)
+    cv = wc.compress_volume(vol, 16)
+    grids = wc.build_grids(cv)
+    ov = oracle_volume(cv)
+    w, h = 320, 240
+    opts = wc.RenderOptions(width=w, height=h)
+    for k, frac in enumerate((0.1, 0.1, 0.35, 0.6)):
+        cam_t = orbit(cv.dims, frac)
+        cam = wc_camera(wc, cam_t)
+        iso = iso_at(vol, 0.45 + 0.05 * k)
+        if k == 0:
+            sess = wc.RenderSession(cv, grids, cam, iso, opts)  # a session of its own (the env is read at creation)
+        stats, rgba, depth = sess.render_frame_host(cam, iso)
+        o, d = orc.camera_rays(cam_t, w, h)
+        orgba, odepth, _ = orc.render(ov, o, d, w, h, iso)
+        assert np.array_equal(rgba.reshape(-1, 4), orgba), (host_patch, k)
+        assert np.array_equal(depth.reshape(-1).view(np.uint32), odepth.view(np.uint32)), (host_patch, k)
+    sess.close()
