@@ -63,7 +63,11 @@ def parse():
     p.add_argument("--max-spec", type=int, default=64)
     p.add_argument("--cache-slots", type=int, default=0, help="LRU budget (0 = reference initial_capacity)")
     p.add_argument("--tile", type=int, default=32)
-    p.add_argument("--force-shard", action="store_true", help="tile sessions + NCCL gather even on one GPU")
+    p.add_argument("--force-shard", action="store_true",
+                   help="tile sessions + the multi-GPU frame assembly even on one GPU")
+    p.add_argument("--assembly", choices=["peer", "nccl"], default="peer",
+                   help="multi-GPU frame assembly: final pixels written into rank 0's frame over peer memory as "
+                        "rays terminate (default), or an NCCL gather to rank 0 + device scatter")
     p.add_argument("--rank-share", type=int, default=0,
                    help="diagnostic: time one rank's session of an N-GPU tile split (rank 0 of N) on this GPU")
     p.add_argument("--group", action="store_true", help="sort entries by block before the raytrace "
@@ -92,7 +96,9 @@ def config_json(args, wl, n_gpus, extra=None):
         "camera": "orbit step 0 (eye = centre + (0, 0, 1.8*max(dims))), fov 45",
         "speculation": True,
         "max_spec": args.max_spec,
-        "parallelism": f"image tiles {args.tile}x{args.tile} dealt round-robin over {n_gpus} GPU(s)",
+        "parallelism": f"image tiles {args.tile}x{args.tile} dealt round-robin over {n_gpus} GPU(s)"
+                       + (f"; frame assembly: {'peer-memory writes into rank 0' if args.assembly == 'peer' else 'NCCL gather'}"
+                          if n_gpus > 1 or args.force_shard else ""),
         "l2": "flushed between timed frames (512 MB device write, outside the frame timing)",
     }
     if extra:
@@ -398,7 +404,7 @@ def run_b200(args):
         t = time.perf_counter()
         if sharded:
             fb, _ = wdist.render_sharded(cv, grids, cam, iso, opts, tile=args.tile,
-                                         split=True if args.force_shard else None)
+                                         split=True if args.force_shard else None, assembly=args.assembly)
         else:
             fb, _ = wc.render(cv, grids, cam, iso, opts)
         barrier()

@@ -27,6 +27,7 @@ extern "C" {
 typedef struct wc_volume wc_volume;
 typedef struct wc_session wc_session;
 typedef struct wc_cache wc_cache;
+typedef struct wc_frame_target wc_frame_target;
 
 /* engine.py:66-77 PassStats (+ evicted, n_entries, n_active_after) */
 typedef struct {
@@ -182,6 +183,21 @@ int wc_session_framebuffer_packed(wc_session *s, void *dst_dev, int64_t stride_w
  * pixel.  Writes frame rgba / depth (DEVICE, u32 per pixel) on `stream`. */
 int wc_scatter_pixels(const void *packed_dev, int64_t stride_words, const void *pixel_ids_dev, int64_t n,
                       void *rgba_dev, void *depth_dev, void *stream);
+/* Multi-GPU frame assembly over peer memory (the fused
+ * option): rank 0 creates a full-frame target (RGBA8 + depth, npix pixels) on
+ * its GPU and exports two CUDA IPC handles (128 bytes); every other rank opens
+ * them.  A session given a target writes each pixel's final value into it the
+ * moment the ray terminates (at reset for rays that miss the volume, in the
+ * pass's composite for the others), so the frame assembles over NVLink while
+ * the remaining passes run and no gather is needed.  Once every rank's frame
+ * has completed, rank 0 downloads the target. */
+int wc_frame_target_create(int64_t npix, wc_frame_target **out);
+int wc_frame_target_ipc_handles(const wc_frame_target *t, void *handles);
+int wc_frame_target_open(const void *handles, int64_t npix, wc_frame_target **out);
+int wc_frame_target_download(const wc_frame_target *t, uint32_t *rgba_host, float *depth_host);
+int wc_frame_target_destroy(wc_frame_target *t);
+/* The session's final pixels also go to `t` (NULL: stop); camera sessions. */
+int wc_session_set_frame_target(wc_session *s, const wc_frame_target *t);
 /* Same into caller-owned DEVICE buffers (for NCCL tile gathers). */
 int wc_session_framebuffer_device(wc_session *s, void *rgba_dev, void *depth_dev);
 /* Device time of the last pass (CUDA events on the session stream). */

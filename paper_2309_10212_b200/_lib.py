@@ -110,6 +110,12 @@ _SIGS = {
     "wc_session_stream": (_i32, [_vp, _vp]),
     "wc_session_framebuffer_packed": (_i32, [_vp, _vp, _i64]),
     "wc_scatter_pixels": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),
+    "wc_frame_target_create": (_i32, [_i64, _vp]),
+    "wc_frame_target_ipc_handles": (_i32, [_vp, _vp]),
+    "wc_frame_target_open": (_i32, [_vp, _i64, _vp]),
+    "wc_frame_target_download": (_i32, [_vp, _vp, _vp]),
+    "wc_frame_target_destroy": (_i32, [_vp]),
+    "wc_session_set_frame_target": (_i32, [_vp, _vp]),
     "wc_session_kernel_profile": (_i32, [_vp, _vp, _i64, _vp]),
     "wc_session_snapshot_wait": (_i32, [_vp, _i64]),
     "wc_session_last_pass_ms": (_i32, [_vp, _vp]),

@@ -21,6 +21,9 @@ struct wc_session {
 struct wc_cache {
     wc::StageCache *c = nullptr;
 };
+struct wc_frame_target {
+    wc::FrameTarget t;
+};
 
 static thread_local std::string g_err;
 
@@ -565,6 +568,59 @@ int wc_session_mask_buffers(wc_session *s, int64_t parts, void **coarse_bm, void
 int wc_session_sync(wc_session *s) {
     WC_API_BEGIN
     s->s->sync_all();
+    WC_API_END
+}
+
+int wc_frame_target_create(int64_t npix, wc_frame_target **out) {
+    WC_API_BEGIN
+    WC_REQUIRE(npix > 0, wc::UsageError, "frame target needs pixels");
+    auto *t = new wc_frame_target();
+    try {
+        t->t.create(npix);
+    } catch (...) {
+        delete t;
+        throw;
+    }
+    *out = t;
+    WC_API_END
+}
+
+int wc_frame_target_ipc_handles(const wc_frame_target *t, void *handles) {
+    WC_API_BEGIN
+    WC_REQUIRE(!t->t.opened, wc::UsageError, "IPC handles come from the target's owner");
+    t->t.ipc_handles(handles);
+    WC_API_END
+}
+
+int wc_frame_target_open(const void *handles, int64_t npix, wc_frame_target **out) {
+    WC_API_BEGIN
+    auto *t = new wc_frame_target();
+    try {
+        t->t.open(handles, npix);
+    } catch (...) {
+        delete t;
+        throw;
+    }
+    *out = t;
+    WC_API_END
+}
+
+int wc_frame_target_download(const wc_frame_target *t, uint32_t *rgba_host, float *depth_host) {
+    WC_API_BEGIN
+    WC_CUDA(cudaMemcpy(rgba_host, t->t.p_rgba, 4 * t->t.npix, cudaMemcpyDeviceToHost));
+    WC_CUDA(cudaMemcpy(depth_host, t->t.p_depth, 4 * t->t.npix, cudaMemcpyDeviceToHost));
+    WC_API_END
+}
+
+int wc_frame_target_destroy(wc_frame_target *t) {
+    WC_API_BEGIN
+    delete t;
+    WC_API_END
+}
+
+int wc_session_set_frame_target(wc_session *s, const wc_frame_target *t) {
+    WC_API_BEGIN
+    s->s->set_frame_target(t ? &t->t : nullptr);
     WC_API_END
 }
 

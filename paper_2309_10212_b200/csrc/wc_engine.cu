@@ -121,7 +121,23 @@ struct RayInitArgs {
     const double *origin_in;     // nullable: camera rays
     const double *dir_in;        // nullable: camera rays
     int nx, ny, nz;
+    const unsigned long long *target;  // nullable: the frame target's {rgba, depth} device addresses (FrameTarget)
 };
+
+// A pixel's final value into the frame target (another rank's framebuffer in
+// peer memory over NVLink, or a local one): written once, when the ray
+// terminates (init or composite), so the full frame is assembled while the
+// remaining passes run.  target[0] == 0: no target.
+__device__ __forceinline__ void target_write(const unsigned long long *target, const uint32_t *pixel_ids, uint32_t r,
+                                             uint32_t rgba, float depth) {
+    if (!target) return;
+    uint32_t *tr = reinterpret_cast<uint32_t *>(target[0]);
+    if (!tr) return;
+    float *td = reinterpret_cast<float *>(target[1]);
+    const uint32_t px = pixel_ids ? pixel_ids[r] : r;
+    tr[px] = rgba;
+    td[px] = depth;
+}
 
 // traversal.py:105-187 (from_camera + from_rays + _tmax_init) for ray r.
 __global__ void k_init_rays(RayInitArgs a, int64_t n, double *origin_out, double *dir, double *t_enter, double *t_exit,
@@ -219,6 +235,7 @@ __global__ void k_init_rays(RayInitArgs a, int64_t n, double *origin_out, double
         if (rgba) {
             rgba[r] = 0xFF000000u;  // BACKGROUND_RGBA (engine.py:29)
             depth[r] = CUDART_INF_F;
+            if (!hit) target_write(a.target, a.pixel_ids, (uint32_t)r, 0xFF000000u, CUDART_INF_F);  // final already
         }
     }
 }
@@ -2254,15 +2271,19 @@ constexpr uint32_t kWarpCompositeSpec = 8;  // n_spec from which a warp composit
 // earliest entry wins ties), then terminate (hit / exited) or keep.
 __device__ __forceinline__ void composite_ray(int64_t i, uint32_t r, float best, int64_t bk, const float4 *rgbz,
                                               const uint8_t *exited, uint8_t *status, uint32_t *rgba, float *depth,
-                                              uint32_t *keep) {
+                                              uint32_t *keep, const unsigned long long *target,
+                                              const uint32_t *pixel_ids) {
     uint32_t kp = 0;
     if (bk >= 0) {
         const float4 c = rgbz[bk];
+        const uint32_t v = rgb_u8((double)c.x) | (rgb_u8((double)c.y) << 8) | (rgb_u8((double)c.z) << 16) | 0xFF000000u;
         depth[r] = best;
-        rgba[r] = rgb_u8((double)c.x) | (rgb_u8((double)c.y) << 8) | (rgb_u8((double)c.z) << 16) | 0xFF000000u;
+        rgba[r] = v;
         status[r] = 1;
+        target_write(target, pixel_ids, r, v, best);
     } else if (exited[r] == 1) {
         status[r] = 2;
+        target_write(target, pixel_ids, r, rgba[r], depth[r]);  // the background it kept
     } else {
         kp = 1;
     }
@@ -2274,7 +2295,8 @@ __device__ __forceinline__ void composite_ray(int64_t i, uint32_t r, float best,
 // the first strict minimum in order.
 __global__ void k_composite(const uint32_t *ctl, const uint32_t *act_list, const uint32_t *emitted,
                             const uint32_t *entry_off, const float4 *rgbz, const uint8_t *exited, uint8_t *status,
-                            uint32_t *rgba, float *depth, uint32_t *keep) {
+                            uint32_t *rgba, float *depth, uint32_t *keep, const unsigned long long *target,
+                            const uint32_t *pixel_ids) {
     pdl_wait();
     const int64_t n_act = ctl[C_NACT];
     if (ctl[C_NSPEC] < kWarpCompositeSpec) {
@@ -2291,7 +2313,7 @@ __global__ void k_composite(const uint32_t *ctl, const uint32_t *act_list, const
                     bk = eo + j;
                 }
             }
-            composite_ray(i, r, best, bk, rgbz, exited, status, rgba, depth, keep);
+            composite_ray(i, r, best, bk, rgbz, exited, status, rgba, depth, keep, target, pixel_ids);
         }
         return;
     }
@@ -2319,7 +2341,7 @@ __global__ void k_composite(const uint32_t *ctl, const uint32_t *act_list, const
             }
         }
         if (lane == 0) composite_ray(i, r, best, bj != 0xFFFFFFFFu ? (int64_t)eo + bj : -1, rgbz, exited, status, rgba,
-                                     depth, keep);
+                                     depth, keep, target, pixel_ids);
     }
 }
 
@@ -2523,6 +2545,48 @@ struct PassEndEpilogue {
     }
 };
 
+// ---------------------------------------------------- frame target (peer memory)
+FrameTarget::~FrameTarget() {
+    if (opened) {
+        if (p_rgba) cudaIpcCloseMemHandle(p_rgba);
+        if (p_depth) cudaIpcCloseMemHandle(p_depth);
+    }
+}
+void FrameTarget::create(int64_t n) {
+    npix = n;
+    rgba.alloc(n);
+    depth.alloc(n);
+    p_rgba = rgba.p;
+    p_depth = depth.p;
+}
+void FrameTarget::ipc_handles(void *out) const {
+    cudaIpcMemHandle_t h[2];
+    WC_CUDA(cudaIpcGetMemHandle(&h[0], p_rgba));
+    WC_CUDA(cudaIpcGetMemHandle(&h[1], p_depth));
+    std::memcpy(out, h, sizeof(h));
+}
+void FrameTarget::open(const void *handles, int64_t n) {
+    cudaIpcMemHandle_t h[2];
+    std::memcpy(h, handles, sizeof(h));
+    npix = n;
+    void *a = nullptr, *b = nullptr;
+    WC_CUDA(cudaIpcOpenMemHandle(&a, h[0], cudaIpcMemLazyEnablePeerAccess));
+    WC_CUDA(cudaIpcOpenMemHandle(&b, h[1], cudaIpcMemLazyEnablePeerAccess));
+    p_rgba = static_cast<uint32_t *>(a);
+    p_depth = static_cast<float *>(b);
+    opened = true;
+}
+
+// The session's pixels go to `t` as they become final (nullptr: none).  The
+// addresses live in device memory, so the captured pass graphs stay valid.
+void Session::set_frame_target(const FrameTarget *t) {
+    const unsigned long long v[2] = {t ? (unsigned long long)(uintptr_t)t->p_rgba : 0ull,
+                                     t ? (unsigned long long)(uintptr_t)t->p_depth : 0ull};
+    if (t && !uniform_origin) throw UsageError("a frame target needs camera rays (pixel ids)");
+    WC_CUDA(cudaMemcpyAsync(tgt.p, v, sizeof(v), cudaMemcpyHostToDevice, st));
+    WC_CUDA(cudaStreamSynchronize(st));
+}
+
 // ---------------------------------------------------- framebuffer read-back
 
 // rays still active after the snapshot pass (their pixels may still change)
@@ -2656,6 +2720,8 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     best.alloc(n);
     plog.alloc((int64_t)kMaxPassLog * L_COUNT);
     fparams.alloc(8);
+    tgt.alloc(2);
+    WC_CUDA(cudaMemsetAsync(tgt.p, 0, 2 * sizeof(unsigned long long), st));
     h_plog.alloc((int64_t)kMaxPassLog * L_COUNT);
     reset(cam, iso_);
     precapture(kPrecapturePasses);
@@ -2726,6 +2792,7 @@ void Session::reset_part(const CameraParams *cam, double iso_, int64_t part, int
     a.nx = vol->nx;
     a.ny = vol->ny;
     a.nz = vol->nz;
+    a.target = tgt.p;
     launch_pdl(k_init_rays, grid_for(n, 256), 256, 0, st, a, n, nullptr, dir.p, t_enter.p, t_exit.p, status.p, exited.p,
                                                   coarse_cell.p, fine_cell.p, coarse_tmax.p, fine_tmax.p, rgba.p,
                                                   depth.p);
@@ -3164,7 +3231,8 @@ void Session::enqueue_pass(int64_t p) {
     // composite + compaction of the surviving rays (next pass's O_Act); the
     // device picks thread or warp per ray by the pass's n_spec
     launch_pdl(k_composite, grid_for((speculation && max_spec >= (int)kWarpCompositeSpec ? 32 : 1) * n, 256), 256, 0, st,
-               ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p, status.p, rgba.p, depth.p, keep.p);
+               ctl, alist, emitted.p, entry_off.p, rgbz.p, exited.p, status.p, rgba.p, depth.p, keep.p, tgt.p,
+               pix.p);
     WC_LAUNCH_CHECK();
     // next pass's active list; the pass record and the next pass's counts
     // (pass_end) as its epilogue

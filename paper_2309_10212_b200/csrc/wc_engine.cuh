@@ -174,6 +174,25 @@ struct CacheStore {
 //   cache: slot_values f32[phys*64], block_of_slot/last_used i32[phys],
 //          slot_of_block i32[n_blocks]
 //   framebuffer: rgba u32[N] (packed RGBA8), depth f32[N]
+// Full-frame RGBA8 + depth on one GPU that every rank's session writes its
+// final pixels into (multi-GPU frame assembly over peer memory): created
+// (and owned) by rank 0, opened by the others through CUDA IPC handles.
+struct FrameTarget {
+    DevBuf<uint32_t> rgba;
+    DevBuf<float> depth;
+    uint32_t *p_rgba = nullptr;  // device addresses in this process (own or opened)
+    float *p_depth = nullptr;
+    bool opened = false;
+    int64_t npix = 0;
+    FrameTarget() = default;
+    FrameTarget(const FrameTarget &) = delete;
+    FrameTarget &operator=(const FrameTarget &) = delete;
+    ~FrameTarget();
+    void create(int64_t n);
+    void ipc_handles(void *out) const;  // 2 x cudaIpcMemHandle_t (128 bytes)
+    void open(const void *handles, int64_t n);
+};
+
 struct Session : CacheStore {
     Volume *vol = nullptr;
     cudaStream_t st = nullptr;
@@ -236,6 +255,7 @@ struct Session : CacheStore {
     DevBuf<uint32_t> plog;          // kMaxPassLog x L_COUNT per-pass records (device)
     PinnedBuf<uint32_t> h_plog;
     DevBuf<double> fparams;         // FrameParams: eye[3], iso, base colour[3] (written by k_frame_start)
+    DevBuf<unsigned long long> tgt;  // frame target {rgba, depth} device addresses (0: none), set_frame_target
     uint32_t frame_no = 0;
     int64_t last_slots_used = 0, last_nvis = 0, last_nactb = 0, last_nent = 0, last_nlong = 0;
     int64_t last_n_spec = 1;
@@ -280,6 +300,7 @@ struct Session : CacheStore {
     // rgba words at dst[0, n), depth bits at dst[stride, stride + n) (stride
     // >= n), stream-ordered on the session stream (no host sync): the send
     // buffer of a tile gather
+    void set_frame_target(const FrameTarget *t);
     void pack_framebuffer(uint32_t *dst, int64_t stride);
 
     double reset_device_ms();  // device time of the last reset, once it has run

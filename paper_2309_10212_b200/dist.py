@@ -5,9 +5,13 @@ an interleaved subset of square tiles as one device session (its own pass
 loop, n_act and n_spec).  Because speculation never changes final pixels
 (engine.py:1-9), the stitched frame equals the single-GPU frame bit for bit.
 The exchange steps are the per-iso range tests (each rank computes a slice,
-two in-place all-gathers assemble them) and the final tile gather: every
-rank's RGBA8+depth (8 B/pixel) goes to rank 0 alone with one NCCL gather
-over NVLink, scattered into the frame on rank 0's GPU (wc_scatter_pixels).
+two in-place all-gathers assemble them) and the frame assembly: by default
+every rank's sessions write each final pixel straight into rank 0's frame
+over NVLink peer memory (FrameTarget, CUDA IPC) the moment its ray
+terminates -- the collective fused into the composite, overlapped with the
+remaining passes; alternatively every rank's RGBA8+depth (8 B/pixel) goes to
+rank 0 alone with one NCCL gather, scattered into the frame on rank 0's GPU
+(wc_scatter_pixels).
 All of it is ordered on the session's CUDA stream, so a frame has no host
 synchronisation besides the pass loop's own (``torch.distributed``; gloo on
 CPU for tests).
@@ -191,13 +195,97 @@ def render_frame_split(sess, cam, iso, group=None, split=None):
     return sess.run()
 
 
+class FrameTarget:
+    """The assembled frame on one GPU (the fused option):
+    RGBA8 + depth for npix pixels that every rank's session writes its final
+    pixels into -- over NVLink peer memory for the other ranks (CUDA IPC) --
+    as its rays terminate, so the frame is complete when the last rank's last
+    pass is, with no gather.  Created by the owner (``handles`` None), opened
+    by the others from the owner's 128-byte IPC handles."""
+
+    def __init__(self, npix: int, handles: bytes | None = None):
+        import ctypes as C
+
+        from . import _lib
+
+        self.npix = int(npix)
+        h = C.c_void_p()
+        if handles is None:
+            _lib.call("wc_frame_target_create", self.npix, C.byref(h))
+        else:
+            buf = C.create_string_buffer(bytes(handles), 128)
+            _lib.call("wc_frame_target_open", buf, self.npix, C.byref(h))
+        self.handle = h.value
+        self.owner = handles is None
+
+    def ipc_handles(self) -> bytes:
+        import ctypes as C
+
+        from . import _lib
+
+        buf = C.create_string_buffer(128)
+        _lib.call("wc_frame_target_ipc_handles", self.handle, buf)
+        return buf.raw
+
+    def download(self, w: int, h: int):
+        """-> (rgba (h,w,4) uint8, depth (h,w) float32) in page-locked host memory."""
+        from . import _lib
+
+        base = _lib.pinned_pool.get(8 * self.npix)
+        rgba = base[:4 * self.npix]
+        depth = base[4 * self.npix:].view(np.float32)
+        _lib.call("wc_frame_target_download", self.handle, _lib.ptr(rgba), _lib.ptr(depth))
+        return rgba.reshape(h, w, 4), depth.reshape(h, w)
+
+    def close(self):
+        from . import _lib
+
+        if self.handle:
+            _lib.call("wc_frame_target_destroy", self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_TARGETS: dict = {}
+
+
+def _frame_target(w: int, h: int, world: int, rank: int, group):
+    """Rank 0's full-frame target, opened by every rank (one per image size
+    and group): the owner's IPC handles travel once, by an object broadcast."""
+    import torch.distributed as dist
+
+    key = (w, h, world, id(group))
+    t = _TARGETS.get(key)
+    if t is None:
+        owner = FrameTarget(w * h) if rank == 0 else None
+        if world > 1:
+            obj = [owner.ipc_handles() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            t = owner if rank == 0 else FrameTarget(w * h, obj[0])
+        else:
+            t = owner
+        _TARGETS.clear()
+        _TARGETS[key] = t
+    return t
+
+
 _SHARD_SESSIONS: dict = {}
 
 
-def render_sharded(cv, grids, cam, iso, opts, tile: int = 32, group=None, split=None):
-    """Render this rank's tiles on its GPU, gather the frame to rank 0.
-    Returns (framebuffer or None, local PassStats list).  The framebuffer
-    pack, the gather and the scatter are ordered on the session's stream."""
+def render_sharded(cv, grids, cam, iso, opts, tile: int = 32, group=None, split=None, assembly: str = "peer"):
+    """Render this rank's tiles on its GPU and assemble the frame on rank 0.
+    Returns (framebuffer or None, local PassStats list).
+
+    assembly="peer" (default): every rank's session writes its final pixels
+    straight into rank 0's frame target over NVLink peer memory as its rays
+    terminate (FrameTarget); a barrier, then rank 0 reads the frame back.
+    assembly="nccl": the framebuffer pack, one NCCL gather to rank 0 and the
+    scatter, ordered on the session's stream."""
     import torch
     import torch.distributed as dist
 
@@ -220,6 +308,20 @@ def render_sharded(cv, grids, cam, iso, opts, tile: int = 32, group=None, split=
         _SHARD_SESSIONS.clear()
         _SHARD_SESSIONS[key] = ent
     s, pix = ent
+    if assembly == "peer":
+        target = _frame_target(opts.width, opts.height, world, rank, group)
+        if getattr(s, "_target", None) is not target:
+            s.set_frame_target(target)
+        stats = render_frame_split(s, cam, iso, group, split)
+        session_stream(s).synchronize()  # this rank's pixels have landed in the target
+        if world > 1:
+            dist.barrier(group=group)
+        if rank != 0:
+            return None, stats
+        rgba, depth = target.download(opts.width, opts.height)
+        return Framebuffer(opts.width, opts.height, rgba, depth, 1.0), stats
+    if getattr(s, "_target", None) is not None:
+        s.set_frame_target(None)
     stats = render_frame_split(s, cam, iso, group, split)
     plan = _gather_plan(opts.width, opts.height, world, tile, dev)
     stream = session_stream(s)

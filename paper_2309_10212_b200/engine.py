@@ -401,6 +401,13 @@ class RenderSession:
         _lib.call("wc_session_pass_stage_ms", self._h, int(pass_index), a)
         return dict(zip(STAGES, [float(x) for x in a]))
 
+    def set_frame_target(self, target) -> None:
+        """Also write every final pixel into ``target`` (dist.FrameTarget: a
+        full-frame buffer on this or a peer GPU) as its ray terminates; None
+        stops.  Pixel positions come from the session's pixel ids."""
+        self._target = target  # (keeps it alive while the session writes into it)
+        _lib.call("wc_session_set_frame_target", self._h, None if target is None else target.handle)
+
     def set_kernel_profile(self, on: bool) -> None:
         """Collect per-kernel device times of passes launched kernel by
         kernel (set_graphs(False)); clears the previous collection."""
