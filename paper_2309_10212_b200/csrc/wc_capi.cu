@@ -758,7 +758,11 @@ int wc_session_rt_inputs(const wc_session *s, uint32_t *block_ray_offsets, uint3
     const wc::Session &S = *s->s;
     if (S.last_nent > 0) download(block_ray_offsets, S.block_ray_off.p, S.last_nvis + 1, S.st);
     else if (block_ray_offsets) block_ray_offsets[0] = 0;
-    download(sorted_entries, S.ent_val.p, S.last_nent, S.st);
+    if (S.group_entries) {
+        download(sorted_entries, S.ent_val.p, S.last_nent, S.st);
+    } else {  // ray-ordered entries: entry k at position k (the permutation is not stored)
+        for (int64_t k = 0; k < S.last_nent; k++) sorted_entries[k] = (uint32_t)k;
+    }
     download(entry_ray, S.ent_ray.p, S.last_nent, S.st);
     WC_CUDA(cudaStreamSynchronize(S.st));
     WC_API_END

@@ -61,6 +61,9 @@
 #ifndef WC_TRAV_DEFER
 #define WC_TRAV_DEFER 1
 #endif
+#ifndef WC_PASS_FORK
+#define WC_PASS_FORK 1
+#endif
 // mark_blocks as one launch (mark_extract) when a bitmap word never straddles an x-row
 #ifndef WC_MARK_FUSED
 #define WC_MARK_FUSED 1
@@ -1840,6 +1843,36 @@ struct BuildEntriesArgs {
     const uint32_t *ctl, *act_list, *emitted, *entry_off, *block_slots, *vis_bm, *vis_word_off;
     uint32_t *ent_key, *ent_val, *ent_ray, *ent_blk;
 };
+// The two halves of k_rt_prep as separate kernels, for the forked pass (the
+// entries need only the traversal and mark_blocks, so they are built on a
+// side branch while the cache is updated; the contributor rows need the
+// slots the decode just mapped).
+__global__ void k_rt_entries(BuildEntriesArgs be) {
+    pdl_wait();
+    const int64_t n_act = be.ctl[C_NACT], n_spec = be.ctl[C_NSPEC];
+    const int64_t n_slots = n_act * n_spec;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_slots; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = (uint32_t)t / (uint32_t)n_spec;  // slots <= rays < 2^32
+        const uint32_t j = (uint32_t)t - i * (uint32_t)n_spec;
+        if (j >= be.emitted[i]) continue;
+        const uint32_t eo = be.entry_off[i] + j;
+        const uint32_t b = be.block_slots[t];
+        WC_DEVICE_CHECK(eo < be.ctl[C_NENT] && b != WC_UINT_MAX);
+        const uint32_t w = b >> 5;
+        be.ent_key[eo] = be.vis_word_off[w] + __popc(be.vis_bm[w] & ((1u << (b & 31)) - 1u));
+        if (be.ent_val) be.ent_val[eo] = eo;
+        be.ent_ray[eo] = be.act_list[i];
+        be.ent_blk[eo] = b;
+    }
+}
+__global__ void k_rt_contrib(const uint32_t *visible_ids, const uint32_t *d_nvis, const int32_t *slot_of_block, int bdx,
+                             int bdy, int bdz, int4 *contrib, uint32_t *err) {
+    pdl_wait();
+    const int64_t nvis = *d_nvis;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvis; v += (int64_t)gridDim.x * blockDim.x)
+        contrib_row(v, visible_ids, slot_of_block, bdx, bdy, bdz, contrib, err);
+}
+
 __global__ void k_rt_prep(BuildEntriesArgs be, const uint32_t *visible_ids, const uint32_t *d_nvis,
                           const int32_t *slot_of_block, int bdx, int bdy, int bdz, int4 *contrib, uint32_t *err) {
     pdl_wait();
@@ -1859,7 +1892,7 @@ __global__ void k_rt_prep(BuildEntriesArgs be, const uint32_t *visible_ids, cons
         WC_DEVICE_CHECK(eo < be.ctl[C_NENT] && b != WC_UINT_MAX);
         const uint32_t w = b >> 5;
         be.ent_key[eo] = be.vis_word_off[w] + __popc(be.vis_bm[w] & ((1u << (b & 31)) - 1u));
-        be.ent_val[eo] = eo;
+        if (be.ent_val) be.ent_val[eo] = eo;
         be.ent_ray[eo] = be.act_list[i];
         be.ent_blk[eo] = b;
     }
@@ -2648,6 +2681,7 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     WC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     WC_CUDA(cudaStreamCreateWithFlags(&st_side, cudaStreamNonBlocking));
     WC_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
+    for (auto &e : ev_fork) WC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     uniform_origin = dirs == nullptr;
     dir.alloc(n * 3);
     if (!uniform_origin) origin.alloc(n * 3);
@@ -2693,6 +2727,8 @@ Session::Session(Volume *v, const CameraParams *cam, const uint32_t *pixel_ids, 
     h_counters.alloc(C_COUNT + kHistBins);
     partials.alloc(scan_scratch_words(std::max<int64_t>({n, nwords, active_ids.n, 1})));
     WC_CUDA(cudaMemsetAsync(partials.p, 0, 4 * partials.n, st));
+    partials_side.alloc(scan_scratch_words(n));  // the forked pass's side-branch scan
+    WC_CUDA(cudaMemsetAsync(partials_side.p, 0, 4 * partials_side.n, st));
 
     slot_of_block.alloc(vol->n_blocks);
     WC_CUDA(cudaMemsetAsync(slot_of_block.p, 0xFF, 4 * vol->n_blocks, st));
@@ -2860,6 +2896,8 @@ Session::~Session() {
         cudaStreamDestroy(st_side);
     }
     if (ev_side) cudaEventDestroy(ev_side);
+    for (auto &e : ev_fork)
+        if (e) cudaEventDestroy(e);
     if (st_copy) {
         cudaStreamSynchronize(st_copy);
         cudaStreamDestroy(st_copy);
@@ -3132,8 +3170,19 @@ void Session::enqueue_pass(int64_t p) {
     // C_WORK, C_NLONG and C_NITEMS are zero here (reset, or the last pass_end)
     launch_traverse(ta, n, 0, st);
     mark(1);
-    // entry compaction: exclusive scan of per-ray emitted counts
-    scan_exclusive_dev(LoadU32{emitted.p}, ctl + C_NACT, n, entry_off.p, ctl + C_NENT, partials.p, st);
+    // Forked pass (WC_PASS_FORK): the entry offsets and the raytrace entries
+    // depend only on the traversal and mark_blocks, so they run on the side
+    // stream (own scan scratch) while the cache lookup, eviction and decode
+    // run on the session stream; the branches join before the raytrace.
+    const bool fork = WC_PASS_FORK && !group_entries;
+    if (fork) {
+        WC_CUDA(cudaEventRecord(ev_fork[0], st));
+        WC_CUDA(cudaStreamWaitEvent(st_side, ev_fork[0], 0));
+        scan_exclusive_dev(LoadU32{emitted.p}, ctl + C_NACT, n, entry_off.p, ctl + C_NENT, partials_side.p, st_side);
+    } else {
+        // entry compaction: exclusive scan of per-ray emitted counts
+        scan_exclusive_dev(LoadU32{emitted.p}, ctl + C_NACT, n, entry_off.p, ctl + C_NENT, partials.p, st);
+    }
     // visible ids (ascending) + active marking, from the maintained
     // summaries: the cost follows the non-zero bitmap words
 #if WC_MARK_FUSED
@@ -3146,6 +3195,15 @@ void Session::enqueue_pass(int64_t p) {
         bitmap_extract_dense(vis_bm.p, nwords, vis_word_off.p, visible_ids.p, ctl + C_NVIS, false, partials.p, st);
         launch_mark_active(visible_ids.p, ctl + C_NVIS, vis_bm.p, vol->bdx, vol->bdy, vol->bdz, n, act_bm.p, st);
         bitmap_extract_dense(act_bm.p, nwords, nullptr, active_ids.p, ctl + C_NACTB, true, partials.p, st);  // clears act_bm
+    }
+    const BuildEntriesArgs be{ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p, vis_word_off.p,
+                              ent_key.p, group_entries ? ent_val.p : nullptr, ent_ray.p, ent_blk.p};
+    if (fork) {  // the entries, keyed by visible rank, on the side branch
+        WC_CUDA(cudaEventRecord(ev_fork[1], st));
+        WC_CUDA(cudaStreamWaitEvent(st_side, ev_fork[1], 0));
+        launch_pdl(k_rt_entries, grid_for(n, 256), 256, 0, st_side, be);
+        WC_LAUNCH_CHECK();
+        WC_CUDA(cudaEventRecord(ev_fork[2], st_side));
     }
     // cache.ensure_resident (cache.py:66-111), sized on the device
     const int64_t nmax = active_ids.n - 1;  // upper bound of the active-block count
@@ -3160,11 +3218,16 @@ void Session::enqueue_pass(int64_t p) {
     mark(3);
 
     // the raytrace's inputs: entries (keyed by visible rank) and contributor rows
-    const BuildEntriesArgs be{ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p, vis_word_off.p,
-                              ent_key.p, ent_val.p, ent_ray.p, ent_blk.p};
-    launch_pdl(k_rt_prep, grid_for(2 * n, 256), 256, 0, st, be, visible_ids.p, ctl + C_NVIS, slot_of_block.p, vol->bdx,
-               vol->bdy, vol->bdz, contrib.p, ctl + C_ERR);
-    WC_LAUNCH_CHECK();
+    if (fork) {
+        launch_pdl(k_rt_contrib, grid_for(n, 256), 256, 0, st, visible_ids.p, ctl + C_NVIS, slot_of_block.p, vol->bdx,
+                   vol->bdy, vol->bdz, contrib.p, ctl + C_ERR);
+        WC_LAUNCH_CHECK();
+        WC_CUDA(cudaStreamWaitEvent(st, ev_fork[2], 0));  // join: the entries are built
+    } else {
+        launch_pdl(k_rt_prep, grid_for(2 * n, 256), 256, 0, st, be, visible_ids.p, ctl + C_NVIS, slot_of_block.p,
+                   vol->bdx, vol->bdy, vol->bdz, contrib.p, ctl + C_ERR);
+        WC_LAUNCH_CHECK();
+    }
     // build_rt_inputs grouping (debug views only: the raytrace is correct on
     // ray order; the radix sort needs the entry and visible counts on the host)
     if (group_entries) {

@@ -231,12 +231,13 @@ struct Session : CacheStore {
     int64_t cap = 0, phys = 0, hw = 0;
     int32_t pass_no = 0;
     // scratch
-    DevBuf<uint32_t> counters, partials;
+    DevBuf<uint32_t> counters, partials, partials_side;
     PinnedBuf<uint32_t> h_counters;
     RadixScratch rs;
     cudaEvent_t ev_frame0 = nullptr, ev_reset_end = nullptr;
     cudaStream_t st_side = nullptr;  // reset: per-iso range tests overlapped with the ray setup
     cudaEvent_t ev_side = nullptr;
+    cudaEvent_t ev_fork[3] = {};  // forked pass: after traverse, after mark_blocks, entries built
     static constexpr int kStages = 6;  // traverse, mark, cache, raytrace inputs (+ grouping), raytrace, composite
     double stage_ms[kStages] = {};
     static constexpr int kMaxPassLog = 128;
