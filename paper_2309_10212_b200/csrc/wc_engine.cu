@@ -71,6 +71,9 @@
 #ifndef WC_DEFER_ITERS
 #define WC_DEFER_ITERS 12
 #endif
+#ifndef WC_DEFER_ITERS_LONG
+#define WC_DEFER_ITERS_LONG 48  // passes of long rays hand off later (C3 third pass, 60K rays at n_spec 34: 0.90 -> 0.85 ms)
+#endif
 #ifndef WC_DEFER_MAX_ACT
 #define WC_DEFER_MAX_ACT 150000  // (a 2-way share's second pass, 205K rays: 0.145 -> 0.157 ms handed off)
 #endif
@@ -456,9 +459,9 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
     int iters = 0;
     // (passes of short rays only: with n_spec >= WC_WARP_LONG_SPEC most rays
     // would be handed off -- a whole frame's third pass: 0.29 -> 0.36 ms)
-    const int defer_k = a.long_q && a.n_act <= (int64_t)WC_DEFER_MAX_ACT && a.n_spec < WC_WARP_LONG_SPEC
-                            ? WC_DEFER_ITERS
-                            : 0x7fffffff;
+    const int defer_k = !a.long_q || a.n_act > (int64_t)WC_DEFER_MAX_ACT
+                            ? 0x7fffffff
+                            : (a.n_spec < WC_WARP_LONG_SPEC ? WC_DEFER_ITERS : WC_DEFER_ITERS_LONG);
 #endif
     bool plain = false;
     auto plain_cell = [&]() {
