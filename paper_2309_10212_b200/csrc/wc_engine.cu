@@ -74,6 +74,12 @@
 #ifndef WC_DEFER_ITERS_LONG
 #define WC_DEFER_ITERS_LONG 48  // passes of long rays hand off later (C3 third pass, 60K rays at n_spec 34: 0.90 -> 0.85 ms)
 #endif
+#ifndef WC_DEFER_CAP
+#define WC_DEFER_CAP 16384
+#endif
+#ifndef WC_DEFER_ITERS_BIG
+#define WC_DEFER_ITERS_BIG 0x7fffffff  // passes of more short rays: off (24: C3 -0.03 ms, C5 +0.13 ms mean)
+#endif
 #ifndef WC_DEFER_MAX_ACT
 #define WC_DEFER_MAX_ACT 150000  // (a 2-way share's second pass, 205K rays: 0.145 -> 0.157 ms handed off)
 #endif
@@ -459,9 +465,11 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
     int iters = 0;
     // (passes of short rays only: with n_spec >= WC_WARP_LONG_SPEC most rays
     // would be handed off -- a whole frame's third pass: 0.29 -> 0.36 ms)
-    const int defer_k = !a.long_q || a.n_act > (int64_t)WC_DEFER_MAX_ACT
-                            ? 0x7fffffff
-                            : (a.n_spec < WC_WARP_LONG_SPEC ? WC_DEFER_ITERS : WC_DEFER_ITERS_LONG);
+    const bool long_rays = a.n_spec >= WC_WARP_LONG_SPEC;
+    const int defer_k = !a.long_q ? 0x7fffffff
+                        : a.n_act > (int64_t)WC_DEFER_MAX_ACT
+                            ? (long_rays ? 0x7fffffff : WC_DEFER_ITERS_BIG)
+                            : (long_rays ? WC_DEFER_ITERS_LONG : WC_DEFER_ITERS);
 #endif
     bool plain = false;
     auto plain_cell = [&]() {
@@ -700,7 +708,12 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
             have = false;
         }
 #if WC_TRAV_DEFER
-        else if (++iters >= defer_k) {  // hand the ray to k_traverse_long (same iterator, same slots)
+        // hand the ray to k_traverse_long (same iterator, same slots) -- in
+        // passes of more than WC_DEFER_MAX_ACT rays only once the work has run
+        // out (the tail), and at most WC_DEFER_CAP rays a pass: when most rays
+        // walk long (an isovalue that few rays hit), the lanes keep them
+        else if (++iters >= defer_k && (exhausted || a.n_act <= (int64_t)WC_DEFER_MAX_ACT) &&
+                 *reinterpret_cast<volatile uint32_t *>(a.n_long) < WC_DEFER_CAP) {
             a.emitted[i] = (uint32_t)emitted;
             a.coarse_cell[r] = (uint32_t)(c.cx + cdx * (c.cy + cdy * c.cz));
             a.fine_cell[r] = in_fine_run ? (uint32_t)(f.cx + fdx * (f.cy + fdy * f.cz)) : WC_UINT_MAX;
