@@ -104,11 +104,6 @@
 #define WC_DEC_PREC 8
 #endif
 // k_traverse: idle lanes that trigger a refill of the warp
-// rays reserved per warp and work-counter round trip in large passes (0: one
-// atomic per refill, for exactly the idle lanes)
-#ifndef WC_REFILL_POOL
-#define WC_REFILL_POOL 0
-#endif
 #ifndef WC_REFILL_MIN
 #define WC_REFILL_MIN 8
 #endif
@@ -342,11 +337,12 @@ __global__ void k_compact_index(Pred pred, int64_t n, const uint32_t *off, uint3
 
 // --------------------------------------------------------------- traverse
 
-// Mark block b visible: one RED.OR per distinct block among the lanes that
-// emit together (warp match), traversal emission fused with mark_blocks
-// (engine.py:97-106).
+// Mark block b visible: traversal emission fused with mark_blocks
+// (engine.py:97-106), one fire-and-forget RED.OR per emit.  (De-duplicating
+// the lanes that emit the same block with a warp match first, WC_MARK_MATCH=1,
+// costs more than the L2 atomics it saves: C3 traversal 0.72 -> 0.76 ms.)
 #ifndef WC_MARK_MATCH
-#define WC_MARK_MATCH 1
+#define WC_MARK_MATCH 0
 #endif
 __device__ __forceinline__ void mark_visible(uint32_t *bm, uint32_t b) {
 #if !WC_MARK_MATCH
@@ -493,49 +489,18 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
         return false;
 #endif
     };
-#if WC_REFILL_POOL
-    // In large passes a warp reserves its ray indices WC_REFILL_POOL at a
-    // time, one block ahead, so the work counter's round trip overlaps the
-    // current rays (cur .. cur + cur_left: the block in use; nxt: lane 0's
-    // pending atomic, read at the next refill that needs it).  Warp-uniform.
-    const bool pooled =
-        a.n_act > (int64_t)WC_REFILL_POOL * 8 * (((int64_t)gridDim.x * blockDim.x) >> 5);
-    uint32_t cur = 0, cur_left = 0, nxt = 0;
-    if (pooled && lane == 0) nxt = atomicAdd(a.work, (uint32_t)WC_REFILL_POOL);
-#endif
     for (;;) {
         if (!exhausted) {  // refill idle lanes (warp-uniform branch)
             const uint32_t need = __ballot_sync(0xffffffffu, !have);
             // batched: the refill path (ray loads, FP64 deltas) runs for at
             // least WC_REFILL_MIN lanes at once, unless the warp is all idle
             if (need && (__popc(need) >= WC_REFILL_MIN || need == 0xffffffffu)) {
-                const uint32_t k = (uint32_t)__popc(need), rank = (uint32_t)__popc(need & lt);
-                uint32_t mine;
-#if WC_REFILL_POOL
-                if (pooled) {
-                    if (cur_left >= k) {
-                        mine = cur + rank;
-                        cur += k;
-                        cur_left -= k;
-                    } else {  // the rest of this block, then the reserved one
-                        const uint32_t nf = __shfl_sync(0xffffffffu, nxt, 0);
-                        mine = rank < cur_left ? cur + rank : nf + (rank - cur_left);
-                        cur = nf + (k - cur_left);
-                        cur_left = (uint32_t)WC_REFILL_POOL - (k - cur_left);
-                        if (lane == 0) nxt = atomicAdd(a.work, (uint32_t)WC_REFILL_POOL);
-                    }
-                    // indices only grow: once one is past the rays, all later ones are
-                    if (cur >= a.n_act) exhausted = true;
-                } else
-#endif
-                {
-                    const int leader = __ffs(need) - 1;
-                    uint32_t first = 0;
-                    if (lane == leader) first = atomicAdd(a.work, k);
-                    first = __shfl_sync(0xffffffffu, first, leader);
-                    if (first + k >= a.n_act) exhausted = true;
-                    mine = first + rank;
-                }
+                const int leader = __ffs(need) - 1;
+                uint32_t first = 0;
+                if (lane == leader) first = atomicAdd(a.work, (uint32_t)__popc(need));
+                first = __shfl_sync(0xffffffffu, first, leader);
+                if (first + __popc(need) >= a.n_act) exhausted = true;
+                const uint32_t mine = first + __popc(need & lt);
                 if (!have && mine < a.n_act) {
                     have = true;
 #if WC_TRAV_DEFER
