@@ -25,6 +25,9 @@
 // Resident CTAs (of 128 threads) per SM requested from ptxas for the two
 // float64-heavy kernels; trades registers for latency hiding (tuned on B200
 // with scripts/gpu_variants.sh).
+#ifndef WC_SENTINEL_LATE
+#define WC_SENTINEL_LATE 1
+#endif
 #ifndef WC_TRAVERSE_MIN_CTAS
 #define WC_TRAVERSE_MIN_CTAS 5
 #endif
@@ -694,10 +697,12 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
             finished = emitted == a.n_spec || ray_done;
         }
         if (finished) {  // save the iterator past the last emit (traversal.py:388-403)
+#if !WC_SENTINEL_LATE
             for (int k = emitted; k < a.n_spec; k++) {  // traversal.py:423-424 sentinels
                 a.block_slots[base + k] = WC_UINT_MAX;
                 a.ray_slots[base + k] = WC_UINT_MAX;
             }
+#endif
             a.emitted[i] = (uint32_t)emitted;
             if (ray_done) {
                 a.exited[r] = 1;
@@ -809,10 +814,12 @@ __global__ void __launch_bounds__(128, WC_TQ_MIN_CTAS) k_traverse_q(TraverseArgs
 
     auto finish = [&](bool ray_done, uint32_t c_lin, double ctx, double cty, double ctz, bool in_fine, uint32_t f_lin,
                       double ftx, double fty, double ftz) {
+#if !WC_SENTINEL_LATE
         for (int k = emitted; k < a.n_spec; k++) {  // traversal.py:423-424 sentinels
             a.block_slots[base + k] = WC_UINT_MAX;
             a.ray_slots[base + k] = WC_UINT_MAX;
         }
+#endif
         a.emitted[i] = (uint32_t)emitted;
         if (ray_done) {
             a.exited[r] = 1;
@@ -1224,10 +1231,12 @@ __device__ __forceinline__ void warp_trace_ray(const TraverseArgs &a, int64_t i,
                 }
             }
         }
+#if !WC_SENTINEL_LATE
         for (int k = emitted + lane; k < a.n_spec; k += 32) {  // traversal.py:423-424 sentinels
             a.block_slots[base + k] = WC_UINT_MAX;
             a.ray_slots[base + k] = WC_UINT_MAX;
         }
+#endif
         if (lane == 0) {
             a.emitted[i] = (uint32_t)emitted;
             if (ray_done) {
@@ -1866,7 +1875,19 @@ __device__ __forceinline__ void contrib_row(int64_t v, const uint32_t *visible_i
 struct BuildEntriesArgs {
     const uint32_t *ctl, *act_list, *emitted, *entry_off, *block_slots, *vis_bm, *vis_word_off;
     uint32_t *ent_key, *ent_val, *ent_ray, *ent_blk;
+    uint32_t *sent_block, *sent_ray;  // the slot lists again: their sentinels are written here (WC_SENTINEL_LATE)
 };
+// traversal.py:423-424: a ray's slots past its last emit hold sentinels.
+// With WC_SENTINEL_LATE the traversal skips them (a thread-per-ray lane wrote
+// them one by one, scattered, up to 2 x 63 per ray) and the entry builder,
+// which visits every slot (thread per slot), writes them coalesced; nothing
+// reads the slot lists in between.
+__device__ __forceinline__ void write_sentinel(const BuildEntriesArgs &be, int64_t t) {
+#if WC_SENTINEL_LATE
+    be.sent_block[t] = WC_UINT_MAX;
+    be.sent_ray[t] = WC_UINT_MAX;
+#endif
+}
 // The two halves of k_rt_prep as separate kernels, for the forked pass (the
 // entries need only the traversal and mark_blocks, so they are built on a
 // side branch while the cache is updated; the contributor rows need the
@@ -1878,7 +1899,10 @@ __global__ void k_rt_entries(BuildEntriesArgs be) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_slots; t += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t i = (uint32_t)t / (uint32_t)n_spec;  // slots <= rays < 2^32
         const uint32_t j = (uint32_t)t - i * (uint32_t)n_spec;
-        if (j >= be.emitted[i]) continue;
+        if (j >= be.emitted[i]) {
+            write_sentinel(be, t);
+            continue;
+        }
         const uint32_t eo = be.entry_off[i] + j;
         const uint32_t b = be.block_slots[t];
         WC_DEVICE_CHECK(eo < be.ctl[C_NENT] && b != WC_UINT_MAX);
@@ -1910,7 +1934,10 @@ __global__ void k_rt_prep(BuildEntriesArgs be, const uint32_t *visible_ids, cons
         }
         const uint32_t i = (uint32_t)t / (uint32_t)n_spec;  // slots <= rays < 2^32
         const uint32_t j = (uint32_t)t - i * (uint32_t)n_spec;
-        if (j >= be.emitted[i]) continue;
+        if (j >= be.emitted[i]) {
+            write_sentinel(be, t);
+            continue;
+        }
         const uint32_t eo = be.entry_off[i] + j;
         const uint32_t b = be.block_slots[t];
         WC_DEVICE_CHECK(eo < be.ctl[C_NENT] && b != WC_UINT_MAX);
@@ -3221,7 +3248,8 @@ void Session::enqueue_pass(int64_t p) {
         bitmap_extract_dense(act_bm.p, nwords, nullptr, active_ids.p, ctl + C_NACTB, true, partials.p, st);  // clears act_bm
     }
     const BuildEntriesArgs be{ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p, vis_word_off.p,
-                              ent_key.p, group_entries ? ent_val.p : nullptr, ent_ray.p, ent_blk.p};
+                              ent_key.p, group_entries ? ent_val.p : nullptr, ent_ray.p, ent_blk.p,
+                              block_slots.p, ray_slots.p};
     if (fork) {  // the entries, keyed by visible rank, on the side branch
         WC_CUDA(cudaEventRecord(ev_fork[1], st));
         WC_CUDA(cudaStreamWaitEvent(st_side, ev_fork[1], 0));
