@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256, WC_DENSE_MIN_CTAS)
                    uint32_t *__restrict__ vis_word_off, uint32_t *__restrict__ vis_ids, uint32_t *d_nvis,
                    uint32_t *__restrict__ act_ids, uint32_t *d_nact, uint64_t *scratch, ScanEpoch ep) {
     pdl_wait();
-    __shared__ uint32_t swv[32], swa[32], slb[64];
+    __shared__ uint32_t swv[32], swa[32];
     __shared__ uint32_t s_exv, s_exa, s_ticket;
     const uint32_t epoch = resolve_epoch(ep);
     const int64_t chunk = 256LL * 4 * q16;

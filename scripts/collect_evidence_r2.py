@@ -56,6 +56,23 @@ def main():
         d = json.loads(out)
         d = {"what": f"ncu --set full --clock-control none of {what}, cold caches, serialised", **d}
         json.dump(d, open(os.path.join(args.dst, f"r02_ncu_full_k_{k}.json"), "w"), indent=1)
+    # the traversal summary bench.py cites in its roofline (r02_k_traverse_ncu.json)
+    p = os.path.join(args.dst, "r02_k_traverse_ncu.json")
+    d = json.load(open(p))
+    f = json.load(open(os.path.join(args.dst, "r02_ncu_full_k_traverse.json")))["full_capture"]
+    num = lambda k: float(f[k].split()[0])
+    d["duration_us"] = num("gpu__time_duration.sum")
+    d["dram_bytes_per_launch"] = int(round((num("dram__bytes_read.sum") + num("dram__bytes_write.sum")) * 1e6))
+    d["dram_gbs"] = round(d["dram_bytes_per_launch"] / d["duration_us"] / 1e3, 1)
+    d["warp_exec_threads_per_instr"] = num("smsp__thread_inst_executed_per_inst_executed.ratio")
+    d["warp_exec_efficiency"] = round(d["warp_exec_threads_per_instr"] / 32, 4)
+    d["l2_hit_rate"] = num("lts__t_sector_hit_rate.pct") / 100
+    d["l1_hit_rate"] = num("l1tex__t_sector_hit_rate.pct") / 100
+    d["warps_active"] = num("sm__warps_active.avg.pct_of_peak_sustained_active") / 100
+    d["issue_active"] = num("smsp__issue_active.avg.pct_of_peak_sustained_active") / 100
+    d["fp64_pipe"] = num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active") / 100
+    d["registers"] = f["launch__registers_per_thread"]
+    json.dump(d, open(p, "w"), indent=1)
     print("collected into", args.dst)
 
 
