@@ -522,9 +522,7 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
                     fdel_y = dy != 0.0 ? 4.0 / fabs(dy) : CUDART_INF;
                     fdel_z = dz != 0.0 ? 4.0 / fabs(dz) : CUDART_INF;
                     const uint32_t cc = a.coarse_cell[r];
-                    c.cx = (int)(cc % (uint32_t)cdx);
-                    c.cy = (int)((cc / (uint32_t)cdx) % (uint32_t)cdy);
-                    c.cz = (int)(cc / ((uint32_t)cdx * (uint32_t)cdy));
+                    unlinear3(cc, a.cdv_x, a.cdv_xy, c.cx, c.cy, c.cz);
                     c.tx = a.coarse_tmax[3 * (int64_t)r];
                     c.ty = a.coarse_tmax[3 * (int64_t)r + 1];
                     c.tz = a.coarse_tmax[3 * (int64_t)r + 2];
@@ -532,9 +530,7 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
                     in_fine_run = fc != WC_UINT_MAX;
                     f.cx = f.cy = f.cz = 0;
                     if (in_fine_run) {
-                        f.cx = (int)(fc % (uint32_t)fdx);
-                        f.cy = (int)((fc / (uint32_t)fdx) % (uint32_t)fdy);
-                        f.cz = (int)(fc / ((uint32_t)fdx * (uint32_t)fdy));
+                        unlinear3(fc, a.fdv_x, a.fdv_xy, f.cx, f.cy, f.cz);
                         fm = __ldg(a.cell_mask + cc);
                         plain = plain_cell();
                     }
@@ -879,9 +875,7 @@ __global__ void __launch_bounds__(128, WC_TQ_MIN_CTAS) k_traverse_q(TraverseArgs
                     fdel_y = dy != 0.0 ? 4.0 / fabs(dy) : CUDART_INF;
                     fdel_z = dz != 0.0 ? 4.0 / fabs(dz) : CUDART_INF;
                     const uint32_t cc = a.coarse_cell[r];
-                    c.cx = (int)(cc % (uint32_t)cdx);
-                    c.cy = (int)((cc / (uint32_t)cdx) % (uint32_t)cdy);
-                    c.cz = (int)(cc / ((uint32_t)cdx * (uint32_t)cdy));
+                    unlinear3(cc, a.cdv_x, a.cdv_xy, c.cx, c.cy, c.cz);
                     c.tx = a.coarse_tmax[3 * (int64_t)r];
                     c.ty = a.coarse_tmax[3 * (int64_t)r + 1];
                     c.tz = a.coarse_tmax[3 * (int64_t)r + 2];
@@ -945,9 +939,7 @@ __global__ void __launch_bounds__(128, WC_TQ_MIN_CTAS) k_traverse_q(TraverseArgs
             const int ccx = (int)(cxyz & 1023u), ccy = (int)((cxyz >> 10) & 1023u), ccz = (int)(cxyz >> 20);
             Dda f;
             if (fc0 != WC_UINT_MAX) {  // resumed run: the saved fine iterator
-                f.cx = (int)(fc0 % (uint32_t)fdx);
-                f.cy = (int)((fc0 / (uint32_t)fdx) % (uint32_t)fdy);
-                f.cz = (int)(fc0 / ((uint32_t)fdx * (uint32_t)fdy));
+                unlinear3(fc0, a.fdv_x, a.fdv_xy, f.cx, f.cy, f.cz);
                 f.tx = S.s0[q][lane];
                 f.ty = S.s1[q][lane];
                 f.tz = S.s2[q][lane];
@@ -1039,9 +1031,7 @@ __device__ __forceinline__ void warp_trace_ray(const TraverseArgs &a, int64_t i,
         const double cdel_z = dz != 0.0 ? 16.0 / fabs(dz) : CUDART_INF;
         Dda c, f;
         const uint32_t cc = a.coarse_cell[r];
-        c.cx = (int)(cc % (uint32_t)cdx);
-        c.cy = (int)((cc / (uint32_t)cdx) % (uint32_t)cdy);
-        c.cz = (int)(cc / ((uint32_t)cdx * (uint32_t)cdy));
+        unlinear3(cc, a.cdv_x, a.cdv_xy, c.cx, c.cy, c.cz);
         c.tx = a.coarse_tmax[3 * (int64_t)r];
         c.ty = a.coarse_tmax[3 * (int64_t)r + 1];
         c.tz = a.coarse_tmax[3 * (int64_t)r + 2];
@@ -1049,9 +1039,7 @@ __device__ __forceinline__ void warp_trace_ray(const TraverseArgs &a, int64_t i,
         bool in_fine_run = fc != WC_UINT_MAX;
         f.cx = f.cy = f.cz = 0;
         if (in_fine_run) {
-            f.cx = (int)(fc % (uint32_t)fdx);
-            f.cy = (int)((fc / (uint32_t)fdx) % (uint32_t)fdy);
-            f.cz = (int)(fc / ((uint32_t)fdx * (uint32_t)fdy));
+            unlinear3(fc, a.fdv_x, a.fdv_xy, f.cx, f.cy, f.cz);
         }
         f.tx = a.fine_tmax[3 * (int64_t)r];
         f.ty = a.fine_tmax[3 * (int64_t)r + 1];
@@ -1440,6 +1428,10 @@ __global__ void __launch_bounds__(128) k_traverse_long(TraverseArgs a_in) {
 }
 
 void launch_traverse(TraverseArgs ta, int64_t n_grid, int variant, cudaStream_t st) {
+    ta.cdv_x = FastDiv((uint32_t)ta.cdx);
+    ta.cdv_xy = FastDiv((uint32_t)ta.cdx * (uint32_t)ta.cdy);
+    ta.fdv_x = FastDiv((uint32_t)ta.fdx);
+    ta.fdv_xy = FastDiv((uint32_t)ta.fdx * (uint32_t)ta.fdy);
     ta.warp_max = variant == 1 ? 0u : (variant == 2 ? 0xFFFFFFFFu : (uint32_t)WC_WARP_TRAVERSE_MAX);
     ta.warp_max_long = variant == 0 ? (uint32_t)WC_WARP_TRAVERSE_MAX_LONG : ta.warp_max;
 #if WC_TRAVERSE_Q
@@ -1967,6 +1959,7 @@ struct RaytraceArgs {
     const int4 *contrib;
     const float *slot_values;
     int bdx, bdy, bdz, nx, ny, nz;
+    FastDiv bdv_x, bdv_xy;  // bdx, bdx bdy
     RayView rays;
     const double *fp;  // FrameParams (device): [3] iso, [4..6] base colour
     float4 *rgbz;
@@ -2042,9 +2035,7 @@ __device__ __forceinline__ EntryCtx entry_ctx(const RaytraceArgs &a, const RayVi
     e.k = a.identity ? (uint32_t)j : a.ent_val[j];
     e.r = a.ent_ray[e.k];
     const uint32_t b = a.ent_blk[e.k];
-    e.bx = (int)(b % (uint32_t)a.bdx);
-    e.by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy);
-    e.bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
+    unlinear3(b, a.bdv_x, a.bdv_xy, e.bx, e.by, e.bz);
     const int4 c0 = a.contrib[2 * v], c1 = a.contrib[2 * v + 1];
     e.field = SlotField{a.slot_values, c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
     e.cx = max(0, min(4, a.nx - 1 - 4 * e.bx));
@@ -2167,8 +2158,8 @@ __global__ void __launch_bounds__(128, WC_RAYTRACE_MIN_CTAS) k_rt_solve(SplitArg
         const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
         const uint32_t k = info.x, r = info.y, b = info.z, code = info.w;
         const int lx = code & 7, ly = (code >> 3) & 7, lz = (code >> 6) & 7, seq = code >> 9;
-        const int bx = (int)(b % (uint32_t)a.bdx), by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy),
-                  bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
+        int bx, by, bz;
+        unlinear3(b, a.bdv_x, a.bdv_xy, bx, by, bz);
         double o[3], d[3];
         rv.load(r, o, d);
         const double th = solve_cell(c, o, d, 4 * bx + lx, 4 * by + ly, 4 * bz + lz, rv.t_enter[r], iso);
@@ -2191,8 +2182,8 @@ __device__ __forceinline__ void shade_entry(const SplitArgs &s, const RayView &r
     const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
     const uint32_t r = info.y, b = info.z, code = info.w;
     const int lx = code & 7, ly = (code >> 3) & 7, lz = (code >> 6) & 7;
-    const int bx = (int)(b % (uint32_t)a.bdx), by = (int)((b / (uint32_t)a.bdx) % (uint32_t)a.bdy),
-              bz = (int)(b / ((uint32_t)a.bdx * (uint32_t)a.bdy));
+    int bx, by, bz;
+    unlinear3(b, a.bdv_x, a.bdv_xy, bx, by, bz);
     double o[3], d[3];
     rv.load(r, o, d);
     float rgb[3];
@@ -3306,6 +3297,8 @@ void Session::enqueue_pass(int64_t p) {
     ra.slot_values = slot_values.p;
     ra.bdx = vol->bdx;
     ra.bdy = vol->bdy;
+    ra.bdv_x = FastDiv((uint32_t)vol->bdx);
+    ra.bdv_xy = FastDiv((uint32_t)vol->bdx * (uint32_t)vol->bdy);
     ra.bdz = vol->bdz;
     ra.nx = vol->nx;
     ra.ny = vol->ny;

@@ -105,6 +105,7 @@ struct TraverseArgs {
     const uint32_t *coarse_bm;                // per-iso coarse range-test bitmap (k_iso_bitmap)
     const unsigned long long *cell_mask;  // per-iso fine tests, one word per coarse cell (k_iso_cell_mask)
     int fdx, fdy, fdz, cdx, cdy, cdz;
+    FastDiv cdv_x, cdv_xy, fdv_x, fdv_xy;  // cdx, cdx cdy, fdx, fdx fdy (set by launch_traverse)
     double iso;
     uint32_t *block_slots, *ray_slots, *emitted, *vis_bm;
     uint32_t *work;        // persistent-kernel ray counter (zeroed per pass)
