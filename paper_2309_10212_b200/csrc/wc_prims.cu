@@ -240,8 +240,10 @@ __global__ void __launch_bounds__(256, WC_DENSE_MIN_CTAS)
     __shared__ uint32_t swv[32], swa[32];
     __shared__ uint32_t s_exv, s_exa, s_ticket;
     const uint32_t epoch = resolve_epoch(ep);
+    // (32-bit index arithmetic: bitmaps of < 2^32 words; a 64-bit division
+    // is a ~70-instruction subroutine call)
     const int64_t chunk = 256LL * 4 * q16;
-    const int64_t ntiles = (nwords - 1) / chunk + 1;
+    const int64_t ntiles = (int64_t)((uint32_t)(nwords - 1) / (uint32_t)chunk) + 1;
     const int64_t last = ntiles - 1;
     bool lt = false;
     uint32_t tk = 0;
@@ -277,8 +279,9 @@ __global__ void __launch_bounds__(256, WC_DENSE_MIN_CTAS)
     // row coordinates of each word (bitmasks over the thread's words)
     uint32_t m_wx = 0, m_by = 0, m_bz = 0;  // bit k: word k has x-word > 0 / y > 0 / z > 0
     {
-        int64_t wx = w0 % wx_words, row = w0 / wx_words;
-        int64_t by = row % bdy, bz = row / bdy;
+        const uint32_t w0u = (uint32_t)w0, rowu = w0u / (uint32_t)wx_words;
+        int64_t wx = w0u - rowu * (uint32_t)wx_words, row = rowu;
+        int64_t by = rowu % (uint32_t)bdy, bz = rowu / (uint32_t)bdy;
 #pragma unroll
         for (int k = 0; k < 4 * Q; k++) {
             m_wx |= (uint32_t)(wx > 0) << k;
@@ -436,7 +439,7 @@ struct SinkBitsIdx {
         uint32_t v = bm[w];
         if (word_offsets) word_offsets[w] = prefix;
         if (clear) bm[w] = 0u;
-        const uint32_t base = (uint32_t)((w % id_mod) * 32);
+        const uint32_t base = ((uint32_t)w % (uint32_t)id_mod) * 32u;  // (w < 2^32)
         while (v) {
             ids[prefix++] = base + __ffs(v) - 1;
             v &= v - 1;

@@ -346,9 +346,10 @@ __global__ void __launch_bounds__(kScanThreads)
     if constexpr (HasCtaHooks<Load>::value) ld.cta_begin();
     __syncthreads();  // every CTA has read the count before it takes a ticket
     const int64_t n = s_n;
+    // (32-bit divisions: counts < 2^32; a 64-bit one is a subroutine call)
     const int64_t ntiles = n > 0 ? (n - 1) / kScanTile + 1 : 1;
-    const int64_t m = (ntiles + gridDim.x - 1) / gridDim.x;  // tiles per CTA
-    const int64_t last = (ntiles - 1) / m;
+    const int64_t m = ((uint32_t)ntiles + gridDim.x - 1) / gridDim.x;  // tiles per CTA
+    const int64_t last = (uint32_t)(ntiles - 1) / (uint32_t)m;
     bool lt = false;
     uint32_t tk = 0;
     if (threadIdx.x == 0) tk = take_ticket(scratch, lt);
