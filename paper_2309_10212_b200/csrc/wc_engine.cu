@@ -569,7 +569,7 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
         if (!in_fine_run) {
             if (CA == 1) {  // one coarse step (traversal.py:332-386)
                 const double t = dda_step(c, sx, sy, sz, 4.0 * fdel_x, 4.0 * fdel_y, 4.0 * fdel_z);
-                if (t > te || c.cx < 0 || c.cx >= cdx || c.cy < 0 || c.cy >= cdy || c.cz < 0 || c.cz >= cdz) {
+                if (t > te || (unsigned)c.cx >= (unsigned)cdx || (unsigned)c.cy >= (unsigned)cdy || (unsigned)c.cz >= (unsigned)cdz) {
                     ray_done = true;
                     finished = true;
                 } else {
@@ -599,8 +599,8 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
                         if (t > te || (unsigned)v >= (unsigned)pick3(ax, cdx, cdy, cdz)) {
 #else
                         const double t = dda_step(g, sx, sy, sz, 4.0 * fdel_x, 4.0 * fdel_y, 4.0 * fdel_z);
-                        if (t > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 ||
-                            g.cz >= cdz) {
+                        if (t > te || (unsigned)g.cx >= (unsigned)cdx || (unsigned)g.cy >= (unsigned)cdy ||
+                            (unsigned)g.cz >= (unsigned)cdz) {
 #endif
                             done = true;
                         } else {
@@ -678,12 +678,12 @@ __device__ __forceinline__ void traverse_rays_thread(TraverseArgs a) {
 #else
                 const double t = dda_step(f, sx, sy, sz, fdel_x, fdel_y, fdel_z);
                 if (!plain &&
-                    (t > te || f.cx < 0 || f.cx >= fdx || f.cy < 0 || f.cy >= fdy || f.cz < 0 || f.cz >= fdz)) {
+                    (t > te || (unsigned)f.cx >= (unsigned)fdx || (unsigned)f.cy >= (unsigned)fdy || (unsigned)f.cz >= (unsigned)fdz)) {
                     in_fine_run = false;
                     ray_done = true;
                     break;
                 }
-                if ((f.cx >> 2) != c.cx || (f.cy >> 2) != c.cy || (f.cz >> 2) != c.cz) {
+                if ((((f.cx >> 2) ^ c.cx) | ((f.cy >> 2) ^ c.cy) | ((f.cz >> 2) ^ c.cz)) != 0) {
                     in_fine_run = false;
                     break;
                 }
@@ -906,8 +906,8 @@ __global__ void __launch_bounds__(128, WC_TQ_MIN_CTAS) k_traverse_q(TraverseArgs
                 for (int j = 0; j < CA; j++) {
                     if (!done) {
                         const double t = dda_step(g, sx, sy, sz, 4.0 * fdel_x, 4.0 * fdel_y, 4.0 * fdel_z);
-                        if (t > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 ||
-                            g.cz >= cdz) {
+                        if (t > te || (unsigned)g.cx >= (unsigned)cdx || (unsigned)g.cy >= (unsigned)cdy ||
+                            (unsigned)g.cz >= (unsigned)cdz) {
                             done = true;
                         } else {
                             cell[j] = (uint32_t)(g.cx + cdx * (g.cy + cdy * g.cz));
@@ -972,7 +972,7 @@ __global__ void __launch_bounds__(128, WC_TQ_MIN_CTAS) k_traverse_q(TraverseArgs
                     mark_visible(a.vis_bm, f_lin);
                 }
                 const double t = dda_step(f, sx, sy, sz, fdel_x, fdel_y, fdel_z);
-                if (t > te || f.cx < 0 || f.cx >= fdx || f.cy < 0 || f.cy >= fdy || f.cz < 0 || f.cz >= fdz) {
+                if (t > te || (unsigned)f.cx >= (unsigned)fdx || (unsigned)f.cy >= (unsigned)fdy || (unsigned)f.cz >= (unsigned)fdz) {
                     in_run = false;
                     ray_done = true;
                     break;
@@ -1057,7 +1057,7 @@ __device__ __forceinline__ void warp_trace_ray(const TraverseArgs &a, int64_t i,
                 bool valid = lane <= kFineRun;
                 for (int j = 0; j < lane && valid; j++) {
                     const double t = dda_step(g, sx, sy, sz, fdel_x, fdel_y, fdel_z);
-                    if (t > te || g.cx < 0 || g.cx >= fdx || g.cy < 0 || g.cy >= fdy || g.cz < 0 || g.cz >= fdz ||
+                    if (t > te || (unsigned)g.cx >= (unsigned)fdx || (unsigned)g.cy >= (unsigned)fdy || (unsigned)g.cz >= (unsigned)fdz ||
                         (g.cx >> 2) != c.cx || (g.cy >> 2) != c.cy || (g.cz >> 2) != c.cz)
                         valid = false;  // the run ended before cell k
                 }
@@ -1067,7 +1067,7 @@ __device__ __forceinline__ void warp_trace_ray(const TraverseArgs &a, int64_t i,
                 if (valid) {
                     cell = (uint32_t)(g.cx + fdx * (g.cy + fdy * g.cz));
                     const double t = dda_step(h, sx, sy, sz, fdel_x, fdel_y, fdel_z);
-                    if (t > te || h.cx < 0 || h.cx >= fdx || h.cy < 0 || h.cy >= fdy || h.cz < 0 || h.cz >= fdz)
+                    if (t > te || (unsigned)h.cx >= (unsigned)fdx || (unsigned)h.cy >= (unsigned)fdy || (unsigned)h.cz >= (unsigned)fdz)
                         term = 2;
                     else if ((h.cx >> 2) != c.cx || (h.cy >> 2) != c.cy || (h.cz >> 2) != c.cz)
                         term = 1;
@@ -1109,7 +1109,7 @@ __device__ __forceinline__ void warp_trace_ray(const TraverseArgs &a, int64_t i,
                 bool valid = true, term_here = false;
                 for (int j = 0; j <= lane && valid; j++) {
                     tk = dda_step(g, sx, sy, sz, cdel_x, cdel_y, cdel_z);
-                    if (tk > te || g.cx < 0 || g.cx >= cdx || g.cy < 0 || g.cy >= cdy || g.cz < 0 || g.cz >= cdz) {
+                    if (tk > te || (unsigned)g.cx >= (unsigned)cdx || (unsigned)g.cy >= (unsigned)cdy || (unsigned)g.cz >= (unsigned)cdz) {
                         valid = false;
                         term_here = j == lane;
                     }
@@ -1153,8 +1153,8 @@ __device__ __forceinline__ void warp_trace_ray(const TraverseArgs &a, int64_t i,
                             cnt++;
                         }
                         const double t = dda_step(fj, sx, sy, sz, fdel_x, fdel_y, fdel_z);
-                        if (t > te || fj.cx < 0 || fj.cx >= fdx || fj.cy < 0 || fj.cy >= fdy || fj.cz < 0 ||
-                            fj.cz >= fdz) {
+                        if (t > te || (unsigned)fj.cx >= (unsigned)fdx || (unsigned)fj.cy >= (unsigned)fdy ||
+                            (unsigned)fj.cz >= (unsigned)fdz) {
                             exits = true;
                             break;
                         }
@@ -1194,8 +1194,8 @@ __device__ __forceinline__ void warp_trace_ray(const TraverseArgs &a, int64_t i,
                         for (int k = 0; k < kFineRun; k++) {
                             seen += (uint32_t)((mk >> fine_local(fs)) & 1ull);
                             const double t = dda_step(fs, sx, sy, sz, fdel_x, fdel_y, fdel_z);
-                            ex = t > te || fs.cx < 0 || fs.cx >= fdx || fs.cy < 0 || fs.cy >= fdy || fs.cz < 0 ||
-                                 fs.cz >= fdz;
+                            ex = t > te || (unsigned)fs.cx >= (unsigned)fdx || (unsigned)fs.cy >= (unsigned)fdy ||
+                                 (unsigned)fs.cz >= (unsigned)fdz;
                             lv = !ex && ((fs.cx >> 2) != g.cx || (fs.cy >> 2) != g.cy || (fs.cz >> 2) != g.cz);
                             if (seen == take || ex || lv) break;
                         }
