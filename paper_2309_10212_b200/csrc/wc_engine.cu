@@ -1326,20 +1326,24 @@ __global__ void __launch_bounds__(256, WC_ISO_MIN_CTAS) k_iso_cell_mask(const us
     const int lane = threadIdx.x & 31, half = lane >> 4, row = lane & 15;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // (the warp's 2 kU cells share one coarse-bitmap word: c0 % (2 kU) == 0)
+    static_assert(32 % (2 * kU) == 0, "a warp's cells must not straddle a bitmap word");
+    const uint32_t sel = half ? 0x7632u : 0x5410u;  // this half-warp's 16-bit halves of two ballots
     for (int64_t c0 = c_begin + w0 * 2 * kU; c0 < n_coarse; c0 += nw * 2 * kU) {
         uint4 w[kU];
         bool on[kU];
+        const uint32_t cw = iso_nan ? 0u : coarse_bm[c0 >> 5] >> (c0 & 31);
 #pragma unroll
         for (int u = 0; u < kU; u++) {
             const int64_t c = c0 + 2 * u + half;
-            on[u] = c < n_coarse && !iso_nan && ((coarse_bm[c >> 5] >> (c & 31)) & 1u);
+            on[u] = c < n_coarse && ((cw >> (2 * u + half)) & 1u);
             w[u] = on[u] ? __ldg(reinterpret_cast<const uint4 *>(q + c * 64) + row) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < kU; u++) {
             const int64_t c = c0 + 2 * u + half;
             const uint32_t ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-            unsigned long long m = 0;
+            uint32_t b[4];
 #pragma unroll
             for (int x = 0; x < 4; x++) {
                 const uint32_t lo = ws[x] & 0xFFFFu, hi = ws[x] >> 16;
@@ -1353,9 +1357,11 @@ __global__ void __launch_bounds__(256, WC_ISO_MIN_CTAS) k_iso_cell_mask(const us
                          iso_in_q(make_ushort2((unsigned short)lo, (unsigned short)hi), qi, mm,
                                   fx + (int64_t)fdx * (fy + (int64_t)fdy * fz), iso);
                 }
-                const uint32_t b = __ballot_sync(0xffffffffu, in);
-                m |= (unsigned long long)((b >> (16 * half)) & 0xFFFFu) << (16 * x);
+                b[x] = __ballot_sync(0xffffffffu, in);
             }
+            // bits [16x, 16x + 16) of the cell's mask: this half-warp's half of ballot x
+            const unsigned long long m =
+                (unsigned long long)__byte_perm(b[0], b[1], sel) | ((unsigned long long)__byte_perm(b[2], b[3], sel) << 32);
             if (row == 0 && c < n_coarse) cell_mask[c] = m;
         }
     }
