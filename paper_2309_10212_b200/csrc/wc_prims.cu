@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(256, WC_DENSE_MIN_CTAS)
     uint32_t m_wx = 0, m_by = 0, m_bz = 0;  // bit k: word k has x-word > 0 / y > 0 / z > 0
     {
         const uint32_t w0u = (uint32_t)w0, rowu = w0u / (uint32_t)wx_words;
-        int64_t wx = w0u - rowu * (uint32_t)wx_words, row = rowu;
+        int64_t wx = w0u - rowu * (uint32_t)wx_words;
         int64_t by = rowu % (uint32_t)bdy, bz = rowu / (uint32_t)bdy;
 #pragma unroll
         for (int k = 0; k < 4 * Q; k++) {
