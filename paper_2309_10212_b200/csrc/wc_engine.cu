@@ -1847,11 +1847,12 @@ struct DenseFieldView {  // fully decoded volume, x-fastest
 // Also clears the visibility bitmap for the next pass (its ranks were last
 // read by k_build_entries): every visible id zeroes its word.
 __device__ __forceinline__ void contrib_row(int64_t v, const uint32_t *visible_ids, const int32_t *slot_of_block,
-                                            int bdx, int bdy, int bdz, int4 *contrib, uint32_t *err) {
+                                            int bdx, int bdy, int bdz, const FastDiv &dv_x, const FastDiv &dv_xy,
+                                            int4 *contrib, uint32_t *err) {
     {
         const uint32_t b = visible_ids[v];
-        const int bx = (int)(b % (uint32_t)bdx), by = (int)((b / (uint32_t)bdx) % (uint32_t)bdy),
-                  bz = (int)(b / ((uint32_t)bdx * (uint32_t)bdy));
+        int bx, by, bz;
+        unlinear3(b, dv_x, dv_xy, bx, by, bz);
         int s[8];
 #pragma unroll
         for (int o = 0; o < 8; o++) {
@@ -1912,22 +1913,23 @@ __global__ void k_rt_entries(BuildEntriesArgs be) {
     }
 }
 __global__ void k_rt_contrib(const uint32_t *visible_ids, const uint32_t *d_nvis, const int32_t *slot_of_block, int bdx,
-                             int bdy, int bdz, int4 *contrib, uint32_t *err) {
+                             int bdy, int bdz, FastDiv dv_x, FastDiv dv_xy, int4 *contrib, uint32_t *err) {
     pdl_wait();
     const int64_t nvis = *d_nvis;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvis; v += (int64_t)gridDim.x * blockDim.x)
-        contrib_row(v, visible_ids, slot_of_block, bdx, bdy, bdz, contrib, err);
+        contrib_row(v, visible_ids, slot_of_block, bdx, bdy, bdz, dv_x, dv_xy, contrib, err);
 }
 
 __global__ void k_rt_prep(BuildEntriesArgs be, const uint32_t *visible_ids, const uint32_t *d_nvis,
-                          const int32_t *slot_of_block, int bdx, int bdy, int bdz, int4 *contrib, uint32_t *err) {
+                          const int32_t *slot_of_block, int bdx, int bdy, int bdz, FastDiv dv_x, FastDiv dv_xy,
+                          int4 *contrib, uint32_t *err) {
     pdl_wait();
     const int64_t n_act = be.ctl[C_NACT], n_spec = be.ctl[C_NSPEC];
     const int64_t n_slots = n_act * n_spec, nvis = *d_nvis;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_slots + nvis;
          t += (int64_t)gridDim.x * blockDim.x) {
         if (t >= n_slots) {
-            contrib_row(t - n_slots, visible_ids, slot_of_block, bdx, bdy, bdz, contrib, err);
+            contrib_row(t - n_slots, visible_ids, slot_of_block, bdx, bdy, bdz, dv_x, dv_xy, contrib, err);
             continue;
         }
         const uint32_t i = (uint32_t)t / (uint32_t)n_spec;  // slots <= rays < 2^32
@@ -3244,6 +3246,7 @@ void Session::enqueue_pass(int64_t p) {
         launch_mark_active(visible_ids.p, ctl + C_NVIS, vis_bm.p, vol->bdx, vol->bdy, vol->bdz, n, act_bm.p, st);
         bitmap_extract_dense(act_bm.p, nwords, nullptr, active_ids.p, ctl + C_NACTB, true, partials.p, st);  // clears act_bm
     }
+    const FastDiv ra_bdv_x((uint32_t)vol->bdx), ra_bdv_xy((uint32_t)vol->bdx * (uint32_t)vol->bdy);
     const BuildEntriesArgs be{ctl, alist, emitted.p, entry_off.p, block_slots.p, vis_bm.p, vis_word_off.p,
                               ent_key.p, group_entries ? ent_val.p : nullptr, ent_ray.p, ent_blk.p,
                               block_slots.p, ray_slots.p};
@@ -3269,12 +3272,12 @@ void Session::enqueue_pass(int64_t p) {
     // the raytrace's inputs: entries (keyed by visible rank) and contributor rows
     if (fork) {
         launch_pdl(k_rt_contrib, grid_for(n, 256), 256, 0, st, visible_ids.p, ctl + C_NVIS, slot_of_block.p, vol->bdx,
-                   vol->bdy, vol->bdz, contrib.p, ctl + C_ERR);
+                   vol->bdy, vol->bdz, ra_bdv_x, ra_bdv_xy, contrib.p, ctl + C_ERR);
         WC_LAUNCH_CHECK();
         WC_CUDA(cudaStreamWaitEvent(st, ev_fork[2], 0));  // join: the entries are built
     } else {
         launch_pdl(k_rt_prep, grid_for(2 * n, 256), 256, 0, st, be, visible_ids.p, ctl + C_NVIS, slot_of_block.p,
-                   vol->bdx, vol->bdy, vol->bdz, contrib.p, ctl + C_ERR);
+                   vol->bdx, vol->bdy, vol->bdz, ra_bdv_x, ra_bdv_xy, contrib.p, ctl + C_ERR);
         WC_LAUNCH_CHECK();
     }
     // build_rt_inputs grouping (debug views only: the raytrace is correct on
